@@ -1,0 +1,275 @@
+/*
+ * ddsim.h -- C-ABI of the B200-native batched what-if simulator.
+ *
+ * Plain pointers and sizes only: no torch types, no C++ types.  Every entry
+ * point returns an int status (0 = OK, else a KS_ERR_* code whose stable name
+ * is ks_error_name(code)); a human-readable detail for the last failure on the
+ * calling thread is ks_last_error_detail().  These names are exactly the
+ * KernsimError names of the reference (pkg/src/kernsim/errors.py:11-140), so a
+ * host binding re-raises the same exception class.
+ *
+ * Which reference interface each entry point replaces:
+ *
+ *   ks_graph_create        freeze of kernsim.graph.DependencyGraph
+ *                          (pkg/src/kernsim/graph.py:75-126): CSR, topological
+ *                          order (verify_acyclic, graph.py:129-148), lane
+ *                          chaining check, value-slot compilation.
+ *   ks_simulate            kernsim.sim.simulate (pkg/src/kernsim/sim.py:89-142)
+ *                          for S scenarios at once; policy ids map to
+ *                          DefaultSchedule / PrioritySchedule (sim.py:66-86) and
+ *                          VdnnPrefetchPolicy (scenarios.py:593-630).  Durations
+ *                          per scenario replace scale_durations / set_duration
+ *                          (transform.py:174-183, 293-297) and the inserted
+ *                          task table replaces sequenced insert_task
+ *                          (transform.py:204-246) of whatif_distributed
+ *                          (scenarios.py:194-241).
+ *   ks_simulate_host       the same with HOST buffers (H2D/D2H inside the call),
+ *                          i.e. what a ctypes binding of simulate() calls.
+ *   ks_toposort            verify_acyclic (graph.py:129-148): Kahn order with
+ *                          smallest-id tie-break, computed on the device.
+ *   ks_ingest              build_graph + link_syncs + compute_gaps
+ *                          (graph.py:198-312) and check_lane_overlaps
+ *                          (trace.py:255-265) over columnar trace records.
+ *   ks_map_layers          map_tasks_to_layers (layers.py:50-81).
+ */
+#ifndef DDSIM_H_
+#define DDSIM_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+/* ---- status codes (names == reference KernsimError.name) ---------------- */
+enum {
+  KS_OK = 0,
+  KS_ERR_DEADLOCK = 1,            /* "Deadlock"            errors.py:87   */
+  KS_ERR_CYCLE = 2,               /* "CycleDetected"       errors.py:57   */
+  KS_ERR_INVALID = 3,             /* "InvalidArgument"     (ValueError)   */
+  KS_ERR_CUDA = 4,                /* "CudaError"                          */
+  KS_ERR_OOM = 5,                 /* "OutOfMemory"                        */
+  KS_ERR_UNSUPPORTED = 6,         /* "Unsupported"                        */
+  KS_ERR_ORPHAN = 7,              /* "OrphanKernel"        errors.py:53   */
+  KS_ERR_AMBIGUOUS = 8,           /* "AmbiguousMarker"     errors.py:67   */
+  KS_ERR_OVERLAP = 9,             /* "OverlapViolation"    errors.py:34   */
+  KS_ERR_BAD_PIPELINE = 10,       /* "BadPipeline"         errors.py:117  */
+  KS_ERR_NO_DEVICE = 11           /* "NoDevice"                           */
+};
+
+/* ---- schedule policies (sim.py:152-165, scenarios.py:633) -------------- */
+enum { KS_POLICY_DEFAULT = 0, KS_POLICY_PRIORITY = 1, KS_POLICY_VDNN = 2 };
+
+/* ---- per-task flags ----------------------------------------------------- */
+enum {
+  KS_TASK_COMM = 1,          /* Task.is_comm (graph.py:59-61)                    */
+  KS_TASK_VDNN_MALLOC = 2    /* name startswith "cudaMalloc_vdnn" (scenarios.py:621) */
+};
+
+typedef struct ks_graph ks_graph; /* opaque, device-resident, immutable */
+
+/* A dependency graph in dense form.  Task i (0..n_tasks-1) is an arbitrary
+ * dense index chosen by the caller; id_rank[i] must order tasks exactly as
+ * their external ids do (ties in the scheduler break on id, sim.py:55-63). */
+typedef struct {
+  int32_t n_tasks;
+  int32_t n_lanes;
+  const int64_t* duration;    /* [n_tasks] ns                               */
+  const int64_t* gap;         /* [n_tasks] ns                               */
+  const int64_t* ready_time;  /* [n_tasks] ns (Task.ready_time)             */
+  const int32_t* lane;        /* [n_tasks] 0..n_lanes-1                     */
+  const int32_t* id_rank;     /* [n_tasks] rank of external id              */
+  const int32_t* priority;    /* [n_tasks] Task.priority                    */
+  const uint8_t* flags;       /* [n_tasks] KS_TASK_*; may be NULL           */
+  const uint32_t* group;      /* [n_tasks] scale group (0 = untouched); NULL */
+  int64_t n_edges;            /* multiset: (u,v) may repeat (kinds differ)  */
+  const int32_t* edge_src;
+  const int32_t* edge_dst;
+  const int32_t* lane_order_ptr; /* [n_lanes+1] or NULL (= nothing chained) */
+  const int32_t* lane_order;     /* dense indices, per lane, in order        */
+  /* Permutable chains (inserted-task table).  Chain c owns members
+   * chain_member[chain_ptr[c] .. chain_ptr[c+1]); its members sit on one lane,
+   * are NOT in lane_order and carry no edges among themselves: their on-lane
+   * order is the per-scenario permutation ks_scenarios_desc.chain_perm.  The
+   * head/tail tasks (lane neighbours, -1 = none) join the chain's ends. */
+  int32_t n_chains;
+  const int32_t* chain_ptr;      /* [n_chains+1]                             */
+  const int32_t* chain_member;   /* dense indices                            */
+  const int32_t* chain_head;     /* [n_chains]                               */
+  const int32_t* chain_tail;     /* [n_chains]                               */
+} ks_graph_desc;
+
+typedef struct {
+  int32_t n_tasks;
+  int32_t n_lanes;
+  int32_t n_edges_unique;
+  int32_t chained;          /* 1: every task is lane-chained -> max-plus path */
+  int32_t n_ordered;        /* tasks in the topological prefix (n_tasks if acyclic) */
+  int32_t n_slots;          /* value slots live at once (smem + spill)       */
+  int32_t n_slots_smem;
+  int32_t n_levels;         /* longest chain length (levels)                 */
+} ks_graph_info;
+
+/* Build the device-resident frozen graph on `device`.  Frozen row r holds the
+ * task order_out[r] (dense input index); rows 0..n_ordered-1 are a topological
+ * order.  order_out may be NULL. */
+int ks_graph_create(const ks_graph_desc* desc, int device, ks_graph** out,
+                    int32_t* order_out);
+int ks_graph_get_info(const ks_graph* g, ks_graph_info* info);
+/* level[r] (frozen rows, -1 for unordered rows). */
+int ks_graph_levels(const ks_graph* g, int32_t* level_out);
+int ks_graph_destroy(ks_graph* g);
+
+/* One scale step of a scenario: tasks whose group id lies in [group_lo,
+ * group_hi] get d <- round_half_up(d * num / den) (transform.py:174-183).
+ * Steps of one scenario apply in order (sequential rounding). */
+typedef struct {
+  int32_t group_lo;
+  int32_t group_hi;
+  int64_t num;
+  int64_t den;
+} ks_scale_step;
+
+typedef struct {
+  int32_t n_scenarios;
+  /* Dense per-(task, scenario) durations, frozen rows, scenario-minor:
+   * dense[r * dense_ld + s].  dense_kind 0 = none, 1 = int32, 2 = int64.
+   * Device pointer for ks_simulate, host pointer for ks_simulate_host. */
+  int32_t dense_kind;
+  const void* dense;
+  int64_t dense_ld;
+  /* Sparse per-task overrides (set_duration per scenario), HOST arrays:
+   * task override_task[k] (frozen row) gets override[k * n_scenarios + s]. */
+  int32_t n_overrides;
+  const int32_t* override_task;
+  const int64_t* override;
+  /* Scale program, HOST arrays: scenario s applies
+   * scale[scale_ptr[s] .. scale_ptr[s+1]) in order.  NULL = none. */
+  const int32_t* scale_ptr;
+  const ks_scale_step* scale;
+  /* Inserted-task table, HOST arrays: chain_perm[s * perm_ld + off_c + k] is
+   * the member (0-based within chain c) placed k-th on the lane; chain_present
+   * [s * n_chains + c] = 0 drops the chain's tasks AND their edges. NULL =
+   * identity order / all present. */
+  const int16_t* chain_perm;
+  int32_t perm_ld;
+  const uint8_t* chain_present;
+  /* VdnnPrefetchPolicy.conv_order rank per frozen row (HOST, -1 = none). */
+  const int32_t* vdnn_rank;
+} ks_scenarios_desc;
+
+/* Outputs.  For ks_simulate these are DEVICE pointers; for ks_simulate_host
+ * HOST pointers.  Any may be NULL (not produced).
+ *   start[r * start_ld + s]   frozen row r, scenario s; -1 for absent tasks
+ *   makespan[s]
+ *   lane_busy[s * n_lanes + l]
+ *   schedule[s * n_tasks + k] frozen row dispatched k-th (Alg.1 order) --
+ *                             produced by the list-scheduling kernel only
+ *   dispatched[s]             tasks dispatched (n_tasks unless Deadlock) */
+typedef struct {
+  int64_t* start;
+  int64_t start_ld;
+  int64_t* makespan;
+  int64_t* lane_busy;
+  int32_t* schedule;
+  int32_t* dispatched;
+} ks_sim_out;
+
+enum { KS_PATH_AUTO = 0, KS_PATH_MAXPLUS = 1, KS_PATH_LISTSCHED = 2 };
+
+/* Simulate all scenarios on the graph's device, asynchronously on `stream`
+ * (a cudaStream_t; NULL = legacy default stream).  `path` forces a kernel
+ * (AUTO: max-plus when the graph is chained and no schedule is requested). */
+int ks_simulate(const ks_graph* g, const ks_scenarios_desc* sc, int policy,
+                int path, const ks_sim_out* out, void* stream);
+
+/* Same, HOST buffers in and out: dense durations are streamed to the device
+ * in scenario chunks and results copied back, overlapped on two streams.
+ * Synchronous. */
+int ks_simulate_host(const ks_graph* g, const ks_scenarios_desc* sc,
+                     int policy, int path, const ks_sim_out* out);
+
+/* verify_acyclic: Kahn order with smallest-id tie-break (graph.py:129-148),
+ * computed on the device.  order_out[k] = dense input index; returns
+ * KS_ERR_CYCLE if fewer than n_tasks could be ordered (*n_out = ordered). */
+int ks_toposort(const ks_graph* g, int32_t* order_out, int32_t* n_out);
+
+/* ---- trace ingest (graph.py:198-312, trace.py:255-265) ------------------ */
+typedef struct {
+  int64_t n;                   /* events (document order)                  */
+  const int64_t* id;           /* external ids                              */
+  const uint8_t* kind;         /* TaskKind code: see KS_KIND_*              */
+  const int32_t* lane;         /* lane index                                */
+  const int64_t* start;        /* ns                                        */
+  const int64_t* duration;     /* ns                                        */
+  const int64_t* correlation;  /* -1 = none                                 */
+  const int32_t* sync_target;  /* lane index or -1 (device-wide)            */
+  const uint8_t* is_dtoh;      /* name startswith "memcpy_dtoh"             */
+  int32_t n_lanes;
+  const uint8_t* lane_class;   /* [n_lanes] 0 cpu, 1 gpu, 2 comm            */
+  const int32_t* lane_rank;    /* [n_lanes] rank of str(lane) (sorting)     */
+  int32_t strict;              /* OrphanKernel instead of dropping           */
+} ks_trace_cols;
+
+enum {
+  KS_KIND_CPU_API = 0, KS_KIND_CPU_OTHER = 1, KS_KIND_GPU_KERNEL = 2,
+  KS_KIND_GPU_MEMCPY = 3, KS_KIND_DATA_LOAD = 4, KS_KIND_COMM = 5,
+  KS_KIND_SYNC = 6
+};
+enum {
+  KS_EDGE_LANE_SEQ_CPU = 0, KS_EDGE_LANE_SEQ_GPU = 1,
+  KS_EDGE_LAUNCH_CORRELATION = 2, KS_EDGE_SYNC_BLOCK = 3,
+  KS_EDGE_COMM_ORDER = 4, KS_EDGE_INJECTED = 5
+};
+
+/* Output of ks_ingest (HOST buffers, caller-allocated; capacities given).
+ * Edge k: (edge_src[k], edge_dst[k], edge_kind[k]) as event indices.
+ * lane_order: events sorted per lane by (start, id), grouped by lane index;
+ * lane_order_ptr[n_lanes+1].  gap[n] per event. */
+typedef struct {
+  int64_t edge_cap;
+  int64_t n_edges;
+  int32_t* edge_src;
+  int32_t* edge_dst;
+  uint8_t* edge_kind;
+  int32_t* lane_order;        /* [n]                                      */
+  int32_t* lane_order_ptr;    /* [n_lanes+1]                              */
+  int64_t* gap;               /* [n]                                      */
+  int32_t* launcher;          /* [n] event index of the LaunchCorrelation source or -1 */
+  int64_t bad_a, bad_b;       /* OverlapViolation / OrphanKernel ids      */
+} ks_ingest_out;
+
+int ks_ingest(const ks_trace_cols* tc, int device, int check_overlaps,
+              ks_ingest_out* out);
+
+/* ---- layer mapping (layers.py:30-81) ------------------------------------ */
+typedef struct {
+  int64_t n;                  /* markers                                   */
+  const int32_t* lane;        /* cpu lane index                            */
+  const int64_t* start;
+  const int64_t* end;
+  const int32_t* tag;         /* (layer, phase) tag id; tags are ranked so
+                                 that tag order == (layer, phase.value) order */
+} ks_marker_cols;
+
+/* tag_out[i]: tag id for event i, or -1 (unmapped).  CPU-kind events are
+ * mapped by innermost containing marker; GPU-kind events inherit from
+ * launcher[i].  Returns KS_ERR_AMBIGUOUS (bad_a = event id) on a non-nested
+ * tie. */
+int ks_map_layers(const ks_trace_cols* tc, const int32_t* launcher,
+                  const ks_marker_cols* mc, int device, int32_t* tag_out,
+                  int64_t* bad_event);
+
+/* ---- misc ---------------------------------------------------------------- */
+const char* ks_error_name(int code);
+const char* ks_last_error_detail(void);
+int ks_device_count(int* n);
+/* Number of kernels this library launched on the calling process so far. */
+int64_t ks_launch_count(void);
+const char* ks_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DDSIM_H_ */

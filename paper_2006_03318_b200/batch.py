@@ -1,0 +1,279 @@
+"""Batched simulation: many what-if scenarios of one frozen graph at once.
+
+This is the additive API that replaces the reference's per-scenario loop
+(``kernsim sweep``: copy -> apply_pipeline -> simulate per point,
+pkg/src/kernsim/cli.py:185-193).  A scenario is a row of a table:
+
+* dense durations   dur[r][s] for every frozen row r (Monte-Carlo jitter),
+* overrides         per-scenario durations of a few tasks (set_duration),
+* scale programs    sequential half-up Shrink steps on task groups
+                    (scale_durations, transform.py:174-183),
+* chains            per-scenario order / presence of inserted tasks on one
+                    lane (sequenced insert_task, transform.py:204-246).
+
+Compilers below turn the reference's sweeps (AMP, per-layer Shrink,
+data-parallel bandwidth x workers x bucket order) into such tables; the
+device evaluates all scenarios in one launch (maxplus_sim).
+"""
+
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from fractions import Fraction
+
+import numpy as np
+
+from . import _native as N
+from .comm import COLLECTIVE_LANE, NetworkConfig, allreduce_duration, earliest_weight_update_task
+from .comm import last_backward_gpu_task
+from .errors import BadPipeline, Deadlock, MissingLayer, NoWeightUpdate
+from .frozen import ChainSpec, FrozenGraph
+from .graph import DependencyGraph, EdgeKind, Task
+from .trace import GradientBucketMap, TaskKind
+from .transform import Selector
+
+POLICY_IDS = {"default": N.KS_POLICY_DEFAULT, "priority": N.KS_POLICY_PRIORITY,
+              "vdnn_prefetch": N.KS_POLICY_VDNN}
+
+
+@dataclass
+class BatchResult:
+    frozen: FrozenGraph
+    makespan: np.ndarray                 # [S] int64
+    lane_busy: np.ndarray | None         # [S][L] int64
+    start: np.ndarray | None             # [rows][S] int64 (frozen rows), -1 = absent
+    schedule: np.ndarray | None = None   # [S][N] frozen rows in dispatch order
+
+    def start_of(self, s: int) -> dict[int, int]:
+        col = self.start[:, s]
+        ids = self.frozen.row_ids
+        keep = col >= 0
+        return dict(zip(ids[keep].tolist(), col[keep].tolist()))
+
+    def lane_busy_of(self, s: int, present_lanes=None) -> dict:
+        fz = self.frozen
+        used = np.zeros(fz.L, bool)
+        if present_lanes is None:
+            used[fz.lane] = True
+        else:
+            used[list(present_lanes)] = True
+        return {fz.lanes[j]: int(self.lane_busy[s, j]) for j in range(fz.L) if used[j]}
+
+
+@dataclass
+class ScenarioTable:
+    n_scenarios: int
+    dense: object = None                 # np.ndarray / torch.Tensor [rows][ld] int32|int64
+    overrides: dict = field(default_factory=dict)   # frozen row -> int64[S]
+    scale_ptr: np.ndarray | None = None  # int32[S+1]
+    scale: np.ndarray | None = None      # SCALE_STEP_DTYPE[...]
+    chain_perm: np.ndarray | None = None # int16[S][sum B]
+    chain_present: np.ndarray | None = None  # uint8[S][n_chains]
+    vdnn_rank: np.ndarray | None = None  # int32[rows]
+
+    def desc(self, keep: list) -> N.ScenariosDesc:
+        sc = N.ScenariosDesc()
+        S = self.n_scenarios
+        sc.n_scenarios = S
+        if self.dense is not None:
+            d = self.dense
+            dt = str(d.dtype)
+            sc.dense_kind = 1 if dt.endswith("int32") else 2
+            if not dt.endswith(("int32", "int64")):
+                raise ValueError("dense durations must be int32 or int64")
+            sc.dense = N.ptr(d)
+            sc.dense_ld = int(d.shape[1]) if d.ndim == 2 else S
+            if hasattr(d, "stride") and callable(d.stride):
+                sc.dense_ld = int(d.stride(0))
+            elif isinstance(d, np.ndarray):
+                sc.dense_ld = d.strides[0] // d.itemsize
+        if self.overrides:
+            rows = np.array(sorted(self.overrides), np.int32)
+            vals = np.ascontiguousarray(np.stack([np.asarray(self.overrides[r], np.int64)
+                                                  for r in rows.tolist()]))
+            if vals.shape[1] != S:
+                raise ValueError("override rows must have n_scenarios entries")
+            keep += [rows, vals]
+            sc.n_overrides = len(rows)
+            sc.override_task, sc.override = rows.ctypes.data, vals.ctypes.data
+        if self.scale_ptr is not None:
+            sp = N.c_i32(self.scale_ptr)
+            st = np.ascontiguousarray(self.scale, N.SCALE_STEP_DTYPE)
+            if st.size == 0:
+                st = np.zeros(1, N.SCALE_STEP_DTYPE)
+            keep += [sp, st]
+            sc.scale_ptr, sc.scale = sp.ctypes.data, st.ctypes.data
+        if self.chain_perm is not None:
+            pm = np.ascontiguousarray(self.chain_perm, np.int16)
+            keep.append(pm)
+            sc.chain_perm, sc.perm_ld = pm.ctypes.data, pm.shape[1]
+        if self.chain_present is not None:
+            pr = np.ascontiguousarray(self.chain_present, np.uint8)
+            keep.append(pr)
+            sc.chain_present = pr.ctypes.data
+        if self.vdnn_rank is not None:
+            vr = N.c_i32(self.vdnn_rank)
+            keep.append(vr)
+            sc.vdnn_rank = vr.ctypes.data
+        return sc
+
+
+def simulate_batch(frozen: FrozenGraph, table: ScenarioTable, policy: str = "default",
+                   want_start: bool = True, want_schedule: bool = False,
+                   path: int = N.KS_PATH_AUTO) -> BatchResult:
+    """Host buffers in/out (ks_simulate_host): the reference-facing call."""
+    S = table.n_scenarios
+    if frozen.n_ordered < frozen.n:
+        missing = frozen.unordered_ids()
+        raise Deadlock(f"{len(missing)} tasks never became ready (first ids: {missing[:10]})")
+    keep: list = []
+    sc = table.desc(keep)
+    rows, L = frozen.n, frozen.L
+    ms = np.zeros(S, np.int64)
+    lb = np.zeros((S, max(L, 1)), np.int64)
+    start = np.empty((max(rows, 1), S), np.int64) if want_start else None
+    sched = np.empty((S, max(rows, 1)), np.int32) if want_schedule else None
+    out = N.SimOut()
+    out.makespan, out.lane_busy = ms.ctypes.data, lb.ctypes.data
+    if start is not None:
+        out.start, out.start_ld = start.ctypes.data, S
+    if sched is not None:
+        out.schedule = sched.ctypes.data
+        path = N.KS_PATH_LISTSCHED
+    N.check(N.lib().ks_simulate_host(frozen.handle, C.byref(sc), POLICY_IDS[policy], path,
+                                     C.byref(out)), "simulate_batch")
+    return BatchResult(frozen=frozen, makespan=ms, lane_busy=lb[:, :L],
+                       start=None if start is None else start[:rows], schedule=sched)
+
+
+def simulate_batch_device(frozen: FrozenGraph, table: ScenarioTable, *, makespan, lane_busy=None,
+                          start=None, start_ld: int | None = None, stream: int = 0,
+                          policy: str = "default", path: int = N.KS_PATH_AUTO) -> None:
+    """Device tensors in/out (ks_simulate): asynchronous on ``stream``
+    (a cudaStream_t as int, e.g. torch.cuda.current_stream().cuda_stream)."""
+    keep: list = []
+    sc = table.desc(keep)
+    out = N.SimOut()
+    out.makespan = N.ptr(makespan)
+    out.lane_busy = N.ptr(lane_busy)
+    if start is not None:
+        out.start = N.ptr(start)
+        out.start_ld = start_ld if start_ld is not None else int(start.stride(0))
+    N.check(N.lib().ks_simulate(frozen.handle, C.byref(sc), POLICY_IDS[policy], path,
+                                C.byref(out), C.c_void_p(stream)), "simulate_batch_device")
+
+
+# ------------------------------------------------------------------ compilers
+
+def compile_scale_sweep(graph: DependencyGraph, scenarios: list[list[tuple[Selector, object]]]):
+    """Per-scenario lists of (selector, factor) Shrink steps -> (group_of per
+    task in graph.tasks order, scale_ptr, scale steps).
+
+    Tasks are grouped by their membership signature over every distinct
+    selector; a step then touches the groups whose signature contains its
+    selector (one ks_scale_step per group)."""
+    sels: dict[object, int] = {}
+    for steps in scenarios:
+        for sel, _f in steps:
+            key = repr(sel.to_object())
+            if key not in sels:
+                sels[key] = (len(sels), sel)
+    tasks = list(graph.tasks.values())
+    sig_of_task = []
+    sel_list = sorted(sels.values(), key=lambda x: x[0])
+    for t in tasks:
+        sig_of_task.append(tuple(i for i, s in sel_list if s.matches(t)))
+    group_id: dict[tuple, int] = {(): 0}
+    group_of = np.zeros(len(tasks), np.uint32)
+    for i, sig in enumerate(sig_of_task):
+        if sig not in group_id:
+            group_id[sig] = len(group_id)
+        group_of[i] = group_id[sig]
+    groups_with: dict[int, list[int]] = {i: [] for i, _ in sel_list}
+    for sig, gid in group_id.items():
+        for i in sig:
+            groups_with[i].append(gid)
+    ptr = [0]
+    steps_out = []
+    for steps in scenarios:
+        for sel, factor in steps:
+            f = Fraction(str(factor)) if not isinstance(factor, Fraction) else factor
+            if f <= 0:
+                raise BadPipeline(f"scale factor must be positive, got {f}")
+            for gid in sorted(groups_with[sels[repr(sel.to_object())][0]]):
+                steps_out.append((gid, gid, f.numerator, f.denominator))
+        ptr.append(len(steps_out))
+    arr = np.zeros(len(steps_out), N.SCALE_STEP_DTYPE)
+    for k, (lo, hi, num, den) in enumerate(steps_out):
+        arr[k] = (lo, hi, num, den)
+    return group_of, np.array(ptr, np.int32), arr
+
+
+@dataclass
+class DistributedSweep:
+    frozen: FrozenGraph
+    table: ScenarioTable
+    member_ids: list[int]
+    configs: list[dict]
+    perms: np.ndarray
+
+
+def distributed_sweep(graph: DependencyGraph, buckets: GradientBucketMap, configs: list[dict],
+                      perms: np.ndarray | None = None, device: int | None = None) -> DistributedSweep:
+    """Data-parallel what-if table: one allReduce per non-empty bucket on
+    comm:collective (whatif_distributed, scenarios.py:194-241) with a
+    per-scenario network config (bandwidth x workers ...) and bucket order.
+
+    Scenario s equals the reference pipeline whose sequenced inserts are
+    applied in order perms[s] (the lane order of sequenced inserts is their
+    insertion order); workers == 1 drops the inserts (empty pipeline)."""
+    wu = earliest_weight_update_task(graph)
+    if wu is None:
+        raise NoWeightUpdate("no weight-update tasks in the graph")
+    g = graph.copy()
+    head_order = g.lane_order.get(COLLECTIVE_LANE, [])
+    head = head_order[-1] if head_order else None
+    nid = g.next_id()
+    members, sizes = [], []
+    for b in buckets.buckets():
+        layers = buckets.layers_of_bucket(b)
+        if not layers:
+            continue
+        size = buckets.bucket_size_bytes[b]
+        tid = nid + len(members)
+        g.tasks[tid] = Task(id=tid, kind=TaskKind.COMM, name=f"allreduce_bucket_{b}",
+                            lane=COLLECTIVE_LANE, duration=0, size_bytes=size)
+        for layer in layers:
+            src = last_backward_gpu_task(graph, layer)
+            if src is None:
+                raise MissingLayer(f"bucket {b}: layer {layer!r} has no backward GPU tasks")
+            g.edges.add((src.id, tid, EdgeKind.INJECTED))
+        g.edges.add((tid, wu.id, EdgeKind.INJECTED))
+        members.append(tid)
+        sizes.append(size)
+    B = len(members)
+    S = len(configs)
+    fz = FrozenGraph.from_graph(g, chains=[ChainSpec(members=members, head=head)] if B else None,
+                                device=device)
+    if perms is None:
+        perms = np.tile(np.arange(B, dtype=np.int16), (S, 1))
+    perms = np.asarray(perms, np.int16).reshape(S, B)
+    present = np.ones((S, 1), np.uint8)
+    ovr = {}
+    if B:
+        dur = np.zeros((B, S), np.int64)
+        for s, cfg_obj in enumerate(configs):
+            cfg = NetworkConfig.from_object(cfg_obj)
+            if cfg.n_workers == 1:
+                present[s, 0] = 0
+                continue
+            for k, size in enumerate(sizes):
+                dur[k, s] = allreduce_duration(size, cfg)
+        idx = {int(t): i for i, t in enumerate(fz.ids)}
+        for k, tid in enumerate(members):
+            ovr[int(fz.row_of[idx[tid]])] = dur[k]
+    table = ScenarioTable(n_scenarios=S, overrides=ovr, chain_perm=perms if B else None,
+                          chain_present=present if B else None)
+    return DistributedSweep(frozen=fz, table=table, member_ids=members, configs=configs,
+                            perms=perms)

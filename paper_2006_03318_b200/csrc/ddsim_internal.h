@@ -1,0 +1,125 @@
+// Internal layout shared by the host compiler (graph.cu) and the kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <cuda.h>
+#include <stdint.h>
+
+#include "../../include/ddsim.h"
+
+namespace ddsim {
+
+// One instruction of the compiled max-plus program: a task, or a permutable
+// chain (kind == 1) whose members are expanded per scenario.  64 bytes so a
+// chunk of records moves with one cp.async.bulk.
+struct alignas(16) NodeRec {
+  long long dur;    // base duration (ns)
+  long long gap;    // gap (ns)
+  long long ready;  // Task.ready_time floor (ns)
+  int out_slot;     // value slot receiving rel = start+dur+gap, -1 = none
+  int pred0;        // value slots of predecessors, -1 = none
+  int pred1;
+  int extra_off;    // further pred slots in extra[extra_off .. +nextra)
+  int nextra;
+  unsigned group;   // scale group (0 = untouched by every scale step)
+  int ovr_row;      // row of the per-scenario override table, -1 = none
+  int lane;
+  int row;          // frozen output row (kind 0) / chain index (kind 1)
+  int kind;         // 0 task, 1 chain macro
+};
+static_assert(sizeof(NodeRec) == 64, "NodeRec must be 64 bytes");
+
+struct ChainDesc {
+  int first_row;   // members occupy frozen rows first_row .. first_row+B-1
+  int B;
+  int head_slot;   // slot of the head's rel (-1 = none)
+  int tail_slot;   // slot receiving the last member's rel (-1 = no tail)
+  int member_off;  // index of the first member record in `members`
+  int perm_off;    // column offset of this chain in a scenario's perm row
+  int lane;
+  int pad;
+};
+
+struct ScaleStepDev {
+  int lo, hi;
+  long long num, den;
+};
+
+struct MaxplusParams {
+  const NodeRec* prog;
+  int n_rec;
+  const int* extra;
+  const ChainDesc* chains;
+  const NodeRec* members;
+  int ksm;                // slots held in shared memory
+  int kglob;              // spilled slots
+  long long* gslots;      // [kglob][s_pad]
+  long long s_pad;
+  int S;
+  int L;
+  int n_chains;
+  // duration sources
+  const long long* dense64;  // [rows][ld] or null
+  long long dense_ld;
+  int dense_kind;            // 0 none, 1 int32 (TMA tiles), 2 int64
+  const long long* ovr;      // [n_ovr][S]
+  const int* scale_ptr;      // [S+1] or null
+  const ScaleStepDev* scale;
+  const short* perm;         // [S][perm_ld] or null
+  int perm_ld;
+  const unsigned char* present;  // [S][n_chains] or null
+  // outputs
+  long long* start;
+  long long start_ld;
+  long long* makespan;
+  long long* lane_busy;      // [S][L]
+};
+
+struct ListParams {
+  int N, L, S;
+  const int* child_ptr;  // [N+1] frozen rows, multiset
+  const int* child;
+  const int* indeg;      // multiset in-degree
+  const int* lane;
+  const long long* dur;
+  const long long* gap;
+  const long long* ready;
+  const int* id_rank;
+  const int* prio;
+  const unsigned char* flags;
+  const unsigned* group;
+  const int* vrank;      // [N] or null
+  int policy;
+  int zero_time;         // verify_acyclic mode: all times 0
+  // durations
+  const int* dense32;
+  const long long* dense64;
+  long long dense_ld;
+  const int* ovr_row;    // [N] or null
+  const long long* ovr;  // [n_ovr][S]
+  const int* scale_ptr;
+  const ScaleStepDev* scale;
+  // scratch [S][N] / [S][L]
+  long long* rdy;
+  int* rem;
+  int* front;
+  long long* lane_prog;
+  // outputs
+  long long* start; long long start_ld;
+  long long* makespan;
+  long long* lane_busy;
+  int* schedule;
+  int* dispatched;
+};
+
+// kernel launchers (maxplus.cu / listsched.cu)
+cudaError_t launch_maxplus(const MaxplusParams& p, const int* dense32,
+                           cudaStream_t stream);
+cudaError_t launch_listsched(const ListParams& p, cudaStream_t stream);
+cudaError_t launch_fill_i64(long long* p, long long v, long long n, cudaStream_t s);
+cudaError_t launch_fill_i32(int* p, int v, long long n, cudaStream_t s);
+cudaError_t launch_patch_ovr(NodeRec* prog, int n_rec, const int* ovr_map, cudaStream_t st);
+int maxplus_block_dim(int S, int dmode, int num_sms);
+
+void note_launch(int n = 1);
+
+}  // namespace ddsim

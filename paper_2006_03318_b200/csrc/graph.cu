@@ -1,0 +1,1076 @@
+// Graph compiler + C-ABI of libddsim.
+//
+// ks_graph_create freezes a kernsim DependencyGraph (pkg/src/kernsim/graph.py:
+// 75-126) into device-resident arrays:
+//   * the lane-chaining check that licenses the max-plus path (every task in
+//     its lane's lane_order chain, consecutive pairs joined by an edge; see
+//     sim.py:113-130 -- lane exclusivity then never binds);
+//   * a topological order of the (deduplicated) edge set, depth-first so that
+//     a produced value is consumed soon after (Kahn with a LIFO frontier,
+//     lane successors pushed before cross-lane children);
+//   * value-slot allocation: every task whose rel = start+dur+gap is read by a
+//     later task gets a slot for its live range (linear scan); short ranges go
+//     to shared memory, long ones to a global spill area;
+//   * the multiset CSR + in-degrees the list scheduler needs (sim.py:95-106).
+#include <algorithm>
+#include <atomic>
+#include <cstring>
+#include <functional>
+#include <numeric>
+#include <queue>
+#include <string>
+#include <vector>
+
+#include "ddsim_internal.h"
+
+namespace ddsim {
+
+static thread_local std::string g_last_error;
+static std::atomic<long long> g_launches{0};
+void note_launch(int n) { g_launches.fetch_add(n); }
+
+struct KsError {
+  int code;
+  std::string msg;
+};
+
+static void fail(int code, const std::string& msg) { throw KsError{code, msg}; }
+
+#define CUDA_TRY(expr)                                                                 \
+  do {                                                                                 \
+    cudaError_t e_ = (expr);                                                           \
+    if (e_ != cudaSuccess)                                                             \
+      fail(e_ == cudaErrorMemoryAllocation ? KS_ERR_OOM : KS_ERR_CUDA,                 \
+           std::string(#expr) + ": " + cudaGetErrorString(e_));                        \
+  } while (0)
+
+template <class T>
+static T* dev_upload(const std::vector<T>& v) {
+  if (v.empty()) return nullptr;
+  T* p = nullptr;
+  CUDA_TRY(cudaMalloc(&p, v.size() * sizeof(T)));
+  CUDA_TRY(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
+  return p;
+}
+
+constexpr int kSmemSlotsMax = 24;
+constexpr int kShortRange = 48;
+
+}  // namespace ddsim
+
+using namespace ddsim;
+
+struct ks_graph {
+  int device = 0;
+  int n = 0, L = 0;
+  int n_ordered = 0;
+  int n_edges_unique = 0;
+  bool chained = false;
+  int n_slots = 0, ksm = 0, kglob = 0;
+  int n_rec = 0;
+  int n_levels = 0;
+  int n_chains = 0;
+  int perm_ld = 0;
+  bool rows_are_records = true;  // no chains: record i writes row i
+  std::vector<int> order;        // frozen row -> input index
+  std::vector<int> row_of;       // input index -> frozen row
+  std::vector<int> level;        // per frozen row
+  std::vector<int> rank_row;     // id rank per frozen row
+  // device
+  NodeRec* d_prog = nullptr;
+  int* d_extra = nullptr;
+  ChainDesc* d_chains = nullptr;
+  NodeRec* d_members = nullptr;
+  int* d_child_ptr = nullptr;
+  int* d_child = nullptr;
+  int* d_indeg = nullptr;
+  int* d_lane = nullptr;
+  long long* d_dur = nullptr;
+  long long* d_gap = nullptr;
+  long long* d_ready = nullptr;
+  int* d_rank = nullptr;
+  int* d_prio = nullptr;
+  unsigned char* d_flags = nullptr;
+  unsigned* d_group = nullptr;
+};
+
+namespace {
+
+struct DevGuard {
+  int prev = -1;
+  explicit DevGuard(int dev) {
+    cudaGetDevice(&prev);
+    if (prev != dev) cudaSetDevice(dev);
+  }
+  ~DevGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+void compile_graph(const ks_graph_desc* d, ks_graph* g) {
+  const int n = d->n_tasks;
+  const int L = d->n_lanes;
+  if (n < 0 || L < 0) fail(KS_ERR_INVALID, "negative sizes");
+  if (n > 0 && (!d->duration || !d->gap || !d->lane || !d->id_rank))
+    fail(KS_ERR_INVALID, "missing task arrays");
+  for (int i = 0; i < n; ++i)
+    if (d->lane[i] < 0 || d->lane[i] >= L) fail(KS_ERR_INVALID, "lane index out of range");
+  const long long E = d->n_edges;
+  for (long long k = 0; k < E; ++k) {
+    const int u = d->edge_src[k], v = d->edge_dst[k];
+    if (u < 0 || u >= n || v < 0 || v >= n) fail(KS_ERR_INVALID, "edge endpoint out of range");
+  }
+  g->n = n;
+  g->L = L;
+
+  // ---- chains (inserted-task table) ---------------------------------------
+  const int NC = d->n_chains;
+  std::vector<int> chain_of(n, -1);
+  std::vector<int> ch_lane(NC, -1);
+  for (int c = 0; c < NC; ++c) {
+    for (int k = d->chain_ptr[c]; k < d->chain_ptr[c + 1]; ++k) {
+      const int m = d->chain_member[k];
+      if (m < 0 || m >= n || chain_of[m] >= 0) fail(KS_ERR_INVALID, "bad chain member");
+      chain_of[m] = c;
+      if (ch_lane[c] < 0) ch_lane[c] = d->lane[m];
+      if (d->lane[m] != ch_lane[c]) fail(KS_ERR_INVALID, "chain members must share a lane");
+    }
+    if (d->chain_ptr[c + 1] <= d->chain_ptr[c]) fail(KS_ERR_INVALID, "empty chain");
+  }
+
+  // ---- unique edges ----------------------------------------------------------
+  std::vector<unsigned long long> keys(E);
+  for (long long k = 0; k < E; ++k)
+    keys[k] = ((unsigned long long)(unsigned)d->edge_src[k] << 32) | (unsigned)d->edge_dst[k];
+  std::sort(keys.begin(), keys.end());
+  keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+  g->n_edges_unique = (int)keys.size();
+  auto has_edge = [&](int u, int v) {
+    const unsigned long long k = ((unsigned long long)(unsigned)u << 32) | (unsigned)v;
+    return std::binary_search(keys.begin(), keys.end(), k);
+  };
+
+  // ---- lane chaining check ---------------------------------------------------
+  bool chained = d->lane_order_ptr != nullptr;
+  std::vector<int> lane_succ(n, -1);
+  if (chained) {
+    std::vector<char> seen(n, 0);
+    for (int l = 0; l < L && chained; ++l) {
+      int prev = -1;
+      for (int k = d->lane_order_ptr[l]; k < d->lane_order_ptr[l + 1]; ++k) {
+        const int t = d->lane_order[k];
+        if (t < 0 || t >= n || d->lane[t] != l || seen[t] || chain_of[t] >= 0) {
+          chained = false;
+          break;
+        }
+        seen[t] = 1;
+        if (prev >= 0) {
+          if (!has_edge(prev, t)) {
+            chained = false;
+            break;
+          }
+          lane_succ[prev] = t;
+        }
+        prev = t;
+      }
+    }
+    for (int i = 0; i < n && chained; ++i)
+      if (!seen[i] && chain_of[i] < 0) chained = false;
+  }
+  if (NC > 0 && !chained)
+    fail(KS_ERR_UNSUPPORTED, "permutable chains need an otherwise lane-chained graph");
+  g->chained = chained;
+  g->n_chains = NC;
+
+  // ---- contracted graph (chain -> one node) ---------------------------------
+  const int NN = n + NC;
+  auto X = [&](int t) { return chain_of[t] >= 0 ? n + chain_of[t] : t; };
+  std::vector<unsigned long long> ckeys;
+  ckeys.reserve(keys.size() + 2 * NC);
+  for (unsigned long long k : keys) {
+    const int u = (int)(k >> 32), v = (int)(k & 0xffffffffu);
+    const int xu = X(u), xv = X(v);
+    if (xu == xv) {
+      if (u == v) {
+        ckeys.push_back(((unsigned long long)xu << 32) | (unsigned)xv);  // self loop: cycle
+        continue;
+      }
+      fail(KS_ERR_INVALID, "edge between members of one chain");
+    }
+    ckeys.push_back(((unsigned long long)xu << 32) | (unsigned)xv);
+  }
+  for (int c = 0; c < NC; ++c) {
+    const int h = d->chain_head ? d->chain_head[c] : -1;
+    const int t = d->chain_tail ? d->chain_tail[c] : -1;
+    if (h >= 0) {
+      if (h >= n || chain_of[h] >= 0 || d->lane[h] != ch_lane[c])
+        fail(KS_ERR_INVALID, "bad chain head");
+      ckeys.push_back(((unsigned long long)h << 32) | (unsigned)(n + c));
+    }
+    if (t >= 0) {
+      if (t >= n || chain_of[t] >= 0 || d->lane[t] != ch_lane[c])
+        fail(KS_ERR_INVALID, "bad chain tail");
+      ckeys.push_back(((unsigned long long)(n + c) << 32) | (unsigned)t);
+    }
+  }
+  std::sort(ckeys.begin(), ckeys.end());
+  ckeys.erase(std::unique(ckeys.begin(), ckeys.end()), ckeys.end());
+  std::vector<int> cptr(NN + 1, 0), cadj(ckeys.size()), cindeg(NN, 0);
+  for (unsigned long long k : ckeys) {
+    cptr[(k >> 32) + 1]++;
+    cindeg[k & 0xffffffffu]++;
+  }
+  for (int i = 0; i < NN; ++i) cptr[i + 1] += cptr[i];
+  {
+    std::vector<int> fill(cptr.begin(), cptr.end() - 1);
+    for (unsigned long long k : ckeys) cadj[fill[k >> 32]++] = (int)(k & 0xffffffffu);
+  }
+  // rank of contracted nodes (tie-break for the initial stack)
+  std::vector<int> crank(NN);
+  for (int i = 0; i < n; ++i) crank[i] = d->id_rank[i];
+  for (int c = 0; c < NC; ++c) {
+    int r = INT32_MAX;
+    for (int k = d->chain_ptr[c]; k < d->chain_ptr[c + 1]; ++k)
+      r = std::min(r, d->id_rank[d->chain_member[k]]);
+    crank[n + c] = r;
+  }
+  auto clane = [&](int x) { return x < n ? d->lane[x] : ch_lane[x - n]; };
+
+  // ---- depth-first Kahn (LIFO frontier) --------------------------------------
+  std::vector<int> corder;
+  corder.reserve(NN);
+  {
+    std::vector<int> indeg = cindeg;
+    std::vector<int> init;
+    for (int i = 0; i < NN; ++i)
+      if (indeg[i] == 0) init.push_back(i);
+    std::sort(init.begin(), init.end(), [&](int a, int b) { return crank[a] > crank[b]; });
+    std::vector<int> stack(init);
+    std::vector<int> cross;
+    while (!stack.empty()) {
+      const int x = stack.back();
+      stack.pop_back();
+      corder.push_back(x);
+      cross.clear();
+      int same = -1;
+      for (int k = cptr[x]; k < cptr[x + 1]; ++k) {
+        const int y = cadj[k];
+        if (--indeg[y] == 0) {
+          if (same < 0 && clane(y) == clane(x))
+            same = y;
+          else
+            cross.push_back(y);
+        }
+      }
+      if (same >= 0) stack.push_back(same);
+      std::sort(cross.begin(), cross.end(), [&](int a, int b) { return crank[a] > crank[b]; });
+      for (int y : cross) stack.push_back(y);
+    }
+  }
+  const int R = (int)corder.size();  // records
+
+  // ---- frozen rows ----------------------------------------------------------
+  g->order.clear();
+  g->order.reserve(n);
+  std::vector<int> rec_first_row(R);
+  std::vector<char> placed(n, 0);
+  for (int i = 0; i < R; ++i) {
+    const int x = corder[i];
+    rec_first_row[i] = (int)g->order.size();
+    if (x < n) {
+      g->order.push_back(x);
+      placed[x] = 1;
+    } else {
+      const int c = x - n;
+      for (int k = d->chain_ptr[c]; k < d->chain_ptr[c + 1]; ++k) {
+        g->order.push_back(d->chain_member[k]);
+        placed[d->chain_member[k]] = 1;
+      }
+    }
+  }
+  g->n_ordered = (int)g->order.size();
+  {
+    std::vector<int> rest;
+    for (int i = 0; i < n; ++i)
+      if (!placed[i]) rest.push_back(i);
+    std::sort(rest.begin(), rest.end(),
+              [&](int a, int b) { return d->id_rank[a] < d->id_rank[b]; });
+    for (int t : rest) g->order.push_back(t);
+  }
+  g->row_of.assign(n, -1);
+  for (int r = 0; r < n; ++r) g->row_of[g->order[r]] = r;
+  g->rank_row.resize(n);
+  for (int r = 0; r < n; ++r) g->rank_row[r] = d->id_rank[g->order[r]];
+  g->rows_are_records = (NC == 0);
+
+  // ---- unique preds per task (for records) -----------------------------------
+  std::vector<int> pptr(n + 1, 0), padj(keys.size());
+  for (unsigned long long k : keys) pptr[(k & 0xffffffffu) + 1]++;
+  for (int i = 0; i < n; ++i) pptr[i + 1] += pptr[i];
+  {
+    std::vector<int> fill(pptr.begin(), pptr.end() - 1);
+    for (unsigned long long k : keys) padj[fill[k & 0xffffffffu]++] = (int)(k >> 32);
+  }
+  std::vector<int> tail_of(n, -1);  // task -> chain whose tail it is
+  for (int c = 0; c < NC; ++c) {
+    const int t = d->chain_tail ? d->chain_tail[c] : -1;
+    if (t >= 0) tail_of[t] = c;
+  }
+
+  // ---- levels ------------------------------------------------------------------
+  std::vector<int> clevel(NN, 0);
+  {
+    std::vector<int> rec_of(NN, -1);
+    for (int i = 0; i < R; ++i) rec_of[corder[i]] = i;
+    int maxl = 0;
+    for (int i = 0; i < R; ++i) {
+      const int x = corder[i];
+      const int lv = clevel[x] + 1;
+      clevel[x] = lv;
+      maxl = std::max(maxl, lv);
+      for (int k = cptr[x]; k < cptr[x + 1]; ++k) clevel[cadj[k]] = std::max(clevel[cadj[k]], lv);
+    }
+    g->n_levels = maxl;
+    g->level.assign(n, -1);
+    for (int i = 0; i < R; ++i) {
+      const int x = corder[i];
+      if (x < n)
+        g->level[rec_first_row[i]] = clevel[x] - 1;
+      else
+        for (int k = 0; k < d->chain_ptr[x - n + 1] - d->chain_ptr[x - n]; ++k)
+          g->level[rec_first_row[i] + k] = clevel[x] - 1;
+    }
+  }
+
+  // ---- value live ranges -------------------------------------------------------
+  // values: task t (0..n-1) -> rel(t); chain tail value n + c.
+  const int NV = n + NC;
+  std::vector<int> rec_of_task(n, -1), rec_of_chain(NC, -1);
+  for (int i = 0; i < R; ++i) {
+    const int x = corder[i];
+    if (x < n)
+      rec_of_task[x] = i;
+    else
+      rec_of_chain[x - n] = i;
+  }
+  auto rec_of_val = [&](int t) { return chain_of[t] >= 0 ? rec_of_chain[chain_of[t]] : rec_of_task[t]; };
+  std::vector<int> last_use(NV, -1);
+  // inputs of each record
+  std::vector<std::vector<int>> rec_inputs(R);
+  for (int i = 0; i < R; ++i) {
+    const int x = corder[i];
+    auto& in = rec_inputs[i];
+    auto add_task_preds = [&](int t) {
+      for (int k = pptr[t]; k < pptr[t + 1]; ++k) in.push_back(padj[k]);
+    };
+    if (x < n) {
+      add_task_preds(x);
+      if (tail_of[x] >= 0) in.push_back(n + tail_of[x]);
+    } else {
+      const int c = x - n;
+      for (int k = d->chain_ptr[c]; k < d->chain_ptr[c + 1]; ++k) add_task_preds(d->chain_member[k]);
+      const int h = d->chain_head ? d->chain_head[c] : -1;
+      if (h >= 0) in.push_back(h);
+    }
+    std::sort(in.begin(), in.end());
+    in.erase(std::unique(in.begin(), in.end()), in.end());
+    for (int v : in) last_use[v] = std::max(last_use[v], i);
+  }
+
+  // ---- slot allocation (linear scan, allocate-then-free) ----------------------
+  std::vector<int> slot(NV, -1);
+  std::vector<char> in_glob(NV, 0);
+  std::priority_queue<int, std::vector<int>, std::greater<int>> free_s, free_g;
+  int next_s = 0, next_g = 0;
+  auto alloc = [&](int v, int i) {
+    if (last_use[v] < 0) return;  // nobody reads it
+    const bool short_range = (last_use[v] - i) <= kShortRange;
+    if (short_range) {
+      if (!free_s.empty()) {
+        slot[v] = free_s.top();
+        free_s.pop();
+        return;
+      }
+      if (next_s < kSmemSlotsMax) {
+        slot[v] = next_s++;
+        return;
+      }
+    }
+    in_glob[v] = 1;
+    if (!free_g.empty()) {
+      slot[v] = free_g.top();
+      free_g.pop();
+    } else {
+      slot[v] = next_g++;
+    }
+  };
+  for (int i = 0; i < R; ++i) {
+    const int x = corder[i];
+    if (x < n) {
+      alloc(x, i);
+    } else {
+      const int c = x - n;
+      for (int k = d->chain_ptr[c]; k < d->chain_ptr[c + 1]; ++k) alloc(d->chain_member[k], i);
+      if (d->chain_tail && d->chain_tail[c] >= 0) alloc(n + c, i);
+    }
+    for (int v : rec_inputs[i])
+      if (last_use[v] == i && slot[v] >= 0) {
+        (in_glob[v] ? free_g : free_s).push(slot[v]);
+      }
+  }
+  g->ksm = next_s;
+  g->kglob = next_g;
+  g->n_slots = next_s + next_g;
+  auto final_slot = [&](int v) { return slot[v] < 0 ? -1 : (in_glob[v] ? g->ksm + slot[v] : slot[v]); };
+
+  // ---- records -----------------------------------------------------------------
+  std::vector<NodeRec> prog(R), members;
+  std::vector<int> extra;
+  std::vector<ChainDesc> chains(NC);
+  auto make_task_rec = [&](int t, std::vector<int> preds) {
+    NodeRec r;
+    memset(&r, 0, sizeof(r));
+    r.dur = d->duration[t];
+    r.gap = d->gap[t];
+    r.ready = d->ready_time ? d->ready_time[t] : 0;
+    r.out_slot = final_slot(t);
+    std::vector<int> ps;
+    for (int v : preds) ps.push_back(final_slot(v));
+    r.pred0 = ps.size() > 0 ? ps[0] : -1;
+    r.pred1 = ps.size() > 1 ? ps[1] : -1;
+    r.extra_off = 0;
+    r.nextra = ps.size() > 2 ? (int)ps.size() - 2 : 0;
+    if (r.nextra) {
+      r.extra_off = (int)extra.size();
+      for (size_t k = 2; k < ps.size(); ++k) extra.push_back(ps[k]);
+    }
+    r.group = d->group ? d->group[t] : 0u;
+    r.ovr_row = -1;
+    r.lane = d->lane[t];
+    r.row = g->row_of[t];
+    r.kind = 0;
+    return r;
+  };
+  int perm_off = 0;
+  for (int i = 0; i < R; ++i) {
+    const int x = corder[i];
+    if (x < n) {
+      std::vector<int> preds;
+      for (int k = pptr[x]; k < pptr[x + 1]; ++k) preds.push_back(padj[k]);
+      if (tail_of[x] >= 0) preds.push_back(n + tail_of[x]);
+      prog[i] = make_task_rec(x, preds);
+    } else {
+      const int c = x - n;
+      NodeRec r;
+      memset(&r, 0, sizeof(r));
+      r.kind = 1;
+      r.row = c;
+      r.out_slot = r.pred0 = r.pred1 = -1;
+      r.ovr_row = -1;
+      prog[i] = r;
+      ChainDesc& ch = chains[c];
+      ch.first_row = rec_first_row[i];
+      ch.B = d->chain_ptr[c + 1] - d->chain_ptr[c];
+      const int h = d->chain_head ? d->chain_head[c] : -1;
+      ch.head_slot = h >= 0 ? final_slot(h) : -1;
+      ch.tail_slot = (d->chain_tail && d->chain_tail[c] >= 0) ? final_slot(n + c) : -1;
+      ch.member_off = (int)members.size();
+      ch.perm_off = perm_off;
+      ch.lane = ch_lane[c];
+      ch.pad = 0;
+      perm_off += ch.B;
+      for (int k = d->chain_ptr[c]; k < d->chain_ptr[c + 1]; ++k) {
+        const int m = d->chain_member[k];
+        std::vector<int> preds;
+        for (int q = pptr[m]; q < pptr[m + 1]; ++q) preds.push_back(padj[q]);
+        members.push_back(make_task_rec(m, preds));
+      }
+    }
+  }
+  g->perm_ld = perm_off;
+  g->n_rec = R;
+
+  // ---- list-scheduler arrays (frozen rows, multiset edges) -------------------
+  std::vector<int> ch_ptr(n + 1, 0), ch_adj(E), indeg(n, 0);
+  for (long long k = 0; k < E; ++k) {
+    ch_ptr[g->row_of[d->edge_src[k]] + 1]++;
+    indeg[g->row_of[d->edge_dst[k]]]++;
+  }
+  for (int i = 0; i < n; ++i) ch_ptr[i + 1] += ch_ptr[i];
+  {
+    std::vector<int> fill(ch_ptr.begin(), ch_ptr.end() - 1);
+    for (long long k = 0; k < E; ++k)
+      ch_adj[fill[g->row_of[d->edge_src[k]]]++] = g->row_of[d->edge_dst[k]];
+  }
+  std::vector<int> lane_r(n), rank_r(n), prio_r(n);
+  std::vector<long long> dur_r(n), gap_r(n), ready_r(n);
+  std::vector<unsigned char> flags_r(n);
+  std::vector<unsigned> group_r(n);
+  for (int r = 0; r < n; ++r) {
+    const int t = g->order[r];
+    lane_r[r] = d->lane[t];
+    rank_r[r] = d->id_rank[t];
+    prio_r[r] = d->priority ? d->priority[t] : 0;
+    dur_r[r] = d->duration[t];
+    gap_r[r] = d->gap[t];
+    ready_r[r] = d->ready_time ? d->ready_time[t] : 0;
+    flags_r[r] = d->flags ? d->flags[t] : 0;
+    group_r[r] = d->group ? d->group[t] : 0u;
+  }
+
+  // ---- upload -----------------------------------------------------------------
+  g->d_prog = dev_upload(prog);
+  g->d_extra = dev_upload(extra);
+  g->d_chains = dev_upload(chains);
+  g->d_members = dev_upload(members);
+  g->d_child_ptr = dev_upload(ch_ptr);
+  g->d_child = dev_upload(ch_adj);
+  g->d_indeg = dev_upload(indeg);
+  g->d_lane = dev_upload(lane_r);
+  g->d_dur = dev_upload(dur_r);
+  g->d_gap = dev_upload(gap_r);
+  g->d_ready = dev_upload(ready_r);
+  g->d_rank = dev_upload(rank_r);
+  g->d_prio = dev_upload(prio_r);
+  g->d_flags = dev_upload(flags_r);
+  g->d_group = dev_upload(group_r);
+}
+
+void free_graph(ks_graph* g) {
+  if (!g) return;
+  void* ptrs[] = {g->d_prog,  g->d_extra, g->d_chains, g->d_members, g->d_child_ptr,
+                  g->d_child, g->d_indeg, g->d_lane,   g->d_dur,     g->d_gap,
+                  g->d_ready, g->d_rank,  g->d_prio,   g->d_flags,   g->d_group};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  delete g;
+}
+
+// ---- per-call scenario tables ---------------------------------------------------
+struct ScenTables {
+  std::vector<void*> bufs;
+  int* scale_ptr = nullptr;
+  ScaleStepDev* scale = nullptr;
+  long long* ovr = nullptr;
+  int* ovr_map = nullptr;
+  short* perm = nullptr;
+  unsigned char* present = nullptr;
+  int* vrank = nullptr;
+  cudaStream_t st = nullptr;
+  template <class T>
+  T* up(const T* host, size_t count) {
+    if (!host || count == 0) return nullptr;
+    T* p = nullptr;
+    CUDA_TRY(cudaMallocAsync(&p, count * sizeof(T), st));
+    bufs.push_back(p);
+    CUDA_TRY(cudaMemcpyAsync(p, host, count * sizeof(T), cudaMemcpyHostToDevice, st));
+    return p;
+  }
+  template <class T>
+  T* scratch(size_t count) {
+    T* p = nullptr;
+    if (count == 0) return nullptr;
+    CUDA_TRY(cudaMallocAsync(&p, count * sizeof(T), st));
+    bufs.push_back(p);
+    return p;
+  }
+  ~ScenTables() {
+    for (void* p : bufs) cudaFreeAsync(p, st);
+  }
+  // host staging must outlive async copies: keep vectors alive
+  std::vector<std::vector<char>> keep;
+};
+
+void build_tables(const ks_graph* g, const ks_scenarios_desc* sc, ScenTables& T, bool need_ovr_map,
+                  bool need_vrank) {
+  const int S = sc->n_scenarios;
+  if (sc->scale_ptr && sc->scale) {
+    const int nsteps = sc->scale_ptr[S] - sc->scale_ptr[0];
+    if (sc->scale_ptr[0] != 0) fail(KS_ERR_INVALID, "scale_ptr[0] must be 0");
+    for (int k = 0; k < nsteps; ++k)
+      if (sc->scale[k].num <= 0 || sc->scale[k].den <= 0)
+        fail(KS_ERR_BAD_PIPELINE, "scale factor must be positive");
+    T.scale_ptr = T.up(sc->scale_ptr, (size_t)S + 1);
+    // ks_scale_step and ScaleStepDev share layout (int,int,ll,ll)
+    static_assert(sizeof(ks_scale_step) == sizeof(ScaleStepDev), "layout");
+    T.scale = reinterpret_cast<ScaleStepDev*>(
+        T.up(reinterpret_cast<const ScaleStepDev*>(sc->scale), (size_t)std::max(nsteps, 1)));
+  }
+  if (sc->n_overrides > 0) {
+    T.ovr = T.up(reinterpret_cast<const long long*>(sc->override), (size_t)sc->n_overrides * S);
+    if (need_ovr_map) {
+      T.keep.emplace_back(sizeof(int) * (size_t)g->n);
+      int* map = reinterpret_cast<int*>(T.keep.back().data());
+      std::fill(map, map + g->n, -1);
+      for (int k = 0; k < sc->n_overrides; ++k) {
+        const int r = sc->override_task[k];
+        if (r < 0 || r >= g->n) fail(KS_ERR_INVALID, "override row out of range");
+        map[r] = k;
+      }
+      T.ovr_map = T.up(map, (size_t)g->n);
+    }
+  }
+  if (g->n_chains > 0) {
+    if (sc->chain_perm) {
+      if (sc->perm_ld < g->perm_ld) fail(KS_ERR_INVALID, "perm_ld too small");
+      T.perm = T.up(sc->chain_perm, (size_t)S * sc->perm_ld);
+    }
+    if (sc->chain_present) T.present = T.up(sc->chain_present, (size_t)S * g->n_chains);
+  }
+  if (need_vrank && sc->vdnn_rank) T.vrank = T.up(sc->vdnn_rank, (size_t)g->n);
+}
+
+}  // namespace
+
+namespace ddsim {
+__global__ void patch_ovr_kernel(NodeRec* prog, int n_rec, const int* ovr_map) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n_rec; i += gridDim.x * blockDim.x) {
+    NodeRec& r = prog[i];
+    if (r.kind == 0) r.ovr_row = ovr_map[r.row];
+  }
+}
+cudaError_t launch_patch_ovr(NodeRec* prog, int n_rec, const int* ovr_map, cudaStream_t st) {
+  patch_ovr_kernel<<<std::min(148 * 4, (n_rec + 255) / 256), 256, 0, st>>>(prog, n_rec, ovr_map);
+  note_launch();
+  return cudaGetLastError();
+}
+}  // namespace ddsim
+
+namespace {
+
+int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, int path,
+                  const ks_sim_out* out, cudaStream_t stream) {
+  if (!g || !sc || !out) fail(KS_ERR_INVALID, "null argument");
+  const int S = sc->n_scenarios;
+  if (S <= 0) fail(KS_ERR_INVALID, "n_scenarios must be positive");
+  if (policy < 0 || policy > 2) fail(KS_ERR_INVALID, "unknown policy");
+  bool use_max = path == KS_PATH_MAXPLUS ||
+                 (path == KS_PATH_AUTO && g->chained && out->schedule == nullptr);
+  if (use_max && !g->chained) fail(KS_ERR_INVALID, "max-plus path needs a lane-chained graph");
+  if (!use_max && g->n_chains > 0)
+    fail(KS_ERR_UNSUPPORTED, "list scheduling of permutable chains is not supported");
+  if (g->n_ordered < g->n) {
+    // A cycle: Alg. 1 stalls with exactly the non-Kahn-reachable tasks left.
+    fail(KS_ERR_DEADLOCK, std::to_string(g->n - g->n_ordered) + " tasks never became ready");
+  }
+  DevGuard guard(g->device);
+  ScenTables T;
+  T.st = stream;
+  const bool dense = sc->dense_kind != 0 && sc->dense != nullptr;
+  build_tables(g, sc, T, true, policy == KS_POLICY_VDNN);
+
+  if (use_max) {
+    MaxplusParams p;
+    memset(&p, 0, sizeof(p));
+    p.n_rec = g->n_rec;
+    p.prog = g->d_prog;
+    if (T.ovr_map && g->n_rec > 0) {
+      // per-call override rows: patch a copy of the program
+      NodeRec* prog2 = T.scratch<NodeRec>(g->n_rec);
+      CUDA_TRY(cudaMemcpyAsync(prog2, g->d_prog, sizeof(NodeRec) * g->n_rec,
+                               cudaMemcpyDeviceToDevice, stream));
+      CUDA_TRY(launch_patch_ovr(prog2, g->n_rec, T.ovr_map, stream));
+      p.prog = prog2;
+    }
+    p.extra = g->d_extra;
+    p.chains = g->d_chains;
+    p.members = g->d_members;
+    p.n_chains = g->n_chains;
+    if (T.ovr_map && g->perm_ld > 0) {
+      NodeRec* mem2 = T.scratch<NodeRec>(g->perm_ld);
+      CUDA_TRY(cudaMemcpyAsync(mem2, g->d_members, sizeof(NodeRec) * g->perm_ld,
+                               cudaMemcpyDeviceToDevice, stream));
+      CUDA_TRY(launch_patch_ovr(mem2, g->perm_ld, T.ovr_map, stream));
+      p.members = mem2;
+    }
+    p.ksm = g->ksm;
+    p.kglob = g->kglob;
+    p.S = S;
+    p.L = g->L;
+    int dmode = 0;
+    if (dense) {
+      if (g->n_chains > 0) fail(KS_ERR_UNSUPPORTED, "dense durations with permutable chains");
+      if (sc->dense_ld < S) fail(KS_ERR_INVALID, "dense_ld < n_scenarios");
+      if (sc->dense_kind == 1) {
+        const bool aligned = (reinterpret_cast<uintptr_t>(sc->dense) % 16 == 0) && (sc->dense_ld % 4 == 0);
+        dmode = (aligned && g->n_rec > 0) ? 1 : -1;
+        if (dmode < 0) fail(KS_ERR_INVALID, "int32 dense durations need 16B alignment and dense_ld % 4 == 0");
+      } else {
+        dmode = 2;
+        p.dense64 = reinterpret_cast<const long long*>(sc->dense);
+      }
+      p.dense_ld = sc->dense_ld;
+    }
+    p.dense_kind = dmode;
+    p.ovr = T.ovr;
+    p.scale_ptr = T.scale_ptr;
+    p.scale = T.scale;
+    p.perm = T.perm;
+    p.perm_ld = sc->perm_ld;
+    p.present = T.present;
+    p.start = reinterpret_cast<long long*>(out->start);
+    p.start_ld = out->start_ld;
+    p.makespan = reinterpret_cast<long long*>(out->makespan);
+    p.lane_busy = reinterpret_cast<long long*>(out->lane_busy);
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device);
+    const int BD = maxplus_block_dim(S, dmode, nsm);
+    p.s_pad = (long long)((S + BD - 1) / BD) * BD;
+    if (p.kglob > 0) p.gslots = T.scratch<long long>((size_t)p.kglob * p.s_pad);
+    CUDA_TRY(launch_maxplus(p, dense && dmode == 1 ? reinterpret_cast<const int*>(sc->dense) : nullptr,
+                            stream));
+    if (out->dispatched) CUDA_TRY(launch_fill_i32(out->dispatched, g->n, S, stream));
+  } else {
+    ListParams p;
+    memset(&p, 0, sizeof(p));
+    p.N = g->n;
+    p.L = g->L;
+    p.S = S;
+    p.child_ptr = g->d_child_ptr;
+    p.child = g->d_child;
+    p.indeg = g->d_indeg;
+    p.lane = g->d_lane;
+    p.dur = g->d_dur;
+    p.gap = g->d_gap;
+    p.ready = g->d_ready;
+    p.id_rank = g->d_rank;
+    p.prio = g->d_prio;
+    p.flags = g->d_flags;
+    p.group = g->d_group;
+    p.vrank = T.vrank;
+    p.policy = policy;
+    p.zero_time = 0;
+    if (dense) {
+      if (sc->dense_kind == 1)
+        p.dense32 = reinterpret_cast<const int*>(sc->dense);
+      else
+        p.dense64 = reinterpret_cast<const long long*>(sc->dense);
+      p.dense_ld = sc->dense_ld;
+    }
+    p.ovr_row = T.ovr_map;
+    p.ovr = T.ovr;
+    p.scale_ptr = T.scale_ptr;
+    p.scale = T.scale;
+    const size_t N = std::max(g->n, 1);
+    p.rdy = T.scratch<long long>(2 * N * S);
+    p.rem = T.scratch<int>(N * S);
+    p.front = T.scratch<int>(N * S);
+    p.start = reinterpret_cast<long long*>(out->start);
+    p.start_ld = out->start_ld;
+    p.makespan = reinterpret_cast<long long*>(out->makespan);
+    p.lane_busy = reinterpret_cast<long long*>(out->lane_busy);
+    p.schedule = out->schedule;
+    p.dispatched = out->dispatched;
+    CUDA_TRY(launch_listsched(p, stream));
+  }
+  CUDA_TRY(cudaGetLastError());
+  return KS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* ks_error_name(int code) {
+  switch (code) {
+    case KS_OK: return "OK";
+    case KS_ERR_DEADLOCK: return "Deadlock";
+    case KS_ERR_CYCLE: return "CycleDetected";
+    case KS_ERR_INVALID: return "InvalidArgument";
+    case KS_ERR_CUDA: return "CudaError";
+    case KS_ERR_OOM: return "OutOfMemory";
+    case KS_ERR_UNSUPPORTED: return "Unsupported";
+    case KS_ERR_ORPHAN: return "OrphanKernel";
+    case KS_ERR_AMBIGUOUS: return "AmbiguousMarker";
+    case KS_ERR_OVERLAP: return "OverlapViolation";
+    case KS_ERR_BAD_PIPELINE: return "BadPipeline";
+    case KS_ERR_NO_DEVICE: return "NoDevice";
+    default: return "KernsimError";
+  }
+}
+
+const char* ks_last_error_detail(void) { return g_last_error.c_str(); }
+
+const char* ks_version(void) { return "ddsim 0.1.0 sm_100a"; }
+
+int64_t ks_launch_count(void) { return g_launches.load(); }
+
+int ks_device_count(int* n) {
+  int c = 0;
+  cudaError_t e = cudaGetDeviceCount(&c);
+  if (n) *n = (e == cudaSuccess) ? c : 0;
+  if (e != cudaSuccess) {
+    g_last_error = cudaGetErrorString(e);
+    return KS_ERR_NO_DEVICE;
+  }
+  return KS_OK;
+}
+
+#define KS_GUARD_BEGIN try {
+#define KS_GUARD_END                                              \
+  }                                                               \
+  catch (const KsError& e) {                                      \
+    g_last_error = e.msg;                                         \
+    return e.code;                                                \
+  }                                                               \
+  catch (const std::bad_alloc&) {                                 \
+    g_last_error = "host allocation failed";                      \
+    return KS_ERR_OOM;                                            \
+  }                                                               \
+  catch (...) {                                                   \
+    g_last_error = "unexpected exception";                        \
+    return KS_ERR_INVALID;                                        \
+  }
+
+int ks_graph_create(const ks_graph_desc* desc, int device, ks_graph** out, int32_t* order_out) {
+  KS_GUARD_BEGIN
+  if (!desc || !out) fail(KS_ERR_INVALID, "null argument");
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) fail(KS_ERR_NO_DEVICE, "no CUDA device");
+  if (device < 0 || device >= ndev) fail(KS_ERR_INVALID, "bad device");
+  DevGuard guard(device);
+  ks_graph* g = new ks_graph();
+  g->device = device;
+  try {
+    compile_graph(desc, g);
+  } catch (...) {
+    free_graph(g);
+    throw;
+  }
+  if (order_out) std::copy(g->order.begin(), g->order.end(), order_out);
+  *out = g;
+  return KS_OK;
+  KS_GUARD_END
+}
+
+int ks_graph_get_info(const ks_graph* g, ks_graph_info* info) {
+  if (!g || !info) return KS_ERR_INVALID;
+  info->n_tasks = g->n;
+  info->n_lanes = g->L;
+  info->n_edges_unique = g->n_edges_unique;
+  info->chained = g->chained ? 1 : 0;
+  info->n_ordered = g->n_ordered;
+  info->n_slots = g->n_slots;
+  info->n_slots_smem = g->ksm;
+  info->n_levels = g->n_levels;
+  return KS_OK;
+}
+
+int ks_graph_levels(const ks_graph* g, int32_t* level_out) {
+  if (!g || !level_out) return KS_ERR_INVALID;
+  std::copy(g->level.begin(), g->level.end(), level_out);
+  return KS_OK;
+}
+
+int ks_graph_destroy(ks_graph* g) {
+  if (!g) return KS_OK;
+  DevGuard guard(g->device);
+  free_graph(g);
+  return KS_OK;
+}
+
+int ks_simulate(const ks_graph* g, const ks_scenarios_desc* sc, int policy, int path,
+                const ks_sim_out* out, void* stream) {
+  KS_GUARD_BEGIN
+  return simulate_impl(g, sc, policy, path, out, reinterpret_cast<cudaStream_t>(stream));
+  KS_GUARD_END
+}
+
+int ks_toposort(const ks_graph* g, int32_t* order_out, int32_t* n_out) {
+  KS_GUARD_BEGIN
+  if (!g) fail(KS_ERR_INVALID, "null graph");
+  DevGuard guard(g->device);
+  const int n = g->n;
+  if (n == 0) {
+    if (n_out) *n_out = 0;
+    return KS_OK;
+  }
+  cudaStream_t st;
+  CUDA_TRY(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  int rc = KS_OK;
+  {
+    ScenTables T;
+    T.st = st;
+    ListParams p;
+    memset(&p, 0, sizeof(p));
+    p.N = n;
+    p.L = g->L;
+    p.S = 1;
+    p.child_ptr = g->d_child_ptr;
+    p.child = g->d_child;
+    p.indeg = g->d_indeg;
+    p.lane = g->d_lane;
+    p.dur = g->d_dur;
+    p.gap = g->d_gap;
+    p.ready = g->d_ready;
+    p.id_rank = g->d_rank;
+    p.prio = g->d_prio;
+    p.flags = g->d_flags;
+    p.group = g->d_group;
+    p.policy = KS_POLICY_DEFAULT;
+    p.zero_time = 1;
+    p.rdy = T.scratch<long long>(2 * (size_t)n);
+    p.rem = T.scratch<int>(n);
+    p.front = T.scratch<int>(n);
+    p.schedule = T.scratch<int>(n);
+    p.dispatched = T.scratch<int>(1);
+    CUDA_TRY(launch_listsched(p, st));
+    std::vector<int> sched(n);
+    int nd = 0;
+    CUDA_TRY(cudaMemcpyAsync(sched.data(), p.schedule, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaMemcpyAsync(&nd, p.dispatched, sizeof(int), cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(cudaStreamSynchronize(st));
+    for (int k = 0; k < nd; ++k) order_out[k] = g->order[sched[k]];
+    if (n_out) *n_out = nd;
+    if (nd < n) {
+      g_last_error = "dependency cycle";
+      rc = KS_ERR_CYCLE;
+    }
+  }
+  cudaStreamSynchronize(st);
+  cudaStreamDestroy(st);
+  return rc;
+  KS_GUARD_END
+}
+
+}  // extern "C"
+
+// ---- host-buffer entry point --------------------------------------------------
+namespace {
+
+struct ChunkBufs {
+  void* dense = nullptr;
+  long long* start = nullptr;
+  long long* makespan = nullptr;
+  long long* lane_busy = nullptr;
+  int* schedule = nullptr;
+  int* dispatched = nullptr;
+};
+
+int simulate_host_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, int path,
+                       const ks_sim_out* out) {
+  if (!g || !sc || !out) fail(KS_ERR_INVALID, "null argument");
+  const int S = sc->n_scenarios;
+  if (S <= 0) fail(KS_ERR_INVALID, "n_scenarios must be positive");
+  DevGuard guard(g->device);
+  const long long N = std::max(g->n, 1);
+  const bool dense = sc->dense_kind != 0 && sc->dense != nullptr;
+  const size_t esz = dense ? (sc->dense_kind == 1 ? 4 : 8) : 0;
+  // chunk so that dense-in + start-out of one chunk stay near 4 GiB
+  const long long per_scen = N * ((long long)esz + (out->start ? 8 : 0)) + 64;
+  long long sc_chunk = std::max<long long>(4, (4ll << 30) / per_scen);
+  sc_chunk = std::min<long long>(sc_chunk, S);
+  sc_chunk = (sc_chunk + 3) / 4 * 4;
+  const int nchunks = (int)((S + sc_chunk - 1) / sc_chunk);
+  cudaStream_t st[2];
+  CUDA_TRY(cudaStreamCreateWithFlags(&st[0], cudaStreamNonBlocking));
+  CUDA_TRY(cudaStreamCreateWithFlags(&st[1], cudaStreamNonBlocking));
+  ChunkBufs buf[2];
+  const long long ldc = sc_chunk;  // multiple of 4
+  auto alloc = [&](ChunkBufs& b) {
+    if (dense) CUDA_TRY(cudaMalloc(&b.dense, esz * N * ldc));
+    if (out->start) CUDA_TRY(cudaMalloc(&b.start, 8 * N * ldc));
+    if (out->makespan) CUDA_TRY(cudaMalloc(&b.makespan, 8 * ldc));
+    if (out->lane_busy) CUDA_TRY(cudaMalloc(&b.lane_busy, 8 * ldc * std::max(g->L, 1)));
+    if (out->schedule) CUDA_TRY(cudaMalloc(&b.schedule, 4 * N * ldc));
+    if (out->dispatched) CUDA_TRY(cudaMalloc(&b.dispatched, 4 * ldc));
+  };
+  auto release = [&]() {
+    for (auto& b : buf) {
+      void* ps[] = {b.dense, b.start, b.makespan, b.lane_busy, b.schedule, b.dispatched};
+      for (void* p : ps)
+        if (p) cudaFree(p);
+    }
+    cudaStreamDestroy(st[0]);
+    cudaStreamDestroy(st[1]);
+  };
+  int rc = KS_OK;
+  try {
+    alloc(buf[0]);
+    if (nchunks > 1) alloc(buf[1]);
+    // per-chunk host slices of the scenario tables (kept alive to the end)
+    std::vector<std::vector<int>> sptr(nchunks);
+    std::vector<std::vector<long long>> ovr(nchunks);
+    std::vector<std::vector<short>> perm(nchunks);
+    std::vector<std::vector<unsigned char>> pres(nchunks);
+    for (int c = 0; c < nchunks; ++c) {
+      const long long s0 = c * sc_chunk;
+      const int n_s = (int)std::min<long long>(sc_chunk, S - s0);
+      ChunkBufs& b = buf[c & 1];
+      cudaStream_t stream = st[c & 1];
+      ks_scenarios_desc sub = *sc;
+      sub.n_scenarios = n_s;
+      if (dense) {
+        CUDA_TRY(cudaMemcpy2DAsync(b.dense, esz * ldc,
+                                   static_cast<const char*>(sc->dense) + esz * s0, esz * sc->dense_ld,
+                                   esz * n_s, g->n, cudaMemcpyHostToDevice, stream));
+        sub.dense = b.dense;
+        sub.dense_ld = ldc;
+      }
+      if (sc->scale_ptr && sc->scale) {
+        sptr[c].resize(n_s + 1);
+        for (int k = 0; k <= n_s; ++k) sptr[c][k] = sc->scale_ptr[s0 + k] - sc->scale_ptr[s0];
+        sub.scale_ptr = sptr[c].data();
+        sub.scale = sc->scale + sc->scale_ptr[s0];
+      }
+      if (sc->n_overrides > 0) {
+        ovr[c].resize((size_t)sc->n_overrides * n_s);
+        for (int k = 0; k < sc->n_overrides; ++k)
+          memcpy(&ovr[c][(size_t)k * n_s], sc->override + (size_t)k * S + s0, 8 * (size_t)n_s);
+        sub.override = reinterpret_cast<const int64_t*>(ovr[c].data());
+      }
+      if (sc->chain_perm) {
+        perm[c].assign(sc->chain_perm + s0 * sc->perm_ld, sc->chain_perm + (s0 + n_s) * sc->perm_ld);
+        sub.chain_perm = perm[c].data();
+      }
+      if (sc->chain_present && g->n_chains > 0) {
+        pres[c].assign(sc->chain_present + s0 * g->n_chains,
+                       sc->chain_present + (s0 + n_s) * g->n_chains);
+        sub.chain_present = pres[c].data();
+      }
+      ks_sim_out o;
+      o.start = reinterpret_cast<int64_t*>(b.start);
+      o.start_ld = ldc;
+      o.makespan = reinterpret_cast<int64_t*>(b.makespan);
+      o.lane_busy = reinterpret_cast<int64_t*>(b.lane_busy);
+      o.schedule = b.schedule;
+      o.dispatched = b.dispatched;
+      simulate_impl(g, &sub, policy, path, &o, stream);
+      if (out->start)
+        CUDA_TRY(cudaMemcpy2DAsync(out->start + s0, 8 * out->start_ld, b.start, 8 * ldc, 8 * n_s,
+                                   g->n, cudaMemcpyDeviceToHost, stream));
+      if (out->makespan)
+        CUDA_TRY(cudaMemcpyAsync(out->makespan + s0, b.makespan, 8 * n_s, cudaMemcpyDeviceToHost,
+                                 stream));
+      if (out->lane_busy)
+        CUDA_TRY(cudaMemcpyAsync(out->lane_busy + s0 * g->L, b.lane_busy, 8 * (size_t)n_s * g->L,
+                                 cudaMemcpyDeviceToHost, stream));
+      if (out->schedule)
+        CUDA_TRY(cudaMemcpyAsync(out->schedule + s0 * g->n, b.schedule, 4 * (size_t)n_s * g->n,
+                                 cudaMemcpyDeviceToHost, stream));
+      if (out->dispatched)
+        CUDA_TRY(cudaMemcpyAsync(out->dispatched + s0, b.dispatched, 4 * n_s, cudaMemcpyDeviceToHost,
+                                 stream));
+    }
+    CUDA_TRY(cudaStreamSynchronize(st[0]));
+    CUDA_TRY(cudaStreamSynchronize(st[1]));
+  } catch (...) {
+    cudaStreamSynchronize(st[0]);
+    cudaStreamSynchronize(st[1]);
+    release();
+    throw;
+  }
+  release();
+  return rc;
+}
+
+}  // namespace
+
+extern "C" int ks_simulate_host(const ks_graph* g, const ks_scenarios_desc* sc, int policy,
+                                int path, const ks_sim_out* out) {
+  KS_GUARD_BEGIN
+  return simulate_host_impl(g, sc, policy, path, out);
+  KS_GUARD_END
+}

@@ -1,0 +1,267 @@
+// listsched_sim: exact Alg. 1 event loop (pkg/src/kernsim/sim.py:89-142) for
+// graphs whose tasks are not all lane-chained (unsequenced inserts of
+// p3 / vdnn / gist / dgc / blueconnect), and the dispatch order
+// (schedule_trace) of any graph.
+//
+// One warp owns one scenario.  Each step the warp scans the frontier for the
+// arg-min of (max(lane_progress[lane], ready), id) (SchedulePolicy.choose,
+// sim.py:55-63) with a shuffle reduction; PrioritySchedule (sim.py:72-86) and
+// VdnnPrefetchPolicy (scenarios.py:618-630) are extra reductions over the same
+// frontier.  The frontier lives in shared memory (SoA, cached keys: a task's
+// ready time is final once it enters the frontier) and spills to global
+// memory past kFrontCap entries.  With zero_time set every key is 0 and the
+// dispatch order is Kahn's smallest-id order (verify_acyclic, graph.py:129-148).
+#include "ddsim_internal.h"
+
+#include <climits>
+
+namespace ddsim {
+
+constexpr int kFrontCap = 2048;
+
+__device__ __forceinline__ long long ls_scale(long long d, long long num, long long den) {
+  const bool neg = d < 0;
+  const unsigned long long a = neg ? (unsigned long long)(-d) : (unsigned long long)d;
+  const unsigned __int128 x = (unsigned __int128)a * (unsigned long long)num * 2u + (unsigned long long)den;
+  const unsigned long long q = (unsigned long long)(x / ((unsigned __int128)(unsigned long long)den * 2u));
+  return neg ? -(long long)q : (long long)q;
+}
+
+struct Front {
+  long long* rdy;
+  int* v;
+  int* rank;
+  int* lane;
+  // global spill (index >= kFrontCap)
+  long long* g_rdy;
+  int* g_v;
+  __device__ __forceinline__ void get(int i, const ListParams& p, long long& r, int& vv, int& rk,
+                                      int& ln) const {
+    if (i < kFrontCap) {
+      r = rdy[i];
+      vv = v[i];
+      rk = rank[i];
+      ln = lane[i];
+    } else {
+      r = g_rdy[i - kFrontCap];
+      vv = g_v[i - kFrontCap];
+      rk = p.id_rank[vv];
+      ln = p.lane[vv];
+    }
+  }
+  __device__ __forceinline__ void put(int i, const ListParams& p, long long r, int vv) const {
+    if (i < kFrontCap) {
+      rdy[i] = r;
+      v[i] = vv;
+      rank[i] = p.id_rank[vv];
+      lane[i] = p.lane[vv];
+    } else {
+      g_rdy[i - kFrontCap] = r;
+      g_v[i - kFrontCap] = vv;
+    }
+  }
+};
+
+__device__ __forceinline__ void argmin_reduce(long long& e, int& r, int& pos) {
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    const long long oe = __shfl_xor_sync(0xffffffffu, e, off);
+    const int orr = __shfl_xor_sync(0xffffffffu, r, off);
+    const int op = __shfl_xor_sync(0xffffffffu, pos, off);
+    if (oe < e || (oe == e && orr < r)) {
+      e = oe;
+      r = orr;
+      pos = op;
+    }
+  }
+}
+
+// arg-max of (key, -rank)
+__device__ __forceinline__ void argmax_reduce(int& key, int& r, int& pos) {
+#pragma unroll
+  for (int off = 16; off; off >>= 1) {
+    const int ok = __shfl_xor_sync(0xffffffffu, key, off);
+    const int orr = __shfl_xor_sync(0xffffffffu, r, off);
+    const int op = __shfl_xor_sync(0xffffffffu, pos, off);
+    if (ok > key || (ok == key && orr < r)) {
+      key = ok;
+      r = orr;
+      pos = op;
+    }
+  }
+}
+
+__global__ void __launch_bounds__(32) listsched_kernel(const ListParams p) {
+  extern __shared__ __align__(16) unsigned char smem[];
+  const int lane = threadIdx.x;
+  const int s = blockIdx.x;
+  Front fr;
+  fr.rdy = reinterpret_cast<long long*>(smem);
+  fr.v = reinterpret_cast<int*>(fr.rdy + kFrontCap);
+  fr.rank = fr.v + kFrontCap;
+  fr.lane = fr.rank + kFrontCap;
+  long long* lp = reinterpret_cast<long long*>(fr.lane + kFrontCap);  // [L]
+  long long* lb = lp + p.L;                                            // [L]
+  __shared__ int Fsh;
+
+  const long long N = p.N;
+  long long* rdy = p.rdy + (long long)s * N;
+  int* rem = p.rem + (long long)s * N;
+  fr.g_rdy = p.rdy + (long long)p.S * N + (long long)s * N;  // spill: second half
+  fr.g_v = p.front + (long long)s * N;
+  int e0 = 0, e1 = 0;
+  if (p.scale_ptr) {
+    e0 = p.scale_ptr[s];
+    e1 = p.scale_ptr[s + 1];
+  }
+  if (lane == 0) Fsh = 0;
+  __syncwarp();
+  for (int v = lane; v < p.N; v += 32) {
+    const int d = p.indeg[v];
+    rem[v] = d;
+    const long long r0 = p.zero_time ? 0 : p.ready[v];
+    rdy[v] = r0;
+    if (d == 0) fr.put(atomicAdd(&Fsh, 1), p, r0, v);
+  }
+  for (int l = lane; l < p.L; l += 32) {
+    lp[l] = 0;
+    lb[l] = 0;
+  }
+  __syncwarp();
+
+  int nd = 0;
+  long long ms = 0;
+  const bool vdnn = p.policy == KS_POLICY_VDNN;
+  for (;;) {
+    const int F = *((volatile int*)&Fsh);
+    if (F == 0) break;
+    int elig = -1;
+    if (vdnn) {
+      // eligible malloc: max (conv rank, -id) among frontier mallocs
+      int bk = INT_MIN, br = INT_MAX, bpos = -1;
+      for (int i = lane; i < F; i += 32) {
+        long long r;
+        int vv, rk, ln;
+        fr.get(i, p, r, vv, rk, ln);
+        if (!(p.flags[vv] & KS_TASK_VDNN_MALLOC)) continue;
+        const int key = p.vrank ? p.vrank[vv] : -1;
+        if (key > bk || (key == bk && rk < br)) {
+          bk = key;
+          br = rk;
+          bpos = i;
+        }
+      }
+      argmax_reduce(bk, br, bpos);
+      if (bpos >= 0) {
+        long long r;
+        int rk, ln;
+        fr.get(bpos, p, r, elig, rk, ln);
+      }
+    }
+    long long be = LLONG_MAX;
+    int br = INT_MAX, bpos = -1;
+    for (int i = lane; i < F; i += 32) {
+      long long r;
+      int vv, rk, ln;
+      fr.get(i, p, r, vv, rk, ln);
+      if (vdnn && (p.flags[vv] & KS_TASK_VDNN_MALLOC) && vv != elig) continue;
+      const long long eff = p.zero_time ? 0 : max(lp[ln], r);
+      if (eff < be || (eff == be && rk < br)) {
+        be = eff;
+        br = rk;
+        bpos = i;
+      }
+    }
+    argmin_reduce(be, br, bpos);
+    if (p.policy == KS_POLICY_PRIORITY) {
+      long long r0;
+      int v0, rk0, ln0;
+      fr.get(bpos, p, r0, v0, rk0, ln0);
+      if (p.flags[v0] & KS_TASK_COMM) {
+        int bk = INT_MIN, br2 = INT_MAX, bpos2 = -1;
+        for (int i = lane; i < F; i += 32) {
+          long long r;
+          int vv, rk, ln;
+          fr.get(i, p, r, vv, rk, ln);
+          if (!(p.flags[vv] & KS_TASK_COMM)) continue;
+          const long long eff = max(lp[ln], r);
+          if (eff != be) continue;
+          const int key = p.prio[vv];
+          if (key > bk || (key == bk && rk < br2)) {
+            bk = key;
+            br2 = rk;
+            bpos2 = i;
+          }
+        }
+        argmax_reduce(bk, br2, bpos2);
+        bpos = bpos2;
+      }
+    }
+    long long rv;
+    int v, rk, ln;
+    fr.get(bpos, p, rv, v, rk, ln);
+    __syncwarp();
+    long long d = 0, g = 0, st = 0;
+    if (!p.zero_time) {
+      if (p.dense32)
+        d = p.dense32[(long long)v * p.dense_ld + s];
+      else if (p.dense64)
+        d = p.dense64[(long long)v * p.dense_ld + s];
+      else
+        d = p.dur[v];
+      if (p.ovr_row && p.ovr_row[v] >= 0) d = p.ovr[(long long)p.ovr_row[v] * p.S + s];
+      const unsigned grp = p.group ? p.group[v] : 0u;
+      if (grp != 0u)
+        for (int e = e0; e < e1; ++e) {
+          const ScaleStepDev sd = p.scale[e];
+          if (grp >= (unsigned)sd.lo && grp <= (unsigned)sd.hi) d = ls_scale(d, sd.num, sd.den);
+        }
+      g = p.gap[v];
+      st = max(lp[ln], rv);
+    }
+    const long long fin = st + d;
+    const long long rel = fin + g;
+    if (lane == 0) {
+      if (bpos != F - 1) {
+        long long r2;
+        int v2, rk2, ln2;
+        fr.get(F - 1, p, r2, v2, rk2, ln2);
+        fr.put(bpos, p, r2, v2);
+      }
+      Fsh = F - 1;
+      lp[ln] = rel;
+      lb[ln] += d;
+      if (p.start) p.start[(long long)v * p.start_ld + s] = st;
+      if (p.schedule) p.schedule[(long long)s * N + nd] = v;
+    }
+    ms = max(ms, fin);
+    ++nd;
+    __syncwarp();
+    const int c0 = p.child_ptr[v], c1 = p.child_ptr[v + 1];
+    for (int j = c0 + lane; j < c1; j += 32) {
+      const int c = p.child[j];
+      const long long old = atomicMax(&rdy[c], rel);
+      if (atomicSub(&rem[c], 1) == 1) fr.put(atomicAdd(&Fsh, 1), p, max(old, rel), c);
+    }
+    __syncwarp();
+  }
+  if (lane == 0) {
+    if (p.makespan) p.makespan[s] = ms;
+    if (p.dispatched) p.dispatched[s] = nd;
+  }
+  if (p.lane_busy)
+    for (int l = lane; l < p.L; l += 32) p.lane_busy[(long long)s * p.L + l] = lb[l];
+}
+
+cudaError_t launch_listsched(const ListParams& p, cudaStream_t stream) {
+  const size_t smem = (size_t)kFrontCap * (8 + 4 + 4 + 4) + (size_t)p.L * 16;
+  if (smem > 220 * 1024) return cudaErrorInvalidValue;
+  cudaError_t err = cudaFuncSetAttribute(listsched_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
+  listsched_kernel<<<p.S, 32, smem, stream>>>(p);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace ddsim
