@@ -1,0 +1,334 @@
+"""Benchmark: batched simulate() throughput on BASELINE config 4.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[3]): Monte-Carlo duration-jitter sweep of a
+100k-task GPT-style iteration graph (1 CPU thread + 2 CUDA streams),
+65,536 scenarios per GPU.  Scenario s of task v runs for
+d' = floor((2 d k + 1000) / 2000) with k ~ U{900..1100} (round_half_up of
+d * k/1000, transform.py:174-183), materialised as int32 [rows][S] in HBM.
+
+A step = one pass of the hot path (maxplus_sim) over one batch: start times
+of every (task, scenario), per-scenario makespan and lane busy times.
+`value` = scenario x task updates / s with inputs resident in HBM; `e2e` =
+the same through the C-ABI host-buffer entry point (ks_simulate_host), with
+the H2D of durations and D2H of all results inside the timed region.
+
+Multi-GPU (torchrun): one process per GPU, scenarios sharded (weak scaling:
+65,536 per GPU), no data-path collective; barrier + max-over-ranks timing.
+
+--impl reference: the reference algorithm (Alg. 1, sim.py:89-142) as the C
+oracle port on the host cores (the reference is pure Python and cannot be
+installed on the GPU box), same metric.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+N_TASKS = 100_000
+S_PER_GPU = 65_536
+METRIC = "scenario x task updates/sec"
+UNIT = "updates/s"
+BYTES_PER_UPDATE = 12  # int32 duration read + int64 start write
+
+
+def _dist():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return ws, rank, local
+
+
+def _peaks():
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return float(d.get("hbm_gbs", 6551.0)), "measured"
+    return 6650.0, "fallback"
+
+
+def _ncu_traffic(kernel: str):
+    p = ROOT / "profiles" / "ncu_summary.json"
+    if not p.exists():
+        return None
+    try:
+        d = json.loads(p.read_text())
+        rec = d.get(kernel)
+        return None if rec is None else rec.get("dram_bytes_per_launch")
+    except Exception:  # noqa: BLE001
+        return None
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md)."""
+
+    def __init__(self, index: int):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.p = None
+
+    def stop(self) -> dict:
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi missing"]}
+        self.p.terminate()
+        self.p.wait()
+        rows = [l.split(",") for l in Path(self.f.name).read_text().splitlines() if l.strip()]
+        sm = [float(r[1]) for r in rows if len(r) > 2 and r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if len(r) > 2 and r[2].strip().replace(".", "").isdigit()]
+        reasons = set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for r in rows:
+            for k, nm in enumerate(names):
+                if len(r) > 5 + k and "Active" in r[5 + k] and "Not" not in r[5 + k]:
+                    reasons.add(nm)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
+                "samples": len(rows)}
+
+
+def build_workload(device: int):
+    from paper_2006_03318_b200.frozen import FrozenGraph
+    from paper_2006_03318_b200.workloads import gpt_trace
+
+    w = gpt_trace(seed=0, n_tasks=N_TASKS)
+    fz = FrozenGraph.from_graph(w.graph, device=device)
+    return w, fz
+
+
+def cpu_baseline(w, fz, target_s: float = 12.0) -> dict:
+    """The reference algorithm (C port of Alg. 1) on the host cores, on a
+    bounded sample of the same workload (scenarios of the same jitter law)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    from oracle import OracleGraph  # CPU baseline leg (checker library)
+
+    threads = os.cpu_count() or 1
+    og = OracleGraph.from_graph(w.graph)
+    base = og.dur
+    rng = np.random.default_rng(1234)
+    S = threads * 2
+    t_used = 0.0
+    upd = 0
+    while True:
+        k = rng.integers(900, 1101, size=(len(base), S))
+        dense = np.ascontiguousarray(((2 * base[:, None] * k + 1000) // 2000).astype(np.int32))
+        t0 = time.perf_counter()
+        _ms, _st, u = og.simulate_batch(dense, threads, "default")
+        dt = time.perf_counter() - t0
+        t_used += dt
+        upd += u
+        if t_used >= target_s or S >= 4096:
+            break
+        S = min(4096, max(S * 2, int(S * target_s / max(dt, 1e-3) * 0.5)))
+    return {"value": upd / t_used, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample": f"{upd // len(base)} scenarios x {len(base)} tasks of the config-4 graph, "
+                      f"{t_used:.1f} s wall, oracle/ddsim_oracle.c Alg.1 port (pthreads)"}
+
+
+def run_reference(args):
+    ws, rank, _local = _dist()
+    if rank != 0:
+        return
+    from paper_2006_03318_b200.workloads import gpt_trace
+
+    w = gpt_trace(seed=0, n_tasks=N_TASKS)
+
+    class _F:  # cpu_baseline only needs w
+        pass
+    vals = []
+    cb = None
+    for i in range(args.warmup + args.steps):
+        cb = cpu_baseline(w, _F, target_s=3.0 if i < args.warmup else 6.0)
+        if i >= args.warmup:
+            vals.append(cb["value"])
+    v = statistics.median(vals)
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws,
+            "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": "config4 monte-carlo jitter: gpt-style 100k tasks (1 cpu + 2 "
+                                   "streams), jitter k~U{900..1100}", "tasks": N_TASKS,
+                       "scenarios_per_step": "sample (see cpu_baseline.sample)"},
+            "cpu_baseline": dict(cb, value=v),
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+
+    ws, rank, local = _dist()
+    dev = local
+    torch.cuda.set_device(dev)
+    if ws > 1:
+        import torch.distributed as dist
+
+        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+    from paper_2006_03318_b200 import _native as N
+    from paper_2006_03318_b200.batch import ScenarioTable, simulate_batch_device
+
+    w, fz = build_workload(dev)
+    S = args.scenarios
+    rows, L = fz.n, fz.L
+    # ---- device-resident inputs: dense jitter durations [rows][S] int32 ----
+    base = torch.from_numpy(fz.duration[fz.order].copy()).to(f"cuda:{dev}")
+    dense = torch.empty((rows, S), dtype=torch.int32, device=f"cuda:{dev}")
+    gen = torch.Generator(device=f"cuda:{dev}")
+    gen.manual_seed(1000 + rank)
+    step_rows = max(1, (1 << 28) // S)
+    for r0 in range(0, rows, step_rows):
+        r1 = min(rows, r0 + step_rows)
+        k = torch.randint(900, 1101, (r1 - r0, S), generator=gen, device=f"cuda:{dev}",
+                          dtype=torch.int64)
+        dense[r0:r1] = ((2 * base[r0:r1, None] * k + 1000) // 2000).to(torch.int32)
+        del k
+    start = torch.empty((rows, S), dtype=torch.int64, device=f"cuda:{dev}")
+    ms = torch.empty(S, dtype=torch.int64, device=f"cuda:{dev}")
+    lb = torch.empty((S, L), dtype=torch.int64, device=f"cuda:{dev}")
+    table = ScenarioTable(n_scenarios=S, dense=dense)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        simulate_batch_device(fz, table, makespan=ms, lane_busy=lb, start=start,
+                              stream=stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    clocks = Clocks(dev) if rank == 0 else None
+    time.sleep(0.3 if clocks else 0)
+    l0 = N.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    torch.cuda.synchronize()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = N.launch_count() - l0
+    elapsed_ms = e0.elapsed_time(e1)
+    if ws > 1:
+        t = torch.tensor([elapsed_ms], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        elapsed_ms = float(t.item())
+        dist.barrier()
+    clk = clocks.stop() if clocks else None
+    updates_per_step = rows * S
+    total = updates_per_step * args.steps * ws
+    value = total / (elapsed_ms / 1e3)
+    per_launch_ms = elapsed_ms / args.steps
+    peak, peak_src = _peaks()
+    achieved = updates_per_step * BYTES_PER_UPDATE / (per_launch_ms / 1e3) / 1e9
+
+    # sanity: spot-check one scenario against the device list scheduler path is
+    # done in tests; here only assert the makespan is positive
+    assert int(ms[0].item()) > 0
+
+    # ---- e2e through the host-buffer C-ABI (H2D + D2H inside the timed region)
+    e2e = None
+    if not args.no_e2e:
+        S_e = S
+        h_dense = torch.empty((rows, S_e), dtype=torch.int32, pin_memory=True)
+        h_dense.copy_(dense[:, :S_e])
+        h_start = torch.empty((rows, S_e), dtype=torch.int64, pin_memory=True)
+        h_ms = np.empty(S_e, np.int64)
+        h_lb = np.empty((S_e, L), np.int64)
+        import ctypes as C
+
+        def e2e_step():
+            sc = N.ScenariosDesc()
+            sc.n_scenarios = S_e
+            sc.dense_kind = 1
+            sc.dense = h_dense.data_ptr()
+            sc.dense_ld = S_e
+            out = N.SimOut()
+            out.start, out.start_ld = h_start.data_ptr(), S_e
+            out.makespan, out.lane_busy = h_ms.ctypes.data, h_lb.ctypes.data
+            N.check(N.lib().ks_simulate_host(fz.handle, C.byref(sc), 0, 0, C.byref(out)))
+
+        e2e_step()
+        if ws > 1:
+            dist.barrier()
+        t0 = time.perf_counter()
+        n_e2e = max(1, min(args.steps, 2))
+        for _ in range(n_e2e):
+            e2e_step()
+        dt = time.perf_counter() - t0
+        if ws > 1:
+            t = torch.tensor([dt], device=f"cuda:{dev}", dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        assert np.array_equal(h_ms, ms[:S_e].cpu().numpy()), "e2e result differs from device run"
+        e2e = {"value": rows * S_e * n_e2e * ws / dt, "unit": UNIT,
+               "h2d_bytes_per_step": rows * S_e * 4,
+               "d2h_bytes_per_step": rows * S_e * 8 + S_e * 8 + S_e * L * 8}
+
+    cb = None
+    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+        cb = cpu_baseline(w, fz)
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": per_launch_ms, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": "config4 monte-carlo jitter: gpt-style iteration graph "
+                                   f"({rows} tasks, 1 cpu thread + 2 streams), {S} scenarios "
+                                   "per GPU, k~U{900..1100} int32 durations resident in HBM",
+                       "tasks": rows, "scenarios_per_gpu": S, "lanes": L,
+                       "l2": "inputs (26 GB) >> 126 MB L2; no flush needed",
+                       "graph_slots_smem": fz.info.n_slots_smem,
+                       "graph_slots_spill": fz.info.n_slots - fz.info.n_slots_smem},
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": updates_per_step * BYTES_PER_UPDATE,
+                         "traffic": _ncu_traffic("maxplus_kernel")},
+            "cpu_baseline": cb,
+            "e2e": e2e,
+            "gpu_launches": launches,
+            "clocks": clk,
+        }
+        print(json.dumps(line), flush=True)
+    if ws > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--scenarios", type=int, default=S_PER_GPU)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

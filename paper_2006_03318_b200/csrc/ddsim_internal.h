@@ -28,6 +28,43 @@ struct alignas(16) NodeRec {
 };
 static_assert(sizeof(NodeRec) == 64, "NodeRec must be 64 bytes");
 
+// Compact record of the dense-duration program (no chains): 16 bytes.
+// op bits say where the predecessors' rel values are: in registers (the two
+// previous records -- most lane-chain and launch edges are that short), in
+// shared-memory slots s0/s1, or (rare, DOP_SLOW) in the side tables / global
+// spill slots.
+struct alignas(16) DenseRec {
+  long long gap;
+  short s0, s1;         // shared-memory slot ids (DOP_S0 / DOP_S1)
+  short out;            // slot receiving rel (DOP_OUT_SMEM / DOP_OUT_GLOBAL)
+  unsigned char lane;
+  unsigned char op;
+};
+static_assert(sizeof(DenseRec) == 16, "DenseRec must be 16 bytes");
+enum {
+  DOP_PREV = 1, DOP_PREV2 = 2, DOP_S0 = 4, DOP_S1 = 8, DOP_SLOW = 16,
+  DOP_OUT_SMEM = 32, DOP_OUT_GLOBAL = 64
+};
+
+struct DenseParams {
+  const DenseRec* prog;
+  int n_rec;
+  const int* side_off;        // [n_rec+1] slow-path pred slot ids (smem < ksm <= global)
+  const int* side_slots;
+  const long long* side_ready;  // [n_rec] ready floor (or null)
+  int ksm, kglob;
+  long long* gslots;
+  long long s_pad;
+  int S, L;
+  int V;                      // scenarios per thread (1 or 2)
+  const long long* dense64;   // int64 mode
+  long long dense_ld;
+  long long* start;
+  long long start_ld;
+  long long* makespan;
+  long long* lane_busy;
+};
+
 struct ChainDesc {
   int first_row;   // members occupy frozen rows first_row .. first_row+B-1
   int B;
@@ -114,11 +151,14 @@ struct ListParams {
 // kernel launchers (maxplus.cu / listsched.cu)
 cudaError_t launch_maxplus(const MaxplusParams& p, const int* dense32,
                            cudaStream_t stream);
+cudaError_t launch_maxplus_dense(const DenseParams& p, const int* dense32, int dkind,
+                                 cudaStream_t stream);
 cudaError_t launch_listsched(const ListParams& p, cudaStream_t stream);
 cudaError_t launch_fill_i64(long long* p, long long v, long long n, cudaStream_t s);
 cudaError_t launch_fill_i32(int* p, int v, long long n, cudaStream_t s);
 cudaError_t launch_patch_ovr(NodeRec* prog, int n_rec, const int* ovr_map, cudaStream_t st);
 int maxplus_block_dim(int S, int dmode, int num_sms);
+int maxplus_dense_block_dim(int S, int V, int num_sms);
 
 void note_launch(int n = 1);
 

@@ -76,6 +76,13 @@ struct ks_graph {
   std::vector<int> row_of;       // input index -> frozen row
   std::vector<int> level;        // per frozen row
   std::vector<int> rank_row;     // id rank per frozen row
+  // dense-duration program (no chains, <= 255 lanes)
+  bool has_dense = false;
+  int dksm = 0, dkglob = 0;
+  DenseRec* d_dprog = nullptr;
+  int* d_side_off = nullptr;
+  int* d_side_slots = nullptr;
+  long long* d_side_ready = nullptr;
   // device
   NodeRec* d_prog = nullptr;
   int* d_extra = nullptr;
@@ -492,6 +499,109 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   g->perm_ld = perm_off;
   g->n_rec = R;
 
+  // ---- dense program: register forwarding for the two previous records ----
+  if (NC == 0 && L <= 255) {
+    std::vector<int> pos(n, -1);
+    for (int i = 0; i < R; ++i) pos[corder[i]] = i;
+    std::vector<int> far_use(n, -1);  // last consumer more than 2 records later
+    for (int i = 0; i < R; ++i) {
+      const int v = corder[i];
+      for (int k = pptr[v]; k < pptr[v + 1]; ++k) {
+        const int u = padj[k];
+        if (i - pos[u] > 2) far_use[u] = std::max(far_use[u], i);
+      }
+    }
+    std::vector<int> dslot(n, -1);
+    std::vector<char> dglob(n, 0);
+    std::priority_queue<int, std::vector<int>, std::greater<int>> fs, fg;
+    int ns = 0, ngl = 0;
+    std::vector<std::vector<int>> frees_at(R);
+    for (int i = 0; i < R; ++i) {
+      const int v = corder[i];
+      if (far_use[v] >= 0) {
+        const bool shrt = far_use[v] - i <= kShortRange;
+        if (shrt && !fs.empty()) {
+          dslot[v] = fs.top();
+          fs.pop();
+        } else if (shrt && ns < kSmemSlotsMax) {
+          dslot[v] = ns++;
+        } else {
+          dglob[v] = 1;
+          if (!fg.empty()) {
+            dslot[v] = fg.top();
+            fg.pop();
+          } else {
+            dslot[v] = ngl++;
+          }
+        }
+        frees_at[far_use[v]].push_back(v);
+      }
+      for (int u : frees_at[i]) (dglob[u] ? fg : fs).push(dslot[u]);
+    }
+    g->dksm = ns;
+    g->dkglob = ngl;
+    std::vector<DenseRec> dprog(R);
+    std::vector<int> side_off(R + 1, 0);
+    std::vector<int> side_slots;
+    std::vector<long long> side_ready;
+    bool any_ready = false;
+    bool ok = ns + ngl < 32000;
+    for (int i = 0; i < R && ok; ++i) {
+      const int v = corder[i];
+      DenseRec r;
+      memset(&r, 0, sizeof(r));
+      r.gap = d->gap[v];
+      r.lane = (unsigned char)d->lane[v];
+      unsigned op = 0;
+      if (dslot[v] >= 0) {
+        op |= dglob[v] ? DOP_OUT_GLOBAL : DOP_OUT_SMEM;
+        r.out = (short)(dglob[v] ? ns + dslot[v] : dslot[v]);
+      }
+      int nsm_pred = 0;
+      for (int k = pptr[v]; k < pptr[v + 1]; ++k) {
+        const int u = padj[k];
+        const int dist = i - pos[u];
+        if (dist == 1) {
+          op |= DOP_PREV;
+        } else if (dist == 2) {
+          op |= DOP_PREV2;
+        } else if (!dglob[u] && nsm_pred == 0) {
+          op |= DOP_S0;
+          r.s0 = (short)dslot[u];
+          ++nsm_pred;
+        } else if (!dglob[u] && nsm_pred == 1) {
+          op |= DOP_S1;
+          r.s1 = (short)dslot[u];
+          ++nsm_pred;
+        } else {
+          op |= DOP_SLOW;
+          side_slots.push_back(dglob[u] ? ns + dslot[u] : dslot[u]);
+        }
+      }
+      side_off[i + 1] = (int)side_slots.size();
+      const long long rt = d->ready_time ? d->ready_time[v] : 0;
+      if (rt != 0) {
+        op |= DOP_SLOW;
+        any_ready = true;
+      }
+      r.op = (unsigned char)op;
+      dprog[i] = r;
+    }
+    if (ok) {
+      if (any_ready) {
+        side_ready.resize(R);
+        for (int i = 0; i < R; ++i) side_ready[i] = d->ready_time[corder[i]];
+      }
+      g->has_dense = true;
+      g->d_dprog = dev_upload(dprog);
+      if (!side_slots.empty()) {
+        g->d_side_off = dev_upload(side_off);
+        g->d_side_slots = dev_upload(side_slots);
+      }
+      g->d_side_ready = dev_upload(side_ready);
+    }
+  }
+
   // ---- list-scheduler arrays (frozen rows, multiset edges) -------------------
   std::vector<int> ch_ptr(n + 1, 0), ch_adj(E), indeg(n, 0);
   for (long long k = 0; k < E; ++k) {
@@ -540,6 +650,9 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
 
 void free_graph(ks_graph* g) {
   if (!g) return;
+  void* dptrs[] = {g->d_dprog, g->d_side_off, g->d_side_slots, g->d_side_ready};
+  for (void* p : dptrs)
+    if (p) cudaFree(p);
   void* ptrs[] = {g->d_prog,  g->d_extra, g->d_chains, g->d_members, g->d_child_ptr,
                   g->d_child, g->d_indeg, g->d_lane,   g->d_dur,     g->d_gap,
                   g->d_ready, g->d_rank,  g->d_prio,   g->d_flags,   g->d_group};
@@ -648,7 +761,6 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
   if (policy < 0 || policy > 2) fail(KS_ERR_INVALID, "unknown policy");
   bool use_max = path == KS_PATH_MAXPLUS ||
                  (path == KS_PATH_AUTO && g->chained && out->schedule == nullptr);
-  if (use_max && !g->chained) fail(KS_ERR_INVALID, "max-plus path needs a lane-chained graph");
   if (!use_max && g->n_chains > 0)
     fail(KS_ERR_UNSUPPORTED, "list scheduling of permutable chains is not supported");
   if (g->n_ordered < g->n) {
@@ -661,7 +773,44 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
   const bool dense = sc->dense_kind != 0 && sc->dense != nullptr;
   build_tables(g, sc, T, true, policy == KS_POLICY_VDNN);
 
-  if (use_max) {
+  if (use_max && dense && g->has_dense && sc->n_overrides == 0 && !sc->scale_ptr) {
+    DenseParams p;
+    memset(&p, 0, sizeof(p));
+    p.prog = g->d_dprog;
+    p.n_rec = g->n_rec;
+    p.side_off = g->d_side_off;
+    p.side_slots = g->d_side_slots;
+    p.V = (S % 2 == 0 && out->start_ld % 2 == 0 && sc->dense_ld % 2 == 0 &&
+           reinterpret_cast<uintptr_t>(out->start) % 16 == 0) ? 2 : 1;
+    p.side_ready = g->d_side_ready;
+    p.ksm = g->dksm;
+    p.kglob = g->dkglob;
+    p.S = S;
+    p.L = g->L;
+    if (sc->dense_ld < S) fail(KS_ERR_INVALID, "dense_ld < n_scenarios");
+    const int dk = sc->dense_kind == 1 ? 1 : 2;
+    if (dk == 1 && (reinterpret_cast<uintptr_t>(sc->dense) % 16 != 0 || sc->dense_ld % 4 != 0))
+      fail(KS_ERR_INVALID, "int32 dense durations need 16B alignment and dense_ld % 4 == 0");
+    if (dk == 2) p.dense64 = reinterpret_cast<const long long*>(sc->dense);
+    p.dense_ld = sc->dense_ld;
+    p.start = reinterpret_cast<long long*>(out->start);
+    p.start_ld = out->start_ld;
+    p.makespan = reinterpret_cast<long long*>(out->makespan);
+    p.lane_busy = reinterpret_cast<long long*>(out->lane_busy);
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device);
+    const int BD = maxplus_dense_block_dim(S, p.V, nsm);
+    p.s_pad = (long long)((S + BD * p.V - 1) / (BD * p.V)) * BD * p.V;
+    if (p.kglob > 0) p.gslots = T.scratch<long long>((size_t)p.kglob * p.s_pad);
+    if (g->n_rec > 0) {
+      CUDA_TRY(launch_maxplus_dense(p, dk == 1 ? reinterpret_cast<const int*>(sc->dense) : nullptr,
+                                    dk, stream));
+    } else {
+      if (out->makespan) CUDA_TRY(launch_fill_i64(p.makespan, 0, S, stream));
+      if (out->lane_busy) CUDA_TRY(launch_fill_i64(p.lane_busy, 0, (long long)S * g->L, stream));
+    }
+    if (out->dispatched) CUDA_TRY(launch_fill_i32(out->dispatched, g->n, S, stream));
+  } else if (use_max) {
     MaxplusParams p;
     memset(&p, 0, sizeof(p));
     p.n_rec = g->n_rec;

@@ -211,7 +211,7 @@ __global__ void __launch_bounds__(256) maxplus_kernel(const __grid_constant__ CU
     const NodeRec* R = pstage + st * kChunk;
     const int* T = tstage + st * kChunk * BD;
     const int nrec = min(kChunk, p.n_rec - c * kChunk);
-#pragma unroll 4
+#pragma unroll 1
     for (int j = 0; j < nrec; ++j) {
       const int kind = R[j].kind;
       if (kind != 0) {

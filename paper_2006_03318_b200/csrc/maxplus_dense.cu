@@ -1,0 +1,276 @@
+// maxplus_dense: max-plus simulate() for dense per-scenario durations
+// (Monte-Carlo jitter, BASELINE config 4).  Same recurrence as maxplus.cu
+// (sim.py:89-142 on lane-chained graphs == synthetic.py:35-48):
+//     start(v) = max(ready, max_{u->v} start(u) + dur(u) + gap(u))
+// Specialisation for the HBM-bound case:
+//   * V scenarios per thread (int32 pairs in, 128-bit int64 stores out);
+//   * 16-byte program records + the [rows x (V*BD)] int32 duration tile of
+//     each chunk staged by cp.async.bulk / 2D TMA on one mbarrier, kStages
+//     chunks ahead;
+//   * rel of the two previous records in registers; only values read more
+//     than two records later go through shared memory (compiled slots).
+#include "ddsim_internal.h"
+
+#include <algorithm>
+#include <climits>
+#include <cudaTypedefs.h>
+
+namespace ddsim {
+
+namespace {
+constexpr int kChunkD = 16;
+constexpr int kStagesD = 4;
+
+__device__ __forceinline__ unsigned su32(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void d_mbar_init(unsigned long long* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void d_expect(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void d_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra W_%=;\n}\n" ::"r"(su32(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void d_bulk(void* dst, const void* src, unsigned bytes,
+                                       unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(su32(dst)), "l"(src), "r"(bytes), "r"(su32(bar)) : "memory");
+}
+__device__ __forceinline__ void d_tile(void* dst, const CUtensorMap* map, int x, int y,
+                                       unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(su32(dst)), "l"(map), "r"(x), "r"(y), "r"(su32(bar))
+      : "memory");
+}
+
+template <int V>
+struct Vec {
+  long long v[V];
+};
+
+template <int V>
+__device__ __forceinline__ void vmax(Vec<V>& a, const Vec<V>& b) {
+#pragma unroll
+  for (int i = 0; i < V; ++i) a.v[i] = max(a.v[i], b.v[i]);
+}
+}  // namespace
+
+// V scenarios per thread; DK: 1 = int32 durations via TMA tiles,
+// 2 = int64 durations via direct global loads.
+template <int V, int DK>
+__global__ void __launch_bounds__(256) maxplus_dense_kernel(const __grid_constant__ CUtensorMap tmap,
+                                                            const DenseParams p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int BD = blockDim.x;
+  const int W = BD * V;  // scenarios per CTA
+  const int tid = threadIdx.x;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem);
+  DenseRec* pst = reinterpret_cast<DenseRec*>(smem + 128);
+  unsigned char* cur = smem + 128 + kStagesD * kChunkD * sizeof(DenseRec);
+  int* tst = reinterpret_cast<int*>(cur);
+  if (DK == 1) cur += (size_t)kStagesD * kChunkD * W * sizeof(int);
+  Vec<V>* slots = reinterpret_cast<Vec<V>*>(cur);  // [ksm][BD]
+  cur += (size_t)p.ksm * BD * sizeof(Vec<V>);
+  Vec<V>* lb = reinterpret_cast<Vec<V>*>(cur);     // [L][BD]
+
+  const int s0 = blockIdx.x * W;
+  const int s = s0 + tid * V;         // first scenario of this thread
+  const bool act = s < p.S;           // S % V == 0 is guaranteed by the host
+  for (int l = 0; l < p.L; ++l) {
+    Vec<V> z;
+#pragma unroll
+    for (int i = 0; i < V; ++i) z.v[i] = 0;
+    lb[l * BD + tid] = z;
+  }
+  const int nchunks = (p.n_rec + kChunkD - 1) / kChunkD;
+  const unsigned tile_bytes = DK == 1 ? (unsigned)(kChunkD * W * sizeof(int)) : 0u;
+  auto issue = [&](int c) {
+    const int st = c % kStagesD;
+    const int nrec = min(kChunkD, p.n_rec - c * kChunkD);
+    const unsigned pb = (unsigned)(nrec * sizeof(DenseRec));
+    d_expect(&bars[st], pb + tile_bytes);
+    d_bulk(pst + st * kChunkD, p.prog + (long long)c * kChunkD, pb, &bars[st]);
+    if (DK == 1) d_tile(tst + st * kChunkD * W, &tmap, s0, c * kChunkD, &bars[st]);
+  };
+  if (tid == 0) {
+    for (int i = 0; i < kStagesD; ++i) d_mbar_init(&bars[i]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int c = 0; c < min(kStagesD, nchunks); ++c) issue(c);
+
+  Vec<V> ms, prev, prev2;
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    ms.v[i] = 0;
+    prev.v[i] = LLONG_MIN;
+    prev2.v[i] = LLONG_MIN;
+  }
+  const long long ld = p.start_ld;
+  long long* sp = (act && p.start) ? p.start + s : nullptr;  // advanced one row per record
+  const long long* dp = DK == 2 ? p.dense64 + (act ? s : 0) : nullptr;
+  for (int c = 0; c < nchunks; ++c) {
+    const int st = c % kStagesD;
+    d_wait(&bars[st], (unsigned)((c / kStagesD) & 1));
+    const DenseRec* R = pst + st * kChunkD;
+    const int* T = tst + st * kChunkD * W + tid * V;
+    const int nrec = min(kChunkD, p.n_rec - c * kChunkD);
+#pragma unroll 2
+    for (int j = 0; j < nrec; ++j) {
+      const DenseRec r = R[j];
+      Vec<V> d;
+      if (DK == 1) {
+        if (V == 2) {
+          const int2 t2 = *reinterpret_cast<const int2*>(T + j * W);
+          d.v[0] = t2.x;
+          d.v[V - 1] = t2.y;
+        } else {
+          d.v[0] = T[j * W];
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < V; ++i) d.v[i] = dp[i];
+        dp += p.dense_ld;
+      }
+      Vec<V> sv;
+#pragma unroll
+      for (int i = 0; i < V; ++i) sv.v[i] = 0;
+      const unsigned op = r.op;
+      if (op & DOP_PREV) vmax(sv, prev);
+      if (op & DOP_PREV2) vmax(sv, prev2);
+      if (op & DOP_S0) vmax(sv, slots[r.s0 * BD + tid]);
+      if (op & DOP_S1) vmax(sv, slots[r.s1 * BD + tid]);
+      if (op & DOP_SLOW) {
+        const int row = c * kChunkD + j;
+        if (p.side_ready) {
+          const long long rd = p.side_ready[row];
+#pragma unroll
+          for (int i = 0; i < V; ++i) sv.v[i] = max(sv.v[i], rd);
+        }
+        if (p.side_off)
+          for (int k = p.side_off[row]; k < p.side_off[row + 1]; ++k) {
+            const int code = p.side_slots[k];
+            if (code < p.ksm) {
+              vmax(sv, slots[code * BD + tid]);
+            } else if (act) {
+              const long long* g = p.gslots + (long long)(code - p.ksm) * p.s_pad + s;
+#pragma unroll
+              for (int i = 0; i < V; ++i) sv.v[i] = max(sv.v[i], g[i]);
+            }
+          }
+      }
+      if (sp) {
+        if (V == 2)
+          __stcs(reinterpret_cast<longlong2*>(sp), make_longlong2(sv.v[0], sv.v[V - 1]));
+        else
+          __stcs(sp, sv.v[0]);
+        sp += ld;
+      }
+      Vec<V> rel;
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        const long long fin = sv.v[i] + d.v[i];
+        ms.v[i] = max(ms.v[i], fin);
+        rel.v[i] = fin + r.gap;
+      }
+      if (op & DOP_OUT_SMEM) slots[r.out * BD + tid] = rel;
+      if ((op & DOP_OUT_GLOBAL) && act) {
+        long long* g = p.gslots + (long long)(r.out - p.ksm) * p.s_pad + s;
+#pragma unroll
+        for (int i = 0; i < V; ++i) g[i] = rel.v[i];
+      }
+      Vec<V>& acc = lb[r.lane * BD + tid];
+#pragma unroll
+      for (int i = 0; i < V; ++i) acc.v[i] += d.v[i];
+      prev2 = prev;
+      prev = rel;
+    }
+    __syncthreads();
+    if (tid == 0 && c + kStagesD < nchunks) issue(c + kStagesD);
+  }
+  if (act) {
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      if (p.makespan) p.makespan[s + i] = ms.v[i];
+      if (p.lane_busy)
+        for (int l = 0; l < p.L; ++l) p.lane_busy[(long long)(s + i) * p.L + l] = lb[l * BD + tid].v[i];
+    }
+  }
+}
+
+static size_t dense_smem(int V, int dk, int BD, int ksm, int L) {
+  size_t b = 128 + (size_t)kStagesD * kChunkD * sizeof(DenseRec);
+  if (dk == 1) b += (size_t)kStagesD * kChunkD * BD * V * sizeof(int);
+  return b + (size_t)ksm * BD * V * 8 + (size_t)L * BD * V * 8;
+}
+
+// Threads per CTA: two CTAs per SM cover all scenarios in one wave.
+int maxplus_dense_block_dim(int S, int V, int num_sms) {
+  long long per = (S / V + 2LL * num_sms - 1) / (2LL * num_sms);
+  int bd = (int)(((per + 31) / 32) * 32);
+  const int cap = 256 / V;  // TMA box inner extent <= 256 elements
+  return bd < 32 ? 32 : (bd > cap ? cap : bd);
+}
+
+template <int V, int DK>
+static cudaError_t launch_v(const CUtensorMap& tmap, const DenseParams& p, int grid, int BD,
+                            size_t smem, cudaStream_t stream) {
+  cudaError_t err = cudaFuncSetAttribute(maxplus_dense_kernel<V, DK>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
+  maxplus_dense_kernel<V, DK><<<grid, BD, smem, stream>>>(tmap, p);
+  return cudaSuccess;
+}
+
+cudaError_t launch_maxplus_dense(const DenseParams& p, const int* dense32, int dkind,
+                                 cudaStream_t stream) {
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int V = p.V == 2 ? 2 : 1;
+  const int BD = maxplus_dense_block_dim(p.S, V, nsm);
+  const int W = BD * V;
+  const int grid = (p.S + W - 1) / W;
+  if ((long long)grid * W > p.s_pad) return cudaErrorInvalidValue;
+  const size_t smem = dense_smem(V, dkind, BD, p.ksm, p.L);
+  CUtensorMap tmap;
+  memset(&tmap, 0, sizeof(tmap));
+  if (dkind == 1) {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+            cudaSuccess || q != cudaDriverEntryPointSuccess)
+      return cudaErrorNotSupported;
+    auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    cuuint64_t dims[2] = {(cuuint64_t)p.S, (cuuint64_t)p.n_rec};
+    cuuint64_t strides[1] = {(cuuint64_t)(p.dense_ld * sizeof(int))};
+    cuuint32_t box[2] = {(cuuint32_t)W, (cuuint32_t)kChunkD};
+    cuuint32_t estr[2] = {1, 1};
+    if (enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, const_cast<int*>(dense32), dims, strides, box,
+            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+      return cudaErrorInvalidValue;
+  }
+  cudaError_t err;
+  if (V == 2)
+    err = dkind == 1 ? launch_v<2, 1>(tmap, p, grid, BD, smem, stream)
+                     : launch_v<2, 2>(tmap, p, grid, BD, smem, stream);
+  else
+    err = dkind == 1 ? launch_v<1, 1>(tmap, p, grid, BD, smem, stream)
+                     : launch_v<1, 2>(tmap, p, grid, BD, smem, stream);
+  if (err != cudaSuccess) return err;
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace ddsim

@@ -116,11 +116,11 @@ def _genspec_graph(golden, name):
 
 @pytest.mark.parametrize("name", ["genspec_1001", "genspec_7", "gpu_bound", "distributed_4"])
 @pytest.mark.parametrize("dtype", [np.int32, np.int64])
-def test_batch_dense_durations_vs_oracle(golden, name, dtype):
+@pytest.mark.parametrize("S", [300, 301])
+def test_batch_dense_durations_vs_oracle(golden, name, dtype, S):
     g = _genspec_graph(golden, name)
     fz = FrozenGraph.from_graph(g)
     assert fz.chained
-    S = 300
     rng = np.random.default_rng(0)
     base = fz.duration[fz.order]                        # frozen rows
     k = rng.integers(900, 1101, size=(fz.n, S))
