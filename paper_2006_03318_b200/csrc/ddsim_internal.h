@@ -43,8 +43,11 @@ struct alignas(16) DenseRec {
 static_assert(sizeof(DenseRec) == 16, "DenseRec must be 16 bytes");
 enum {
   DOP_PREV = 1, DOP_PREV2 = 2, DOP_S0 = 4, DOP_S1 = 8, DOP_SLOW = 16,
-  DOP_OUT_SMEM = 32, DOP_OUT_GLOBAL = 64
+  DOP_OUT_SMEM = 32, DOP_OUT_GLOBAL = 64,
+  DOP_MS = 128          // contributes to makespan (last task of its lane)
 };
+// DenseRec.lane high bit: record has a non-zero gap
+enum { DLANE_GAP = 0x80 };
 
 struct DenseParams {
   const DenseRec* prog;
@@ -57,6 +60,7 @@ struct DenseParams {
   long long s_pad;
   int S, L;
   int V;                      // scenarios per thread (1 or 2)
+  int* neg_flag;              // set when a negative duration is seen (exact rerun)
   const long long* dense64;   // int64 mode
   long long dense_ld;
   long long* start;
@@ -109,6 +113,7 @@ struct MaxplusParams {
   long long start_ld;
   long long* makespan;
   long long* lane_busy;      // [S][L]
+  const int* run_if;         // non-null: run only if *run_if != 0 (exact fallback)
 };
 
 struct ListParams {

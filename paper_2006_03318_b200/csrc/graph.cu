@@ -500,7 +500,10 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   g->n_rec = R;
 
   // ---- dense program: register forwarding for the two previous records ----
-  if (NC == 0 && L <= 255) {
+  bool nonneg = true;
+  for (int i = 0; i < n && nonneg; ++i)
+    if (d->gap[i] < 0 || (d->ready_time && d->ready_time[i] < 0)) nonneg = false;
+  if (NC == 0 && L <= 127 && nonneg) {
     std::vector<int> pos(n, -1);
     for (int i = 0; i < R; ++i) pos[corder[i]] = i;
     std::vector<int> far_use(n, -1);  // last consumer more than 2 records later
@@ -540,6 +543,8 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     }
     g->dksm = ns;
     g->dkglob = ngl;
+    std::vector<int> lane_last(L, -1);
+    for (int i = 0; i < R; ++i) lane_last[d->lane[corder[i]]] = i;
     std::vector<DenseRec> dprog(R);
     std::vector<int> side_off(R + 1, 0);
     std::vector<int> side_slots;
@@ -551,8 +556,9 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
       DenseRec r;
       memset(&r, 0, sizeof(r));
       r.gap = d->gap[v];
-      r.lane = (unsigned char)d->lane[v];
+      r.lane = (unsigned char)(d->lane[v] | (r.gap != 0 ? DLANE_GAP : 0));
       unsigned op = 0;
+      if (!chained || lane_last[d->lane[v]] == i) op |= DOP_MS;
       if (dslot[v] >= 0) {
         op |= dglob[v] ? DOP_OUT_GLOBAL : DOP_OUT_SMEM;
         r.out = (short)(dglob[v] ? ns + dslot[v] : dslot[v]);
@@ -803,8 +809,34 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
     p.s_pad = (long long)((S + BD * p.V - 1) / (BD * p.V)) * BD * p.V;
     if (p.kglob > 0) p.gslots = T.scratch<long long>((size_t)p.kglob * p.s_pad);
     if (g->n_rec > 0) {
+      int* flag = T.scratch<int>(1);
+      CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), stream));
+      p.neg_flag = flag;
       CUDA_TRY(launch_maxplus_dense(p, dk == 1 ? reinterpret_cast<const int*>(sc->dense) : nullptr,
                                     dk, stream));
+      // exact rerun (general kernel, full int64 semantics) only if a negative
+      // duration was seen: the CTAs of this launch exit at once otherwise
+      MaxplusParams q;
+      memset(&q, 0, sizeof(q));
+      q.prog = g->d_prog;
+      q.n_rec = g->n_rec;
+      q.extra = g->d_extra;
+      q.ksm = g->ksm;
+      q.kglob = g->kglob;
+      q.S = S;
+      q.L = g->L;
+      q.dense_kind = dk;
+      q.dense64 = p.dense64;
+      q.dense_ld = sc->dense_ld;
+      q.start = p.start;
+      q.start_ld = p.start_ld;
+      q.makespan = p.makespan;
+      q.lane_busy = p.lane_busy;
+      q.run_if = flag;
+      const int BDq = maxplus_block_dim(S, dk, nsm);
+      q.s_pad = (long long)((S + BDq - 1) / BDq) * BDq;
+      if (q.kglob > 0) q.gslots = T.scratch<long long>((size_t)q.kglob * q.s_pad);
+      CUDA_TRY(launch_maxplus(q, dk == 1 ? reinterpret_cast<const int*>(sc->dense) : nullptr, stream));
     } else {
       if (out->makespan) CUDA_TRY(launch_fill_i64(p.makespan, 0, S, stream));
       if (out->lane_busy) CUDA_TRY(launch_fill_i64(p.lane_busy, 0, (long long)S * g->L, stream));

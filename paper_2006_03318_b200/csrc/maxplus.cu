@@ -162,6 +162,7 @@ template <int DMODE>
 __global__ void __launch_bounds__(256) maxplus_kernel(const __grid_constant__ CUtensorMap tmap,
                                                       const MaxplusParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
+  if (p.run_if != nullptr && *((volatile const int*)p.run_if) == 0) return;
   const int BD = blockDim.x;
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem);
   NodeRec* pstage = reinterpret_cast<NodeRec*>(smem + 128);

@@ -65,6 +65,13 @@ __device__ __forceinline__ void vmax(Vec<V>& a, const Vec<V>& b) {
 
 // V scenarios per thread; DK: 1 = int32 durations via TMA tiles,
 // 2 = int64 durations via direct global loads.
+//
+// Fast-path facts (host-checked: gaps and ready times >= 0, lanes chained;
+// device-checked: durations >= 0, else *neg_flag is set and the host's exact
+// kernel reruns the launch): every rel >= fin >= start >= 0, so the 0 floor of
+// start() is implied by any predecessor, and the makespan is the max finish of
+// the last task of each lane (flagged DOP_MS) because a lane's finishes never
+// decrease along its chain.
 template <int V, int DK>
 __global__ void __launch_bounds__(256) maxplus_dense_kernel(const __grid_constant__ CUtensorMap tmap,
                                                             const DenseParams p) {
@@ -82,8 +89,8 @@ __global__ void __launch_bounds__(256) maxplus_dense_kernel(const __grid_constan
   Vec<V>* lb = reinterpret_cast<Vec<V>*>(cur);     // [L][BD]
 
   const int s0 = blockIdx.x * W;
-  const int s = s0 + tid * V;         // first scenario of this thread
-  const bool act = s < p.S;           // S % V == 0 is guaranteed by the host
+  const int s = s0 + tid * V;
+  const bool act = s < p.S;
   for (int l = 0; l < p.L; ++l) {
     Vec<V> z;
 #pragma unroll
@@ -109,101 +116,128 @@ __global__ void __launch_bounds__(256) maxplus_dense_kernel(const __grid_constan
   if (tid == 0)
     for (int c = 0; c < min(kStagesD, nchunks); ++c) issue(c);
 
-  Vec<V> ms, prev, prev2;
+  Vec<V> ms, ra, rb;  // rb: rel of the previous record, ra: of the one before
 #pragma unroll
-  for (int i = 0; i < V; ++i) {
-    ms.v[i] = 0;
-    prev.v[i] = LLONG_MIN;
-    prev2.v[i] = LLONG_MIN;
-  }
+  for (int i = 0; i < V; ++i) ms.v[i] = ra.v[i] = rb.v[i] = 0;
+  long long neg = 0;
   const long long ld = p.start_ld;
-  long long* sp = (act && p.start) ? p.start + s : nullptr;  // advanced one row per record
+  long long* sp = (act && p.start) ? p.start + s : nullptr;
   const long long* dp = DK == 2 ? p.dense64 + (act ? s : 0) : nullptr;
+  const int bdv = BD;
+
+  // one record; `pv` = rel of the previous record, `pv2` = the one before;
+  // the result is written over pv2 (so the two registers alternate roles)
+  auto step = [&](const DenseRec& r, const int* Trow, int row, const Vec<V>& pv, Vec<V>& pv2) {
+    Vec<V> d;
+    if (DK == 1) {
+      if (V == 2) {
+        const int2 t2 = *reinterpret_cast<const int2*>(Trow);
+        d.v[0] = t2.x;
+        d.v[V - 1] = t2.y;
+        neg |= (long long)(t2.x | t2.y);
+      } else {
+        d.v[0] = Trow[0];
+        neg |= d.v[0];
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        d.v[i] = dp[i];
+        neg |= d.v[i];
+      }
+      dp += p.dense_ld;
+    }
+    const unsigned op = r.op;
+    Vec<V> sv;
+    // first source initialises sv (no 0 floor needed: all rel >= 0)
+    if (op & DOP_PREV) {
+      sv = pv;
+      if (op & DOP_PREV2) vmax(sv, pv2);
+    } else if (op & DOP_PREV2) {
+      sv = pv2;
+    } else {
+#pragma unroll
+      for (int i = 0; i < V; ++i) sv.v[i] = 0;
+    }
+    if (op & DOP_S0) vmax(sv, slots[r.s0 * bdv + tid]);
+    if (op & DOP_S1) vmax(sv, slots[r.s1 * bdv + tid]);
+    if (op & DOP_SLOW) {
+      if (p.side_ready) {
+        const long long rd = p.side_ready[row];
+#pragma unroll
+        for (int i = 0; i < V; ++i) sv.v[i] = max(sv.v[i], rd);
+      }
+      if (p.side_off)
+        for (int k = p.side_off[row]; k < p.side_off[row + 1]; ++k) {
+          const int code = p.side_slots[k];
+          if (code < p.ksm) {
+            vmax(sv, slots[code * bdv + tid]);
+          } else if (act) {
+            const long long* g = p.gslots + (long long)(code - p.ksm) * p.s_pad + s;
+#pragma unroll
+            for (int i = 0; i < V; ++i) sv.v[i] = max(sv.v[i], g[i]);
+          }
+        }
+    }
+    if (sp) {
+      if (V == 2)
+        __stcs(reinterpret_cast<longlong2*>(sp), make_longlong2(sv.v[0], sv.v[V - 1]));
+      else
+        __stcs(sp, sv.v[0]);
+      sp += ld;
+    }
+    const unsigned ln = r.lane;
+    Vec<V> rel;
+#pragma unroll
+    for (int i = 0; i < V; ++i) rel.v[i] = sv.v[i] + d.v[i];
+    if (op & DOP_MS) vmax(ms, rel);
+    if (ln & DLANE_GAP) {
+#pragma unroll
+      for (int i = 0; i < V; ++i) rel.v[i] += r.gap;
+    }
+    if (op & DOP_OUT_SMEM) slots[r.out * bdv + tid] = rel;
+    if ((op & DOP_OUT_GLOBAL) && act) {
+      long long* g = p.gslots + (long long)(r.out - p.ksm) * p.s_pad + s;
+#pragma unroll
+      for (int i = 0; i < V; ++i) g[i] = rel.v[i];
+    }
+    Vec<V>& acc = lb[(ln & 0x7f) * bdv + tid];
+#pragma unroll
+    for (int i = 0; i < V; ++i) acc.v[i] += d.v[i];
+    pv2 = rel;
+  };
+
   for (int c = 0; c < nchunks; ++c) {
     const int st = c % kStagesD;
     d_wait(&bars[st], (unsigned)((c / kStagesD) & 1));
     const DenseRec* R = pst + st * kChunkD;
     const int* T = tst + st * kChunkD * W + tid * V;
     const int nrec = min(kChunkD, p.n_rec - c * kChunkD);
-#pragma unroll 2
-    for (int j = 0; j < nrec; ++j) {
-      const DenseRec r = R[j];
-      Vec<V> d;
-      if (DK == 1) {
-        if (V == 2) {
-          const int2 t2 = *reinterpret_cast<const int2*>(T + j * W);
-          d.v[0] = t2.x;
-          d.v[V - 1] = t2.y;
-        } else {
-          d.v[0] = T[j * W];
-        }
-      } else {
-#pragma unroll
-        for (int i = 0; i < V; ++i) d.v[i] = dp[i];
-        dp += p.dense_ld;
-      }
-      Vec<V> sv;
-#pragma unroll
-      for (int i = 0; i < V; ++i) sv.v[i] = 0;
-      const unsigned op = r.op;
-      if (op & DOP_PREV) vmax(sv, prev);
-      if (op & DOP_PREV2) vmax(sv, prev2);
-      if (op & DOP_S0) vmax(sv, slots[r.s0 * BD + tid]);
-      if (op & DOP_S1) vmax(sv, slots[r.s1 * BD + tid]);
-      if (op & DOP_SLOW) {
-        const int row = c * kChunkD + j;
-        if (p.side_ready) {
-          const long long rd = p.side_ready[row];
-#pragma unroll
-          for (int i = 0; i < V; ++i) sv.v[i] = max(sv.v[i], rd);
-        }
-        if (p.side_off)
-          for (int k = p.side_off[row]; k < p.side_off[row + 1]; ++k) {
-            const int code = p.side_slots[k];
-            if (code < p.ksm) {
-              vmax(sv, slots[code * BD + tid]);
-            } else if (act) {
-              const long long* g = p.gslots + (long long)(code - p.ksm) * p.s_pad + s;
-#pragma unroll
-              for (int i = 0; i < V; ++i) sv.v[i] = max(sv.v[i], g[i]);
-            }
-          }
-      }
-      if (sp) {
-        if (V == 2)
-          __stcs(reinterpret_cast<longlong2*>(sp), make_longlong2(sv.v[0], sv.v[V - 1]));
-        else
-          __stcs(sp, sv.v[0]);
-        sp += ld;
-      }
-      Vec<V> rel;
-#pragma unroll
-      for (int i = 0; i < V; ++i) {
-        const long long fin = sv.v[i] + d.v[i];
-        ms.v[i] = max(ms.v[i], fin);
-        rel.v[i] = fin + r.gap;
-      }
-      if (op & DOP_OUT_SMEM) slots[r.out * BD + tid] = rel;
-      if ((op & DOP_OUT_GLOBAL) && act) {
-        long long* g = p.gslots + (long long)(r.out - p.ksm) * p.s_pad + s;
-#pragma unroll
-        for (int i = 0; i < V; ++i) g[i] = rel.v[i];
-      }
-      Vec<V>& acc = lb[r.lane * BD + tid];
-#pragma unroll
-      for (int i = 0; i < V; ++i) acc.v[i] += d.v[i];
-      prev2 = prev;
-      prev = rel;
+    const int row0 = c * kChunkD;
+    int j = 0;
+    // records alternate between the ra/rb registers: no moves
+    for (; j + 1 < nrec; j += 2) {
+      step(R[j], T + j * W, row0 + j, rb, ra);          // new rel -> ra
+      step(R[j + 1], T + (j + 1) * W, row0 + j + 1, ra, rb);  // new rel -> rb
+    }
+    if (j < nrec) {
+      step(R[j], T + j * W, row0 + j, rb, ra);
+      // keep the invariant "rb = previous record" for the next chunk
+      Vec<V> t = ra;
+      ra = rb;
+      rb = t;
     }
     __syncthreads();
     if (tid == 0 && c + kStagesD < nchunks) issue(c + kStagesD);
   }
   if (act) {
+    if (neg < 0 && p.neg_flag) atomicOr(p.neg_flag, 1);
 #pragma unroll
     for (int i = 0; i < V; ++i) {
       if (p.makespan) p.makespan[s + i] = ms.v[i];
       if (p.lane_busy)
-        for (int l = 0; l < p.L; ++l) p.lane_busy[(long long)(s + i) * p.L + l] = lb[l * BD + tid].v[i];
+        for (int l = 0; l < p.L; ++l)
+          p.lane_busy[(long long)(s + i) * p.L + l] = lb[l * BD + tid].v[i];
     }
   }
 }

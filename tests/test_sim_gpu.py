@@ -175,3 +175,21 @@ def test_listsched_batch_with_scale_vs_oracle(golden):
             scale_durations(h, sel, Fraction(str(f)))
         st, ms, lb, _ = OracleGraph.from_graph(h).simulate("priority")
         assert res.makespan[s] == ms and res.start_of(s) == st
+
+
+def test_batch_dense_negative_durations_take_exact_path(golden):
+    """Negative durations void the fast-path facts; the device flags them and
+    the exact kernel reruns the launch (results must still match Alg. 1)."""
+    g = _genspec_graph(golden, "genspec_1003")
+    fz = FrozenGraph.from_graph(g)
+    S = 64
+    rng = np.random.default_rng(5)
+    base = fz.duration[fz.order]
+    dense = (base[:, None] + rng.integers(-3000, 3000, size=(fz.n, S))).astype(np.int32)
+    res = simulate_batch(fz, ScenarioTable(n_scenarios=S, dense=dense))
+    og = OracleGraph.from_graph(g)
+    for s in (0, 17, 63):
+        d = np.empty(fz.n, np.int64)
+        d[fz.order] = dense[:, s]
+        st, ms, lb, _ = og.simulate("default", dur=d)
+        assert res.makespan[s] == ms and res.start_of(s) == st
