@@ -63,8 +63,34 @@ __device__ __forceinline__ void vmax(Vec<V>& a, const Vec<V>& b) {
 }
 }  // namespace
 
-// V scenarios per thread; DK: 1 = int32 durations via TMA tiles,
-// 2 = int64 durations via direct global loads.
+__device__ __forceinline__ int4 lds128(unsigned a) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int2 lds64i(unsigned a) {
+  int2 v;
+  asm volatile("ld.shared.v2.s32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int lds32i(unsigned a) {
+  int v;
+  asm volatile("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ long long lds64(unsigned a) {
+  long long v;
+  asm volatile("ld.shared.s64 %0, [%1];" : "=l"(v) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void sts64(unsigned a, long long v) {
+  asm volatile("st.shared.s64 [%0], %1;" ::"r"(a), "l"(v) : "memory");
+}
+
+// V scenarios per thread; DK: 1 = int32 durations via TMA tiles, 2 = int64
+// durations via direct global loads; NL: lanes kept in registers (0 = lane
+// busy accumulated in shared memory, any lane count).
 //
 // Fast-path facts (host-checked: gaps and ready times >= 0, lanes chained;
 // device-checked: durations >= 0, else *neg_flag is set and the host's exact
@@ -72,7 +98,7 @@ __device__ __forceinline__ void vmax(Vec<V>& a, const Vec<V>& b) {
 // start() is implied by any predecessor, and the makespan is the max finish of
 // the last task of each lane (flagged DOP_MS) because a lane's finishes never
 // decrease along its chain.
-template <int V, int DK>
+template <int V, int DK, int NL>
 __global__ void __launch_bounds__(256) maxplus_dense_kernel(const __grid_constant__ CUtensorMap tmap,
                                                             const DenseParams p) {
   extern __shared__ __align__(128) unsigned char smem[];
@@ -81,22 +107,23 @@ __global__ void __launch_bounds__(256) maxplus_dense_kernel(const __grid_constan
   const int tid = threadIdx.x;
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem);
   DenseRec* pst = reinterpret_cast<DenseRec*>(smem + 128);
-  unsigned char* cur = smem + 128 + kStagesD * kChunkD * sizeof(DenseRec);
-  int* tst = reinterpret_cast<int*>(cur);
-  if (DK == 1) cur += (size_t)kStagesD * kChunkD * W * sizeof(int);
-  Vec<V>* slots = reinterpret_cast<Vec<V>*>(cur);  // [ksm][BD]
-  cur += (size_t)p.ksm * BD * sizeof(Vec<V>);
-  Vec<V>* lb = reinterpret_cast<Vec<V>*>(cur);     // [L][BD]
+  const unsigned sbase = su32(smem);
+  const unsigned prog_s = sbase + 128;
+  const unsigned tile_s = prog_s + kStagesD * kChunkD * (unsigned)sizeof(DenseRec);
+  const unsigned tile_bytes_all = DK == 1 ? (unsigned)(kStagesD * kChunkD * W * 4) : 0u;
+  const unsigned slot_s = tile_s + tile_bytes_all;              // [ksm][BD] x (8V)
+  const unsigned lb_s = slot_s + (unsigned)(p.ksm * BD * 8 * V);  // [L][BD] x (8V)
+  const unsigned col = (unsigned)(tid * 8 * V);                 // this thread's column
+  const unsigned slot_pitch = (unsigned)(BD * 8 * V);
+  int* tst = reinterpret_cast<int*>(smem + (tile_s - sbase));
 
   const int s0 = blockIdx.x * W;
   const int s = s0 + tid * V;
   const bool act = s < p.S;
-  for (int l = 0; l < p.L; ++l) {
-    Vec<V> z;
+  if (NL == 0)
+    for (int l = 0; l < p.L; ++l)
 #pragma unroll
-    for (int i = 0; i < V; ++i) z.v[i] = 0;
-    lb[l * BD + tid] = z;
-  }
+      for (int i = 0; i < V; ++i) sts64(lb_s + l * slot_pitch + col + 8 * i, 0);
   const int nchunks = (p.n_rec + kChunkD - 1) / kChunkD;
   const unsigned tile_bytes = DK == 1 ? (unsigned)(kChunkD * W * sizeof(int)) : 0u;
   auto issue = [&](int c) {
@@ -116,116 +143,167 @@ __global__ void __launch_bounds__(256) maxplus_dense_kernel(const __grid_constan
   if (tid == 0)
     for (int c = 0; c < min(kStagesD, nchunks); ++c) issue(c);
 
-  Vec<V> ms, ra, rb;  // rb: rel of the previous record, ra: of the one before
+  long long ms[V], ra[V], rb[V], lbr[NL > 0 ? NL : 1][V];
 #pragma unroll
-  for (int i = 0; i < V; ++i) ms.v[i] = ra.v[i] = rb.v[i] = 0;
-  long long neg = 0;
+  for (int i = 0; i < V; ++i) {
+    ms[i] = ra[i] = rb[i] = 0;
+#pragma unroll
+    for (int l = 0; l < (NL > 0 ? NL : 1); ++l) lbr[l][i] = 0;
+  }
+  int neg = 0;
   const long long ld = p.start_ld;
   long long* sp = (act && p.start) ? p.start + s : nullptr;
   const long long* dp = DK == 2 ? p.dense64 + (act ? s : 0) : nullptr;
-  const int bdv = BD;
+  const int ksm = p.ksm;
+  const unsigned row_pitch = (unsigned)(W * 4);
 
-  // one record; `pv` = rel of the previous record, `pv2` = the one before;
-  // the result is written over pv2 (so the two registers alternate roles)
-  auto step = [&](const DenseRec& r, const int* Trow, int row, const Vec<V>& pv, Vec<V>& pv2) {
-    Vec<V> d;
-    if (DK == 1) {
-      if (V == 2) {
-        const int2 t2 = *reinterpret_cast<const int2*>(Trow);
-        d.v[0] = t2.x;
-        d.v[V - 1] = t2.y;
-        neg |= (long long)(t2.x | t2.y);
-      } else {
-        d.v[0] = Trow[0];
-        neg |= d.v[0];
-      }
-    } else {
-#pragma unroll
-      for (int i = 0; i < V; ++i) {
-        d.v[i] = dp[i];
-        neg |= d.v[i];
-      }
-      dp += p.dense_ld;
-    }
-    const unsigned op = r.op;
-    Vec<V> sv;
-    // first source initialises sv (no 0 floor needed: all rel >= 0)
+  // one record: `pv` = rel of the previous record, `pv2` = the one before;
+  // the result overwrites pv2 (the two registers alternate roles)
+  auto step = [&](int4 raw, long long dv0, long long dv1, int row, const long long* pv,
+                  long long* pv2) {
+    const long long gap = ((long long)(unsigned)raw.y << 32) | (unsigned)raw.x;
+    const unsigned w = (unsigned)raw.w;
+    const unsigned op = w >> 24;
+    long long dv[V];
+    dv[0] = dv0;
+    if (V == 2) dv[V - 1] = dv1;
+    long long sv[V];
     if (op & DOP_PREV) {
-      sv = pv;
-      if (op & DOP_PREV2) vmax(sv, pv2);
-    } else if (op & DOP_PREV2) {
-      sv = pv2;
+#pragma unroll
+      for (int i = 0; i < V; ++i) sv[i] = pv[i];
+      if (op & DOP_PREV2)
+#pragma unroll
+        for (int i = 0; i < V; ++i) sv[i] = max(sv[i], pv2[i]);
     } else {
 #pragma unroll
-      for (int i = 0; i < V; ++i) sv.v[i] = 0;
+      for (int i = 0; i < V; ++i) sv[i] = (op & DOP_PREV2) ? pv2[i] : 0;
     }
-    if (op & DOP_S0) vmax(sv, slots[r.s0 * bdv + tid]);
-    if (op & DOP_S1) vmax(sv, slots[r.s1 * bdv + tid]);
+    if (op & DOP_S0) {
+      const unsigned a = slot_s + (unsigned)((raw.z << 16) >> 16) * slot_pitch + col;
+#pragma unroll
+      for (int i = 0; i < V; ++i) sv[i] = max(sv[i], lds64(a + 8 * i));
+    }
+    if (op & DOP_S1) {
+      const unsigned a = slot_s + (unsigned)(raw.z >> 16) * slot_pitch + col;
+#pragma unroll
+      for (int i = 0; i < V; ++i) sv[i] = max(sv[i], lds64(a + 8 * i));
+    }
     if (op & DOP_SLOW) {
       if (p.side_ready) {
         const long long rd = p.side_ready[row];
 #pragma unroll
-        for (int i = 0; i < V; ++i) sv.v[i] = max(sv.v[i], rd);
+        for (int i = 0; i < V; ++i) sv[i] = max(sv[i], rd);
       }
       if (p.side_off)
         for (int k = p.side_off[row]; k < p.side_off[row + 1]; ++k) {
           const int code = p.side_slots[k];
-          if (code < p.ksm) {
-            vmax(sv, slots[code * bdv + tid]);
-          } else if (act) {
-            const long long* g = p.gslots + (long long)(code - p.ksm) * p.s_pad + s;
+          if (code < ksm) {
 #pragma unroll
-            for (int i = 0; i < V; ++i) sv.v[i] = max(sv.v[i], g[i]);
+            for (int i = 0; i < V; ++i)
+              sv[i] = max(sv[i], lds64(slot_s + code * slot_pitch + col + 8 * i));
+          } else if (act) {
+            const long long* g = p.gslots + (long long)(code - ksm) * p.s_pad + s;
+#pragma unroll
+            for (int i = 0; i < V; ++i) sv[i] = max(sv[i], g[i]);
           }
         }
     }
     if (sp) {
-      if (V == 2)
-        __stcs(reinterpret_cast<longlong2*>(sp), make_longlong2(sv.v[0], sv.v[V - 1]));
-      else
-        __stcs(sp, sv.v[0]);
+#pragma unroll
+      for (int i = 0; i < V; ++i) __stcs(sp + i, sv[i]);
       sp += ld;
     }
-    const unsigned ln = r.lane;
-    Vec<V> rel;
+    const unsigned ln = (w >> 16) & 0xffu;
+    long long rel[V];
 #pragma unroll
-    for (int i = 0; i < V; ++i) rel.v[i] = sv.v[i] + d.v[i];
-    if (op & DOP_MS) vmax(ms, rel);
-    if (ln & DLANE_GAP) {
+    for (int i = 0; i < V; ++i) rel[i] = sv[i] + dv[i];
+    if (op & DOP_MS)
 #pragma unroll
-      for (int i = 0; i < V; ++i) rel.v[i] += r.gap;
+      for (int i = 0; i < V; ++i) ms[i] = max(ms[i], rel[i]);
+    if (ln & DLANE_GAP)
+#pragma unroll
+      for (int i = 0; i < V; ++i) rel[i] += gap;
+    if (op & (DOP_OUT_SMEM | DOP_OUT_GLOBAL)) {
+      const int out = (int)(w << 16) >> 16;
+      if (op & DOP_OUT_SMEM) {
+        const unsigned a = slot_s + (unsigned)out * slot_pitch + col;
+#pragma unroll
+        for (int i = 0; i < V; ++i) sts64(a + 8 * i, rel[i]);
+      } else if (act) {
+        long long* g = p.gslots + (long long)(out - ksm) * p.s_pad + s;
+#pragma unroll
+        for (int i = 0; i < V; ++i) g[i] = rel[i];
+      }
     }
-    if (op & DOP_OUT_SMEM) slots[r.out * bdv + tid] = rel;
-    if ((op & DOP_OUT_GLOBAL) && act) {
-      long long* g = p.gslots + (long long)(r.out - p.ksm) * p.s_pad + s;
+    const unsigned lane = ln & 0x7fu;
+    if (NL > 0) {
 #pragma unroll
-      for (int i = 0; i < V; ++i) g[i] = rel.v[i];
+      for (int l = 0; l < (NL > 0 ? NL : 1); ++l)
+        if (lane == (unsigned)l)
+#pragma unroll
+          for (int i = 0; i < V; ++i) lbr[l][i] += dv[i];
+    } else {
+      const unsigned a = lb_s + lane * slot_pitch + col;
+#pragma unroll
+      for (int i = 0; i < V; ++i) sts64(a + 8 * i, lds64(a + 8 * i) + dv[i]);
     }
-    Vec<V>& acc = lb[(ln & 0x7f) * bdv + tid];
 #pragma unroll
-    for (int i = 0; i < V; ++i) acc.v[i] += d.v[i];
-    pv2 = rel;
+    for (int i = 0; i < V; ++i) pv2[i] = rel[i];
+  };
+
+  auto load_d = [&](unsigned trow, long long& x, long long& y) {
+    if (DK == 1) {
+      if (V == 2) {
+        const int2 t2 = lds64i(trow);
+        x = t2.x;
+        y = t2.y;
+        neg |= t2.x | t2.y;
+      } else {
+        const int t1 = lds32i(trow);
+        x = t1;
+        y = 0;
+        neg |= t1;
+      }
+    } else {
+      x = dp[0];
+      y = V == 2 ? dp[V - 1] : 0;
+      neg |= (int)((x | y) >> 32);
+      dp += p.dense_ld;
+    }
   };
 
   for (int c = 0; c < nchunks; ++c) {
     const int st = c % kStagesD;
     d_wait(&bars[st], (unsigned)((c / kStagesD) & 1));
-    const DenseRec* R = pst + st * kChunkD;
-    const int* T = tst + st * kChunkD * W + tid * V;
+    const unsigned rec0 = prog_s + (unsigned)(st * kChunkD * sizeof(DenseRec));
+    const unsigned t0 = tile_s + (unsigned)(st * kChunkD) * row_pitch + (unsigned)(tid * 4 * V);
     const int nrec = min(kChunkD, p.n_rec - c * kChunkD);
     const int row0 = c * kChunkD;
     int j = 0;
-    // records alternate between the ra/rb registers: no moves
+    // records alternate between the ra / rb registers (no moves); the next
+    // record and duration pair are loaded before the current one is used
+    int4 rawA = lds128(rec0);
+    long long xa, ya;
+    load_d(t0, xa, ya);
     for (; j + 1 < nrec; j += 2) {
-      step(R[j], T + j * W, row0 + j, rb, ra);          // new rel -> ra
-      step(R[j + 1], T + (j + 1) * W, row0 + j + 1, ra, rb);  // new rel -> rb
+      const int4 rawB = lds128(rec0 + (unsigned)(j + 1) * 16u);
+      long long xb, yb;
+      load_d(t0 + (unsigned)(j + 1) * row_pitch, xb, yb);
+      step(rawA, xa, ya, row0 + j, rb, ra);
+      if (j + 2 < nrec) {
+        rawA = lds128(rec0 + (unsigned)(j + 2) * 16u);
+        load_d(t0 + (unsigned)(j + 2) * row_pitch, xa, ya);
+      }
+      step(rawB, xb, yb, row0 + j + 1, ra, rb);
     }
     if (j < nrec) {
-      step(R[j], T + j * W, row0 + j, rb, ra);
-      // keep the invariant "rb = previous record" for the next chunk
-      Vec<V> t = ra;
-      ra = rb;
-      rb = t;
+      step(rawA, xa, ya, row0 + j, rb, ra);
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        const long long t = ra[i];
+        ra[i] = rb[i];
+        rb[i] = t;
+      }
     }
     __syncthreads();
     if (tid == 0 && c + kStagesD < nchunks) issue(c + kStagesD);
@@ -234,10 +312,20 @@ __global__ void __launch_bounds__(256) maxplus_dense_kernel(const __grid_constan
     if (neg < 0 && p.neg_flag) atomicOr(p.neg_flag, 1);
 #pragma unroll
     for (int i = 0; i < V; ++i) {
-      if (p.makespan) p.makespan[s + i] = ms.v[i];
+      if (p.makespan) p.makespan[s + i] = ms[i];
       if (p.lane_busy)
-        for (int l = 0; l < p.L; ++l)
-          p.lane_busy[(long long)(s + i) * p.L + l] = lb[l * BD + tid].v[i];
+        for (int l = 0; l < p.L; ++l) {
+          long long v;
+          if (NL > 0) {
+            v = 0;
+#pragma unroll
+            for (int q = 0; q < (NL > 0 ? NL : 1); ++q)
+              if (q == l) v = lbr[q][i];
+          } else {
+            v = lds64(lb_s + l * slot_pitch + col + 8 * i);
+          }
+          p.lane_busy[(long long)(s + i) * p.L + l] = v;
+        }
     }
   }
 }
@@ -256,14 +344,21 @@ int maxplus_dense_block_dim(int S, int V, int num_sms) {
   return bd < 32 ? 32 : (bd > cap ? cap : bd);
 }
 
+template <int V, int DK, int NL>
+static cudaError_t launch_vl(const CUtensorMap& tmap, const DenseParams& p, int grid, int BD,
+                             size_t smem, cudaStream_t stream) {
+  cudaError_t err = cudaFuncSetAttribute(maxplus_dense_kernel<V, DK, NL>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (err != cudaSuccess) return err;
+  maxplus_dense_kernel<V, DK, NL><<<grid, BD, smem, stream>>>(tmap, p);
+  return cudaSuccess;
+}
+
 template <int V, int DK>
 static cudaError_t launch_v(const CUtensorMap& tmap, const DenseParams& p, int grid, int BD,
                             size_t smem, cudaStream_t stream) {
-  cudaError_t err = cudaFuncSetAttribute(maxplus_dense_kernel<V, DK>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (err != cudaSuccess) return err;
-  maxplus_dense_kernel<V, DK><<<grid, BD, smem, stream>>>(tmap, p);
-  return cudaSuccess;
+  if (p.L <= 4) return launch_vl<V, DK, 4>(tmap, p, grid, BD, smem, stream);
+  return launch_vl<V, DK, 0>(tmap, p, grid, BD, smem, stream);
 }
 
 cudaError_t launch_maxplus_dense(const DenseParams& p, const int* dense32, int dkind,
