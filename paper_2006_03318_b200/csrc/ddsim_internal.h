@@ -69,6 +69,41 @@ struct DenseParams {
   long long* lane_busy;
 };
 
+// Lane-register program record (maxplus_lanes.cu): 16 bytes.
+// h = own lane (2 bits) | predecessor-lane mask (5 bits; bit 4 = temp lane
+// holding the rare predecessors) << 2 | gap != 0 << 7.
+struct alignas(16) LaneRec {
+  long long gap;
+  short s0, s1;          // smem slots of rare predecessors (LREC_S0 / LREC_S1)
+  short out;             // slot receiving rel (LREC_OUT_SMEM: smem id, LREC_OUT_GLOBAL: global id)
+  unsigned char rare;
+  unsigned char h;
+};
+static_assert(sizeof(LaneRec) == 16, "LaneRec must be 16 bytes");
+enum {
+  LREC_S0 = 1, LREC_S1 = 2, LREC_SIDE = 4, LREC_MS = 8, LREC_OUT_SMEM = 16, LREC_OUT_GLOBAL = 32,
+  LREC_PRE = 7, LREC_POST = 56
+};
+
+struct LaneParams {
+  const LaneRec* prog;
+  int n_rec;
+  const int* side_off;
+  const int* side_slots;       // < ksm: smem slot, else global slot + ksm
+  const long long* side_ready;
+  int ksm, kglob;
+  long long* gslots;
+  long long s_pad;
+  int S, L;
+  const long long* dense64;
+  long long dense_ld;
+  long long* start;
+  long long start_ld;
+  long long* makespan;
+  long long* lane_busy;
+  int* neg_flag;
+};
+
 struct ChainDesc {
   int first_row;   // members occupy frozen rows first_row .. first_row+B-1
   int B;
@@ -158,6 +193,9 @@ cudaError_t launch_maxplus(const MaxplusParams& p, const int* dense32,
                            cudaStream_t stream);
 cudaError_t launch_maxplus_dense(const DenseParams& p, const int* dense32, int dkind,
                                  cudaStream_t stream);
+cudaError_t launch_maxplus_lanes(const LaneParams& p, const int* dense32, int dkind,
+                                 cudaStream_t stream);
+int maxplus_lanes_block_dim(int S, int num_sms);
 cudaError_t launch_listsched(const ListParams& p, cudaStream_t stream);
 cudaError_t launch_fill_i64(long long* p, long long v, long long n, cudaStream_t s);
 cudaError_t launch_fill_i32(int* p, int v, long long n, cudaStream_t s);

@@ -20,6 +20,7 @@
 #include <queue>
 #include <string>
 #include <vector>
+#include <cstdlib>
 
 #include "ddsim_internal.h"
 
@@ -76,6 +77,13 @@ struct ks_graph {
   std::vector<int> row_of;       // input index -> frozen row
   std::vector<int> level;        // per frozen row
   std::vector<int> rank_row;     // id rank per frozen row
+  // lane-register program (chained, <= 4 lanes, no chains)
+  bool has_lanes = false;
+  int lksm = 0, lkglob = 0;
+  LaneRec* d_lprog = nullptr;
+  int* d_lside_off = nullptr;
+  int* d_lside_slots = nullptr;
+  long long* d_lside_ready = nullptr;
   // dense-duration program (no chains, <= 255 lanes)
   bool has_dense = false;
   int dksm = 0, dkglob = 0;
@@ -608,6 +616,120 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     }
   }
 
+  // ---- lane-register program (maxplus_lanes.cu) ------------------------------
+  if (NC == 0 && chained && L <= 4 && nonneg && R == n) {
+    std::vector<int> pos(n, -1);
+    for (int i = 0; i < R; ++i) pos[corder[i]] = i;
+    // which predecessor reads are lane heads at read time?
+    std::vector<int> head(L, -1);
+    std::vector<int> far_use(n, -1);      // last slot read of each value
+    std::vector<unsigned> hmask(R, 0);
+    std::vector<std::vector<int>> slot_preds(R);
+    for (int i = 0; i < R; ++i) {
+      const int v = corder[i];
+      const int l = d->lane[v];
+      unsigned mask = 0;
+      for (int k = pptr[v]; k < pptr[v + 1]; ++k) {
+        const int u = padj[k];
+        const int m = d->lane[u];
+        if (head[m] == u) {
+          if (m != l) mask |= 1u << m;
+        } else {
+          slot_preds[i].push_back(u);
+          far_use[u] = std::max(far_use[u], i);
+        }
+      }
+      hmask[i] = mask;
+      head[l] = v;
+    }
+    std::vector<int> lslot(n, -1);
+    std::vector<char> lglob(n, 0);
+    std::priority_queue<int, std::vector<int>, std::greater<int>> fs, fg;
+    int ns = 0, ngl = 0;
+    std::vector<std::vector<int>> frees_at(R);
+    for (int i = 0; i < R; ++i) {
+      const int v = corder[i];
+      if (far_use[v] >= 0) {
+        const bool shrt = far_use[v] - i <= kShortRange;
+        if (shrt && !fs.empty()) {
+          lslot[v] = fs.top();
+          fs.pop();
+        } else if (shrt && ns < kSmemSlotsMax) {
+          lslot[v] = ns++;
+        } else {
+          lglob[v] = 1;
+          if (!fg.empty()) {
+            lslot[v] = fg.top();
+            fg.pop();
+          } else {
+            lslot[v] = ngl++;
+          }
+        }
+        frees_at[far_use[v]].push_back(v);
+      }
+      for (int u : frees_at[i]) (lglob[u] ? fg : fs).push(lslot[u]);
+    }
+    std::vector<int> lane_last(L, -1);
+    for (int i = 0; i < R; ++i) lane_last[d->lane[corder[i]]] = i;
+    std::vector<LaneRec> lprog(R);
+    std::vector<int> lside_off(R + 1, 0), lside_slots;
+    bool any_ready = false;
+    for (int i = 0; i < R; ++i) {
+      const int v = corder[i];
+      LaneRec r;
+      memset(&r, 0, sizeof(r));
+      r.gap = d->gap[v];
+      unsigned rare = 0;
+      int nsm_pred = 0;
+      for (int u : slot_preds[i]) {
+        if (!lglob[u] && nsm_pred == 0) {
+          rare |= LREC_S0;
+          r.s0 = (short)lslot[u];
+          ++nsm_pred;
+        } else if (!lglob[u] && nsm_pred == 1) {
+          rare |= LREC_S1;
+          r.s1 = (short)lslot[u];
+          ++nsm_pred;
+        } else {
+          rare |= LREC_SIDE;
+          lside_slots.push_back(lglob[u] ? ns + lslot[u] : lslot[u]);
+        }
+      }
+      lside_off[i + 1] = (int)lside_slots.size();
+      const long long rt = d->ready_time ? d->ready_time[v] : 0;
+      if (rt != 0) {
+        rare |= LREC_SIDE;
+        any_ready = true;
+      }
+      unsigned mask = hmask[i];
+      if (rare & LREC_PRE) mask |= 16u;  // temp lane carries the rare predecessors
+      if (lane_last[d->lane[v]] == i) rare |= LREC_MS;
+      if (lslot[v] >= 0) {
+        rare |= lglob[v] ? LREC_OUT_GLOBAL : LREC_OUT_SMEM;
+        r.out = (short)lslot[v];
+      }
+      r.rare = (unsigned char)rare;
+      r.h = (unsigned char)((unsigned)d->lane[v] | (mask << 2) | (r.gap != 0 ? 128u : 0u));
+      lprog[i] = r;
+    }
+    if (ns + ngl < 32000) {
+      std::vector<long long> lready;
+      if (any_ready) {
+        lready.resize(R);
+        for (int i = 0; i < R; ++i) lready[i] = d->ready_time[corder[i]];
+      }
+      g->has_lanes = true;
+      g->lksm = ns;
+      g->lkglob = ngl;
+      g->d_lprog = dev_upload(lprog);
+      if (!lside_slots.empty()) {
+        g->d_lside_off = dev_upload(lside_off);
+        g->d_lside_slots = dev_upload(lside_slots);
+      }
+      g->d_lside_ready = dev_upload(lready);
+    }
+  }
+
   // ---- list-scheduler arrays (frozen rows, multiset edges) -------------------
   std::vector<int> ch_ptr(n + 1, 0), ch_adj(E), indeg(n, 0);
   for (long long k = 0; k < E; ++k) {
@@ -656,7 +778,8 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
 
 void free_graph(ks_graph* g) {
   if (!g) return;
-  void* dptrs[] = {g->d_dprog, g->d_side_off, g->d_side_slots, g->d_side_ready};
+  void* dptrs[] = {g->d_dprog,   g->d_side_off,   g->d_side_slots,  g->d_side_ready,
+                   g->d_lprog,   g->d_lside_off,  g->d_lside_slots, g->d_lside_ready};
   for (void* p : dptrs)
     if (p) cudaFree(p);
   void* ptrs[] = {g->d_prog,  g->d_extra, g->d_chains, g->d_members, g->d_child_ptr,
@@ -779,7 +902,65 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
   const bool dense = sc->dense_kind != 0 && sc->dense != nullptr;
   build_tables(g, sc, T, true, policy == KS_POLICY_VDNN);
 
-  if (use_max && dense && g->has_dense && sc->n_overrides == 0 && !sc->scale_ptr) {
+  const bool lanes_ok = use_max && dense && g->has_lanes && sc->n_overrides == 0 &&
+                        !sc->scale_ptr && S % 2 == 0 && sc->dense_ld % 2 == 0 &&
+                        (out->start == nullptr ||
+                         (out->start_ld % 2 == 0 && reinterpret_cast<uintptr_t>(out->start) % 16 == 0)) &&
+                        getenv("DDSIM_NO_LANES") == nullptr;
+  if (lanes_ok) {
+    LaneParams p;
+    memset(&p, 0, sizeof(p));
+    p.prog = g->d_lprog;
+    p.n_rec = g->n_rec;
+    p.side_off = g->d_lside_off;
+    p.side_slots = g->d_lside_slots;
+    p.side_ready = g->d_lside_ready;
+    p.ksm = g->lksm;
+    p.kglob = g->lkglob;
+    p.S = S;
+    p.L = g->L;
+    const int dk = sc->dense_kind == 1 ? 1 : 2;
+    if (dk == 1 && (reinterpret_cast<uintptr_t>(sc->dense) % 16 != 0 || sc->dense_ld % 4 != 0))
+      fail(KS_ERR_INVALID, "int32 dense durations need 16B alignment and dense_ld % 4 == 0");
+    if (dk == 2) p.dense64 = reinterpret_cast<const long long*>(sc->dense);
+    p.dense_ld = sc->dense_ld;
+    p.start = reinterpret_cast<long long*>(out->start);
+    p.start_ld = out->start_ld;
+    p.makespan = reinterpret_cast<long long*>(out->makespan);
+    p.lane_busy = reinterpret_cast<long long*>(out->lane_busy);
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device);
+    const int BD = maxplus_lanes_block_dim(S, nsm);
+    p.s_pad = (long long)((S + 2 * BD - 1) / (2 * BD)) * 2 * BD;
+    if (p.kglob > 0) p.gslots = T.scratch<long long>((size_t)p.kglob * p.s_pad);
+    int* flag = T.scratch<int>(1);
+    CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), stream));
+    p.neg_flag = flag;
+    CUDA_TRY(launch_maxplus_lanes(p, dk == 1 ? reinterpret_cast<const int*>(sc->dense) : nullptr, dk,
+                                  stream));
+    MaxplusParams q;
+    memset(&q, 0, sizeof(q));
+    q.prog = g->d_prog;
+    q.n_rec = g->n_rec;
+    q.extra = g->d_extra;
+    q.ksm = g->ksm;
+    q.kglob = g->kglob;
+    q.S = S;
+    q.L = g->L;
+    q.dense_kind = dk;
+    q.dense64 = p.dense64;
+    q.dense_ld = sc->dense_ld;
+    q.start = p.start;
+    q.start_ld = p.start_ld;
+    q.makespan = p.makespan;
+    q.lane_busy = p.lane_busy;
+    q.run_if = flag;
+    const int BDq = maxplus_block_dim(S, dk, nsm);
+    q.s_pad = (long long)((S + BDq - 1) / BDq) * BDq;
+    if (q.kglob > 0) q.gslots = T.scratch<long long>((size_t)q.kglob * q.s_pad);
+    CUDA_TRY(launch_maxplus(q, dk == 1 ? reinterpret_cast<const int*>(sc->dense) : nullptr, stream));
+    if (out->dispatched) CUDA_TRY(launch_fill_i32(out->dispatched, g->n, S, stream));
+  } else if (use_max && dense && g->has_dense && sc->n_overrides == 0 && !sc->scale_ptr) {
     DenseParams p;
     memset(&p, 0, sizeof(p));
     p.prog = g->d_dprog;
