@@ -113,8 +113,7 @@ _SIGNATURES = [
     ("ks_simulate_host", C.c_int, [P, C.POINTER(ScenariosDesc), C.c_int, C.c_int, C.POINTER(SimOut)]),
     ("ks_toposort", C.c_int, [P, P, C.POINTER(C.c_int32)]),
     ("ks_ingest", C.c_int, [C.POINTER(TraceCols), C.c_int, C.c_int, C.POINTER(IngestOut)]),
-    ("ks_map_layers", C.c_int, [C.POINTER(TraceCols), P, C.POINTER(MarkerCols), C.c_int, P,
-                                C.POINTER(C.c_int64)]),
+    ("ks_map_layers", C.c_int, [C.POINTER(TraceCols), P, C.POINTER(MarkerCols), C.c_int, P, P]),
     ("ks_error_name", C.c_char_p, [C.c_int]),
     ("ks_last_error_detail", C.c_char_p, []),
     ("ks_device_count", C.c_int, [C.POINTER(C.c_int)]),

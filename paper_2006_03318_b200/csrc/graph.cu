@@ -27,6 +27,7 @@
 namespace ddsim {
 
 static thread_local std::string g_last_error;
+void set_last_error(const std::string& msg) { g_last_error = msg; }
 static std::atomic<long long> g_launches{0};
 void note_launch(int n) { g_launches.fetch_add(n); }
 
@@ -1175,6 +1176,7 @@ int ks_device_count(int* n) {
   }                                                               \
   catch (const KsError& e) {                                      \
     g_last_error = e.msg;                                         \
+    cudaGetLastError();                                           \
     return e.code;                                                \
   }                                                               \
   catch (const std::bad_alloc&) {                                 \

@@ -60,7 +60,7 @@ struct Pool {
   template <class T>
   T* up(const T* h, size_t n) {
     T* p = get<T>(n);
-    if (n) ICUDA(cudaMemcpyAsync(p, h, n * sizeof(T), cudaMemcpyHostToDevice, st));
+    if (n && h) ICUDA(cudaMemcpyAsync(p, h, n * sizeof(T), cudaMemcpyHostToDevice, st));
     return p;
   }
   ~Pool() {
@@ -406,9 +406,8 @@ __global__ void fill_i_k(int* a, int v, long long n) {
     a[i] = v;
 }
 
-thread_local std::string g_ingest_err;
-
 }  // namespace
+void set_last_error(const std::string& msg);
 }  // namespace ddsim
 
 using namespace ddsim;
@@ -565,7 +564,7 @@ extern "C" int ks_ingest(const ks_trace_cols* tc, int device, int check_overlaps
     lane_bounds_k<<<blocks_for(n), TPB, 0, st>>>(sperm, skl, n, seg_first,
                                                  seg_last);
     note_launch(3);
-    int* d_gl = P.up(gpu_lanes_h.data(), (size_t)std::max(G, 1));
+    int* d_gl = G > 0 ? P.up(gpu_lanes_h.data(), (size_t)G) : P.get<int>(1);
     sync_link_k<<<blocks_for(c_sync), TPB, 0, st>>>(
         d_kind, d_start, d_corr, d_st, d_dtoh, d_lane, d_id, n, d_gl, G, seg_first, seg_last, st_ls,
         sperm, gpu_sk, gpu_si, n, esrc + c_lane + c_launch, edst + c_lane + c_launch,
@@ -597,13 +596,17 @@ extern "C" int ks_ingest(const ks_trace_cols* tc, int device, int check_overlaps
     out->lane_order_ptr[L] = pos;
     out->n_edges = m;
   } catch (const IngestError& e) {
-    g_ingest_err = e.msg;
+    set_last_error(e.msg);
     rc = e.code;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    rc = KS_ERR_INVALID;
   } catch (...) {
     rc = KS_ERR_INVALID;
   }
   cudaStreamSynchronize(st);
   cudaStreamDestroy(st);
+  if (rc != KS_OK) cudaGetLastError();  // do not leave a non-sticky error for later calls
   return rc;
 }
 
@@ -681,12 +684,16 @@ extern "C" int ks_map_layers(const ks_trace_cols* tc, const int32_t* launcher,
       throw IngestError{KS_ERR_AMBIGUOUS, "ambiguous marker"};
     }
   } catch (const IngestError& e) {
-    g_ingest_err = e.msg;
+    set_last_error(e.msg);
     rc = e.code;
+  } catch (const std::exception& e) {
+    set_last_error(e.what());
+    rc = KS_ERR_INVALID;
   } catch (...) {
     rc = KS_ERR_INVALID;
   }
   cudaStreamSynchronize(st);
   cudaStreamDestroy(st);
+  if (rc != KS_OK) cudaGetLastError();  // do not leave a non-sticky error for later calls
   return rc;
 }

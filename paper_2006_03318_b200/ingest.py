@@ -143,7 +143,8 @@ def build_graph_device(trace: TraceDocument, strict: bool = False) -> Dependency
     lop = res.lane_order_ptr
     # lane_order insertion order: lanes sorted by their text (graph.py:222)
     for j in sorted(range(len(cols.lanes)), key=lambda j: str(cols.lanes[j])):
-        g.lane_order[cols.lanes[j]] = ids[res.lane_order[lop[j]:lop[j + 1]]].tolist()
+        if lop[j + 1] > lop[j]:  # lanes only named as a sync target carry no events
+            g.lane_order[cols.lanes[j]] = ids[res.lane_order[lop[j]:lop[j + 1]]].tolist()
     verify_acyclic(g)
     return g
 
