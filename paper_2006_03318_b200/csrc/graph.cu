@@ -46,9 +46,13 @@ static void fail(int code, const std::string& msg) { throw KsError{code, msg}; }
            std::string(#expr) + ": " + cudaGetErrorString(e_));                        \
   } while (0)
 
+// DDSIM_COMPILE_ONLY=1: run the graph compiler without a device (CPU tests of
+// the compiler itself); such handles cannot simulate.
+static bool g_compile_only = false;
+
 template <class T>
 static T* dev_upload(const std::vector<T>& v) {
-  if (v.empty()) return nullptr;
+  if (v.empty() || g_compile_only) return nullptr;
   T* p = nullptr;
   CUDA_TRY(cudaMalloc(&p, v.size() * sizeof(T)));
   CUDA_TRY(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
@@ -260,8 +264,8 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   {
     std::vector<int> indeg = cindeg;
     std::vector<int> init;
-    for (int i = 0; i < NN; ++i)
-      if (indeg[i] == 0) init.push_back(i);
+    for (int i = 0; i < NN; ++i)  // chain members are represented by their chain node
+      if (indeg[i] == 0 && !(i < n && chain_of[i] >= 0)) init.push_back(i);
     std::sort(init.begin(), init.end(), [&](int a, int b) { return crank[a] > crank[b]; });
     std::vector<int> stack(init);
     std::vector<int> cross;
@@ -886,6 +890,7 @@ namespace {
 int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, int path,
                   const ks_sim_out* out, cudaStream_t stream) {
   if (!g || !sc || !out) fail(KS_ERR_INVALID, "null argument");
+  if (g->device < 0) fail(KS_ERR_NO_DEVICE, "graph was compiled without a device");
   const int S = sc->n_scenarios;
   if (S <= 0) fail(KS_ERR_INVALID, "n_scenarios must be positive");
   if (policy < 0 || policy > 2) fail(KS_ERR_INVALID, "unknown policy");
@@ -1191,6 +1196,20 @@ int ks_device_count(int* n) {
 int ks_graph_create(const ks_graph_desc* desc, int device, ks_graph** out, int32_t* order_out) {
   KS_GUARD_BEGIN
   if (!desc || !out) fail(KS_ERR_INVALID, "null argument");
+  g_compile_only = getenv("DDSIM_COMPILE_ONLY") != nullptr;
+  if (g_compile_only) {
+    ks_graph* g = new ks_graph();
+    g->device = -1;
+    try {
+      compile_graph(desc, g);
+    } catch (...) {
+      free_graph(g);
+      throw;
+    }
+    if (order_out) std::copy(g->order.begin(), g->order.end(), order_out);
+    *out = g;
+    return KS_OK;
+  }
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) fail(KS_ERR_NO_DEVICE, "no CUDA device");
   if (device < 0 || device >= ndev) fail(KS_ERR_INVALID, "bad device");
@@ -1230,6 +1249,10 @@ int ks_graph_levels(const ks_graph* g, int32_t* level_out) {
 
 int ks_graph_destroy(ks_graph* g) {
   if (!g) return KS_OK;
+  if (g->device < 0) {
+    delete g;
+    return KS_OK;
+  }
   DevGuard guard(g->device);
   free_graph(g);
   return KS_OK;
