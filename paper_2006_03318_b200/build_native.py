@@ -46,11 +46,24 @@ def _run(cmd: list[str], log: Path | None = None) -> str:
     return out
 
 
+def _embed_sources() -> None:
+    """csrc/lanes_body.cuh -> generated/lanes_body_src.inc (NVRTC source text)."""
+    body = (CSRC / "lanes_body.cuh").read_text()
+    gen = CSRC / "generated"
+    gen.mkdir(exist_ok=True)
+    out = gen / "lanes_body_src.inc"
+    text = 'static const char* kLanesBodySrc = R"DDSIM_SRC(' + body + ')DDSIM_SRC";\n'
+    if not out.exists() or out.read_text() != text:
+        out.write_text(text)
+
+
 def build_library(verbose: bool = False) -> Path:
     BUILD.mkdir(parents=True, exist_ok=True)
+    _embed_sources()
     nvcc = _nvcc()
     sources = sorted(CSRC.glob("*.cu"))
-    headers = sorted(CSRC.glob("*.h")) + [ROOT / "include" / "ddsim.h"]
+    headers = (sorted(CSRC.glob("*.h")) + sorted(CSRC.glob("*.cuh"))
+               + sorted((CSRC / "generated").glob("*.inc")) + [ROOT / "include" / "ddsim.h"])
     newest_h = max(h.stat().st_mtime for h in headers)
 
     def compile_one(src: Path) -> Path:
@@ -65,7 +78,7 @@ def build_library(verbose: bool = False) -> Path:
         objs = list(ex.map(compile_one, sources))
     tmp = LIB.with_suffix(".so.tmp")
     _run([nvcc, "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", str(tmp),
-          *map(str, objs), "-lcuda" if False else "-lcudart_static", "-lrt", "-ldl", "-lpthread"])
+          *map(str, objs), "-lcudart_static", "-lrt", "-ldl", "-lpthread"])
     os.replace(tmp, LIB)
     if verbose:
         print(f"built {LIB}")

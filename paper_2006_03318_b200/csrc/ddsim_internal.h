@@ -4,6 +4,8 @@
 #include <cuda.h>
 #include <stdint.h>
 
+#include <vector>
+
 #include "../../include/ddsim.h"
 
 namespace ddsim {
@@ -194,7 +196,11 @@ cudaError_t launch_maxplus(const MaxplusParams& p, const int* dense32,
 cudaError_t launch_maxplus_dense(const DenseParams& p, const int* dense32, int dkind,
                                  cudaStream_t stream);
 cudaError_t launch_maxplus_lanes(const LaneParams& p, const int* dense32, int dkind,
-                                 cudaStream_t stream);
+                                 const std::vector<int>* codes, cudaStream_t stream);
+cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const void* tmap128, int dkind,
+                                     const std::vector<int>& codes, int grid, int BD, size_t smem,
+                                     cudaStream_t stream);
+const char* jit_log();
 int maxplus_lanes_block_dim(int S, int num_sms);
 cudaError_t launch_listsched(const ListParams& p, cudaStream_t stream);
 cudaError_t launch_fill_i64(long long* p, long long v, long long n, cudaStream_t s);

@@ -85,6 +85,7 @@ struct ks_graph {
   // lane-register program (chained, <= 4 lanes, no chains)
   bool has_lanes = false;
   int lksm = 0, lkglob = 0;
+  std::vector<int> lane_codes;  // handler codes in decreasing frequency
   LaneRec* d_lprog = nullptr;
   int* d_lside_off = nullptr;
   int* d_lside_slots = nullptr;
@@ -718,6 +719,13 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
       lprog[i] = r;
     }
     if (ns + ngl < 32000) {
+      std::vector<long long> freq(256, 0);
+      for (int i = 0; i < R; ++i) freq[lprog[i].h]++;
+      g->lane_codes.clear();
+      for (int c = 0; c < 256; ++c)
+        if (freq[c]) g->lane_codes.push_back(c);
+      std::stable_sort(g->lane_codes.begin(), g->lane_codes.end(),
+                       [&](int a, int b) { return freq[a] > freq[b]; });
       std::vector<long long> lready;
       if (any_ready) {
         lready.resize(R);
@@ -943,7 +951,7 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
     CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), stream));
     p.neg_flag = flag;
     CUDA_TRY(launch_maxplus_lanes(p, dk == 1 ? reinterpret_cast<const int*>(sc->dense) : nullptr, dk,
-                                  stream));
+                                  &g->lane_codes, stream));
     MaxplusParams q;
     memset(&q, 0, sizeof(q));
     q.prog = g->d_prog;

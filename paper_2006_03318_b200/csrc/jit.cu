@@ -1,0 +1,167 @@
+// Per-graph specialisation of the maxplus_lanes kernel with NVRTC.
+//
+// The static kernel dispatches each record through a 256-way switch that
+// nvcc lowers to an 8-level branch tree.  A graph only uses a handful of
+// handler codes (own lane x predecessor-lane mask x gap), so the graph
+// compiler records them with their frequencies and this file compiles, once
+// per distinct code list, a kernel whose dispatch is an if-chain over exactly
+// those codes in frequency order (the common record resolves in 1-2
+// compares).  NVRTC and the driver entry points are resolved at run time;
+// if either is unavailable the static kernel runs instead (same results).
+#include <dlfcn.h>
+
+#include <cstring>
+#include <map>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "ddsim_internal.h"
+
+namespace ddsim {
+namespace {
+
+#include "generated/lanes_body_src.inc"  // const char* kLanesBodySrc
+
+typedef int nvrtcResult_t;
+typedef void* nvrtcProgram_t;
+struct Nvrtc {
+  bool ok = false;
+  nvrtcResult_t (*create)(nvrtcProgram_t*, const char*, const char*, int, const char* const*,
+                          const char* const*) = nullptr;
+  nvrtcResult_t (*compile)(nvrtcProgram_t, int, const char* const*) = nullptr;
+  nvrtcResult_t (*cubin_size)(nvrtcProgram_t, size_t*) = nullptr;
+  nvrtcResult_t (*cubin)(nvrtcProgram_t, char*) = nullptr;
+  nvrtcResult_t (*log_size)(nvrtcProgram_t, size_t*) = nullptr;
+  nvrtcResult_t (*log)(nvrtcProgram_t, char*) = nullptr;
+  nvrtcResult_t (*destroy)(nvrtcProgram_t*) = nullptr;
+};
+
+struct Driver {
+  bool ok = false;
+  CUresult (*load)(CUmodule*, const void*) = nullptr;
+  CUresult (*getfn)(CUfunction*, CUmodule, const char*) = nullptr;
+  CUresult (*setattr)(CUfunction, CUfunction_attribute, int) = nullptr;
+  CUresult (*launch)(CUfunction, unsigned, unsigned, unsigned, unsigned, unsigned, unsigned,
+                     unsigned, CUstream, void**, void**) = nullptr;
+};
+
+std::mutex g_mu;
+Nvrtc g_nv;
+Driver g_drv;
+bool g_init = false;
+std::map<std::string, CUfunction> g_cache;
+std::string g_jit_log;
+
+template <class F>
+bool sym(void* h, const char* name, F& out) {
+  out = reinterpret_cast<F>(dlsym(h, name));
+  return out != nullptr;
+}
+
+template <class F>
+bool drv(const char* name, F& out) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess)
+    return false;
+  out = reinterpret_cast<F>(p);
+  return true;
+}
+
+void init_locked() {
+  if (g_init) return;
+  g_init = true;
+  if (getenv("DDSIM_NO_JIT")) return;
+  const char* libs[] = {"libnvrtc.so.12", "libnvrtc.so", "/usr/local/cuda/lib64/libnvrtc.so"};
+  void* h = nullptr;
+  for (const char* l : libs)
+    if ((h = dlopen(l, RTLD_NOW | RTLD_LOCAL)) != nullptr) break;
+  if (!h) return;
+  g_nv.ok = sym(h, "nvrtcCreateProgram", g_nv.create) && sym(h, "nvrtcCompileProgram", g_nv.compile) &&
+            sym(h, "nvrtcGetCUBINSize", g_nv.cubin_size) && sym(h, "nvrtcGetCUBIN", g_nv.cubin) &&
+            sym(h, "nvrtcGetProgramLogSize", g_nv.log_size) &&
+            sym(h, "nvrtcGetProgramLog", g_nv.log) && sym(h, "nvrtcDestroyProgram", g_nv.destroy);
+  g_drv.ok = drv("cuModuleLoadData", g_drv.load) && drv("cuModuleGetFunction", g_drv.getfn) &&
+             drv("cuFuncSetAttribute", g_drv.setattr) && drv("cuLaunchKernel", g_drv.launch);
+}
+
+std::string make_source(const std::vector<int>& codes, int dk) {
+  std::string disp = "#define DDSIM_DISPATCH(h) ";
+  for (size_t i = 0; i < codes.size(); ++i) {
+    const int c = codes[i];
+    disp += (i ? "else if (h == " : "if (h == ") + std::to_string(c) + "u) hstep<" +
+            std::to_string(c & 3) + ", " + std::to_string((c >> 2) & 31) + ", " +
+            std::to_string((c >> 7) & 1) + ">(S, d0, d1, gap, sp, ld, store); ";
+  }
+  disp += "else __trap();\n";
+  std::string src = "#define DDSIM_LANES_NO_STD_TYPES 1\n" + disp + kLanesBodySrc;
+  src += "\nextern \"C\" __global__ void __launch_bounds__(256) ddsim_lanes_jit("
+         "const __grid_constant__ ddsim_lanes::Tmap tmap, const ddsim_lanes::Params p) {\n"
+         "  ddsim_lanes::lanes_body<" + std::to_string(dk) + ">(&tmap, p);\n}\n";
+  return src;
+}
+
+CUfunction get_function(const std::vector<int>& codes, int dk, int device) {
+  std::string key = std::to_string(device) + ":" + std::to_string(dk) + ":";
+  for (int c : codes) key += std::to_string(c) + ",";
+  std::lock_guard<std::mutex> lk(g_mu);
+  init_locked();
+  if (!g_nv.ok || !g_drv.ok) return nullptr;
+  auto it = g_cache.find(key);
+  if (it != g_cache.end()) return it->second;
+  const std::string src = make_source(codes, dk);
+  nvrtcProgram_t prog = nullptr;
+  CUfunction fn = nullptr;
+  if (g_nv.create(&prog, src.c_str(), "ddsim_lanes_jit.cu", 0, nullptr, nullptr) == 0) {
+    const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo"};
+    const int rc = g_nv.compile(prog, 3, opts);
+    size_t ls = 0;
+    g_nv.log_size(prog, &ls);
+    g_jit_log.assign(ls, '\0');
+    if (ls) g_nv.log(prog, &g_jit_log[0]);
+    if (rc == 0) {
+      size_t n = 0;
+      g_nv.cubin_size(prog, &n);
+      std::vector<char> bin(n);
+      g_nv.cubin(prog, bin.data());
+      CUmodule mod = nullptr;
+      if (g_drv.load(&mod, bin.data()) == CUDA_SUCCESS &&
+          g_drv.getfn(&fn, mod, "ddsim_lanes_jit") != CUDA_SUCCESS)
+        fn = nullptr;
+    }
+    g_nv.destroy(&prog);
+  }
+  g_cache[key] = fn;  // nullptr is cached too: do not retry a failing compile
+  return fn;
+}
+
+}  // namespace
+
+// Launch the specialised kernel; cudaErrorNotSupported when JIT is unavailable
+// (the caller then launches the static kernel).
+cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const void* tmap128, int dkind,
+                                     const std::vector<int>& codes, int grid, int BD, size_t smem,
+                                     cudaStream_t stream) {
+  if (codes.empty() || codes.size() > 32) return cudaErrorNotSupported;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  CUfunction fn = get_function(codes, dkind, dev);
+  if (!fn) return cudaErrorNotSupported;
+  if (g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem) != CUDA_SUCCESS)
+    return cudaErrorNotSupported;
+  alignas(64) unsigned char tm[128];
+  memcpy(tm, tmap128, 128);
+  LaneParams pp = p;
+  void* args[] = {tm, &pp};
+  if (g_drv.launch(fn, grid, 1, 1, BD, 1, 1, (unsigned)smem, (CUstream)stream, args, nullptr) !=
+      CUDA_SUCCESS)
+    return cudaErrorLaunchFailure;
+  note_launch();
+  return cudaSuccess;
+}
+
+const char* jit_log() { return g_jit_log.c_str(); }
+
+}  // namespace ddsim

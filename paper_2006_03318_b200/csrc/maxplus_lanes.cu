@@ -23,104 +23,6 @@
 #include <climits>
 #include <cudaTypedefs.h>
 
-namespace ddsim {
-
-namespace {
-constexpr int kChunkL = 16;
-constexpr int kStagesL = 4;
-constexpr int NLANE = 4;  // register lanes; index 4 = temp (rare predecessors)
-
-__device__ __forceinline__ unsigned su32l(const void* p) {
-  return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void l_mbar_init(unsigned long long* bar) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32l(bar)) : "memory");
-}
-__device__ __forceinline__ void l_expect(unsigned long long* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32l(bar)),
-               "r"(bytes) : "memory");
-}
-__device__ __forceinline__ void l_wait(unsigned long long* bar, unsigned parity) {
-  asm volatile(
-      "{\n.reg .pred p;\nW_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
-      "@!p bra W_%=;\n}\n" ::"r"(su32l(bar)), "r"(parity) : "memory");
-}
-__device__ __forceinline__ void l_bulk(void* dst, const void* src, unsigned bytes,
-                                       unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-      ::"r"(su32l(dst)), "l"(src), "r"(bytes), "r"(su32l(bar)) : "memory");
-}
-__device__ __forceinline__ void l_tile(void* dst, const CUtensorMap* map, int x, int y,
-                                       unsigned long long* bar) {
-  asm volatile(
-      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-      " [%0], [%1, {%2, %3}], [%4];" ::"r"(su32l(dst)), "l"(map), "r"(x), "r"(y), "r"(su32l(bar))
-      : "memory");
-}
-
-struct St {
-  long long lv[NLANE + 1][2];  // lane heads' rel (+ temp), 2 scenarios
-  long long lb[NLANE][2];      // lane busy
-};
-
-template <int OWN, int MASK, int GAP>
-__device__ __forceinline__ void hstep(St& S, long long d0, long long d1, long long gap,
-                                      long long*& sp, long long ld, bool store) {
-  long long a = S.lv[OWN][0], b = S.lv[OWN][1];
-#pragma unroll
-  for (int m = 0; m <= NLANE; ++m)
-    if (((MASK >> m) & 1) && m != OWN) {
-      a = max(a, S.lv[m][0]);
-      b = max(b, S.lv[m][1]);
-    }
-  if (store) {
-    __stcs(reinterpret_cast<longlong2*>(sp), make_longlong2(a, b));
-    sp += ld;
-  }
-  a += d0;
-  b += d1;
-  if (GAP) {
-    a += gap;
-    b += gap;
-  }
-  S.lv[OWN][0] = a;
-  S.lv[OWN][1] = b;
-  S.lb[OWN][0] += d0;
-  S.lb[OWN][1] += d1;
-}
-
-__device__ __forceinline__ long long own_get(const St& S, int own, int i) {
-  switch (own) {
-    case 0: return S.lv[0][i];
-    case 1: return S.lv[1][i];
-    case 2: return S.lv[2][i];
-    default: return S.lv[3][i];
-  }
-}
-
-__device__ __forceinline__ int4 l_lds128(unsigned a) {
-  int4 v;
-  asm volatile("ld.shared.v4.s32 {%0,%1,%2,%3}, [%4];"
-               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ int2 l_lds64i(unsigned a) {
-  int2 v;
-  asm volatile("ld.shared.v2.s32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ longlong2 l_lds128ll(unsigned a) {
-  longlong2 v;
-  asm volatile("ld.shared.v2.s64 {%0,%1}, [%2];" : "=l"(v.x), "=l"(v.y) : "r"(a));
-  return v;
-}
-__device__ __forceinline__ void l_sts128ll(unsigned a, long long x, long long y) {
-  asm volatile("st.shared.v2.s64 [%0], {%1,%2};" ::"r"(a), "l"(x), "l"(y) : "memory");
-}
-}  // namespace
-
 #define HCASE(h)                                                                      \
   case h:                                                                             \
     hstep<(h) & 3, ((h) >> 2) & 31, ((h) >> 7) & 1>(S, d0, d1, gap, sp, ld, store); \
@@ -129,180 +31,25 @@ __device__ __forceinline__ void l_sts128ll(unsigned a, long long x, long long y)
   HCASE(b + 6) HCASE(b + 7)
 #define HCASE64(b) HCASE8(b) HCASE8(b + 8) HCASE8(b + 16) HCASE8(b + 24) HCASE8(b + 32) \
   HCASE8(b + 40) HCASE8(b + 48) HCASE8(b + 56)
+#define DDSIM_DISPATCH(h) switch (h) { HCASE64(0) HCASE64(64) HCASE64(128) HCASE64(192) }
+#include "lanes_body.cuh"
+#undef DDSIM_DISPATCH
+
+namespace ddsim {
+
+static_assert(sizeof(LaneRec) == sizeof(ddsim_lanes::Rec), "record layouts differ");
+static_assert(sizeof(LaneParams) == sizeof(ddsim_lanes::Params), "param layouts differ");
 
 // DK: 1 = int32 durations via TMA tiles, 2 = int64 durations (direct loads).
 template <int DK>
-__global__ void __launch_bounds__(256) maxplus_lanes_kernel(const __grid_constant__ CUtensorMap tmap,
-                                                            const LaneParams p) {
-  extern __shared__ __align__(128) unsigned char smem[];
-  const int BD = blockDim.x;
-  const int W = BD * 2;
-  const int tid = threadIdx.x;
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem);
-  LaneRec* pst = reinterpret_cast<LaneRec*>(smem + 128);
-  const unsigned sbase = su32l(smem);
-  const unsigned prog_s = sbase + 128;
-  const unsigned tile_s = prog_s + kStagesL * kChunkL * (unsigned)sizeof(LaneRec);
-  const unsigned tile_all = DK == 1 ? (unsigned)(kStagesL * kChunkL * W * 4) : 0u;
-  const unsigned slot_s = tile_s + tile_all;                 // [ksm][BD] x 16 B
-  const unsigned col = (unsigned)(tid * 16);
-  const unsigned slot_pitch = (unsigned)(BD * 16);
-  int* tst = reinterpret_cast<int*>(smem + (tile_s - sbase));
-  const int s0 = blockIdx.x * W;
-  const int s = s0 + tid * 2;
-  const bool act = s < p.S;  // S is even (host)
-  const int nchunks = (p.n_rec + kChunkL - 1) / kChunkL;
-  const unsigned tile_bytes = DK == 1 ? (unsigned)(kChunkL * W * 4) : 0u;
-  auto issue = [&](int c) {
-    const int st = c % kStagesL;
-    const int nrec = min(kChunkL, p.n_rec - c * kChunkL);
-    const unsigned pb = (unsigned)(nrec * sizeof(LaneRec));
-    l_expect(&bars[st], pb + tile_bytes);
-    l_bulk(pst + st * kChunkL, p.prog + (long long)c * kChunkL, pb, &bars[st]);
-    if (DK == 1) l_tile(tst + st * kChunkL * W, &tmap, s0, c * kChunkL, &bars[st]);
-  };
-  if (tid == 0) {
-    for (int i = 0; i < kStagesL; ++i) l_mbar_init(&bars[i]);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-  }
-  __syncthreads();
-  if (tid == 0)
-    for (int c = 0; c < min(kStagesL, nchunks); ++c) issue(c);
-
-  St S;
-#pragma unroll
-  for (int l = 0; l <= NLANE; ++l) S.lv[l][0] = S.lv[l][1] = 0;
-#pragma unroll
-  for (int l = 0; l < NLANE; ++l) S.lb[l][0] = S.lb[l][1] = 0;
-  long long ms0 = 0, ms1 = 0;
-  int neg = 0;
-  const long long ld = p.start_ld;
-  const bool store = act && p.start != nullptr;
-  long long* sp = store ? p.start + s : nullptr;
-  const long long* dp = DK == 2 ? p.dense64 + (act ? s : 0) : nullptr;
-  const unsigned row_pitch = (unsigned)(W * 4);
-  const int ksm = p.ksm;
-
-  for (int c = 0; c < nchunks; ++c) {
-    const int st = c % kStagesL;
-    l_wait(&bars[st], (unsigned)((c / kStagesL) & 1));
-    const unsigned rec0 = prog_s + (unsigned)(st * kChunkL * sizeof(LaneRec));
-    const unsigned t0 = tile_s + (unsigned)(st * kChunkL) * row_pitch + (unsigned)(tid * 8);
-    const int nrec = min(kChunkL, p.n_rec - c * kChunkL);
-    int4 raw = l_lds128(rec0);
-    int2 dd = DK == 1 ? l_lds64i(t0) : make_int2(0, 0);
-    for (int j = 0; j < nrec; ++j) {
-      const int4 r = raw;
-      long long d0, d1;
-      if (DK == 1) {
-        d0 = (unsigned)dd.x;
-        d1 = (unsigned)dd.y;
-        neg |= dd.x | dd.y;
-      } else {
-        d0 = dp[0];
-        d1 = dp[1];
-        neg |= (int)((d0 | d1) >> 32);
-        dp += p.dense_ld;
-      }
-      if (j + 1 < nrec) {  // prefetch the next record and duration pair
-        raw = l_lds128(rec0 + (unsigned)(j + 1) * 16u);
-        if (DK == 1) dd = l_lds64i(t0 + (unsigned)(j + 1) * row_pitch);
-      }
-      const long long gap = ((long long)(unsigned)r.y << 32) | (unsigned)r.x;
-      const unsigned w = (unsigned)r.w;
-      const unsigned h = w >> 24;
-      const unsigned rare = (w >> 16) & 0xffu;
-      if (rare & LREC_PRE) {
-        // predecessors that are no longer lane heads (+ ready floor) -> temp lane
-        long long x0 = 0, x1 = 0;
-        const int row = c * kChunkL + j;
-        if (rare & LREC_S0) {
-          const longlong2 v = l_lds128ll(slot_s + (unsigned)((r.z << 16) >> 16) * slot_pitch + col);
-          x0 = max(x0, v.x);
-          x1 = max(x1, v.y);
-        }
-        if (rare & LREC_S1) {
-          const longlong2 v = l_lds128ll(slot_s + (unsigned)(r.z >> 16) * slot_pitch + col);
-          x0 = max(x0, v.x);
-          x1 = max(x1, v.y);
-        }
-        if (rare & LREC_SIDE) {
-          if (p.side_ready) {
-            x0 = max(x0, p.side_ready[row]);
-            x1 = max(x1, p.side_ready[row]);
-          }
-          if (p.side_off)
-            for (int k = p.side_off[row]; k < p.side_off[row + 1]; ++k) {
-              const int code = p.side_slots[k];
-              if (code < ksm) {
-                const longlong2 v = l_lds128ll(slot_s + (unsigned)code * slot_pitch + col);
-                x0 = max(x0, v.x);
-                x1 = max(x1, v.y);
-              } else if (act) {
-                const long long* g = p.gslots + (long long)(code - ksm) * p.s_pad + s;
-                x0 = max(x0, g[0]);
-                x1 = max(x1, g[1]);
-              }
-            }
-        }
-        S.lv[NLANE][0] = x0;
-        S.lv[NLANE][1] = x1;
-      }
-      switch (h) {
-        HCASE64(0)
-        HCASE64(64)
-        HCASE64(128)
-        HCASE64(192)
-      }
-      if (rare & LREC_POST) {
-        const int own = (int)(h & 3);
-        const long long r0 = own_get(S, own, 0), r1 = own_get(S, own, 1);
-        if (rare & LREC_MS) {
-          const long long g2 = (h >> 7) & 1 ? gap : 0;
-          ms0 = max(ms0, r0 - g2);
-          ms1 = max(ms1, r1 - g2);
-        }
-        if (rare & LREC_OUT_SMEM) {
-          l_sts128ll(slot_s + (unsigned)((w << 16) >> 16) * slot_pitch + col, r0, r1);
-        } else if ((rare & LREC_OUT_GLOBAL) && act) {
-          long long* g = p.gslots + (long long)((int)(w << 16) >> 16) * p.s_pad + s;
-          g[0] = r0;
-          g[1] = r1;
-        }
-      }
-    }
-    __syncthreads();
-    if (tid == 0 && c + kStagesL < nchunks) issue(c + kStagesL);
-  }
-  if (act) {
-    if (neg < 0 && p.neg_flag) atomicOr(p.neg_flag, 1);
-    if (p.makespan) {
-      p.makespan[s] = ms0;
-      p.makespan[s + 1] = ms1;
-    }
-    if (p.lane_busy)
-      for (int l = 0; l < p.L; ++l) {
-        long long v0 = 0, v1 = 0;
-#pragma unroll
-        for (int q = 0; q < NLANE; ++q)
-          if (q == l) {
-            v0 = S.lb[q][0];
-            v1 = S.lb[q][1];
-          }
-        p.lane_busy[(long long)s * p.L + l] = v0;
-        p.lane_busy[(long long)(s + 1) * p.L + l] = v1;
-      }
-  }
+__global__ void __launch_bounds__(256) maxplus_lanes_kernel(const __grid_constant__ ddsim_lanes::Tmap tmap,
+                                                            const ddsim_lanes::Params p) {
+  ddsim_lanes::lanes_body<DK>(&tmap, p);
 }
 
-#undef HCASE
-#undef HCASE8
-#undef HCASE64
-
 static size_t lanes_smem(int dk, int BD, int ksm) {
-  size_t b = 128 + (size_t)kStagesL * kChunkL * sizeof(LaneRec);
-  if (dk == 1) b += (size_t)kStagesL * kChunkL * BD * 2 * 4;
+  size_t b = 128 + (size_t)ddsim_lanes::kStagesL * ddsim_lanes::kChunkL * sizeof(ddsim_lanes::Rec);
+  if (dk == 1) b += (size_t)ddsim_lanes::kStagesL * ddsim_lanes::kChunkL * BD * 2 * 4;
   return b + (size_t)ksm * BD * 16;
 }
 
@@ -316,7 +63,7 @@ int maxplus_lanes_block_dim(int S, int num_sms) {
 }
 
 cudaError_t launch_maxplus_lanes(const LaneParams& p, const int* dense32, int dkind,
-                                 cudaStream_t stream) {
+                                 const std::vector<int>* codes, cudaStream_t stream) {
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
@@ -336,21 +83,28 @@ cudaError_t launch_maxplus_lanes(const LaneParams& p, const int* dense32, int dk
     auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
     cuuint64_t dims[2] = {(cuuint64_t)p.S, (cuuint64_t)p.n_rec};
     cuuint64_t strides[1] = {(cuuint64_t)(p.dense_ld * sizeof(int))};
-    cuuint32_t box[2] = {(cuuint32_t)W, (cuuint32_t)kChunkL};
+    cuuint32_t box[2] = {(cuuint32_t)W, (cuuint32_t)ddsim_lanes::kChunkL};
     cuuint32_t estr[2] = {1, 1};
     if (enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, const_cast<int*>(dense32), dims, strides, box,
             estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
             CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
+  }
+  // per-graph specialised dispatch first (NVRTC); the static kernel otherwise
+  if (codes != nullptr) {
+    const cudaError_t e = launch_maxplus_lanes_jit(p, &tmap, dkind, *codes, grid, BD, smem, stream);
+    if (e == cudaSuccess) return cudaGetLastError();
+  }
+  if (dkind == 1) {
     cudaError_t err = cudaFuncSetAttribute(maxplus_lanes_kernel<1>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
-    maxplus_lanes_kernel<1><<<grid, BD, smem, stream>>>(tmap, p);
+    maxplus_lanes_kernel<1><<<grid, BD, smem, stream>>>(*reinterpret_cast<const ddsim_lanes::Tmap*>(&tmap), *reinterpret_cast<const ddsim_lanes::Params*>(&p));
   } else {
     cudaError_t err = cudaFuncSetAttribute(maxplus_lanes_kernel<2>,
                                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (err != cudaSuccess) return err;
-    maxplus_lanes_kernel<2><<<grid, BD, smem, stream>>>(tmap, p);
+    maxplus_lanes_kernel<2><<<grid, BD, smem, stream>>>(*reinterpret_cast<const ddsim_lanes::Tmap*>(&tmap), *reinterpret_cast<const ddsim_lanes::Params*>(&p));
   }
   note_launch();
   return cudaGetLastError();
