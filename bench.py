@@ -228,6 +228,8 @@ def run_ours(args):
     e1.record(stream)
     torch.cuda.synchronize()
     launches = N.launch_count() - l0
+    jit = (N.lib().ks_jit_log() or b"").decode()
+    kernel_name = "ddsim_lanes_jit (NVRTC-specialised)" if "compiled" in jit else "static"
     elapsed_ms = e0.elapsed_time(e1)
     if ws > 1:
         t = torch.tensor([elapsed_ms], device=f"cuda:{dev}")
@@ -307,6 +309,7 @@ def run_ours(args):
             "cpu_baseline": cb,
             "e2e": e2e,
             "gpu_launches": launches,
+            "kernel": kernel_name,
             "clocks": clk,
         }
         print(json.dumps(line), flush=True)

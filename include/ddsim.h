@@ -268,6 +268,8 @@ int ks_device_count(int* n);
 /* Number of kernels this library launched on the calling process so far. */
 int64_t ks_launch_count(void);
 const char* ks_version(void);
+/* Diagnostics of the per-graph NVRTC specialisation (status + compile log). */
+const char* ks_jit_log(void);
 
 #ifdef __cplusplus
 }

@@ -119,6 +119,7 @@ _SIGNATURES = [
     ("ks_device_count", C.c_int, [C.POINTER(C.c_int)]),
     ("ks_launch_count", C.c_int64, []),
     ("ks_version", C.c_char_p, []),
+    ("ks_jit_log", C.c_char_p, []),
 ]
 EXPORTED_SYMBOLS = [s[0] for s in _SIGNATURES]
 

@@ -78,13 +78,18 @@ void init_locked() {
   void* h = nullptr;
   for (const char* l : libs)
     if ((h = dlopen(l, RTLD_NOW | RTLD_LOCAL)) != nullptr) break;
-  if (!h) return;
+  if (!h) {
+    g_jit_log = std::string("dlopen nvrtc failed: ") + (dlerror() ? dlerror() : "?");
+    return;
+  }
   g_nv.ok = sym(h, "nvrtcCreateProgram", g_nv.create) && sym(h, "nvrtcCompileProgram", g_nv.compile) &&
             sym(h, "nvrtcGetCUBINSize", g_nv.cubin_size) && sym(h, "nvrtcGetCUBIN", g_nv.cubin) &&
             sym(h, "nvrtcGetProgramLogSize", g_nv.log_size) &&
             sym(h, "nvrtcGetProgramLog", g_nv.log) && sym(h, "nvrtcDestroyProgram", g_nv.destroy);
   g_drv.ok = drv("cuModuleLoadData", g_drv.load) && drv("cuModuleGetFunction", g_drv.getfn) &&
              drv("cuFuncSetAttribute", g_drv.setattr) && drv("cuLaunchKernel", g_drv.launch);
+  g_jit_log = std::string("nvrtc ") + (g_nv.ok ? "ok" : "missing symbols") + ", driver " +
+              (g_drv.ok ? "ok" : "missing entry points");
 }
 
 std::string make_source(const std::vector<int>& codes, int dk) {
@@ -96,7 +101,7 @@ std::string make_source(const std::vector<int>& codes, int dk) {
             std::to_string((c >> 7) & 1) + ">(S, d0, d1, gap, sp, ld, store); ";
   }
   disp += "else __trap();\n";
-  std::string src = "#define DDSIM_LANES_NO_STD_TYPES 1\n" + disp + kLanesBodySrc;
+  std::string src = "#define DDSIM_LANES_NO_STD_TYPES 1\n#define DDSIM_UNROLL 1\n" + disp + kLanesBodySrc;
   src += "\nextern \"C\" __global__ void __launch_bounds__(256) ddsim_lanes_jit("
          "const __grid_constant__ ddsim_lanes::Tmap tmap, const ddsim_lanes::Params p) {\n"
          "  ddsim_lanes::lanes_body<" + std::to_string(dk) + ">(&tmap, p);\n}\n";
@@ -119,17 +124,29 @@ CUfunction get_function(const std::vector<int>& codes, int dk, int device) {
     const int rc = g_nv.compile(prog, 3, opts);
     size_t ls = 0;
     g_nv.log_size(prog, &ls);
-    g_jit_log.assign(ls, '\0');
-    if (ls) g_nv.log(prog, &g_jit_log[0]);
+    if (ls > 1) {
+      std::string lg(ls, '\0');
+      g_nv.log(prog, &lg[0]);
+      lg.resize(ls - 1);
+      g_jit_log += "\nnvrtc log: " + lg;
+    }
     if (rc == 0) {
       size_t n = 0;
       g_nv.cubin_size(prog, &n);
       std::vector<char> bin(n);
       g_nv.cubin(prog, bin.data());
       CUmodule mod = nullptr;
-      if (g_drv.load(&mod, bin.data()) == CUDA_SUCCESS &&
-          g_drv.getfn(&fn, mod, "ddsim_lanes_jit") != CUDA_SUCCESS)
+      const CUresult lr = g_drv.load(&mod, bin.data());
+      if (lr != CUDA_SUCCESS) {
+        g_jit_log += "\ncuModuleLoadData failed: " + std::to_string((int)lr);
+      } else if (g_drv.getfn(&fn, mod, "ddsim_lanes_jit") != CUDA_SUCCESS) {
+        g_jit_log += "\ncuModuleGetFunction failed";
         fn = nullptr;
+      } else {
+        g_jit_log += "\ncompiled " + key;
+      }
+    } else {
+      g_jit_log += "\nnvrtc compile failed rc=" + std::to_string(rc);
     }
     g_nv.destroy(&prog);
   }
@@ -144,20 +161,29 @@ CUfunction get_function(const std::vector<int>& codes, int dk, int device) {
 cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const void* tmap128, int dkind,
                                      const std::vector<int>& codes, int grid, int BD, size_t smem,
                                      cudaStream_t stream) {
-  if (codes.empty() || codes.size() > 32) return cudaErrorNotSupported;
+  if (codes.empty() || codes.size() > 32) {
+    g_jit_log += "\nskipped: " + std::to_string(codes.size()) + " handler codes";
+    return cudaErrorNotSupported;
+  }
   int dev = 0;
   cudaGetDevice(&dev);
   CUfunction fn = get_function(codes, dkind, dev);
   if (!fn) return cudaErrorNotSupported;
-  if (g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem) != CUDA_SUCCESS)
+  const CUresult ar = g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
+  if (ar != CUDA_SUCCESS) {
+    g_jit_log += "\ncuFuncSetAttribute failed: " + std::to_string((int)ar);
     return cudaErrorNotSupported;
+  }
   alignas(64) unsigned char tm[128];
   memcpy(tm, tmap128, 128);
   LaneParams pp = p;
   void* args[] = {tm, &pp};
-  if (g_drv.launch(fn, grid, 1, 1, BD, 1, 1, (unsigned)smem, (CUstream)stream, args, nullptr) !=
-      CUDA_SUCCESS)
-    return cudaErrorLaunchFailure;
+  const CUresult r = g_drv.launch(fn, grid, 1, 1, BD, 1, 1, (unsigned)smem, (CUstream)stream, args,
+                                  nullptr);
+  if (r != CUDA_SUCCESS) {
+    g_jit_log += "\ncuLaunchKernel failed: " + std::to_string((int)r);
+    return cudaErrorNotSupported;
+  }
   note_launch();
   return cudaSuccess;
 }
@@ -165,3 +191,5 @@ cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const void* tmap128, i
 const char* jit_log() { return g_jit_log.c_str(); }
 
 }  // namespace ddsim
+
+extern "C" const char* ks_jit_log(void) { return ddsim::jit_log(); }

@@ -155,7 +155,8 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p) {
   const int tid = threadIdx.x;
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem);
   Rec* pst = reinterpret_cast<Rec*>(smem + 128);
-  const unsigned sbase = su32l(smem);
+  unsigned sbase = su32l(smem);
+  asm volatile("" : "+r"(sbase));  // keep in a register (no per-record rematerialisation)
   const unsigned prog_s = sbase + 128;
   const unsigned tile_s = prog_s + kStagesL * kChunkL * (unsigned)sizeof(Rec);
   const unsigned tile_all = DK == 1 ? (unsigned)(kStagesL * kChunkL * W * 4) : 0u;
@@ -207,7 +208,7 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p) {
     const int nrec = min(kChunkL, p.n_rec - c * kChunkL);
     int4 raw = l_lds128(rec0);
     int2 dd = DK == 1 ? l_lds64i(t0) : make_int2(0, 0);
-    for (int j = 0; j < nrec; ++j) {
+    auto record = [&](int j) {
       const int4 r = raw;
       long long d0, d1;
       if (DK == 1) {
@@ -281,7 +282,19 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p) {
           g[1] = r1;
         }
       }
+        };
+#ifdef DDSIM_UNROLL
+    if (nrec == kChunkL) {
+#pragma unroll
+      for (int j = 0; j < kChunkL; ++j) record(j);
+    } else {
+#pragma unroll 1
+      for (int j = 0; j < nrec; ++j) record(j);
     }
+#else
+#pragma unroll 1
+    for (int j = 0; j < nrec; ++j) record(j);
+#endif
     __syncthreads();
     if (tid == 0 && c + kStagesL < nchunks) issue(c + kStagesL);
   }
