@@ -197,9 +197,10 @@ cudaError_t launch_maxplus_dense(const DenseParams& p, const int* dense32, int d
                                  cudaStream_t stream);
 cudaError_t launch_maxplus_lanes(const LaneParams& p, const int* dense32, int dkind,
                                  const std::vector<int>* codes, cudaStream_t stream);
-cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const void* tmap128, int dkind,
+cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const void* tmap128, int dkind, int V,
                                      const std::vector<int>& codes, int grid, int BD, size_t smem,
                                      cudaStream_t stream);
+int maxplus_lanes_vec(int S);
 const char* jit_log();
 int maxplus_lanes_block_dim(int S, int num_sms);
 cudaError_t launch_listsched(const ListParams& p, cudaStream_t stream);

@@ -917,10 +917,7 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
   build_tables(g, sc, T, true, policy == KS_POLICY_VDNN);
 
   const bool lanes_ok = use_max && dense && g->has_lanes && sc->n_overrides == 0 &&
-                        !sc->scale_ptr && S % 2 == 0 && sc->dense_ld % 2 == 0 &&
-                        (out->start == nullptr ||
-                         (out->start_ld % 2 == 0 && reinterpret_cast<uintptr_t>(out->start) % 16 == 0)) &&
-                        getenv("DDSIM_NO_LANES") == nullptr;
+                        !sc->scale_ptr && getenv("DDSIM_NO_LANES") == nullptr;
   if (lanes_ok) {
     LaneParams p;
     memset(&p, 0, sizeof(p));
@@ -945,7 +942,8 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device);
     const int BD = maxplus_lanes_block_dim(S, nsm);
-    p.s_pad = (long long)((S + 2 * BD - 1) / (2 * BD)) * 2 * BD;
+    const int LV = maxplus_lanes_vec(S);
+    p.s_pad = (long long)((S + LV * BD - 1) / (LV * BD)) * LV * BD;
     if (p.kglob > 0) p.gslots = T.scratch<long long>((size_t)p.kglob * p.s_pad);
     int* flag = T.scratch<int>(1);
     CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), stream));

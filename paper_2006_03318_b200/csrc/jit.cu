@@ -92,31 +92,35 @@ void init_locked() {
               (g_drv.ok ? "ok" : "missing entry points");
 }
 
-std::string make_source(const std::vector<int>& codes, int dk) {
+std::string make_source(const std::vector<int>& codes, int dk, int V) {
   std::string disp = "#define DDSIM_DISPATCH(h) ";
   for (size_t i = 0; i < codes.size(); ++i) {
     const int c = codes[i];
     disp += (i ? "else if (h == " : "if (h == ") + std::to_string(c) + "u) hstep<" +
             std::to_string(c & 3) + ", " + std::to_string((c >> 2) & 31) + ", " +
-            std::to_string((c >> 7) & 1) + ">(S, d0, d1, gap, sp, ld, store); ";
+            std::to_string((c >> 7) & 1) + ", V>(S, d0, d1, gap, sp, ld, store); ";
   }
   disp += "else __trap();\n";
-  std::string src = "#define DDSIM_LANES_NO_STD_TYPES 1\n#define DDSIM_UNROLL 1\n" + disp + kLanesBodySrc;
+  std::string src = "#define DDSIM_LANES_NO_STD_TYPES 1\n";
+  if (const char* u = getenv("DDSIM_JIT_UNROLL")) src += std::string("#define DDSIM_UNROLL ") + u + "\n";
+  src += disp + kLanesBodySrc;
   src += "\nextern \"C\" __global__ void __launch_bounds__(256) ddsim_lanes_jit("
          "const __grid_constant__ ddsim_lanes::Tmap tmap, const ddsim_lanes::Params p) {\n"
-         "  ddsim_lanes::lanes_body<" + std::to_string(dk) + ">(&tmap, p);\n}\n";
+         "  ddsim_lanes::lanes_body<" + std::to_string(dk) + ", " + std::to_string(V) +
+         ">(&tmap, p);\n}\n";
   return src;
 }
 
-CUfunction get_function(const std::vector<int>& codes, int dk, int device) {
-  std::string key = std::to_string(device) + ":" + std::to_string(dk) + ":";
+CUfunction get_function(const std::vector<int>& codes, int dk, int V, int device) {
+  std::string key = std::to_string(device) + ":" + std::to_string(dk) + ":" + std::to_string(V) + ":";
+  if (const char* u = getenv("DDSIM_JIT_UNROLL")) key += std::string("u") + u + ":";
   for (int c : codes) key += std::to_string(c) + ",";
   std::lock_guard<std::mutex> lk(g_mu);
   init_locked();
   if (!g_nv.ok || !g_drv.ok) return nullptr;
   auto it = g_cache.find(key);
   if (it != g_cache.end()) return it->second;
-  const std::string src = make_source(codes, dk);
+  const std::string src = make_source(codes, dk, V);
   nvrtcProgram_t prog = nullptr;
   CUfunction fn = nullptr;
   if (g_nv.create(&prog, src.c_str(), "ddsim_lanes_jit.cu", 0, nullptr, nullptr) == 0) {
@@ -158,7 +162,7 @@ CUfunction get_function(const std::vector<int>& codes, int dk, int device) {
 
 // Launch the specialised kernel; cudaErrorNotSupported when JIT is unavailable
 // (the caller then launches the static kernel).
-cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const void* tmap128, int dkind,
+cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const void* tmap128, int dkind, int V,
                                      const std::vector<int>& codes, int grid, int BD, size_t smem,
                                      cudaStream_t stream) {
   if (codes.empty() || codes.size() > 32) {
@@ -167,7 +171,7 @@ cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const void* tmap128, i
   }
   int dev = 0;
   cudaGetDevice(&dev);
-  CUfunction fn = get_function(codes, dkind, dev);
+  CUfunction fn = get_function(codes, dkind, V, dev);
   if (!fn) return cudaErrorNotSupported;
   const CUresult ar = g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
   if (ar != CUDA_SUCCESS) {

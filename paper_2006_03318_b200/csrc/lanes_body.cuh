@@ -84,39 +84,43 @@ __device__ __forceinline__ void l_tile(void* dst, const Tmap* map, int x, int y,
 }
 __device__ __forceinline__ long long lmax(long long a, long long b) { return a > b ? a : b; }
 
+template <int V>
 struct St {
-  long long lv[NLANE + 1][2];  // lane heads' rel (+ temp), 2 scenarios
-  long long lb[NLANE][2];      // lane busy
+  long long lv[NLANE + 1][V];  // lane heads' rel (+ temp), V scenarios
+  long long lb[NLANE][V];      // lane busy
 };
 
-template <int OWN, int MASK, int GAP>
-__device__ __forceinline__ void hstep(St& S, long long d0, long long d1, long long gap,
+template <int OWN, int MASK, int GAP, int V>
+__device__ __forceinline__ void hstep(St<V>& S, long long d0, long long d1, long long gap,
                                       long long*& sp, long long ld, bool store) {
-  long long a = S.lv[OWN][0], b = S.lv[OWN][1];
+  long long a = S.lv[OWN][0], b = S.lv[OWN][V - 1];
 #pragma unroll
   for (int m = 0; m <= NLANE; ++m)
     if (((MASK >> m) & 1) && m != OWN) {
       a = lmax(a, S.lv[m][0]);
-      b = lmax(b, S.lv[m][1]);
+      if (V == 2) b = lmax(b, S.lv[m][V - 1]);
     }
   if (store) {
     __stcs(sp, a);
-    __stcs(sp + 1, b);
+    if (V == 2) __stcs(sp + 1, b);
     sp += ld;
   }
   a += d0;
-  b += d1;
+  if (V == 2) b += d1;
   if (GAP) {
     a += gap;
-    b += gap;
+    if (V == 2) b += gap;
   }
   S.lv[OWN][0] = a;
-  S.lv[OWN][1] = b;
   S.lb[OWN][0] += d0;
-  S.lb[OWN][1] += d1;
+  if (V == 2) {
+    S.lv[OWN][V - 1] = b;
+    S.lb[OWN][V - 1] += d1;
+  }
 }
 
-__device__ __forceinline__ long long own_get(const St& S, int own, int i) {
+template <int V>
+__device__ __forceinline__ long long own_get(const St<V>& S, int own, int i) {
   switch (own) {
     case 0: return S.lv[0][i];
     case 1: return S.lv[1][i];
@@ -145,13 +149,34 @@ __device__ __forceinline__ void l_sts128ll(unsigned a, long long x, long long y)
   asm volatile("st.shared.v2.s64 [%0], {%1,%2};" ::"r"(a), "l"(x), "l"(y) : "memory");
 }
 
+// Load / store the V values of one slot column.
+template <int V>
+__device__ __forceinline__ void slot_ld(unsigned a, long long& x0, long long& x1) {
+  if (V == 2) {
+    const longlong2 v = l_lds128ll(a);
+    x0 = v.x;
+    x1 = v.y;
+  } else {
+    asm volatile("ld.shared.s64 %0, [%1];" : "=l"(x0) : "r"(a));
+    x1 = x0;
+  }
+}
+template <int V>
+__device__ __forceinline__ void slot_st(unsigned a, long long x0, long long x1) {
+  if (V == 2)
+    l_sts128ll(a, x0, x1);
+  else
+    asm volatile("st.shared.s64 [%0], %1;" ::"r"(a), "l"(x0) : "memory");
+}
+
 // The kernel body; DDSIM_DISPATCH(h) must expand to the handler dispatch
-// (it sees S, d0, d1, gap, sp, ld, store).
-template <int DK>
+// (it sees S, d0, d1, gap, sp, ld, store and the template parameter V).
+// Each thread owns V consecutive scenarios (V = 1 or 2).
+template <int DK, int V>
 __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int BD = blockDim.x;
-  const int W = BD * 2;
+  const int W = BD * V;  // scenarios per CTA
   const int tid = threadIdx.x;
   unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem);
   Rec* pst = reinterpret_cast<Rec*>(smem + 128);
@@ -160,13 +185,13 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p) {
   const unsigned prog_s = sbase + 128;
   const unsigned tile_s = prog_s + kStagesL * kChunkL * (unsigned)sizeof(Rec);
   const unsigned tile_all = DK == 1 ? (unsigned)(kStagesL * kChunkL * W * 4) : 0u;
-  const unsigned slot_s = tile_s + tile_all;                 // [ksm][BD] x 16 B
-  const unsigned col = (unsigned)(tid * 16);
-  const unsigned slot_pitch = (unsigned)(BD * 16);
+  const unsigned slot_s = tile_s + tile_all;                  // [ksm][BD] x (8 V) B
+  const unsigned col = (unsigned)(tid * 8 * V);
+  const unsigned slot_pitch = (unsigned)(BD * 8 * V);
   int* tst = reinterpret_cast<int*>(smem + (tile_s - sbase));
   const int s0 = blockIdx.x * W;
-  const int s = s0 + tid * 2;
-  const bool act = s < p.S;  // S is even (host)
+  const int s = s0 + tid * V;
+  const bool act = s < p.S;  // S % V == 0 (host)
   const int nchunks = (p.n_rec + kChunkL - 1) / kChunkL;
   const unsigned tile_bytes = DK == 1 ? (unsigned)(kChunkL * W * 4) : 0u;
   auto issue = [&](int c) {
@@ -186,11 +211,15 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p) {
   if (tid == 0)
     for (int c = 0; c < min(kStagesL, nchunks); ++c) issue(c);
 
-  St S;
+  St<V> S;
 #pragma unroll
-  for (int l = 0; l <= NLANE; ++l) S.lv[l][0] = S.lv[l][1] = 0;
+  for (int l = 0; l <= NLANE; ++l)
 #pragma unroll
-  for (int l = 0; l < NLANE; ++l) S.lb[l][0] = S.lb[l][1] = 0;
+    for (int i = 0; i < V; ++i) S.lv[l][i] = 0;
+#pragma unroll
+  for (int l = 0; l < NLANE; ++l)
+#pragma unroll
+    for (int i = 0; i < V; ++i) S.lb[l][i] = 0;
   long long ms0 = 0, ms1 = 0;
   int neg = 0;
   const long long ld = p.start_ld;
@@ -204,26 +233,38 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p) {
     const int st = c % kStagesL;
     l_wait(&bars[st], (unsigned)((c / kStagesL) & 1));
     const unsigned rec0 = prog_s + (unsigned)(st * kChunkL * sizeof(Rec));
-    const unsigned t0 = tile_s + (unsigned)(st * kChunkL) * row_pitch + (unsigned)(tid * 8);
+    const unsigned t0 = tile_s + (unsigned)(st * kChunkL) * row_pitch + (unsigned)(tid * 4 * V);
     const int nrec = min(kChunkL, p.n_rec - c * kChunkL);
     int4 raw = l_lds128(rec0);
-    int2 dd = DK == 1 ? l_lds64i(t0) : make_int2(0, 0);
+    int2 dd = make_int2(0, 0);
+    if (DK == 1) {
+      if (V == 2)
+        dd = l_lds64i(t0);
+      else
+        asm volatile("ld.shared.s32 %0, [%1];" : "=r"(dd.x) : "r"(t0));
+    }
     auto record = [&](int j) {
       const int4 r = raw;
-      long long d0, d1;
+      long long d0, d1 = 0;
       if (DK == 1) {
         d0 = (unsigned)dd.x;
-        d1 = (unsigned)dd.y;
+        if (V == 2) d1 = (unsigned)dd.y;
         neg |= dd.x | dd.y;
       } else {
         d0 = dp[0];
-        d1 = dp[1];
+        if (V == 2) d1 = dp[1];
         neg |= (int)((d0 | d1) >> 32);
         dp += p.dense_ld;
       }
-      if (j + 1 < nrec) {  // prefetch the next record and duration pair
+      if (j + 1 < nrec) {  // prefetch the next record and durations
         raw = l_lds128(rec0 + (unsigned)(j + 1) * 16u);
-        if (DK == 1) dd = l_lds64i(t0 + (unsigned)(j + 1) * row_pitch);
+        if (DK == 1) {
+          const unsigned ta = t0 + (unsigned)(j + 1) * row_pitch;
+          if (V == 2)
+            dd = l_lds64i(ta);
+          else
+            asm volatile("ld.shared.s32 %0, [%1];" : "=r"(dd.x) : "r"(ta));
+        }
       }
       const long long gap = ((long long)(unsigned)r.y << 32) | (unsigned)r.x;
       const unsigned w = (unsigned)r.w;
@@ -231,17 +272,17 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p) {
       const unsigned rare = (w >> 16) & 0xffu;
       if (rare & R_PRE) {
         // predecessors that are no longer lane heads (+ ready floor) -> temp lane
-        long long x0 = 0, x1 = 0;
+        long long x0 = 0, x1 = 0, y0, y1;
         const int row = c * kChunkL + j;
         if (rare & R_S0) {
-          const longlong2 v = l_lds128ll(slot_s + (unsigned)((r.z << 16) >> 16) * slot_pitch + col);
-          x0 = lmax(x0, v.x);
-          x1 = lmax(x1, v.y);
+          slot_ld<V>(slot_s + (unsigned)((r.z << 16) >> 16) * slot_pitch + col, y0, y1);
+          x0 = lmax(x0, y0);
+          x1 = lmax(x1, y1);
         }
         if (rare & R_S1) {
-          const longlong2 v = l_lds128ll(slot_s + (unsigned)(r.z >> 16) * slot_pitch + col);
-          x0 = lmax(x0, v.x);
-          x1 = lmax(x1, v.y);
+          slot_ld<V>(slot_s + (unsigned)(r.z >> 16) * slot_pitch + col, y0, y1);
+          x0 = lmax(x0, y0);
+          x1 = lmax(x1, y1);
         }
         if (rare & R_SIDE) {
           if (p.side_ready) {
@@ -252,40 +293,40 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p) {
             for (int k = p.side_off[row]; k < p.side_off[row + 1]; ++k) {
               const int code = p.side_slots[k];
               if (code < ksm) {
-                const longlong2 v = l_lds128ll(slot_s + (unsigned)code * slot_pitch + col);
-                x0 = lmax(x0, v.x);
-                x1 = lmax(x1, v.y);
+                slot_ld<V>(slot_s + (unsigned)code * slot_pitch + col, y0, y1);
+                x0 = lmax(x0, y0);
+                x1 = lmax(x1, y1);
               } else if (act) {
                 const long long* g = p.gslots + (long long)(code - ksm) * p.s_pad + s;
                 x0 = lmax(x0, g[0]);
-                x1 = lmax(x1, g[1]);
+                x1 = lmax(x1, g[V - 1]);
               }
             }
         }
         S.lv[NLANE][0] = x0;
-        S.lv[NLANE][1] = x1;
+        S.lv[NLANE][V - 1] = V == 2 ? x1 : x0;
       }
       DDSIM_DISPATCH(h)
       if (rare & R_POST) {
         const int own = (int)(h & 3);
-        const long long r0 = own_get(S, own, 0), r1 = own_get(S, own, 1);
+        const long long r0 = own_get<V>(S, own, 0), r1 = own_get<V>(S, own, V - 1);
         if (rare & R_MS) {
           const long long g2 = (h >> 7) & 1 ? gap : 0;
           ms0 = lmax(ms0, r0 - g2);
           ms1 = lmax(ms1, r1 - g2);
         }
         if (rare & R_OUT_SMEM) {
-          l_sts128ll(slot_s + (unsigned)((w << 16) >> 16) * slot_pitch + col, r0, r1);
+          slot_st<V>(slot_s + (unsigned)((w << 16) >> 16) * slot_pitch + col, r0, r1);
         } else if ((rare & R_OUT_GLOBAL) && act) {
           long long* g = p.gslots + (long long)((int)(w << 16) >> 16) * p.s_pad + s;
           g[0] = r0;
-          g[1] = r1;
+          if (V == 2) g[1] = r1;
         }
       }
-        };
+    };
 #ifdef DDSIM_UNROLL
     if (nrec == kChunkL) {
-#pragma unroll
+#pragma unroll DDSIM_UNROLL
       for (int j = 0; j < kChunkL; ++j) record(j);
     } else {
 #pragma unroll 1
@@ -302,7 +343,7 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p) {
     if (neg < 0 && p.neg_flag) atomicOr(p.neg_flag, 1);
     if (p.makespan) {
       p.makespan[s] = ms0;
-      p.makespan[s + 1] = ms1;
+      if (V == 2) p.makespan[s + 1] = ms1;
     }
     if (p.lane_busy)
       for (int l = 0; l < p.L; ++l) {
@@ -311,10 +352,10 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p) {
         for (int q = 0; q < NLANE; ++q)
           if (q == l) {
             v0 = S.lb[q][0];
-            v1 = S.lb[q][1];
+            v1 = S.lb[q][V - 1];
           }
         p.lane_busy[(long long)s * p.L + l] = v0;
-        p.lane_busy[(long long)(s + 1) * p.L + l] = v1;
+        if (V == 2) p.lane_busy[(long long)(s + 1) * p.L + l] = v1;
       }
   }
 }

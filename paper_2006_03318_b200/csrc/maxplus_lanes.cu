@@ -25,7 +25,7 @@
 
 #define HCASE(h)                                                                      \
   case h:                                                                             \
-    hstep<(h) & 3, ((h) >> 2) & 31, ((h) >> 7) & 1>(S, d0, d1, gap, sp, ld, store); \
+    hstep<(h) & 3, ((h) >> 2) & 31, ((h) >> 7) & 1, V>(S, d0, d1, gap, sp, ld, store); \
     break;
 #define HCASE8(b) HCASE(b) HCASE(b + 1) HCASE(b + 2) HCASE(b + 3) HCASE(b + 4) HCASE(b + 5) \
   HCASE(b + 6) HCASE(b + 7)
@@ -41,25 +41,35 @@ static_assert(sizeof(LaneRec) == sizeof(ddsim_lanes::Rec), "record layouts diffe
 static_assert(sizeof(LaneParams) == sizeof(ddsim_lanes::Params), "param layouts differ");
 
 // DK: 1 = int32 durations via TMA tiles, 2 = int64 durations (direct loads).
-template <int DK>
+template <int DK, int V>
 __global__ void __launch_bounds__(256) maxplus_lanes_kernel(const __grid_constant__ ddsim_lanes::Tmap tmap,
                                                             const ddsim_lanes::Params p) {
-  ddsim_lanes::lanes_body<DK>(&tmap, p);
+  ddsim_lanes::lanes_body<DK, V>(&tmap, p);
 }
 
-static size_t lanes_smem(int dk, int BD, int ksm) {
+static size_t lanes_smem(int dk, int BD, int V, int ksm) {
   size_t b = 128 + (size_t)ddsim_lanes::kStagesL * ddsim_lanes::kChunkL * sizeof(ddsim_lanes::Rec);
-  if (dk == 1) b += (size_t)ddsim_lanes::kStagesL * ddsim_lanes::kChunkL * BD * 2 * 4;
-  return b + (size_t)ksm * BD * 16;
+  if (dk == 1) b += (size_t)ddsim_lanes::kStagesL * ddsim_lanes::kChunkL * BD * V * 4;
+  return b + (size_t)ksm * BD * 8 * V;
 }
 
-// 2 scenarios per thread; two CTAs per SM cover S in one wave.  BD is a
-// multiple of 16 (not 32) so the grid is close to 2 x #SMs.
+// V scenarios per thread (env DDSIM_LANES_V overrides: 1 or 2); two CTAs per
+// SM cover S in one wave.  BD is a multiple of 16 so the grid is close to
+// 2 x #SMs; the TMA box (BD * V ints) stays <= 256.
+int maxplus_lanes_vec(int S) {
+  const char* e = getenv("DDSIM_LANES_V");
+  int v = e ? atoi(e) : 1;
+  if (v != 1 && v != 2) v = 1;
+  if (S % v) v = 1;
+  return v;
+}
 int maxplus_lanes_block_dim(int S, int num_sms) {
-  const long long threads = (S + 1) / 2;
+  const int V = maxplus_lanes_vec(S);
+  const long long threads = (S + V - 1) / V;
   long long per = (threads + 2LL * num_sms - 1) / (2LL * num_sms);
   int bd = (int)(((per + 15) / 16) * 16);
-  return bd < 32 ? 32 : (bd > 128 ? 128 : bd);
+  const int cap = 256 / V;
+  return bd < 32 ? 32 : (bd > cap ? cap : bd);
 }
 
 cudaError_t launch_maxplus_lanes(const LaneParams& p, const int* dense32, int dkind,
@@ -67,11 +77,12 @@ cudaError_t launch_maxplus_lanes(const LaneParams& p, const int* dense32, int dk
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const int V = maxplus_lanes_vec(p.S);
   const int BD = maxplus_lanes_block_dim(p.S, nsm);
-  const int W = BD * 2;
+  const int W = BD * V;
   const int grid = (p.S + W - 1) / W;
   if ((long long)grid * W > p.s_pad) return cudaErrorInvalidValue;
-  const size_t smem = lanes_smem(dkind, BD, p.ksm);
+  const size_t smem = lanes_smem(dkind, BD, V, p.ksm);
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
   if (dkind == 1) {
@@ -92,20 +103,27 @@ cudaError_t launch_maxplus_lanes(const LaneParams& p, const int* dense32, int dk
   }
   // per-graph specialised dispatch first (NVRTC); the static kernel otherwise
   if (codes != nullptr) {
-    const cudaError_t e = launch_maxplus_lanes_jit(p, &tmap, dkind, *codes, grid, BD, smem, stream);
+    const cudaError_t e = launch_maxplus_lanes_jit(p, &tmap, dkind, V, *codes, grid, BD, smem, stream);
     if (e == cudaSuccess) return cudaGetLastError();
   }
-  if (dkind == 1) {
-    cudaError_t err = cudaFuncSetAttribute(maxplus_lanes_kernel<1>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (err != cudaSuccess) return err;
-    maxplus_lanes_kernel<1><<<grid, BD, smem, stream>>>(*reinterpret_cast<const ddsim_lanes::Tmap*>(&tmap), *reinterpret_cast<const ddsim_lanes::Params*>(&p));
+  const ddsim_lanes::Tmap& tm = *reinterpret_cast<const ddsim_lanes::Tmap*>(&tmap);
+  const ddsim_lanes::Params& pp = *reinterpret_cast<const ddsim_lanes::Params*>(&p);
+  cudaError_t err;
+#define LAUNCH_L(DK, VV)                                                                   \
+  err = cudaFuncSetAttribute(maxplus_lanes_kernel<DK, VV>,                                 \
+                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
+  if (err != cudaSuccess) return err;                                                      \
+  maxplus_lanes_kernel<DK, VV><<<grid, BD, smem, stream>>>(tm, pp);
+  if (dkind == 1 && V == 2) {
+    LAUNCH_L(1, 2)
+  } else if (dkind == 1) {
+    LAUNCH_L(1, 1)
+  } else if (V == 2) {
+    LAUNCH_L(2, 2)
   } else {
-    cudaError_t err = cudaFuncSetAttribute(maxplus_lanes_kernel<2>,
-                                           cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-    if (err != cudaSuccess) return err;
-    maxplus_lanes_kernel<2><<<grid, BD, smem, stream>>>(*reinterpret_cast<const ddsim_lanes::Tmap*>(&tmap), *reinterpret_cast<const ddsim_lanes::Params*>(&p));
+    LAUNCH_L(2, 1)
   }
+#undef LAUNCH_L
   note_launch();
   return cudaGetLastError();
 }
