@@ -58,7 +58,7 @@ static size_t lanes_smem(int dk, int BD, int V, int ksm) {
 // 2 x #SMs; the TMA box (BD * V ints) stays <= 256.
 int maxplus_lanes_vec(int S) {
   const char* e = getenv("DDSIM_LANES_V");
-  int v = e ? atoi(e) : 1;
+  int v = e ? atoi(e) : 2;
   if (v != 1 && v != 2) v = 1;
   if (S % v) v = 1;
   return v;

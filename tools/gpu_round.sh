@@ -1,12 +1,9 @@
 #!/bin/bash
-# One GPU session: parity tests, bench, ncu launch list + full capture.
-set -x
+# One GPU session: parity tests, smoke, bench (both arms), ncu launch list + full capture.
 mkdir -p gpurun_out
-timeout 600 python -m pytest tests -m gpu -x -q > gpurun_out/tests.log 2>&1
-tail -3 gpurun_out/tests.log
-timeout 900 python bench.py > gpurun_out/bench.log 2>&1
-tail -1 gpurun_out/bench.log
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 20 --csv --log-file gpurun_out/launches.csv python bench.py --steps 2 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1
-tail -2 gpurun_out/ncu_launch.log
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:maxplus_dense -s 1 -c 1 -o gpurun_out/prof_dense python bench.py --scenarios 8192 --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1
-tail -2 gpurun_out/ncu_full.log
+timeout 900 python -m pytest tests -m gpu -q > gpurun_out/tests.log 2>&1; tail -2 gpurun_out/tests.log
+timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; tail -1 gpurun_out/smoke.log
+timeout 900 python bench.py > gpurun_out/bench.log 2>&1; tail -1 gpurun_out/bench.log | cut -c1-400
+timeout 600 python bench.py --impl reference > gpurun_out/bench_ref.log 2>&1; tail -1 gpurun_out/bench_ref.log | cut -c1-300
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -k regex:"lanes|maxplus|listsched" -c 12 --csv --log-file gpurun_out/launches.csv python bench.py --steps 4 --warmup 3 --no-e2e --no-cpu-baseline > gpurun_out/ncu_launch.log 2>&1; tail -1 gpurun_out/ncu_launch.log | cut -c1-200
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:lanes -s 1 -c 1 -o gpurun_out/prof_hot python bench.py --steps 1 --warmup 1 --no-e2e --no-cpu-baseline > gpurun_out/ncu_full.log 2>&1; tail -1 gpurun_out/ncu_full.log
