@@ -127,20 +127,16 @@ def cpu_baseline(w, fz, target_s: float = 12.0) -> dict:
     og = OracleGraph.from_graph(w.graph)
     base = og.dur
     rng = np.random.default_rng(1234)
-    S = threads * 2
+    S = threads * 16  # one batch: 16 scenarios per thread
     t_used = 0.0
     upd = 0
-    while True:
+    while t_used < target_s:
         k = rng.integers(900, 1101, size=(len(base), S))
         dense = np.ascontiguousarray(((2 * base[:, None] * k + 1000) // 2000).astype(np.int32))
         t0 = time.perf_counter()
         _ms, _st, u = og.simulate_batch(dense, threads, "default")
-        dt = time.perf_counter() - t0
-        t_used += dt
+        t_used += time.perf_counter() - t0
         upd += u
-        if t_used >= target_s or S >= 4096:
-            break
-        S = min(4096, max(S * 2, int(S * target_s / max(dt, 1e-3) * 0.5)))
     return {"value": upd / t_used, "unit": UNIT, "cores": threads, "kind": "port",
             "sample": f"{upd // len(base)} scenarios x {len(base)} tasks of the config-4 graph, "
                       f"{t_used:.1f} s wall, oracle/ddsim_oracle.c Alg.1 port (pthreads)"}
@@ -159,7 +155,7 @@ def run_reference(args):
     vals = []
     cb = None
     for i in range(args.warmup + args.steps):
-        cb = cpu_baseline(w, _F, target_s=3.0 if i < args.warmup else 6.0)
+        cb = cpu_baseline(w, _F, target_s=2.0 if i < args.warmup else 12.0 / max(args.steps, 1))
         if i >= args.warmup:
             vals.append(cb["value"])
     v = statistics.median(vals)
