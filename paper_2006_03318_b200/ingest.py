@@ -220,5 +220,29 @@ def map_layers_device(graph: DependencyGraph, markers: list[LayerMarker],
     return out
 
 
-__all__ = ["IngestResult", "ingest_arrays", "ingest_columns", "build_graph_device",
+def map_layers_arrays(cols: TraceColumns, launcher: np.ndarray, m_lane, m_start, m_end, m_tag,
+                      device: int | None = None) -> np.ndarray:
+    """Columnar layer mapping (config 5): tag id per event or -1."""
+    device = N.env_device() if device is None else device
+    N.require_device(device)
+    keep: list = []
+    tc = _trace_cols_struct(cols, False, keep)
+    mc = N.MarkerCols()
+    arrs = {"lane": N.c_i32(m_lane), "start": N.c_i64(m_start), "end": N.c_i64(m_end),
+            "tag": N.c_i32(m_tag)}
+    mc.n = len(arrs["lane"])
+    for k, a in arrs.items():
+        keep.append(a)
+        setattr(mc, k, N.ptr(a))
+    la = N.c_i32(launcher)
+    tag = np.full(cols.n, -1, np.int32)
+    bad = np.zeros(1, np.int64)
+    rc = N.lib().ks_map_layers(tc, la.ctypes.data, mc, device, tag.ctypes.data, bad.ctypes.data)
+    if rc == N.KS_ERR_AMBIGUOUS:
+        raise AmbiguousMarker(f"task {int(bad[0])} falls inside overlapping markers")
+    N.check(rc, "ks_map_layers")
+    return tag
+
+
+__all__ = ["map_layers_arrays","IngestResult", "ingest_arrays", "ingest_columns", "build_graph_device",
            "map_layers_device", "CPU_KINDS", "GPU_KINDS", "KIND_OF_CODE"]

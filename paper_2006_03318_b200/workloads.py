@@ -247,3 +247,86 @@ def jitter_matrix(base_rows: np.ndarray, S: int, seed: int = 0, out=None) -> np.
 
 def columns_of(trace: TraceDocument) -> TraceColumns:
     return TraceColumns.from_events(list(trace.events))
+
+
+def ingest_columns(n_records: int = 10_000_000, seed: int = 0, n_threads: int = 8,
+                   streams_per_thread: int = 2, with_markers: bool = True):
+    """Config 5: a columnar CUPTI-like trace of ~n_records events (no Python
+    objects per event).  Per CPU thread: launches (kernels), 2 % memcpy
+    launches (half ``memcpy_dtoh_async``), 0.5 % syncs (stream / device-wide),
+    1 % DataLoad; each launch's GPU task goes to one of the thread's streams,
+    starting at max(stream free, launch end) (prefix-max form).  Markers (one
+    per ~20 CPU tasks) are attached as ``cols.markers`` (lane, start, end, tag).
+    """
+    rng = np.random.default_rng(seed)
+    lanes: list[LaneId] = []
+    for t in range(n_threads):
+        lanes.append(LaneId.parse(f"cpu:{t}"))
+    for t in range(n_threads):
+        for k in range(streams_per_thread):
+            lanes.append(LaneId.parse(f"gpu:0:{t * streams_per_thread + k + 1}"))
+    per_thread = n_records // n_threads
+    ids, kinds, lane, start, dur, corr, st, dtoh = [], [], [], [], [], [], [], []
+    mk = {"lane": [], "start": [], "end": [], "tag": []}
+    next_id = 0
+    next_corr = 1
+    for t in range(n_threads):
+        # CPU events: c of them, g of which launch a GPU task (total ~ per_thread)
+        c = int(per_thread / 1.96)
+        r = rng.random(c)
+        is_sync = r < 0.005
+        is_load = (r >= 0.005) & (r < 0.015)
+        is_mcpy = (r >= 0.015) & (r < 0.035)
+        is_launch = ~(is_sync | is_load)
+        cd = rng.integers(3000, 9001, c).astype(np.int64)
+        cd[is_load] = rng.integers(20_000, 200_000, int(is_load.sum()))
+        cd[is_sync] = rng.integers(1_000, 50_000, int(is_sync.sum()))
+        cg = rng.integers(0, 4001, c).astype(np.int64)
+        cstart = np.concatenate([[0], np.cumsum(cd + cg)[:-1]])
+        ckind = np.full(c, 0, np.uint8)          # CpuApi
+        ckind[is_load] = 4                       # DataLoad
+        ckind[is_sync] = 6                       # Sync
+        cid = next_id + np.arange(c, dtype=np.int64)
+        next_id += c
+        ccorr = np.full(c, -1, np.int64)
+        nl = int(is_launch.sum())
+        ccorr[is_launch] = next_corr + np.arange(nl)
+        csync = np.full(c, -1, np.int32)
+        streams = n_threads + t * streams_per_thread + rng.integers(0, streams_per_thread, c)
+        dev_wide = is_sync & (rng.random(c) < 0.3)
+        csync[is_sync & ~dev_wide] = streams[is_sync & ~dev_wide].astype(np.int32)
+        cdtoh = (is_mcpy & (rng.random(c) < 0.5)).astype(np.uint8)
+        ids.append(cid); kinds.append(ckind); lane.append(np.full(c, t, np.int32))
+        start.append(cstart); dur.append(cd); corr.append(ccorr); st.append(csync); dtoh.append(cdtoh)
+        # GPU tasks of the launches
+        li = np.nonzero(is_launch)[0]
+        gl = streams[li].astype(np.int32)
+        gd = rng.integers(2_000, 120_000, nl).astype(np.int64)
+        gkind = np.where(is_mcpy[li], 3, 2).astype(np.uint8)
+        lend = cstart[li] + cd[li]
+        gstart = np.empty(nl, np.int64)
+        for s_ in np.unique(gl):
+            m = np.nonzero(gl == s_)[0]
+            D = np.concatenate([[0], np.cumsum(gd[m])[:-1]])
+            gstart[m] = np.maximum.accumulate(lend[m] - D) + D
+        gid = next_id + np.arange(nl, dtype=np.int64)
+        next_id += nl
+        ids.append(gid); kinds.append(gkind); lane.append(gl); start.append(gstart)
+        dur.append(gd); corr.append(next_corr + np.arange(nl)); st.append(np.full(nl, -1, np.int32))
+        dtoh.append(np.zeros(nl, np.uint8))
+        next_corr += nl
+        if with_markers:
+            # one marker per 20 consecutive CPU events, tags cycling over 400 layers x 3 phases
+            b = np.arange(0, c, 20)
+            e = np.minimum(b + 19, c - 1)
+            mk["lane"].append(np.full(b.size, t, np.int32))
+            mk["start"].append(cstart[b])
+            mk["end"].append(cstart[e] + cd[e])
+            mk["tag"].append((np.arange(b.size) % 1200).astype(np.int32))
+    cols = TraceColumns(id=np.concatenate(ids), kind=np.concatenate(kinds),
+                        lane=np.concatenate(lane), start=np.concatenate(start),
+                        duration=np.concatenate(dur), correlation=np.concatenate(corr),
+                        sync_target=np.concatenate(st), is_dtoh=np.concatenate(dtoh), lanes=lanes)
+    if with_markers:
+        cols.markers = {k: np.concatenate(v) for k, v in mk.items()}
+    return cols
