@@ -365,3 +365,179 @@ int64_t ora_simulate_batch(const ora_graph* g, const int32_t* dense, int64_t ld,
   free(indeg);
   return total;
 }
+
+/* ======================================================================
+ * Ingest restatement (TEST INFRASTRUCTURE): build_graph rules 1-5 + gaps
+ * (pkg/src/kernsim/graph.py:189-312) and map_tasks_to_layers
+ * (layers.py:30-81), written the straightforward way (sorts + scans).
+ * ==================================================================== */
+typedef struct {
+  int64_t n;
+  const int64_t *id, *start, *dur, *corr;
+  const uint8_t *kind, *is_dtoh;
+  const int32_t *lane, *sync_target;
+  int32_t n_lanes;
+  const uint8_t* lane_class; /* 0 cpu 1 gpu 2 comm */
+} ora_trace;
+
+static int is_cpu_k(int k) { return k == 0 || k == 1 || k == 4 || k == 6; }
+static int is_gpu_k(int k) { return k == 2 || k == 3; }
+
+static const ora_trace* g_sort_tr;
+static int cmp_lane_start_id(const void* a, const void* b) {
+  const int i = *(const int*)a, j = *(const int*)b;
+  const ora_trace* t = g_sort_tr;
+  if (t->lane[i] != t->lane[j]) return t->lane[i] < t->lane[j] ? -1 : 1;
+  if (t->start[i] != t->start[j]) return t->start[i] < t->start[j] ? -1 : 1;
+  if (t->id[i] != t->id[j]) return t->id[i] < t->id[j] ? -1 : 1;
+  return 0;
+}
+
+/* stream entries (lane, launch start, id) */
+typedef struct {
+  int32_t lane;
+  int64_t ls, id;
+  int32_t idx;
+} ora_entry;
+static int cmp_entry(const void* a, const void* b) {
+  const ora_entry *x = (const ora_entry*)a, *y = (const ora_entry*)b;
+  if (x->lane != y->lane) return x->lane < y->lane ? -1 : 1;
+  if (x->ls != y->ls) return x->ls < y->ls ? -1 : 1;
+  if (x->id != y->id) return x->id < y->id ? -1 : 1;
+  return 0;
+}
+typedef struct {
+  int64_t key;
+  int32_t idx;
+} ora_kv;
+static int cmp_kv(const void* a, const void* b) {
+  const ora_kv *x = (const ora_kv*)a, *y = (const ora_kv*)b;
+  if (x->key != y->key) return x->key < y->key ? -1 : 1;
+  return x->idx < y->idx ? -1 : (x->idx > y->idx);
+}
+
+/* Returns the number of edges written (src, dst, kind as event indices,
+ * kinds 0 LaneSeqCpu 1 LaneSeqGpu 2 LaunchCorrelation 3 SyncBlock 4 CommOrder);
+ * gap[n], launcher[n].  Edges may be written in any order. */
+int64_t ora_build_graph(const ora_trace* t, int32_t* esrc, int32_t* edst, uint8_t* ekind,
+                        int64_t* gap, int32_t* launcher) {
+  const int64_t n = t->n;
+  int64_t m = 0;
+  int32_t* perm = (int32_t*)malloc(sizeof(int32_t) * (size_t)(n > 0 ? n : 1));
+  for (int64_t i = 0; i < n; ++i) perm[i] = (int32_t)i;
+  g_sort_tr = t;
+  qsort(perm, (size_t)n, sizeof(int32_t), cmp_lane_start_id);
+  for (int64_t i = 0; i < n; ++i) gap[i] = 0;
+  for (int64_t k = 0; k + 1 < n; ++k) {
+    const int a = perm[k], b = perm[k + 1];
+    if (t->lane[a] != t->lane[b]) continue;
+    const int cls = t->lane_class[t->lane[a]];
+    esrc[m] = a; edst[m] = b; ekind[m] = cls == 0 ? 0 : (cls == 1 ? 1 : 4); ++m;
+    if (cls == 0) {
+      const int64_t d = t->start[b] - (t->start[a] + t->dur[a]);
+      gap[a] = d > 0 ? d : 0;
+    }
+  }
+  /* rule 3: last CPU-kind event per correlation (document order) */
+  ora_kv* cpu = (ora_kv*)malloc(sizeof(ora_kv) * (size_t)(n > 0 ? n : 1));
+  ora_kv* gpu = (ora_kv*)malloc(sizeof(ora_kv) * (size_t)(n > 0 ? n : 1));
+  int64_t nc = 0, ng = 0;
+  for (int64_t i = 0; i < n; ++i) {
+    if (t->corr[i] < 0) continue;
+    if (is_cpu_k(t->kind[i])) { cpu[nc].key = t->corr[i]; cpu[nc].idx = (int32_t)i; ++nc; }
+    if (is_gpu_k(t->kind[i])) { gpu[ng].key = t->corr[i]; gpu[ng].idx = (int32_t)i; ++ng; }
+  }
+  qsort(cpu, (size_t)nc, sizeof(ora_kv), cmp_kv);
+  qsort(gpu, (size_t)ng, sizeof(ora_kv), cmp_kv);
+  for (int64_t i = 0; i < n; ++i) {
+    launcher[i] = -1;
+    if (!is_gpu_k(t->kind[i]) || t->corr[i] < 0) continue;
+    int64_t lo = 0, hi = nc; /* upper_bound(corr) - 1 */
+    while (lo < hi) { int64_t mid = (lo + hi) / 2; if (cpu[mid].key <= t->corr[i]) lo = mid + 1; else hi = mid; }
+    if (lo > 0 && cpu[lo - 1].key == t->corr[i]) {
+      launcher[i] = cpu[lo - 1].idx;
+      esrc[m] = launcher[i]; edst[m] = (int32_t)i; ekind[m] = 2; ++m;
+    }
+  }
+  /* rule 4 */
+  ora_entry* ent = (ora_entry*)malloc(sizeof(ora_entry) * (size_t)(n > 0 ? n : 1));
+  int64_t ne = 0;
+  for (int64_t i = 0; i < n; ++i)
+    if (is_gpu_k(t->kind[i]) && launcher[i] >= 0) {
+      ent[ne].lane = t->lane[i]; ent[ne].ls = t->start[launcher[i]]; ent[ne].id = t->id[i];
+      ent[ne].idx = (int32_t)i; ++ne;
+    }
+  qsort(ent, (size_t)ne, sizeof(ora_entry), cmp_entry);
+  int64_t* seg_b = (int64_t*)calloc((size_t)t->n_lanes + 1, sizeof(int64_t));
+  int64_t* seg_e = (int64_t*)calloc((size_t)t->n_lanes + 1, sizeof(int64_t));
+  for (int64_t k = 0; k < ne; ++k) {
+    if (k == 0 || ent[k - 1].lane != ent[k].lane) seg_b[ent[k].lane] = k;
+    seg_e[ent[k].lane] = k + 1;
+  }
+  char* has_ev = (char*)calloc((size_t)t->n_lanes + 1, 1);
+  for (int64_t i = 0; i < n; ++i) has_ev[t->lane[i]] = 1;
+  for (int64_t e = 0; e < n; ++e) {
+    const int k = t->kind[e];
+    int targets[1024];
+    int nt = 0;
+    int64_t exclude = -1;
+    if (k == 6) {
+      if (t->sync_target[e] >= 0) targets[nt++] = t->sync_target[e];
+      else
+        for (int l = 0; l < t->n_lanes && nt < 1024; ++l)
+          if (t->lane_class[l] == 1 && has_ev[l]) targets[nt++] = l;
+    } else if (is_cpu_k(k) && t->is_dtoh[e] && t->corr[e] >= 0) {
+      int64_t lo = 0, hi = ng; /* lower_bound: first GPU event with the correlation */
+      while (lo < hi) { int64_t mid = (lo + hi) / 2; if (gpu[mid].key < t->corr[e]) lo = mid + 1; else hi = mid; }
+      if (lo >= ng || gpu[lo].key != t->corr[e]) continue;
+      targets[nt++] = t->lane[gpu[lo].idx];
+      exclude = gpu[lo].idx;
+    } else {
+      continue;
+    }
+    for (int q = 0; q < nt; ++q) {
+      const int l = targets[q];
+      /* newest entry with launch start < e.start, skipping `exclude` (graph.py:269-276) */
+      int32_t best = -1;
+      for (int64_t p = seg_b[l]; p < seg_e[l]; ++p) {
+        if (ent[p].ls >= t->start[e]) break;
+        if (ent[p].idx != exclude) best = ent[p].idx;
+      }
+      if (best >= 0) { esrc[m] = best; edst[m] = (int32_t)e; ekind[m] = 3; ++m; }
+    }
+  }
+  free(perm); free(cpu); free(gpu); free(ent); free(seg_b); free(seg_e); free(has_ev);
+  return m;
+}
+
+/* map_tasks_to_layers: CPU-kind events by innermost containing marker on the
+ * same lane ((length, tag, list order) minimum; ambiguity if the best two are
+ * not nested), GPU-kind events inherit their launcher's tag.  Returns -1 or
+ * the index of the first ambiguous event.  Markers are scanned per task from
+ * a per-lane list (O(N * markers per lane) -- test sizes only). */
+int64_t ora_map_layers(const ora_trace* t, const int32_t* launcher, int64_t M, const int32_t* mlane,
+                       const int64_t* mstart, const int64_t* mend, const int32_t* mtag, int32_t* tag_out) {
+  int64_t bad = -1;
+  for (int64_t i = 0; i < t->n; ++i) {
+    tag_out[i] = -1;
+    if (!is_cpu_k(t->kind[i]) || t->lane[i] < 0) continue;
+    const int64_t s = t->start[i], e = t->start[i] + t->dur[i];
+    int64_t a = -1, b = -1;
+    for (int64_t j = 0; j < M; ++j) {
+      if (mlane[j] != t->lane[i] || mstart[j] > s || mend[j] < e) continue;
+      const int64_t len = mend[j] - mstart[j];
+      if (a < 0 || len < mend[a] - mstart[a] || (len == mend[a] - mstart[a] && (mtag[j] < mtag[a]))) {
+        b = a; a = j;
+      } else if (b < 0 || len < mend[b] - mstart[b] || (len == mend[b] - mstart[b] && mtag[j] < mtag[b])) {
+        b = j;
+      }
+    }
+    if (a < 0) continue;
+    if (b >= 0 && !(mstart[b] <= mstart[a] && mend[a] <= mend[b]) && bad < 0) bad = i;
+    tag_out[i] = mtag[a];
+  }
+  for (int64_t i = 0; i < t->n; ++i)
+    if (is_gpu_k(t->kind[i]) && launcher[i] >= 0 && tag_out[launcher[i]] >= 0)
+      tag_out[i] = tag_out[launcher[i]];
+  return bad;
+}

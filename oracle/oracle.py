@@ -181,3 +181,60 @@ class OracleGraph:
 
 def scale(d: int, num: int, den: int) -> int:
     return int(lib().ora_scale(d, num, den))
+
+
+class _OraTrace(C.Structure):
+    _fields_ = [("n", C.c_int64), ("id", C.c_void_p), ("start", C.c_void_p), ("dur", C.c_void_p),
+                ("corr", C.c_void_p), ("kind", C.c_void_p), ("is_dtoh", C.c_void_p),
+                ("lane", C.c_void_p), ("sync_target", C.c_void_p), ("n_lanes", C.c_int32),
+                ("lane_class", C.c_void_p)]
+
+
+def _trace_struct(cols):
+    keep = {
+        "id": np.ascontiguousarray(cols.id, np.int64), "start": np.ascontiguousarray(cols.start, np.int64),
+        "dur": np.ascontiguousarray(cols.duration, np.int64),
+        "corr": np.ascontiguousarray(cols.correlation, np.int64),
+        "kind": np.ascontiguousarray(cols.kind, np.uint8),
+        "is_dtoh": np.ascontiguousarray(cols.is_dtoh, np.uint8),
+        "lane": np.ascontiguousarray(cols.lane, np.int32),
+        "sync_target": np.ascontiguousarray(cols.sync_target, np.int32),
+        "lane_class": np.ascontiguousarray(cols.lane_class_codes(), np.uint8),
+    }
+    t = _OraTrace()
+    t.n = int(cols.n)
+    t.n_lanes = len(cols.lanes)
+    for k, a in keep.items():
+        setattr(t, k, a.ctypes.data if a.size else None)
+    return t, keep
+
+
+def build_graph_columns(cols):
+    """-> (edge set {(src_idx, dst_idx, kind_code)}, gap[n], launcher[n])."""
+    h = lib()
+    h.ora_build_graph.argtypes = [C.POINTER(_OraTrace)] + [C.c_void_p] * 5
+    h.ora_build_graph.restype = C.c_int64
+    t, keep = _trace_struct(cols)
+    n = max(int(cols.n), 1)
+    cap = 3 * n + int(np.sum(cols.kind == 6)) * (len(cols.lanes) + 1) + 16
+    s, d, k = np.empty(cap, np.int32), np.empty(cap, np.int32), np.empty(cap, np.uint8)
+    gap, launcher = np.empty(n, np.int64), np.empty(n, np.int32)
+    m = h.ora_build_graph(C.byref(t), s.ctypes.data, d.ctypes.data, k.ctypes.data,
+                          gap.ctypes.data, launcher.ctypes.data)
+    del keep
+    return set(zip(s[:m].tolist(), d[:m].tolist(), k[:m].tolist())), gap[:cols.n], launcher[:cols.n]
+
+
+def map_layers_columns(cols, launcher, m_lane, m_start, m_end, m_tag):
+    h = lib()
+    h.ora_map_layers.argtypes = [C.POINTER(_OraTrace), C.c_void_p, C.c_int64] + [C.c_void_p] * 5
+    h.ora_map_layers.restype = C.c_int64
+    t, keep = _trace_struct(cols)
+    arrs = [np.ascontiguousarray(m_lane, np.int32), np.ascontiguousarray(m_start, np.int64),
+            np.ascontiguousarray(m_end, np.int64), np.ascontiguousarray(m_tag, np.int32)]
+    la = np.ascontiguousarray(launcher, np.int32)
+    out = np.full(max(int(cols.n), 1), -1, np.int32)
+    bad = h.ora_map_layers(C.byref(t), la.ctypes.data, len(arrs[0]),
+                           *[a.ctypes.data if a.size else None for a in arrs], out.ctypes.data)
+    del keep
+    return out[:cols.n], int(bad)

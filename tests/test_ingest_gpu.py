@@ -154,3 +154,25 @@ def test_apply_pipeline_graphs_match_reference(golden):
         out = apply_pipeline(base, TransformPipeline.from_object(rec["pipeline"]))
         want = graph_from_obj(rec["graph"])
         assert out.to_object() == want.to_object(), (rec["case"], rec["scenario"])
+
+
+@pytest.mark.parametrize("n", [120_000])
+def test_columnar_ingest_matches_oracle_at_scale(n):
+    """Config-5 generator (8 CPU threads x 16 streams, memcpys incl. blocking
+    dtoh, stream + device-wide syncs, data loads): device ingest + layer
+    mapping vs the C oracle's restatement of the reference rules."""
+    from oracle import build_graph_columns, map_layers_columns
+    from paper_2006_03318_b200.ingest import map_layers_arrays
+    cols = W.ingest_columns(n, seed=3)
+    res = ingest_arrays(cols, check_overlaps=True)
+    edges, gap, launcher = build_graph_columns(cols)
+    got = set(zip(res.edge_src.tolist(), res.edge_dst.tolist(), res.edge_kind.tolist()))
+    assert len(got) == len(res.edge_src)           # no duplicate triples
+    assert got == edges
+    assert np.array_equal(res.gap, gap)
+    assert np.array_equal(res.launcher, launcher)
+    m = cols.markers
+    tags = map_layers_arrays(cols, res.launcher, m["lane"], m["start"], m["end"], m["tag"])
+    want, bad = map_layers_columns(cols, launcher, m["lane"], m["start"], m["end"], m["tag"])
+    assert bad == -1
+    assert np.array_equal(tags, want)

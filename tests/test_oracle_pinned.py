@@ -92,3 +92,42 @@ def test_distributed_fixture_values(golden, bw, expect):
             assert w["report"]["predicted_makespan_ns"] == expect
             return
     raise AssertionError("fixture missing")
+
+
+EDGE_CODES = {"LaneSeqCpu": 0, "LaneSeqGpu": 1, "LaunchCorrelation": 2, "SyncBlock": 3,
+              "CommOrder": 4}
+
+
+def test_oracle_ingest_matches_reference_graphs(golden):
+    """ora_build_graph / ora_map_layers reproduce the reference's build_graph
+    + map_tasks_to_layers on every golden trace."""
+    import json as _json
+    from oracle import build_graph_columns, map_layers_columns
+    from paper_2006_03318_b200.trace import TraceColumns, parse_trace
+    for case in golden["cases"]:
+        doc = parse_trace(_json.dumps(case["doc"]))
+        cols = TraceColumns.from_events(list(doc.events))
+        edges, gap, launcher = build_graph_columns(cols)
+        ids = cols.id.tolist()
+        got = {(ids[u], ids[v], k) for u, v, k in edges}
+        want = {(u, v, EDGE_CODES[k]) for u, v, k in case["graph"]["edges"]}
+        assert got == want, case["name"]
+        gaps = {t["id"]: t["gap_ns"] for t in case["graph"]["tasks"]}
+        assert dict(zip(ids, gap.tolist())) == gaps, case["name"]
+        # layers: markers in list order, tags ranked by (layer, phase)
+        markers = list(doc.layer_markers)
+        tags = sorted({(m.layer, m.phase.value) for m in markers})
+        tid = {t: i for i, t in enumerate(tags)}
+        lane_ix = {ln: i for i, ln in enumerate(cols.lanes)}
+        ml = [lane_ix.get(m.cpu_lane, -2) for m in markers]
+        tag, bad = map_layers_columns(cols, launcher, ml, [m.start for m in markers],
+                                      [m.end for m in markers],
+                                      [tid[(m.layer, m.phase.value)] for m in markers])
+        assert bad == -1
+        lay = {t["id"]: (t["layer"], t["phase"]) for t in case["graph"]["tasks"]}
+        for i, x in enumerate(ids):
+            exp = lay[x]
+            got_t = None if tag[i] < 0 else tags[tag[i]]
+            if got_t is not None and got_t[0] == "*":
+                got_t = ("_global", got_t[1])
+            assert (got_t if got_t else (None, None)) == exp, (case["name"], x)
