@@ -201,6 +201,10 @@ cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const void* tmap128, i
                                      const std::vector<int>& codes, int grid, int BD, size_t smem,
                                      cudaStream_t stream);
 int maxplus_lanes_vec(int S);
+cudaError_t launch_expand_durations(const long long* base, const unsigned* group,
+                                    const int* ovr_map, const long long* ovr, const int* scale_ptr,
+                                    const ScaleStepDev* scale, int rows, int S, long long ld,
+                                    long long* out, cudaStream_t st);
 const char* jit_log();
 int maxplus_lanes_block_dim(int S, int num_sms);
 cudaError_t launch_listsched(const ListParams& p, cudaStream_t stream);

@@ -916,7 +916,28 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
   const bool dense = sc->dense_kind != 0 && sc->dense != nullptr;
   build_tables(g, sc, T, true, policy == KS_POLICY_VDNN);
 
-  const bool lanes_ok = use_max && dense && g->has_lanes && sc->n_overrides == 0 &&
+  // Derived durations on a lanes-eligible graph: expand them into a dense
+  // int64 matrix (one thread per element; L2-resident at the sizes where the
+  // derived path is used) and run the lanes kernel on it.
+  ks_scenarios_desc expanded;
+  const bool expand = use_max && !dense && g->has_lanes && g->n_rec > 0 &&
+                      (long long)g->n * S * 8 <= (8LL << 30) && getenv("DDSIM_NO_EXPAND") == nullptr &&
+                      getenv("DDSIM_NO_LANES") == nullptr;
+  if (expand) {
+    long long* buf = T.scratch<long long>((size_t)g->n * S);
+    CUDA_TRY(launch_expand_durations(g->d_dur, g->d_group, T.ovr_map, T.ovr, T.scale_ptr, T.scale,
+                                     g->n, S, S, buf, stream));
+    expanded = *sc;
+    expanded.dense_kind = 2;
+    expanded.dense = buf;
+    expanded.dense_ld = S;
+    expanded.n_overrides = 0;
+    expanded.scale_ptr = nullptr;
+    expanded.scale = nullptr;
+    sc = &expanded;
+  }
+  const bool dense_now = sc->dense_kind != 0 && sc->dense != nullptr;
+  const bool lanes_ok = use_max && dense_now && g->has_lanes && sc->n_overrides == 0 &&
                         !sc->scale_ptr && getenv("DDSIM_NO_LANES") == nullptr;
   if (lanes_ok) {
     LaneParams p;
@@ -972,7 +993,7 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
     if (q.kglob > 0) q.gslots = T.scratch<long long>((size_t)q.kglob * q.s_pad);
     CUDA_TRY(launch_maxplus(q, dk == 1 ? reinterpret_cast<const int*>(sc->dense) : nullptr, stream));
     if (out->dispatched) CUDA_TRY(launch_fill_i32(out->dispatched, g->n, S, stream));
-  } else if (use_max && dense && g->has_dense && sc->n_overrides == 0 && !sc->scale_ptr) {
+  } else if (use_max && dense_now && g->has_dense && sc->n_overrides == 0 && !sc->scale_ptr) {
     DenseParams p;
     memset(&p, 0, sizeof(p));
     p.prog = g->d_dprog;
@@ -1064,7 +1085,7 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
     p.S = S;
     p.L = g->L;
     int dmode = 0;
-    if (dense) {
+    if (dense_now) {
       if (g->n_chains > 0) fail(KS_ERR_UNSUPPORTED, "dense durations with permutable chains");
       if (sc->dense_ld < S) fail(KS_ERR_INVALID, "dense_ld < n_scenarios");
       if (sc->dense_kind == 1) {
@@ -1093,7 +1114,7 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
     const int BD = maxplus_block_dim(S, dmode, nsm);
     p.s_pad = (long long)((S + BD - 1) / BD) * BD;
     if (p.kglob > 0) p.gslots = T.scratch<long long>((size_t)p.kglob * p.s_pad);
-    CUDA_TRY(launch_maxplus(p, dense && dmode == 1 ? reinterpret_cast<const int*>(sc->dense) : nullptr,
+    CUDA_TRY(launch_maxplus(p, dense_now && dmode == 1 ? reinterpret_cast<const int*>(sc->dense) : nullptr,
                             stream));
     if (out->dispatched) CUDA_TRY(launch_fill_i32(out->dispatched, g->n, S, stream));
   } else {
@@ -1116,7 +1137,7 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
     p.vrank = T.vrank;
     p.policy = policy;
     p.zero_time = 0;
-    if (dense) {
+    if (dense_now) {
       if (sc->dense_kind == 1)
         p.dense32 = reinterpret_cast<const int*>(sc->dense);
       else

@@ -350,3 +350,44 @@ cudaError_t launch_fill_i32(int* p, int v, long long n, cudaStream_t s) {
 }
 
 }  // namespace ddsim
+
+namespace ddsim {
+
+// Derived durations -> dense int64 [rows][ld]: d = base[r], the scenario's
+// override if the row has one, then its scale steps in order (sequential
+// half-up, transform.py:174-183).  One thread per (row, scenario) element.
+__global__ void expand_durations_kernel(const long long* base, const unsigned* group,
+                                        const int* ovr_map, const long long* ovr,
+                                        const int* scale_ptr, const ScaleStepDev* scale, int rows,
+                                        int S, long long ld, long long* out) {
+  const long long total = (long long)rows * S;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int r = (int)(i / S), s = (int)(i % S);
+    long long d = base[r];
+    if (ovr_map && ovr_map[r] >= 0) d = ovr[(long long)ovr_map[r] * S + s];
+    const unsigned g = group ? group[r] : 0u;
+    if (g != 0u && scale_ptr) {
+      for (int e = scale_ptr[s]; e < scale_ptr[s + 1]; ++e) {
+        const ScaleStepDev st = scale[e];
+        if (g >= (unsigned)st.lo && g <= (unsigned)st.hi) d = scale_half_up(d, st.num, st.den);
+      }
+    }
+    out[(long long)r * ld + s] = d;
+  }
+}
+
+cudaError_t launch_expand_durations(const long long* base, const unsigned* group,
+                                    const int* ovr_map, const long long* ovr, const int* scale_ptr,
+                                    const ScaleStepDev* scale, int rows, int S, long long ld,
+                                    long long* out, cudaStream_t st) {
+  const long long total = (long long)rows * S;
+  if (total == 0) return cudaSuccess;
+  const int grid = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
+  expand_durations_kernel<<<grid, 256, 0, st>>>(base, group, ovr_map, ovr, scale_ptr, scale, rows,
+                                                S, ld, out);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace ddsim

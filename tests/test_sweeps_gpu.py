@@ -21,7 +21,10 @@ def _small_training(seed=3, buckets_mb=6.0):
                             sync_every=60, seed=seed, buckets_mb=buckets_mb)
 
 
-def test_per_layer_shrink_sweep_vs_oracle():
+@pytest.mark.parametrize("mode", ["expand+lanes", "general"])
+def test_per_layer_shrink_sweep_vs_oracle(mode, monkeypatch):
+    if mode == "general":
+        monkeypatch.setenv("DDSIM_NO_EXPAND", "1")
     w = _small_training()
     g = w.graph
     scen = [[(And([GPU_TASKS, ByLayer(l)]), "1/2")] for l in w.layers] + [[]]
