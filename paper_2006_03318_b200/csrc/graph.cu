@@ -924,20 +924,24 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
                       (long long)g->n * S * 8 <= (8LL << 30) && getenv("DDSIM_NO_EXPAND") == nullptr &&
                       getenv("DDSIM_NO_LANES") == nullptr;
   if (expand) {
-    long long* buf = T.scratch<long long>((size_t)g->n * S);
+    const long long eld = (S + 1) / 2 * 2;  // TMA: 16 B row pitch
+    long long* buf = T.scratch<long long>((size_t)g->n * eld);
     CUDA_TRY(launch_expand_durations(g->d_dur, g->d_group, T.ovr_map, T.ovr, T.scale_ptr, T.scale,
-                                     g->n, S, S, buf, stream));
+                                     g->n, S, eld, buf, stream));
     expanded = *sc;
     expanded.dense_kind = 2;
     expanded.dense = buf;
-    expanded.dense_ld = S;
+    expanded.dense_ld = eld;
     expanded.n_overrides = 0;
     expanded.scale_ptr = nullptr;
     expanded.scale = nullptr;
     sc = &expanded;
   }
   const bool dense_now = sc->dense_kind != 0 && sc->dense != nullptr;
-  const bool lanes_ok = use_max && dense_now && g->has_lanes && sc->n_overrides == 0 &&
+  const bool tma_ok =
+      dense_now && reinterpret_cast<uintptr_t>(sc->dense) % 16 == 0 &&
+      (sc->dense_kind == 1 ? sc->dense_ld % 4 == 0 : sc->dense_ld % 2 == 0);
+  const bool lanes_ok = use_max && dense_now && tma_ok && g->has_lanes && sc->n_overrides == 0 &&
                         !sc->scale_ptr && getenv("DDSIM_NO_LANES") == nullptr;
   if (lanes_ok) {
     LaneParams p;

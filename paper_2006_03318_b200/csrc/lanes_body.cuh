@@ -184,7 +184,8 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p) {
   asm volatile("" : "+r"(sbase));  // keep in a register (no per-record rematerialisation)
   const unsigned prog_s = sbase + 128;
   const unsigned tile_s = prog_s + kStagesL * kChunkL * (unsigned)sizeof(Rec);
-  const unsigned tile_all = DK == 1 ? (unsigned)(kStagesL * kChunkL * W * 4) : 0u;
+  constexpr unsigned ES = DK == 1 ? 4u : 8u;  // tile element bytes (int32 / int64 durations)
+  const unsigned tile_all = (unsigned)(kStagesL * kChunkL * W) * ES;
   const unsigned slot_s = tile_s + tile_all;                  // [ksm][BD] x (8 V) B
   const unsigned col = (unsigned)(tid * 8 * V);
   const unsigned slot_pitch = (unsigned)(BD * 8 * V);
@@ -193,14 +194,15 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p) {
   const int s = s0 + tid * V;
   const bool act = s < p.S;  // S % V == 0 (host)
   const int nchunks = (p.n_rec + kChunkL - 1) / kChunkL;
-  const unsigned tile_bytes = DK == 1 ? (unsigned)(kChunkL * W * 4) : 0u;
+  const unsigned tile_bytes = (unsigned)(kChunkL * W) * ES;
   auto issue = [&](int c) {
     const int st = c % kStagesL;
     const int nrec = min(kChunkL, p.n_rec - c * kChunkL);
     const unsigned pb = (unsigned)(nrec * sizeof(Rec));
     l_expect(&bars[st], pb + tile_bytes);
     l_bulk(pst + st * kChunkL, p.prog + (long long)c * kChunkL, pb, &bars[st]);
-    if (DK == 1) l_tile(tst + st * kChunkL * W, tmap, s0, c * kChunkL, &bars[st]);
+    l_tile(reinterpret_cast<unsigned char*>(tst) + (size_t)st * kChunkL * W * ES, tmap, s0,
+           c * kChunkL, &bars[st]);
   };
   if (tid == 0) {
     for (int i = 0; i < kStagesL; ++i) l_mbar_init(&bars[i]);
@@ -225,46 +227,50 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p) {
   const long long ld = p.start_ld;
   const bool store = act && p.start != nullptr;
   long long* sp = store ? p.start + s : nullptr;
-  const long long* dp = DK == 2 ? p.dense64 + (act ? s : 0) : nullptr;
-  const unsigned row_pitch = (unsigned)(W * 4);
+  const unsigned row_pitch = (unsigned)W * ES;
   const int ksm = p.ksm;
 
   for (int c = 0; c < nchunks; ++c) {
     const int st = c % kStagesL;
     l_wait(&bars[st], (unsigned)((c / kStagesL) & 1));
     const unsigned rec0 = prog_s + (unsigned)(st * kChunkL * sizeof(Rec));
-    const unsigned t0 = tile_s + (unsigned)(st * kChunkL) * row_pitch + (unsigned)(tid * 4 * V);
+    const unsigned t0 = tile_s + (unsigned)(st * kChunkL) * row_pitch + (unsigned)tid * ES * V;
     const int nrec = min(kChunkL, p.n_rec - c * kChunkL);
     int4 raw = l_lds128(rec0);
-    int2 dd = make_int2(0, 0);
-    if (DK == 1) {
-      if (V == 2)
-        dd = l_lds64i(t0);
-      else
-        asm volatile("ld.shared.s32 %0, [%1];" : "=r"(dd.x) : "r"(t0));
-    }
+    long long dx, dy;  // durations of the next record (prefetched)
+    auto load_d = [&](unsigned ta) {
+      if (DK == 1) {
+        if (V == 2) {
+          const int2 t2 = l_lds64i(ta);
+          dx = (unsigned)t2.x;
+          dy = (unsigned)t2.y;
+          neg |= t2.x | t2.y;
+        } else {
+          int t1;
+          asm volatile("ld.shared.s32 %0, [%1];" : "=r"(t1) : "r"(ta));
+          dx = (unsigned)t1;
+          dy = 0;
+          neg |= t1;
+        }
+      } else {
+        if (V == 2) {
+          const longlong2 t2 = l_lds128ll(ta);
+          dx = t2.x;
+          dy = t2.y;
+        } else {
+          asm volatile("ld.shared.s64 %0, [%1];" : "=l"(dx) : "r"(ta));
+          dy = 0;
+        }
+        neg |= (int)((dx | dy) >> 32);
+      }
+    };
+    load_d(t0);
     auto record = [&](int j) {
       const int4 r = raw;
-      long long d0, d1 = 0;
-      if (DK == 1) {
-        d0 = (unsigned)dd.x;
-        if (V == 2) d1 = (unsigned)dd.y;
-        neg |= dd.x | dd.y;
-      } else {
-        d0 = dp[0];
-        if (V == 2) d1 = dp[1];
-        neg |= (int)((d0 | d1) >> 32);
-        dp += p.dense_ld;
-      }
+      const long long d0 = dx, d1 = dy;
       if (j + 1 < nrec) {  // prefetch the next record and durations
         raw = l_lds128(rec0 + (unsigned)(j + 1) * 16u);
-        if (DK == 1) {
-          const unsigned ta = t0 + (unsigned)(j + 1) * row_pitch;
-          if (V == 2)
-            dd = l_lds64i(ta);
-          else
-            asm volatile("ld.shared.s32 %0, [%1];" : "=r"(dd.x) : "r"(ta));
-        }
+        load_d(t0 + (unsigned)(j + 1) * row_pitch);
       }
       const long long gap = ((long long)(unsigned)r.y << 32) | (unsigned)r.x;
       const unsigned w = (unsigned)r.w;

@@ -49,7 +49,7 @@ __global__ void __launch_bounds__(256) maxplus_lanes_kernel(const __grid_constan
 
 static size_t lanes_smem(int dk, int BD, int V, int ksm) {
   size_t b = 128 + (size_t)ddsim_lanes::kStagesL * ddsim_lanes::kChunkL * sizeof(ddsim_lanes::Rec);
-  if (dk == 1) b += (size_t)ddsim_lanes::kStagesL * ddsim_lanes::kChunkL * BD * V * 4;
+  b += (size_t)ddsim_lanes::kStagesL * ddsim_lanes::kChunkL * BD * V * (dk == 1 ? 4 : 8);
   return b + (size_t)ksm * BD * 8 * V;
 }
 
@@ -58,7 +58,9 @@ static size_t lanes_smem(int dk, int BD, int V, int ksm) {
 // 2 x #SMs; the TMA box (BD * V ints) stays <= 256.
 int maxplus_lanes_vec(int S) {
   const char* e = getenv("DDSIM_LANES_V");
-  int v = e ? atoi(e) : 2;
+  // two scenarios per thread only when there are enough scenarios to keep
+  // ~4 warps per SM busy with V = 2; small sweeps want more threads instead
+  int v = e ? atoi(e) : (S >= 2 * 148 * 64 ? 2 : 1);
   if (v != 1 && v != 2) v = 1;
   if (S % v) v = 1;
   return v;
@@ -85,20 +87,24 @@ cudaError_t launch_maxplus_lanes(const LaneParams& p, const int* dense32, int dk
   const size_t smem = lanes_smem(dkind, BD, V, p.ksm);
   CUtensorMap tmap;
   memset(&tmap, 0, sizeof(tmap));
-  if (dkind == 1) {
+  {
     cudaDriverEntryPointQueryResult q;
     void* fn = nullptr;
     if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
             cudaSuccess || q != cudaDriverEntryPointSuccess)
       return cudaErrorNotSupported;
     auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    const size_t es = dkind == 1 ? 4 : 8;
+    const void* base = dkind == 1 ? static_cast<const void*>(dense32)
+                                  : static_cast<const void*>(p.dense64);
     cuuint64_t dims[2] = {(cuuint64_t)p.S, (cuuint64_t)p.n_rec};
-    cuuint64_t strides[1] = {(cuuint64_t)(p.dense_ld * sizeof(int))};
+    cuuint64_t strides[1] = {(cuuint64_t)(p.dense_ld * es)};
     cuuint32_t box[2] = {(cuuint32_t)W, (cuuint32_t)ddsim_lanes::kChunkL};
     cuuint32_t estr[2] = {1, 1};
-    if (enc(&tmap, CU_TENSOR_MAP_DATA_TYPE_INT32, 2, const_cast<int*>(dense32), dims, strides, box,
-            estr, CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    if (enc(&tmap, dkind == 1 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_INT64, 2,
+            const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
       return cudaErrorInvalidValue;
   }
   // per-graph specialised dispatch first (NVRTC); the static kernel otherwise
