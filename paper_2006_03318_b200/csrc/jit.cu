@@ -10,6 +10,8 @@
 // if either is unavailable the static kernel runs instead (same results).
 #include <dlfcn.h>
 
+#include <cstdio>
+
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -103,7 +105,18 @@ std::string make_source(const std::vector<int>& codes, int dk, int V) {
   disp += "else __trap();\n";
   std::string src = "#define DDSIM_LANES_NO_STD_TYPES 1\n";
   if (const char* u = getenv("DDSIM_JIT_UNROLL")) src += std::string("#define DDSIM_UNROLL ") + u + "\n";
-  src += disp + kLanesBodySrc;
+  std::string body = kLanesBodySrc;
+  if (const char* alt = getenv("DDSIM_LANES_BODY")) {  // experiments: alternative body file
+    if (FILE* f = fopen(alt, "rb")) {
+      std::string b;
+      char buf[4096];
+      size_t k;
+      while ((k = fread(buf, 1, sizeof buf, f)) > 0) b.append(buf, k);
+      fclose(f);
+      body = b;
+    }
+  }
+  src += disp + body;
   src += "\nextern \"C\" __global__ void __launch_bounds__(256) ddsim_lanes_jit("
          "const __grid_constant__ ddsim_lanes::Tmap tmap, const ddsim_lanes::Params p) {\n"
          "  ddsim_lanes::lanes_body<" + std::to_string(dk) + ", " + std::to_string(V) +
@@ -114,6 +127,7 @@ std::string make_source(const std::vector<int>& codes, int dk, int V) {
 CUfunction get_function(const std::vector<int>& codes, int dk, int V, int device) {
   std::string key = std::to_string(device) + ":" + std::to_string(dk) + ":" + std::to_string(V) + ":";
   if (const char* u = getenv("DDSIM_JIT_UNROLL")) key += std::string("u") + u + ":";
+  if (const char* b = getenv("DDSIM_LANES_BODY")) key += std::string("b") + b + ":";
   for (int c : codes) key += std::to_string(c) + ",";
   std::lock_guard<std::mutex> lk(g_mu);
   init_locked();

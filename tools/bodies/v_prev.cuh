@@ -1,0 +1,363 @@
+// Device body of the maxplus_lanes kernel, shared by the statically compiled
+// kernel (maxplus_lanes.cu, 256-way switch dispatch) and the per-graph
+// NVRTC-specialised kernel (jit.cu, if-chain over the handler codes the graph
+// uses, in frequency order).  Self-contained: NVRTC compiles it without any
+// host header.  See maxplus_lanes.cu for the algorithm.
+#pragma once
+
+#ifndef DDSIM_LANES_NO_STD_TYPES
+#include <climits>
+#endif
+
+namespace ddsim_lanes {
+
+// 16-byte program record.  h = own lane (2 bits) | predecessor-lane mask
+// (5 bits; bit 4 = temp lane holding the rare predecessors) << 2 | gap!=0 << 7.
+struct alignas(16) Rec {
+  long long gap;
+  short s0, s1;   // smem slots of rare predecessors (R_S0 / R_S1)
+  short out;      // slot receiving rel (R_OUT_SMEM: smem id, R_OUT_GLOBAL: global id)
+  unsigned char rare;
+  unsigned char h;
+};
+enum {
+  R_S0 = 1, R_S1 = 2, R_SIDE = 4, R_MS = 8, R_OUT_SMEM = 16, R_OUT_GLOBAL = 32,
+  R_PRE = 7, R_POST = 56
+};
+
+struct Params {
+  const Rec* prog;
+  int n_rec;
+  const int* side_off;
+  const int* side_slots;  // < ksm: smem slot, else global slot + ksm
+  const long long* side_ready;
+  int ksm, kglob;
+  long long* gslots;
+  long long s_pad;
+  int S, L;
+  const long long* dense64;
+  long long dense_ld;
+  long long* start;
+  long long start_ld;
+  long long* makespan;
+  long long* lane_busy;
+  int* neg_flag;
+};
+
+// CUtensorMap-compatible opaque kernel parameter (128 B, 64 B aligned)
+struct alignas(64) Tmap {
+  unsigned long long w[16];
+};
+
+constexpr int kChunkL = 16;
+constexpr int kStagesL = 4;
+constexpr int NLANE = 4;  // register lanes; index 4 = temp (rare predecessors)
+
+__device__ __forceinline__ unsigned su32l(const void* p) {
+  return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void l_mbar_init(unsigned long long* bar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(su32l(bar)) : "memory");
+}
+__device__ __forceinline__ void l_expect(unsigned long long* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su32l(bar)),
+               "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void l_wait(unsigned long long* bar, unsigned parity) {
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra W_%=;\n}\n" ::"r"(su32l(bar)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ void l_bulk(void* dst, const void* src, unsigned bytes,
+                                       unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+      ::"r"(su32l(dst)), "l"(src), "r"(bytes), "r"(su32l(bar)) : "memory");
+}
+__device__ __forceinline__ void l_tile(void* dst, const Tmap* map, int x, int y,
+                                       unsigned long long* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+      " [%0], [%1, {%2, %3}], [%4];" ::"r"(su32l(dst)), "l"(map), "r"(x), "r"(y), "r"(su32l(bar))
+      : "memory");
+}
+__device__ __forceinline__ long long lmax(long long a, long long b) { return a > b ? a : b; }
+
+template <int V>
+struct St {
+  long long lv[NLANE + 1][V];  // lane heads' rel (+ temp), V scenarios
+  long long lb[NLANE][V];      // lane busy
+};
+
+template <int OWN, int MASK, int GAP, int V>
+__device__ __forceinline__ void hstep(St<V>& S, long long d0, long long d1, long long gap,
+                                      long long*& sp, long long ld, bool store) {
+  long long a = S.lv[OWN][0], b = S.lv[OWN][V - 1];
+#pragma unroll
+  for (int m = 0; m <= NLANE; ++m)
+    if (((MASK >> m) & 1) && m != OWN) {
+      a = lmax(a, S.lv[m][0]);
+      if (V == 2) b = lmax(b, S.lv[m][V - 1]);
+    }
+  if (store) {
+    __stcs(sp, a);
+    if (V == 2) __stcs(sp + 1, b);
+    sp += ld;
+  }
+  a += d0;
+  if (V == 2) b += d1;
+  if (GAP) {
+    a += gap;
+    if (V == 2) b += gap;
+  }
+  S.lv[OWN][0] = a;
+  S.lb[OWN][0] += d0;
+  if (V == 2) {
+    S.lv[OWN][V - 1] = b;
+    S.lb[OWN][V - 1] += d1;
+  }
+}
+
+template <int V>
+__device__ __forceinline__ long long own_get(const St<V>& S, int own, int i) {
+  switch (own) {
+    case 0: return S.lv[0][i];
+    case 1: return S.lv[1][i];
+    case 2: return S.lv[2][i];
+    default: return S.lv[3][i];
+  }
+}
+
+__device__ __forceinline__ int4 l_lds128(unsigned a) {
+  int4 v;
+  asm volatile("ld.shared.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ int2 l_lds64i(unsigned a) {
+  int2 v;
+  asm volatile("ld.shared.v2.s32 {%0,%1}, [%2];" : "=r"(v.x), "=r"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ longlong2 l_lds128ll(unsigned a) {
+  longlong2 v;
+  asm volatile("ld.shared.v2.s64 {%0,%1}, [%2];" : "=l"(v.x), "=l"(v.y) : "r"(a));
+  return v;
+}
+__device__ __forceinline__ void l_sts128ll(unsigned a, long long x, long long y) {
+  asm volatile("st.shared.v2.s64 [%0], {%1,%2};" ::"r"(a), "l"(x), "l"(y) : "memory");
+}
+
+// Load / store the V values of one slot column.
+template <int V>
+__device__ __forceinline__ void slot_ld(unsigned a, long long& x0, long long& x1) {
+  if (V == 2) {
+    const longlong2 v = l_lds128ll(a);
+    x0 = v.x;
+    x1 = v.y;
+  } else {
+    asm volatile("ld.shared.s64 %0, [%1];" : "=l"(x0) : "r"(a));
+    x1 = x0;
+  }
+}
+template <int V>
+__device__ __forceinline__ void slot_st(unsigned a, long long x0, long long x1) {
+  if (V == 2)
+    l_sts128ll(a, x0, x1);
+  else
+    asm volatile("st.shared.s64 [%0], %1;" ::"r"(a), "l"(x0) : "memory");
+}
+
+// The kernel body; DDSIM_DISPATCH(h) must expand to the handler dispatch
+// (it sees S, d0, d1, gap, sp, ld, store and the template parameter V).
+// Each thread owns V consecutive scenarios (V = 1 or 2).
+template <int DK, int V>
+__device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int BD = blockDim.x;
+  const int W = BD * V;  // scenarios per CTA
+  const int tid = threadIdx.x;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem);
+  Rec* pst = reinterpret_cast<Rec*>(smem + 128);
+  unsigned sbase = su32l(smem);
+  asm volatile("" : "+r"(sbase));  // keep in a register (no per-record rematerialisation)
+  const unsigned prog_s = sbase + 128;
+  const unsigned tile_s = prog_s + kStagesL * kChunkL * (unsigned)sizeof(Rec);
+  const unsigned tile_all = DK == 1 ? (unsigned)(kStagesL * kChunkL * W * 4) : 0u;
+  const unsigned slot_s = tile_s + tile_all;                  // [ksm][BD] x (8 V) B
+  const unsigned col = (unsigned)(tid * 8 * V);
+  const unsigned slot_pitch = (unsigned)(BD * 8 * V);
+  int* tst = reinterpret_cast<int*>(smem + (tile_s - sbase));
+  const int s0 = blockIdx.x * W;
+  const int s = s0 + tid * V;
+  const bool act = s < p.S;  // S % V == 0 (host)
+  const int nchunks = (p.n_rec + kChunkL - 1) / kChunkL;
+  const unsigned tile_bytes = DK == 1 ? (unsigned)(kChunkL * W * 4) : 0u;
+  auto issue = [&](int c) {
+    const int st = c % kStagesL;
+    const int nrec = min(kChunkL, p.n_rec - c * kChunkL);
+    const unsigned pb = (unsigned)(nrec * sizeof(Rec));
+    l_expect(&bars[st], pb + tile_bytes);
+    l_bulk(pst + st * kChunkL, p.prog + (long long)c * kChunkL, pb, &bars[st]);
+    if (DK == 1) l_tile(tst + st * kChunkL * W, tmap, s0, c * kChunkL, &bars[st]);
+  };
+  if (tid == 0) {
+    for (int i = 0; i < kStagesL; ++i) l_mbar_init(&bars[i]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int c = 0; c < min(kStagesL, nchunks); ++c) issue(c);
+
+  St<V> S;
+#pragma unroll
+  for (int l = 0; l <= NLANE; ++l)
+#pragma unroll
+    for (int i = 0; i < V; ++i) S.lv[l][i] = 0;
+#pragma unroll
+  for (int l = 0; l < NLANE; ++l)
+#pragma unroll
+    for (int i = 0; i < V; ++i) S.lb[l][i] = 0;
+  long long ms0 = 0, ms1 = 0;
+  int neg = 0;
+  const long long ld = p.start_ld;
+  const bool store = act && p.start != nullptr;
+  long long* sp = store ? p.start + s : nullptr;
+  const long long* dp = DK == 2 ? p.dense64 + (act ? s : 0) : nullptr;
+  const unsigned row_pitch = (unsigned)(W * 4);
+  const int ksm = p.ksm;
+
+  for (int c = 0; c < nchunks; ++c) {
+    const int st = c % kStagesL;
+    l_wait(&bars[st], (unsigned)((c / kStagesL) & 1));
+    const unsigned rec0 = prog_s + (unsigned)(st * kChunkL * sizeof(Rec));
+    const unsigned t0 = tile_s + (unsigned)(st * kChunkL) * row_pitch + (unsigned)(tid * 4 * V);
+    const int nrec = min(kChunkL, p.n_rec - c * kChunkL);
+    int4 raw = l_lds128(rec0);
+    int2 dd = make_int2(0, 0);
+    if (DK == 1) {
+      if (V == 2)
+        dd = l_lds64i(t0);
+      else
+        asm volatile("ld.shared.s32 %0, [%1];" : "=r"(dd.x) : "r"(t0));
+    }
+    auto record = [&](int j) {
+      const int4 r = raw;
+      long long d0, d1 = 0;
+      if (DK == 1) {
+        d0 = (unsigned)dd.x;
+        if (V == 2) d1 = (unsigned)dd.y;
+        neg |= dd.x | dd.y;
+      } else {
+        d0 = dp[0];
+        if (V == 2) d1 = dp[1];
+        neg |= (int)((d0 | d1) >> 32);
+        dp += p.dense_ld;
+      }
+      if (j + 1 < nrec) {  // prefetch the next record and durations
+        raw = l_lds128(rec0 + (unsigned)(j + 1) * 16u);
+        if (DK == 1) {
+          const unsigned ta = t0 + (unsigned)(j + 1) * row_pitch;
+          if (V == 2)
+            dd = l_lds64i(ta);
+          else
+            asm volatile("ld.shared.s32 %0, [%1];" : "=r"(dd.x) : "r"(ta));
+        }
+      }
+      const long long gap = ((long long)(unsigned)r.y << 32) | (unsigned)r.x;
+      const unsigned w = (unsigned)r.w;
+      const unsigned h = w >> 24;
+      const unsigned rare = (w >> 16) & 0xffu;
+      if (rare & R_PRE) {
+        // predecessors that are no longer lane heads (+ ready floor) -> temp lane
+        long long x0 = 0, x1 = 0, y0, y1;
+        const int row = c * kChunkL + j;
+        if (rare & R_S0) {
+          slot_ld<V>(slot_s + (unsigned)((r.z << 16) >> 16) * slot_pitch + col, y0, y1);
+          x0 = lmax(x0, y0);
+          x1 = lmax(x1, y1);
+        }
+        if (rare & R_S1) {
+          slot_ld<V>(slot_s + (unsigned)(r.z >> 16) * slot_pitch + col, y0, y1);
+          x0 = lmax(x0, y0);
+          x1 = lmax(x1, y1);
+        }
+        if (rare & R_SIDE) {
+          if (p.side_ready) {
+            x0 = lmax(x0, p.side_ready[row]);
+            x1 = lmax(x1, p.side_ready[row]);
+          }
+          if (p.side_off)
+            for (int k = p.side_off[row]; k < p.side_off[row + 1]; ++k) {
+              const int code = p.side_slots[k];
+              if (code < ksm) {
+                slot_ld<V>(slot_s + (unsigned)code * slot_pitch + col, y0, y1);
+                x0 = lmax(x0, y0);
+                x1 = lmax(x1, y1);
+              } else if (act) {
+                const long long* g = p.gslots + (long long)(code - ksm) * p.s_pad + s;
+                x0 = lmax(x0, g[0]);
+                x1 = lmax(x1, g[V - 1]);
+              }
+            }
+        }
+        S.lv[NLANE][0] = x0;
+        S.lv[NLANE][V - 1] = V == 2 ? x1 : x0;
+      }
+      DDSIM_DISPATCH(h)
+      if (rare & R_POST) {
+        const int own = (int)(h & 3);
+        const long long r0 = own_get<V>(S, own, 0), r1 = own_get<V>(S, own, V - 1);
+        if (rare & R_MS) {
+          const long long g2 = (h >> 7) & 1 ? gap : 0;
+          ms0 = lmax(ms0, r0 - g2);
+          ms1 = lmax(ms1, r1 - g2);
+        }
+        if (rare & R_OUT_SMEM) {
+          slot_st<V>(slot_s + (unsigned)((w << 16) >> 16) * slot_pitch + col, r0, r1);
+        } else if ((rare & R_OUT_GLOBAL) && act) {
+          long long* g = p.gslots + (long long)((int)(w << 16) >> 16) * p.s_pad + s;
+          g[0] = r0;
+          if (V == 2) g[1] = r1;
+        }
+      }
+    };
+#ifdef DDSIM_UNROLL
+    if (nrec == kChunkL) {
+#pragma unroll DDSIM_UNROLL
+      for (int j = 0; j < kChunkL; ++j) record(j);
+    } else {
+#pragma unroll 1
+      for (int j = 0; j < nrec; ++j) record(j);
+    }
+#else
+#pragma unroll 1
+    for (int j = 0; j < nrec; ++j) record(j);
+#endif
+    __syncthreads();
+    if (tid == 0 && c + kStagesL < nchunks) issue(c + kStagesL);
+  }
+  if (act) {
+    if (neg < 0 && p.neg_flag) atomicOr(p.neg_flag, 1);
+    if (p.makespan) {
+      p.makespan[s] = ms0;
+      if (V == 2) p.makespan[s + 1] = ms1;
+    }
+    if (p.lane_busy)
+      for (int l = 0; l < p.L; ++l) {
+        long long v0 = 0, v1 = 0;
+#pragma unroll
+        for (int q = 0; q < NLANE; ++q)
+          if (q == l) {
+            v0 = S.lb[q][0];
+            v1 = S.lb[q][V - 1];
+          }
+        p.lane_busy[(long long)s * p.L + l] = v0;
+        if (V == 2) p.lane_busy[(long long)(s + 1) * p.L + l] = v1;
+      }
+  }
+}
+
+}  // namespace ddsim_lanes
