@@ -184,8 +184,7 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p) {
   asm volatile("" : "+r"(sbase));  // keep in a register (no per-record rematerialisation)
   const unsigned prog_s = sbase + 128;
   const unsigned tile_s = prog_s + kStagesL * kChunkL * (unsigned)sizeof(Rec);
-  constexpr unsigned ES = DK == 1 ? 4u : 8u;  // tile element bytes (int32 / int64 durations)
-  const unsigned tile_all = (unsigned)(kStagesL * kChunkL * W) * ES;
+  const unsigned tile_all = DK == 1 ? (unsigned)(kStagesL * kChunkL * W * 4) : 0u;
   const unsigned slot_s = tile_s + tile_all;                  // [ksm][BD] x (8 V) B
   const unsigned col = (unsigned)(tid * 8 * V);
   const unsigned slot_pitch = (unsigned)(BD * 8 * V);
@@ -194,15 +193,14 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p) {
   const int s = s0 + tid * V;
   const bool act = s < p.S;  // S % V == 0 (host)
   const int nchunks = (p.n_rec + kChunkL - 1) / kChunkL;
-  const unsigned tile_bytes = (unsigned)(kChunkL * W) * ES;
+  const unsigned tile_bytes = DK == 1 ? (unsigned)(kChunkL * W * 4) : 0u;
   auto issue = [&](int c) {
     const int st = c % kStagesL;
     const int nrec = min(kChunkL, p.n_rec - c * kChunkL);
     const unsigned pb = (unsigned)(nrec * sizeof(Rec));
     l_expect(&bars[st], pb + tile_bytes);
     l_bulk(pst + st * kChunkL, p.prog + (long long)c * kChunkL, pb, &bars[st]);
-    l_tile(reinterpret_cast<unsigned char*>(tst) + (size_t)st * kChunkL * W * ES, tmap, s0,
-           c * kChunkL, &bars[st]);
+    if (DK == 1) l_tile(tst + st * kChunkL * W, tmap, s0, c * kChunkL, &bars[st]);
   };
   if (tid == 0) {
     for (int i = 0; i < kStagesL; ++i) l_mbar_init(&bars[i]);
@@ -227,33 +225,24 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p) {
   const long long ld = p.start_ld;
   const bool store = act && p.start != nullptr;
   long long* sp = store ? p.start + s : nullptr;
-  const unsigned row_pitch = (unsigned)W * ES;
+  const long long* dp = DK == 2 ? p.dense64 + (act ? s : 0) : nullptr;
+  const unsigned row_pitch = (unsigned)(W * 4);
   const int ksm = p.ksm;
 
   for (int c = 0; c < nchunks; ++c) {
     const int st = c % kStagesL;
     l_wait(&bars[st], (unsigned)((c / kStagesL) & 1));
     const unsigned rec0 = prog_s + (unsigned)(st * kChunkL * sizeof(Rec));
-    const unsigned t0 = tile_s + (unsigned)(st * kChunkL) * row_pitch + (unsigned)tid * ES * V;
+    const unsigned t0 = tile_s + (unsigned)(st * kChunkL) * row_pitch + (unsigned)(tid * 4 * V);
     const int nrec = min(kChunkL, p.n_rec - c * kChunkL);
     int4 raw = l_lds128(rec0);
-    // prefetched durations of the next record: int32 pair (DK 1) / int64 pair (DK 2)
     int2 dd = make_int2(0, 0);
-    longlong2 dq = make_longlong2(0, 0);
-    auto load_d = [&](unsigned ta) {
-      if (DK == 1) {
-        if (V == 2)
-          dd = l_lds64i(ta);
-        else
-          asm volatile("ld.shared.s32 %0, [%1];" : "=r"(dd.x) : "r"(ta));
-      } else {
-        if (V == 2)
-          dq = l_lds128ll(ta);
-        else
-          asm volatile("ld.shared.s64 %0, [%1];" : "=l"(dq.x) : "r"(ta));
-      }
-    };
-    load_d(t0);
+    if (DK == 1) {
+      if (V == 2)
+        dd = l_lds64i(t0);
+      else
+        asm volatile("ld.shared.s32 %0, [%1];" : "=r"(dd.x) : "r"(t0));
+    }
     auto record = [&](int j) {
       const int4 r = raw;
       long long d0, d1 = 0;
@@ -262,13 +251,20 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p) {
         if (V == 2) d1 = (unsigned)dd.y;
         neg |= dd.x | dd.y;
       } else {
-        d0 = dq.x;
-        if (V == 2) d1 = dq.y;
+        d0 = dp[0];
+        if (V == 2) d1 = dp[1];
         neg |= (int)((d0 | d1) >> 32);
+        dp += p.dense_ld;
       }
       if (j + 1 < nrec) {  // prefetch the next record and durations
         raw = l_lds128(rec0 + (unsigned)(j + 1) * 16u);
-        load_d(t0 + (unsigned)(j + 1) * row_pitch);
+        if (DK == 1) {
+          const unsigned ta = t0 + (unsigned)(j + 1) * row_pitch;
+          if (V == 2)
+            dd = l_lds64i(ta);
+          else
+            asm volatile("ld.shared.s32 %0, [%1];" : "=r"(dd.x) : "r"(ta));
+        }
       }
       const long long gap = ((long long)(unsigned)r.y << 32) | (unsigned)r.x;
       const unsigned w = (unsigned)r.w;
