@@ -123,7 +123,13 @@ int ks_graph_destroy(ks_graph* g);
 
 /* One scale step of a scenario: tasks whose group id lies in [group_lo,
  * group_hi] get d <- round_half_up(d * num / den) (transform.py:174-183).
- * Steps of one scenario apply in order (sequential rounding). */
+ * Steps of one scenario apply in order (sequential rounding).
+ * num == den == 0 (KS_STEP_REMOVE) removes the matched tasks instead
+ * (remove_task, transform.py:249-265: parents x children spliced, the removed
+ * task's gap discarded); their start reads -1.  Removal is exact on the
+ * max-plus path only (lane-chained graphs); list scheduling rejects it with
+ * KS_ERR_UNSUPPORTED. */
+#define KS_STEP_REMOVE 0
 typedef struct {
   int32_t group_lo;
   int32_t group_hi;

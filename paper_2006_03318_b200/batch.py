@@ -7,7 +7,9 @@ pkg/src/kernsim/cli.py:185-193).  A scenario is a row of a table:
 * dense durations   dur[r][s] for every frozen row r (Monte-Carlo jitter),
 * overrides         per-scenario durations of a few tasks (set_duration),
 * scale programs    sequential half-up Shrink steps on task groups
-                    (scale_durations, transform.py:174-183),
+                    (scale_durations, transform.py:174-183); a step whose
+                    factor is ``REMOVE`` removes the group's tasks instead
+                    (remove_task, transform.py:249-265),
 * chains            per-scenario order / presence of inserted tasks on one
                     lane (sequenced insert_task, transform.py:204-246).
 
@@ -33,6 +35,8 @@ from .graph import DependencyGraph, EdgeKind, Task
 from .trace import GradientBucketMap, TaskKind
 from .transform import Selector
 
+REMOVE = "remove"  # a compile_scale_sweep factor: remove the selected tasks
+
 POLICY_IDS = {"default": N.KS_POLICY_DEFAULT, "priority": N.KS_POLICY_PRIORITY,
               "vdnn_prefetch": N.KS_POLICY_VDNN}
 
@@ -52,9 +56,13 @@ class BatchResult:
         return dict(zip(ids[keep].tolist(), col[keep].tolist()))
 
     def lane_busy_of(self, s: int, present_lanes=None) -> dict:
+        """lane_busy dict of scenario s keyed like sim.py:124 (lanes that still
+        hold a task: absent chains and removed tasks drop out)."""
         fz = self.frozen
         used = np.zeros(fz.L, bool)
-        if present_lanes is None:
+        if present_lanes is None and self.start is not None:
+            used[fz.lane[fz.order][self.start[:, s] >= 0]] = True
+        elif present_lanes is None:
             used[fz.lane] = True
         else:
             used[list(present_lanes)] = True
@@ -198,6 +206,10 @@ def compile_scale_sweep(graph: DependencyGraph, scenarios: list[list[tuple[Selec
     steps_out = []
     for steps in scenarios:
         for sel, factor in steps:
+            if isinstance(factor, str) and factor == REMOVE:
+                for gid in sorted(groups_with[sels[repr(sel.to_object())][0]]):
+                    steps_out.append((gid, gid, 0, 0))  # KS_STEP_REMOVE
+                continue
             f = Fraction(str(factor)) if not isinstance(factor, Fraction) else factor
             if f <= 0:
                 raise BadPipeline(f"scale factor must be positive, got {f}")

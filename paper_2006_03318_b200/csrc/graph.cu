@@ -813,6 +813,7 @@ struct ScenTables {
   short* perm = nullptr;
   unsigned char* present = nullptr;
   int* vrank = nullptr;
+  bool has_remove = false;  // a scale step removes tasks (KS_STEP_REMOVE)
   cudaStream_t st = nullptr;
   template <class T>
   T* up(const T* host, size_t count) {
@@ -844,9 +845,14 @@ void build_tables(const ks_graph* g, const ks_scenarios_desc* sc, ScenTables& T,
   if (sc->scale_ptr && sc->scale) {
     const int nsteps = sc->scale_ptr[S] - sc->scale_ptr[0];
     if (sc->scale_ptr[0] != 0) fail(KS_ERR_INVALID, "scale_ptr[0] must be 0");
-    for (int k = 0; k < nsteps; ++k)
+    for (int k = 0; k < nsteps; ++k) {
+      if (sc->scale[k].num == 0 && sc->scale[k].den == 0) {  // KS_STEP_REMOVE
+        T.has_remove = true;
+        continue;
+      }
       if (sc->scale[k].num <= 0 || sc->scale[k].den <= 0)
         fail(KS_ERR_BAD_PIPELINE, "scale factor must be positive");
+    }
     T.scale_ptr = T.up(sc->scale_ptr, (size_t)S + 1);
     // ks_scale_step and ScaleStepDev share layout (int,int,ll,ll)
     static_assert(sizeof(ks_scale_step) == sizeof(ScaleStepDev), "layout");
@@ -915,12 +921,17 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
   T.st = stream;
   const bool dense = sc->dense_kind != 0 && sc->dense != nullptr;
   build_tables(g, sc, T, true, policy == KS_POLICY_VDNN);
+  if (dense && (sc->scale_ptr || sc->n_overrides > 0))
+    fail(KS_ERR_INVALID, "dense durations exclude overrides and scale steps");
+  if (T.has_remove && !use_max)
+    fail(KS_ERR_UNSUPPORTED,
+         "removal steps need the max-plus path (lane-chained graph); apply remove_task structurally");
 
   // Derived durations on a lanes-eligible graph: expand them into a dense
   // int64 matrix (one thread per element; L2-resident at the sizes where the
   // derived path is used) and run the lanes kernel on it.
   ks_scenarios_desc expanded;
-  const bool expand = use_max && !dense && g->has_lanes && g->n_rec > 0 &&
+  const bool expand = use_max && !dense && !T.has_remove && g->has_lanes && g->n_rec > 0 &&
                       (long long)g->n * S * 8 <= (8LL << 30) && getenv("DDSIM_NO_EXPAND") == nullptr &&
                       getenv("DDSIM_NO_LANES") == nullptr;
   if (expand) {

@@ -103,22 +103,32 @@ __device__ __forceinline__ void slot_put(const MaxplusParams& p, const ThreadCtx
     p.gslots[(long long)(k - p.ksm) * p.s_pad + t.s] = v;
 }
 
+// A step with num == 0 (KS_STEP_REMOVE) removes the matched tasks
+// (remove_task, transform.py:249-265): *removed is set and d is meaningless.
 __device__ __forceinline__ long long derive_duration(const MaxplusParams& p, const ThreadCtx& t,
-                                                     long long dur, int ovr_row, unsigned group) {
+                                                     long long dur, int ovr_row, unsigned group,
+                                                     bool& removed) {
   long long d = dur;
+  removed = false;
   if (ovr_row >= 0) d = p.ovr[(long long)ovr_row * p.S + t.sc];
   if (group != 0u) {
     for (int e = t.e0; e < t.e1; ++e) {
       const ScaleStepDev st = p.scale[e];
-      if (group >= (unsigned)st.lo && group <= (unsigned)st.hi) d = scale_half_up(d, st.num, st.den);
+      if (group >= (unsigned)st.lo && group <= (unsigned)st.hi) {
+        if (st.num == 0)
+          removed = true;
+        else
+          d = scale_half_up(d, st.num, st.den);
+      }
     }
   }
   return d;
 }
 
+// max over the predecessors' values (no ready time; LLONG_MIN if none)
 __device__ __forceinline__ long long pred_max(const MaxplusParams& p, const ThreadCtx& t,
                                               const NodeRec& r) {
-  long long st = r.ready;
+  long long st = LLONG_MIN;
   if (r.pred0 >= 0) st = max(st, slot_get(p, t, r.pred0));
   if (r.pred1 >= 0) st = max(st, slot_get(p, t, r.pred1));
   for (int k = 0; k < r.nextra; ++k) st = max(st, slot_get(p, t, __ldg(&p.extra[r.extra_off + k])));
@@ -136,8 +146,16 @@ __device__ __forceinline__ void run_chain(const MaxplusParams& p, ThreadCtx& t, 
     for (int k = 0; k < ch.B; ++k) {
       const int m = p.perm ? (int)p.perm[(long long)t.sc * p.perm_ld + ch.perm_off + k] : k;
       const NodeRec mr = p.members[ch.member_off + m];
-      long long st = max(pred_max(p, t, mr), prev);
-      const long long d = derive_duration(p, t, mr.dur, mr.ovr_row, mr.group);
+      const long long pm = max(pred_max(p, t, mr), prev);
+      bool rm;
+      const long long d = derive_duration(p, t, mr.dur, mr.ovr_row, mr.group, rm);
+      if (rm) {  // spliced out: its parents feed its children and lane successor
+        if (t.act && p.start) __stcs(&p.start[(long long)mr.row * p.start_ld + t.s], -1ll);
+        prev = pm;
+        if (mr.out_slot >= 0) slot_put(p, t, mr.out_slot, prev);
+        continue;
+      }
+      const long long st = max(pm, mr.ready);
       if (t.act && p.start) __stcs(&p.start[(long long)mr.row * p.start_ld + t.s], st);
       const long long fin = st + d;
       prev = fin + mr.gap;
@@ -220,15 +238,22 @@ __global__ void __launch_bounds__(256) maxplus_kernel(const __grid_constant__ CU
         continue;
       }
       const NodeRec r = R[j];
-      const long long stv = pred_max(p, t, r);
+      const long long pm = pred_max(p, t, r);
       long long d;
       if (DMODE == 1) {
         d = (long long)T[j * BD + t.tid];
       } else if (DMODE == 2) {
         d = p.dense64[(long long)r.row * p.dense_ld + t.sc];
       } else {
-        d = derive_duration(p, t, r.dur, r.ovr_row, r.group);
+        bool rm;
+        d = derive_duration(p, t, r.dur, r.ovr_row, r.group, rm);
+        if (rm) {  // removed (remove_task): start -1, value passes through
+          if (t.act && p.start) __stcs(&p.start[(long long)r.row * p.start_ld + t.s], -1ll);
+          if (r.out_slot >= 0) slot_put(p, t, r.out_slot, pm);
+          continue;
+        }
       }
+      const long long stv = max(pm, r.ready);
       if (t.act && p.start) __stcs(&p.start[(long long)r.row * p.start_ld + t.s], stv);
       const long long fin = stv + d;
       if (r.out_slot >= 0) slot_put(p, t, r.out_slot, fin + r.gap);

@@ -76,3 +76,90 @@ def test_distributed_sweep_reorders_change_makespan():
     sw = distributed_sweep(w.graph, buckets, [cfg, cfg], perms)
     res = simulate_batch(sw.frozen, sw.table)
     assert res.makespan[0] > 0 and res.makespan[1] > 0
+
+
+def test_removal_steps_vs_remove_task():
+    """KS_STEP_REMOVE scenarios (batched remove_task, transform.py:249-265)
+    against the oracle on graphs where remove_task was applied structurally:
+    layer removals, kind removals, a whole lane removed, removal mixed with
+    Shrink."""
+    from paper_2006_03318_b200.batch import REMOVE
+    from paper_2006_03318_b200.trace import TaskKind
+    from paper_2006_03318_b200.transform import ByKind, ByLane, LaneClass, Not
+    w = _small_training(seed=11)
+    g = w.graph
+    mem = ByKind(TaskKind.GPU_MEMCPY)
+    scen = [[], [(ByLayer(w.layers[3]), REMOVE)], [(And([GPU_TASKS, ByLayer(w.layers[7])]), REMOVE)],
+            [(mem, REMOVE)], [(ByLane(LaneClass.GPU_STREAM), REMOVE)],
+            [(GPU_TASKS, "1/2"), (ByLayer(w.layers[1]), REMOVE), (GPU_TASKS, "3/2")],
+            [(ByKind(TaskKind.SYNC), REMOVE), (ByLayer(w.layers[2]), "0.25")],
+            [(And([ByLayer(w.layers[5]), Not(GPU_TASKS)]), REMOVE)]]
+    group_of, ptr, steps = compile_scale_sweep(g, scen)
+    fz = FrozenGraph.from_graph(g, group_of=group_of)
+    res = simulate_batch(fz, ScenarioTable(n_scenarios=len(scen), scale_ptr=ptr, scale=steps))
+    for s, sc in enumerate(scen):
+        pipe = [{"op": "remove", "selector": sel.to_object()} if f == REMOVE else
+                {"op": "scale", "selector": sel.to_object(), "factor": f} for sel, f in sc]
+        h = apply_pipeline(g, TransformPipeline(steps=pipe))
+        st, ms, lb, _ = OracleGraph.from_graph(h).simulate("default")
+        assert res.makespan[s] == ms, s
+        assert res.start_of(s) == st, s
+        assert {str(k): v for k, v in res.lane_busy_of(s).items()} == {str(k): v for k, v in lb.items()}, s
+
+
+def test_removal_inside_permutable_chain():
+    """Removing chain members (inserted allReduces) per scenario: equals the
+    reference's sequenced inserts in perm order followed by remove_task."""
+    from paper_2006_03318_b200.batch import REMOVE  # noqa: F401  (num=den=0 steps)
+    from paper_2006_03318_b200 import _native as N
+    from paper_2006_03318_b200.comm import COLLECTIVE_LANE, earliest_weight_update_task
+    from paper_2006_03318_b200.comm import last_backward_gpu_task
+    from paper_2006_03318_b200.frozen import ChainSpec
+    from paper_2006_03318_b200.graph import EdgeKind, Task
+    from paper_2006_03318_b200.trace import TaskKind
+    from paper_2006_03318_b200.transform import remove_task
+    w = _small_training(seed=5)
+    g = w.graph.copy()
+    wu = earliest_weight_update_task(g)
+    head_order = list(g.lane_order.get(COLLECTIVE_LANE, []))
+    nid = g.next_id()
+    members = []
+    for k, layer in enumerate(w.layers[:5]):
+        tid = nid + k
+        g.tasks[tid] = Task(id=tid, kind=TaskKind.COMM, name=f"ar{k}", lane=COLLECTIVE_LANE,
+                            duration=1000 * (k + 1), gap=7 * k)
+        g.edges.add((last_backward_gpu_task(w.graph, layer).id, tid, EdgeKind.INJECTED))
+        g.edges.add((tid, wu.id, EdgeKind.INJECTED))
+        members.append(tid)
+    group_of = np.zeros(len(g.tasks), np.uint32)
+    ids = list(g.tasks)
+    for k, tid in enumerate(members):
+        group_of[ids.index(tid)] = k + 1
+    fz = FrozenGraph.from_graph(g, group_of=group_of, chains=[ChainSpec(members=members, head=head_order[-1] if head_order else None)])
+    rng = np.random.default_rng(1)
+    S = 12
+    perms = np.array([rng.permutation(5) for _ in range(S)], np.int16)
+    removed = [sorted(rng.choice(5, size=rng.integers(0, 4), replace=False).tolist())
+               for _ in range(S)]
+    removed[0], removed[1] = [], [0, 1, 2, 3, 4]
+    ptr, steps = [0], []
+    for rm in removed:
+        steps += [(k + 1, k + 1, 0, 0) for k in rm]
+        ptr.append(len(steps))
+    arr = np.zeros(max(len(steps), 1), N.SCALE_STEP_DTYPE)
+    for i, st in enumerate(steps):
+        arr[i] = st
+    res = simulate_batch(fz, ScenarioTable(n_scenarios=S, scale_ptr=np.array(ptr, np.int32),
+                                           scale=arr[:len(steps)], chain_perm=perms))
+    for s in range(S):
+        h = g.copy()
+        order = head_order + [members[k] for k in perms[s]]
+        h.lane_order[COLLECTIVE_LANE] = list(order)
+        for a, b in zip(order, order[1:]):
+            h.edges.add((a, b, EdgeKind.COMM_ORDER))
+        for k in removed[s]:
+            remove_task(h, members[k])
+        st, ms, lb, _ = OracleGraph.from_graph(h).simulate("default")
+        assert res.makespan[s] == ms, s
+        assert res.start_of(s) == st, s
+        assert {str(k): v for k, v in res.lane_busy_of(s).items()} == {str(k): v for k, v in lb.items()}, s
