@@ -251,8 +251,8 @@ def run_ours(args):
         h_dense = torch.empty((rows, S_e), dtype=torch.int32, pin_memory=True)
         h_dense.copy_(dense[:, :S_e])
         h_start = torch.empty((rows, S_e), dtype=torch.int64, pin_memory=True)
-        h_ms = np.empty(S_e, np.int64)
-        h_lb = np.empty((S_e, L), np.int64)
+        h_ms = torch.empty(S_e, dtype=torch.int64, pin_memory=True).numpy()
+        h_lb = torch.empty((S_e, L), dtype=torch.int64, pin_memory=True).numpy()
         import ctypes as C
 
         def e2e_step():

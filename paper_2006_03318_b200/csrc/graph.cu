@@ -14,7 +14,9 @@
 //   * the multiset CSR + in-degrees the list scheduler needs (sim.py:95-106).
 #include <algorithm>
 #include <atomic>
+#include <cstdio>
 #include <cstring>
+#include <deque>
 #include <functional>
 #include <numeric>
 #include <queue>
@@ -1376,7 +1378,30 @@ struct ChunkBufs {
   long long* lane_busy = nullptr;
   int* schedule = nullptr;
   int* dispatched = nullptr;
+  char* staging = nullptr;  // pinned: small outputs bound for pageable memory
 };
+
+// Small per-chunk outputs (makespan, lane_busy, dispatched) headed for
+// pageable host memory go through pinned staging and a stream-ordered host
+// memcpy: a direct cudaMemcpyAsync into pageable memory blocks the issuing
+// thread until the stream drains, which serialised the chunk pipeline.
+struct HostCopy {
+  void* dst;
+  const void* src;
+  size_t bytes;
+};
+void CUDART_CB host_copy_fn(void* p) {
+  const HostCopy* c = static_cast<const HostCopy*>(p);
+  memcpy(c->dst, c->src, c->bytes);
+}
+bool host_pinned(const void* p) {
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost || a.type == cudaMemoryTypeManaged;
+}
 
 int simulate_host_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, int path,
                        const ks_sim_out* out) {
@@ -1401,12 +1426,38 @@ int simulate_host_impl(const ks_graph* g, const ks_scenarios_desc* sc, int polic
   long long sc_chunk = std::max<long long>(4, (long long)(chunk_gb * (1ll << 30)) / per_scen);
   sc_chunk = std::min<long long>(sc_chunk, S);
   sc_chunk = (sc_chunk + 3) / 4 * 4;
-  const int nchunks = (int)((S + sc_chunk - 1) / sc_chunk);
+  // chunk boundaries: a 1/4 then a 1/2 chunk so the first D2H starts early and
+  // the D2H queue never waits for a full-size H2D, then full chunks (two
+  // device buffer sets, alternating streams)
+  std::vector<long long> bounds{0};
+  if (S > sc_chunk)
+    for (long long part : {sc_chunk / 4, sc_chunk / 2}) {
+      part = (part + 3) / 4 * 4;
+      if (part >= 4 && bounds.back() + part < S) bounds.push_back(bounds.back() + part);
+    }
+  while (bounds.back() < S) bounds.push_back(std::min<long long>(S, bounds.back() + sc_chunk));
+  const int nchunks = (int)bounds.size() - 1;
   cudaStream_t st[2];
   CUDA_TRY(cudaStreamCreateWithFlags(&st[0], cudaStreamNonBlocking));
   CUDA_TRY(cudaStreamCreateWithFlags(&st[1], cudaStreamNonBlocking));
   ChunkBufs buf[2];
   const long long ldc = sc_chunk;  // multiple of 4
+  const size_t stage_bytes = (size_t)ldc * (8 + 8 * std::max(g->L, 1) + 4);
+  const bool ms_pinned = !out->makespan || host_pinned(out->makespan);
+  const bool lb_pinned = !out->lane_busy || host_pinned(out->lane_busy);
+  const bool dp_pinned = !out->dispatched || host_pinned(out->dispatched);
+  std::deque<HostCopy> copies;
+  // D2H of n bytes from device src to host dst (staged at stage_off if dst is pageable)
+  auto d2h = [&](void* dst, const void* src, size_t n, bool pinned, ChunkBufs& b, size_t stage_off,
+                 cudaStream_t stream) {
+    if (pinned) {
+      CUDA_TRY(cudaMemcpyAsync(dst, src, n, cudaMemcpyDeviceToHost, stream));
+      return;
+    }
+    CUDA_TRY(cudaMemcpyAsync(b.staging + stage_off, src, n, cudaMemcpyDeviceToHost, stream));
+    copies.push_back(HostCopy{dst, b.staging + stage_off, n});
+    CUDA_TRY(cudaLaunchHostFunc(stream, host_copy_fn, &copies.back()));
+  };
   auto alloc = [&](ChunkBufs& b) {
     if (dense) CUDA_TRY(cudaMalloc(&b.dense, esz * N * ldc));
     if (out->start) CUDA_TRY(cudaMalloc(&b.start, 8 * N * ldc));
@@ -1414,12 +1465,14 @@ int simulate_host_impl(const ks_graph* g, const ks_scenarios_desc* sc, int polic
     if (out->lane_busy) CUDA_TRY(cudaMalloc(&b.lane_busy, 8 * ldc * std::max(g->L, 1)));
     if (out->schedule) CUDA_TRY(cudaMalloc(&b.schedule, 4 * N * ldc));
     if (out->dispatched) CUDA_TRY(cudaMalloc(&b.dispatched, 4 * ldc));
+    CUDA_TRY(cudaHostAlloc(&b.staging, stage_bytes, cudaHostAllocDefault));
   };
   auto release = [&]() {
     for (auto& b : buf) {
       void* ps[] = {b.dense, b.start, b.makespan, b.lane_busy, b.schedule, b.dispatched};
       for (void* p : ps)
         if (p) cudaFree(p);
+      if (b.staging) cudaFreeHost(b.staging);
     }
     cudaStreamDestroy(st[0]);
     cudaStreamDestroy(st[1]);
@@ -1428,18 +1481,47 @@ int simulate_host_impl(const ks_graph* g, const ks_scenarios_desc* sc, int polic
   try {
     alloc(buf[0]);
     if (nchunks > 1) alloc(buf[1]);
+    // DDSIM_HOST_TRACE=1: per-chunk event timeline on stderr (diagnostics)
+    const bool trace = getenv("DDSIM_HOST_TRACE") != nullptr;
+    std::vector<cudaEvent_t> ev;
+    auto mark = [&](cudaStream_t s) {
+      if (!trace) return;
+      cudaEvent_t e;
+      cudaEventCreate(&e);
+      cudaEventRecord(e, s);
+      ev.push_back(e);
+    };
     // per-chunk host slices of the scenario tables (kept alive to the end)
     std::vector<std::vector<int>> sptr(nchunks);
     std::vector<std::vector<long long>> ovr(nchunks);
     std::vector<std::vector<short>> perm(nchunks);
     std::vector<std::vector<unsigned char>> pres(nchunks);
+    // Copies run FIFO per direction (chunk c's H2D after chunk c-1's, same for
+    // D2H): concurrent same-direction copies would split the link, and both
+    // buffer sets would drain at once instead of one refilling while the
+    // other drains (measured on B200: H2D then overlaps D2H).
+    cudaEvent_t h2d_done[2], d2h_done[2];
+    for (int k = 0; k < 2; ++k) {
+      CUDA_TRY(cudaEventCreateWithFlags(&h2d_done[k], cudaEventDisableTiming));
+      CUDA_TRY(cudaEventCreateWithFlags(&d2h_done[k], cudaEventDisableTiming));
+    }
+    struct EvGuard {
+      cudaEvent_t* a;
+      ~EvGuard() {
+        for (int k = 0; k < 4; ++k) cudaEventDestroy(a[k]);
+      }
+    };
+    cudaEvent_t evs[4] = {h2d_done[0], h2d_done[1], d2h_done[0], d2h_done[1]};
+    EvGuard evg{evs};
     for (int c = 0; c < nchunks; ++c) {
-      const long long s0 = c * sc_chunk;
-      const int n_s = (int)std::min<long long>(sc_chunk, S - s0);
+      const long long s0 = bounds[c];
+      const int n_s = (int)(bounds[c + 1] - s0);
       ChunkBufs& b = buf[c & 1];
       cudaStream_t stream = st[c & 1];
       ks_scenarios_desc sub = *sc;
       sub.n_scenarios = n_s;
+      mark(stream);
+      if (c > 0) CUDA_TRY(cudaStreamWaitEvent(stream, h2d_done[(c - 1) & 1], 0));
       if (dense) {
         CUDA_TRY(cudaMemcpy2DAsync(b.dense, esz * ldc,
                                    static_cast<const char*>(sc->dense) + esz * s0, esz * sc->dense_ld,
@@ -1475,25 +1557,40 @@ int simulate_host_impl(const ks_graph* g, const ks_scenarios_desc* sc, int polic
       o.lane_busy = reinterpret_cast<int64_t*>(b.lane_busy);
       o.schedule = b.schedule;
       o.dispatched = b.dispatched;
+      CUDA_TRY(cudaEventRecord(h2d_done[c & 1], stream));
+      mark(stream);
       simulate_impl(g, &sub, policy, path, &o, stream);
+      mark(stream);
+      if (c > 0) CUDA_TRY(cudaStreamWaitEvent(stream, d2h_done[(c - 1) & 1], 0));
+      mark(stream);
       if (out->start)
         CUDA_TRY(cudaMemcpy2DAsync(out->start + s0, 8 * out->start_ld, b.start, 8 * ldc, 8 * n_s,
                                    g->n, cudaMemcpyDeviceToHost, stream));
-      if (out->makespan)
-        CUDA_TRY(cudaMemcpyAsync(out->makespan + s0, b.makespan, 8 * n_s, cudaMemcpyDeviceToHost,
-                                 stream));
+      if (out->makespan) d2h(out->makespan + s0, b.makespan, 8 * n_s, ms_pinned, b, 0, stream);
       if (out->lane_busy)
-        CUDA_TRY(cudaMemcpyAsync(out->lane_busy + s0 * g->L, b.lane_busy, 8 * (size_t)n_s * g->L,
-                                 cudaMemcpyDeviceToHost, stream));
+        d2h(out->lane_busy + s0 * g->L, b.lane_busy, 8 * (size_t)n_s * g->L, lb_pinned, b,
+            8 * (size_t)ldc, stream);
       if (out->schedule)
         CUDA_TRY(cudaMemcpyAsync(out->schedule + s0 * g->n, b.schedule, 4 * (size_t)n_s * g->n,
                                  cudaMemcpyDeviceToHost, stream));
       if (out->dispatched)
-        CUDA_TRY(cudaMemcpyAsync(out->dispatched + s0, b.dispatched, 4 * n_s, cudaMemcpyDeviceToHost,
-                                 stream));
+        d2h(out->dispatched + s0, b.dispatched, 4 * n_s, dp_pinned, b,
+            (size_t)ldc * (8 + 8 * std::max(g->L, 1)), stream);
+      CUDA_TRY(cudaEventRecord(d2h_done[c & 1], stream));
+      mark(stream);
     }
     CUDA_TRY(cudaStreamSynchronize(st[0]));
     CUDA_TRY(cudaStreamSynchronize(st[1]));
+    if (trace && !ev.empty()) {
+      fprintf(stderr, "ks_simulate_host: %d chunks of %lld scenarios\n", nchunks, sc_chunk);
+      for (size_t k = 0; k + 4 < ev.size(); k += 5) {
+        float t[5];
+        for (int j = 0; j < 5; ++j) cudaEventElapsedTime(&t[j], ev[0], ev[k + j]);
+        fprintf(stderr, "  chunk %zu: issue %.1f  h2d..%.1f  kernel..%.1f  d2h %.1f-%.1f ms\n",
+                k / 5, t[0], t[1], t[2], t[3], t[4]);
+      }
+      for (auto e : ev) cudaEventDestroy(e);
+    }
   } catch (...) {
     cudaStreamSynchronize(st[0]);
     cudaStreamSynchronize(st[1]);
