@@ -31,6 +31,8 @@
  *                          (graph.py:198-312) and check_lane_overlaps
  *                          (trace.py:255-265) over columnar trace records.
  *   ks_map_layers          map_tasks_to_layers (layers.py:50-81).
+ *   ks_breakdown           compute_breakdown / per_layer_breakdown
+ *                          (breakdown.py:42-111) for S scenarios.
  */
 #ifndef DDSIM_H_
 #define DDSIM_H_
@@ -195,6 +197,33 @@ int ks_simulate(const ks_graph* g, const ks_scenarios_desc* sc, int policy,
  * Synchronous. */
 int ks_simulate_host(const ks_graph* g, const ks_scenarios_desc* sc,
                      int policy, int path, const ks_sim_out* out);
+
+/* ---- runtime breakdown (breakdown.py:42-111) ---------------------------- */
+enum { KS_BD_CPU = 0, KS_BD_GPU = 1, KS_BD_COMM = 2, KS_BD_CPU_DATALOAD = 3 };
+typedef struct {
+  const uint8_t* row_class;   /* HOST [n_tasks] by frozen row: KS_BD_* (lane class;
+                               * DataLoad tasks on CPU lanes are KS_BD_CPU_DATALOAD) */
+  int32_t comm_as_gpu;        /* compute_breakdown keyword arguments          */
+  int32_t dataload_as_cpu;
+  int32_t gaps_as_cpu_busy;
+  const int32_t* row_layer;   /* HOST [n_tasks] layer index by frozen row (the
+                               * host maps "no layer" to its own index); NULL =
+                               * no per-layer output                           */
+  int32_t n_layers;
+} ks_breakdown_desc;
+
+/* compute_breakdown / per_layer_breakdown of a max-plus batch, on the device,
+ * asynchronously on `stream`.  start / makespan are ks_simulate's DEVICE
+ * outputs for the same graph and scenario table `sc` (durations are re-derived
+ * from sc).  Outputs (DEVICE):
+ *   parts[s * 4 + {0,1,2,3}] = cpu_only, gpu_only, parallel, idle (ns; the four
+ *                              sum to makespan[s]); all -1 if a lane's
+ *                              intervals were not sorted (negative durations)
+ *   layer_busy[(layer * 2 + {0 cpu, 1 gpu}) * S + s]  (may be NULL)
+ * Needs a lane-chained graph (KS_ERR_UNSUPPORTED otherwise). */
+int ks_breakdown(const ks_graph* g, const ks_scenarios_desc* sc, const int64_t* start,
+                 int64_t start_ld, const int64_t* makespan, const ks_breakdown_desc* bd,
+                 int64_t* parts, int64_t* layer_busy, void* stream);
 
 /* verify_acyclic: Kahn order with smallest-id tie-break (graph.py:129-148),
  * computed on the device.  order_out[k] = dense input index; returns

@@ -83,6 +83,14 @@ class SimOut(C.Structure):
                 ("schedule", P), ("dispatched", P)]
 
 
+class BreakdownDesc(C.Structure):
+    _fields_ = [("row_class", P), ("comm_as_gpu", C.c_int32), ("dataload_as_cpu", C.c_int32),
+                ("gaps_as_cpu_busy", C.c_int32), ("row_layer", P), ("n_layers", C.c_int32)]
+
+
+KS_BD_CPU, KS_BD_GPU, KS_BD_COMM, KS_BD_CPU_DATALOAD = 0, 1, 2, 3
+
+
 class TraceCols(C.Structure):
     _fields_ = [
         ("n", C.c_int64), ("id", P), ("kind", P), ("lane", P), ("start", P), ("duration", P),
@@ -112,6 +120,8 @@ _SIGNATURES = [
     ("ks_simulate", C.c_int, [P, C.POINTER(ScenariosDesc), C.c_int, C.c_int, C.POINTER(SimOut), P]),
     ("ks_simulate_host", C.c_int, [P, C.POINTER(ScenariosDesc), C.c_int, C.c_int, C.POINTER(SimOut)]),
     ("ks_toposort", C.c_int, [P, P, C.POINTER(C.c_int32)]),
+    ("ks_breakdown", C.c_int, [P, C.POINTER(ScenariosDesc), P, C.c_int64, P,
+                               C.POINTER(BreakdownDesc), P, P, P]),
     ("ks_ingest", C.c_int, [C.POINTER(TraceCols), C.c_int, C.c_int, C.POINTER(IngestOut)]),
     ("ks_map_layers", C.c_int, [C.POINTER(TraceCols), P, C.POINTER(MarkerCols), C.c_int, P, P]),
     ("ks_error_name", C.c_char_p, [C.c_int]),

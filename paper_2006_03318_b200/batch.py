@@ -29,7 +29,7 @@ import numpy as np
 from . import _native as N
 from .comm import COLLECTIVE_LANE, NetworkConfig, allreduce_duration, earliest_weight_update_task
 from .comm import last_backward_gpu_task
-from .errors import BadPipeline, Deadlock, MissingLayer, NoWeightUpdate
+from .errors import BadPipeline, Deadlock, MissingLayer, NoWeightUpdate, Unsupported
 from .frozen import ChainSpec, FrozenGraph
 from .graph import DependencyGraph, EdgeKind, Task
 from .trace import GradientBucketMap, TaskKind
@@ -48,6 +48,9 @@ class BatchResult:
     lane_busy: np.ndarray | None         # [S][L] int64
     start: np.ndarray | None             # [rows][S] int64 (frozen rows), -1 = absent
     schedule: np.ndarray | None = None   # [S][N] frozen rows in dispatch order
+    parts: np.ndarray | None = None      # [S][4] cpu_only, gpu_only, parallel, idle
+    layer_busy: np.ndarray | None = None # [n_layers][2][S] per-layer cpu / gpu ns
+    layer_names: list | None = None
 
     def start_of(self, s: int) -> dict[int, int]:
         col = self.start[:, s]
@@ -67,6 +70,50 @@ class BatchResult:
         else:
             used[list(present_lanes)] = True
         return {fz.lanes[j]: int(self.lane_busy[s, j]) for j in range(fz.L) if used[j]}
+
+
+    def breakdown_of(self, s: int):
+        """compute_breakdown (breakdown.py:42-98) of scenario s as the
+        reference's BreakdownReport, from the device-computed parts."""
+        from .breakdown import BreakdownReport
+        if self.parts is None:
+            raise ValueError("simulate_batch(..., breakdown=True) computes the breakdown")
+        c, g, par, idle = (int(x) for x in self.parts[s])
+        if c < 0:
+            raise Unsupported(f"scenario {s}: lane intervals not in lane order (negative durations)")
+        per_layer = {}
+        if self.layer_busy is not None:
+            fz = self.frozen
+            rc = fz.row_classes()
+            rows = rc != N.KS_BD_COMM
+            if self.start is not None:
+                rows &= self.start[:, s] >= 0
+            present = np.unique(_row_layer_ids(fz)[rows])
+            per_layer = {self.layer_names[k]: (int(self.layer_busy[k, 0, s]),
+                                               int(self.layer_busy[k, 1, s])) for k in present}
+        return BreakdownReport(cpu_only=c, gpu_only=g, parallel=par, idle=idle,
+                               total=int(self.makespan[s]), per_layer=per_layer)
+
+
+def _row_layer_ids(fz: FrozenGraph) -> np.ndarray:
+    """Layer index per frozen row (names sorted; None -> UNMAPPED_LAYER)."""
+    cached = getattr(fz, "_row_layer_cache", None)
+    if cached is not None:
+        return cached[0]
+    from .layers import UNMAPPED_LAYER
+    names = [UNMAPPED_LAYER if x is None else x
+             for x in (fz.task_layers or [None] * fz.n)]
+    uniq = sorted(set(names))
+    ix = {k: i for i, k in enumerate(uniq)}
+    per_task = np.fromiter((ix[k] for k in names), np.int32, len(names))
+    row = np.ascontiguousarray(per_task[fz.order] if fz.n else per_task, np.int32)
+    fz._row_layer_cache = (row, uniq)
+    return row
+
+
+def layer_names_of(fz: FrozenGraph) -> list:
+    _row_layer_ids(fz)
+    return fz._row_layer_cache[1]
 
 
 @dataclass
@@ -127,10 +174,29 @@ class ScenarioTable:
         return sc
 
 
+def _host_empty(shape) -> np.ndarray:
+    """int64 host array; page-locked when large, so that ks_simulate_host's
+    chunked device->host copies run asynchronously (a copy into pageable
+    memory blocks the issuing thread and serialises the chunk pipeline)."""
+    n = int(np.prod(shape))
+    if n * 8 >= (64 << 20):
+        import torch
+
+        return torch.empty(shape, dtype=torch.int64, pin_memory=True).numpy()
+    return np.empty(shape, np.int64)
+
+
 def simulate_batch(frozen: FrozenGraph, table: ScenarioTable, policy: str = "default",
                    want_start: bool = True, want_schedule: bool = False,
-                   path: int = N.KS_PATH_AUTO) -> BatchResult:
-    """Host buffers in/out (ks_simulate_host): the reference-facing call."""
+                   path: int = N.KS_PATH_AUTO, breakdown: bool = False,
+                   comm_as_gpu: bool = True, dataload_as_cpu: bool = True,
+                   gaps_as_cpu_busy: bool = True) -> BatchResult:
+    """Host buffers in/out (ks_simulate_host): the reference-facing call.
+    breakdown=True also runs compute_breakdown / per_layer_breakdown for
+    every scenario on the device (ks_breakdown; max-plus graphs)."""
+    if breakdown:
+        return _simulate_batch_with_breakdown(frozen, table, policy, want_start, comm_as_gpu,
+                                              dataload_as_cpu, gaps_as_cpu_busy)
     S = table.n_scenarios
     if frozen.n_ordered < frozen.n:
         missing = frozen.unordered_ids()
@@ -140,7 +206,7 @@ def simulate_batch(frozen: FrozenGraph, table: ScenarioTable, policy: str = "def
     rows, L = frozen.n, frozen.L
     ms = np.zeros(S, np.int64)
     lb = np.zeros((S, max(L, 1)), np.int64)
-    start = np.empty((max(rows, 1), S), np.int64) if want_start else None
+    start = _host_empty((max(rows, 1), S)) if want_start else None
     sched = np.empty((S, max(rows, 1)), np.int32) if want_schedule else None
     out = N.SimOut()
     out.makespan, out.lane_busy = ms.ctypes.data, lb.ctypes.data
@@ -153,6 +219,68 @@ def simulate_batch(frozen: FrozenGraph, table: ScenarioTable, policy: str = "def
                                      C.byref(out)), "simulate_batch")
     return BatchResult(frozen=frozen, makespan=ms, lane_busy=lb[:, :L],
                        start=None if start is None else start[:rows], schedule=sched)
+
+
+def _simulate_batch_with_breakdown(frozen, table, policy, want_start, comm_as_gpu, dataload_as_cpu,
+                                   gaps_as_cpu_busy) -> BatchResult:
+    import torch
+
+    if frozen.n_ordered < frozen.n:
+        missing = frozen.unordered_ids()
+        raise Deadlock(f"{len(missing)} tasks never became ready (first ids: {missing[:10]})")
+    if not frozen.chained:
+        raise Unsupported("the batched breakdown needs a lane-chained graph (max-plus path); "
+                          "use breakdown.compute_breakdown on a SimulationResult")
+    dev = torch.device("cuda", frozen.device)
+    S, rows, L = table.n_scenarios, frozen.n, frozen.L
+    dtab = table
+    if table.dense is not None and not (hasattr(table.dense, "is_cuda") and table.dense.is_cuda):
+        dtab = ScenarioTable(**{**table.__dict__, "dense": torch.as_tensor(
+            np.ascontiguousarray(table.dense)).to(dev)})
+    ms = torch.empty(S, dtype=torch.int64, device=dev)
+    lb = torch.empty((S, max(L, 1)), dtype=torch.int64, device=dev)
+    st = torch.empty((max(rows, 1), S), dtype=torch.int64, device=dev)
+    parts = torch.empty((S, 4), dtype=torch.int64, device=dev)
+    row_layer = _row_layer_ids(frozen)
+    names = layer_names_of(frozen)
+    lbz = torch.empty((max(len(names), 1), 2, S), dtype=torch.int64, device=dev)
+    with torch.cuda.device(dev):
+        stream = torch.cuda.current_stream().cuda_stream
+        simulate_batch_device(frozen, dtab, makespan=ms, lane_busy=lb, start=st, start_ld=S,
+                              stream=stream, policy=policy)
+        breakdown_batch_device(frozen, dtab, start=st, makespan=ms, parts=parts, layer_busy=lbz,
+                               stream=stream, comm_as_gpu=comm_as_gpu,
+                               dataload_as_cpu=dataload_as_cpu, gaps_as_cpu_busy=gaps_as_cpu_busy,
+                               row_layer=row_layer, n_layers=len(names))
+        torch.cuda.current_stream().synchronize()
+    return BatchResult(frozen=frozen, makespan=ms.cpu().numpy(), lane_busy=lb.cpu().numpy()[:, :L],
+                       start=st.cpu().numpy()[:rows] if want_start else None,
+                       parts=parts.cpu().numpy(), layer_busy=lbz.cpu().numpy(), layer_names=names)
+
+
+def breakdown_batch_device(frozen: FrozenGraph, table: ScenarioTable, *, start, makespan, parts,
+                           layer_busy=None, stream: int = 0, comm_as_gpu: bool = True,
+                           dataload_as_cpu: bool = True, gaps_as_cpu_busy: bool = True,
+                           row_layer=None, n_layers: int = 0, start_ld: int | None = None) -> None:
+    """ks_breakdown on device tensors (start / makespan from
+    simulate_batch_device on the same table); asynchronous on ``stream``."""
+    keep: list = []
+    sc = table.desc(keep)
+    bd = N.BreakdownDesc()
+    rc = frozen.row_classes()
+    keep.append(rc)
+    bd.row_class = rc.ctypes.data if rc.size else None
+    bd.comm_as_gpu, bd.dataload_as_cpu = int(comm_as_gpu), int(dataload_as_cpu)
+    bd.gaps_as_cpu_busy = int(gaps_as_cpu_busy)
+    if layer_busy is not None:
+        rl = N.c_i32(row_layer if row_layer is not None else _row_layer_ids(frozen))
+        keep.append(rl)
+        bd.row_layer = rl.ctypes.data if rl.size else None
+        bd.n_layers = n_layers or len(layer_names_of(frozen))
+    ld = start_ld if start_ld is not None else int(start.stride(0))
+    N.check(N.lib().ks_breakdown(frozen.handle, C.byref(sc), N.ptr(start), ld, N.ptr(makespan),
+                                 C.byref(bd), N.ptr(parts), N.ptr(layer_busy), C.c_void_p(stream)),
+            "ks_breakdown")
 
 
 def simulate_batch_device(frozen: FrozenGraph, table: ScenarioTable, *, makespan, lane_busy=None,

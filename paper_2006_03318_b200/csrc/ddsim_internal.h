@@ -205,6 +205,38 @@ cudaError_t launch_expand_durations(const long long* base, const unsigned* group
                                     const int* ovr_map, const long long* ovr, const int* scale_ptr,
                                     const ScaleStepDev* scale, int rows, int S, long long ld,
                                     long long* out, cudaStream_t st);
+// Batched runtime breakdown (breakdown.py:42-111) over a max-plus result.
+struct BdChain {
+  int lane, pos;            // inserted after `pos` static rows of its lane
+  int B, member_off, perm_off, pad;
+};
+struct BreakdownParams {
+  int n, L, S, n_chains;
+  const int* lane_ptr;      // [L+1] static lane sequences (frozen rows)
+  const int* lane_rows;
+  const int* lane_chain;    // [L] chain on the lane or -1
+  const BdChain* chains;
+  const int* member_rows;   // [perm_ld] frozen rows of chain members
+  const short* perm;        // [S][perm_ld] or null
+  int perm_ld;
+  const unsigned char* present;  // [S][n_chains] or null
+  const unsigned char* row_class;  // [n] KS_BD_*
+  const long long* gap;     // [n] by row
+  int dkind;                // 1 = int32, 2 = int64 durations [row][dld]
+  const void* dur;
+  long long dld;
+  const long long* start;
+  long long start_ld;
+  const long long* makespan;
+  int comm_as_gpu, dataload_as_cpu, gaps_as_cpu_busy;
+  long long* parts;         // [S][4] cpu_only, gpu_only, parallel, idle (-1: precondition failed)
+  // per-layer busy (per_layer_breakdown): [n_layers][2][S]
+  const int* row_layer;     // [n] or null
+  long long* layer_busy;
+  int n_layers;
+};
+cudaError_t launch_breakdown(const BreakdownParams& p, cudaStream_t stream);
+
 const char* jit_log();
 int maxplus_lanes_block_dim(int S, int num_sms);
 cudaError_t launch_listsched(const ListParams& p, cudaStream_t stream);

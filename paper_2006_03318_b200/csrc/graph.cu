@@ -115,6 +115,14 @@ struct ks_graph {
   int* d_prio = nullptr;
   unsigned char* d_flags = nullptr;
   unsigned* d_group = nullptr;
+  // breakdown geometry (chained graphs): per-lane static row sequences and
+  // where each permutable chain sits in its lane
+  bool bd_ok = false;
+  int* d_bd_ptr = nullptr;
+  int* d_bd_rows = nullptr;
+  int* d_bd_lane_chain = nullptr;
+  BdChain* d_bd_chains = nullptr;
+  int* d_bd_member_rows = nullptr;
 };
 
 namespace {
@@ -789,12 +797,50 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   g->d_prio = dev_upload(prio_r);
   g->d_flags = dev_upload(flags_r);
   g->d_group = dev_upload(group_r);
+
+  // ---- breakdown geometry -------------------------------------------------------
+  if (chained && L > 0) {
+    std::vector<int> bptr(L + 1, 0), brows, lane_chain(L, -1), pos_in_lane(n, -1);
+    for (int l = 0; l < L; ++l) {
+      for (int k = d->lane_order_ptr[l]; k < d->lane_order_ptr[l + 1]; ++k) {
+        pos_in_lane[d->lane_order[k]] = (int)brows.size() - bptr[l];
+        brows.push_back(g->row_of[d->lane_order[k]]);
+      }
+      bptr[l + 1] = (int)brows.size();
+    }
+    bool ok = true;
+    std::vector<BdChain> bch(NC);
+    std::vector<int> mrows(members.size());
+    for (size_t k = 0; k < members.size(); ++k) mrows[k] = members[k].row;
+    for (int c = 0; c < NC && ok; ++c) {
+      const int l = ch_lane[c];
+      if (lane_chain[l] >= 0) ok = false;  // one permutable chain per lane
+      lane_chain[l] = c;
+      const int h = d->chain_head ? d->chain_head[c] : -1;
+      bch[c].lane = l;
+      bch[c].pos = h >= 0 ? pos_in_lane[h] + 1 : 0;
+      bch[c].B = chains[c].B;
+      bch[c].member_off = chains[c].member_off;
+      bch[c].perm_off = chains[c].perm_off;
+      bch[c].pad = 0;
+    }
+    if (ok) {
+      g->bd_ok = true;
+      g->d_bd_ptr = dev_upload(bptr);
+      g->d_bd_rows = dev_upload(brows);
+      g->d_bd_lane_chain = dev_upload(lane_chain);
+      g->d_bd_chains = dev_upload(bch);
+      g->d_bd_member_rows = dev_upload(mrows);
+    }
+  }
 }
 
 void free_graph(ks_graph* g) {
   if (!g) return;
   void* dptrs[] = {g->d_dprog,   g->d_side_off,   g->d_side_slots,  g->d_side_ready,
-                   g->d_lprog,   g->d_lside_off,  g->d_lside_slots, g->d_lside_ready};
+                   g->d_lprog,   g->d_lside_off,  g->d_lside_slots, g->d_lside_ready,
+                   g->d_bd_ptr,  g->d_bd_rows,    g->d_bd_lane_chain, g->d_bd_chains,
+                   g->d_bd_member_rows};
   for (void* p : dptrs)
     if (p) cudaFree(p);
   void* ptrs[] = {g->d_prog,  g->d_extra, g->d_chains, g->d_members, g->d_child_ptr,
@@ -1602,6 +1648,86 @@ int simulate_host_impl(const ks_graph* g, const ks_scenarios_desc* sc, int polic
 }
 
 }  // namespace
+
+namespace {
+
+int breakdown_impl(const ks_graph* g, const ks_scenarios_desc* sc, const int64_t* start,
+                   int64_t start_ld, const int64_t* makespan, const ks_breakdown_desc* bd,
+                   int64_t* parts, int64_t* layer_busy, cudaStream_t stream) {
+  if (!g || !sc || !bd || !start || !makespan) fail(KS_ERR_INVALID, "null argument");
+  if (g->device < 0) fail(KS_ERR_NO_DEVICE, "graph was compiled without a device");
+  const int S = sc->n_scenarios;
+  if (S <= 0) fail(KS_ERR_INVALID, "n_scenarios must be positive");
+  if (!g->bd_ok)
+    fail(KS_ERR_UNSUPPORTED,
+         "batched breakdown needs a lane-chained graph (at most one permutable chain per lane)");
+  if (g->L > 32) fail(KS_ERR_UNSUPPORTED, "batched breakdown supports at most 32 lanes");
+  if (!bd->row_class) fail(KS_ERR_INVALID, "row_class is required");
+  if (layer_busy && bd->row_layer) {
+    for (int r = 0; r < g->n; ++r)
+      if (bd->row_layer[r] < 0 || bd->row_layer[r] >= bd->n_layers)
+        fail(KS_ERR_INVALID, "row_layer out of range");
+  }
+  DevGuard guard(g->device);
+  ScenTables T;
+  T.st = stream;
+  build_tables(g, sc, T, true, false);
+  BreakdownParams p;
+  memset(&p, 0, sizeof(p));
+  p.n = g->n;
+  p.L = g->L;
+  p.S = S;
+  p.n_chains = g->n_chains;
+  p.lane_ptr = g->d_bd_ptr;
+  p.lane_rows = g->d_bd_rows;
+  p.lane_chain = g->d_bd_lane_chain;
+  p.chains = g->d_bd_chains;
+  p.member_rows = g->d_bd_member_rows;
+  p.perm = T.perm;
+  p.perm_ld = sc->perm_ld;
+  p.present = T.present;
+  p.row_class = T.up(bd->row_class, (size_t)g->n);
+  p.gap = g->d_gap;
+  if (sc->dense_kind != 0 && sc->dense != nullptr) {
+    if (sc->dense_ld < S) fail(KS_ERR_INVALID, "dense_ld < n_scenarios");
+    p.dkind = sc->dense_kind == 1 ? 1 : 2;
+    p.dur = sc->dense;
+    p.dld = sc->dense_ld;
+  } else {
+    // derived durations (base, overrides, scale steps) materialised once
+    long long* buf = T.scratch<long long>((size_t)g->n * S);
+    CUDA_TRY(launch_expand_durations(g->d_dur, g->d_group, T.ovr_map, T.ovr, T.scale_ptr, T.scale,
+                                     g->n, S, S, buf, stream));
+    p.dkind = 2;
+    p.dur = buf;
+    p.dld = S;
+  }
+  p.start = reinterpret_cast<const long long*>(start);
+  p.start_ld = start_ld;
+  p.makespan = reinterpret_cast<const long long*>(makespan);
+  p.comm_as_gpu = bd->comm_as_gpu;
+  p.dataload_as_cpu = bd->dataload_as_cpu;
+  p.gaps_as_cpu_busy = bd->gaps_as_cpu_busy;
+  p.parts = reinterpret_cast<long long*>(parts);
+  if (layer_busy && bd->row_layer) {
+    p.row_layer = T.up(bd->row_layer, (size_t)g->n);
+    p.layer_busy = reinterpret_cast<long long*>(layer_busy);
+    p.n_layers = bd->n_layers;
+  }
+  if (g->n > 0) CUDA_TRY(launch_breakdown(p, stream));
+  return KS_OK;
+}
+
+}  // namespace
+
+extern "C" int ks_breakdown(const ks_graph* g, const ks_scenarios_desc* sc, const int64_t* start,
+                            int64_t start_ld, const int64_t* makespan, const ks_breakdown_desc* bd,
+                            int64_t* parts, int64_t* layer_busy, void* stream) {
+  KS_GUARD_BEGIN
+  return breakdown_impl(g, sc, start, start_ld, makespan, bd, parts, layer_busy,
+                        static_cast<cudaStream_t>(stream));
+  KS_GUARD_END
+}
 
 extern "C" int ks_simulate_host(const ks_graph* g, const ks_scenarios_desc* sc, int policy,
                                 int path, const ks_sim_out* out) {

@@ -395,7 +395,9 @@ __global__ void expand_durations_kernel(const long long* base, const unsigned* g
     if (g != 0u && scale_ptr) {
       for (int e = scale_ptr[s]; e < scale_ptr[s + 1]; ++e) {
         const ScaleStepDev st = scale[e];
-        if (g >= (unsigned)st.lo && g <= (unsigned)st.hi) d = scale_half_up(d, st.num, st.den);
+        // num == 0: a removal step (the row's start reads -1; d is unused)
+        if (g >= (unsigned)st.lo && g <= (unsigned)st.hi && st.num != 0)
+          d = scale_half_up(d, st.num, st.den);
       }
     }
     out[(long long)r * ld + s] = d;

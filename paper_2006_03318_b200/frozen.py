@@ -33,7 +33,7 @@ class ChainSpec:
 class FrozenGraph:
     def __init__(self, *, ids, duration, gap, ready, lane, priority, flags, group, edge_src,
                  edge_dst, lane_order_ptr, lane_order, lanes, chains=None, device=0,
-                 task_layers=None):
+                 task_layers=None, dataload=None):
         if not os.environ.get("DDSIM_COMPILE_ONLY"):
             N.require_device(device)
         self.device = device
@@ -50,7 +50,8 @@ class FrozenGraph:
         self.group = np.ascontiguousarray(group, dtype=np.uint32)
         self.edge_src = N.c_i32(edge_src)
         self.edge_dst = N.c_i32(edge_dst)
-        self.task_layers = task_layers
+        self.task_layers = task_layers    # per input task: layer name or None
+        self.dataload = dataload          # per input task: TaskKind.DATA_LOAD
         rank = np.empty(self.n, np.int32)
         rank[np.argsort(self.ids, kind="stable")] = np.arange(self.n, dtype=np.int32)
         self.id_rank = rank
@@ -128,6 +129,17 @@ class FrozenGraph:
         N.check(N.lib().ks_graph_levels(self._h, N.ptr(out)))
         return out
 
+    def row_classes(self) -> np.ndarray:
+        """KS_BD_* per frozen row (breakdown.py:57-67 lane classes; DataLoad
+        tasks on CPU lanes flagged separately)."""
+        lane_cls = np.array([N.KS_BD_CPU if ln.is_cpu else N.KS_BD_GPU if ln.is_gpu
+                             else N.KS_BD_COMM for ln in self.lanes] or [0], np.uint8)
+        cls = lane_cls[self.lane[self.order]] if self.n else np.zeros(0, np.uint8)
+        if self.dataload is not None:
+            dl = np.asarray(self.dataload, bool)[self.order]
+            cls = np.where(dl & (cls == N.KS_BD_CPU), N.KS_BD_CPU_DATALOAD, cls).astype(np.uint8)
+        return np.ascontiguousarray(cls, np.uint8)
+
     def unordered_ids(self) -> list[int]:
         return sorted(int(i) for i in self.row_ids[self.n_ordered:])
 
@@ -190,10 +202,12 @@ class FrozenGraph:
             for j in range(len(lanes)):
                 lo += per_lane[j]
                 lop.append(len(lo))
+        layers = [t.layer[0] if t.layer is not None else None for t in vals]
+        dataload = np.fromiter((t.kind is TaskKind.DATA_LOAD for t in vals), bool, n)
         return FrozenGraph(ids=ids, duration=duration, gap=gap, ready=ready, lane=lane,
                            priority=prio, flags=flags, group=group, edge_src=src, edge_dst=dst,
                            lane_order_ptr=lop, lane_order=lo, lanes=lanes, chains=chains,
-                           device=device)
+                           device=device, task_layers=layers, dataload=dataload)
 
     def toposort(self) -> tuple[list[int], bool]:
         """verify_acyclic order (smallest-id Kahn) computed on the device."""

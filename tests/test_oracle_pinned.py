@@ -131,3 +131,19 @@ def test_oracle_ingest_matches_reference_graphs(golden):
             if got_t is not None and got_t[0] == "*":
                 got_t = ("_global", got_t[1])
             assert (got_t if got_t else (None, None)) == exp, (case["name"], x)
+
+
+def test_breakdown_oracle_matches_reference_reports(golden):
+    """oracle/breakdown_oracle.py against the reference's own whatif reports
+    (predicted_breakdown of the transformed graph and its schedule)."""
+    from breakdown_oracle import breakdown
+    n = 0
+    for rec in golden["whatif"]:
+        if "graph" not in rec or "error" in rec.get("sim", {}):
+            continue
+        g = graph_from_obj(rec["graph"])
+        start = {int(k): v for k, v in rec["sim"]["start"].items()}
+        got = breakdown(g.tasks, start, rec["sim"]["makespan"])
+        assert got == rec["report"]["predicted_breakdown"], (rec["case"], rec["scenario"])
+        n += 1
+    assert n >= 25
