@@ -230,6 +230,8 @@ struct BreakdownParams {
   const long long* makespan;
   int comm_as_gpu, dataload_as_cpu, gaps_as_cpu_busy;
   long long* parts;         // [S][4] cpu_only, gpu_only, parallel, idle (-1: precondition failed)
+  int K;                    // time windows per scenario (parallel merge)
+  int* bad;                 // [S] scratch: scenario has a negative duration
   // per-layer busy (per_layer_breakdown): [n_layers][2][S]
   const int* row_layer;     // [n] or null
   long long* layer_busy;

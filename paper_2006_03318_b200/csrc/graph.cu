@@ -118,6 +118,7 @@ struct ks_graph {
   // breakdown geometry (chained graphs): per-lane static row sequences and
   // where each permutable chain sits in its lane
   bool bd_ok = false;
+  bool gap_nonneg = true;
   int* d_bd_ptr = nullptr;
   int* d_bd_rows = nullptr;
   int* d_bd_lane_chain = nullptr;
@@ -799,6 +800,8 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   g->d_group = dev_upload(group_r);
 
   // ---- breakdown geometry -------------------------------------------------------
+  for (int i = 0; i < n; ++i)
+    if (d->gap[i] < 0) g->gap_nonneg = false;
   if (chained && L > 0) {
     std::vector<int> bptr(L + 1, 0), brows, lane_chain(L, -1), pos_in_lane(n, -1);
     for (int l = 0; l < L; ++l) {
@@ -1662,6 +1665,7 @@ int breakdown_impl(const ks_graph* g, const ks_scenarios_desc* sc, const int64_t
     fail(KS_ERR_UNSUPPORTED,
          "batched breakdown needs a lane-chained graph (at most one permutable chain per lane)");
   if (g->L > 32) fail(KS_ERR_UNSUPPORTED, "batched breakdown supports at most 32 lanes");
+  if (!g->gap_nonneg) fail(KS_ERR_UNSUPPORTED, "batched breakdown needs non-negative gaps");
   if (!bd->row_class) fail(KS_ERR_INVALID, "row_class is required");
   if (layer_busy && bd->row_layer) {
     for (int r = 0; r < g->n; ++r)
@@ -1709,6 +1713,18 @@ int breakdown_impl(const ks_graph* g, const ks_scenarios_desc* sc, const int64_t
   p.dataload_as_cpu = bd->dataload_as_cpu;
   p.gaps_as_cpu_busy = bd->gaps_as_cpu_busy;
   p.parts = reinterpret_cast<long long*>(parts);
+  p.bad = T.scratch<int>((size_t)S);
+  {
+    // time windows per scenario: enough (scenario, window) threads to fill the
+    // GPU, at least ~512 rows of work per window
+    int nsm = 148;
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device);
+    const long long target = (long long)nsm * 2048;
+    long long K = (target + S - 1) / S;
+    K = std::min<long long>(K, std::max(1, g->n / 512));
+    p.K = (int)std::max<long long>(1, std::min<long long>(K, 65535));
+    if (const char* e = getenv("DDSIM_BD_WINDOWS")) p.K = std::max(1, atoi(e));
+  }
   if (layer_busy && bd->row_layer) {
     p.row_layer = T.up(bd->row_layer, (size_t)g->n);
     p.layer_busy = reinterpret_cast<long long*>(layer_busy);
