@@ -33,7 +33,7 @@ from .errors import BadPipeline, Deadlock, MissingLayer, NoWeightUpdate, Unsuppo
 from .frozen import ChainSpec, FrozenGraph
 from .graph import DependencyGraph, EdgeKind, Task
 from .trace import GradientBucketMap, TaskKind
-from .transform import Selector
+from .transform import Selector, TransformPipeline
 
 REMOVE = "remove"  # a compile_scale_sweep factor: remove the selected tasks
 
@@ -348,6 +348,124 @@ def compile_scale_sweep(graph: DependencyGraph, scenarios: list[list[tuple[Selec
     for k, (lo, hi, num, den) in enumerate(steps_out):
         arr[k] = (lo, hi, num, den)
     return group_of, np.array(ptr, np.int32), arr
+
+
+BATCHABLE_OPS = frozenset({"scale", "set_duration", "set_priority", "remove"})
+
+
+def compile_pipelines(graph: DependencyGraph, pipelines: list, device: int | None = None):
+    """Compile what-if pipelines (TransformPipeline, apply_pipeline semantics,
+    transform.py:285-399) into one scenario table over a frozen copy of
+    ``graph``: scale -> scale steps, set_duration -> per-scenario overrides,
+    remove -> KS_STEP_REMOVE steps, set_priority -> nothing (a lane-chained
+    graph's schedule does not depend on the policy or priorities).
+
+    Selections are evaluated on ``graph`` itself: scale / set_duration /
+    set_priority do not change the attributes selectors read, and removal is
+    final, so each step touches the same tasks as on the progressively
+    transformed graph.  Returns (FrozenGraph, ScenarioTable); raises
+    Unsupported for insert ops or an unchained graph."""
+    from .errors import UnknownTask
+    from .transform import select
+
+    pipes = [p if isinstance(p, TransformPipeline) else TransformPipeline.from_object(p)
+             for p in pipelines]
+    # 1. distinct selections
+    sel_ix: dict = {}
+    sel_sets: list[frozenset] = []
+    plan = []  # per pipeline: [(op, sel index, payload)]
+
+    def sel_of(step) -> int:
+        if "task_id" in step:
+            tid = step["task_id"]
+            if tid not in graph.tasks:
+                raise UnknownTask(f"task {tid} does not exist")
+            key = ("id", tid)
+            ids = frozenset([tid])
+        else:
+            key = ("sel", repr(step["selector"]))
+            if key in sel_ix:
+                return sel_ix[key]
+            ids = frozenset(select(graph, Selector.from_object(step["selector"])))
+        if key not in sel_ix:
+            sel_ix[key] = len(sel_sets)
+            sel_sets.append(ids)
+        return sel_ix[key]
+
+    for pipe in pipes:
+        ops = []
+        for step in pipe.steps:
+            op = step.get("op")
+            if op not in BATCHABLE_OPS:
+                raise Unsupported(f"pipeline op {op!r} has no scenario-table form "
+                                  "(run it through apply_pipeline + simulate)")
+            if op == "set_priority":
+                continue
+            if op == "scale":
+                f = Fraction(str(step["factor"]))
+                if f <= 0:
+                    raise BadPipeline(f"scale factor must be positive, got {f}")
+                ops.append(("scale", sel_of(step), f))
+            elif op == "set_duration":
+                ops.append(("set", sel_of(step), int(step["duration_ns"])))
+            else:
+                ops.append(("remove", sel_of(step), None))
+        plan.append(ops)
+    # 2. groups = membership signatures over the selections
+    member: dict[int, list[int]] = {}
+    for k, ids in enumerate(sel_sets):
+        for tid in ids:
+            member.setdefault(tid, []).append(k)
+    tasks = list(graph.tasks)
+    group_id: dict[tuple, int] = {(): 0}
+    group_of = np.zeros(len(tasks), np.uint32)
+    for i, tid in enumerate(tasks):
+        sig = tuple(member.get(tid, ()))
+        gid = group_id.setdefault(sig, len(group_id))
+        group_of[i] = gid
+    groups_of_sel: dict[int, list[int]] = {k: [] for k in range(len(sel_sets))}
+    for sig, gid in group_id.items():
+        for k in sig:
+            groups_of_sel[k].append(gid)
+    fz = FrozenGraph.from_graph(graph, group_of=group_of, device=device)
+    if not fz.chained:
+        raise Unsupported("compile_pipelines needs a lane-chained graph (max-plus path)")
+    # 3. per-scenario programs
+    S = len(pipes)
+    ptr = [0]
+    steps_out: list = []
+    ovr: dict[int, np.ndarray] = {}
+    index = {int(t): i for i, t in enumerate(fz.ids)}
+    base_rows = fz.duration
+    for s, ops in enumerate(plan):
+        prog: list = []          # [gid, num, den] in order
+        removed: set[int] = set()
+        for op, k, payload in ops:
+            gids = groups_of_sel[k]
+            if op == "scale":
+                prog += [[g, payload.numerator, payload.denominator] for g in gids if g not in removed]
+            elif op == "remove":
+                removed.update(gids)
+            else:  # set_duration of one task: earlier scales of its group are void
+                (tid,) = sel_sets[k]
+                g = gids[0]
+                if g in removed:
+                    raise UnknownTask(f"task {tid} does not exist")
+                prog = [e for e in prog if e[0] != g]
+                row = int(fz.row_of[index[tid]])
+                if row not in ovr:
+                    ovr[row] = np.full(S, base_rows[index[tid]], np.int64)
+                ovr[row][s] = payload
+        steps_out += [(g, g, num, den) for g, num, den in prog if g not in removed]
+        steps_out += [(g, g, 0, 0) for g in sorted(removed)]
+        ptr.append(len(steps_out))
+    arr = np.zeros(len(steps_out), N.SCALE_STEP_DTYPE)
+    for i, st in enumerate(steps_out):
+        arr[i] = st
+    table = ScenarioTable(n_scenarios=S, overrides=ovr,
+                          scale_ptr=np.array(ptr, np.int32) if steps_out else None,
+                          scale=arr if steps_out else None)
+    return fz, table
 
 
 @dataclass
