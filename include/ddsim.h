@@ -33,6 +33,10 @@
  *   ks_map_layers          map_tasks_to_layers (layers.py:50-81).
  *   ks_breakdown           compute_breakdown / per_layer_breakdown
  *                          (breakdown.py:42-111) for S scenarios.
+ *   ks_trace_parse         parse_trace (trace.py:281-328) straight into
+ *                          columns (host, multi-threaded), same validation
+ *                          and error precedence.
+ *   ks_trace_write         dump_trace (trace.py:331-379) from columns.
  */
 #ifndef DDSIM_H_
 #define DDSIM_H_
@@ -57,7 +61,9 @@ enum {
   KS_ERR_AMBIGUOUS = 8,           /* "AmbiguousMarker"     errors.py:67   */
   KS_ERR_OVERLAP = 9,             /* "OverlapViolation"    errors.py:34   */
   KS_ERR_BAD_PIPELINE = 10,       /* "BadPipeline"         errors.py:117  */
-  KS_ERR_NO_DEVICE = 11           /* "NoDevice"                           */
+  KS_ERR_NO_DEVICE = 11,          /* "NoDevice"                           */
+  KS_ERR_MALFORMED = 12,          /* "MalformedDocument"   errors.py:26   */
+  KS_ERR_SCHEMA = 13              /* "SchemaViolation"     errors.py:30   */
 };
 
 /* ---- schedule policies (sim.py:152-165, scenarios.py:633) -------------- */
@@ -295,6 +301,95 @@ typedef struct {
 int ks_map_layers(const ks_trace_cols* tc, const int32_t* launcher,
                   const ks_marker_cols* mc, int device, int32_t* tag_out,
                   int64_t* bad_event);
+
+/* ---- trace documents (trace.py:92-379) ---------------------------------- */
+typedef struct ks_trace ks_trace; /* opaque parsed document (host memory) */
+
+typedef struct {
+  int64_t n_events;
+  int32_t n_lanes;        /* lanes [0, n_event_lanes) are events' lanes in
+                           * order of first appearance, then sync targets
+                           * (TraceColumns.from_events order); the rest are
+                           * lanes named only by layer markers              */
+  int32_t n_event_lanes;
+  int64_t n_names;        /* distinct event names, first-appearance order   */
+  int64_t n_markers;
+  int32_t n_layers;       /* distinct marker layer names                    */
+  int64_t lane_bytes, name_bytes, layer_bytes;
+  /* byte spans of the "gradient_buckets" / "metadata" values in the input
+   * text (-1 = absent); the host validates these small objects itself. */
+  int64_t buckets_off, buckets_len;
+  int64_t metadata_off, metadata_len;
+} ks_trace_info;
+
+typedef struct {              /* caller-allocated [n_events]; NULL = skip */
+  int64_t* id;
+  uint8_t* kind;              /* KS_KIND_*                                 */
+  int32_t* lane;
+  int64_t* start;             /* ns (us_to_ns, half-up)                    */
+  int64_t* duration;
+  int64_t* correlation;       /* -1 = none                                 */
+  int32_t* sync_target;       /* lane index, -1 = none                     */
+  uint8_t* is_dtoh;           /* name startswith "memcpy_dtoh"             */
+  int32_t* name_id;
+  int64_t* size_bytes;        /* -1 = none                                 */
+} ks_trace_event_cols;
+
+typedef struct {              /* caller-allocated [n_markers]              */
+  int32_t* lane;
+  int64_t* start;
+  int64_t* end;
+  int32_t* layer_id;
+  uint8_t* phase;             /* 0 Forward, 1 Backward, 2 WeightUpdate     */
+} ks_trace_marker_cols;
+
+/* Parse + validate a UTF-8 trace document.  n_threads <= 0: all host cores.
+ * Errors: KS_ERR_MALFORMED, KS_ERR_SCHEMA, KS_ERR_OVERLAP (err_ids[0..1] =
+ * the two event ids), KS_ERR_UNSUPPORTED (values a Python int/str could hold
+ * but the columns cannot: ids >= 2^63, float names, non-ASCII numeric
+ * strings).  Detail text via ks_last_error_detail(). */
+int ks_trace_parse(const char* text, int64_t len, int n_threads, ks_trace** out,
+                   int64_t* err_ids);
+int ks_trace_get_info(const ks_trace* t, ks_trace_info* info);
+int ks_trace_events(const ks_trace* t, const ks_trace_event_cols* cols);
+int ks_trace_markers(const ks_trace* t, const ks_trace_marker_cols* cols);
+/* which: 0 lanes, 1 names, 2 layers.  bytes[offsets[i] .. offsets[i+1]). */
+int ks_trace_strings(const ks_trace* t, int which, char* bytes, int64_t* offsets);
+void ks_trace_destroy(ks_trace* t);
+
+typedef struct {
+  int64_t n_events;
+  const int64_t* id;
+  const uint8_t* kind;
+  const int32_t* lane;
+  const int64_t* start;
+  const int64_t* duration;
+  const int64_t* correlation;   /* -1 = none; NULL = none for all            */
+  const int32_t* sync_target;   /* -1 = none; may be NULL                    */
+  const int32_t* name_id;
+  const int64_t* size_bytes;    /* -1 = none; may be NULL                    */
+  int32_t n_lanes;
+  const char* lane_bytes;
+  const int64_t* lane_off;      /* [n_lanes+1]                               */
+  int64_t n_names;
+  const char* name_bytes;
+  const int64_t* name_off;
+  int64_t n_markers;
+  const int32_t* m_lane;
+  const int64_t* m_start;
+  const int64_t* m_end;
+  const int32_t* m_layer;
+  const uint8_t* m_phase;
+  int32_t n_layers;
+  const char* layer_bytes;
+  const int64_t* layer_off;
+  const char* extra_json;       /* raw extra top-level members, or NULL     */
+} ks_trace_write_desc;
+
+/* Columns -> document text in a malloc'ed buffer (free: ks_buffer_free). */
+int ks_trace_write(const ks_trace_write_desc* d, int n_threads, char** out,
+                   int64_t* out_len);
+void ks_buffer_free(char* p);
 
 /* ---- misc ---------------------------------------------------------------- */
 const char* ks_error_name(int code);

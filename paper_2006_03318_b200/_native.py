@@ -33,6 +33,8 @@ KS_ERR_AMBIGUOUS = 8
 KS_ERR_OVERLAP = 9
 KS_ERR_BAD_PIPELINE = 10
 KS_ERR_NO_DEVICE = 11
+KS_ERR_MALFORMED = 12
+KS_ERR_SCHEMA = 13
 
 KS_POLICY_DEFAULT, KS_POLICY_PRIORITY, KS_POLICY_VDNN = 0, 1, 2
 KS_PATH_AUTO, KS_PATH_MAXPLUS, KS_PATH_LISTSCHED = 0, 1, 2
@@ -111,6 +113,39 @@ class MarkerCols(C.Structure):
     _fields_ = [("n", C.c_int64), ("lane", P), ("start", P), ("end", P), ("tag", P)]
 
 
+class TraceInfo(C.Structure):
+    _fields_ = [
+        ("n_events", C.c_int64), ("n_lanes", C.c_int32), ("n_event_lanes", C.c_int32),
+        ("n_names", C.c_int64), ("n_markers", C.c_int64), ("n_layers", C.c_int32),
+        ("lane_bytes", C.c_int64), ("name_bytes", C.c_int64), ("layer_bytes", C.c_int64),
+        ("buckets_off", C.c_int64), ("buckets_len", C.c_int64),
+        ("metadata_off", C.c_int64), ("metadata_len", C.c_int64),
+    ]
+
+
+class TraceEventCols(C.Structure):
+    _fields_ = [(n, P) for n in ("id", "kind", "lane", "start", "duration", "correlation",
+                                 "sync_target", "is_dtoh", "name_id", "size_bytes")]
+
+
+class TraceMarkerCols(C.Structure):
+    _fields_ = [(n, P) for n in ("lane", "start", "end", "layer_id", "phase")]
+
+
+class TraceWriteDesc(C.Structure):
+    _fields_ = [
+        ("n_events", C.c_int64), ("id", P), ("kind", P), ("lane", P), ("start", P),
+        ("duration", P), ("correlation", P), ("sync_target", P), ("name_id", P),
+        ("size_bytes", P),
+        ("n_lanes", C.c_int32), ("lane_bytes", P), ("lane_off", P),
+        ("n_names", C.c_int64), ("name_bytes", P), ("name_off", P),
+        ("n_markers", C.c_int64), ("m_lane", P), ("m_start", P), ("m_end", P),
+        ("m_layer", P), ("m_phase", P),
+        ("n_layers", C.c_int32), ("layer_bytes", P), ("layer_off", P),
+        ("extra_json", C.c_char_p),
+    ]
+
+
 # name, restype, argtypes
 _SIGNATURES = [
     ("ks_graph_create", C.c_int, [C.POINTER(GraphDesc), C.c_int, C.POINTER(P), P]),
@@ -124,6 +159,15 @@ _SIGNATURES = [
                                C.POINTER(BreakdownDesc), P, P, P]),
     ("ks_ingest", C.c_int, [C.POINTER(TraceCols), C.c_int, C.c_int, C.POINTER(IngestOut)]),
     ("ks_map_layers", C.c_int, [C.POINTER(TraceCols), P, C.POINTER(MarkerCols), C.c_int, P, P]),
+    ("ks_trace_parse", C.c_int, [C.c_char_p, C.c_int64, C.c_int, C.POINTER(P), P]),
+    ("ks_trace_get_info", C.c_int, [P, C.POINTER(TraceInfo)]),
+    ("ks_trace_events", C.c_int, [P, C.POINTER(TraceEventCols)]),
+    ("ks_trace_markers", C.c_int, [P, C.POINTER(TraceMarkerCols)]),
+    ("ks_trace_strings", C.c_int, [P, C.c_int, P, P]),
+    ("ks_trace_destroy", None, [P]),
+    ("ks_trace_write", C.c_int, [C.POINTER(TraceWriteDesc), C.c_int, C.POINTER(P),
+                                 C.POINTER(C.c_int64)]),
+    ("ks_buffer_free", None, [P]),
     ("ks_error_name", C.c_char_p, [C.c_int]),
     ("ks_last_error_detail", C.c_char_p, []),
     ("ks_device_count", C.c_int, [C.POINTER(C.c_int)]),
@@ -177,6 +221,8 @@ _ERROR_CLASS = {
     KS_ERR_AMBIGUOUS: "AmbiguousMarker",
     KS_ERR_BAD_PIPELINE: "BadPipeline",
     KS_ERR_NO_DEVICE: "NoDevice",
+    KS_ERR_MALFORMED: "MalformedDocument",
+    KS_ERR_SCHEMA: "SchemaViolation",
 }
 
 

@@ -29,6 +29,9 @@ NVCC_FLAGS = [
 ]
 
 
+GXX_FLAGS = ["-O3", "-std=c++17", "-fPIC", "-pthread", "-Wall", "-Wno-unused-function"]
+
+
 def _nvcc() -> str:
     for cand in (os.environ.get("NVCC"), "/usr/local/cuda/bin/nvcc", shutil.which("nvcc")):
         if cand and Path(cand).exists():
@@ -61,7 +64,7 @@ def build_library(verbose: bool = False) -> Path:
     BUILD.mkdir(parents=True, exist_ok=True)
     _embed_sources()
     nvcc = _nvcc()
-    sources = sorted(CSRC.glob("*.cu"))
+    sources = sorted(CSRC.glob("*.cu")) + sorted(CSRC.glob("*.cpp"))
     headers = (sorted(CSRC.glob("*.h")) + sorted(CSRC.glob("*.cuh"))
                + sorted((CSRC / "generated").glob("*.inc")) + [ROOT / "include" / "ddsim.h"])
     newest_h = max(h.stat().st_mtime for h in headers)
@@ -70,8 +73,12 @@ def build_library(verbose: bool = False) -> Path:
         obj = BUILD / (src.stem + ".o")
         if obj.exists() and obj.stat().st_mtime > max(src.stat().st_mtime, newest_h):
             return obj
-        _run([nvcc, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)],
-             BUILD / (src.stem + ".ptxas.log"))
+        if src.suffix == ".cpp":  # host-only code: plain g++
+            _run(["g++", *GXX_FLAGS, "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)],
+                 BUILD / (src.stem + ".gxx.log"))
+        else:
+            _run([nvcc, *NVCC_FLAGS, "-I", str(ROOT / "include"), "-c", str(src), "-o", str(obj)],
+                 BUILD / (src.stem + ".ptxas.log"))
         return obj
 
     with ThreadPoolExecutor(max_workers=min(8, len(sources))) as ex:

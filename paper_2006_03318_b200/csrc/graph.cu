@@ -141,6 +141,29 @@ struct DevGuard {
   }
 };
 
+// LSD radix sort of 64-bit keys, 16-bit digits; digits that are constant
+// across all keys are skipped (edge keys are (u << 32 | v) with u, v < n).
+static void radix_sort_u64(std::vector<unsigned long long>& a) {
+  const size_t n = a.size();
+  if (n < 4096) {
+    std::sort(a.begin(), a.end());
+    return;
+  }
+  unsigned long long all_or = 0, all_and = ~0ull;
+  for (unsigned long long x : a) { all_or |= x; all_and &= x; }
+  std::vector<unsigned long long> b(n);
+  std::vector<size_t> cnt(65536);
+  for (int sh = 0; sh < 64; sh += 16) {
+    if ((((all_or ^ all_and) >> sh) & 0xffffull) == 0) continue;  // digit constant
+    std::fill(cnt.begin(), cnt.end(), 0);
+    for (unsigned long long x : a) ++cnt[(x >> sh) & 0xffff];
+    size_t o = 0;
+    for (size_t& c : cnt) { size_t t = c; c = o; o += t; }
+    for (unsigned long long x : a) b[cnt[(x >> sh) & 0xffff]++] = x;
+    a.swap(b);
+  }
+}
+
 void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   const int n = d->n_tasks;
   const int L = d->n_lanes;
@@ -176,7 +199,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   std::vector<unsigned long long> keys(E);
   for (long long k = 0; k < E; ++k)
     keys[k] = ((unsigned long long)(unsigned)d->edge_src[k] << 32) | (unsigned)d->edge_dst[k];
-  std::sort(keys.begin(), keys.end());
+  radix_sort_u64(keys);
   keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
   g->n_edges_unique = (int)keys.size();
   auto has_edge = [&](int u, int v) {
@@ -247,7 +270,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
       ckeys.push_back(((unsigned long long)(n + c) << 32) | (unsigned)t);
     }
   }
-  std::sort(ckeys.begin(), ckeys.end());
+  radix_sort_u64(ckeys);
   ckeys.erase(std::unique(ckeys.begin(), ckeys.end()), ckeys.end());
   std::vector<int> cptr(NN + 1, 0), cadj(ckeys.size()), cindeg(NN, 0);
   for (unsigned long long k : ckeys) {
@@ -1248,6 +1271,8 @@ const char* ks_error_name(int code) {
     case KS_ERR_OVERLAP: return "OverlapViolation";
     case KS_ERR_BAD_PIPELINE: return "BadPipeline";
     case KS_ERR_NO_DEVICE: return "NoDevice";
+    case KS_ERR_MALFORMED: return "MalformedDocument";
+    case KS_ERR_SCHEMA: return "SchemaViolation";
     default: return "KernsimError";
   }
 }

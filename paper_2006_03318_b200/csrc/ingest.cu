@@ -17,6 +17,10 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <atomic>
+#include <chrono>
+#include <cstdio>
+#include <cstdlib>
 #include <climits>
 #include <string>
 #include <vector>
@@ -199,17 +203,26 @@ __global__ void stream_keys_k(const unsigned char* kind, const int* lane, const 
 }
 
 // rule 4 (syncs + blocking dtoh): one candidate per (event, target lane slot)
+__global__ void sync_src_flag_k(const unsigned char* kind, const unsigned char* is_dtoh,
+                                const long long* corr, long long n, unsigned char* flag) {
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n;
+       i += (long long)gridDim.x * blockDim.x) {
+    const int k = kind[i];
+    flag[i] = (k == KS_KIND_SYNC) || (is_cpu_kind(k) && is_dtoh[i] && corr[i] >= 0);
+  }
+}
+
 __global__ void sync_link_k(const unsigned char* kind, const long long* start, const long long* corr,
                             const int* sync_target, const unsigned char* is_dtoh, const int* lane,
-                            const long long* ids, long long n, const int* gpu_lanes, int n_gpu,
+                            const int* srcs, long long n_src, const int* gpu_lanes, int n_gpu,
                             const int* seg_first, const int* seg_last, const long long* st_ls,
                             const int* st_idx, const long long* gpu_sorted_key,
                             const int* gpu_sorted_idx, long long n_gpu_keyed, int* esrc, int* edst,
                             unsigned char* ekind, unsigned char* eflag) {
-  const long long total = n * (long long)(n_gpu + 1);
+  const long long total = n_src * (long long)(n_gpu + 1);
   for (long long c = blockIdx.x * (long long)blockDim.x + threadIdx.x; c < total;
        c += (long long)gridDim.x * blockDim.x) {
-    const long long e = c / (n_gpu + 1);
+    const long long e = srcs[c / (n_gpu + 1)];
     const int slot = (int)(c % (n_gpu + 1));
     eflag[c] = 0;
     const int k = kind[e];
@@ -412,10 +425,43 @@ void set_last_error(const std::string& msg);
 
 using namespace ddsim;
 
+// DDSIM_INGEST_TIMING=1: synchronize and print the wall time of each stage
+struct StageTimer {
+  const char* what;
+  cudaStream_t st;
+  bool on;
+  std::chrono::steady_clock::time_point t0;
+  StageTimer(const char* w, cudaStream_t s)
+      : what(w), st(s), on(std::getenv("DDSIM_INGEST_TIMING") != nullptr),
+        t0(std::chrono::steady_clock::now()) {}
+  void mark(const char* stage) {
+    if (!on) return;
+    cudaStreamSynchronize(st);
+    auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[%s] %-12s %8.3f ms\n", what, stage,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  }
+};
+
+// Keep freed stream-ordered memory in the device pool between calls (the
+// default release threshold returns it to the driver at every synchronize).
+static void keep_pool(int device) {
+  static std::atomic<unsigned> done{0};
+  if (device < 0 || device >= 32 || (done.load() >> device) & 1u) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done.fetch_or(1u << device);
+}
+
 extern "C" int ks_ingest(const ks_trace_cols* tc, int device, int check_overlaps,
                          ks_ingest_out* out) {
   if (!tc || !out) return KS_ERR_INVALID;
   cudaSetDevice(device);
+  keep_pool(device);
   const long long n = tc->n;
   const int L = tc->n_lanes;
   out->n_edges = 0;
@@ -427,6 +473,7 @@ extern "C" int ks_ingest(const ks_trace_cols* tc, int device, int check_overlaps
   cudaStream_t st;
   if (cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking) != cudaSuccess) return KS_ERR_CUDA;
   int rc = KS_OK;
+  StageTimer T_("ks_ingest", st);
   try {
     Pool P{st};
     long long* d_id = P.up(reinterpret_cast<const long long*>(tc->id), n);
@@ -438,6 +485,7 @@ extern "C" int ks_ingest(const ks_trace_cols* tc, int device, int check_overlaps
     int* d_st = P.up(tc->sync_target, n);
     unsigned char* d_dtoh = P.up(tc->is_dtoh, n);
     unsigned char* d_lclass = P.up(tc->lane_class, (size_t)L);
+    T_.mark("upload");
     long long* d_end = P.get<long long>(n);
     end_k<<<blocks_for(n), TPB, 0, st>>>(d_start, d_dur, d_end, n);
     note_launch();
@@ -472,6 +520,7 @@ extern "C" int ks_ingest(const ks_trace_cols* tc, int device, int check_overlaps
       }
     }
 
+    T_.mark("overlap");
     // ---- rules 1, 2, 5: lane order (lane, start, id) + gaps ---------------------
     int* perm = P.get<int>(n);
     iota_k<<<blocks_for(n), TPB, 0, st>>>(perm, n);
@@ -486,20 +535,35 @@ extern "C" int ks_ingest(const ks_trace_cols* tc, int device, int check_overlaps
     lane_bounds_k<<<blocks_for(n), TPB, 0, st>>>(perm, d_lane, n, lane_first, lane_last);
     note_launch(3);
 
-    // candidate edge buffers: [lane n][launch n][sync n*(G+1)]
-    std::vector<int> gpu_lanes_h;
-    for (int l = 0; l < L; ++l) {
-      // GPU lanes present as an event lane (sorted by text rank for determinism)
-      if (tc->lane_class[l] == 1) gpu_lanes_h.push_back(l);
+    T_.mark("lane-sort");
+    // lanes that carry events (lane_bounds of the sorted view), GPU ones in index order
+    std::vector<int> lf(L), ll(L);
+    ICUDA(cudaMemcpyAsync(lf.data(), lane_first, sizeof(int) * L, cudaMemcpyDeviceToHost, st));
+    ICUDA(cudaMemcpyAsync(ll.data(), lane_last, sizeof(int) * L, cudaMemcpyDeviceToHost, st));
+    // rule-4 sources: Sync events and CPU memcpy_dtoh launches (compacted list)
+    int* ssrc = P.get<int>(n);
+    int* d_ns = P.get<int>(1);
+    {
+      unsigned char* sflag = P.get<unsigned char>(n);
+      sync_src_flag_k<<<blocks_for(n), TPB, 0, st>>>(d_kind, d_dtoh, d_corr, n, sflag);
+      int* all = P.get<int>(n);
+      iota_k<<<blocks_for(n), TPB, 0, st>>>(all, n);
+      note_launch(2);
+      size_t tmp = 0;
+      cub::DeviceSelect::Flagged(nullptr, tmp, all, sflag, ssrc, d_ns, (int)n, st);
+      void* t = P.get<unsigned char>(tmp);
+      ICUDA(cub::DeviceSelect::Flagged(t, tmp, all, sflag, ssrc, d_ns, (int)n, st));
+      note_launch();
     }
-    // keep only lanes that carry events
-    std::vector<char> has_ev(L, 0);
-    for (long long i = 0; i < n; ++i) has_ev[tc->lane[i]] = 1;
-    gpu_lanes_h.erase(std::remove_if(gpu_lanes_h.begin(), gpu_lanes_h.end(),
-                                     [&](int l) { return !has_ev[l]; }),
-                      gpu_lanes_h.end());
+    int ns = 0;
+    ICUDA(cudaMemcpyAsync(&ns, d_ns, sizeof(int), cudaMemcpyDeviceToHost, st));
+    ICUDA(cudaStreamSynchronize(st));
+    std::vector<int> gpu_lanes_h;
+    for (int l = 0; l < L; ++l)
+      if (tc->lane_class[l] == 1 && ll[l] > lf[l]) gpu_lanes_h.push_back(l);
     const int G = (int)gpu_lanes_h.size();
-    const long long c_lane = n, c_launch = n, c_sync = n * (long long)(G + 1);
+    // candidate edge buffers: [lane n][launch n][sync ns*(G+1)]
+    const long long c_lane = n, c_launch = n, c_sync = (long long)ns * (G + 1);
     const long long C = c_lane + c_launch + c_sync;
     int* esrc = P.get<int>(C);
     int* edst = P.get<int>(C);
@@ -510,6 +574,7 @@ extern "C" int ks_ingest(const ks_trace_cols* tc, int device, int check_overlaps
                                                 ekind, eflag, d_gap);
     note_launch();
 
+    T_.mark("lane-edges");
     // ---- rule 3: launch correlation ---------------------------------------------
     long long* cpu_key = P.get<long long>(n);
     long long* gpu_key = P.get<long long>(n);
@@ -540,6 +605,7 @@ extern "C" int ks_ingest(const ks_trace_cols* tc, int device, int check_overlaps
       }
     }
 
+    T_.mark("launch-join");
     // ---- rule 4: stream tasks sorted by (lane, launch start, id) ------------------
     int* skl = P.get<int>(n);
     long long* skls = P.get<long long>(n);
@@ -564,28 +630,28 @@ extern "C" int ks_ingest(const ks_trace_cols* tc, int device, int check_overlaps
     lane_bounds_k<<<blocks_for(n), TPB, 0, st>>>(sperm, skl, n, seg_first,
                                                  seg_last);
     note_launch(3);
+    T_.mark("stream-sort");
     int* d_gl = G > 0 ? P.up(gpu_lanes_h.data(), (size_t)G) : P.get<int>(1);
     sync_link_k<<<blocks_for(c_sync), TPB, 0, st>>>(
-        d_kind, d_start, d_corr, d_st, d_dtoh, d_lane, d_id, n, d_gl, G, seg_first, seg_last, st_ls,
+        d_kind, d_start, d_corr, d_st, d_dtoh, d_lane, ssrc, ns, d_gl, G, seg_first, seg_last, st_ls,
         sperm, gpu_sk, gpu_si, n, esrc + c_lane + c_launch, edst + c_lane + c_launch,
         ekind + c_lane + c_launch, eflag + c_lane + c_launch);
     note_launch();
 
+    T_.mark("sync-link");
     // ---- compact + copy back ------------------------------------------------------
     int* os = P.get<int>(C);
     int* od = P.get<int>(C);
     unsigned char* ok = P.get<unsigned char>(C);
     const long long m = compact_edges(P, esrc, edst, ekind, eflag, C, os, od, ok);
     if (m > out->edge_cap) throw IngestError{KS_ERR_INVALID, "edge capacity too small"};
+    T_.mark("compact");
     ICUDA(cudaMemcpyAsync(out->edge_src, os, sizeof(int) * m, cudaMemcpyDeviceToHost, st));
     ICUDA(cudaMemcpyAsync(out->edge_dst, od, sizeof(int) * m, cudaMemcpyDeviceToHost, st));
     ICUDA(cudaMemcpyAsync(out->edge_kind, ok, m, cudaMemcpyDeviceToHost, st));
     ICUDA(cudaMemcpyAsync(out->lane_order, perm, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
     ICUDA(cudaMemcpyAsync(out->gap, d_gap, sizeof(long long) * n, cudaMemcpyDeviceToHost, st));
     ICUDA(cudaMemcpyAsync(out->launcher, d_launcher, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
-    std::vector<int> lf(L), ll(L);
-    ICUDA(cudaMemcpyAsync(lf.data(), lane_first, sizeof(int) * L, cudaMemcpyDeviceToHost, st));
-    ICUDA(cudaMemcpyAsync(ll.data(), lane_last, sizeof(int) * L, cudaMemcpyDeviceToHost, st));
     ICUDA(cudaStreamSynchronize(st));
     // lane_order_ptr: lanes appear in index order in the sorted view
     int pos = 0;
@@ -595,6 +661,7 @@ extern "C" int ks_ingest(const ks_trace_cols* tc, int device, int check_overlaps
     }
     out->lane_order_ptr[L] = pos;
     out->n_edges = m;
+    T_.mark("copy-back");
   } catch (const IngestError& e) {
     set_last_error(e.msg);
     rc = e.code;
@@ -606,6 +673,7 @@ extern "C" int ks_ingest(const ks_trace_cols* tc, int device, int check_overlaps
   }
   cudaStreamSynchronize(st);
   cudaStreamDestroy(st);
+  T_.mark("release");
   if (rc != KS_OK) cudaGetLastError();  // do not leave a non-sticky error for later calls
   return rc;
 }
@@ -615,6 +683,7 @@ extern "C" int ks_map_layers(const ks_trace_cols* tc, const int32_t* launcher,
                              int64_t* bad_event) {
   if (!tc || !mc || !tag_out) return KS_ERR_INVALID;
   cudaSetDevice(device);
+  keep_pool(device);
   const long long n = tc->n, M = mc->n;
   const int L = tc->n_lanes;
   if (bad_event) *bad_event = -1;

@@ -10,6 +10,8 @@ from __future__ import annotations
 
 import ctypes as C
 import os
+import sys
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -18,6 +20,17 @@ from . import _native as N
 from .trace import LaneId, TaskKind
 
 VDNN_MALLOC_PREFIX = "cudaMalloc_vdnn"  # scenarios.py:619-622
+_T = [0.0]
+
+
+def _tick(what):
+    """DDSIM_INGEST_TIMING=1: wall time of the freeze steps."""
+    if not os.environ.get("DDSIM_INGEST_TIMING"):
+        return
+    t = time.perf_counter()
+    if what is not None:
+        print(f"[FrozenGraph] {what:14s} {1e3 * (t - _T[0]):8.3f} ms", file=sys.stderr)
+    _T[0] = t
 
 
 @dataclass
@@ -36,6 +49,7 @@ class FrozenGraph:
                  task_layers=None, dataload=None):
         if not os.environ.get("DDSIM_COMPILE_ONLY"):
             N.require_device(device)
+        _tick(None)
         self.device = device
         self.ids = N.c_i64(ids)                      # dense input index -> external id
         self.n = int(self.ids.shape[0])
@@ -84,8 +98,10 @@ class FrozenGraph:
             d.chain_ptr, d.chain_member, d.chain_head, d.chain_tail = (a.ctypes.data for a in arrs)
         order = np.empty(self.n, np.int32)
         h = C.c_void_p()
+        _tick("host prep")
         N.check(N.lib().ks_graph_create(C.byref(d), device, C.byref(h), N.ptr(order)),
                 "ks_graph_create")
+        _tick("ks_graph_create")
         self._h = h
         del keep
         info = N.GraphInfo()
@@ -97,6 +113,7 @@ class FrozenGraph:
         self.row_of[order] = np.arange(self.n, dtype=np.int32)
         self.chained = bool(info.chained)
         self.n_ordered = int(info.n_ordered)
+        _tick("post")
 
     @property
     def handle(self):

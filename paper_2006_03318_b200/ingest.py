@@ -17,6 +17,9 @@ Python objects per task).
 
 from __future__ import annotations
 
+import os
+import sys
+import time
 from dataclasses import dataclass
 
 import numpy as np
@@ -78,9 +81,23 @@ def _trace_cols_struct(cols: TraceColumns, strict: bool, keep: list) -> N.TraceC
     return tc
 
 
+_T = [0.0]
+
+
+def _tick(what):
+    """DDSIM_INGEST_TIMING=1: wall time of the host-side steps."""
+    if not os.environ.get("DDSIM_INGEST_TIMING"):
+        return
+    t = time.perf_counter()
+    if what is not None:
+        print(f"[ingest_arrays] {what:12s} {1e3 * (t - _T[0]):8.3f} ms", file=sys.stderr)
+    _T[0] = t
+
+
 def ingest_arrays(cols: TraceColumns, strict: bool = False, check_overlaps: bool = False,
                   device: int | None = None) -> IngestResult:
     device = N.env_device() if device is None else device
+    _tick(None)
     N.require_device(device)
     keep: list = []
     tc = _trace_cols_struct(cols, strict, keep)
@@ -98,6 +115,7 @@ def ingest_arrays(cols: TraceColumns, strict: bool = False, check_overlaps: bool
     for k, a in bufs.items():
         setattr(out, k, a.ctypes.data)
     out.edge_cap = cap
+    _tick("host prep")
     rc = N.lib().ks_ingest(tc, device, 1 if check_overlaps else 0, out)
     if rc == N.KS_ERR_OVERLAP:
         a, b = int(out.bad_a), int(out.bad_b)
@@ -108,6 +126,7 @@ def ingest_arrays(cols: TraceColumns, strict: bool = False, check_overlaps: bool
         raise OrphanKernel(f"GPU task {int(out.bad_a)} correlation {int(cols.correlation[i])} "
                            "has no CPU launch")
     N.check(rc, "ks_ingest")
+    _tick("ks_ingest")
     m = int(out.n_edges)
     return IngestResult(cols=cols, edge_src=bufs["edge_src"][:m].copy(),
                         edge_dst=bufs["edge_dst"][:m].copy(),

@@ -330,3 +330,38 @@ def ingest_columns(n_records: int = 10_000_000, seed: int = 0, n_threads: int = 
     if with_markers:
         cols.markers = {k: np.concatenate(v) for k, v in mk.items()}
     return cols
+
+
+KERNEL_NAMES = ("sgemm_128x64_nn", "scudnn_winograd_fwd", "elementwise_add", "batchnorm_fwd",
+                "relu_fwd", "softmax_bwd")
+
+
+def ingest_document_columns(n_records: int = 10_000_000, seed: int = 0, **kw):
+    """Config 5 as a full trace document in columnar form (columnar.ColumnarTrace):
+    ``ingest_columns`` plus event names (launch / memcpy_dtoh / sync / dataload
+    APIs, cycled kernel names) and markers named ``layer_NNNN`` x phase, so
+    ``columnar.dump_trace_columns`` renders a valid kernsim JSON trace."""
+    from .columnar import ColumnarTrace
+
+    cols = ingest_columns(n_records, seed=seed, **kw)
+    names = ["cudaLaunchKernel", "memcpy_dtoh_async", "cudaStreamSynchronize",
+             "cudaDeviceSynchronize", "dataload_next_batch", "memcpy_async",
+             *KERNEL_NAMES]
+    k = cols.kind
+    name_id = np.zeros(cols.n, np.int32)
+    name_id[(k == 0) & (cols.is_dtoh == 1)] = 1
+    name_id[(k == 6) & (cols.sync_target >= 0)] = 2
+    name_id[(k == 6) & (cols.sync_target < 0)] = 3
+    name_id[k == 4] = 4
+    name_id[k == 3] = 5
+    gk = k == 2
+    name_id[gk] = 6 + (cols.id[gk] % len(KERNEL_NAMES)).astype(np.int32)
+    m = cols.markers
+    n_layers = int(m["tag"].max()) // 3 + 1 if m["tag"].size else 0
+    layers = [f"layer_{i:04d}" for i in range(n_layers)]
+    cols.names = None
+    return ColumnarTrace(cols=cols, name_id=name_id, names=names,
+                         size_bytes=np.full(cols.n, -1, np.int64), n_event_lanes=len(cols.lanes),
+                         m_lane=m["lane"].astype(np.int32), m_start=m["start"], m_end=m["end"],
+                         m_layer=(m["tag"] // 3).astype(np.int32),
+                         m_phase=(m["tag"] % 3).astype(np.uint8), layers=layers)
