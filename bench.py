@@ -233,6 +233,21 @@ def run_ours(args):
         elapsed_ms = float(t.item())
         dist.barrier()
     clk = clocks.stop() if clocks else None
+    # the single result collective of a sharded sweep: every rank's
+    # per-scenario makespan + lane busy gathered once over NCCL, outside the timed steps
+    gather = None
+    if ws > 1:
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        flat = torch.cat([ms, lb.reshape(-1)])
+        bufs = [torch.empty_like(flat) for _ in range(ws)]
+        dist.barrier()
+        g0.record(stream)
+        dist.all_gather(bufs, flat)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        assert torch.equal(bufs[rank], flat)
+        gather = {"collective": "all_gather (nccl)", "bytes_per_rank": flat.numel() * 8,
+                  "ms": g0.elapsed_time(g1)}
     updates_per_step = rows * S
     total = updates_per_step * args.steps * ws
     value = total / (elapsed_ms / 1e3)
@@ -301,10 +316,11 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": updates_per_step * BYTES_PER_UPDATE,
-                         "traffic": _ncu_traffic("maxplus_kernel")},
+                         "traffic": _ncu_traffic("ddsim_lanes_jit")},
             "cpu_baseline": cb,
             "e2e": e2e,
             "gpu_launches": launches,
+            "result_gather": gather,
             "kernel": kernel_name,
             "clocks": clk,
         }

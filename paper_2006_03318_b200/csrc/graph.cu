@@ -17,10 +17,15 @@
 #include <cstdio>
 #include <cstring>
 #include <deque>
+#include <chrono>
+#include <cstdio>
 #include <functional>
 #include <numeric>
 #include <queue>
 #include <string>
+#include <exception>
+#include <mutex>
+#include <thread>
 #include <vector>
 #include <cstdlib>
 
@@ -60,6 +65,55 @@ static T* dev_upload(const std::vector<T>& v) {
   CUDA_TRY(cudaMemcpy(p, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice));
   return p;
 }
+
+// Split [0, n) over the host cores (independent iterations only).
+template <class F>
+static void host_parallel_for(long long n, F f) {
+  unsigned hw = std::thread::hardware_concurrency();
+  long long K = std::max(1LL, std::min<long long>(hw ? hw : 1, n / 262144));
+  if (K <= 1) {
+    f(0LL, n);
+    return;
+  }
+  std::vector<std::thread> th;
+  const long long step = (n + K - 1) / K;
+  for (long long k = 0; k < K; ++k) {
+    const long long b = k * step, e = std::min(n, b + step);
+    if (b < e) th.emplace_back(f, b, e);
+  }
+  for (auto& t : th) t.join();
+}
+
+// Independent compile sections on their own threads (the CUDA device is
+// per-thread state: set it in each); the first exception is rethrown on join.
+struct ConcurrentSections {
+  int device;
+  std::vector<std::thread> th;
+  std::vector<std::exception_ptr> err;
+  std::mutex mu;
+  explicit ConcurrentSections(int dev) : device(dev) {}
+  template <class F>
+  void run(F f) {
+    th.emplace_back([this, f]() mutable {
+      try {
+        if (device >= 0 && !g_compile_only) cudaSetDevice(device);
+        f();
+      } catch (...) {
+        std::lock_guard<std::mutex> lk(mu);
+        err.push_back(std::current_exception());
+      }
+    });
+  }
+  void join() {
+    for (auto& t : th) t.join();
+    th.clear();
+    if (!err.empty()) std::rethrow_exception(err.front());
+  }
+  ~ConcurrentSections() {
+    for (auto& t : th)
+      if (t.joinable()) t.join();
+  }
+};
 
 constexpr int kSmemSlotsMax = 24;
 constexpr int kShortRange = 48;
@@ -164,7 +218,20 @@ static void radix_sort_u64(std::vector<unsigned long long>& a) {
   }
 }
 
+struct HostTimer {  // DDSIM_INGEST_TIMING=1: wall time of compile_graph's sections
+  bool on = std::getenv("DDSIM_INGEST_TIMING") != nullptr;
+  std::chrono::steady_clock::time_point t0 = std::chrono::steady_clock::now();
+  void mark(const char* what) {
+    if (!on) return;
+    auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "[compile_graph] %-13s %8.3f ms\n", what,
+                 std::chrono::duration<double, std::milli>(t1 - t0).count());
+    t0 = t1;
+  }
+};
+
 void compile_graph(const ks_graph_desc* d, ks_graph* g) {
+  HostTimer gt;
   const int n = d->n_tasks;
   const int L = d->n_lanes;
   if (n < 0 || L < 0) fail(KS_ERR_INVALID, "negative sizes");
@@ -195,18 +262,37 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     if (d->chain_ptr[c + 1] <= d->chain_ptr[c]) fail(KS_ERR_INVALID, "empty chain");
   }
 
+  gt.mark("chains");
   // ---- unique edges ----------------------------------------------------------
+  // sorted unique (u << 32 | v): counting sort by u, then each (short) out list by v
   std::vector<unsigned long long> keys(E);
-  for (long long k = 0; k < E; ++k)
-    keys[k] = ((unsigned long long)(unsigned)d->edge_src[k] << 32) | (unsigned)d->edge_dst[k];
-  radix_sort_u64(keys);
-  keys.erase(std::unique(keys.begin(), keys.end()), keys.end());
+  {
+    std::vector<long long> cnt((size_t)n + 1, 0);
+    for (long long k = 0; k < E; ++k) cnt[(size_t)d->edge_src[k] + 1]++;
+    for (int i = 0; i < n; ++i) cnt[(size_t)i + 1] += cnt[(size_t)i];
+    std::vector<long long> fill(cnt.begin(), cnt.end() - 1);
+    for (long long k = 0; k < E; ++k)
+      keys[(size_t)fill[(size_t)d->edge_src[k]]++] =
+          ((unsigned long long)(unsigned)d->edge_src[k] << 32) | (unsigned)d->edge_dst[k];
+    size_t o = 0;
+    for (int u = 0; u < n; ++u) {
+      auto b = keys.begin() + cnt[(size_t)u], e = keys.begin() + cnt[(size_t)u + 1];
+      if (e - b > 1) std::sort(b, e);
+      for (auto it = b; it != e; ++it)
+        if (it == b || *it != *(it - 1)) keys[o++] = *it;
+    }
+    keys.resize(o);
+  }
   g->n_edges_unique = (int)keys.size();
+  std::vector<int> optr(n + 1, 0);  // out-edge ranges of the sorted unique keys
+  for (unsigned long long k : keys) optr[(k >> 32) + 1]++;
+  for (int i = 0; i < n; ++i) optr[i + 1] += optr[i];
   auto has_edge = [&](int u, int v) {
     const unsigned long long k = ((unsigned long long)(unsigned)u << 32) | (unsigned)v;
-    return std::binary_search(keys.begin(), keys.end(), k);
+    return std::binary_search(keys.begin() + optr[u], keys.begin() + optr[u + 1], k);
   };
 
+  gt.mark("unique-edges");
   // ---- lane chaining check ---------------------------------------------------
   bool chained = d->lane_order_ptr != nullptr;
   std::vector<int> lane_succ(n, -1);
@@ -239,12 +325,15 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   g->chained = chained;
   g->n_chains = NC;
 
+  gt.mark("chain-check");
   // ---- contracted graph (chain -> one node) ---------------------------------
   const int NN = n + NC;
   auto X = [&](int t) { return chain_of[t] >= 0 ? n + chain_of[t] : t; };
   std::vector<unsigned long long> ckeys;
   ckeys.reserve(keys.size() + 2 * NC);
-  for (unsigned long long k : keys) {
+  if (NC == 0) ckeys = keys;  // no chain: the contracted graph is the unique graph
+  for (size_t q = 0; NC > 0 && q < keys.size(); ++q) {
+    const unsigned long long k = keys[q];
     const int u = (int)(k >> 32), v = (int)(k & 0xffffffffu);
     const int xu = X(u), xv = X(v);
     if (xu == xv) {
@@ -270,8 +359,10 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
       ckeys.push_back(((unsigned long long)(n + c) << 32) | (unsigned)t);
     }
   }
-  radix_sort_u64(ckeys);
-  ckeys.erase(std::unique(ckeys.begin(), ckeys.end()), ckeys.end());
+  if (NC > 0) {
+    radix_sort_u64(ckeys);
+    ckeys.erase(std::unique(ckeys.begin(), ckeys.end()), ckeys.end());
+  }
   std::vector<int> cptr(NN + 1, 0), cadj(ckeys.size()), cindeg(NN, 0);
   for (unsigned long long k : ckeys) {
     cptr[(k >> 32) + 1]++;
@@ -293,6 +384,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   }
   auto clane = [&](int x) { return x < n ? d->lane[x] : ch_lane[x - n]; };
 
+  gt.mark("contract");
   // ---- depth-first Kahn (LIFO frontier) --------------------------------------
   std::vector<int> corder;
   corder.reserve(NN);
@@ -326,6 +418,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   }
   const int R = (int)corder.size();  // records
 
+  gt.mark("toposort");
   // ---- frozen rows ----------------------------------------------------------
   g->order.clear();
   g->order.reserve(n);
@@ -360,6 +453,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   for (int r = 0; r < n; ++r) g->rank_row[r] = d->id_rank[g->order[r]];
   g->rows_are_records = (NC == 0);
 
+  gt.mark("rows");
   // ---- unique preds per task (for records) -----------------------------------
   std::vector<int> pptr(n + 1, 0), padj(keys.size());
   for (unsigned long long k : keys) pptr[(k & 0xffffffffu) + 1]++;
@@ -374,6 +468,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     if (t >= 0) tail_of[t] = c;
   }
 
+  gt.mark("preds");
   // ---- levels ------------------------------------------------------------------
   std::vector<int> clevel(NN, 0);
   {
@@ -399,6 +494,22 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     }
   }
 
+  gt.mark("levels");
+  // ---- the four builders below (general records, dense program, lane program,
+  // list-scheduler arrays) read only the shared graph above: run concurrently
+  std::vector<NodeRec> prog(R), members;
+  std::vector<int> extra;
+  std::vector<ChainDesc> chains(NC);
+  bool nonneg = true;
+  for (int i = 0; i < n && nonneg; ++i)
+    if (d->gap[i] < 0 || (d->ready_time && d->ready_time[i] < 0)) nonneg = false;
+  std::vector<int> ch_ptr(n + 1, 0), ch_adj(E), indeg(n, 0);
+  std::vector<int> lane_r(n), rank_r(n), prio_r(n);
+  std::vector<long long> dur_r(n), gap_r(n), ready_r(n);
+  std::vector<unsigned char> flags_r(n);
+  std::vector<unsigned> group_r(n);
+  ConcurrentSections sect(g->device);
+  sect.run([&] {
   // ---- value live ranges -------------------------------------------------------
   // values: task t (0..n-1) -> rel(t); chain tail value n + c.
   const int NV = n + NC;
@@ -412,11 +523,13 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   }
   auto rec_of_val = [&](int t) { return chain_of[t] >= 0 ? rec_of_chain[chain_of[t]] : rec_of_task[t]; };
   std::vector<int> last_use(NV, -1);
-  // inputs of each record
-  std::vector<std::vector<int>> rec_inputs(R);
+  // inputs of each record (flat CSR: rin_ptr / rin)
+  std::vector<int> rin_ptr(R + 1, 0), rin;
+  rin.reserve(keys.size() + 2 * (size_t)NC);
+  std::vector<int> in;
   for (int i = 0; i < R; ++i) {
     const int x = corder[i];
-    auto& in = rec_inputs[i];
+    in.clear();
     auto add_task_preds = [&](int t) {
       for (int k = pptr[t]; k < pptr[t + 1]; ++k) in.push_back(padj[k]);
     };
@@ -429,9 +542,13 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
       const int h = d->chain_head ? d->chain_head[c] : -1;
       if (h >= 0) in.push_back(h);
     }
-    std::sort(in.begin(), in.end());
-    in.erase(std::unique(in.begin(), in.end()), in.end());
+    if (in.size() > 1) {
+      std::sort(in.begin(), in.end());
+      in.erase(std::unique(in.begin(), in.end()), in.end());
+    }
     for (int v : in) last_use[v] = std::max(last_use[v], i);
+    rin.insert(rin.end(), in.begin(), in.end());
+    rin_ptr[i + 1] = (int)rin.size();
   }
 
   // ---- slot allocation (linear scan, allocate-then-free) ----------------------
@@ -470,8 +587,8 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
       for (int k = d->chain_ptr[c]; k < d->chain_ptr[c + 1]; ++k) alloc(d->chain_member[k], i);
       if (d->chain_tail && d->chain_tail[c] >= 0) alloc(n + c, i);
     }
-    for (int v : rec_inputs[i])
-      if (last_use[v] == i && slot[v] >= 0) {
+    for (int q = rin_ptr[i]; q < rin_ptr[i + 1]; ++q)
+      if (const int v = rin[q]; last_use[v] == i && slot[v] >= 0) {
         (in_glob[v] ? free_g : free_s).push(slot[v]);
       }
   }
@@ -481,25 +598,21 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   auto final_slot = [&](int v) { return slot[v] < 0 ? -1 : (in_glob[v] ? g->ksm + slot[v] : slot[v]); };
 
   // ---- records -----------------------------------------------------------------
-  std::vector<NodeRec> prog(R), members;
-  std::vector<int> extra;
-  std::vector<ChainDesc> chains(NC);
-  auto make_task_rec = [&](int t, std::vector<int> preds) {
+  auto make_task_rec = [&](int t, const std::vector<int>& preds) {
     NodeRec r;
     memset(&r, 0, sizeof(r));
     r.dur = d->duration[t];
     r.gap = d->gap[t];
     r.ready = d->ready_time ? d->ready_time[t] : 0;
     r.out_slot = final_slot(t);
-    std::vector<int> ps;
-    for (int v : preds) ps.push_back(final_slot(v));
-    r.pred0 = ps.size() > 0 ? ps[0] : -1;
-    r.pred1 = ps.size() > 1 ? ps[1] : -1;
+    const size_t np = preds.size();
+    r.pred0 = np > 0 ? final_slot(preds[0]) : -1;
+    r.pred1 = np > 1 ? final_slot(preds[1]) : -1;
     r.extra_off = 0;
-    r.nextra = ps.size() > 2 ? (int)ps.size() - 2 : 0;
+    r.nextra = np > 2 ? (int)np - 2 : 0;
     if (r.nextra) {
       r.extra_off = (int)extra.size();
-      for (size_t k = 2; k < ps.size(); ++k) extra.push_back(ps[k]);
+      for (size_t k = 2; k < np; ++k) extra.push_back(final_slot(preds[k]));
     }
     r.group = d->group ? d->group[t] : 0u;
     r.ovr_row = -1;
@@ -509,10 +622,11 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     return r;
   };
   int perm_off = 0;
+  std::vector<int> preds;
   for (int i = 0; i < R; ++i) {
     const int x = corder[i];
     if (x < n) {
-      std::vector<int> preds;
+      preds.clear();
       for (int k = pptr[x]; k < pptr[x + 1]; ++k) preds.push_back(padj[k]);
       if (tail_of[x] >= 0) preds.push_back(n + tail_of[x]);
       prog[i] = make_task_rec(x, preds);
@@ -538,7 +652,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
       perm_off += ch.B;
       for (int k = d->chain_ptr[c]; k < d->chain_ptr[c + 1]; ++k) {
         const int m = d->chain_member[k];
-        std::vector<int> preds;
+        preds.clear();
         for (int q = pptr[m]; q < pptr[m + 1]; ++q) preds.push_back(padj[q]);
         members.push_back(make_task_rec(m, preds));
       }
@@ -547,10 +661,9 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   g->perm_ld = perm_off;
   g->n_rec = R;
 
+  });
+  sect.run([&] {
   // ---- dense program: register forwarding for the two previous records ----
-  bool nonneg = true;
-  for (int i = 0; i < n && nonneg; ++i)
-    if (d->gap[i] < 0 || (d->ready_time && d->ready_time[i] < 0)) nonneg = false;
   if (NC == 0 && L <= 127 && nonneg) {
     std::vector<int> pos(n, -1);
     for (int i = 0; i < R; ++i) pos[corder[i]] = i;
@@ -566,7 +679,16 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     std::vector<char> dglob(n, 0);
     std::priority_queue<int, std::vector<int>, std::greater<int>> fs, fg;
     int ns = 0, ngl = 0;
-    std::vector<std::vector<int>> frees_at(R);
+    std::vector<int> fa_ptr(R + 1, 0), fa;  // values freed after record i (CSR)
+    for (int i = 0; i < R; ++i)
+      if (far_use[corder[i]] >= 0) fa_ptr[far_use[corder[i]] + 1]++;
+    for (int i = 0; i < R; ++i) fa_ptr[i + 1] += fa_ptr[i];
+    fa.resize(fa_ptr[R]);
+    {
+      std::vector<int> fill(fa_ptr.begin(), fa_ptr.end() - 1);
+      for (int i = 0; i < R; ++i)
+        if (far_use[corder[i]] >= 0) fa[fill[far_use[corder[i]]]++] = corder[i];
+    }
     for (int i = 0; i < R; ++i) {
       const int v = corder[i];
       if (far_use[v] >= 0) {
@@ -585,9 +707,8 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
             dslot[v] = ngl++;
           }
         }
-        frees_at[far_use[v]].push_back(v);
       }
-      for (int u : frees_at[i]) (dglob[u] ? fg : fs).push(dslot[u]);
+      for (int q = fa_ptr[i]; q < fa_ptr[i + 1]; ++q) (dglob[fa[q]] ? fg : fs).push(dslot[fa[q]]);
     }
     g->dksm = ns;
     g->dkglob = ngl;
@@ -656,6 +777,8 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     }
   }
 
+  });
+  sect.run([&] {
   // ---- lane-register program (maxplus_lanes.cu) ------------------------------
   if (NC == 0 && chained && L <= 4 && nonneg && R == n) {
     std::vector<int> pos(n, -1);
@@ -686,7 +809,16 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     std::vector<char> lglob(n, 0);
     std::priority_queue<int, std::vector<int>, std::greater<int>> fs, fg;
     int ns = 0, ngl = 0;
-    std::vector<std::vector<int>> frees_at(R);
+    std::vector<int> fa_ptr(R + 1, 0), fa;  // values freed after record i (CSR)
+    for (int i = 0; i < R; ++i)
+      if (far_use[corder[i]] >= 0) fa_ptr[far_use[corder[i]] + 1]++;
+    for (int i = 0; i < R; ++i) fa_ptr[i + 1] += fa_ptr[i];
+    fa.resize(fa_ptr[R]);
+    {
+      std::vector<int> fill(fa_ptr.begin(), fa_ptr.end() - 1);
+      for (int i = 0; i < R; ++i)
+        if (far_use[corder[i]] >= 0) fa[fill[far_use[corder[i]]]++] = corder[i];
+    }
     for (int i = 0; i < R; ++i) {
       const int v = corder[i];
       if (far_use[v] >= 0) {
@@ -705,9 +837,8 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
             lslot[v] = ngl++;
           }
         }
-        frees_at[far_use[v]].push_back(v);
       }
-      for (int u : frees_at[i]) (lglob[u] ? fg : fs).push(lslot[u]);
+      for (int q = fa_ptr[i]; q < fa_ptr[i + 1]; ++q) (lglob[fa[q]] ? fg : fs).push(lslot[fa[q]]);
     }
     std::vector<int> lane_last(L, -1);
     for (int i = 0; i < R; ++i) lane_last[d->lane[corder[i]]] = i;
@@ -777,23 +908,27 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     }
   }
 
+  });
+  sect.run([&] {
   // ---- list-scheduler arrays (frozen rows, multiset edges) -------------------
-  std::vector<int> ch_ptr(n + 1, 0), ch_adj(E), indeg(n, 0);
+  std::vector<int> esr(E), edr(E);  // edge endpoints as frozen rows
+  host_parallel_for(E, [&](long long b, long long e) {
+    for (long long k = b; k < e; ++k) {
+      esr[k] = g->row_of[d->edge_src[k]];
+      edr[k] = g->row_of[d->edge_dst[k]];
+    }
+  });
   for (long long k = 0; k < E; ++k) {
-    ch_ptr[g->row_of[d->edge_src[k]] + 1]++;
-    indeg[g->row_of[d->edge_dst[k]]]++;
+    ch_ptr[esr[k] + 1]++;
+    indeg[edr[k]]++;
   }
   for (int i = 0; i < n; ++i) ch_ptr[i + 1] += ch_ptr[i];
   {
     std::vector<int> fill(ch_ptr.begin(), ch_ptr.end() - 1);
-    for (long long k = 0; k < E; ++k)
-      ch_adj[fill[g->row_of[d->edge_src[k]]]++] = g->row_of[d->edge_dst[k]];
+    for (long long k = 0; k < E; ++k) ch_adj[fill[esr[k]]++] = edr[k];
   }
-  std::vector<int> lane_r(n), rank_r(n), prio_r(n);
-  std::vector<long long> dur_r(n), gap_r(n), ready_r(n);
-  std::vector<unsigned char> flags_r(n);
-  std::vector<unsigned> group_r(n);
-  for (int r = 0; r < n; ++r) {
+  host_parallel_for(n, [&](long long b, long long e) {
+  for (int r = (int)b; r < (int)e; ++r) {
     const int t = g->order[r];
     lane_r[r] = d->lane[t];
     rank_r[r] = d->id_rank[t];
@@ -804,7 +939,11 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     flags_r[r] = d->flags ? d->flags[t] : 0;
     group_r[r] = d->group ? d->group[t] : 0u;
   }
+  });
 
+  });
+  sect.join();
+  gt.mark("programs");
   // ---- upload -----------------------------------------------------------------
   g->d_prog = dev_upload(prog);
   g->d_extra = dev_upload(extra);
@@ -822,6 +961,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   g->d_flags = dev_upload(flags_r);
   g->d_group = dev_upload(group_r);
 
+  gt.mark("upload");
   // ---- breakdown geometry -------------------------------------------------------
   for (int i = 0; i < n; ++i)
     if (d->gap[i] < 0) g->gap_nonneg = false;

@@ -671,9 +671,9 @@ extern "C" int ks_ingest(const ks_trace_cols* tc, int device, int check_overlaps
   } catch (...) {
     rc = KS_ERR_INVALID;
   }
+  T_.mark("release");
   cudaStreamSynchronize(st);
   cudaStreamDestroy(st);
-  T_.mark("release");
   if (rc != KS_OK) cudaGetLastError();  // do not leave a non-sticky error for later calls
   return rc;
 }

@@ -66,8 +66,11 @@ class FrozenGraph:
         self.edge_dst = N.c_i32(edge_dst)
         self.task_layers = task_layers    # per input task: layer name or None
         self.dataload = dataload          # per input task: TaskKind.DATA_LOAD
-        rank = np.empty(self.n, np.int32)
-        rank[np.argsort(self.ids, kind="stable")] = np.arange(self.n, dtype=np.int32)
+        if self.n < 2 or bool(np.all(self.ids[1:] > self.ids[:-1])):
+            rank = np.arange(self.n, dtype=np.int32)  # ids already ascending (document order)
+        else:
+            rank = np.empty(self.n, np.int32)
+            rank[np.argsort(self.ids, kind="stable")] = np.arange(self.n, dtype=np.int32)
         self.id_rank = rank
         self.chains = chains or []
         keep = []
