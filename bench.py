@@ -262,7 +262,8 @@ def run_ours(args):
     # ---- e2e through the host-buffer C-ABI (H2D + D2H inside the timed region)
     e2e = None
     if not args.no_e2e:
-        S_e = S
+        # pinned host buffers are (4 + 8) B per update: cap them at ~80 GB per node
+        S_e = S if ws == 1 else max(1024, (S // ws) // 32 * 32)
         h_dense = torch.empty((rows, S_e), dtype=torch.int32, pin_memory=True)
         h_dense.copy_(dense[:, :S_e])
         h_start = torch.empty((rows, S_e), dtype=torch.int64, pin_memory=True)
