@@ -80,7 +80,8 @@ class Clocks:
         self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
         q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,"
+             "clocks.mem,temperature.memory,temperature.gpu")
         try:
             self.p = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}",
                                        "--format=csv,noheader,nounits", "-lms", "200"],
@@ -103,9 +104,21 @@ class Clocks:
                 if len(r) > 5 + k and "Active" in r[5 + k] and "Not" not in r[5 + k]:
                     reasons.add(nm)
         os.unlink(self.f.name)
+
+        def col(k):
+            out = []
+            for r in rows:
+                try:
+                    out.append(float(r[k]))
+                except (IndexError, ValueError):
+                    pass
+            return out
+        mem, tmem, tgpu = col(9), col(10), col(11)
         return {"sm_mhz": statistics.median(sm) if sm else None,
                 "sm_max_mhz": max(mx) if mx else None, "reasons": sorted(reasons),
-                "samples": len(rows)}
+                "samples": len(rows), "mem_mhz": statistics.median(mem) if mem else None,
+                "hbm_temp_c_max": max(tmem) if tmem else None,
+                "gpu_temp_c_max": max(tgpu) if tgpu else None}
 
 
 def build_workload(device: int):
@@ -259,6 +272,21 @@ def run_ours(args):
     # done in tests; here only assert the makespan is positive
     assert int(ms[0].item()) > 0
 
+    # speed of light of this exact traffic pattern: a library int32 -> int64
+    # widening copy over the same matrices (26 GB read + 52 GB write, no compute)
+    def probe():
+        N.check(N.lib().ks_probe_widen(dense.data_ptr(), start.data_ptr(), rows * S,
+                                       stream.cuda_stream), "ks_probe_widen")
+    p0, p1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    probe()
+    torch.cuda.synchronize()
+    p0.record(stream)
+    for _ in range(3):
+        probe()
+    p1.record(stream)
+    torch.cuda.synchronize()
+    pattern_gbs = updates_per_step * BYTES_PER_UPDATE / (p0.elapsed_time(p1) / 3 / 1e3) / 1e9
+
     # ---- e2e through the host-buffer C-ABI (H2D + D2H inside the timed region)
     e2e = None
     if not args.no_e2e:
@@ -317,7 +345,12 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": updates_per_step * BYTES_PER_UPDATE,
-                         "traffic": _ncu_traffic("ddsim_lanes_jit")},
+                         "traffic": _ncu_traffic("ddsim_lanes_jit"),
+                         "pattern_copy_gbs": pattern_gbs,
+                         "pattern_frac": achieved / pattern_gbs,
+                         "pattern": "ks_probe_widen: int32 -> int64 stream over the same "
+                                    "[rows][S] matrices (4 B read + 8 B write per update, "
+                                    "no recurrence)"},
             "cpu_baseline": cb,
             "e2e": e2e,
             "gpu_launches": launches,

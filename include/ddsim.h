@@ -400,6 +400,10 @@ int64_t ks_launch_count(void);
 const char* ks_version(void);
 /* Diagnostics of the per-graph NVRTC specialisation (status + compile log). */
 const char* ks_jit_log(void);
+/* Traffic-pattern probe (bench.py): dst[i] = src[i] for n int32 -> int64 on
+ * the device, asynchronously on `stream` -- the lanes kernel's compulsory HBM
+ * traffic without the recurrence.  16-byte aligned pointers. */
+int ks_probe_widen(const int32_t* src, int64_t* dst, int64_t n, void* stream);
 
 #ifdef __cplusplus
 }

@@ -174,6 +174,7 @@ _SIGNATURES = [
     ("ks_launch_count", C.c_int64, []),
     ("ks_version", C.c_char_p, []),
     ("ks_jit_log", C.c_char_p, []),
+    ("ks_probe_widen", C.c_int, [P, P, C.c_int64, P]),
 ]
 EXPORTED_SYMBOLS = [s[0] for s in _SIGNATURES]
 

@@ -1,0 +1,50 @@
+// probe.cu -- traffic-pattern speed of light for the config-4 kernel.
+//
+// ks_probe_widen streams n int32 in and n int64 out (sign-extended): exactly
+// the compulsory HBM traffic of the lanes kernel (4 B duration read + 8 B
+// start write per (task, scenario) update) with no recurrence, so bench.py can
+// report how close the simulator gets to what this read/write mix allows on
+// the device, next to the copy peak in MEASURED_PEAKS.json.
+#include "ddsim_internal.h"
+
+namespace ddsim {
+
+__global__ void __launch_bounds__(256) probe_widen_kernel(const int4* __restrict__ src,
+                                                          longlong2* __restrict__ dst,
+                                                          long long n4) {
+  const long long stride = (long long)gridDim.x * blockDim.x;
+  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += stride) {
+    const int4 v = __ldcs(src + i);
+    __stcs(dst + 2 * i, make_longlong2(v.x, v.y));
+    __stcs(dst + 2 * i + 1, make_longlong2(v.z, v.w));
+  }
+}
+
+__global__ void probe_widen_tail(const int* src, long long* dst, long long from, long long n) {
+  const long long i = from + blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  if (i < n) dst[i] = src[i];
+}
+
+}  // namespace ddsim
+
+extern "C" int ks_probe_widen(const int32_t* src, int64_t* dst, int64_t n, void* stream) {
+  using namespace ddsim;
+  if (n < 0 || (n > 0 && (!src || !dst))) return KS_ERR_INVALID;
+  if ((reinterpret_cast<uintptr_t>(src) | reinterpret_cast<uintptr_t>(dst)) % 16 != 0)
+    return KS_ERR_INVALID;
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  int dev = 0, nsm = 148;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  const long long n4 = n / 4;
+  if (n4 > 0) {
+    probe_widen_kernel<<<nsm * 8, 256, 0, st>>>(reinterpret_cast<const int4*>(src),
+                                               reinterpret_cast<longlong2*>(dst), n4);
+    note_launch();
+  }
+  if (n % 4) {
+    probe_widen_tail<<<1, 4, 0, st>>>(src, reinterpret_cast<long long*>(dst), n4 * 4, n);
+    note_launch();
+  }
+  return cudaGetLastError() == cudaSuccess ? KS_OK : KS_ERR_CUDA;
+}

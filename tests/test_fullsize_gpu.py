@@ -1,0 +1,100 @@
+"""BASELINE configs at their full graph sizes (the bench's own workloads),
+spot-checked scenario by scenario against the C oracle (Alg. 1, sim.py:89-142)
+plus size-independent properties over every scenario:
+
+* config 4: 100k-task GPT-style graph, 2,048 jitter scenarios (bench uses 65,536);
+  exact for sampled scenarios; for all: makespan >= every lane busy total and
+  makespan == max over rows of start + duration (gap excluded, sim.py:125);
+* config 2: 400 per-layer Shrink scenarios on the 30k-task BERT-like graph;
+  shrinking never lengthens a lane-chained schedule (monotone max-plus);
+* config 3: 4,000 bandwidth x workers x bucket-order scenarios; workers == 1
+  equals the baseline (scenarios.py:197-199) and makespan is non-increasing in
+  bandwidth for a fixed worker count and bucket order.
+"""
+
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+from oracle import OracleGraph
+from paper_2006_03318_b200 import workloads as W
+from paper_2006_03318_b200.batch import (ScenarioTable, compile_scale_sweep, distributed_sweep,
+                                         simulate_batch)
+from paper_2006_03318_b200.frozen import FrozenGraph
+from paper_2006_03318_b200.scenarios import whatif_distributed
+from paper_2006_03318_b200.transform import (GPU_TASKS, And, ByLayer, TransformPipeline,
+                                             apply_pipeline, scale_durations)
+
+pytestmark = pytest.mark.gpu
+
+
+def test_config4_full_graph():
+    w = W.gpt_trace(seed=0, n_tasks=100_000)
+    fz = FrozenGraph.from_graph(w.graph)
+    assert fz.chained and fz.n >= 99_000
+    S = 2048
+    base = fz.duration[fz.order]
+    rng = np.random.default_rng(11)
+    k = rng.integers(900, 1101, size=(fz.n, S))
+    dense = ((2 * base[:, None] * k + 1000) // 2000).astype(np.int32)
+    res = simulate_batch(fz, ScenarioTable(n_scenarios=S, dense=dense))
+    og = OracleGraph.from_graph(w.graph)
+    for s in (0, 777, S - 1):
+        d = np.empty(fz.n, np.int64)
+        d[fz.order] = dense[:, s]
+        st, ms, lb, _ = og.simulate("default", dur=d)
+        assert res.makespan[s] == ms
+        assert res.start_of(s) == st
+    # properties over every scenario
+    fin = res.start + dense.astype(np.int64)
+    assert np.array_equal(res.makespan, fin.max(axis=0))
+    assert np.all(res.makespan[:, None] >= res.lane_busy)
+    assert np.array_equal(res.lane_busy.sum(axis=1), dense.astype(np.int64).sum(axis=0))
+
+
+def test_config2_full_sweep():
+    w = W.bert_trace(buckets_mb=None)
+    g = w.graph
+    scen = [[(And([GPU_TASKS, ByLayer(l)]), "1/2")] for l in w.layers]
+    group_of, ptr, steps = compile_scale_sweep(g, scen + [[]])
+    fz = FrozenGraph.from_graph(g, group_of=group_of)
+    S = len(scen) + 1
+    res = simulate_batch(fz, ScenarioTable(n_scenarios=S, scale_ptr=ptr, scale=steps))
+    base = int(res.makespan[-1])
+    assert np.all(res.makespan[:-1] <= base)          # shrinking never hurts
+    for s in (0, len(scen) // 2, len(scen) - 1):
+        h = g.copy()
+        for sel, f in scen[s]:
+            scale_durations(h, sel, Fraction(f))
+        st, ms, _lb, _ = OracleGraph.from_graph(h).simulate("default")
+        assert res.makespan[s] == ms and res.start_of(s) == st
+
+
+def test_config3_full_sweep():
+    w = W.bert_trace(buckets_mb=25.0)
+    g = w.graph
+    buckets = w.trace.gradient_buckets
+    B = len([b for b in buckets.buckets() if buckets.layers_of_bucket(b)])
+    bws = (1, 5, 10, 25, 50, 100, 200, 400, 800, 1600)
+    workers = (1, 2, 4, 8, 16, 32, 64, 128)
+    rng = np.random.default_rng(0)
+    orders = [rng.permutation(B) for _ in range(50)]
+    configs, perms = [], []
+    for o in orders:
+        for nw in workers:
+            for bw in bws:
+                configs.append({"bandwidth_gbps": bw, "workers": nw})
+                perms.append(o)
+    sw = distributed_sweep(g, buckets, configs, np.array(perms, np.int16))
+    res = simulate_batch(sw.frozen, sw.table)
+    ms = res.makespan.reshape(len(orders), len(workers), len(bws))
+    baseline = OracleGraph.from_graph(g).simulate("default")[1]
+    assert np.all(ms[:, 0, :] == baseline)              # one worker: no allreduce inserted
+    assert np.all(np.diff(ms, axis=2) <= 0)             # more bandwidth never hurts
+    for s in (1, 1234, len(configs) - 1):
+        pipe = whatif_distributed(g, buckets=buckets, **configs[s])
+        steps = [pipe.steps[k] for k in perms[s]] if pipe.steps else []
+        h = apply_pipeline(g, TransformPipeline(steps=steps))
+        st, m, _lb, _ = OracleGraph.from_graph(h).simulate("default")
+        assert res.makespan[s] == m and res.start_of(s) == st

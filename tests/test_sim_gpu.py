@@ -196,3 +196,25 @@ def test_batch_dense_negative_durations_take_exact_path(golden):
         d[fz.order] = dense[:, s]
         st, ms, lb, _ = og.simulate("default", dur=d)
         assert res.makespan[s] == ms and res.start_of(s) == st
+
+
+def test_batch_dense_int32_durations_with_int64_sums(golden):
+    """int32 durations whose sums pass 2^31: start times are int64 (no
+    wrap-around anywhere on the int32-input path); results match Alg. 1."""
+    g = _genspec_graph(golden, "gpu_bound")
+    fz = FrozenGraph.from_graph(g)
+    assert fz.chained
+    S = 128
+    rng = np.random.default_rng(9)
+    dense = rng.integers(0, 2**31 - 1, size=(fz.n, S)).astype(np.int32)
+    dense[:, : S // 2] //= 1 << 12          # half the scenarios stay small (fast path result)
+    res = simulate_batch(fz, ScenarioTable(n_scenarios=S, dense=dense))
+    og = OracleGraph.from_graph(g)
+    assert int(res.makespan.max()) > 2**31
+    for s in (0, 5, S // 2 - 1, S // 2, S - 1):
+        d = np.empty(fz.n, np.int64)
+        d[fz.order] = dense[:, s]
+        st, ms, lb, _ = og.simulate("default", dur=d)
+        assert res.makespan[s] == ms and res.start_of(s) == st
+        assert {str(k2): v for k2, v in res.lane_busy_of(s).items()} == \
+            {str(k2): v for k2, v in lb.items()}
