@@ -94,8 +94,9 @@ void init_locked() {
               (g_drv.ok ? "ok" : "missing entry points");
 }
 
-std::string make_source(const std::vector<int>& codes, int dk, int V) {
+std::string make_source(const std::vector<int>& codes, int dk, int V, bool dyn) {
   std::string disp = "#define DDSIM_DISPATCH(h) ";
+  if (dyn) disp += "hstep_dyn<V>(S, h, d0, d1, gap, sp, ld, store); if (0) ";
   for (size_t i = 0; i < codes.size(); ++i) {
     const int c = codes[i];
     disp += (i ? "else if (h == " : "if (h == ") + std::to_string(c) + "u) hstep<" +
@@ -124,8 +125,9 @@ std::string make_source(const std::vector<int>& codes, int dk, int V) {
   return src;
 }
 
-CUfunction get_function(const std::vector<int>& codes, int dk, int V, int device) {
-  std::string key = std::to_string(device) + ":" + std::to_string(dk) + ":" + std::to_string(V) + ":";
+CUfunction get_function(const std::vector<int>& codes, int dk, int V, bool dyn, int device) {
+  std::string key = std::to_string(device) + ":" + std::to_string(dk) + ":" + std::to_string(V) +
+                    (dyn ? ":dyn:" : ":");
   if (const char* u = getenv("DDSIM_JIT_UNROLL")) key += std::string("u") + u + ":";
   if (const char* b = getenv("DDSIM_LANES_BODY")) key += std::string("b") + b + ":";
   for (int c : codes) key += std::to_string(c) + ",";
@@ -134,7 +136,7 @@ CUfunction get_function(const std::vector<int>& codes, int dk, int V, int device
   if (!g_nv.ok || !g_drv.ok) return nullptr;
   auto it = g_cache.find(key);
   if (it != g_cache.end()) return it->second;
-  const std::string src = make_source(codes, dk, V);
+  const std::string src = make_source(codes, dk, V, dyn);
   nvrtcProgram_t prog = nullptr;
   CUfunction fn = nullptr;
   if (g_nv.create(&prog, src.c_str(), "ddsim_lanes_jit.cu", 0, nullptr, nullptr) == 0) {
@@ -185,7 +187,12 @@ cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const void* tmap128, i
   }
   int dev = 0;
   cudaGetDevice(&dev);
-  CUfunction fn = get_function(codes, dkind, V, dev);
+  // latency-bound launches (fewer CTAs than SMs) take the branch-free handler
+  bool dyn = grid < 148;
+  int nsm = 148;
+  if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) dyn = grid < nsm;
+  if (const char* e = getenv("DDSIM_LANES_DYN")) dyn = atoi(e) != 0;
+  CUfunction fn = get_function(codes, dkind, V, dyn, dev);
   if (!fn) return cudaErrorNotSupported;
   const CUresult ar = g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
   if (ar != CUDA_SUCCESS) {

@@ -119,6 +119,44 @@ __device__ __forceinline__ void hstep(St<V>& S, long long d0, long long d1, long
   }
 }
 
+// Branch-free handler for latency-bound launches (few scenarios, so few warps
+// per SM): own lane and predecessor-lane mask are data, not code, so a record
+// costs a balanced max tree + add + predicated write-back instead of a chain of
+// compare-and-branch through the handler if-chain.  All values are >= 0 on
+// this path (device-checked), so 0 is the identity of max.
+template <int V>
+__device__ __forceinline__ void hstep_dyn(St<V>& S, unsigned h, long long d0, long long d1,
+                                          long long gap, long long*& sp, long long ld,
+                                          bool store) {
+  const unsigned own = h & 3u;
+  const unsigned m = ((h >> 2) & 31u) | (1u << own);
+  long long a[NLANE + 1], b[NLANE + 1];
+#pragma unroll
+  for (int l = 0; l <= NLANE; ++l) {
+    a[l] = (m >> l) & 1u ? S.lv[l][0] : 0;
+    b[l] = (m >> l) & 1u ? S.lv[l][V - 1] : 0;
+  }
+  long long x = lmax(lmax(lmax(a[0], a[1]), lmax(a[2], a[3])), a[4]);
+  long long y = lmax(lmax(lmax(b[0], b[1]), lmax(b[2], b[3])), b[4]);
+  if (store) {
+    __stcs(sp, x);
+    if (V == 2) __stcs(sp + 1, y);
+    sp += ld;
+  }
+  x += d0 + gap;
+  y += d1 + gap;
+#pragma unroll
+  for (int l = 0; l < NLANE; ++l) {
+    const bool mine = own == (unsigned)l;
+    S.lv[l][0] = mine ? x : S.lv[l][0];
+    S.lb[l][0] += mine ? d0 : 0;
+    if (V == 2) {
+      S.lv[l][V - 1] = mine ? y : S.lv[l][V - 1];
+      S.lb[l][V - 1] += mine ? d1 : 0;
+    }
+  }
+}
+
 template <int V>
 __device__ __forceinline__ long long own_get(const St<V>& S, int own, int i) {
   switch (own) {

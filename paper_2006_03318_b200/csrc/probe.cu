@@ -9,14 +9,24 @@
 
 namespace ddsim {
 
-__global__ void __launch_bounds__(256) probe_widen_kernel(const int4* __restrict__ src,
+// thread t of a warp reads int2 t (8 B) and writes longlong2 t (16 B): the
+// 256 B in / 512 B out per warp-step shape of the lanes kernel's V = 2 tiles;
+// four independent steps in flight per thread.
+__global__ void __launch_bounds__(256) probe_widen_kernel(const int2* __restrict__ src,
                                                           longlong2* __restrict__ dst,
-                                                          long long n4) {
+                                                          long long n2) {
   const long long stride = (long long)gridDim.x * blockDim.x;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < n4; i += stride) {
-    const int4 v = __ldcs(src + i);
-    __stcs(dst + 2 * i, make_longlong2(v.x, v.y));
-    __stcs(dst + 2 * i + 1, make_longlong2(v.z, v.w));
+  long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x;
+  for (; i + 3 * stride < n2; i += 4 * stride) {
+    int2 v[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) v[k] = __ldcs(src + i + k * stride);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) __stcs(dst + i + k * stride, make_longlong2(v[k].x, v[k].y));
+  }
+  for (; i < n2; i += stride) {
+    const int2 v = __ldcs(src + i);
+    __stcs(dst + i, make_longlong2(v.x, v.y));
   }
 }
 
@@ -36,14 +46,14 @@ extern "C" int ks_probe_widen(const int32_t* src, int64_t* dst, int64_t n, void*
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const long long n4 = n / 4;
-  if (n4 > 0) {
-    probe_widen_kernel<<<nsm * 8, 256, 0, st>>>(reinterpret_cast<const int4*>(src),
-                                               reinterpret_cast<longlong2*>(dst), n4);
+  const long long n2 = n / 2;
+  if (n2 > 0) {
+    probe_widen_kernel<<<nsm * 8, 256, 0, st>>>(reinterpret_cast<const int2*>(src),
+                                               reinterpret_cast<longlong2*>(dst), n2);
     note_launch();
   }
-  if (n % 4) {
-    probe_widen_tail<<<1, 4, 0, st>>>(src, reinterpret_cast<long long*>(dst), n4 * 4, n);
+  if (n % 2) {
+    probe_widen_tail<<<1, 1, 0, st>>>(src, reinterpret_cast<long long*>(dst), n2 * 2, n);
     note_launch();
   }
   return cudaGetLastError() == cudaSuccess ? KS_OK : KS_ERR_CUDA;
