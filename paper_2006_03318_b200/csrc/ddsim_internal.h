@@ -84,8 +84,24 @@ struct alignas(16) LaneRec {
 static_assert(sizeof(LaneRec) == 16, "LaneRec must be 16 bytes");
 enum {
   LREC_S0 = 1, LREC_S1 = 2, LREC_SIDE = 4, LREC_MS = 8, LREC_OUT_SMEM = 16, LREC_OUT_GLOBAL = 32,
-  LREC_PRE = 7, LREC_POST = 56
+  LREC_CHAIN = 64,  // permutable chain (s0 = chain id): its members in the scenario's order
+  LREC_NOP = 128,   // row of a chain member after the chain record (nothing to do)
+  LREC_PRE = 7 | 64 | 128, LREC_POST = 56
 };
+
+// Permutable chain on the lanes path: members mem_off .. mem_off+B-1, member k
+// on frozen row (chain record's row) + k; the scenario order is
+// perm[s * perm_ld + perm_off + q].
+struct LaneChainDev {
+  int lane, B, mem_off, perm_off;
+};
+struct LaneMemberDev {
+  long long gap;
+  int pred_off, npred;   // predecessor slot codes lpreds[pred_off ..] (< ksm smem, else global)
+  int out;               // slot code receiving the member's rel, -1 = none
+  int pad;
+};
+static_assert(sizeof(LaneMemberDev) == 24, "LaneMemberDev layout");
 
 struct LaneParams {
   const LaneRec* prog;
@@ -104,6 +120,15 @@ struct LaneParams {
   long long* makespan;
   long long* lane_busy;
   int* neg_flag;
+  // permutable chains (null when the graph has none)
+  const LaneChainDev* chains;
+  const LaneMemberDev* members;
+  const int* preds;
+  const short* perm;          // [S][perm_ld] or null (identity order)
+  const unsigned char* present;  // [S][n_chains] or null (all present)
+  const int* dense32;         // int32 durations (chain members read them directly)
+  int perm_ld;
+  int n_chains;
 };
 
 struct ChainDesc {

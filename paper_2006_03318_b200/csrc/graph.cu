@@ -140,12 +140,16 @@ struct ks_graph {
   std::vector<int> rank_row;     // id rank per frozen row
   // lane-register program (chained, <= 4 lanes, no chains)
   bool has_lanes = false;
+  int ln_rec = 0;          // lanes records (= frozen rows)
   int lksm = 0, lkglob = 0;
   std::vector<int> lane_codes;  // handler codes in decreasing frequency
   LaneRec* d_lprog = nullptr;
   int* d_lside_off = nullptr;
   int* d_lside_slots = nullptr;
   long long* d_lside_ready = nullptr;
+  LaneChainDev* d_lchains = nullptr;    // permutable chains on the lanes path
+  LaneMemberDev* d_lmembers = nullptr;
+  int* d_lpreds = nullptr;
   // dense-duration program (no chains, <= 255 lanes)
   bool has_dense = false;
   int dksm = 0, dkglob = 0;
@@ -780,49 +784,85 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   });
   sect.run([&] {
   // ---- lane-register program (maxplus_lanes.cu) ------------------------------
-  if (NC == 0 && chained && L <= 4 && nonneg && R == n) {
-    std::vector<int> pos(n, -1);
-    for (int i = 0; i < R; ++i) pos[corder[i]] = i;
-    // which predecessor reads are lane heads at read time?
-    std::vector<int> head(L, -1);
-    std::vector<int> far_use(n, -1);      // last slot read of each value
-    std::vector<unsigned> hmask(R, 0);
-    std::vector<std::vector<int>> slot_preds(R);
+  // One emitted record per frozen row: a task, or for a permutable chain a
+  // chain record on its first member row followed by B-1 no-op rows (so the
+  // duration tiles of 16 rows stay aligned with 16 records).  Chain members
+  // read all their predecessors from slots and publish their values to slots;
+  // the chain's last value becomes the lane head of its lane (the tail task
+  // reads it as its own lane).
+  if (chained && L <= 4 && nonneg && g->n_ordered == n && NC < 32768) {
+    const int RE = n;  // emitted records == frozen rows
+    std::vector<int> ekind(RE, 0), eid(RE, -1);  // 0 task, 1 chain (eid = chain), 2 no-op
     for (int i = 0; i < R; ++i) {
-      const int v = corder[i];
-      const int l = d->lane[v];
-      unsigned mask = 0;
-      for (int k = pptr[v]; k < pptr[v + 1]; ++k) {
-        const int u = padj[k];
-        const int m = d->lane[u];
-        if (head[m] == u) {
-          if (m != l) mask |= 1u << m;
-        } else {
-          slot_preds[i].push_back(u);
-          far_use[u] = std::max(far_use[u], i);
-        }
+      const int x = corder[i];
+      const int r0 = rec_first_row[i];
+      if (x < n) {
+        eid[r0] = x;
+      } else {
+        const int c = x - n;
+        ekind[r0] = 1;
+        eid[r0] = c;
+        for (int k = 1; k < d->chain_ptr[c + 1] - d->chain_ptr[c]; ++k) ekind[r0 + k] = 2;
       }
-      hmask[i] = mask;
-      head[l] = v;
+    }
+    // which predecessor reads are lane heads at read time?
+    std::vector<int> head(L, -1);          // task id, or -2 - c after chain c
+    std::vector<int> far_use(n, -1);       // last slot read of each task value
+    std::vector<unsigned> hmask(RE, 0);
+    std::vector<int> sp_ptr(RE + 1, 0), sp_list;  // slot-read predecessors per record (CSR)
+    for (int r = 0; r < RE; ++r) {
+      if (ekind[r] == 0) {
+        const int v = eid[r];
+        const int l = d->lane[v];
+        unsigned mask = 0;
+        for (int k = pptr[v]; k < pptr[v + 1]; ++k) {
+          const int u = padj[k];
+          const int m = d->lane[u];
+          if (head[m] == u) {
+            if (m != l) mask |= 1u << m;
+          } else {
+            sp_list.push_back(u);
+            far_use[u] = std::max(far_use[u], r);
+          }
+        }
+        hmask[r] = mask;
+        head[l] = v;
+      } else if (ekind[r] == 1) {
+        const int c = eid[r];
+        for (int k = d->chain_ptr[c]; k < d->chain_ptr[c + 1]; ++k) {
+          const int m = d->chain_member[k];
+          for (int q = pptr[m]; q < pptr[m + 1]; ++q) far_use[padj[q]] = std::max(far_use[padj[q]], r);
+        }
+        head[ch_lane[c]] = -2 - c;
+      }
+      sp_ptr[r + 1] = (int)sp_list.size();
     }
     std::vector<int> lslot(n, -1);
     std::vector<char> lglob(n, 0);
     std::priority_queue<int, std::vector<int>, std::greater<int>> fs, fg;
     int ns = 0, ngl = 0;
-    std::vector<int> fa_ptr(R + 1, 0), fa;  // values freed after record i (CSR)
-    for (int i = 0; i < R; ++i)
-      if (far_use[corder[i]] >= 0) fa_ptr[far_use[corder[i]] + 1]++;
-    for (int i = 0; i < R; ++i) fa_ptr[i + 1] += fa_ptr[i];
-    fa.resize(fa_ptr[R]);
+    auto for_values = [&](int r, auto fn) {  // task values produced by record r
+      if (ekind[r] == 0) {
+        fn(eid[r]);
+      } else if (ekind[r] == 1) {
+        const int c = eid[r];
+        for (int k = d->chain_ptr[c]; k < d->chain_ptr[c + 1]; ++k) fn(d->chain_member[k]);
+      }
+    };
+    std::vector<int> fa_ptr(RE + 1, 0), fa;  // values freed after record r (CSR)
+    for (int r = 0; r < RE; ++r)
+      for_values(r, [&](int v) { if (far_use[v] >= 0) fa_ptr[far_use[v] + 1]++; });
+    for (int r = 0; r < RE; ++r) fa_ptr[r + 1] += fa_ptr[r];
+    fa.resize(fa_ptr[RE]);
     {
       std::vector<int> fill(fa_ptr.begin(), fa_ptr.end() - 1);
-      for (int i = 0; i < R; ++i)
-        if (far_use[corder[i]] >= 0) fa[fill[far_use[corder[i]]]++] = corder[i];
+      for (int r = 0; r < RE; ++r)
+        for_values(r, [&](int v) { if (far_use[v] >= 0) fa[fill[far_use[v]]++] = v; });
     }
-    for (int i = 0; i < R; ++i) {
-      const int v = corder[i];
-      if (far_use[v] >= 0) {
-        const bool shrt = far_use[v] - i <= kShortRange;
+    for (int r = 0; r < RE; ++r) {
+      for_values(r, [&](int v) {
+        if (far_use[v] < 0) return;
+        const bool shrt = far_use[v] - r <= kShortRange;
         if (shrt && !fs.empty()) {
           lslot[v] = fs.top();
           fs.pop();
@@ -837,55 +877,91 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
             lslot[v] = ngl++;
           }
         }
-      }
-      for (int q = fa_ptr[i]; q < fa_ptr[i + 1]; ++q) (lglob[fa[q]] ? fg : fs).push(lslot[fa[q]]);
+      });
+      for (int q = fa_ptr[r]; q < fa_ptr[r + 1]; ++q) (lglob[fa[q]] ? fg : fs).push(lslot[fa[q]]);
     }
+    auto code_of = [&](int u) { return lglob[u] ? ns + lslot[u] : lslot[u]; };
     std::vector<int> lane_last(L, -1);
-    for (int i = 0; i < R; ++i) lane_last[d->lane[corder[i]]] = i;
-    std::vector<LaneRec> lprog(R);
-    std::vector<int> lside_off(R + 1, 0), lside_slots;
+    for (int r = 0; r < RE; ++r)
+      if (ekind[r] == 0) lane_last[d->lane[eid[r]]] = r;
+    std::vector<LaneRec> lprog(RE);
+    std::vector<int> lside_off(RE + 1, 0), lside_slots;
+    std::vector<LaneChainDev> lchains(NC);
+    std::vector<LaneMemberDev> lmembers;
+    std::vector<int> lpreds;
     bool any_ready = false;
-    for (int i = 0; i < R; ++i) {
-      const int v = corder[i];
-      LaneRec r;
-      memset(&r, 0, sizeof(r));
-      r.gap = d->gap[v];
+    for (int r = 0; r < RE; ++r) {
+      LaneRec rec;
+      memset(&rec, 0, sizeof(rec));
+      if (ekind[r] != 0) {
+        rec.rare = (unsigned char)(ekind[r] == 1 ? LREC_CHAIN : LREC_NOP);
+        if (ekind[r] == 1) {
+          const int c = eid[r];
+          rec.s0 = (short)c;
+          rec.h = (unsigned char)ch_lane[c];
+          LaneChainDev& lc = lchains[c];
+          lc.lane = ch_lane[c];
+          lc.B = d->chain_ptr[c + 1] - d->chain_ptr[c];
+          lc.mem_off = (int)lmembers.size();
+          lc.perm_off = chains[c].perm_off;
+          for (int k = d->chain_ptr[c]; k < d->chain_ptr[c + 1]; ++k) {
+            const int m = d->chain_member[k];
+            LaneMemberDev md;
+            memset(&md, 0, sizeof(md));
+            md.gap = d->gap[m];
+            md.pred_off = (int)lpreds.size();
+            for (int q = pptr[m]; q < pptr[m + 1]; ++q) lpreds.push_back(code_of(padj[q]));
+            md.npred = (int)lpreds.size() - md.pred_off;
+            md.out = lslot[m] >= 0 ? code_of(m) : -1;
+            if (d->ready_time && d->ready_time[m] != 0) any_ready = true;
+            lmembers.push_back(md);
+          }
+        }
+        lside_off[r + 1] = (int)lside_slots.size();
+        lprog[r] = rec;
+        continue;
+      }
+      const int v = eid[r];
+      rec.gap = d->gap[v];
       unsigned rare = 0;
       int nsm_pred = 0;
-      for (int u : slot_preds[i]) {
+      for (int q = sp_ptr[r]; q < sp_ptr[r + 1]; ++q) {
+        const int u = sp_list[q];
         if (!lglob[u] && nsm_pred == 0) {
           rare |= LREC_S0;
-          r.s0 = (short)lslot[u];
+          rec.s0 = (short)lslot[u];
           ++nsm_pred;
         } else if (!lglob[u] && nsm_pred == 1) {
           rare |= LREC_S1;
-          r.s1 = (short)lslot[u];
+          rec.s1 = (short)lslot[u];
           ++nsm_pred;
         } else {
           rare |= LREC_SIDE;
-          lside_slots.push_back(lglob[u] ? ns + lslot[u] : lslot[u]);
+          lside_slots.push_back(code_of(u));
         }
       }
-      lside_off[i + 1] = (int)lside_slots.size();
+      lside_off[r + 1] = (int)lside_slots.size();
       const long long rt = d->ready_time ? d->ready_time[v] : 0;
       if (rt != 0) {
         rare |= LREC_SIDE;
         any_ready = true;
       }
-      unsigned mask = hmask[i];
+      unsigned mask = hmask[r];
       if (rare & LREC_PRE) mask |= 16u;  // temp lane carries the rare predecessors
-      if (lane_last[d->lane[v]] == i) rare |= LREC_MS;
+      if (lane_last[d->lane[v]] == r) rare |= LREC_MS;
       if (lslot[v] >= 0) {
         rare |= lglob[v] ? LREC_OUT_GLOBAL : LREC_OUT_SMEM;
-        r.out = (short)lslot[v];
+        rec.out = (short)lslot[v];
       }
-      r.rare = (unsigned char)rare;
-      r.h = (unsigned char)((unsigned)d->lane[v] | (mask << 2) | (r.gap != 0 ? 128u : 0u));
-      lprog[i] = r;
+      rec.rare = (unsigned char)rare;
+      rec.h = (unsigned char)((unsigned)d->lane[v] | (mask << 2) | (rec.gap != 0 ? 128u : 0u));
+      lprog[r] = rec;
     }
-    if (ns + ngl < 32000) {
+    // chain members with ready floors stay on the general kernel
+    if (ns + ngl < 32000 && !(NC > 0 && any_ready)) {
       std::vector<long long> freq(256, 0);
-      for (int i = 0; i < R; ++i) freq[lprog[i].h]++;
+      for (int r = 0; r < RE; ++r)
+        if (ekind[r] == 0) freq[lprog[r].h]++;
       g->lane_codes.clear();
       for (int c = 0; c < 256; ++c)
         if (freq[c]) g->lane_codes.push_back(c);
@@ -893,10 +969,11 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
                        [&](int a, int b) { return freq[a] > freq[b]; });
       std::vector<long long> lready;
       if (any_ready) {
-        lready.resize(R);
-        for (int i = 0; i < R; ++i) lready[i] = d->ready_time[corder[i]];
+        lready.resize(RE);
+        for (int r = 0; r < RE; ++r) lready[r] = ekind[r] == 0 ? d->ready_time[eid[r]] : 0;
       }
       g->has_lanes = true;
+      g->ln_rec = RE;
       g->lksm = ns;
       g->lkglob = ngl;
       g->d_lprog = dev_upload(lprog);
@@ -905,6 +982,11 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
         g->d_lside_slots = dev_upload(lside_slots);
       }
       g->d_lside_ready = dev_upload(lready);
+      if (NC > 0) {
+        g->d_lchains = dev_upload(lchains);
+        g->d_lmembers = dev_upload(lmembers);
+        g->d_lpreds = dev_upload(lpreds);
+      }
     }
   }
 
@@ -1006,7 +1088,7 @@ void free_graph(ks_graph* g) {
   void* dptrs[] = {g->d_dprog,   g->d_side_off,   g->d_side_slots,  g->d_side_ready,
                    g->d_lprog,   g->d_lside_off,  g->d_lside_slots, g->d_lside_ready,
                    g->d_bd_ptr,  g->d_bd_rows,    g->d_bd_lane_chain, g->d_bd_chains,
-                   g->d_bd_member_rows};
+                   g->d_bd_member_rows, g->d_lchains, g->d_lmembers, g->d_lpreds};
   for (void* p : dptrs)
     if (p) cudaFree(p);
   void* ptrs[] = {g->d_prog,  g->d_extra, g->d_chains, g->d_members, g->d_child_ptr,
@@ -1145,6 +1227,7 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
   // int64 matrix (one thread per element; L2-resident at the sizes where the
   // derived path is used) and run the lanes kernel on it.
   ks_scenarios_desc expanded;
+  const ks_scenarios_desc* orig_sc = sc;
   const bool expand = use_max && !dense && !T.has_remove && g->has_lanes && g->n_rec > 0 &&
                       (long long)g->n * S * 8 <= (8LL << 30) && getenv("DDSIM_NO_EXPAND") == nullptr &&
                       getenv("DDSIM_NO_LANES") == nullptr;
@@ -1162,17 +1245,52 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
     expanded.scale = nullptr;
     sc = &expanded;
   }
+  // program / chain / override / scale tables of the general kernel's derived mode
+  auto fill_general = [&](MaxplusParams& q) {
+    q.n_rec = g->n_rec;
+    q.prog = g->d_prog;
+    if (T.ovr_map && g->n_rec > 0) {
+      // per-call override rows: patch a copy of the program
+      NodeRec* prog2 = T.scratch<NodeRec>(g->n_rec);
+      CUDA_TRY(cudaMemcpyAsync(prog2, g->d_prog, sizeof(NodeRec) * g->n_rec,
+                               cudaMemcpyDeviceToDevice, stream));
+      CUDA_TRY(launch_patch_ovr(prog2, g->n_rec, T.ovr_map, stream));
+      q.prog = prog2;
+    }
+    q.extra = g->d_extra;
+    q.chains = g->d_chains;
+    q.members = g->d_members;
+    q.n_chains = g->n_chains;
+    if (T.ovr_map && g->perm_ld > 0) {
+      NodeRec* mem2 = T.scratch<NodeRec>(g->perm_ld);
+      CUDA_TRY(cudaMemcpyAsync(mem2, g->d_members, sizeof(NodeRec) * g->perm_ld,
+                               cudaMemcpyDeviceToDevice, stream));
+      CUDA_TRY(launch_patch_ovr(mem2, g->perm_ld, T.ovr_map, stream));
+      q.members = mem2;
+    }
+    q.ksm = g->ksm;
+    q.kglob = g->kglob;
+    q.ovr = T.ovr;
+    q.scale_ptr = T.scale_ptr;
+    q.scale = T.scale;
+    q.perm = T.perm;
+    q.perm_ld = orig_sc->perm_ld;
+    q.present = T.present;
+  };
   const bool dense_now = sc->dense_kind != 0 && sc->dense != nullptr;
   const bool tma_ok =
       dense_now && reinterpret_cast<uintptr_t>(sc->dense) % 16 == 0 &&
       (sc->dense_kind == 1 ? sc->dense_ld % 4 == 0 : sc->dense_ld % 2 == 0);
+  // permutable chains run on the lanes path only for derived (expanded)
+  // durations: the exact fallback for them is the general kernel's derived mode
   const bool lanes_ok = use_max && dense_now && tma_ok && g->has_lanes && sc->n_overrides == 0 &&
-                        !sc->scale_ptr && getenv("DDSIM_NO_LANES") == nullptr;
+                        !sc->scale_ptr && (g->n_chains == 0 || expand) &&
+                        getenv("DDSIM_NO_LANES") == nullptr;
   if (lanes_ok) {
     LaneParams p;
     memset(&p, 0, sizeof(p));
     p.prog = g->d_lprog;
-    p.n_rec = g->n_rec;
+    p.n_rec = g->ln_rec;
     p.side_off = g->d_lside_off;
     p.side_slots = g->d_lside_slots;
     p.side_ready = g->d_lside_ready;
@@ -1184,7 +1302,17 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
     if (dk == 1 && (reinterpret_cast<uintptr_t>(sc->dense) % 16 != 0 || sc->dense_ld % 4 != 0))
       fail(KS_ERR_INVALID, "int32 dense durations need 16B alignment and dense_ld % 4 == 0");
     if (dk == 2) p.dense64 = reinterpret_cast<const long long*>(sc->dense);
+    if (dk == 1) p.dense32 = reinterpret_cast<const int*>(sc->dense);
     p.dense_ld = sc->dense_ld;
+    if (g->n_chains > 0) {
+      p.chains = g->d_lchains;
+      p.members = g->d_lmembers;
+      p.preds = g->d_lpreds;
+      p.perm = T.perm;
+      p.perm_ld = sc->perm_ld;
+      p.present = T.present;
+      p.n_chains = g->n_chains;
+    }
     p.start = reinterpret_cast<long long*>(out->start);
     p.start_ld = out->start_ld;
     p.makespan = reinterpret_cast<long long*>(out->makespan);
@@ -1217,7 +1345,12 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
     q.makespan = p.makespan;
     q.lane_busy = p.lane_busy;
     q.run_if = flag;
-    const int BDq = maxplus_block_dim(S, dk, nsm);
+    if (g->n_chains > 0) {  // exact rerun in derived mode (chains + original tables)
+      fill_general(q);
+      q.dense_kind = 0;
+      q.dense64 = nullptr;
+    }
+    const int BDq = maxplus_block_dim(S, q.dense_kind, nsm);
     q.s_pad = (long long)((S + BDq - 1) / BDq) * BDq;
     if (q.kglob > 0) q.gslots = T.scratch<long long>((size_t)q.kglob * q.s_pad);
     CUDA_TRY(launch_maxplus(q, dk == 1 ? reinterpret_cast<const int*>(sc->dense) : nullptr, stream));
@@ -1288,29 +1421,7 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
   } else if (use_max) {
     MaxplusParams p;
     memset(&p, 0, sizeof(p));
-    p.n_rec = g->n_rec;
-    p.prog = g->d_prog;
-    if (T.ovr_map && g->n_rec > 0) {
-      // per-call override rows: patch a copy of the program
-      NodeRec* prog2 = T.scratch<NodeRec>(g->n_rec);
-      CUDA_TRY(cudaMemcpyAsync(prog2, g->d_prog, sizeof(NodeRec) * g->n_rec,
-                               cudaMemcpyDeviceToDevice, stream));
-      CUDA_TRY(launch_patch_ovr(prog2, g->n_rec, T.ovr_map, stream));
-      p.prog = prog2;
-    }
-    p.extra = g->d_extra;
-    p.chains = g->d_chains;
-    p.members = g->d_members;
-    p.n_chains = g->n_chains;
-    if (T.ovr_map && g->perm_ld > 0) {
-      NodeRec* mem2 = T.scratch<NodeRec>(g->perm_ld);
-      CUDA_TRY(cudaMemcpyAsync(mem2, g->d_members, sizeof(NodeRec) * g->perm_ld,
-                               cudaMemcpyDeviceToDevice, stream));
-      CUDA_TRY(launch_patch_ovr(mem2, g->perm_ld, T.ovr_map, stream));
-      p.members = mem2;
-    }
-    p.ksm = g->ksm;
-    p.kglob = g->kglob;
+    fill_general(p);
     p.S = S;
     p.L = g->L;
     int dmode = 0;
@@ -1328,12 +1439,6 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
       p.dense_ld = sc->dense_ld;
     }
     p.dense_kind = dmode;
-    p.ovr = T.ovr;
-    p.scale_ptr = T.scale_ptr;
-    p.scale = T.scale;
-    p.perm = T.perm;
-    p.perm_ld = sc->perm_ld;
-    p.present = T.present;
     p.start = reinterpret_cast<long long*>(out->start);
     p.start_ld = out->start_ld;
     p.makespan = reinterpret_cast<long long*>(out->makespan);

@@ -22,7 +22,17 @@ struct alignas(16) Rec {
 };
 enum {
   R_S0 = 1, R_S1 = 2, R_SIDE = 4, R_MS = 8, R_OUT_SMEM = 16, R_OUT_GLOBAL = 32,
-  R_PRE = 7, R_POST = 56
+  R_CHAIN = 64, R_NOP = 128, R_PRE = 7 | 64 | 128, R_POST = 56
+};
+
+struct Chain {
+  int lane, B, mem_off, perm_off;
+};
+struct Member {
+  long long gap;
+  int pred_off, npred;
+  int out;
+  int pad;
 };
 
 struct Params {
@@ -42,6 +52,14 @@ struct Params {
   long long* makespan;
   long long* lane_busy;
   int* neg_flag;
+  const Chain* chains;
+  const Member* members;
+  const int* preds;
+  const short* perm;
+  const unsigned char* present;
+  const int* dense32;
+  int perm_ld;
+  int n_chains;
 };
 
 // CUtensorMap-compatible opaque kernel parameter (128 B, 64 B aligned)
@@ -167,6 +185,25 @@ __device__ __forceinline__ long long own_get(const St<V>& S, int own, int i) {
   }
 }
 
+template <int V>
+__device__ __forceinline__ void own_set(St<V>& S, int own, int i, long long v) {
+  switch (own) {
+    case 0: S.lv[0][i] = v; break;
+    case 1: S.lv[1][i] = v; break;
+    case 2: S.lv[2][i] = v; break;
+    default: S.lv[3][i] = v; break;
+  }
+}
+template <int V>
+__device__ __forceinline__ void busy_add(St<V>& S, int own, int i, long long v) {
+  switch (own) {
+    case 0: S.lb[0][i] += v; break;
+    case 1: S.lb[1][i] += v; break;
+    case 2: S.lb[2][i] += v; break;
+    default: S.lb[3][i] += v; break;
+  }
+}
+
 __device__ __forceinline__ int4 l_lds128(unsigned a) {
   int4 v;
   asm volatile("ld.shared.v4.s32 {%0,%1,%2,%3}, [%4];"
@@ -268,6 +305,67 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p) {
   const unsigned row_pitch = (unsigned)W * ES;
   const int ksm = p.ksm;
 
+  // Permutable chain (inserted-task table, e.g. AllReduce buckets in a
+  // per-scenario order): members run back to back on the chain's lane in the
+  // scenario's order; every member predecessor is read from a slot; member k
+  // writes frozen row `row + k`.  An absent chain leaves no start (-1), its
+  // consumers see 0 (the identity of max here) and its lane head unchanged.
+  auto slot_val = [&](int code, int i) -> long long {
+    if (code < ksm) {
+      long long v;
+      asm volatile("ld.shared.s64 %0, [%1];"
+                   : "=l"(v) : "r"(slot_s + (unsigned)code * slot_pitch + col + 8u * i));
+      return v;
+    }
+    return act ? p.gslots[(long long)(code - ksm) * p.s_pad + s + i] : 0;
+  };
+  auto slot_set = [&](int code, int i, long long v) {
+    if (code < ksm)
+      asm volatile("st.shared.s64 [%0], %1;"
+                   ::"r"(slot_s + (unsigned)code * slot_pitch + col + 8u * i), "l"(v) : "memory");
+    else if (act)
+      p.gslots[(long long)(code - ksm) * p.s_pad + s + i] = v;
+  };
+  auto chain_record = [&](int cid, int row) {
+    const Chain ch = p.chains[cid];
+#pragma unroll
+    for (int i = 0; i < V; ++i) {
+      const long long sc = s + i;
+      const bool pres = !act || p.present == nullptr || p.present[sc * p.n_chains + cid] != 0;
+      long long prev = own_get<V>(S, ch.lane, i);
+      long long lbadd = 0, msv = 0;
+      for (int q = 0; q < ch.B; ++q) {
+        const int k = (p.perm != nullptr && act) ? (int)p.perm[sc * p.perm_ld + ch.perm_off + q] : q;
+        const Member M = p.members[ch.mem_off + k];
+        if (!pres) {
+          if (store) __stcs(sp + (long long)k * ld + i, -1ll);
+          if (M.out >= 0) slot_set(M.out, i, 0);
+          continue;
+        }
+        long long x = prev;
+        for (int e = 0; e < M.npred; ++e) x = lmax(x, slot_val(p.preds[M.pred_off + e], i));
+        long long d = 0;
+        if (act) {
+          const long long at = (long long)(row + k) * p.dense_ld + sc;
+          d = DK == 1 ? (long long)p.dense32[at] : p.dense64[at];
+        }
+        neg |= (int)(d >> 32);
+        if (store) __stcs(sp + (long long)k * ld + i, x);
+        const long long fin = x + d;
+        prev = fin + M.gap;
+        msv = lmax(msv, fin);
+        lbadd += d;
+        if (M.out >= 0) slot_set(M.out, i, prev);
+      }
+      if (pres) {
+        own_set<V>(S, ch.lane, i, prev);
+        busy_add<V>(S, ch.lane, i, lbadd);
+        if (i == 0) ms0 = lmax(ms0, msv);
+        else ms1 = lmax(ms1, msv);
+      }
+    }
+  };
+
   for (int c = 0; c < nchunks; ++c) {
     const int st = c % kStagesL;
     l_wait(&bars[st], (unsigned)((c / kStagesL) & 1));
@@ -313,6 +411,11 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p) {
       const unsigned h = w >> 24;
       const unsigned rare = (w >> 16) & 0xffu;
       if (rare & R_PRE) {
+        if (rare & (R_CHAIN | R_NOP)) {
+          if (rare & R_CHAIN) chain_record((int)(short)(r.z & 0xffff), c * kChunkL + j);
+          if (store) sp += ld;
+          return;
+        }
         // predecessors that are no longer lane heads (+ ready floor) -> temp lane
         long long x0 = 0, x1 = 0, y0, y1;
         const int row = c * kChunkL + j;
