@@ -30,12 +30,17 @@ def alloc(seed):
     return dense, start
 
 
+ENQ = []
+
+
 def timed(fn, n):
     a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     torch.cuda.synchronize()
     a.record()
+    t0 = time.perf_counter()
     for _ in range(n):
         fn()
+    ENQ.append((time.perf_counter() - t0) * 1e3 / n)  # host ms per enqueued step
     b.record()
     torch.cuda.synchronize()
     return a.elapsed_time(b) / n
@@ -52,9 +57,10 @@ for rep in range(int(sys.argv[1]) if len(sys.argv) > 1 else 2):
         simulate_batch_device(fz, table, makespan=ms, lane_busy=lb, start=start, stream=st)
     step()
     res = [timed(step, 5) for _ in range(3)]
-    cp = timed(lambda: start.copy_(dense), 3)
-    print(f"alloc {rep}: dense@{dense.data_ptr():#x} start@{start.data_ptr():#x} "
-          f"sim ms {['%.2f' % x for x in res]} copy {cp:.2f} ms", flush=True)
+    from paper_2006_03318_b200 import _native as N
+    cp = timed(lambda: N.lib().ks_probe_widen(dense.data_ptr(), start.data_ptr(), rows * S, st), 3)
+    print(f"alloc {rep}: sim ms {['%.2f' % x for x in res]} probe-copy {cp:.2f} ms "
+          f"host enqueue ms/step {['%.3f' % x for x in ENQ[-4:-1]]}", flush=True)
     del dense, start, table
     torch.cuda.empty_cache()
     time.sleep(1)
