@@ -120,7 +120,11 @@ struct LaneParams {
   long long* makespan;
   long long* lane_busy;
   int* neg_flag;
-  // permutable chains (null when the graph has none)
+};
+
+// Permutable chains on the lanes path (a separate kernel parameter of the
+// chain variant; mirrors ddsim_lanes::ChainParams).
+struct LaneChainParams {
   const LaneChainDev* chains;
   const LaneMemberDev* members;
   const int* preds;
@@ -220,9 +224,11 @@ cudaError_t launch_maxplus(const MaxplusParams& p, const int* dense32,
                            cudaStream_t stream);
 cudaError_t launch_maxplus_dense(const DenseParams& p, const int* dense32, int dkind,
                                  cudaStream_t stream);
-cudaError_t launch_maxplus_lanes(const LaneParams& p, const int* dense32, int dkind,
+cudaError_t launch_maxplus_lanes(const LaneParams& p, const LaneChainParams* cp, const int* dense32,
+                                 int dkind,
                                  const std::vector<int>* codes, cudaStream_t stream);
-cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const void* tmap128, int dkind, int V,
+cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const LaneChainParams* cp,
+                                     const void* tmap128, int dkind, int V,
                                      const std::vector<int>& codes, int grid, int BD, size_t smem,
                                      cudaStream_t stream);
 int maxplus_lanes_vec(int S);

@@ -1302,16 +1302,18 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
     if (dk == 1 && (reinterpret_cast<uintptr_t>(sc->dense) % 16 != 0 || sc->dense_ld % 4 != 0))
       fail(KS_ERR_INVALID, "int32 dense durations need 16B alignment and dense_ld % 4 == 0");
     if (dk == 2) p.dense64 = reinterpret_cast<const long long*>(sc->dense);
-    if (dk == 1) p.dense32 = reinterpret_cast<const int*>(sc->dense);
     p.dense_ld = sc->dense_ld;
+    LaneChainParams cp;
+    memset(&cp, 0, sizeof(cp));
     if (g->n_chains > 0) {
-      p.chains = g->d_lchains;
-      p.members = g->d_lmembers;
-      p.preds = g->d_lpreds;
-      p.perm = T.perm;
-      p.perm_ld = sc->perm_ld;
-      p.present = T.present;
-      p.n_chains = g->n_chains;
+      cp.chains = g->d_lchains;
+      cp.members = g->d_lmembers;
+      cp.preds = g->d_lpreds;
+      cp.perm = T.perm;
+      cp.perm_ld = sc->perm_ld;
+      cp.present = T.present;
+      cp.n_chains = g->n_chains;
+      if (dk == 1) cp.dense32 = reinterpret_cast<const int*>(sc->dense);
     }
     p.start = reinterpret_cast<long long*>(out->start);
     p.start_ld = out->start_ld;
@@ -1326,7 +1328,8 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
     int* flag = T.scratch<int>(1);
     CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), stream));
     p.neg_flag = flag;
-    CUDA_TRY(launch_maxplus_lanes(p, dk == 1 ? reinterpret_cast<const int*>(sc->dense) : nullptr, dk,
+    CUDA_TRY(launch_maxplus_lanes(p, g->n_chains > 0 ? &cp : nullptr,
+                                  dk == 1 ? reinterpret_cast<const int*>(sc->dense) : nullptr, dk,
                                   &g->lane_codes, stream));
     MaxplusParams q;
     memset(&q, 0, sizeof(q));

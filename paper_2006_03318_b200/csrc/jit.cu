@@ -94,7 +94,7 @@ void init_locked() {
               (g_drv.ok ? "ok" : "missing entry points");
 }
 
-std::string make_source(const std::vector<int>& codes, int dk, int V, bool dyn) {
+std::string make_source(const std::vector<int>& codes, int dk, int V, bool dyn, bool ch) {
   std::string disp = "#define DDSIM_DISPATCH(h) ";
   if (dyn) disp += "hstep_dyn<V>(S, h, d0, d1, gap, sp, ld, store); if (0) ";
   for (size_t i = 0; i < codes.size(); ++i) {
@@ -119,15 +119,17 @@ std::string make_source(const std::vector<int>& codes, int dk, int V, bool dyn) 
   }
   src += disp + body;
   src += "\nextern \"C\" __global__ void __launch_bounds__(256) ddsim_lanes_jit("
-         "const __grid_constant__ ddsim_lanes::Tmap tmap, const ddsim_lanes::Params p) {\n"
+         "const __grid_constant__ ddsim_lanes::Tmap tmap, const ddsim_lanes::Params p" +
+         std::string(ch ? ", const __grid_constant__ ddsim_lanes::ChainParams cp" : "") + ") {\n"
          "  ddsim_lanes::lanes_body<" + std::to_string(dk) + ", " + std::to_string(V) +
-         ">(&tmap, p);\n}\n";
+         (ch ? ", true>(&tmap, p, &cp);\n}\n" : ", false>(&tmap, p);\n}\n");
   return src;
 }
 
-CUfunction get_function(const std::vector<int>& codes, int dk, int V, bool dyn, int device) {
+CUfunction get_function(const std::vector<int>& codes, int dk, int V, bool dyn, bool ch,
+                        int device) {
   std::string key = std::to_string(device) + ":" + std::to_string(dk) + ":" + std::to_string(V) +
-                    (dyn ? ":dyn:" : ":");
+                    (dyn ? ":dyn" : "") + (ch ? ":ch:" : ":");
   if (const char* u = getenv("DDSIM_JIT_UNROLL")) key += std::string("u") + u + ":";
   if (const char* b = getenv("DDSIM_LANES_BODY")) key += std::string("b") + b + ":";
   for (int c : codes) key += std::to_string(c) + ",";
@@ -136,7 +138,7 @@ CUfunction get_function(const std::vector<int>& codes, int dk, int V, bool dyn, 
   if (!g_nv.ok || !g_drv.ok) return nullptr;
   auto it = g_cache.find(key);
   if (it != g_cache.end()) return it->second;
-  const std::string src = make_source(codes, dk, V, dyn);
+  const std::string src = make_source(codes, dk, V, dyn, ch);
   nvrtcProgram_t prog = nullptr;
   CUfunction fn = nullptr;
   if (g_nv.create(&prog, src.c_str(), "ddsim_lanes_jit.cu", 0, nullptr, nullptr) == 0) {
@@ -178,7 +180,8 @@ CUfunction get_function(const std::vector<int>& codes, int dk, int V, bool dyn, 
 
 // Launch the specialised kernel; cudaErrorNotSupported when JIT is unavailable
 // (the caller then launches the static kernel).
-cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const void* tmap128, int dkind, int V,
+cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const LaneChainParams* cp,
+                                     const void* tmap128, int dkind, int V,
                                      const std::vector<int>& codes, int grid, int BD, size_t smem,
                                      cudaStream_t stream) {
   if (codes.empty() || codes.size() > 32) {
@@ -192,7 +195,7 @@ cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const void* tmap128, i
   int nsm = 148;
   if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) dyn = grid < nsm;
   if (const char* e = getenv("DDSIM_LANES_DYN")) dyn = atoi(e) != 0;
-  CUfunction fn = get_function(codes, dkind, V, dyn, dev);
+  CUfunction fn = get_function(codes, dkind, V, dyn, cp != nullptr, dev);
   if (!fn) return cudaErrorNotSupported;
   const CUresult ar = g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
   if (ar != CUDA_SUCCESS) {
@@ -202,7 +205,9 @@ cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const void* tmap128, i
   alignas(64) unsigned char tm[128];
   memcpy(tm, tmap128, 128);
   LaneParams pp = p;
-  void* args[] = {tm, &pp};
+  LaneChainParams cpv{};
+  if (cp) cpv = *cp;
+  void* args[] = {tm, &pp, &cpv};
   const CUresult r = g_drv.launch(fn, grid, 1, 1, BD, 1, 1, (unsigned)smem, (CUstream)stream, args,
                                   nullptr);
   if (r != CUDA_SUCCESS) {

@@ -22,7 +22,7 @@ struct alignas(16) Rec {
 };
 enum {
   R_S0 = 1, R_S1 = 2, R_SIDE = 4, R_MS = 8, R_OUT_SMEM = 16, R_OUT_GLOBAL = 32,
-  R_CHAIN = 64, R_NOP = 128, R_PRE = 7 | 64 | 128, R_POST = 56
+  R_CHAIN = 64, R_NOP = 128, R_PRE = 7, R_POST = 56
 };
 
 struct Chain {
@@ -52,6 +52,11 @@ struct Params {
   long long* makespan;
   long long* lane_busy;
   int* neg_flag;
+};
+
+// Permutable-chain tables: a separate kernel parameter of the chain variant
+// only (growing Params changes the hot loop's code generation).
+struct ChainParams {
   const Chain* chains;
   const Member* members;
   const int* preds;
@@ -244,11 +249,81 @@ __device__ __forceinline__ void slot_st(unsigned a, long long x0, long long x1) 
     asm volatile("st.shared.s64 [%0], %1;" ::"r"(a), "l"(x0) : "memory");
 }
 
+// Permutable chain (inserted-task table, e.g. AllReduce buckets in a
+// per-scenario order): members run back to back on the chain's lane in the
+// scenario's order; every member predecessor is read from a slot; member k
+// writes frozen row `row + k`.  An absent chain leaves no start (-1), its
+// consumers see 0 (the identity of max here) and its lane head unchanged.
+// Only instantiated for graphs with chains (lanes_body<..., CH = true>).
+template <int DK, int V>
+__device__ __forceinline__ void chain_record(const Params& p, const ChainParams& cp, St<V>& S,
+                                             int cid, int row,
+                                             long long s, bool act, bool store, long long* sp,
+                                             long long ld, unsigned slot_s, unsigned slot_pitch,
+                                             unsigned col, long long& ms0, long long& ms1,
+                                             int& neg) {
+  const int ksm = p.ksm;
+  auto slot_addr = [&](int code, int i) { return slot_s + (unsigned)code * slot_pitch + col + 8u * i; };
+  const Chain ch = cp.chains[cid];
+#pragma unroll
+  for (int i = 0; i < V; ++i) {
+    const long long sc = s + i;
+    const bool pres = !act || cp.present == nullptr || cp.present[sc * cp.n_chains + cid] != 0;
+    long long prev = own_get<V>(S, ch.lane, i);
+    long long lbadd = 0, msv = 0;
+    for (int q = 0; q < ch.B; ++q) {
+      const int k = (cp.perm != nullptr && act) ? (int)cp.perm[sc * cp.perm_ld + ch.perm_off + q] : q;
+      const Member M = cp.members[ch.mem_off + k];
+      long long val = -1;  // start written for member k
+      if (pres) {
+        long long x = prev;
+        for (int e = 0; e < M.npred; ++e) {
+          const int code = cp.preds[M.pred_off + e];
+          long long v = 0;
+          if (code < ksm)
+            asm volatile("ld.shared.s64 %0, [%1];" : "=l"(v) : "r"(slot_addr(code, i)));
+          else if (act)
+            v = p.gslots[(long long)(code - ksm) * p.s_pad + sc];
+          x = lmax(x, v);
+        }
+        long long d = 0;
+        if (act) {
+          const long long at = (long long)(row + k) * p.dense_ld + sc;
+          d = DK == 1 ? (long long)cp.dense32[at] : p.dense64[at];
+        }
+        neg |= (int)(d >> 32);
+        val = x;
+        const long long fin = x + d;
+        prev = fin + M.gap;
+        msv = lmax(msv, fin);
+        lbadd += d;
+      }
+      if (store) __stcs(sp + (long long)k * ld + i, val);
+      if (M.out >= 0) {
+        const long long o = pres ? prev : 0;
+        if (M.out < ksm)
+          asm volatile("st.shared.s64 [%0], %1;" ::"r"(slot_addr(M.out, i)), "l"(o) : "memory");
+        else if (act)
+          p.gslots[(long long)(M.out - ksm) * p.s_pad + sc] = o;
+      }
+    }
+    if (pres) {
+      own_set<V>(S, ch.lane, i, prev);
+      busy_add<V>(S, ch.lane, i, lbadd);
+      if (i == 0) ms0 = lmax(ms0, msv);
+      else ms1 = lmax(ms1, msv);
+    }
+  }
+}
+
 // The kernel body; DDSIM_DISPATCH(h) must expand to the handler dispatch
 // (it sees S, d0, d1, gap, sp, ld, store and the template parameter V).
 // Each thread owns V consecutive scenarios (V = 1 or 2).
-template <int DK, int V>
-__device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p) {
+// CH: the graph has permutable chains (chain / no-op records).  Without them
+// the chain code is compiled out, so the hot loop keeps its registers.
+template <int DK, int V, bool CH = false>
+__device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
+                                           const ChainParams* cpp = nullptr) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int BD = blockDim.x;
   const int W = BD * V;  // scenarios per CTA
@@ -305,66 +380,6 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p) {
   const unsigned row_pitch = (unsigned)W * ES;
   const int ksm = p.ksm;
 
-  // Permutable chain (inserted-task table, e.g. AllReduce buckets in a
-  // per-scenario order): members run back to back on the chain's lane in the
-  // scenario's order; every member predecessor is read from a slot; member k
-  // writes frozen row `row + k`.  An absent chain leaves no start (-1), its
-  // consumers see 0 (the identity of max here) and its lane head unchanged.
-  auto slot_val = [&](int code, int i) -> long long {
-    if (code < ksm) {
-      long long v;
-      asm volatile("ld.shared.s64 %0, [%1];"
-                   : "=l"(v) : "r"(slot_s + (unsigned)code * slot_pitch + col + 8u * i));
-      return v;
-    }
-    return act ? p.gslots[(long long)(code - ksm) * p.s_pad + s + i] : 0;
-  };
-  auto slot_set = [&](int code, int i, long long v) {
-    if (code < ksm)
-      asm volatile("st.shared.s64 [%0], %1;"
-                   ::"r"(slot_s + (unsigned)code * slot_pitch + col + 8u * i), "l"(v) : "memory");
-    else if (act)
-      p.gslots[(long long)(code - ksm) * p.s_pad + s + i] = v;
-  };
-  auto chain_record = [&](int cid, int row) {
-    const Chain ch = p.chains[cid];
-#pragma unroll
-    for (int i = 0; i < V; ++i) {
-      const long long sc = s + i;
-      const bool pres = !act || p.present == nullptr || p.present[sc * p.n_chains + cid] != 0;
-      long long prev = own_get<V>(S, ch.lane, i);
-      long long lbadd = 0, msv = 0;
-      for (int q = 0; q < ch.B; ++q) {
-        const int k = (p.perm != nullptr && act) ? (int)p.perm[sc * p.perm_ld + ch.perm_off + q] : q;
-        const Member M = p.members[ch.mem_off + k];
-        if (!pres) {
-          if (store) __stcs(sp + (long long)k * ld + i, -1ll);
-          if (M.out >= 0) slot_set(M.out, i, 0);
-          continue;
-        }
-        long long x = prev;
-        for (int e = 0; e < M.npred; ++e) x = lmax(x, slot_val(p.preds[M.pred_off + e], i));
-        long long d = 0;
-        if (act) {
-          const long long at = (long long)(row + k) * p.dense_ld + sc;
-          d = DK == 1 ? (long long)p.dense32[at] : p.dense64[at];
-        }
-        neg |= (int)(d >> 32);
-        if (store) __stcs(sp + (long long)k * ld + i, x);
-        const long long fin = x + d;
-        prev = fin + M.gap;
-        msv = lmax(msv, fin);
-        lbadd += d;
-        if (M.out >= 0) slot_set(M.out, i, prev);
-      }
-      if (pres) {
-        own_set<V>(S, ch.lane, i, prev);
-        busy_add<V>(S, ch.lane, i, lbadd);
-        if (i == 0) ms0 = lmax(ms0, msv);
-        else ms1 = lmax(ms1, msv);
-      }
-    }
-  };
 
   for (int c = 0; c < nchunks; ++c) {
     const int st = c % kStagesL;
@@ -410,12 +425,16 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p) {
       const unsigned w = (unsigned)r.w;
       const unsigned h = w >> 24;
       const unsigned rare = (w >> 16) & 0xffu;
-      if (rare & R_PRE) {
+      if constexpr (CH) {
         if (rare & (R_CHAIN | R_NOP)) {
-          if (rare & R_CHAIN) chain_record((int)(short)(r.z & 0xffff), c * kChunkL + j);
+          if (rare & R_CHAIN)
+            chain_record<DK, V>(p, *cpp, S, (int)(short)(r.z & 0xffff), c * kChunkL + j, s, act,
+                                store, sp, ld, slot_s, slot_pitch, col, ms0, ms1, neg);
           if (store) sp += ld;
           return;
         }
+      }
+      if (rare & R_PRE) {
         // predecessors that are no longer lane heads (+ ready floor) -> temp lane
         long long x0 = 0, x1 = 0, y0, y1;
         const int row = c * kChunkL + j;

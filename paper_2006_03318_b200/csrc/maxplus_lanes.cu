@@ -39,12 +39,19 @@ namespace ddsim {
 
 static_assert(sizeof(LaneRec) == sizeof(ddsim_lanes::Rec), "record layouts differ");
 static_assert(sizeof(LaneParams) == sizeof(ddsim_lanes::Params), "param layouts differ");
+static_assert(sizeof(LaneChainParams) == sizeof(ddsim_lanes::ChainParams), "chain layouts differ");
 
 // DK: 1 = int32 durations via TMA tiles, 2 = int64 durations (direct loads).
 template <int DK, int V>
 __global__ void __launch_bounds__(256) maxplus_lanes_kernel(const __grid_constant__ ddsim_lanes::Tmap tmap,
                                                             const ddsim_lanes::Params p) {
-  ddsim_lanes::lanes_body<DK, V>(&tmap, p);
+  ddsim_lanes::lanes_body<DK, V, false>(&tmap, p);
+}
+template <int DK, int V>
+__global__ void __launch_bounds__(256) maxplus_lanes_chain_kernel(
+    const __grid_constant__ ddsim_lanes::Tmap tmap, const ddsim_lanes::Params p,
+    const __grid_constant__ ddsim_lanes::ChainParams cp) {
+  ddsim_lanes::lanes_body<DK, V, true>(&tmap, p, &cp);
 }
 
 static size_t lanes_smem(int dk, int BD, int V, int ksm) {
@@ -74,7 +81,8 @@ int maxplus_lanes_block_dim(int S, int num_sms) {
   return bd < 32 ? 32 : (bd > cap ? cap : bd);
 }
 
-cudaError_t launch_maxplus_lanes(const LaneParams& p, const int* dense32, int dkind,
+cudaError_t launch_maxplus_lanes(const LaneParams& p, const LaneChainParams* cp, const int* dense32,
+                                 int dkind,
                                  const std::vector<int>* codes, cudaStream_t stream) {
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
@@ -109,17 +117,26 @@ cudaError_t launch_maxplus_lanes(const LaneParams& p, const int* dense32, int dk
   }
   // per-graph specialised dispatch first (NVRTC); the static kernel otherwise
   if (codes != nullptr) {
-    const cudaError_t e = launch_maxplus_lanes_jit(p, &tmap, dkind, V, *codes, grid, BD, smem, stream);
+    const cudaError_t e =
+        launch_maxplus_lanes_jit(p, cp, &tmap, dkind, V, *codes, grid, BD, smem, stream);
     if (e == cudaSuccess) return cudaGetLastError();
   }
   const ddsim_lanes::Tmap& tm = *reinterpret_cast<const ddsim_lanes::Tmap*>(&tmap);
   const ddsim_lanes::Params& pp = *reinterpret_cast<const ddsim_lanes::Params*>(&p);
   cudaError_t err;
-#define LAUNCH_L(DK, VV)                                                                   \
-  err = cudaFuncSetAttribute(maxplus_lanes_kernel<DK, VV>,                                 \
-                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);      \
-  if (err != cudaSuccess) return err;                                                      \
-  maxplus_lanes_kernel<DK, VV><<<grid, BD, smem, stream>>>(tm, pp);
+#define LAUNCH_L(DK, VV)                                                                      \
+  if (cp != nullptr) {                                                                        \
+    err = cudaFuncSetAttribute(maxplus_lanes_chain_kernel<DK, VV>,                            \
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
+    if (err != cudaSuccess) return err;                                                       \
+    maxplus_lanes_chain_kernel<DK, VV><<<grid, BD, smem, stream>>>(                           \
+        tm, pp, *reinterpret_cast<const ddsim_lanes::ChainParams*>(cp));                       \
+  } else {                                                                                    \
+    err = cudaFuncSetAttribute(maxplus_lanes_kernel<DK, VV>,                                  \
+                               cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);       \
+    if (err != cudaSuccess) return err;                                                       \
+    maxplus_lanes_kernel<DK, VV><<<grid, BD, smem, stream>>>(tm, pp);                         \
+  }
   if (dkind == 1 && V == 2) {
     LAUNCH_L(1, 2)
   } else if (dkind == 1) {

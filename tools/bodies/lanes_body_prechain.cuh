@@ -1,4 +1,4 @@
-static const char* kLanesBodySrc = R"DDSIM_SRC(// Device body of the maxplus_lanes kernel, shared by the statically compiled
+// Device body of the maxplus_lanes kernel, shared by the statically compiled
 // kernel (maxplus_lanes.cu, 256-way switch dispatch) and the per-graph
 // NVRTC-specialised kernel (jit.cu, if-chain over the handler codes the graph
 // uses, in frequency order).  Self-contained: NVRTC compiles it without any
@@ -22,17 +22,7 @@ struct alignas(16) Rec {
 };
 enum {
   R_S0 = 1, R_S1 = 2, R_SIDE = 4, R_MS = 8, R_OUT_SMEM = 16, R_OUT_GLOBAL = 32,
-  R_CHAIN = 64, R_NOP = 128, R_PRE = 7, R_POST = 56
-};
-
-struct Chain {
-  int lane, B, mem_off, perm_off;
-};
-struct Member {
-  long long gap;
-  int pred_off, npred;
-  int out;
-  int pad;
+  R_PRE = 7, R_POST = 56
 };
 
 struct Params {
@@ -52,19 +42,6 @@ struct Params {
   long long* makespan;
   long long* lane_busy;
   int* neg_flag;
-};
-
-// Permutable-chain tables: a separate kernel parameter of the chain variant
-// only (growing Params changes the hot loop's code generation).
-struct ChainParams {
-  const Chain* chains;
-  const Member* members;
-  const int* preds;
-  const short* perm;
-  const unsigned char* present;
-  const int* dense32;
-  int perm_ld;
-  int n_chains;
 };
 
 // CUtensorMap-compatible opaque kernel parameter (128 B, 64 B aligned)
@@ -190,25 +167,6 @@ __device__ __forceinline__ long long own_get(const St<V>& S, int own, int i) {
   }
 }
 
-template <int V>
-__device__ __forceinline__ void own_set(St<V>& S, int own, int i, long long v) {
-  switch (own) {
-    case 0: S.lv[0][i] = v; break;
-    case 1: S.lv[1][i] = v; break;
-    case 2: S.lv[2][i] = v; break;
-    default: S.lv[3][i] = v; break;
-  }
-}
-template <int V>
-__device__ __forceinline__ void busy_add(St<V>& S, int own, int i, long long v) {
-  switch (own) {
-    case 0: S.lb[0][i] += v; break;
-    case 1: S.lb[1][i] += v; break;
-    case 2: S.lb[2][i] += v; break;
-    default: S.lb[3][i] += v; break;
-  }
-}
-
 __device__ __forceinline__ int4 l_lds128(unsigned a) {
   int4 v;
   asm volatile("ld.shared.v4.s32 {%0,%1,%2,%3}, [%4];"
@@ -249,81 +207,11 @@ __device__ __forceinline__ void slot_st(unsigned a, long long x0, long long x1) 
     asm volatile("st.shared.s64 [%0], %1;" ::"r"(a), "l"(x0) : "memory");
 }
 
-// Permutable chain (inserted-task table, e.g. AllReduce buckets in a
-// per-scenario order): members run back to back on the chain's lane in the
-// scenario's order; every member predecessor is read from a slot; member k
-// writes frozen row `row + k`.  An absent chain leaves no start (-1), its
-// consumers see 0 (the identity of max here) and its lane head unchanged.
-// Only instantiated for graphs with chains (lanes_body<..., CH = true>).
-template <int DK, int V>
-__device__ __forceinline__ void chain_record(const Params& p, const ChainParams& cp, St<V>& S,
-                                             int cid, int row,
-                                             long long s, bool act, bool store, long long* sp,
-                                             long long ld, unsigned slot_s, unsigned slot_pitch,
-                                             unsigned col, long long& ms0, long long& ms1,
-                                             int& neg) {
-  const int ksm = p.ksm;
-  auto slot_addr = [&](int code, int i) { return slot_s + (unsigned)code * slot_pitch + col + 8u * i; };
-  const Chain ch = cp.chains[cid];
-#pragma unroll
-  for (int i = 0; i < V; ++i) {
-    const long long sc = s + i;
-    const bool pres = !act || cp.present == nullptr || cp.present[sc * cp.n_chains + cid] != 0;
-    long long prev = own_get<V>(S, ch.lane, i);
-    long long lbadd = 0, msv = 0;
-    for (int q = 0; q < ch.B; ++q) {
-      const int k = (cp.perm != nullptr && act) ? (int)cp.perm[sc * cp.perm_ld + ch.perm_off + q] : q;
-      const Member M = cp.members[ch.mem_off + k];
-      long long val = -1;  // start written for member k
-      if (pres) {
-        long long x = prev;
-        for (int e = 0; e < M.npred; ++e) {
-          const int code = cp.preds[M.pred_off + e];
-          long long v = 0;
-          if (code < ksm)
-            asm volatile("ld.shared.s64 %0, [%1];" : "=l"(v) : "r"(slot_addr(code, i)));
-          else if (act)
-            v = p.gslots[(long long)(code - ksm) * p.s_pad + sc];
-          x = lmax(x, v);
-        }
-        long long d = 0;
-        if (act) {
-          const long long at = (long long)(row + k) * p.dense_ld + sc;
-          d = DK == 1 ? (long long)cp.dense32[at] : p.dense64[at];
-        }
-        neg |= (int)(d >> 32);
-        val = x;
-        const long long fin = x + d;
-        prev = fin + M.gap;
-        msv = lmax(msv, fin);
-        lbadd += d;
-      }
-      if (store) __stcs(sp + (long long)k * ld + i, val);
-      if (M.out >= 0) {
-        const long long o = pres ? prev : 0;
-        if (M.out < ksm)
-          asm volatile("st.shared.s64 [%0], %1;" ::"r"(slot_addr(M.out, i)), "l"(o) : "memory");
-        else if (act)
-          p.gslots[(long long)(M.out - ksm) * p.s_pad + sc] = o;
-      }
-    }
-    if (pres) {
-      own_set<V>(S, ch.lane, i, prev);
-      busy_add<V>(S, ch.lane, i, lbadd);
-      if (i == 0) ms0 = lmax(ms0, msv);
-      else ms1 = lmax(ms1, msv);
-    }
-  }
-}
-
 // The kernel body; DDSIM_DISPATCH(h) must expand to the handler dispatch
 // (it sees S, d0, d1, gap, sp, ld, store and the template parameter V).
 // Each thread owns V consecutive scenarios (V = 1 or 2).
-// CH: the graph has permutable chains (chain / no-op records).  Without them
-// the chain code is compiled out, so the hot loop keeps its registers.
 template <int DK, int V, bool CH = false>
-__device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
-                                           const ChainParams* cpp = nullptr) {
+__device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int BD = blockDim.x;
   const int W = BD * V;  // scenarios per CTA
@@ -380,7 +268,6 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
   const unsigned row_pitch = (unsigned)W * ES;
   const int ksm = p.ksm;
 
-
   for (int c = 0; c < nchunks; ++c) {
     const int st = c % kStagesL;
     l_wait(&bars[st], (unsigned)((c / kStagesL) & 1));
@@ -425,15 +312,6 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
       const unsigned w = (unsigned)r.w;
       const unsigned h = w >> 24;
       const unsigned rare = (w >> 16) & 0xffu;
-      if constexpr (CH) {
-        if (rare & (R_CHAIN | R_NOP)) {
-          if (rare & R_CHAIN)
-            chain_record<DK, V>(p, *cpp, S, (int)(short)(r.z & 0xffff), c * kChunkL + j, s, act,
-                                store, sp, ld, slot_s, slot_pitch, col, ms0, ms1, neg);
-          if (store) sp += ld;
-          return;
-        }
-      }
       if (rare & R_PRE) {
         // predecessors that are no longer lane heads (+ ready floor) -> temp lane
         long long x0 = 0, x1 = 0, y0, y1;
@@ -525,4 +403,3 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
 }
 
 }  // namespace ddsim_lanes
-)DDSIM_SRC";
