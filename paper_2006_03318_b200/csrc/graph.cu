@@ -333,9 +333,8 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   // ---- contracted graph (chain -> one node) ---------------------------------
   const int NN = n + NC;
   auto X = [&](int t) { return chain_of[t] >= 0 ? n + chain_of[t] : t; };
-  std::vector<unsigned long long> ckeys;
-  ckeys.reserve(keys.size() + 2 * NC);
-  if (NC == 0) ckeys = keys;  // no chain: the contracted graph is the unique graph
+  std::vector<unsigned long long> ckeys;  // without chains the contracted graph is `keys`
+  if (NC > 0) ckeys.reserve(keys.size() + 2 * NC);
   for (size_t q = 0; NC > 0 && q < keys.size(); ++q) {
     const unsigned long long k = keys[q];
     const int u = (int)(k >> 32), v = (int)(k & 0xffffffffu);
@@ -367,16 +366,15 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     radix_sort_u64(ckeys);
     ckeys.erase(std::unique(ckeys.begin(), ckeys.end()), ckeys.end());
   }
-  std::vector<int> cptr(NN + 1, 0), cadj(ckeys.size()), cindeg(NN, 0);
-  for (unsigned long long k : ckeys) {
+  const std::vector<unsigned long long>& CK = NC > 0 ? ckeys : keys;  // sorted by (u, v)
+  std::vector<int> cptr(NN + 1, 0), cadj(CK.size()), cindeg(NN, 0);
+  for (size_t q = 0; q < CK.size(); ++q) {
+    const unsigned long long k = CK[q];
     cptr[(k >> 32) + 1]++;
     cindeg[k & 0xffffffffu]++;
+    cadj[q] = (int)(k & 0xffffffffu);
   }
   for (int i = 0; i < NN; ++i) cptr[i + 1] += cptr[i];
-  {
-    std::vector<int> fill(cptr.begin(), cptr.end() - 1);
-    for (unsigned long long k : ckeys) cadj[fill[k >> 32]++] = (int)(k & 0xffffffffu);
-  }
   // rank of contracted nodes (tie-break for the initial stack)
   std::vector<int> crank(NN);
   for (int i = 0; i < n; ++i) crank[i] = d->id_rank[i];

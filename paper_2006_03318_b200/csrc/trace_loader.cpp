@@ -89,6 +89,17 @@ struct Err {
 
 inline bool is_ws(char c) { return c == ' ' || c == '\t' || c == '\n' || c == '\r'; }
 
+// bytes that end a plain run inside a JSON string: quote, backslash, controls
+struct StrSpecial {
+  bool t[256] = {};
+  StrSpecial() {
+    for (int c = 0; c < 0x20; ++c) t[c] = true;
+    t[(unsigned char)'"'] = true;
+    t[(unsigned char)'\\'] = true;
+  }
+};
+const StrSpecial kStrSpecial;
+
 struct Lexer {
   const char* s;
   const char* e;
@@ -118,6 +129,7 @@ struct Lexer {
     const char* b = cur;
     bool esc = false;
     for (;;) {
+      while (cur < e && !kStrSpecial.t[(unsigned char)*cur]) ++cur;  // plain bytes
       if (cur >= e) { fail(); return false; }
       unsigned char c = (unsigned char)*cur;
       if (c == '"') break;
@@ -1260,6 +1272,25 @@ void merge_markers(ks_trace& t, std::vector<MarkerChunk>& chunks) {
 bool first_duplicate(const ks_trace& t, int64_t& dup) {
   if (t.n_events < 2) return false;
   const size_t C = t.ev.size();
+  {  // common case: ids strictly increasing in document order -> no duplicate
+    std::vector<char> inc(C, 1);
+    parallel_chunks(C, [&](size_t c) {
+      const auto& v = t.ev[c].id;
+      for (size_t j = 1; j < v.size(); ++j)
+        if (v[j] <= v[j - 1]) { inc[c] = 0; return; }
+    });
+    bool ok = true;
+    int64_t last = INT64_MIN;
+    bool have = false;
+    for (size_t c = 0; c < C && ok; ++c) {
+      if (!inc[c]) { ok = false; break; }
+      if (t.ev[c].id.empty()) continue;
+      if (have && t.ev[c].id.front() <= last) ok = false;
+      last = t.ev[c].id.back();
+      have = true;
+    }
+    if (ok) return false;
+  }
   std::vector<int64_t> los(C, INT64_MAX), his(C, INT64_MIN);
   parallel_chunks(C, [&](size_t c) {
     for (int64_t v : t.ev[c].id) { los[c] = std::min(los[c], v); his[c] = std::max(his[c], v); }
