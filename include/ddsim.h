@@ -204,6 +204,15 @@ int ks_simulate(const ks_graph* g, const ks_scenarios_desc* sc, int policy,
 int ks_simulate_host(const ks_graph* g, const ks_scenarios_desc* sc,
                      int policy, int path, const ks_sim_out* out);
 
+/* The same over several devices of one process: graphs[k] is the graph
+ * frozen on device k (same description, so the same frozen row order); the
+ * scenarios are split into n_graphs contiguous shards simulated concurrently
+ * (one host thread per device), each writing its slice of the HOST outputs
+ * directly -- no inter-GPU exchange is needed.  Synchronous. */
+int ks_simulate_host_multi(const ks_graph* const* graphs, int n_graphs,
+                           const ks_scenarios_desc* sc, int policy, int path,
+                           const ks_sim_out* out);
+
 /* ---- runtime breakdown (breakdown.py:42-111) ---------------------------- */
 enum { KS_BD_CPU = 0, KS_BD_GPU = 1, KS_BD_COMM = 2, KS_BD_CPU_DATALOAD = 3 };
 typedef struct {

@@ -154,6 +154,8 @@ _SIGNATURES = [
     ("ks_graph_destroy", C.c_int, [P]),
     ("ks_simulate", C.c_int, [P, C.POINTER(ScenariosDesc), C.c_int, C.c_int, C.POINTER(SimOut), P]),
     ("ks_simulate_host", C.c_int, [P, C.POINTER(ScenariosDesc), C.c_int, C.c_int, C.POINTER(SimOut)]),
+    ("ks_simulate_host_multi", C.c_int, [P, C.c_int, C.POINTER(ScenariosDesc), C.c_int, C.c_int,
+                                         C.POINTER(SimOut)]),
     ("ks_toposort", C.c_int, [P, P, C.POINTER(C.c_int32)]),
     ("ks_breakdown", C.c_int, [P, C.POINTER(ScenariosDesc), P, C.c_int64, P,
                                C.POINTER(BreakdownDesc), P, P, P]),

@@ -190,10 +190,13 @@ def simulate_batch(frozen: FrozenGraph, table: ScenarioTable, policy: str = "def
                    want_start: bool = True, want_schedule: bool = False,
                    path: int = N.KS_PATH_AUTO, breakdown: bool = False,
                    comm_as_gpu: bool = True, dataload_as_cpu: bool = True,
-                   gaps_as_cpu_busy: bool = True) -> BatchResult:
+                   gaps_as_cpu_busy: bool = True, devices=None) -> BatchResult:
     """Host buffers in/out (ks_simulate_host): the reference-facing call.
     breakdown=True also runs compute_breakdown / per_layer_breakdown for
-    every scenario on the device (ks_breakdown; max-plus graphs)."""
+    every scenario on the device (ks_breakdown; max-plus graphs).
+    devices=[d0, d1, ...]: scenarios split into contiguous shards simulated
+    concurrently on those devices of this process (ks_simulate_host_multi;
+    the graph is replicated per device once)."""
     if breakdown:
         return _simulate_batch_with_breakdown(frozen, table, policy, want_start, comm_as_gpu,
                                               dataload_as_cpu, gaps_as_cpu_busy)
@@ -215,8 +218,16 @@ def simulate_batch(frozen: FrozenGraph, table: ScenarioTable, policy: str = "def
     if sched is not None:
         out.schedule = sched.ctypes.data
         path = N.KS_PATH_LISTSCHED
-    N.check(N.lib().ks_simulate_host(frozen.handle, C.byref(sc), POLICY_IDS[policy], path,
-                                     C.byref(out)), "simulate_batch")
+    if devices is not None and len(devices) > 1:
+        if breakdown:
+            raise Unsupported("breakdown=True runs on one device")
+        graphs = [frozen.on_device(int(d)) for d in devices]
+        arr = (C.c_void_p * len(graphs))(*[gr.handle.value for gr in graphs])
+        N.check(N.lib().ks_simulate_host_multi(arr, len(graphs), C.byref(sc), POLICY_IDS[policy],
+                                               path, C.byref(out)), "simulate_batch")
+    else:
+        N.check(N.lib().ks_simulate_host(frozen.handle, C.byref(sc), POLICY_IDS[policy], path,
+                                         C.byref(out)), "simulate_batch")
     return BatchResult(frozen=frozen, makespan=ms, lane_busy=lb[:, :L],
                        start=None if start is None else start[:rows], schedule=sched)
 

@@ -2022,3 +2022,75 @@ extern "C" int ks_simulate_host(const ks_graph* g, const ks_scenarios_desc* sc, 
   return simulate_host_impl(g, sc, policy, path, out);
   KS_GUARD_END
 }
+
+// Scenario shards over several devices (one host thread per device).  Each
+// shard gets a sub-description whose per-scenario tables are sliced (scale
+// programs rebased, overrides repacked) and whose outputs point into the
+// caller's host buffers at the shard's offset.
+extern "C" int ks_simulate_host_multi(const ks_graph* const* graphs, int n_graphs,
+                                      const ks_scenarios_desc* sc, int policy, int path,
+                                      const ks_sim_out* out) {
+  using namespace ddsim;
+  if (!graphs || n_graphs < 1 || !sc || !out) {
+    set_last_error("ks_simulate_host_multi: bad arguments");
+    return KS_ERR_INVALID;
+  }
+  for (int k = 0; k < n_graphs; ++k) {
+    if (!graphs[k] || graphs[k]->n != graphs[0]->n || graphs[k]->L != graphs[0]->L ||
+        graphs[k]->order != graphs[0]->order) {
+      set_last_error("ks_simulate_host_multi: graphs differ (freeze the same description)");
+      return KS_ERR_INVALID;
+    }
+  }
+  const int S = sc->n_scenarios;
+  const ks_graph* g0 = graphs[0];
+  const int K = std::max(1, std::min(n_graphs, S));
+  std::vector<int> bounds(K + 1, 0);
+  for (int k = 0; k <= K; ++k) bounds[k] = (int)((long long)S * k / K);
+  std::vector<int> rc(K, KS_OK);
+  std::vector<std::string> msg(K);
+  std::vector<std::thread> th;
+  for (int k = 0; k < K; ++k) {
+    th.emplace_back([&, k] {
+      const int s0 = bounds[k], ns = bounds[k + 1] - bounds[k];
+      if (ns == 0) return;
+      ks_scenarios_desc sub = *sc;
+      sub.n_scenarios = ns;
+      std::vector<int64_t> ovr;
+      std::vector<int32_t> sptr;
+      if (sc->dense) {
+        const size_t es = sc->dense_kind == 1 ? 4 : 8;
+        sub.dense = static_cast<const char*>(sc->dense) + es * (size_t)s0;
+      }
+      if (sc->n_overrides > 0) {
+        ovr.resize((size_t)sc->n_overrides * ns);
+        for (int j = 0; j < sc->n_overrides; ++j)
+          memcpy(&ovr[(size_t)j * ns], sc->override + (size_t)j * S + s0, 8 * (size_t)ns);
+        sub.override = ovr.data();
+      }
+      if (sc->scale_ptr) {
+        sptr.resize(ns + 1);
+        for (int j = 0; j <= ns; ++j) sptr[j] = sc->scale_ptr[s0 + j] - sc->scale_ptr[s0];
+        sub.scale_ptr = sptr.data();
+        sub.scale = sc->scale + sc->scale_ptr[s0];
+      }
+      if (sc->chain_perm) sub.chain_perm = sc->chain_perm + (size_t)s0 * sc->perm_ld;
+      if (sc->chain_present) sub.chain_present = sc->chain_present + (size_t)s0 * g0->n_chains;
+      ks_sim_out o = *out;
+      if (out->start) o.start = out->start + s0;
+      if (out->makespan) o.makespan = out->makespan + s0;
+      if (out->lane_busy) o.lane_busy = out->lane_busy + (size_t)s0 * g0->L;
+      if (out->schedule) o.schedule = out->schedule + (size_t)s0 * g0->n;
+      if (out->dispatched) o.dispatched = out->dispatched + s0;
+      rc[k] = ks_simulate_host(graphs[k], &sub, policy, path, &o);
+      if (rc[k] != KS_OK) msg[k] = ks_last_error_detail();
+    });
+  }
+  for (auto& t : th) t.join();
+  for (int k = 0; k < K; ++k)
+    if (rc[k] != KS_OK) {
+      set_last_error("device shard " + std::to_string(k) + ": " + msg[k]);
+      return rc[k];
+    }
+  return KS_OK;
+}

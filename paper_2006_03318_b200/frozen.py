@@ -73,6 +73,9 @@ class FrozenGraph:
             rank[np.argsort(self.ids, kind="stable")] = np.arange(self.n, dtype=np.int32)
         self.id_rank = rank
         self.chains = chains or []
+        self._lane_order = (None if lane_order_ptr is None
+                            else (N.c_i32(lane_order_ptr), N.c_i32(lane_order)))
+        self._replicas: dict = {}
         keep = []
         d = N.GraphDesc()
         d.n_tasks, d.n_lanes = self.n, self.L
@@ -121,6 +124,25 @@ class FrozenGraph:
     @property
     def handle(self):
         return self._h
+
+    def on_device(self, device: int) -> "FrozenGraph":
+        """The same frozen graph (same row order) on another device, built once
+        and cached -- the per-device replicas of a multi-GPU sweep."""
+        if device == self.device:
+            return self
+        rep = self._replicas.get(device)
+        if rep is None:
+            lop, lo = self._lane_order if self._lane_order is not None else (None, None)
+            rep = FrozenGraph(ids=self.ids, duration=self.duration, gap=self.gap, ready=self.ready,
+                              lane=self.lane, priority=self.priority, flags=self.flags,
+                              group=self.group, edge_src=self.edge_src, edge_dst=self.edge_dst,
+                              lane_order_ptr=lop, lane_order=lo, lanes=self.lanes,
+                              chains=self.chains, device=device, task_layers=self.task_layers,
+                              dataload=self.dataload)
+            if not np.array_equal(rep.order, self.order):
+                raise RuntimeError("replica froze to a different row order")
+            self._replicas[device] = rep
+        return rep
 
     def close(self):
         h = getattr(self, "_h", None)

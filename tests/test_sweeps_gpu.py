@@ -163,3 +163,35 @@ def test_removal_inside_permutable_chain():
         assert res.makespan[s] == ms, s
         assert res.start_of(s) == st, s
         assert {str(k): v for k, v in res.lane_busy_of(s).items()} == {str(k): v for k, v in lb.items()}, s
+
+
+@pytest.mark.parametrize("S", [1, 7, 64])
+def test_multi_device_shards_match_single(S):
+    """simulate_batch(devices=...) (ks_simulate_host_multi): contiguous
+    scenario shards per device (two shards on device 0 here -- one GPU per
+    box) give exactly the single-call results, for dense jitter, scale
+    programs and the inserted-task table."""
+    w = _small_training()
+    g = w.graph
+    fz = FrozenGraph.from_graph(g)
+    rng = np.random.default_rng(S)
+    base = fz.duration[fz.order]
+    dense = ((2 * base[:, None] * rng.integers(900, 1101, (fz.n, S)) + 1000) // 2000).astype(np.int32)
+    tabs = [(fz, ScenarioTable(n_scenarios=S, dense=dense))]
+    scen = [[(And([GPU_TASKS, ByLayer(w.layers[s % len(w.layers)])]), "1/2")] for s in range(S)]
+    group_of, ptr, steps = compile_scale_sweep(g, scen)
+    fz2 = FrozenGraph.from_graph(g, group_of=group_of)
+    tabs.append((fz2, ScenarioTable(n_scenarios=S, scale_ptr=ptr, scale=steps)))
+    buckets = w.trace.gradient_buckets
+    B = len([b for b in buckets.buckets() if buckets.layers_of_bucket(b)])
+    cfgs = [{"bandwidth_gbps": bw, "workers": 1 + s % 4} for s, bw in
+            zip(range(S), np.tile([1, 10, 40], S))]
+    perms = np.stack([rng.permutation(B) for _ in range(S)]).astype(np.int16)
+    sw = distributed_sweep(g, buckets, cfgs, perms)
+    tabs.append((sw.frozen, sw.table))
+    for f, t in tabs:
+        one = simulate_batch(f, t)
+        two = simulate_batch(f, t, devices=[0, 0])
+        assert np.array_equal(one.makespan, two.makespan)
+        assert np.array_equal(one.lane_busy, two.lane_busy)
+        assert np.array_equal(one.start, two.start)
