@@ -93,11 +93,16 @@ struct ConcurrentSections {
   std::mutex mu;
   explicit ConcurrentSections(int dev) : device(dev) {}
   template <class F>
-  void run(F f) {
-    th.emplace_back([this, f]() mutable {
+  void run(const char* name, F f) {
+    th.emplace_back([this, f, name]() mutable {
       try {
         if (device >= 0 && !g_compile_only) cudaSetDevice(device);
+        const auto t0 = std::chrono::steady_clock::now();
         f();
+        if (std::getenv("DDSIM_INGEST_TIMING"))
+          std::fprintf(stderr, "[compile_graph]   %-11s %8.3f ms (concurrent)\n", name,
+                       std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0)
+                           .count());
       } catch (...) {
         std::lock_guard<std::mutex> lk(mu);
         err.push_back(std::current_exception());
@@ -268,22 +273,55 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
 
   gt.mark("chains");
   // ---- unique edges ----------------------------------------------------------
-  // sorted unique (u << 32 | v): counting sort by u, then each (short) out list by v
+  // sorted unique (u << 32 | v): counting sort by u, then each (short) out list by v.
+  // Threads own disjoint u ranges: each scans all edges but counts / scatters
+  // only its own sources (no shared counters), then dedupes its range.
   std::vector<unsigned long long> keys(E);
   {
+    unsigned hw = std::thread::hardware_concurrency();
+    int T = (int)std::max<long long>(1, std::min<long long>(hw ? hw : 1, E / (1 << 20)));
+    T = std::min(T, std::max(1, n));
+    std::vector<int> ulo(T + 1);
+    for (int t = 0; t <= T; ++t) ulo[t] = (int)((long long)n * t / T);
     std::vector<long long> cnt((size_t)n + 1, 0);
-    for (long long k = 0; k < E; ++k) cnt[(size_t)d->edge_src[k] + 1]++;
+    auto run = [&](auto fn) {
+      if (T == 1) { fn(0); return; }
+      std::vector<std::thread> th;
+      for (int t = 0; t < T; ++t) th.emplace_back(fn, t);
+      for (auto& x : th) x.join();
+    };
+    run([&](int t) {
+      const int lo = ulo[t], hi = ulo[t + 1];
+      for (long long k = 0; k < E; ++k) {
+        const int u = d->edge_src[k];
+        if (u >= lo && u < hi) cnt[(size_t)u + 1]++;
+      }
+    });
     for (int i = 0; i < n; ++i) cnt[(size_t)i + 1] += cnt[(size_t)i];
-    std::vector<long long> fill(cnt.begin(), cnt.end() - 1);
-    for (long long k = 0; k < E; ++k)
-      keys[(size_t)fill[(size_t)d->edge_src[k]]++] =
-          ((unsigned long long)(unsigned)d->edge_src[k] << 32) | (unsigned)d->edge_dst[k];
-    size_t o = 0;
-    for (int u = 0; u < n; ++u) {
-      auto b = keys.begin() + cnt[(size_t)u], e = keys.begin() + cnt[(size_t)u + 1];
-      if (e - b > 1) std::sort(b, e);
-      for (auto it = b; it != e; ++it)
-        if (it == b || *it != *(it - 1)) keys[o++] = *it;
+    std::vector<long long> kept(T, 0);
+    run([&](int t) {
+      const int lo = ulo[t], hi = ulo[t + 1];
+      std::vector<long long> fill(cnt.begin() + lo, cnt.begin() + hi);
+      for (long long k = 0; k < E; ++k) {
+        const int u = d->edge_src[k];
+        if (u >= lo && u < hi)
+          keys[(size_t)fill[(size_t)(u - lo)]++] =
+              ((unsigned long long)(unsigned)u << 32) | (unsigned)d->edge_dst[k];
+      }
+      long long o = cnt[(size_t)lo];  // dedupe in place within the range
+      for (int u = lo; u < hi; ++u) {
+        auto b = keys.begin() + cnt[(size_t)u], e = keys.begin() + cnt[(size_t)u + 1];
+        if (e - b > 1) std::sort(b, e);
+        for (auto it = b; it != e; ++it)
+          if (it == b || *it != *(it - 1)) keys[(size_t)o++] = *it;
+      }
+      kept[t] = o - cnt[(size_t)lo];
+    });
+    size_t o = (size_t)kept[0];  // compact the ranges (range 0 is in place)
+    for (int t = 1; t < T; ++t) {
+      const size_t from = (size_t)cnt[(size_t)ulo[t]];
+      if (from != o) std::memmove(&keys[o], &keys[from], (size_t)kept[t] * sizeof(keys[0]));
+      o += (size_t)kept[t];
     }
     keys.resize(o);
   }
@@ -511,7 +549,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   std::vector<unsigned char> flags_r(n);
   std::vector<unsigned> group_r(n);
   ConcurrentSections sect(g->device);
-  sect.run([&] {
+  sect.run("records", [&] {
   // ---- value live ranges -------------------------------------------------------
   // values: task t (0..n-1) -> rel(t); chain tail value n + c.
   const int NV = n + NC;
@@ -625,7 +663,38 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   };
   int perm_off = 0;
   std::vector<int> preds;
-  for (int i = 0; i < R; ++i) {
+  if (NC == 0) {  // no chains: records are independent -> fill them in parallel
+    std::vector<int> eoff(R + 1, 0);
+    for (int i = 0; i < R; ++i) {
+      const int x = corder[i];
+      eoff[i + 1] = eoff[i] + std::max(0, pptr[x + 1] - pptr[x] - 2);
+    }
+    extra.resize(eoff[R]);
+    host_parallel_for(R, [&](long long b, long long e) {
+      for (int i = (int)b; i < (int)e; ++i) {
+        const int t = corder[i];
+        NodeRec r;
+        memset(&r, 0, sizeof(r));
+        r.dur = d->duration[t];
+        r.gap = d->gap[t];
+        r.ready = d->ready_time ? d->ready_time[t] : 0;
+        r.out_slot = final_slot(t);
+        const int p0 = pptr[t], np = pptr[t + 1] - p0;
+        r.pred0 = np > 0 ? final_slot(padj[p0]) : -1;
+        r.pred1 = np > 1 ? final_slot(padj[p0 + 1]) : -1;
+        r.nextra = np > 2 ? np - 2 : 0;
+        r.extra_off = r.nextra ? eoff[i] : 0;
+        for (int k = 2; k < np; ++k) extra[eoff[i] + k - 2] = final_slot(padj[p0 + k]);
+        r.group = d->group ? d->group[t] : 0u;
+        r.ovr_row = -1;
+        r.lane = d->lane[t];
+        r.row = g->row_of[t];
+        r.kind = 0;
+        prog[i] = r;
+      }
+    });
+  }
+  for (int i = 0; i < R && NC > 0; ++i) {
     const int x = corder[i];
     if (x < n) {
       preds.clear();
@@ -662,9 +731,13 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   }
   g->perm_ld = perm_off;
   g->n_rec = R;
+  g->d_prog = dev_upload(prog);  // uploads overlap the other builders
+  g->d_extra = dev_upload(extra);
+  g->d_chains = dev_upload(chains);
+  g->d_members = dev_upload(members);
 
   });
-  sect.run([&] {
+  sect.run("dense-prog", [&] {
   // ---- dense program: register forwarding for the two previous records ----
   if (NC == 0 && L <= 127 && nonneg) {
     std::vector<int> pos(n, -1);
@@ -780,7 +853,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   }
 
   });
-  sect.run([&] {
+  sect.run("lanes-prog", [&] {
   // ---- lane-register program (maxplus_lanes.cu) ------------------------------
   // One emitted record per frozen row: a task, or for a permutable chain a
   // chain record on its first member row followed by B-1 no-op rows (so the
@@ -989,7 +1062,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   }
 
   });
-  sect.run([&] {
+  sect.run("listsched", [&] {
   // ---- list-scheduler arrays (frozen rows, multiset edges) -------------------
   std::vector<int> esr(E), edr(E);  // edge endpoints as frozen rows
   host_parallel_for(E, [&](long long b, long long e) {
@@ -1021,14 +1094,6 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   }
   });
 
-  });
-  sect.join();
-  gt.mark("programs");
-  // ---- upload -----------------------------------------------------------------
-  g->d_prog = dev_upload(prog);
-  g->d_extra = dev_upload(extra);
-  g->d_chains = dev_upload(chains);
-  g->d_members = dev_upload(members);
   g->d_child_ptr = dev_upload(ch_ptr);
   g->d_child = dev_upload(ch_adj);
   g->d_indeg = dev_upload(indeg);
@@ -1040,7 +1105,10 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   g->d_prio = dev_upload(prio_r);
   g->d_flags = dev_upload(flags_r);
   g->d_group = dev_upload(group_r);
-
+  });
+  sect.join();
+  gt.mark("programs");
+  // ---- upload -----------------------------------------------------------------
   gt.mark("upload");
   // ---- breakdown geometry -------------------------------------------------------
   for (int i = 0; i < n; ++i)
