@@ -187,12 +187,18 @@ def run_ours(args):
     import torch
 
     ws, rank, local = _dist()
-    dev = local
+    # test hooks for the multi-rank flow on a one-GPU box (never set by the driver):
+    # DDSIM_BENCH_SAME_DEVICE=1 puts every rank on device 0, DDSIM_BENCH_BACKEND=gloo
+    dev = 0 if os.environ.get("DDSIM_BENCH_SAME_DEVICE") else local
     torch.cuda.set_device(dev)
     if ws > 1:
         import torch.distributed as dist
 
-        dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        backend = os.environ.get("DDSIM_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev))
+        else:
+            dist.init_process_group(backend)
     from paper_2006_03318_b200 import _native as N
     from paper_2006_03318_b200.batch import ScenarioTable, simulate_batch_device
 
@@ -259,7 +265,8 @@ def run_ours(args):
         g1.record(stream)
         torch.cuda.synchronize()
         assert torch.equal(bufs[rank], flat)
-        gather = {"collective": "all_gather (nccl)", "bytes_per_rank": flat.numel() * 8,
+        gather = {"collective": f"all_gather ({dist.get_backend()})",
+                  "bytes_per_rank": flat.numel() * 8,
                   "ms": g0.elapsed_time(g1)}
     updates_per_step = rows * S
     total = updates_per_step * args.steps * ws
@@ -345,7 +352,8 @@ def run_ours(args):
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": updates_per_step * BYTES_PER_UPDATE,
-                         "traffic": _ncu_traffic("ddsim_lanes_jit"),
+                         # ncu capture of the default workload (65,536 scenarios per GPU)
+                         "traffic": _ncu_traffic("ddsim_lanes_jit") if S == S_PER_GPU else None,
                          "pattern_copy_gbs": pattern_gbs,
                          "pattern_frac": achieved / pattern_gbs,
                          "pattern": "ks_probe_widen: int32 -> int64 stream over the same "
