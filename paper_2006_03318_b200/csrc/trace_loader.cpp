@@ -1005,23 +1005,37 @@ int64_t first_elem_brace(const char* s, int64_t b, int64_t e, bool in_str, int64
   return -1;
 }
 
-PreScan prescan(const char* s, int64_t n, int T) {
+// K work items on T threads (atomic work counter; items are independent)
+template <class F>
+void pool_for(size_t K, int T, F fn) {
+  const int W = (int)std::max<size_t>(1, std::min<size_t>((size_t)std::max(T, 1), K));
+  if (W == 1) {
+    for (size_t k = 0; k < K; ++k) fn(k);
+    return;
+  }
+  std::atomic<size_t> next{0};
+  std::vector<std::thread> th;
+  for (int w = 0; w < W; ++w)
+    th.emplace_back([&] {
+      for (size_t k; (k = next.fetch_add(1)) < K;) fn(k);
+    });
+  for (auto& t : th) t.join();
+}
+
+// K pre-scan chunks (fine-grained, so arrays much smaller than n / T still
+// get many split points) on T threads.
+PreScan prescan(const char* s, int64_t n, int K0, int T) {
   auto tp0 = std::chrono::steady_clock::now();
   PreScan ps;
-  int64_t step = ((n + T - 1) / T + 63) / 64 * 64;
-  size_t K = (size_t)T;
+  int64_t step = ((n + K0 - 1) / K0 + 63) / 64 * 64;
+  size_t K = (size_t)K0;
   ps.begin.resize(K + 1);
   for (size_t k = 0; k <= K; ++k) ps.begin[k] = std::min<int64_t>((int64_t)k * step, n);
   ps.parity.assign(K, 0);
   ps.bs_out.assign(K, 0);
   ps.dA.assign(K, 0);
   ps.dB.assign(K, 0);
-  {
-    std::vector<std::thread> th;
-    for (size_t k = 0; k < K; ++k)
-      th.emplace_back(prescan_chunk, s, ps.begin[k], ps.begin[k + 1], std::ref(ps), k);
-    for (auto& t : th) t.join();
-  }
+  pool_for(K, T, [&](size_t k) { prescan_chunk(s, ps.begin[k], ps.begin[k + 1], ps, k); });
   if (std::getenv("DDSIM_TRACE_TIMING"))
     std::fprintf(stderr, "[prescan] pass1 %.3f s\n",
                  std::chrono::duration<double>(std::chrono::steady_clock::now() - tp0).count());
@@ -1033,14 +1047,9 @@ PreScan prescan(const char* s, int64_t n, int T) {
   }
   auto tq0 = std::chrono::steady_clock::now();
   ps.first2.assign(K, -1);
-  {
-    std::vector<std::thread> th;
-    for (size_t k = 0; k < K; ++k)
-      th.emplace_back([&, k] {
-        ps.first2[k] = first_elem_brace(s, ps.begin[k], ps.begin[k + 1], ps.in_str[k], ps.depth[k]);
-      });
-    for (auto& t : th) t.join();
-  }
+  pool_for(K, T, [&](size_t k) {
+    ps.first2[k] = first_elem_brace(s, ps.begin[k], ps.begin[k + 1], ps.in_str[k], ps.depth[k]);
+  });
   if (std::getenv("DDSIM_TRACE_TIMING"))
     std::fprintf(stderr, "[prescan] pass2 %.3f s\n",
                  std::chrono::duration<double>(std::chrono::steady_clock::now() - tq0).count());
@@ -1113,7 +1122,7 @@ struct ArrayParse {
 
 template <class Chunk, class Elem>
 ArrayParse<Chunk, Elem> parse_array(const char* s, int64_t n, int64_t open,
-                                    const std::vector<int64_t>& sp, Elem elem) {
+                                    const std::vector<int64_t>& sp, Elem elem, int T) {
   ArrayParse<Chunk, Elem> ap;
   size_t K = sp.size() + 1;
   ap.chunks.resize(K);
@@ -1123,13 +1132,7 @@ ArrayParse<Chunk, Elem> parse_array(const char* s, int64_t n, int64_t open,
     int64_t stop = k < sp.size() ? sp[k] : -1;
     res[k] = parse_slice(s, n, from, stop, k == 0, ap.chunks[k], elem);
   };
-  if (K == 1) {
-    run(0);
-  } else {
-    std::vector<std::thread> th;
-    for (size_t k = 0; k < K; ++k) th.emplace_back(run, k);
-    for (auto& t : th) t.join();
-  }
+  pool_for(K, T, run);
   int64_t idx = 0;
   size_t used = 0;
   for (size_t k = 0; k < K; ++k) {
@@ -1456,7 +1459,12 @@ int ks_trace_parse(const char* text, int64_t len, int n_threads, ks_trace** out,
   PreScan ps;
   bool scanned = false;
   auto need_scan = [&] {
-    if (!scanned && T > 1) { ps = prescan(text, len, T * 4); scanned = true; }
+    if (!scanned && T > 1) {
+      // ~2 MB chunks (at least 4 per thread, at most 4096)
+      const int64_t k0 = std::max<int64_t>((int64_t)T * 4, std::min<int64_t>(4096, len >> 21));
+      ps = prescan(text, len, (int)k0, T);
+      scanned = true;
+    }
   };
 
   Lexer L(text, text + len, text);
@@ -1476,7 +1484,7 @@ int ks_trace_parse(const char* text, int64_t len, int n_threads, ks_trace** out,
       sp = split_points(ps, open);
       tick("prescan");
     }
-    auto ap = parse_array<ChunkT>(text, len, open, sp, elem);
+    auto ap = parse_array<ChunkT>(text, len, open, sp, elem, T);
     if (ap.syntax) {
       L.cur = text + std::max<int64_t>(ap.syntax_pos, 0);
       L.fail();
