@@ -8,6 +8,8 @@
 
 #include "../../include/ddsim.h"
 
+#include "host_alloc.h"
+
 namespace ddsim {
 
 // One instruction of the compiled max-plus program: a task, or a permutable

@@ -57,8 +57,9 @@ static void fail(int code, const std::string& msg) { throw KsError{code, msg}; }
 // the compiler itself); such handles cannot simulate.
 static bool g_compile_only = false;
 
-template <class T>
-static T* dev_upload(const std::vector<T>& v) {
+template <class V>
+static auto dev_upload(const V& v) -> typename V::value_type* {
+  using T = typename V::value_type;
   if (v.empty() || g_compile_only) return nullptr;
   T* p = nullptr;
   CUDA_TRY(cudaMalloc(&p, v.size() * sizeof(T)));
@@ -139,10 +140,10 @@ struct ks_graph {
   int n_chains = 0;
   int perm_ld = 0;
   bool rows_are_records = true;  // no chains: record i writes row i
-  std::vector<int> order;        // frozen row -> input index
-  std::vector<int> row_of;       // input index -> frozen row
-  std::vector<int> level;        // per frozen row
-  std::vector<int> rank_row;     // id rank per frozen row
+  hvec<int> order;        // frozen row -> input index
+  hvec<int> row_of;       // input index -> frozen row
+  hvec<int> level;        // per frozen row
+  hvec<int> rank_row;     // id rank per frozen row
   // lane-register program (chained, <= 4 lanes, no chains)
   bool has_lanes = false;
   int ln_rec = 0;          // lanes records (= frozen rows)
@@ -206,7 +207,7 @@ struct DevGuard {
 
 // LSD radix sort of 64-bit keys, 16-bit digits; digits that are constant
 // across all keys are skipped (edge keys are (u << 32 | v) with u, v < n).
-static void radix_sort_u64(std::vector<unsigned long long>& a) {
+static void radix_sort_u64(hvec<unsigned long long>& a) {
   const size_t n = a.size();
   if (n < 4096) {
     std::sort(a.begin(), a.end());
@@ -214,7 +215,7 @@ static void radix_sort_u64(std::vector<unsigned long long>& a) {
   }
   unsigned long long all_or = 0, all_and = ~0ull;
   for (unsigned long long x : a) { all_or |= x; all_and &= x; }
-  std::vector<unsigned long long> b(n);
+  hvec<unsigned long long> b(n);
   std::vector<size_t> cnt(65536);
   for (int sh = 0; sh < 64; sh += 16) {
     if ((((all_or ^ all_and) >> sh) & 0xffffull) == 0) continue;  // digit constant
@@ -258,8 +259,8 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
 
   // ---- chains (inserted-task table) ---------------------------------------
   const int NC = d->n_chains;
-  std::vector<int> chain_of(n, -1);
-  std::vector<int> ch_lane(NC, -1);
+  hvec<int> chain_of(n, -1);
+  hvec<int> ch_lane(NC, -1);
   for (int c = 0; c < NC; ++c) {
     for (int k = d->chain_ptr[c]; k < d->chain_ptr[c + 1]; ++k) {
       const int m = d->chain_member[k];
@@ -276,14 +277,14 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   // sorted unique (u << 32 | v): counting sort by u, then each (short) out list by v.
   // Threads own disjoint u ranges: each scans all edges but counts / scatters
   // only its own sources (no shared counters), then dedupes its range.
-  std::vector<unsigned long long> keys(E);
+  hvec<unsigned long long> keys(E);
   {
     unsigned hw = std::thread::hardware_concurrency();
     int T = (int)std::max<long long>(1, std::min<long long>(hw ? hw : 1, E / (1 << 20)));
     T = std::min(T, std::max(1, n));
-    std::vector<int> ulo(T + 1);
+    hvec<int> ulo(T + 1);
     for (int t = 0; t <= T; ++t) ulo[t] = (int)((long long)n * t / T);
-    std::vector<long long> cnt((size_t)n + 1, 0);
+    hvec<long long> cnt((size_t)n + 1, 0);
     auto run = [&](auto fn) {
       if (T == 1) { fn(0); return; }
       std::vector<std::thread> th;
@@ -298,10 +299,10 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
       }
     });
     for (int i = 0; i < n; ++i) cnt[(size_t)i + 1] += cnt[(size_t)i];
-    std::vector<long long> kept(T, 0);
+    hvec<long long> kept(T, 0);
     run([&](int t) {
       const int lo = ulo[t], hi = ulo[t + 1];
-      std::vector<long long> fill(cnt.begin() + lo, cnt.begin() + hi);
+      hvec<long long> fill(cnt.begin() + lo, cnt.begin() + hi);
       for (long long k = 0; k < E; ++k) {
         const int u = d->edge_src[k];
         if (u >= lo && u < hi)
@@ -326,7 +327,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     keys.resize(o);
   }
   g->n_edges_unique = (int)keys.size();
-  std::vector<int> optr(n + 1, 0);  // out-edge ranges of the sorted unique keys
+  hvec<int> optr(n + 1, 0);  // out-edge ranges of the sorted unique keys
   for (unsigned long long k : keys) optr[(k >> 32) + 1]++;
   for (int i = 0; i < n; ++i) optr[i + 1] += optr[i];
   auto has_edge = [&](int u, int v) {
@@ -337,9 +338,9 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   gt.mark("unique-edges");
   // ---- lane chaining check ---------------------------------------------------
   bool chained = d->lane_order_ptr != nullptr;
-  std::vector<int> lane_succ(n, -1);
+  hvec<int> lane_succ(n, -1);
   if (chained) {
-    std::vector<char> seen(n, 0);
+    hvec<char> seen(n, 0);
     for (int l = 0; l < L && chained; ++l) {
       int prev = -1;
       for (int k = d->lane_order_ptr[l]; k < d->lane_order_ptr[l + 1]; ++k) {
@@ -371,7 +372,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   // ---- contracted graph (chain -> one node) ---------------------------------
   const int NN = n + NC;
   auto X = [&](int t) { return chain_of[t] >= 0 ? n + chain_of[t] : t; };
-  std::vector<unsigned long long> ckeys;  // without chains the contracted graph is `keys`
+  hvec<unsigned long long> ckeys;  // without chains the contracted graph is `keys`
   if (NC > 0) ckeys.reserve(keys.size() + 2 * NC);
   for (size_t q = 0; NC > 0 && q < keys.size(); ++q) {
     const unsigned long long k = keys[q];
@@ -404,8 +405,8 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     radix_sort_u64(ckeys);
     ckeys.erase(std::unique(ckeys.begin(), ckeys.end()), ckeys.end());
   }
-  const std::vector<unsigned long long>& CK = NC > 0 ? ckeys : keys;  // sorted by (u, v)
-  std::vector<int> cptr(NN + 1, 0), cadj(CK.size()), cindeg(NN, 0);
+  const hvec<unsigned long long>& CK = NC > 0 ? ckeys : keys;  // sorted by (u, v)
+  hvec<int> cptr(NN + 1, 0), cadj(CK.size()), cindeg(NN, 0);
   for (size_t q = 0; q < CK.size(); ++q) {
     const unsigned long long k = CK[q];
     cptr[(k >> 32) + 1]++;
@@ -414,7 +415,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   }
   for (int i = 0; i < NN; ++i) cptr[i + 1] += cptr[i];
   // rank of contracted nodes (tie-break for the initial stack)
-  std::vector<int> crank(NN);
+  hvec<int> crank(NN);
   for (int i = 0; i < n; ++i) crank[i] = d->id_rank[i];
   for (int c = 0; c < NC; ++c) {
     int r = INT32_MAX;
@@ -426,16 +427,16 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
 
   gt.mark("contract");
   // ---- depth-first Kahn (LIFO frontier) --------------------------------------
-  std::vector<int> corder;
+  hvec<int> corder;
   corder.reserve(NN);
   {
-    std::vector<int> indeg = cindeg;
-    std::vector<int> init;
+    hvec<int> indeg = cindeg;
+    hvec<int> init;
     for (int i = 0; i < NN; ++i)  // chain members are represented by their chain node
       if (indeg[i] == 0 && !(i < n && chain_of[i] >= 0)) init.push_back(i);
     std::sort(init.begin(), init.end(), [&](int a, int b) { return crank[a] > crank[b]; });
-    std::vector<int> stack(init);
-    std::vector<int> cross;
+    hvec<int> stack(init);
+    hvec<int> cross;
     while (!stack.empty()) {
       const int x = stack.back();
       stack.pop_back();
@@ -462,8 +463,8 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   // ---- frozen rows ----------------------------------------------------------
   g->order.clear();
   g->order.reserve(n);
-  std::vector<int> rec_first_row(R);
-  std::vector<char> placed(n, 0);
+  hvec<int> rec_first_row(R);
+  hvec<char> placed(n, 0);
   for (int i = 0; i < R; ++i) {
     const int x = corder[i];
     rec_first_row[i] = (int)g->order.size();
@@ -480,7 +481,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   }
   g->n_ordered = (int)g->order.size();
   {
-    std::vector<int> rest;
+    hvec<int> rest;
     for (int i = 0; i < n; ++i)
       if (!placed[i]) rest.push_back(i);
     std::sort(rest.begin(), rest.end(),
@@ -495,14 +496,14 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
 
   gt.mark("rows");
   // ---- unique preds per task (for records) -----------------------------------
-  std::vector<int> pptr(n + 1, 0), padj(keys.size());
+  hvec<int> pptr(n + 1, 0), padj(keys.size());
   for (unsigned long long k : keys) pptr[(k & 0xffffffffu) + 1]++;
   for (int i = 0; i < n; ++i) pptr[i + 1] += pptr[i];
   {
-    std::vector<int> fill(pptr.begin(), pptr.end() - 1);
+    hvec<int> fill(pptr.begin(), pptr.end() - 1);
     for (unsigned long long k : keys) padj[fill[k & 0xffffffffu]++] = (int)(k >> 32);
   }
-  std::vector<int> tail_of(n, -1);  // task -> chain whose tail it is
+  hvec<int> tail_of(n, -1);  // task -> chain whose tail it is
   for (int c = 0; c < NC; ++c) {
     const int t = d->chain_tail ? d->chain_tail[c] : -1;
     if (t >= 0) tail_of[t] = c;
@@ -510,9 +511,9 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
 
   gt.mark("preds");
   // ---- levels ------------------------------------------------------------------
-  std::vector<int> clevel(NN, 0);
+  hvec<int> clevel(NN, 0);
   {
-    std::vector<int> rec_of(NN, -1);
+    hvec<int> rec_of(NN, -1);
     for (int i = 0; i < R; ++i) rec_of[corder[i]] = i;
     int maxl = 0;
     for (int i = 0; i < R; ++i) {
@@ -537,23 +538,23 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   gt.mark("levels");
   // ---- the four builders below (general records, dense program, lane program,
   // list-scheduler arrays) read only the shared graph above: run concurrently
-  std::vector<NodeRec> prog(R), members;
-  std::vector<int> extra;
-  std::vector<ChainDesc> chains(NC);
+  hvec<NodeRec> prog(R), members;
+  hvec<int> extra;
+  hvec<ChainDesc> chains(NC);
   bool nonneg = true;
   for (int i = 0; i < n && nonneg; ++i)
     if (d->gap[i] < 0 || (d->ready_time && d->ready_time[i] < 0)) nonneg = false;
-  std::vector<int> ch_ptr(n + 1, 0), ch_adj(E), indeg(n, 0);
-  std::vector<int> lane_r(n), rank_r(n), prio_r(n);
-  std::vector<long long> dur_r(n), gap_r(n), ready_r(n);
-  std::vector<unsigned char> flags_r(n);
-  std::vector<unsigned> group_r(n);
+  hvec<int> ch_ptr(n + 1, 0), ch_adj(E), indeg(n, 0);
+  hvec<int> lane_r(n), rank_r(n), prio_r(n);
+  hvec<long long> dur_r(n), gap_r(n), ready_r(n);
+  hvec<unsigned char> flags_r(n);
+  hvec<unsigned> group_r(n);
   ConcurrentSections sect(g->device);
   sect.run("records", [&] {
   // ---- value live ranges -------------------------------------------------------
   // values: task t (0..n-1) -> rel(t); chain tail value n + c.
   const int NV = n + NC;
-  std::vector<int> rec_of_task(n, -1), rec_of_chain(NC, -1);
+  hvec<int> rec_of_task(n, -1), rec_of_chain(NC, -1);
   for (int i = 0; i < R; ++i) {
     const int x = corder[i];
     if (x < n)
@@ -562,11 +563,11 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
       rec_of_chain[x - n] = i;
   }
   auto rec_of_val = [&](int t) { return chain_of[t] >= 0 ? rec_of_chain[chain_of[t]] : rec_of_task[t]; };
-  std::vector<int> last_use(NV, -1);
+  hvec<int> last_use(NV, -1);
   // inputs of each record (flat CSR: rin_ptr / rin)
-  std::vector<int> rin_ptr(R + 1, 0), rin;
+  hvec<int> rin_ptr(R + 1, 0), rin;
   rin.reserve(keys.size() + 2 * (size_t)NC);
-  std::vector<int> in;
+  hvec<int> in;
   for (int i = 0; i < R; ++i) {
     const int x = corder[i];
     in.clear();
@@ -592,9 +593,9 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   }
 
   // ---- slot allocation (linear scan, allocate-then-free) ----------------------
-  std::vector<int> slot(NV, -1);
-  std::vector<char> in_glob(NV, 0);
-  std::priority_queue<int, std::vector<int>, std::greater<int>> free_s, free_g;
+  hvec<int> slot(NV, -1);
+  hvec<char> in_glob(NV, 0);
+  std::priority_queue<int, hvec<int>, std::greater<int>> free_s, free_g;
   int next_s = 0, next_g = 0;
   auto alloc = [&](int v, int i) {
     if (last_use[v] < 0) return;  // nobody reads it
@@ -638,7 +639,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   auto final_slot = [&](int v) { return slot[v] < 0 ? -1 : (in_glob[v] ? g->ksm + slot[v] : slot[v]); };
 
   // ---- records -----------------------------------------------------------------
-  auto make_task_rec = [&](int t, const std::vector<int>& preds) {
+  auto make_task_rec = [&](int t, const hvec<int>& preds) {
     NodeRec r;
     memset(&r, 0, sizeof(r));
     r.dur = d->duration[t];
@@ -662,9 +663,9 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     return r;
   };
   int perm_off = 0;
-  std::vector<int> preds;
+  hvec<int> preds;
   if (NC == 0) {  // no chains: records are independent -> fill them in parallel
-    std::vector<int> eoff(R + 1, 0);
+    hvec<int> eoff(R + 1, 0);
     for (int i = 0; i < R; ++i) {
       const int x = corder[i];
       eoff[i + 1] = eoff[i] + std::max(0, pptr[x + 1] - pptr[x] - 2);
@@ -740,9 +741,9 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   sect.run("dense-prog", [&] {
   // ---- dense program: register forwarding for the two previous records ----
   if (NC == 0 && L <= 127 && nonneg) {
-    std::vector<int> pos(n, -1);
+    hvec<int> pos(n, -1);
     for (int i = 0; i < R; ++i) pos[corder[i]] = i;
-    std::vector<int> far_use(n, -1);  // last consumer more than 2 records later
+    hvec<int> far_use(n, -1);  // last consumer more than 2 records later
     for (int i = 0; i < R; ++i) {
       const int v = corder[i];
       for (int k = pptr[v]; k < pptr[v + 1]; ++k) {
@@ -750,17 +751,17 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
         if (i - pos[u] > 2) far_use[u] = std::max(far_use[u], i);
       }
     }
-    std::vector<int> dslot(n, -1);
-    std::vector<char> dglob(n, 0);
-    std::priority_queue<int, std::vector<int>, std::greater<int>> fs, fg;
+    hvec<int> dslot(n, -1);
+    hvec<char> dglob(n, 0);
+    std::priority_queue<int, hvec<int>, std::greater<int>> fs, fg;
     int ns = 0, ngl = 0;
-    std::vector<int> fa_ptr(R + 1, 0), fa;  // values freed after record i (CSR)
+    hvec<int> fa_ptr(R + 1, 0), fa;  // values freed after record i (CSR)
     for (int i = 0; i < R; ++i)
       if (far_use[corder[i]] >= 0) fa_ptr[far_use[corder[i]] + 1]++;
     for (int i = 0; i < R; ++i) fa_ptr[i + 1] += fa_ptr[i];
     fa.resize(fa_ptr[R]);
     {
-      std::vector<int> fill(fa_ptr.begin(), fa_ptr.end() - 1);
+      hvec<int> fill(fa_ptr.begin(), fa_ptr.end() - 1);
       for (int i = 0; i < R; ++i)
         if (far_use[corder[i]] >= 0) fa[fill[far_use[corder[i]]]++] = corder[i];
     }
@@ -787,12 +788,12 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     }
     g->dksm = ns;
     g->dkglob = ngl;
-    std::vector<int> lane_last(L, -1);
+    hvec<int> lane_last(L, -1);
     for (int i = 0; i < R; ++i) lane_last[d->lane[corder[i]]] = i;
-    std::vector<DenseRec> dprog(R);
-    std::vector<int> side_off(R + 1, 0);
-    std::vector<int> side_slots;
-    std::vector<long long> side_ready;
+    hvec<DenseRec> dprog(R);
+    hvec<int> side_off(R + 1, 0);
+    hvec<int> side_slots;
+    hvec<long long> side_ready;
     bool any_ready = false;
     bool ok = ns + ngl < 32000;
     for (int i = 0; i < R && ok; ++i) {
@@ -863,7 +864,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   // reads it as its own lane).
   if (chained && L <= 4 && nonneg && g->n_ordered == n && NC < 32768) {
     const int RE = n;  // emitted records == frozen rows
-    std::vector<int> ekind(RE, 0), eid(RE, -1);  // 0 task, 1 chain (eid = chain), 2 no-op
+    hvec<int> ekind(RE, 0), eid(RE, -1);  // 0 task, 1 chain (eid = chain), 2 no-op
     for (int i = 0; i < R; ++i) {
       const int x = corder[i];
       const int r0 = rec_first_row[i];
@@ -877,10 +878,10 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
       }
     }
     // which predecessor reads are lane heads at read time?
-    std::vector<int> head(L, -1);          // task id, or -2 - c after chain c
-    std::vector<int> far_use(n, -1);       // last slot read of each task value
-    std::vector<unsigned> hmask(RE, 0);
-    std::vector<int> sp_ptr(RE + 1, 0), sp_list;  // slot-read predecessors per record (CSR)
+    hvec<int> head(L, -1);          // task id, or -2 - c after chain c
+    hvec<int> far_use(n, -1);       // last slot read of each task value
+    hvec<unsigned> hmask(RE, 0);
+    hvec<int> sp_ptr(RE + 1, 0), sp_list;  // slot-read predecessors per record (CSR)
     for (int r = 0; r < RE; ++r) {
       if (ekind[r] == 0) {
         const int v = eid[r];
@@ -908,9 +909,9 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
       }
       sp_ptr[r + 1] = (int)sp_list.size();
     }
-    std::vector<int> lslot(n, -1);
-    std::vector<char> lglob(n, 0);
-    std::priority_queue<int, std::vector<int>, std::greater<int>> fs, fg;
+    hvec<int> lslot(n, -1);
+    hvec<char> lglob(n, 0);
+    std::priority_queue<int, hvec<int>, std::greater<int>> fs, fg;
     int ns = 0, ngl = 0;
     auto for_values = [&](int r, auto fn) {  // task values produced by record r
       if (ekind[r] == 0) {
@@ -920,13 +921,13 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
         for (int k = d->chain_ptr[c]; k < d->chain_ptr[c + 1]; ++k) fn(d->chain_member[k]);
       }
     };
-    std::vector<int> fa_ptr(RE + 1, 0), fa;  // values freed after record r (CSR)
+    hvec<int> fa_ptr(RE + 1, 0), fa;  // values freed after record r (CSR)
     for (int r = 0; r < RE; ++r)
       for_values(r, [&](int v) { if (far_use[v] >= 0) fa_ptr[far_use[v] + 1]++; });
     for (int r = 0; r < RE; ++r) fa_ptr[r + 1] += fa_ptr[r];
     fa.resize(fa_ptr[RE]);
     {
-      std::vector<int> fill(fa_ptr.begin(), fa_ptr.end() - 1);
+      hvec<int> fill(fa_ptr.begin(), fa_ptr.end() - 1);
       for (int r = 0; r < RE; ++r)
         for_values(r, [&](int v) { if (far_use[v] >= 0) fa[fill[far_use[v]]++] = v; });
     }
@@ -952,14 +953,14 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
       for (int q = fa_ptr[r]; q < fa_ptr[r + 1]; ++q) (lglob[fa[q]] ? fg : fs).push(lslot[fa[q]]);
     }
     auto code_of = [&](int u) { return lglob[u] ? ns + lslot[u] : lslot[u]; };
-    std::vector<int> lane_last(L, -1);
+    hvec<int> lane_last(L, -1);
     for (int r = 0; r < RE; ++r)
       if (ekind[r] == 0) lane_last[d->lane[eid[r]]] = r;
-    std::vector<LaneRec> lprog(RE);
-    std::vector<int> lside_off(RE + 1, 0), lside_slots;
-    std::vector<LaneChainDev> lchains(NC);
-    std::vector<LaneMemberDev> lmembers;
-    std::vector<int> lpreds;
+    hvec<LaneRec> lprog(RE);
+    hvec<int> lside_off(RE + 1, 0), lside_slots;
+    hvec<LaneChainDev> lchains(NC);
+    hvec<LaneMemberDev> lmembers;
+    hvec<int> lpreds;
     bool any_ready = false;
     for (int r = 0; r < RE; ++r) {
       LaneRec rec;
@@ -1030,7 +1031,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     }
     // chain members with ready floors stay on the general kernel
     if (ns + ngl < 32000 && !(NC > 0 && any_ready)) {
-      std::vector<long long> freq(256, 0);
+      hvec<long long> freq(256, 0);
       for (int r = 0; r < RE; ++r)
         if (ekind[r] == 0) freq[lprog[r].h]++;
       g->lane_codes.clear();
@@ -1038,7 +1039,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
         if (freq[c]) g->lane_codes.push_back(c);
       std::stable_sort(g->lane_codes.begin(), g->lane_codes.end(),
                        [&](int a, int b) { return freq[a] > freq[b]; });
-      std::vector<long long> lready;
+      hvec<long long> lready;
       if (any_ready) {
         lready.resize(RE);
         for (int r = 0; r < RE; ++r) lready[r] = ekind[r] == 0 ? d->ready_time[eid[r]] : 0;
@@ -1064,7 +1065,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   });
   sect.run("listsched", [&] {
   // ---- list-scheduler arrays (frozen rows, multiset edges) -------------------
-  std::vector<int> esr(E), edr(E);  // edge endpoints as frozen rows
+  hvec<int> esr(E), edr(E);  // edge endpoints as frozen rows
   host_parallel_for(E, [&](long long b, long long e) {
     for (long long k = b; k < e; ++k) {
       esr[k] = g->row_of[d->edge_src[k]];
@@ -1077,7 +1078,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   }
   for (int i = 0; i < n; ++i) ch_ptr[i + 1] += ch_ptr[i];
   {
-    std::vector<int> fill(ch_ptr.begin(), ch_ptr.end() - 1);
+    hvec<int> fill(ch_ptr.begin(), ch_ptr.end() - 1);
     for (long long k = 0; k < E; ++k) ch_adj[fill[esr[k]]++] = edr[k];
   }
   host_parallel_for(n, [&](long long b, long long e) {
@@ -1114,7 +1115,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   for (int i = 0; i < n; ++i)
     if (d->gap[i] < 0) g->gap_nonneg = false;
   if (chained && L > 0) {
-    std::vector<int> bptr(L + 1, 0), brows, lane_chain(L, -1), pos_in_lane(n, -1);
+    hvec<int> bptr(L + 1, 0), brows, lane_chain(L, -1), pos_in_lane(n, -1);
     for (int l = 0; l < L; ++l) {
       for (int k = d->lane_order_ptr[l]; k < d->lane_order_ptr[l + 1]; ++k) {
         pos_in_lane[d->lane_order[k]] = (int)brows.size() - bptr[l];
@@ -1123,8 +1124,8 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
       bptr[l + 1] = (int)brows.size();
     }
     bool ok = true;
-    std::vector<BdChain> bch(NC);
-    std::vector<int> mrows(members.size());
+    hvec<BdChain> bch(NC);
+    hvec<int> mrows(members.size());
     for (size_t k = 0; k < members.size(); ++k) mrows[k] = members[k].row;
     for (int c = 0; c < NC && ok; ++c) {
       const int l = ch_lane[c];

@@ -47,6 +47,7 @@
 #include <vector>
 
 #include "ddsim.h"
+#include "host_alloc.h"
 
 namespace ddsim {
 void set_last_error(const std::string& msg);  // graph.cu
@@ -657,9 +658,9 @@ std::string with_ctx(const std::string& where, const std::string& m) {
 // --------------------------------------------------------- event sink
 
 struct EventChunk {
-  std::vector<int64_t> id, start, dur, corr, size;
-  std::vector<uint8_t> kind, dtoh;
-  std::vector<int32_t> lane, sync, name;
+  hvec<int64_t> id, start, dur, corr, size;
+  hvec<uint8_t> kind, dtoh;
+  hvec<int32_t> lane, sync, name;
   Interner lanes, names;
   std::vector<int64_t> lane_first_ev, lane_first_sync;  // per local lane, local row (or -1)
   Err err;
