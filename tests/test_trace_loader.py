@@ -109,3 +109,78 @@ def test_large_synthetic_roundtrip_parallel():
         assert np.array_equal(back.m_start, ct.m_start) and np.array_equal(back.m_end, ct.m_end)
         assert [str(back.cols.lanes[i]) for i in back.m_lane] == [str(ct.cols.lanes[i]) for i in ct.m_lane]
         assert [back.layers[i] for i in back.m_layer] == [ct.layers[i] for i in ct.m_layer]
+
+
+def _random_doc(rng, n_events, n_markers):
+    """A random trace document dict with reference-legal events/markers and a
+    mix of number spellings (ints, decimals, exponents, long floats, strings)."""
+    import math
+
+    def t_us(ns):
+        style = rng.integers(0, 6)
+        if style == 0 and ns % 1000 == 0:
+            return ns // 1000
+        if style == 1:
+            return ns / 1000
+        if style == 2:
+            return f"{ns / 1000:.6f}"            # Decimal string
+        if style == 3:
+            return float(f"{ns / 1000:.17g}")    # long float repr
+        if style == 4:
+            return float(f"{ns:.6e}") / 1000
+        return ns / 1000
+    lanes = ["cpu:0", "cpu:1", "gpu:0:7", "gpu:0:8", "comm:ring0"]
+    names = ["cudaLaunchKernel", "sgemm_x", "memcpy_dtoh_async", "q\"uote", "unié", "tab\tx"]
+    t = {ln: 0 for ln in lanes}
+    ev = []
+    corr = 1
+    for i in range(n_events):
+        ln = lanes[int(rng.integers(0, len(lanes)))]
+        if ln.startswith("cpu"):
+            kind = ["CpuApi", "CpuOther", "DataLoad", "Sync"][int(rng.integers(0, 4))]
+        elif ln.startswith("gpu"):
+            kind = ["GpuKernel", "GpuMemcpy"][int(rng.integers(0, 2))]
+        else:
+            kind = "Comm"
+        start = t[ln] + int(rng.integers(0, 5000))
+        dur = int(rng.integers(0, 9000))
+        t[ln] = start + dur
+        e = {"id": i * 3 + 1, "kind": kind, "name": names[int(rng.integers(0, len(names)))],
+             "lane": ln, "start": t_us(start), "duration": t_us(dur)}
+        if kind.startswith("Gpu") or rng.random() < 0.3:
+            e["correlation"] = corr
+            corr += 1
+        if kind == "Sync" and rng.random() < 0.5:
+            e["sync_target"] = "gpu:0:7"
+        if rng.random() < 0.1:
+            e["size_bytes"] = int(rng.integers(0, 1 << 40))
+        if rng.random() < 0.1:
+            e["extra"] = {"nested": [1, {"x": "}]"}]}
+        ev.append(e)
+    mk = []
+    for j in range(n_markers):
+        a = int(rng.integers(0, 10 ** 7))
+        mk.append({"layer": f"l{j}", "phase": ["Forward", "Backward", "WeightUpdate"][j % 3],
+                   "cpu_lane": "cpu:0", "start": t_us(a), "end": t_us(a + 1 + int(rng.integers(0, 10 ** 5)))})
+    return {"schema_version": 1, "time_unit": "microseconds", "events": ev, "layer_markers": mk,
+            "metadata": {"k": "v"}}
+
+
+@pytest.mark.parametrize("seed", range(12))
+def test_random_documents_match_python_parser(seed):
+    """Native reader == the Python parse_trace mirror (pinned on the reference's
+    vectors) on random documents, compact and indented, 1 and 13 threads."""
+    rng = np.random.default_rng(seed)
+    doc = _random_doc(rng, int(rng.integers(0, 3000)), int(rng.integers(0, 40)))
+    for text in (json.dumps(doc), json.dumps(doc, indent=int(rng.integers(0, 4)))):
+        try:
+            want = parse_trace(text)
+        except errors.KernsimError as e:
+            with pytest.raises(errors.KernsimError) as ei:
+                load_trace_columns(text, threads=13)
+            assert ei.value.name == e.name
+            continue
+        for th in (1, 13):
+            assert load_trace_columns(text, threads=th).to_document() == want
+        back = load_trace_columns(dump_trace_columns(load_trace_columns(text)), threads=5)
+        assert back.to_document() == want
