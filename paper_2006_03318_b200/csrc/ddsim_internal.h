@@ -229,8 +229,12 @@ cudaError_t launch_maxplus_dense(const DenseParams& p, const int* dense32, int d
 cudaError_t launch_maxplus_lanes(const LaneParams& p, const LaneChainParams* cp, const int* dense32,
                                  int dkind,
                                  const std::vector<int>* codes, cudaStream_t stream);
+// lane_busy[s][l] = sum of the durations of lane l's present rows (lanes
+// program order); the branch-free lanes handler leaves it to this pass.
+cudaError_t launch_lanes_busy(const LaneParams& p, const int* dense32, bool chains,
+                              cudaStream_t stream);
 cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const LaneChainParams* cp,
-                                     const void* tmap128, int dkind, int V,
+                                     const int* dense32, const void* tmap128, int dkind, int V,
                                      const std::vector<int>& codes, int grid, int BD, size_t smem,
                                      cudaStream_t stream);
 int maxplus_lanes_vec(int S);

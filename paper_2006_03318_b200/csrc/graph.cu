@@ -962,9 +962,12 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     hvec<LaneMemberDev> lmembers;
     hvec<int> lpreds;
     bool any_ready = false;
+    int cur_chain_lane = 0;
     for (int r = 0; r < RE; ++r) {
       LaneRec rec;
       memset(&rec, 0, sizeof(rec));
+      if (ekind[r] == 1) cur_chain_lane = ch_lane[eid[r]];
+      if (ekind[r] == 2) rec.h = (unsigned char)cur_chain_lane;  // member row: the chain's lane
       if (ekind[r] != 0) {
         rec.rare = (unsigned char)(ekind[r] == 1 ? LREC_CHAIN : LREC_NOP);
         if (ekind[r] == 1) {

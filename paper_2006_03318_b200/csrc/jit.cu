@@ -94,7 +94,8 @@ void init_locked() {
               (g_drv.ok ? "ok" : "missing entry points");
 }
 
-std::string make_source(const std::vector<int>& codes, int dk, int V, bool dyn, bool ch) {
+std::string make_source(const std::vector<int>& codes, int dk, int V, bool dyn, bool ch,
+                        bool nolb) {
   std::string disp = "#define DDSIM_DISPATCH(h) ";
   if (dyn) disp += "hstep_dyn<V>(S, h, d0, d1, gap, sp, ld, store); if (0) ";
   for (size_t i = 0; i < codes.size(); ++i) {
@@ -112,6 +113,9 @@ std::string make_source(const std::vector<int>& codes, int dk, int V, bool dyn, 
     src += std::string("#define DDSIM_UNROLL ") + u + "\n";
   else if (dyn)
     src += "#define DDSIM_UNROLL 2\n";
+  // the branch-free handler leaves lane busy to launch_lanes_busy (12 of ~90
+  // instructions per record are select-based lane-busy updates otherwise)
+  if (nolb) src += "#define DDSIM_NO_LB 1\n";
   std::string body = kLanesBodySrc;
   if (const char* alt = getenv("DDSIM_LANES_BODY")) {  // experiments: alternative body file
     if (FILE* f = fopen(alt, "rb")) {
@@ -133,9 +137,9 @@ std::string make_source(const std::vector<int>& codes, int dk, int V, bool dyn, 
 }
 
 CUfunction get_function(const std::vector<int>& codes, int dk, int V, bool dyn, bool ch,
-                        int device) {
+                        bool nolb, int device) {
   std::string key = std::to_string(device) + ":" + std::to_string(dk) + ":" + std::to_string(V) +
-                    (dyn ? ":dyn" : "") + (ch ? ":ch:" : ":");
+                    (dyn ? ":dyn" : "") + (ch ? ":ch" : "") + (nolb ? ":nolb:" : ":");
   if (const char* u = getenv("DDSIM_JIT_UNROLL")) key += std::string("u") + u + ":";
   if (const char* b = getenv("DDSIM_LANES_BODY")) key += std::string("b") + b + ":";
   for (int c : codes) key += std::to_string(c) + ",";
@@ -144,7 +148,7 @@ CUfunction get_function(const std::vector<int>& codes, int dk, int V, bool dyn, 
   if (!g_nv.ok || !g_drv.ok) return nullptr;
   auto it = g_cache.find(key);
   if (it != g_cache.end()) return it->second;
-  const std::string src = make_source(codes, dk, V, dyn, ch);
+  const std::string src = make_source(codes, dk, V, dyn, ch, nolb);
   nvrtcProgram_t prog = nullptr;
   CUfunction fn = nullptr;
   if (g_nv.create(&prog, src.c_str(), "ddsim_lanes_jit.cu", 0, nullptr, nullptr) == 0) {
@@ -187,7 +191,7 @@ CUfunction get_function(const std::vector<int>& codes, int dk, int V, bool dyn, 
 // Launch the specialised kernel; cudaErrorNotSupported when JIT is unavailable
 // (the caller then launches the static kernel).
 cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const LaneChainParams* cp,
-                                     const void* tmap128, int dkind, int V,
+                                     const int* dense32, const void* tmap128, int dkind, int V,
                                      const std::vector<int>& codes, int grid, int BD, size_t smem,
                                      cudaStream_t stream) {
   if (codes.empty() || codes.size() > 32) {
@@ -201,7 +205,11 @@ cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const LaneChainParams*
   int nsm = 148;
   if (cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess) dyn = grid < nsm;
   if (const char* e = getenv("DDSIM_LANES_DYN")) dyn = atoi(e) != 0;
-  CUfunction fn = get_function(codes, dkind, V, dyn, cp != nullptr, dev);
+  // lane busy by a separate pass for the branch-free handler (absent chain
+  // members are recognised by their start -1, so chains need the starts)
+  const bool nolb = dyn && p.lane_busy != nullptr && (cp == nullptr || p.start != nullptr) &&
+                    getenv("DDSIM_DYN_LB") == nullptr;
+  CUfunction fn = get_function(codes, dkind, V, dyn, cp != nullptr, nolb, dev);
   if (!fn) return cudaErrorNotSupported;
   const CUresult ar = g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
   if (ar != CUDA_SUCCESS) {
@@ -211,6 +219,7 @@ cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const LaneChainParams*
   alignas(64) unsigned char tm[128];
   memcpy(tm, tmap128, 128);
   LaneParams pp = p;
+  if (nolb) pp.lane_busy = nullptr;
   LaneChainParams cpv{};
   if (cp) cpv = *cp;
   void* args[] = {tm, &pp, &cpv};
@@ -221,6 +230,7 @@ cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const LaneChainParams*
     return cudaErrorNotSupported;
   }
   note_launch();
+  if (nolb) return launch_lanes_busy(p, dense32, cp != nullptr, stream);
   return cudaSuccess;
 }
 

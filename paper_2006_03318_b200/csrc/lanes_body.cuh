@@ -172,10 +172,14 @@ __device__ __forceinline__ void hstep_dyn(St<V>& S, unsigned h, long long d0, lo
   for (int l = 0; l < NLANE; ++l) {
     const bool mine = own == (unsigned)l;
     S.lv[l][0] = mine ? x : S.lv[l][0];
+#ifndef DDSIM_NO_LB
     S.lb[l][0] += mine ? d0 : 0;
+#endif
     if (V == 2) {
       S.lv[l][V - 1] = mine ? y : S.lv[l][V - 1];
+#ifndef DDSIM_NO_LB
       S.lb[l][V - 1] += mine ? d1 : 0;
+#endif
     }
   }
 }

@@ -81,6 +81,46 @@ int maxplus_lanes_block_dim(int S, int num_sms) {
   return bd < 32 ? 32 : (bd > cap ? cap : bd);
 }
 
+// One thread per scenario walks the rows (coalesced across the warp's
+// scenarios); the lane of a row is in its program record (h & 3); chain member
+// rows with start -1 (absent chain) do not count.
+__global__ void lanes_busy_kernel(const LaneRec* prog, int n_rec, const int* d32,
+                                  const long long* d64, long long dld, const long long* start,
+                                  long long sld, int S, int L, long long* lane_busy) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  long long lb[4] = {0, 0, 0, 0};
+  for (int r = 0; r < n_rec; ++r) {
+    const int l = prog[r].h & 3;
+    const long long d = d32 ? (long long)__ldcs(&d32[(long long)r * dld + s])
+                            : __ldcs(&d64[(long long)r * dld + s]);
+    if (start && (prog[r].rare & (LREC_CHAIN | LREC_NOP)) &&
+        start[(long long)r * sld + s] < 0)
+      continue;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (q == l) lb[q] += d;
+  }
+  for (int l = 0; l < L; ++l) {
+    long long v = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q)
+      if (q == l) v = lb[q];
+    lane_busy[(long long)s * L + l] = v;
+  }
+}
+
+cudaError_t launch_lanes_busy(const LaneParams& p, const int* dense32, bool chains,
+                              cudaStream_t stream) {
+  if (!p.lane_busy || p.S <= 0) return cudaSuccess;
+  if (chains && !p.start) return cudaErrorInvalidValue;  // absent members need the starts
+  lanes_busy_kernel<<<(p.S + 127) / 128, 128, 0, stream>>>(
+      p.prog, p.n_rec, dense32, dense32 ? nullptr : p.dense64, p.dense_ld,
+      chains ? p.start : nullptr, p.start_ld, p.S, p.L, p.lane_busy);
+  note_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_maxplus_lanes(const LaneParams& p, const LaneChainParams* cp, const int* dense32,
                                  int dkind,
                                  const std::vector<int>* codes, cudaStream_t stream) {
@@ -118,7 +158,7 @@ cudaError_t launch_maxplus_lanes(const LaneParams& p, const LaneChainParams* cp,
   // per-graph specialised dispatch first (NVRTC); the static kernel otherwise
   if (codes != nullptr) {
     const cudaError_t e =
-        launch_maxplus_lanes_jit(p, cp, &tmap, dkind, V, *codes, grid, BD, smem, stream);
+        launch_maxplus_lanes_jit(p, cp, dense32, &tmap, dkind, V, *codes, grid, BD, smem, stream);
     if (e == cudaSuccess) return cudaGetLastError();
   }
   const ddsim_lanes::Tmap& tm = *reinterpret_cast<const ddsim_lanes::Tmap*>(&tmap);
