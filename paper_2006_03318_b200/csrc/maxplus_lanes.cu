@@ -81,32 +81,41 @@ int maxplus_lanes_block_dim(int S, int num_sms) {
   return bd < 32 ? 32 : (bd > cap ? cap : bd);
 }
 
-// One thread per scenario walks the rows (coalesced across the warp's
-// scenarios); the lane of a row is in its program record (h & 3); chain member
-// rows with start -1 (absent chain) do not count.
-__global__ void lanes_busy_kernel(const LaneRec* prog, int n_rec, const int* d32,
-                                  const long long* d64, long long dld, const long long* start,
-                                  long long sld, int S, int L, long long* lane_busy) {
-  const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= S) return;
+// Blocks of 32 scenarios x 8 row-strided threads over a chunk of rows
+// (coalesced across the 32 scenarios); per-block sums go to lane_busy with
+// 64-bit atomics (zeroed first).  The lane of a row is in its program record
+// (h & 3); chain member rows with start -1 (absent chain) do not count.
+constexpr int kBusyRowsPerBlock = 512;
+__global__ void __launch_bounds__(256) lanes_busy_kernel(
+    const LaneRec* prog, int n_rec, const int* d32, const long long* d64, long long dld,
+    const long long* start, long long sld, int S, int L, unsigned long long* lane_busy) {
+  __shared__ long long acc[8][4][33];
+  const int tx = threadIdx.x, ty = threadIdx.y;
+  const int s = blockIdx.x * 32 + tx;
+  const int r0 = blockIdx.y * kBusyRowsPerBlock;
+  const int r1 = min(n_rec, r0 + kBusyRowsPerBlock);
   long long lb[4] = {0, 0, 0, 0};
-  for (int r = 0; r < n_rec; ++r) {
-    const int l = prog[r].h & 3;
-    const long long d = d32 ? (long long)__ldcs(&d32[(long long)r * dld + s])
-                            : __ldcs(&d64[(long long)r * dld + s]);
-    if (start && (prog[r].rare & (LREC_CHAIN | LREC_NOP)) &&
-        start[(long long)r * sld + s] < 0)
-      continue;
+  if (s < S) {
+    for (int r = r0 + ty; r < r1; r += 8) {
+      const LaneRec rec = prog[r];
+      const long long d = d32 ? (long long)__ldcs(&d32[(long long)r * dld + s])
+                              : __ldcs(&d64[(long long)r * dld + s]);
+      if (start && (rec.rare & (LREC_CHAIN | LREC_NOP)) && start[(long long)r * sld + s] < 0)
+        continue;
+      const int l = rec.h & 3;
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (q == l) lb[q] += d;
+      for (int q = 0; q < 4; ++q)
+        if (q == l) lb[q] += d;
+    }
   }
-  for (int l = 0; l < L; ++l) {
+#pragma unroll
+  for (int q = 0; q < 4; ++q) acc[ty][q][tx] = lb[q];
+  __syncthreads();
+  if (ty < 4 && ty < L && s < S) {
     long long v = 0;
 #pragma unroll
-    for (int q = 0; q < 4; ++q)
-      if (q == l) v = lb[q];
-    lane_busy[(long long)s * L + l] = v;
+    for (int k = 0; k < 8; ++k) v += acc[k][ty][tx];
+    if (v) atomicAdd(&lane_busy[(long long)s * L + ty], (unsigned long long)v);
   }
 }
 
@@ -114,9 +123,13 @@ cudaError_t launch_lanes_busy(const LaneParams& p, const int* dense32, bool chai
                               cudaStream_t stream) {
   if (!p.lane_busy || p.S <= 0) return cudaSuccess;
   if (chains && !p.start) return cudaErrorInvalidValue;  // absent members need the starts
-  lanes_busy_kernel<<<(p.S + 127) / 128, 128, 0, stream>>>(
+  cudaError_t e = cudaMemsetAsync(p.lane_busy, 0, sizeof(long long) * (size_t)p.S * p.L, stream);
+  if (e != cudaSuccess) return e;
+  const dim3 blk(32, 8), grd((p.S + 31) / 32, (p.n_rec + kBusyRowsPerBlock - 1) / kBusyRowsPerBlock);
+  lanes_busy_kernel<<<grd, blk, 0, stream>>>(
       p.prog, p.n_rec, dense32, dense32 ? nullptr : p.dense64, p.dense_ld,
-      chains ? p.start : nullptr, p.start_ld, p.S, p.L, p.lane_busy);
+      chains ? p.start : nullptr, p.start_ld, p.S, p.L,
+      reinterpret_cast<unsigned long long*>(p.lane_busy));
   note_launch();
   return cudaGetLastError();
 }
