@@ -190,9 +190,13 @@ def config5(n_records: int):
     t_gen = time.perf_counter() - t0
     del ct0
     # warm-up of every stage (allocator, CUB plans, NVRTC-free)
-    ct = load_trace_columns(dump_trace_columns(ingest_document_columns(200_000, seed=1)))
+    # warm-up at full size (device memory pool growth, CUB plans, host huge pages)
+    ct = load_trace_columns(text)
     res = ingest_arrays(ct.cols)
-    frozen_from_ingest(ct, res)
+    tag_m, _ = ct.marker_tags()
+    map_layers_arrays(ct.cols, res.launcher, ct.m_lane, ct.m_start, ct.m_end, tag_m)
+    frozen_from_ingest(ct, res).close()
+    del ct, res
     torch.cuda.synchronize()
     stages = {}
     t0 = time.perf_counter()
