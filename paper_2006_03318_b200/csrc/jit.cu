@@ -116,6 +116,7 @@ std::string make_source(const std::vector<int>& codes, int dk, int V, bool dyn, 
   // the branch-free handler leaves lane busy to launch_lanes_busy (12 of ~90
   // instructions per record are select-based lane-busy updates otherwise)
   if (nolb) src += "#define DDSIM_NO_LB 1\n";
+  if (const char* st = getenv("DDSIM_LANES_STAGES")) src += std::string("#define DDSIM_STAGES ") + st + "\n";
   std::string body = kLanesBodySrc;
   if (const char* alt = getenv("DDSIM_LANES_BODY")) {  // experiments: alternative body file
     if (FILE* f = fopen(alt, "rb")) {
@@ -141,6 +142,7 @@ CUfunction get_function(const std::vector<int>& codes, int dk, int V, bool dyn, 
   std::string key = std::to_string(device) + ":" + std::to_string(dk) + ":" + std::to_string(V) +
                     (dyn ? ":dyn" : "") + (ch ? ":ch" : "") + (nolb ? ":nolb:" : ":");
   if (const char* u = getenv("DDSIM_JIT_UNROLL")) key += std::string("u") + u + ":";
+  if (const char* st = getenv("DDSIM_LANES_STAGES")) key += std::string("st") + st + ":";
   if (const char* b = getenv("DDSIM_LANES_BODY")) key += std::string("b") + b + ":";
   for (int c : codes) key += std::to_string(c) + ",";
   std::lock_guard<std::mutex> lk(g_mu);

@@ -73,7 +73,10 @@ struct alignas(64) Tmap {
 };
 
 constexpr int kChunkL = 16;
-constexpr int kStagesL = 4;
+#ifndef DDSIM_STAGES
+#define DDSIM_STAGES 4
+#endif
+constexpr int kStagesL = DDSIM_STAGES;  // TMA pipeline depth (chunks in flight)
 constexpr int NLANE = 4;  // register lanes; index 4 = temp (rare predecessors)
 
 __device__ __forceinline__ unsigned su32l(const void* p) {

@@ -54,9 +54,18 @@ __global__ void __launch_bounds__(256) maxplus_lanes_chain_kernel(
   ddsim_lanes::lanes_body<DK, V, true>(&tmap, p, &cp);
 }
 
+// TMA pipeline depth of the JIT kernel (DDSIM_LANES_STAGES experiments; the
+// static kernel always uses kStagesL and fits in the larger allocation)
+static int lanes_stages() {
+  const char* e = getenv("DDSIM_LANES_STAGES");
+  const int s = e ? atoi(e) : ddsim_lanes::kStagesL;
+  return s < ddsim_lanes::kStagesL ? ddsim_lanes::kStagesL : (s > 12 ? 12 : s);
+}
+
 static size_t lanes_smem(int dk, int BD, int V, int ksm) {
-  size_t b = 128 + (size_t)ddsim_lanes::kStagesL * ddsim_lanes::kChunkL * sizeof(ddsim_lanes::Rec);
-  b += (size_t)ddsim_lanes::kStagesL * ddsim_lanes::kChunkL * BD * V * (dk == 1 ? 4 : 8);
+  const int stages = lanes_stages();
+  size_t b = 128 + (size_t)stages * ddsim_lanes::kChunkL * sizeof(ddsim_lanes::Rec);
+  b += (size_t)stages * ddsim_lanes::kChunkL * BD * V * (dk == 1 ? 4 : 8);
   return b + (size_t)ksm * BD * 8 * V;
 }
 
