@@ -1428,7 +1428,8 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
     if (q.kglob > 0) q.gslots = T.scratch<long long>((size_t)q.kglob * q.s_pad);
     CUDA_TRY(launch_maxplus(q, dk == 1 ? reinterpret_cast<const int*>(sc->dense) : nullptr, stream));
     if (out->dispatched) CUDA_TRY(launch_fill_i32(out->dispatched, g->n, S, stream));
-  } else if (use_max && dense_now && g->has_dense && sc->n_overrides == 0 && !sc->scale_ptr) {
+  } else if (use_max && dense_now && g->has_dense && sc->n_overrides == 0 && !sc->scale_ptr &&
+             getenv("DDSIM_NO_DENSE") == nullptr) {
     DenseParams p;
     memset(&p, 0, sizeof(p));
     p.prog = g->d_dprog;

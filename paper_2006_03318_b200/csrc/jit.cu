@@ -145,6 +145,7 @@ CUfunction get_function(const std::vector<int>& codes, int dk, int V, bool dyn, 
   if (const char* st = getenv("DDSIM_LANES_STAGES")) key += std::string("st") + st + ":";
   if (const char* b = getenv("DDSIM_LANES_BODY")) key += std::string("b") + b + ":";
   for (int c : codes) key += std::to_string(c) + ",";
+  if (getenv("DDSIM_NO_JIT")) return nullptr;  // checked per call (tests switch paths)
   std::lock_guard<std::mutex> lk(g_mu);
   init_locked();
   if (!g_nv.ok || !g_drv.ok) return nullptr;

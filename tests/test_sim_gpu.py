@@ -218,3 +218,38 @@ def test_batch_dense_int32_durations_with_int64_sums(golden):
         assert res.makespan[s] == ms and res.start_of(s) == st
         assert {str(k2): v for k2, v in res.lane_busy_of(s).items()} == \
             {str(k2): v for k2, v in lb.items()}
+
+
+KERNEL_PATHS = {
+    "lanes-jit": {},
+    "lanes-static": {"DDSIM_NO_JIT": "1"},
+    "lanes-branch-free": {"DDSIM_LANES_DYN": "1"},
+    "lanes-if-chain": {"DDSIM_LANES_DYN": "0"},
+    "dense": {"DDSIM_NO_LANES": "1"},
+    "general": {"DDSIM_NO_LANES": "1", "DDSIM_NO_DENSE": "1"},
+}
+
+
+@pytest.mark.parametrize("kpath", list(KERNEL_PATHS))
+@pytest.mark.parametrize("name", ["genspec_1001", "distributed_4"])
+def test_every_maxplus_kernel_path_matches_oracle(golden, name, kpath, monkeypatch):
+    """The same dense batch through each max-plus kernel (NVRTC lanes kernel
+    with either dispatch, the static lanes kernel, the dense kernel, the
+    general kernel): identical to Alg. 1 scenario by scenario."""
+    for k, v in KERNEL_PATHS[kpath].items():
+        monkeypatch.setenv(k, v)
+    g = _genspec_graph(golden, name)
+    fz = FrozenGraph.from_graph(g)
+    S = 96
+    rng = np.random.default_rng(17)
+    base = fz.duration[fz.order]
+    dense = ((2 * base[:, None] * rng.integers(500, 1501, size=(fz.n, S)) + 1000) // 2000).astype(np.int32)
+    res = simulate_batch(fz, ScenarioTable(n_scenarios=S, dense=dense))
+    og = OracleGraph.from_graph(g)
+    for s in (0, 41, S - 1):
+        d = np.empty(fz.n, np.int64)
+        d[fz.order] = dense[:, s]
+        st, ms, lb, _ = og.simulate("default", dur=d)
+        assert res.makespan[s] == ms and res.start_of(s) == st
+        assert {str(k2): v for k2, v in res.lane_busy_of(s).items()} == \
+            {str(k2): v for k2, v in lb.items()}
