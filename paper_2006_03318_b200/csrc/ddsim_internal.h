@@ -279,6 +279,10 @@ cudaError_t launch_breakdown(const BreakdownParams& p, cudaStream_t stream);
 const char* jit_log();
 int maxplus_lanes_block_dim(int S, int num_sms);
 cudaError_t launch_listsched(const ListParams& p, cudaStream_t stream);
+cudaError_t launch_toposort_lanes(int N, int L, const int* lane_ptr, const int* lane_rows,
+                                  const int* child_ptr, const int* child, const int* indeg,
+                                  const int* rank, int* deg_scratch, int* out, int* count,
+                                  cudaStream_t st);
 cudaError_t launch_fill_i64(long long* p, long long v, long long n, cudaStream_t s);
 cudaError_t launch_fill_i32(int* p, int v, long long n, cudaStream_t s);
 cudaError_t launch_patch_ovr(NodeRec* prog, int n_rec, const int* ovr_map, cudaStream_t st);

@@ -1735,12 +1735,20 @@ int ks_toposort(const ks_graph* g, int32_t* order_out, int32_t* n_out) {
     p.group = g->d_group;
     p.policy = KS_POLICY_DEFAULT;
     p.zero_time = 1;
-    p.rdy = T.scratch<long long>(2 * (size_t)n);
-    p.rem = T.scratch<int>(n);
-    p.front = T.scratch<int>(n);
     p.schedule = T.scratch<int>(n);
     p.dispatched = T.scratch<int>(1);
-    CUDA_TRY(launch_listsched(p, st));
+    if (g->chained && g->n_chains == 0 && g->bd_ok && g->L <= 32 &&
+        getenv("DDSIM_TOPO_LISTSCHED") == nullptr) {
+      // lane-chained: the frontier is the set of lane heads (one warp, lanes in lanes)
+      int* deg = (size_t)n * sizeof(int) > 200 * 1024 ? T.scratch<int>(n) : nullptr;
+      CUDA_TRY(launch_toposort_lanes(n, g->L, g->d_bd_ptr, g->d_bd_rows, g->d_child_ptr, g->d_child,
+                                     g->d_indeg, g->d_rank, deg, p.schedule, p.dispatched, st));
+    } else {
+      p.rdy = T.scratch<long long>(2 * (size_t)n);
+      p.rem = T.scratch<int>(n);
+      p.front = T.scratch<int>(n);
+      CUDA_TRY(launch_listsched(p, st));
+    }
     std::vector<int> sched(n);
     int nd = 0;
     CUDA_TRY(cudaMemcpyAsync(sched.data(), p.schedule, sizeof(int) * n, cudaMemcpyDeviceToHost, st));

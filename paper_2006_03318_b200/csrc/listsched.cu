@@ -265,3 +265,114 @@ cudaError_t launch_listsched(const ListParams& p, cudaStream_t stream) {
 }
 
 }  // namespace ddsim
+
+namespace ddsim {
+
+// verify_acyclic (graph.py:129-148) on a lane-chained graph: a task becomes
+// ready only after its lane predecessor, so the Kahn frontier is a subset of
+// the lane heads.  One warp, one lane per thread: each thread keeps its head's
+// id rank and child range in registers (with the next head prefetched); a
+// step is a warp arg-min over the ready heads' ranks (smallest id first), the
+// winner's children decrement their in-degrees (shared memory when the graph
+// fits, global otherwise) and its lane advances.
+__global__ void __launch_bounds__(32) toposort_lanes_kernel(
+    int N, int L, const int* __restrict__ lane_ptr, const int* __restrict__ lane_rows,
+    const int* __restrict__ child_ptr, const int* __restrict__ child,
+    const int* __restrict__ indeg, const int* __restrict__ rank, int* deg_g, int* out, int* count) {
+  extern __shared__ int sdeg[];
+  int* deg = deg_g ? deg_g : sdeg;
+  const int t = threadIdx.x;
+  for (int i = t; i < N; i += 32) deg[i] = indeg[i];
+  __threadfence_block();
+  __syncwarp();
+  const bool own = t < L;
+  const int len = own ? lane_ptr[t + 1] - lane_ptr[t] : 0;
+  const int* lr = lane_rows + (own ? lane_ptr[t] : 0);
+  int pos = 0;
+  // current head and the prefetched next head: row, id rank, child range and
+  // the first two children (most tasks have one or two)
+  int head = -1, hr = INT_MAX, c0 = 0, c1 = 0, k0 = -1, k1 = -1;
+  int nh = -1, nr = INT_MAX, n0 = 0, n1 = 0, m0 = -1, m1 = -1;
+  auto fetch = [&](int r, int& rr, int& a, int& b, int& x, int& y) {
+    rr = rank[r];
+    a = child_ptr[r];
+    b = child_ptr[r + 1];
+    x = a < b ? child[a] : -1;
+    y = a + 1 < b ? child[a + 1] : -1;
+  };
+  if (len > 0) {
+    head = lr[0];
+    fetch(head, hr, c0, c1, k0, k1);
+  }
+  if (len > 1) {
+    nh = lr[1];
+    fetch(nh, nr, n0, n1, m0, m1);
+  }
+  int step = 0;
+  for (; step < N; ++step) {
+    const bool ready = head >= 0 && *((volatile int*)&deg[head]) == 0;
+    int key = ready ? hr : INT_MAX;
+    int who = t;
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+      const int ok = __shfl_xor_sync(0xffffffffu, key, off);
+      const int ow = __shfl_xor_sync(0xffffffffu, who, off);
+      if (ok < key || (ok == key && ow < who)) {
+        key = ok;
+        who = ow;
+      }
+    }
+    if (key == INT_MAX) break;  // nothing ready: a cycle
+    const int v = __shfl_sync(0xffffffffu, head, who);
+    const int a = __shfl_sync(0xffffffffu, c0, who);
+    const int b = __shfl_sync(0xffffffffu, c1, who);
+    const int x = __shfl_sync(0xffffffffu, k0, who);
+    const int y = __shfl_sync(0xffffffffu, k1, who);
+    if (t == 0) {
+      out[step] = v;
+      if (x >= 0) atomicSub(&deg[x], 1);
+    } else if (t == 1) {
+      if (y >= 0) atomicSub(&deg[y], 1);
+    }
+    for (int k = a + 2 + t; k < b; k += 32) atomicSub(&deg[child[k]], 1);
+    if (t == who) {  // advance the lane; prefetch the head after next
+      ++pos;
+      head = nh;
+      hr = nr;
+      c0 = n0;
+      c1 = n1;
+      k0 = m0;
+      k1 = m1;
+      nh = -1;
+      nr = INT_MAX;
+      if (pos + 1 < len) {
+        nh = lr[pos + 1];
+        fetch(nh, nr, n0, n1, m0, m1);
+      }
+    }
+    if (deg_g) __threadfence_block();
+    __syncwarp();
+  }
+  if (t == 0) *count = step;
+}
+
+cudaError_t launch_toposort_lanes(int N, int L, const int* lane_ptr, const int* lane_rows,
+                                  const int* child_ptr, const int* child, const int* indeg,
+                                  const int* rank, int* deg_scratch, int* out, int* count,
+                                  cudaStream_t st) {
+  if (L > 32) return cudaErrorInvalidValue;
+  const size_t smem = (size_t)N * sizeof(int);
+  const bool in_smem = smem <= 200 * 1024;
+  if (in_smem) {
+    cudaError_t e = cudaFuncSetAttribute(toposort_lanes_kernel,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  toposort_lanes_kernel<<<1, 32, in_smem ? smem : 0, st>>>(N, L, lane_ptr, lane_rows, child_ptr,
+                                                          child, indeg, rank,
+                                                          in_smem ? nullptr : deg_scratch, out, count);
+  note_launch();
+  return cudaGetLastError();
+}
+
+}  // namespace ddsim
