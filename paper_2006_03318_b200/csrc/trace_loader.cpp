@@ -1470,8 +1470,7 @@ int ks_trace_parse(const char* text, int64_t len, int n_threads, ks_trace** out,
 
   Lexer L(text, text + len, text);
   L.ws();
-  Val ver, unit, events_v, markers_v, buckets_v, meta_v;
-  bool events_done = false, markers_done = false;
+  Val ver, unit, events_v, markers_v;
   std::vector<EventChunk> ev_chunks;
   std::vector<int64_t> ev_first;
   std::vector<MarkerChunk> mk_chunks;
@@ -1483,7 +1482,7 @@ int ks_trace_parse(const char* text, int64_t len, int n_threads, ks_trace** out,
     if (T > 1) {
       need_scan();
       sp = split_points(ps, open);
-      tick("prescan");
+      tick("split");
     }
     auto ap = parse_array<ChunkT>(text, len, open, sp, elem, T);
     if (ap.syntax) {
@@ -1493,6 +1492,7 @@ int ks_trace_parse(const char* text, int64_t len, int n_threads, ks_trace** out,
     }
     chunks = std::move(ap.chunks);
     first = std::move(ap.first_index);
+    tick("array");
     L.cur = text + ap.end;
     return true;
   };
@@ -1526,25 +1526,21 @@ int ks_trace_parse(const char* text, int64_t len, int n_threads, ks_trace** out,
           ev_chunks.clear();
           if (!array_of(event_element, ev_chunks, ev_first, L.cur - text)) break;
           events_v.t = V_ARR;
-          events_done = true;
         } else if (key == "layer_markers" && L.peek() == '[') {
           mk_chunks.clear();
           if (!array_of(marker_element, mk_chunks, mk_first, L.cur - text)) break;
           markers_v.t = V_ARR;
-          markers_done = true;
         } else {
           Val v;
           if (!L.value(v)) break;
           if (key == "schema_version") ver = v;
           else if (key == "time_unit") unit = v;
-          else if (key == "events") { events_v = v; events_done = false; ev_chunks.clear(); }
-          else if (key == "layer_markers") { markers_v = v; markers_done = false; mk_chunks.clear(); }
+          else if (key == "events") { events_v = v; ev_chunks.clear(); }
+          else if (key == "layer_markers") { markers_v = v; mk_chunks.clear(); }
           else if (key == "gradient_buckets") {
-            buckets_v = v;
             t->buckets_off = vstart - text;
             t->buckets_len = L.cur - vstart;
           } else if (key == "metadata") {
-            meta_v = v;
             t->metadata_off = vstart - text;
             t->metadata_len = L.cur - vstart;
             t->has_metadata = 1;
@@ -1636,10 +1632,6 @@ int ks_trace_parse(const char* text, int64_t len, int n_threads, ks_trace** out,
     if (marker_overlap(*t, msg)) finish(E_SCHEMA, msg);
     tick("markers");
   }
-  (void)events_done;
-  (void)markers_done;
-  (void)buckets_v;
-  (void)meta_v;
   if (rc != KS_OK) {
     delete t;
     return rc;
