@@ -83,6 +83,10 @@ int maxplus_lanes_vec(int S) {
 }
 int maxplus_lanes_block_dim(int S, int num_sms) {
   const int V = maxplus_lanes_vec(S);
+  if (const char* e = getenv("DDSIM_LANES_BD")) {  // experiments (multiple of 16)
+    const int bd = atoi(e) / 16 * 16;
+    if (bd >= 32 && bd <= 256 / V) return bd;
+  }
   const long long threads = (S + V - 1) / V;
   long long per = (threads + 2LL * num_sms - 1) / (2LL * num_sms);
   int bd = (int)(((per + 15) / 16) * 16);
