@@ -290,5 +290,9 @@ int maxplus_block_dim(int S, int dmode, int num_sms);
 int maxplus_dense_block_dim(int S, int V, int num_sms);
 
 void note_launch(int n = 1);
+// Keep freed stream-ordered memory in the device's default pool between calls
+// (the default release threshold unmaps it at every synchronize, so the next
+// call re-maps: measured +15 ms on the first config-4 launch after a sync).
+void keep_device_pool(int device);
 
 }  // namespace ddsim

@@ -38,6 +38,17 @@ void set_last_error(const std::string& msg) { g_last_error = msg; }
 static std::atomic<long long> g_launches{0};
 void note_launch(int n) { g_launches.fetch_add(n); }
 
+void keep_device_pool(int device) {
+  static std::atomic<unsigned> done{0};
+  if (device < 0 || device >= 32 || (done.load() >> device) & 1u) return;
+  cudaMemPool_t pool;
+  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+    uint64_t thr = ~0ull;
+    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+  }
+  done.fetch_or(1u << device);
+}
+
 struct KsError {
   int code;
   std::string msg;
@@ -1283,6 +1294,7 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
     fail(KS_ERR_DEADLOCK, std::to_string(g->n - g->n_ordered) + " tasks never became ready");
   }
   DevGuard guard(g->device);
+  keep_device_pool(g->device);
   ScenTables T;
   T.st = stream;
   const bool dense = sc->dense_kind != 0 && sc->dense != nullptr;

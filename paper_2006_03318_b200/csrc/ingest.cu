@@ -446,16 +446,7 @@ struct StageTimer {
 
 // Keep freed stream-ordered memory in the device pool between calls (the
 // default release threshold returns it to the driver at every synchronize).
-static void keep_pool(int device) {
-  static std::atomic<unsigned> done{0};
-  if (device < 0 || device >= 32 || (done.load() >> device) & 1u) return;
-  cudaMemPool_t pool;
-  if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-    uint64_t thr = ~0ull;
-    cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-  }
-  done.fetch_or(1u << device);
-}
+static void keep_pool(int device) { keep_device_pool(device); }
 
 extern "C" int ks_ingest(const ks_trace_cols* tc, int device, int check_overlaps,
                          ks_ingest_out* out) {
