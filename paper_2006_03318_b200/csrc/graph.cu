@@ -351,26 +351,44 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   bool chained = d->lane_order_ptr != nullptr;
   hvec<int> lane_succ(n, -1);
   if (chained) {
+    // every position of the lane lists independently: a task passes the lane
+    // test only in its own lane's list, so `seen` is written per lane (the
+    // exchange catches a task listed twice in that list)
+    for (int l = 0; l < L && chained; ++l)
+      if (d->lane_order_ptr[l] > d->lane_order_ptr[l + 1] || d->lane_order_ptr[l] < 0) chained = false;
+    const long long K0 = chained && L > 0 ? d->lane_order_ptr[0] : 0;
+    const long long K = chained && L > 0 ? d->lane_order_ptr[L] : 0;
     hvec<char> seen(n, 0);
-    for (int l = 0; l < L && chained; ++l) {
-      int prev = -1;
-      for (int k = d->lane_order_ptr[l]; k < d->lane_order_ptr[l + 1]; ++k) {
+    hvec<int> lane_at;  // lane of each list position
+    if (K > K0) {
+      lane_at.resize(K - K0);
+      for (int l = 0; l < L; ++l)
+        std::fill(lane_at.begin() + (d->lane_order_ptr[l] - K0),
+                  lane_at.begin() + (d->lane_order_ptr[l + 1] - K0), l);
+    }
+    std::atomic<bool> ok{chained};
+    host_parallel_for(K - K0, [&](long long b, long long e) {
+      bool good = true;
+      for (long long k = K0 + b; k < K0 + e && good; ++k) {
+        const int l = lane_at[k - K0];
         const int t = d->lane_order[k];
-        if (t < 0 || t >= n || d->lane[t] != l || seen[t] || chain_of[t] >= 0) {
-          chained = false;
+        if (t < 0 || t >= n || d->lane[t] != l || chain_of[t] >= 0 ||
+            __atomic_exchange_n(&seen[t], (char)1, __ATOMIC_RELAXED)) {
+          good = false;
           break;
         }
-        seen[t] = 1;
-        if (prev >= 0) {
-          if (!has_edge(prev, t)) {
-            chained = false;
+        if (k > d->lane_order_ptr[l]) {
+          const int prev = d->lane_order[k - 1];
+          if (prev < 0 || prev >= n || !has_edge(prev, t)) {
+            good = false;
             break;
           }
           lane_succ[prev] = t;
         }
-        prev = t;
       }
-    }
+      if (!good) ok.store(false);
+    });
+    chained = ok.load();
     for (int i = 0; i < n && chained; ++i)
       if (!seen[i] && chain_of[i] < 0) chained = false;
   }
@@ -499,10 +517,14 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
               [&](int a, int b) { return d->id_rank[a] < d->id_rank[b]; });
     for (int t : rest) g->order.push_back(t);
   }
-  g->row_of.assign(n, -1);
-  for (int r = 0; r < n; ++r) g->row_of[g->order[r]] = r;
+  g->row_of.resize(n);
   g->rank_row.resize(n);
-  for (int r = 0; r < n; ++r) g->rank_row[r] = d->id_rank[g->order[r]];
+  host_parallel_for(n, [&](long long b, long long e) {  // order is a permutation
+    for (int r = (int)b; r < (int)e; ++r) {
+      g->row_of[g->order[r]] = r;
+      g->rank_row[r] = d->id_rank[g->order[r]];
+    }
+  });
   g->rows_are_records = (NC == 0);
 
   gt.mark("rows");
@@ -549,19 +571,18 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   gt.mark("levels");
   // ---- the four builders below (general records, dense program, lane program,
   // list-scheduler arrays) read only the shared graph above: run concurrently
-  hvec<NodeRec> prog(R), members;
-  hvec<int> extra;
+  hvec<NodeRec> members;
   hvec<ChainDesc> chains(NC);
   bool nonneg = true;
   for (int i = 0; i < n && nonneg; ++i)
     if (d->gap[i] < 0 || (d->ready_time && d->ready_time[i] < 0)) nonneg = false;
-  hvec<int> ch_ptr(n + 1, 0), ch_adj(E), indeg(n, 0);
-  hvec<int> lane_r(n), rank_r(n), prio_r(n);
-  hvec<long long> dur_r(n), gap_r(n), ready_r(n);
-  hvec<unsigned char> flags_r(n);
-  hvec<unsigned> group_r(n);
+  // (each builder allocates its own arrays: first-touch page faults then run
+  // on the builders' threads instead of serially here)
   ConcurrentSections sect(g->device);
   sect.run("records", [&] {
+  HostTimer rt_;
+  hvec<NodeRec> prog(R);
+  hvec<int> extra;
   // ---- value live ranges -------------------------------------------------------
   // values: task t (0..n-1) -> rel(t); chain tail value n + c.
   const int NV = n + NC;
@@ -575,11 +596,25 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   }
   auto rec_of_val = [&](int t) { return chain_of[t] >= 0 ? rec_of_chain[chain_of[t]] : rec_of_task[t]; };
   hvec<int> last_use(NV, -1);
-  // inputs of each record (flat CSR: rin_ptr / rin)
-  hvec<int> rin_ptr(R + 1, 0), rin;
-  rin.reserve(keys.size() + 2 * (size_t)NC);
+  // inputs of each record (flat CSR: rin_ptr / rin); without chains they are
+  // the task's unique predecessors (padj, sorted) and last use is the latest
+  // consumer record over the out-edge ranges -- computed per source, in parallel
+  hvec<int> rin_ptr, rin;
+  if (NC == 0) {
+    host_parallel_for(n, [&](long long b, long long e) {
+      for (int u = (int)b; u < (int)e; ++u) {
+        int m = -1;
+        for (int k = optr[u]; k < optr[u + 1]; ++k)
+          m = std::max(m, rec_of_task[(int)(keys[k] & 0xffffffffu)]);
+        last_use[u] = m;
+      }
+    });
+  } else {
+    rin_ptr.assign(R + 1, 0);
+    rin.reserve(keys.size() + 2 * (size_t)NC);
+  }
   hvec<int> in;
-  for (int i = 0; i < R; ++i) {
+  for (int i = 0; i < R && NC > 0; ++i) {
     const int x = corder[i];
     in.clear();
     auto add_task_preds = [&](int t) {
@@ -603,6 +638,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     rin_ptr[i + 1] = (int)rin.size();
   }
 
+  rt_.mark(" rec:last-use");
   // ---- slot allocation (linear scan, allocate-then-free) ----------------------
   hvec<int> slot(NV, -1);
   hvec<char> in_glob(NV, 0);
@@ -639,11 +675,16 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
       for (int k = d->chain_ptr[c]; k < d->chain_ptr[c + 1]; ++k) alloc(d->chain_member[k], i);
       if (d->chain_tail && d->chain_tail[c] >= 0) alloc(n + c, i);
     }
-    for (int q = rin_ptr[i]; q < rin_ptr[i + 1]; ++q)
-      if (const int v = rin[q]; last_use[v] == i && slot[v] >= 0) {
-        (in_glob[v] ? free_g : free_s).push(slot[v]);
-      }
+    auto release = [&](int v) {
+      if (last_use[v] == i && slot[v] >= 0) (in_glob[v] ? free_g : free_s).push(slot[v]);
+    };
+    if (NC == 0) {
+      for (int q = pptr[x]; q < pptr[x + 1]; ++q) release(padj[q]);
+    } else {
+      for (int q = rin_ptr[i]; q < rin_ptr[i + 1]; ++q) release(rin[q]);
+    }
   }
+  rt_.mark(" rec:slots");
   g->ksm = next_s;
   g->kglob = next_g;
   g->n_slots = next_s + next_g;
@@ -741,6 +782,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
       }
     }
   }
+  rt_.mark(" rec:fill");
   g->perm_ld = perm_off;
   g->n_rec = R;
   g->d_prog = dev_upload(prog);  // uploads overlap the other builders
@@ -970,6 +1012,16 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     hvec<LaneRec> lprog(RE);
     hvec<int> lside_off(RE + 1, 0), lside_slots;
     hvec<LaneChainDev> lchains(NC);
+    hvec<int> lperm(NC, 0);  // chain offsets in the permutation rows (record order, as
+    {                        // the records builder assigns them; not read from it: concurrent)
+      int o = 0;
+      for (int i = 0; i < R; ++i)
+        if (corder[i] >= n) {
+          const int c = corder[i] - n;
+          lperm[c] = o;
+          o += d->chain_ptr[c + 1] - d->chain_ptr[c];
+        }
+    }
     hvec<LaneMemberDev> lmembers;
     hvec<int> lpreds;
     bool any_ready = false;
@@ -989,7 +1041,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
           lc.lane = ch_lane[c];
           lc.B = d->chain_ptr[c + 1] - d->chain_ptr[c];
           lc.mem_off = (int)lmembers.size();
-          lc.perm_off = chains[c].perm_off;
+          lc.perm_off = lperm[c];
           for (int k = d->chain_ptr[c]; k < d->chain_ptr[c + 1]; ++k) {
             const int m = d->chain_member[k];
             LaneMemberDev md;
@@ -1079,6 +1131,11 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   });
   sect.run("listsched", [&] {
   // ---- list-scheduler arrays (frozen rows, multiset edges) -------------------
+  hvec<int> ch_ptr(n + 1, 0), ch_adj(E), indeg(n, 0);
+  hvec<int> lane_r(n), rank_r(n), prio_r(n);
+  hvec<long long> dur_r(n), gap_r(n), ready_r(n);
+  hvec<unsigned char> flags_r(n);
+  hvec<unsigned> group_r(n);
   hvec<int> esr(E), edr(E);  // edge endpoints as frozen rows
   host_parallel_for(E, [&](long long b, long long e) {
     for (long long k = b; k < e; ++k) {

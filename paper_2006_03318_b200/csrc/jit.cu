@@ -106,12 +106,13 @@ std::string make_source(const std::vector<int>& codes, int dk, int V, bool dyn, 
   }
   disp += "else __trap();\n";
   std::string src = "#define DDSIM_LANES_NO_STD_TYPES 1\n";
-  // record-loop unrolling: 2 for the branch-free (latency-bound) handler lets the
-  // next record's decode overlap this record's max-plus chain (config 2 -8 %,
-  // config 3 -26 %); the if-chain handler stays rolled (instruction cache)
+  // record-loop unrolling by 2 lets the next record's decode overlap this
+  // record's max-plus chain: branch-free handler config 2 -8 %, config 3 -26 %;
+  // if-chain handler config 4 -0.5 % (13.55 -> 13.49 ms, 3 interleaved repeats);
+  // 4 is slower (15.3 ms: instruction cache)
   if (const char* u = getenv("DDSIM_JIT_UNROLL"))
     src += std::string("#define DDSIM_UNROLL ") + u + "\n";
-  else if (dyn)
+  else
     src += "#define DDSIM_UNROLL 2\n";
   // the branch-free handler leaves lane busy to launch_lanes_busy (12 of ~90
   // instructions per record are select-based lane-busy updates otherwise)
