@@ -132,6 +132,43 @@ struct ConcurrentSections {
   }
 };
 
+// Free slot ids, smallest first (the order a min-heap gives, so slot
+// assignments are unchanged): a three-level 64-ary bitmap, O(1) per level.
+struct MinFreeSet {
+  std::vector<unsigned long long> b0, b1, b2;
+  size_t cnt = 0;
+  bool empty() const { return cnt == 0; }
+  void push(int x) {
+    const size_t i0 = (size_t)x >> 6, i1 = i0 >> 6, i2 = i1 >> 6;
+    if (i0 >= b0.size()) {
+      b0.resize(std::max(i0 + 1, b0.size() * 2));
+      b1.resize((b0.size() + 63) / 64);
+      b2.resize((b1.size() + 63) / 64);
+    }
+    b0[i0] |= 1ull << (x & 63);
+    b1[i1] |= 1ull << (i0 & 63);
+    b2[i2] |= 1ull << (i1 & 63);
+    ++cnt;
+  }
+  int top() const {
+    size_t i2 = 0;
+    while (!b2[i2]) ++i2;
+    const size_t i1 = i2 * 64 + __builtin_ctzll(b2[i2]);
+    const size_t i0 = i1 * 64 + __builtin_ctzll(b1[i1]);
+    return (int)(i0 * 64 + __builtin_ctzll(b0[i0]));
+  }
+  void pop() {
+    const int x = top();
+    const size_t i0 = (size_t)x >> 6, i1 = i0 >> 6, i2 = i1 >> 6;
+    b0[i0] &= ~(1ull << (x & 63));
+    if (!b0[i0]) {
+      b1[i1] &= ~(1ull << (i0 & 63));
+      if (!b1[i1]) b2[i2] &= ~(1ull << (i1 & 63));
+    }
+    --cnt;
+  }
+};
+
 constexpr int kSmemSlotsMax = 24;
 constexpr int kShortRange = 48;
 
@@ -398,6 +435,21 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   g->n_chains = NC;
 
   gt.mark("chain-check");
+  // ---- unique preds per task (for records) -----------------------------------
+  hvec<int> pptr(n + 1, 0), padj(keys.size());
+  for (unsigned long long k : keys) pptr[(k & 0xffffffffu) + 1]++;
+  for (int i = 0; i < n; ++i) pptr[i + 1] += pptr[i];
+  {
+    hvec<int> fill(pptr.begin(), pptr.end() - 1);
+    for (unsigned long long k : keys) padj[fill[k & 0xffffffffu]++] = (int)(k >> 32);
+  }
+  hvec<int> tail_of(n, -1);  // task -> chain whose tail it is
+  for (int c = 0; c < NC; ++c) {
+    const int t = d->chain_tail ? d->chain_tail[c] : -1;
+    if (t >= 0) tail_of[t] = c;
+  }
+
+  gt.mark("preds");
   // ---- contracted graph (chain -> one node) ---------------------------------
   const int NN = n + NC;
   auto X = [&](int t) { return chain_of[t] >= 0 ? n + chain_of[t] : t; };
@@ -435,14 +487,27 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     ckeys.erase(std::unique(ckeys.begin(), ckeys.end()), ckeys.end());
   }
   const hvec<unsigned long long>& CK = NC > 0 ? ckeys : keys;  // sorted by (u, v)
-  hvec<int> cptr(NN + 1, 0), cadj(CK.size()), cindeg(NN, 0);
-  for (size_t q = 0; q < CK.size(); ++q) {
-    const unsigned long long k = CK[q];
-    cptr[(k >> 32) + 1]++;
-    cindeg[k & 0xffffffffu]++;
-    cadj[q] = (int)(k & 0xffffffffu);
+  hvec<int> cptr, cadj(CK.size()), cindeg;
+  if (NC == 0) {  // the contracted graph is the unique-edge graph: reuse its ranges
+    cptr.assign(optr.begin(), optr.end());
+    cindeg.resize(NN);
+    host_parallel_for(NN, [&](long long b, long long e) {
+      for (long long i = b; i < e; ++i) cindeg[i] = pptr[i + 1] - pptr[i];
+    });
+    host_parallel_for((long long)CK.size(), [&](long long b, long long e) {
+      for (long long q = b; q < e; ++q) cadj[q] = (int)(CK[q] & 0xffffffffu);
+    });
+  } else {
+    cptr.assign(NN + 1, 0);
+    cindeg.assign(NN, 0);
+    for (size_t q = 0; q < CK.size(); ++q) {
+      const unsigned long long k = CK[q];
+      cptr[(k >> 32) + 1]++;
+      cindeg[k & 0xffffffffu]++;
+      cadj[q] = (int)(k & 0xffffffffu);
+    }
+    for (int i = 0; i < NN; ++i) cptr[i + 1] += cptr[i];
   }
-  for (int i = 0; i < NN; ++i) cptr[i + 1] += cptr[i];
   // rank of contracted nodes (tie-break for the initial stack)
   hvec<int> crank(NN);
   for (int i = 0; i < n; ++i) crank[i] = d->id_rank[i];
@@ -528,21 +593,6 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   g->rows_are_records = (NC == 0);
 
   gt.mark("rows");
-  // ---- unique preds per task (for records) -----------------------------------
-  hvec<int> pptr(n + 1, 0), padj(keys.size());
-  for (unsigned long long k : keys) pptr[(k & 0xffffffffu) + 1]++;
-  for (int i = 0; i < n; ++i) pptr[i + 1] += pptr[i];
-  {
-    hvec<int> fill(pptr.begin(), pptr.end() - 1);
-    for (unsigned long long k : keys) padj[fill[k & 0xffffffffu]++] = (int)(k >> 32);
-  }
-  hvec<int> tail_of(n, -1);  // task -> chain whose tail it is
-  for (int c = 0; c < NC; ++c) {
-    const int t = d->chain_tail ? d->chain_tail[c] : -1;
-    if (t >= 0) tail_of[t] = c;
-  }
-
-  gt.mark("preds");
   // ---- levels ------------------------------------------------------------------
   hvec<int> clevel(NN, 0);
   {
@@ -581,35 +631,27 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   ConcurrentSections sect(g->device);
   sect.run("records", [&] {
   HostTimer rt_;
-  hvec<NodeRec> prog(R);
+  uvec<NodeRec> prog(R);
   hvec<int> extra;
   // ---- value live ranges -------------------------------------------------------
   // values: task t (0..n-1) -> rel(t); chain tail value n + c.
   const int NV = n + NC;
   hvec<int> rec_of_task(n, -1), rec_of_chain(NC, -1);
-  for (int i = 0; i < R; ++i) {
-    const int x = corder[i];
-    if (x < n)
-      rec_of_task[x] = i;
-    else
-      rec_of_chain[x - n] = i;
-  }
+  host_parallel_for(R, [&](long long b, long long e) {  // corder: distinct nodes
+    for (int i = (int)b; i < (int)e; ++i) {
+      const int x = corder[i];
+      if (x < n)
+        rec_of_task[x] = i;
+      else
+        rec_of_chain[x - n] = i;
+    }
+  });
   auto rec_of_val = [&](int t) { return chain_of[t] >= 0 ? rec_of_chain[chain_of[t]] : rec_of_task[t]; };
-  hvec<int> last_use(NV, -1);
-  // inputs of each record (flat CSR: rin_ptr / rin); without chains they are
-  // the task's unique predecessors (padj, sorted) and last use is the latest
-  // consumer record over the out-edge ranges -- computed per source, in parallel
+  hvec<int> last_use;
+  // inputs of each record (flat CSR: rin_ptr / rin)
   hvec<int> rin_ptr, rin;
-  if (NC == 0) {
-    host_parallel_for(n, [&](long long b, long long e) {
-      for (int u = (int)b; u < (int)e; ++u) {
-        int m = -1;
-        for (int k = optr[u]; k < optr[u + 1]; ++k)
-          m = std::max(m, rec_of_task[(int)(keys[k] & 0xffffffffu)]);
-        last_use[u] = m;
-      }
-    });
-  } else {
+  if (NC > 0) {
+    last_use.assign(NV, -1);
     rin_ptr.assign(R + 1, 0);
     rin.reserve(keys.size() + 2 * (size_t)NC);
   }
@@ -642,47 +684,85 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   // ---- slot allocation (linear scan, allocate-then-free) ----------------------
   hvec<int> slot(NV, -1);
   hvec<char> in_glob(NV, 0);
-  std::priority_queue<int, hvec<int>, std::greater<int>> free_s, free_g;
+  MinFreeSet free_s, free_g;
   int next_s = 0, next_g = 0;
-  auto alloc = [&](int v, int i) {
-    if (last_use[v] < 0) return;  // nobody reads it
-    const bool short_range = (last_use[v] - i) <= kShortRange;
+  // value v defined by record i, last read by record lu
+  auto alloc_at = [&](int lu, int i, int& sl, char& gl) {
+    if (lu < 0) return;  // nobody reads it
+    const bool short_range = (lu - i) <= kShortRange;
     if (short_range) {
       if (!free_s.empty()) {
-        slot[v] = free_s.top();
+        sl = free_s.top();
         free_s.pop();
         return;
       }
       if (next_s < kSmemSlotsMax) {
-        slot[v] = next_s++;
+        sl = next_s++;
         return;
       }
     }
-    in_glob[v] = 1;
+    gl = 1;
     if (!free_g.empty()) {
-      slot[v] = free_g.top();
+      sl = free_g.top();
       free_g.pop();
     } else {
-      slot[v] = next_g++;
+      sl = next_g++;
     }
   };
-  for (int i = 0; i < R; ++i) {
+  if (NC == 0) {
+    // Record space: without chains every record defines exactly one value, so
+    // the scan reads its arrays sequentially and the predecessors it releases
+    // are recent records (cache-resident); last use and the record-space
+    // predecessor lists are built in parallel. Same scan, same slots.
+    hvec<int> lu_r(R), rptr(R + 1, 0);
+    host_parallel_for(R, [&](long long b, long long e) {
+      for (int i = (int)b; i < (int)e; ++i) {
+        const int x = corder[i];
+        int m = -1;
+        for (int k = optr[x]; k < optr[x + 1]; ++k)
+          m = std::max(m, rec_of_task[(int)(keys[k] & 0xffffffffu)]);
+        lu_r[i] = m;
+        rptr[i + 1] = pptr[x + 1] - pptr[x];
+      }
+    });
+    for (int i = 0; i < R; ++i) rptr[i + 1] += rptr[i];
+    hvec<int> rp(rptr[R]);
+    host_parallel_for(R, [&](long long b, long long e) {
+      for (int i = (int)b; i < (int)e; ++i) {
+        const int x = corder[i];
+        for (int k = pptr[x], o = rptr[i]; k < pptr[x + 1]; ++k, ++o) rp[o] = rec_of_task[padj[k]];
+      }
+    });
+    rt_.mark(" rec:rspace");
+    hvec<int> slot_r(R, -1);
+    hvec<char> glob_r(R, 0);
+    for (int i = 0; i < R; ++i) {
+      alloc_at(lu_r[i], i, slot_r[i], glob_r[i]);
+      for (int q = rptr[i]; q < rptr[i + 1]; ++q)
+        if (const int j = rp[q]; lu_r[j] == i && slot_r[j] >= 0) (glob_r[j] ? free_g : free_s).push(slot_r[j]);
+    }
+    rt_.mark(" rec:scan");
+    host_parallel_for(R, [&](long long b, long long e) {
+      for (int i = (int)b; i < (int)e; ++i) {
+        slot[corder[i]] = slot_r[i];
+        in_glob[corder[i]] = glob_r[i];
+      }
+    });
+  }
+  for (int i = 0; i < R && NC > 0; ++i) {
     const int x = corder[i];
     if (x < n) {
-      alloc(x, i);
+      alloc_at(last_use[x], i, slot[x], in_glob[x]);
     } else {
       const int c = x - n;
-      for (int k = d->chain_ptr[c]; k < d->chain_ptr[c + 1]; ++k) alloc(d->chain_member[k], i);
-      if (d->chain_tail && d->chain_tail[c] >= 0) alloc(n + c, i);
+      for (int k = d->chain_ptr[c]; k < d->chain_ptr[c + 1]; ++k) {
+        const int m = d->chain_member[k];
+        alloc_at(last_use[m], i, slot[m], in_glob[m]);
+      }
+      if (d->chain_tail && d->chain_tail[c] >= 0) alloc_at(last_use[n + c], i, slot[n + c], in_glob[n + c]);
     }
-    auto release = [&](int v) {
-      if (last_use[v] == i && slot[v] >= 0) (in_glob[v] ? free_g : free_s).push(slot[v]);
-    };
-    if (NC == 0) {
-      for (int q = pptr[x]; q < pptr[x + 1]; ++q) release(padj[q]);
-    } else {
-      for (int q = rin_ptr[i]; q < rin_ptr[i + 1]; ++q) release(rin[q]);
-    }
+    for (int q = rin_ptr[i]; q < rin_ptr[i + 1]; ++q)
+      if (const int v = rin[q]; last_use[v] == i && slot[v] >= 0) (in_glob[v] ? free_g : free_s).push(slot[v]);
   }
   rt_.mark(" rec:slots");
   g->ksm = next_s;
@@ -795,18 +875,24 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   // ---- dense program: register forwarding for the two previous records ----
   if (NC == 0 && L <= 127 && nonneg) {
     hvec<int> pos(n, -1);
-    for (int i = 0; i < R; ++i) pos[corder[i]] = i;
-    hvec<int> far_use(n, -1);  // last consumer more than 2 records later
-    for (int i = 0; i < R; ++i) {
-      const int v = corder[i];
-      for (int k = pptr[v]; k < pptr[v + 1]; ++k) {
-        const int u = padj[k];
-        if (i - pos[u] > 2) far_use[u] = std::max(far_use[u], i);
+    host_parallel_for(R, [&](long long b, long long e) {
+      for (int i = (int)b; i < (int)e; ++i) pos[corder[i]] = i;
+    });
+    hvec<int> far_use(n, -1);  // last consumer more than 2 records later (per source)
+    host_parallel_for(n, [&](long long b, long long e) {
+      for (int u = (int)b; u < (int)e; ++u) {
+        if (pos[u] < 0) continue;
+        int m = -1;
+        for (int k = optr[u]; k < optr[u + 1]; ++k) {
+          const int i = pos[(int)(keys[k] & 0xffffffffu)];
+          if (i - pos[u] > 2) m = std::max(m, i);
+        }
+        far_use[u] = m;
       }
-    }
+    });
     hvec<int> dslot(n, -1);
     hvec<char> dglob(n, 0);
-    std::priority_queue<int, hvec<int>, std::greater<int>> fs, fg;
+    MinFreeSet fs, fg;
     int ns = 0, ngl = 0;
     hvec<int> fa_ptr(R + 1, 0), fa;  // values freed after record i (CSR)
     for (int i = 0; i < R; ++i)
@@ -843,13 +929,14 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     g->dkglob = ngl;
     hvec<int> lane_last(L, -1);
     for (int i = 0; i < R; ++i) lane_last[d->lane[corder[i]]] = i;
-    hvec<DenseRec> dprog(R);
+    uvec<DenseRec> dprog(R);
     hvec<int> side_off(R + 1, 0);
     hvec<int> side_slots;
     hvec<long long> side_ready;
-    bool any_ready = false;
     bool ok = ns + ngl < 32000;
-    for (int i = 0; i < R && ok; ++i) {
+    // records are independent given the slots: encode in parallel, side lists
+    // by count / prefix / fill
+    auto encode = [&](int i, DenseRec* out, int* side) {
       const int v = corder[i];
       DenseRec r;
       memset(&r, 0, sizeof(r));
@@ -861,7 +948,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
         op |= dglob[v] ? DOP_OUT_GLOBAL : DOP_OUT_SMEM;
         r.out = (short)(dglob[v] ? ns + dslot[v] : dslot[v]);
       }
-      int nsm_pred = 0;
+      int nsm_pred = 0, nside = 0;
       for (int k = pptr[v]; k < pptr[v + 1]; ++k) {
         const int u = padj[k];
         const int dist = i - pos[u];
@@ -879,18 +966,28 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
           ++nsm_pred;
         } else {
           op |= DOP_SLOW;
-          side_slots.push_back(dglob[u] ? ns + dslot[u] : dslot[u]);
+          if (side) side[nside] = dglob[u] ? ns + dslot[u] : dslot[u];
+          ++nside;
         }
       }
-      side_off[i + 1] = (int)side_slots.size();
-      const long long rt = d->ready_time ? d->ready_time[v] : 0;
-      if (rt != 0) {
-        op |= DOP_SLOW;
-        any_ready = true;
-      }
+      if (d->ready_time && d->ready_time[v] != 0) op |= DOP_SLOW;
       r.op = (unsigned char)op;
-      dprog[i] = r;
+      if (out) *out = r;
+      return nside;
+    };
+    if (ok) {
+      host_parallel_for(R, [&](long long b, long long e) {
+        for (int i = (int)b; i < (int)e; ++i) side_off[i + 1] = encode(i, nullptr, nullptr);
+      });
+      for (int i = 0; i < R; ++i) side_off[i + 1] += side_off[i];
+      side_slots.resize(side_off[R]);
+      host_parallel_for(R, [&](long long b, long long e) {
+        for (int i = (int)b; i < (int)e; ++i) encode(i, &dprog[i], side_slots.data() + side_off[i]);
+      });
     }
+    bool any_ready = false;
+    for (int i = 0; i < R && ok && d->ready_time && !any_ready; ++i)
+      any_ready = d->ready_time[corder[i]] != 0;
     if (ok) {
       if (any_ready) {
         side_ready.resize(R);
@@ -964,7 +1061,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     }
     hvec<int> lslot(n, -1);
     hvec<char> lglob(n, 0);
-    std::priority_queue<int, hvec<int>, std::greater<int>> fs, fg;
+    MinFreeSet fs, fg;
     int ns = 0, ngl = 0;
     auto for_values = [&](int r, auto fn) {  // task values produced by record r
       if (ekind[r] == 0) {

@@ -35,3 +35,25 @@ struct HugeAlloc {
 };
 template <class T>
 using hvec = std::vector<T, HugeAlloc<T>>;
+
+// Same allocator without value-initialisation: `uvec<T> v(n)` leaves POD
+// elements unwritten (for arrays a builder overwrites completely, so the
+// first touch happens on the writer threads instead of in a serial zero fill).
+template <class T>
+struct NoInitAlloc : HugeAlloc<T> {
+  using value_type = T;
+  template <class U>
+  struct rebind { using other = NoInitAlloc<U>; };
+  NoInitAlloc() = default;
+  template <class U>
+  NoInitAlloc(const NoInitAlloc<U>&) {}
+  template <class U, class... A>
+  void construct(U* p, A&&... a) {
+    if constexpr (sizeof...(A) == 0)
+      ::new (static_cast<void*>(p)) U;
+    else
+      ::new (static_cast<void*>(p)) U(static_cast<A&&>(a)...);
+  }
+};
+template <class T>
+using uvec = std::vector<T, NoInitAlloc<T>>;
