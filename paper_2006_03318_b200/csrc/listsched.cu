@@ -221,6 +221,7 @@ __global__ void __launch_bounds__(32) listsched_kernel(const ListParams p) {
     }
     const long long fin = st + d;
     const long long rel = fin + g;
+    __syncwarp();  // every lane has read lp[ln] before lane 0 updates it (racecheck)
     if (lane == 0) {
       if (bpos != F - 1) {
         long long r2;

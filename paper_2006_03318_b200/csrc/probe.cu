@@ -121,6 +121,10 @@ extern "C" int ks_probe_widen(const int32_t* src, int64_t* dst, int64_t n, void*
       probe_widen_kernel<<<nsm * 4, 256, 0, st>>>(s2, d2, n2);
     else if (v == 5)
       probe_widen_kernel<<<nsm * 16, 256, 0, st>>>(s2, d2, n2);
+    else if (v == 6)
+      probe_widen_var<8, true><<<nsm * 16, 256, 0, st>>>(s2, d2, n2);
+    else if (v == 7)
+      probe_widen_kernel<<<nsm * 32, 256, 0, st>>>(s2, d2, n2);
     else
       probe_widen_kernel<<<nsm * 8, 256, 0, st>>>(s2, d2, n2);
     note_launch();
