@@ -30,8 +30,11 @@ __global__ void __launch_bounds__(256) probe_widen_kernel(const int2* __restrict
   }
 }
 
-// experiment variants (DDSIM_PROBE_VARIANT): 1 = eight steps in flight,
-// 2 = write-back (non-streaming) stores, 3 = TMA bulk stores of 8 KB shared tiles
+// variants (DDSIM_PROBE_VARIANT, config-4 size, 1x B200): default 32 CTAs per SM
+// 6.21 TB/s; 8 = 8 CTAs per SM 5.97; 4 = 4 per SM 5.79; 5 = 16 per SM 6.08;
+// 6 = 16 per SM, eight steps in flight 6.17; 1 = 8 per SM, eight in flight 6.08;
+// 2 = write-back (non-streaming) stores 5.93; 3 = TMA bulk stores of 8 KB shared
+// tiles 5.43. The default is the ceiling bench.py reports (pattern_copy_gbs).
 template <int K, bool CS>
 __global__ void __launch_bounds__(256) probe_widen_var(const int2* __restrict__ src,
                                                        longlong2* __restrict__ dst, long long n2) {
@@ -125,8 +128,10 @@ extern "C" int ks_probe_widen(const int32_t* src, int64_t* dst, int64_t n, void*
       probe_widen_var<8, true><<<nsm * 16, 256, 0, st>>>(s2, d2, n2);
     else if (v == 7)
       probe_widen_kernel<<<nsm * 32, 256, 0, st>>>(s2, d2, n2);
-    else
+    else if (v == 8)
       probe_widen_kernel<<<nsm * 8, 256, 0, st>>>(s2, d2, n2);
+    else  // default: the fastest measured shape (6.21 TB/s vs 5.97 at 8 CTAs per SM)
+      probe_widen_kernel<<<nsm * 32, 256, 0, st>>>(s2, d2, n2);
     note_launch();
   }
   if (n % 2) {
