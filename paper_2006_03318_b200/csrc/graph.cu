@@ -436,12 +436,27 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
 
   gt.mark("chain-check");
   // ---- unique preds per task (for records) -----------------------------------
+  // transpose of the unique edges: parallel atomic count / scatter, then each
+  // (short) list sorted -- the same ascending-source lists a sequential
+  // scatter of the (u, v)-sorted keys gives
   hvec<int> pptr(n + 1, 0), padj(keys.size());
-  for (unsigned long long k : keys) pptr[(k & 0xffffffffu) + 1]++;
+  const long long KE = (long long)keys.size();
+  host_parallel_for(KE, [&](long long b, long long e) {
+    for (long long q = b; q < e; ++q) __atomic_fetch_add(&pptr[(keys[q] & 0xffffffffu) + 1], 1, __ATOMIC_RELAXED);
+  });
   for (int i = 0; i < n; ++i) pptr[i + 1] += pptr[i];
   {
     hvec<int> fill(pptr.begin(), pptr.end() - 1);
-    for (unsigned long long k : keys) padj[fill[k & 0xffffffffu]++] = (int)(k >> 32);
+    host_parallel_for(KE, [&](long long b, long long e) {
+      for (long long q = b; q < e; ++q) {
+        const int v = (int)(keys[q] & 0xffffffffu);
+        padj[__atomic_fetch_add(&fill[v], 1, __ATOMIC_RELAXED)] = (int)(keys[q] >> 32);
+      }
+    });
+    host_parallel_for(n, [&](long long b, long long e) {
+      for (long long v = b; v < e; ++v)
+        if (pptr[v + 1] - pptr[v] > 1) std::sort(padj.begin() + pptr[v], padj.begin() + pptr[v + 1]);
+    });
   }
   hvec<int> tail_of(n, -1);  // task -> chain whose tail it is
   for (int c = 0; c < NC; ++c) {
@@ -594,10 +609,43 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
 
   gt.mark("rows");
   // ---- levels ------------------------------------------------------------------
-  hvec<int> clevel(NN, 0);
-  {
-    hvec<int> rec_of(NN, -1);
-    for (int i = 0; i < R; ++i) rec_of[corder[i]] = i;
+  // Without chains: pull form in record space -- level(i) = 1 + max over the
+  // record's predecessors, which are recent records (cache-resident); the
+  // record-space predecessor lists are built in parallel and reused by the
+  // records builder. With chains: push form over the contracted graph.
+  hvec<int> rp_ptr, rp;  // record-space predecessors (NC == 0)
+  if (NC == 0) {
+    hvec<int> rec_of(n, -1);
+    host_parallel_for(R, [&](long long b, long long e) {
+      for (int i = (int)b; i < (int)e; ++i) rec_of[corder[i]] = i;
+    });
+    rp_ptr.assign(R + 1, 0);
+    host_parallel_for(R, [&](long long b, long long e) {
+      for (int i = (int)b; i < (int)e; ++i) rp_ptr[i + 1] = pptr[corder[i] + 1] - pptr[corder[i]];
+    });
+    for (int i = 0; i < R; ++i) rp_ptr[i + 1] += rp_ptr[i];
+    rp.resize(rp_ptr[R]);
+    host_parallel_for(R, [&](long long b, long long e) {
+      for (int i = (int)b; i < (int)e; ++i) {
+        const int x = corder[i];
+        for (int k = pptr[x], o = rp_ptr[i]; k < pptr[x + 1]; ++k, ++o) rp[o] = rec_of[padj[k]];
+      }
+    });
+    hvec<int> lv(R);
+    int maxl = 0;
+    for (int i = 0; i < R; ++i) {
+      int m = 0;
+      for (int q = rp_ptr[i]; q < rp_ptr[i + 1]; ++q) m = std::max(m, lv[rp[q]]);
+      lv[i] = m + 1;
+      maxl = std::max(maxl, m + 1);
+    }
+    g->n_levels = maxl;
+    g->level.assign(n, -1);
+    host_parallel_for(R, [&](long long b, long long e) {  // rows are records without chains
+      for (int i = (int)b; i < (int)e; ++i) g->level[i] = lv[i] - 1;
+    });
+  } else {
+    hvec<int> clevel(NN, 0);
     int maxl = 0;
     for (int i = 0; i < R; ++i) {
       const int x = corder[i];
@@ -714,7 +762,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     // the scan reads its arrays sequentially and the predecessors it releases
     // are recent records (cache-resident); last use and the record-space
     // predecessor lists are built in parallel. Same scan, same slots.
-    hvec<int> lu_r(R), rptr(R + 1, 0);
+    hvec<int> lu_r(R);
     host_parallel_for(R, [&](long long b, long long e) {
       for (int i = (int)b; i < (int)e; ++i) {
         const int x = corder[i];
@@ -722,17 +770,9 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
         for (int k = optr[x]; k < optr[x + 1]; ++k)
           m = std::max(m, rec_of_task[(int)(keys[k] & 0xffffffffu)]);
         lu_r[i] = m;
-        rptr[i + 1] = pptr[x + 1] - pptr[x];
       }
     });
-    for (int i = 0; i < R; ++i) rptr[i + 1] += rptr[i];
-    hvec<int> rp(rptr[R]);
-    host_parallel_for(R, [&](long long b, long long e) {
-      for (int i = (int)b; i < (int)e; ++i) {
-        const int x = corder[i];
-        for (int k = pptr[x], o = rptr[i]; k < pptr[x + 1]; ++k, ++o) rp[o] = rec_of_task[padj[k]];
-      }
-    });
+    const hvec<int>& rptr = rp_ptr;  // record-space predecessors from the levels pass
     rt_.mark(" rec:rspace");
     hvec<int> slot_r(R, -1);
     hvec<char> glob_r(R, 0);
