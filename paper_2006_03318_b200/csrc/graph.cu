@@ -1280,14 +1280,25 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
       edr[k] = g->row_of[d->edge_dst[k]];
     }
   });
-  for (long long k = 0; k < E; ++k) {
-    ch_ptr[esr[k] + 1]++;
-    indeg[edr[k]]++;
-  }
+  // multiset CSR by parallel atomic count / scatter; each child list is then
+  // sorted so the layout is deterministic (the schedulers pick by key, not by
+  // list position)
+  host_parallel_for(E, [&](long long b, long long e) {
+    for (long long k = b; k < e; ++k) {
+      __atomic_fetch_add(&ch_ptr[esr[k] + 1], 1, __ATOMIC_RELAXED);
+      __atomic_fetch_add(&indeg[edr[k]], 1, __ATOMIC_RELAXED);
+    }
+  });
   for (int i = 0; i < n; ++i) ch_ptr[i + 1] += ch_ptr[i];
   {
     hvec<int> fill(ch_ptr.begin(), ch_ptr.end() - 1);
-    for (long long k = 0; k < E; ++k) ch_adj[fill[esr[k]]++] = edr[k];
+    host_parallel_for(E, [&](long long b, long long e) {
+      for (long long k = b; k < e; ++k) ch_adj[__atomic_fetch_add(&fill[esr[k]], 1, __ATOMIC_RELAXED)] = edr[k];
+    });
+    host_parallel_for(n, [&](long long b, long long e) {
+      for (long long r = b; r < e; ++r)
+        if (ch_ptr[r + 1] - ch_ptr[r] > 1) std::sort(ch_adj.begin() + ch_ptr[r], ch_adj.begin() + ch_ptr[r + 1]);
+    });
   }
   host_parallel_for(n, [&](long long b, long long e) {
   for (int r = (int)b; r < (int)e; ++r) {
