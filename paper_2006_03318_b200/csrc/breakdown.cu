@@ -52,8 +52,11 @@ __device__ __forceinline__ long long bd_dur(const BreakdownParams& p, int row, i
   return static_cast<const long long*>(p.dur)[(long long)row * p.dld + s];
 }
 
+// CH: the graph has permutable chains (otherwise a lane's v-th row is a plain lookup)
+template <bool CH>
 __device__ __forceinline__ int bd_row(const BreakdownParams& p, int l, int v, int s, bool chain_on) {
   const int base = p.lane_ptr[l];
+  if (!CH) return p.lane_rows[base + v];
   const int c = p.lane_chain[l];
   if (c < 0 || !chain_on) return p.lane_rows[base + v];
   const BdChain ch = p.chains[c];
@@ -66,12 +69,13 @@ __device__ __forceinline__ int bd_row(const BreakdownParams& p, int l, int v, in
   return p.lane_rows[base + v - ch.B];
 }
 
+template <bool CH>
 __device__ __forceinline__ void bd_prefetch(const BreakdownParams& p, LaneCursor& c, int l, int s) {
   if (c.v >= c.len) {
     c.nrow = -1;
     return;
   }
-  const int row = bd_row(p, l, c.v, s, c.chain_on);
+  const int row = bd_row<CH>(p, l, c.v, s, c.chain_on);
   ++c.v;
   c.nrow = row;
   c.nst = __ldcs(&p.start[(long long)row * p.start_ld + s]);
@@ -81,11 +85,12 @@ __device__ __forceinline__ void bd_prefetch(const BreakdownParams& p, LaneCursor
 }
 
 // advance lane l to its next non-empty interval (cls = -1 when exhausted)
+template <bool CH>
 __device__ __forceinline__ void bd_advance(const BreakdownParams& p, LaneCursor& c, int l, int s) {
   while (c.nrow >= 0) {
     const long long st = c.nst, d = c.nd, gp = c.ngap;
     const int rc = c.nrc;
-    bd_prefetch(p, c, l, s);
+    bd_prefetch<CH>(p, c, l, s);
     if (st < 0) continue;  // removed task / absent chain member (start -1)
     long long e = st + d;
     int cls;
@@ -108,26 +113,28 @@ __device__ __forceinline__ void bd_advance(const BreakdownParams& p, LaneCursor&
 }
 
 // start of the lane's v-th row, -1 for removed / absent tasks
+template <bool CH>
 __device__ __forceinline__ long long bd_key(const BreakdownParams& p, int l, int v, int s, bool on) {
-  return p.start[(long long)bd_row(p, l, v, s, on) * p.start_ld + s];
+  return p.start[(long long)bd_row<CH>(p, l, v, s, on) * p.start_ld + s];
 }
 
 // Position to start lane l's scan for a window beginning at T0: the last row
 // whose start is <= T0 (earlier intervals end before it starts), 0 if none.
+template <bool CH>
 __device__ int bd_seek(const BreakdownParams& p, int l, int len, int s, bool on, long long T0) {
   int lo = 0, hi = len;  // first v with key(v) > T0 lies in [lo, hi]
   while (lo < hi) {
     const int mid = (lo + hi) >> 1;
     int m2 = mid;
-    long long k = bd_key(p, l, m2, s, on);
-    while (k == -1 && m2 + 1 < hi) k = bd_key(p, l, ++m2, s, on);
+    long long k = bd_key<CH>(p, l, m2, s, on);
+    while (k == -1 && m2 + 1 < hi) k = bd_key<CH>(p, l, ++m2, s, on);
     if (k == -1 || k > T0)
       hi = mid;
     else
       lo = m2 + 1;
   }
   int v = lo - 1;
-  while (v > 0 && bd_key(p, l, v, s, on) == -1) --v;
+  while (v > 0 && bd_key<CH>(p, l, v, s, on) == -1) --v;
   return v < 0 ? 0 : v;
 }
 
@@ -147,8 +154,9 @@ __global__ void bd_prepare_kernel(const BreakdownParams p) {
 }
 
 // LM: lane capacity (>= L), a compile-time bound so that the per-lane cursors
-// live in registers (every access below is an unrolled loop over l).
-template <int LM>
+// live in registers (every access below is an unrolled loop over l); EXACT:
+// LM == L (no per-lane bound checks); CH: permutable chains present.
+template <int LM, bool EXACT, bool CH>
 __global__ void __launch_bounds__(128) breakdown_kernel(const BreakdownParams p) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   const int k = blockIdx.y;
@@ -168,22 +176,22 @@ __global__ void __launch_bounds__(128) breakdown_kernel(const BreakdownParams p)
     c.cls = -1;
     c.active = false;
     c.nrow = -1;
-    if (l >= p.L) continue;
-    const int c_ix = p.lane_chain[l];
+    if (!EXACT && l >= p.L) continue;
+    const int c_ix = CH ? p.lane_chain[l] : -1;
     bool chain_on = false;
     int len = p.lane_ptr[l + 1] - p.lane_ptr[l];
-    if (c_ix >= 0) {
+    if (CH && c_ix >= 0) {
       chain_on = p.present == nullptr || p.present[(long long)s * p.n_chains + c_ix] != 0;
       if (chain_on) len += p.chains[c_ix].B;
     }
     c.len = len;
     c.chain_on = chain_on;
-    c.v = len > 0 && T0 > 0 ? bd_seek(p, l, len, s, chain_on, T0) : 0;
-    bd_prefetch(p, c, l, s);
+    c.v = len > 0 && T0 > 0 ? bd_seek<CH>(p, l, len, s, chain_on, T0) : 0;
+    bd_prefetch<CH>(p, c, l, s);
   }
 #pragma unroll
   for (int l = 0; l < LM; ++l)
-    if (l < p.L) bd_advance(p, cur[l], l, s);
+    if (EXACT || l < p.L) bd_advance<CH>(p, cur[l], l, s);
   long long acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;  // cpu_only, gpu_only, parallel, idle
   int cc = 0, gc = 0;
   long long t = T0;
@@ -223,7 +231,7 @@ __global__ void __launch_bounds__(128) breakdown_kernel(const BreakdownParams p)
       if (c.active) {
         if (c.cls == 0) --cc; else --gc;
         c.active = false;
-        bd_advance(p, c, l, s);
+        bd_advance<CH>(p, c, l, s);
       } else {
         if (c.cls == 0) ++cc; else ++gc;
         c.active = true;
@@ -286,14 +294,28 @@ cudaError_t launch_breakdown(const BreakdownParams& p, cudaStream_t stream) {
     bd_prepare_kernel<<<std::min(grid, 148 * 16), BD, 0, stream>>>(p);
     note_launch();
     const dim3 g2(grid, p.K);
-    if (p.L <= 4)
-      breakdown_kernel<4><<<g2, BD, 0, stream>>>(p);
-    else if (p.L <= 8)
-      breakdown_kernel<8><<<g2, BD, 0, stream>>>(p);
-    else if (p.L <= 16)
-      breakdown_kernel<16><<<g2, BD, 0, stream>>>(p);
-    else
-      breakdown_kernel<32><<<g2, BD, 0, stream>>>(p);
+    const bool ch = p.n_chains > 0;
+#define BD_LAUNCH(LM, EX)                                                     \
+  do {                                                                        \
+    if (ch)                                                                   \
+      breakdown_kernel<LM, EX, true><<<g2, BD, 0, stream>>>(p);               \
+    else                                                                      \
+      breakdown_kernel<LM, EX, false><<<g2, BD, 0, stream>>>(p);              \
+  } while (0)
+    switch (p.L) {
+      case 1: BD_LAUNCH(1, true); break;
+      case 2: BD_LAUNCH(2, true); break;
+      case 3: BD_LAUNCH(3, true); break;
+      case 4: BD_LAUNCH(4, true); break;
+      default:
+        if (p.L <= 8)
+          BD_LAUNCH(8, false);
+        else if (p.L <= 16)
+          BD_LAUNCH(16, false);
+        else
+          BD_LAUNCH(32, false);
+    }
+#undef BD_LAUNCH
     note_launch();
   }
   if (p.layer_busy && p.row_layer) {
