@@ -28,6 +28,7 @@
 
 #include <algorithm>
 #include <climits>
+#include <cstdlib>
 
 namespace ddsim {
 
@@ -248,41 +249,68 @@ __global__ void __launch_bounds__(128) breakdown_kernel(const BreakdownParams p)
 // per_layer_breakdown (breakdown.py:100-111): per layer, summed CPU and GPU
 // task durations of the scheduled tasks, comm lanes excluded.
 __device__ __forceinline__ void lb_flush(const BreakdownParams& p, int key, long long acc, int s) {
-  if (key >= 0 && acc != 0) p.layer_busy[(long long)key * p.S + s] += acc;
+  // row chunks of one scenario run in different blocks: accumulate atomically
+  if (key >= 0 && acc != 0)
+    atomicAdd(reinterpret_cast<unsigned long long*>(p.layer_busy + (long long)key * p.S + s),
+              (unsigned long long)acc);
 }
+constexpr int kLbRowChunk = 2048;  // rows per block row (blockIdx.y)
 
-__global__ void layer_busy_kernel(const BreakdownParams p) {
+// NEG: start rows may hold -1 (dropped tasks) and must be read; otherwise
+// only the durations are (a third of the bytes). A layer's CPU launches and GPU
+// kernels interleave in row order, so both classes of the current layer are
+// accumulated in registers and flushed when the layer changes (a flush per
+// class change cost a read-modify-write of [layer][class][S] per row).
+template <bool NEG>
+__global__ void __launch_bounds__(128) layer_busy_kernel(const BreakdownParams p) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= p.S) return;
-  int key = -1;  // run-length accumulator: (layer * 2 + class) of the current run
-  long long acc = 0;
-  constexpr int U = 4;
-  for (int r0 = 0; r0 < p.n; r0 += U) {
+  int lay = -1;  // layer of the current run
+  long long acc_c = 0, acc_g = 0;
+  constexpr int U = 8;  // rows in flight per thread
+  const int rbeg = blockIdx.y * kLbRowChunk;
+  const int rend = min(p.n, rbeg + kLbRowChunk);
+  for (int r0 = rbeg; r0 < rend; r0 += U) {
     long long st[U], d[U];
-    int kk[U];
+    int ly[U], gpu[U];
 #pragma unroll
     for (int j = 0; j < U; ++j) {
       const int row = r0 + j;
-      kk[j] = -1;
-      if (row < p.n) {
+      ly[j] = -1;
+      gpu[j] = 0;
+      st[j] = 0;
+      d[j] = 0;
+      if (row < rend) {
         const int rc = __ldg(&p.row_class[row]);
-        if (rc != BD_COMM) kk[j] = __ldg(&p.row_layer[row]) * 2 + (rc == BD_GPU ? 1 : 0);
-        st[j] = __ldcs(&p.start[(long long)row * p.start_ld + s]);
+        if (rc != BD_COMM) {
+          ly[j] = __ldg(&p.row_layer[row]);
+          gpu[j] = rc == BD_GPU;
+        }
+        if (NEG) st[j] = __ldcs(&p.start[(long long)row * p.start_ld + s]);
         d[j] = bd_dur(p, row, s);
       }
     }
 #pragma unroll
     for (int j = 0; j < U; ++j) {
-      if (kk[j] < 0 || st[j] < 0) continue;
-      if (kk[j] != key) {
-        lb_flush(p, key, acc, s);
-        key = kk[j];
-        acc = 0;
+      if (ly[j] < 0 || (NEG && st[j] < 0)) continue;
+      if (ly[j] != lay) {
+        if (lay >= 0) {
+          lb_flush(p, lay * 2, acc_c, s);
+          lb_flush(p, lay * 2 + 1, acc_g, s);
+        }
+        lay = ly[j];
+        acc_c = acc_g = 0;
       }
-      acc += d[j];
+      if (gpu[j])
+        acc_g += d[j];
+      else
+        acc_c += d[j];
     }
   }
-  lb_flush(p, key, acc, s);
+  if (lay >= 0) {
+    lb_flush(p, lay * 2, acc_c, s);
+    lb_flush(p, lay * 2 + 1, acc_g, s);
+  }
 }
 
 cudaError_t launch_breakdown(const BreakdownParams& p, cudaStream_t stream) {
@@ -321,7 +349,12 @@ cudaError_t launch_breakdown(const BreakdownParams& p, cudaStream_t stream) {
   if (p.layer_busy && p.row_layer) {
     cudaError_t e = launch_fill_i64(p.layer_busy, 0, (long long)p.n_layers * 2 * p.S, stream);
     if (e != cudaSuccess) return e;
-    layer_busy_kernel<<<grid, BD, 0, stream>>>(p);
+    if ((p.n + kLbRowChunk - 1) / kLbRowChunk > 65535) return cudaErrorInvalidValue;  // > 134M rows
+    const dim3 g3(grid, (p.n + kLbRowChunk - 1) / kLbRowChunk);
+    if (p.start_may_be_neg)
+      layer_busy_kernel<true><<<g3, BD, 0, stream>>>(p);
+    else
+      layer_busy_kernel<false><<<g3, BD, 0, stream>>>(p);
     note_launch();
   }
   return cudaGetLastError();

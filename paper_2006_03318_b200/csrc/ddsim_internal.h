@@ -273,6 +273,7 @@ struct BreakdownParams {
   const int* row_layer;     // [n] or null
   long long* layer_busy;
   int n_layers;
+  int start_may_be_neg;     // removal steps / permutable chains: start -1 marks a dropped task
 };
 cudaError_t launch_breakdown(const BreakdownParams& p, cudaStream_t stream);
 

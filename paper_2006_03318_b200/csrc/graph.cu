@@ -2283,6 +2283,7 @@ int breakdown_impl(const ks_graph* g, const ks_scenarios_desc* sc, const int64_t
   p.gaps_as_cpu_busy = bd->gaps_as_cpu_busy;
   p.parts = reinterpret_cast<long long*>(parts);
   p.bad = T.scratch<int>((size_t)S);
+  p.start_may_be_neg = (g->n_chains > 0 || T.has_remove) ? 1 : 0;
   {
     // time windows per scenario: enough (scenario, window) threads to fill the
     // GPU, at least ~512 rows of work per window
