@@ -300,7 +300,12 @@ def run_ours(args):
         # pinned host buffers are (4 + 8) B per update: cap them at ~80 GB per node
         S_e = S if ws == 1 else max(1024, (S // ws) // 32 * 32)
         h_dense = torch.empty((rows, S_e), dtype=torch.int32, pin_memory=True)
-        h_dense.copy_(dense[:, :S_e])
+        if S_e == S:
+            h_dense.copy_(dense)
+        else:  # strided column slice: copy in row blocks (a whole-slice copy stages a
+            step = max(1, (1 << 28) // S_e)  # contiguous device temporary of the full slice)
+            for r0 in range(0, rows, step):
+                h_dense[r0:r0 + step].copy_(dense[r0:r0 + step, :S_e])
         h_start = torch.empty((rows, S_e), dtype=torch.int64, pin_memory=True)
         h_ms = torch.empty(S_e, dtype=torch.int64, pin_memory=True).numpy()
         h_lb = torch.empty((S_e, L), dtype=torch.int64, pin_memory=True).numpy()
