@@ -694,7 +694,6 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
         rec_of_chain[x - n] = i;
     }
   });
-  auto rec_of_val = [&](int t) { return chain_of[t] >= 0 ? rec_of_chain[chain_of[t]] : rec_of_task[t]; };
   hvec<int> last_use;
   // inputs of each record (flat CSR: rin_ptr / rin)
   hvec<int> rin_ptr, rin;

@@ -187,8 +187,13 @@ cudaError_t launch_maxplus_lanes(const LaneParams& p, const LaneChainParams* cp,
         launch_maxplus_lanes_jit(p, cp, dense32, &tmap, dkind, V, *codes, grid, BD, smem, stream);
     if (e == cudaSuccess) return cudaGetLastError();
   }
-  const ddsim_lanes::Tmap& tm = *reinterpret_cast<const ddsim_lanes::Tmap*>(&tmap);
-  const ddsim_lanes::Params& pp = *reinterpret_cast<const ddsim_lanes::Params*>(&p);
+  // the kernels' parameter types mirror the host structs byte for byte
+  static_assert(sizeof(ddsim_lanes::Tmap) == sizeof(CUtensorMap), "tensor map layout");
+  static_assert(sizeof(ddsim_lanes::Params) == sizeof(LaneParams), "lane params layout");
+  ddsim_lanes::Tmap tm;
+  ddsim_lanes::Params pp;
+  memcpy(&tm, &tmap, sizeof(tm));
+  memcpy(&pp, &p, sizeof(pp));
   cudaError_t err;
 #define LAUNCH_L(DK, VV)                                                                      \
   if (cp != nullptr) {                                                                        \
