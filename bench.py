@@ -183,6 +183,24 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def _bind_to_gpu_numa(dev: int):
+    """Run the host side (and first-touch the pinned e2e buffers) on the CPUs
+    local to the GPU's PCIe root (NVML affinity); no-op when NVML is missing."""
+    try:
+        import pynvml
+        pynvml.nvmlInit()
+        h = pynvml.nvmlDeviceGetHandleByIndex(dev)
+        words = pynvml.nvmlDeviceGetCpuAffinity(h, (os.cpu_count() + 63) // 64)
+        cpus = {w * 64 + b for w, m in enumerate(words) for b in range(64) if (m >> b) & 1}
+        cpus &= set(range(os.cpu_count()))
+        if cpus:
+            os.sched_setaffinity(0, cpus)
+            return len(cpus)
+    except Exception:
+        pass
+    return None
+
+
 def run_ours(args):
     import torch
 
@@ -299,6 +317,8 @@ def run_ours(args):
     if not args.no_e2e:
         # pinned host buffers are (4 + 8) B per update: cap them at ~80 GB per node
         S_e = S if ws == 1 else max(1024, (S // ws) // 32 * 32)
+        all_cpus = os.sched_getaffinity(0)
+        numa_cpus = None if os.environ.get("DDSIM_BENCH_NO_NUMA") else _bind_to_gpu_numa(dev)
         h_dense = torch.empty((rows, S_e), dtype=torch.int32, pin_memory=True)
         if S_e == S:
             h_dense.copy_(dense)
@@ -326,7 +346,7 @@ def run_ours(args):
         if ws > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        n_e2e = max(1, min(args.steps, 2))
+        n_e2e = max(1, min(args.steps, 3))
         for _ in range(n_e2e):
             e2e_step()
         dt = time.perf_counter() - t0
@@ -337,7 +357,10 @@ def run_ours(args):
         assert np.array_equal(h_ms, ms[:S_e].cpu().numpy()), "e2e result differs from device run"
         e2e = {"value": rows * S_e * n_e2e * ws / dt, "unit": UNIT,
                "h2d_bytes_per_step": rows * S_e * 4,
-               "d2h_bytes_per_step": rows * S_e * 8 + S_e * 8 + S_e * L * 8}
+               "d2h_bytes_per_step": rows * S_e * 8 + S_e * 8 + S_e * L * 8,
+               "host_cpus_bound": numa_cpus}
+        del h_dense, h_start
+        os.sched_setaffinity(0, all_cpus)  # the CPU baseline uses every core
 
     cb = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
