@@ -4,7 +4,7 @@
 
 Workload (BASELINE.json configs[3]): Monte-Carlo duration-jitter sweep of a
 100k-task GPT-style iteration graph (1 CPU thread + 2 CUDA streams),
-65,536 scenarios per GPU.  Scenario s of task v runs for
+65,536 scenarios.  Scenario s of task v runs for
 d' = floor((2 d k + 1000) / 2000) with k ~ U{900..1100} (round_half_up of
 d * k/1000, transform.py:174-183), materialised as int32 [rows][S] in HBM.
 
@@ -14,8 +14,13 @@ of every (task, scenario), per-scenario makespan and lane busy times.
 the same through the C-ABI host-buffer entry point (ks_simulate_host), with
 the H2D of durations and D2H of all results inside the timed region.
 
-Multi-GPU (torchrun): one process per GPU, scenarios sharded (weak scaling:
-65,536 per GPU), no data-path collective; barrier + max-over-ranks timing.
+Multi-GPU: one process per GPU (torchrun; `--gpus N` without torchrun
+re-launches itself under torch.distributed.run), scenarios sharded, no
+data-path collective; barrier + max-over-ranks timing.  --scaling strong
+(default, BASELINE config 4 as stated: 65,536 scenarios in total, sharded
+across the N GPUs) or weak (65,536 scenarios per GPU).  After timing, every
+rank checks scenarios of its own timed output against the C oracle (Alg. 1)
+and rank 0 prints them as `parity_checked`.
 
 --impl reference: the reference algorithm (Alg. 1, sim.py:89-142) as the C
 oracle port on the host cores (the reference is pure Python and cannot be
@@ -121,6 +126,50 @@ class Clocks:
                 "gpu_temp_c_max": max(tgpu) if tgpu else None}
 
 
+def make_jitter_dense(fz, S: int, seed: int, device: int):
+    """Config-4 jitter durations on the device: int32 [rows][S] (frozen rows),
+    d' = floor((2 d k + 1000) / 2000), k ~ U{900..1100} (torch Generator)."""
+    import torch
+
+    base = torch.from_numpy(fz.duration[fz.order].copy()).to(f"cuda:{device}")
+    dense = torch.empty((fz.n, S), dtype=torch.int32, device=f"cuda:{device}")
+    gen = torch.Generator(device=f"cuda:{device}")
+    gen.manual_seed(seed)
+    step_rows = max(1, (1 << 28) // S)
+    for r0 in range(0, fz.n, step_rows):
+        r1 = min(fz.n, r0 + step_rows)
+        k = torch.randint(900, 1101, (r1 - r0, S), generator=gen, device=f"cuda:{device}",
+                          dtype=torch.int64)
+        dense[r0:r1] = ((2 * base[r0:r1, None] * k + 1000) // 2000).to(torch.int32)
+        del k
+    return dense
+
+
+def oracle_check(w, fz, dense, start, ms, lb, cols) -> list:
+    """Scenarios `cols` of a device result against the C oracle's Alg. 1
+    (checker only, after the timed region): start of every task, makespan,
+    lane busy.  Raises on the first difference."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    from oracle import OracleGraph  # checker
+
+    og = OracleGraph.from_graph(w.graph)
+    done = []
+    for s in cols:
+        d = np.empty(fz.n, np.int64)
+        d[fz.order] = dense[:, s].cpu().numpy()
+        st, m, lbo, _ = og.simulate("default", dur=d)
+        got = start[:, s].cpu().numpy()
+        want = np.array([st[int(t)] for t in fz.row_ids], np.int64)
+        if int(ms[s].item()) != m or not np.array_equal(got, want):
+            raise AssertionError(f"scenario {s}: device result differs from the oracle "
+                                 f"(makespan {int(ms[s].item())} vs {m})")
+        lbd = {str(fz.lanes[j]): int(lb[s, j].item()) for j in range(fz.L)}
+        if lbd != {str(k): v for k, v in lbo.items()}:
+            raise AssertionError(f"scenario {s}: lane busy differs from the oracle")
+        done.append(int(s))
+    return done
+
+
 def build_workload(device: int):
     from paper_2006_03318_b200.frozen import FrozenGraph
     from paper_2006_03318_b200.workloads import gpt_trace
@@ -151,6 +200,7 @@ def cpu_baseline(w, fz, target_s: float = 12.0) -> dict:
         t_used += time.perf_counter() - t0
         upd += u
     return {"value": upd / t_used, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample_scenarios": upd // len(base),
             "sample": f"{upd // len(base)} scenarios x {len(base)} tasks of the config-4 graph, "
                       f"{t_used:.1f} s wall, oracle/ddsim_oracle.c Alg.1 port (pthreads)"}
 
@@ -174,10 +224,11 @@ def run_reference(args):
     v = statistics.median(vals)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "config": {"workload": "config4 monte-carlo jitter: gpt-style 100k tasks (1 cpu + 2 "
                                    "streams), jitter k~U{900..1100}", "tasks": N_TASKS,
-                       "scenarios_per_step": "sample (see cpu_baseline.sample)"},
+                       "scenarios_per_step": "sample (see cpu_baseline.sample)",
+                       "sample_scenarios_per_step": cb["sample_scenarios"]},
             "cpu_baseline": dict(cb, value=v),
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -221,20 +272,10 @@ def run_ours(args):
     from paper_2006_03318_b200.batch import ScenarioTable, simulate_batch_device
 
     w, fz = build_workload(dev)
-    S = args.scenarios
+    S = shard_size(args.scenarios, ws, args.scaling)
     rows, L = fz.n, fz.L
     # ---- device-resident inputs: dense jitter durations [rows][S] int32 ----
-    base = torch.from_numpy(fz.duration[fz.order].copy()).to(f"cuda:{dev}")
-    dense = torch.empty((rows, S), dtype=torch.int32, device=f"cuda:{dev}")
-    gen = torch.Generator(device=f"cuda:{dev}")
-    gen.manual_seed(1000 + rank)
-    step_rows = max(1, (1 << 28) // S)
-    for r0 in range(0, rows, step_rows):
-        r1 = min(rows, r0 + step_rows)
-        k = torch.randint(900, 1101, (r1 - r0, S), generator=gen, device=f"cuda:{dev}",
-                          dtype=torch.int64)
-        dense[r0:r1] = ((2 * base[r0:r1, None] * k + 1000) // 2000).to(torch.int32)
-        del k
+    dense = make_jitter_dense(fz, S, 1000 + rank, dev)
     start = torch.empty((rows, S), dtype=torch.int64, device=f"cuda:{dev}")
     ms = torch.empty(S, dtype=torch.int64, device=f"cuda:{dev}")
     lb = torch.empty((S, L), dtype=torch.int64, device=f"cuda:{dev}")
@@ -293,9 +334,14 @@ def run_ours(args):
     peak, peak_src = _peaks()
     achieved = updates_per_step * BYTES_PER_UPDATE / (per_launch_ms / 1e3) / 1e9
 
-    # sanity: spot-check one scenario against the device list scheduler path is
-    # done in tests; here only assert the makespan is positive
-    assert int(ms[0].item()) > 0
+    # parity of the timed output itself: first, middle and last scenario of this
+    # rank's shard against the C oracle's Alg. 1 (outside the timed region)
+    checked = oracle_check(w, fz, dense, start, ms, lb, sorted({0, S // 2 + 1, S - 1}))
+    if ws > 1:
+        import torch.distributed as dist
+        ok = torch.tensor([len(checked)], device=f"cuda:{dev}")
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        assert int(ok.item()) == len(checked)
 
     # speed of light of this exact traffic pattern: a library int32 -> int64
     # widening copy over the same matrices (26 GB read + 52 GB write, no compute)
@@ -315,8 +361,8 @@ def run_ours(args):
     # ---- e2e through the host-buffer C-ABI (H2D + D2H inside the timed region)
     e2e = None
     if not args.no_e2e:
-        # pinned host buffers are (4 + 8) B per update: cap them at ~80 GB per node
-        S_e = S if ws == 1 else max(1024, (S // ws) // 32 * 32)
+        # same shard as the device-resident run (pinned host buffers: 12 B per update)
+        S_e = S
         all_cpus = os.sched_getaffinity(0)
         numa_cpus = None if os.environ.get("DDSIM_BENCH_NO_NUMA") else _bind_to_gpu_numa(dev)
         def pinned(shape, dtype):
@@ -380,9 +426,8 @@ def run_ours(args):
                "h2d_bytes_per_step": rows * S_e * 4,
                "d2h_bytes_per_step": rows * S_e * 8 + S_e * 8 + S_e * L * 8,
                "host_cpus_bound": numa_cpus}
-        for t, _m in registered:
-            torch.cuda.cudart().cudaHostUnregister(t.data_ptr())
-        del h_dense, h_start, registered
+        del h_dense, h_start
+        _release_registered(registered)
         os.sched_setaffinity(0, all_cpus)  # the CPU baseline uses every core
 
     cb = None
@@ -392,19 +437,25 @@ def run_ours(args):
         line = {
             "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": per_launch_ms, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "int64",
+            "data": "synthetic",
             "config": {"workload": "config4 monte-carlo jitter: gpt-style iteration graph "
-                                   f"({rows} tasks, 1 cpu thread + 2 streams), {S} scenarios "
-                                   "per GPU, k~U{900..1100} int32 durations resident in HBM",
-                       "tasks": rows, "scenarios_per_gpu": S, "lanes": L,
+                                   f"({rows} tasks, 1 cpu thread + 2 streams), {S * ws} "
+                                   f"scenarios ({S} per GPU), k~U{{900..1100}} int32 durations "
+                                   "resident in HBM",
+                       "tasks": rows, "scenarios_total": S * ws, "scenarios_per_gpu": S,
+                       "lanes": L,
                        "l2": "inputs (26 GB) >> 126 MB L2; no flush needed",
                        "graph_slots_smem": fz.info.n_slots_smem,
                        "graph_slots_spill": fz.info.n_slots - fz.info.n_slots_smem},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "peak_source": peak_src,
                          "algorithmic_bytes_per_launch": updates_per_step * BYTES_PER_UPDATE,
-                         # ncu capture of the default workload (65,536 scenarios per GPU)
+                         # from the stored ncu --set full capture of this command
+                         # (profiles/ncu_summary.json), not measured in this run
                          "traffic": _ncu_traffic("ddsim_lanes_jit") if S == S_PER_GPU else None,
+                         "traffic_source": "profiles/ncu_summary.json (stored ncu capture "
+                                           "of the default workload)",
                          "pattern_copy_gbs": pattern_gbs,
                          "pattern_frac": achieved / pattern_gbs,
                          "pattern": "ks_probe_widen: int32 -> int64 stream over the same "
@@ -412,6 +463,9 @@ def run_ours(args):
                                     "no recurrence)"},
             "cpu_baseline": cb,
             "e2e": e2e,
+            "parity_checked": {"scenarios_rank0": checked, "ranks": ws,
+                               "checker": "oracle/ddsim_oracle.c Alg. 1 (sim.py:89-142): "
+                                          "every start, makespan, lane busy"},
             "gpu_launches": launches,
             "result_gather": gather,
             "kernel": kernel_name,
@@ -422,9 +476,50 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+def shard_size(total: int, ws: int, scaling: str) -> int:
+    """Scenarios per rank: strong = the total split over the ranks (a multiple
+    of 32), weak = the total on every rank."""
+    if scaling == "weak" or ws == 1:
+        return total
+    return max(32, (total // ws) // 32 * 32)
+
+
+def _release_registered(registered: list) -> None:
+    """Unregister and unmap the e2e host buffers (huge-page mmaps)."""
+    import torch
+
+    while registered:
+        t, m = registered.pop()
+        rc = torch.cuda.cudart().cudaHostUnregister(t.data_ptr())
+        if int(rc) != 0:
+            print(f"warning: cudaHostUnregister returned {rc}", file=sys.stderr)
+        del t
+        try:
+            m.close()
+        except BufferError:  # a view is still alive; the mapping goes with it
+            pass
+
+
+def _spawn(args_n: int) -> int:
+    """`bench.py --gpus N` outside torchrun: re-launch under torch.distributed.run
+    (one process per GPU, rendezvous on 127.0.0.1) and forward its output."""
+    import socket
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args_n}", "--master-addr=127.0.0.1", f"--master-port={port}",
+           str(Path(__file__).resolve()), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="strong: --scenarios in total over all GPUs (BASELINE config 4); "
+                         "weak: --scenarios per GPU")
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
@@ -432,6 +527,12 @@ def main():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(_spawn(args.gpus))
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    if args.gpus != ws:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE={ws}; measuring {ws} rank(s)",
+              file=sys.stderr)
     if args.impl == "reference":
         run_reference(args)
     else:

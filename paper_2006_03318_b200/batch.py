@@ -127,7 +127,10 @@ class ScenarioTable:
     chain_present: np.ndarray | None = None  # uint8[S][n_chains]
     vdnn_rank: np.ndarray | None = None  # int32[rows]
 
-    def desc(self, keep: list) -> N.ScenariosDesc:
+    def desc(self, keep: list, rows: int | None = None) -> N.ScenariosDesc:
+        """C descriptor of the table.  ``rows`` (the frozen graph's row
+        count) is checked against a dense table: the kernels read
+        dense[r * ld + s] for every frozen row r and scenario s."""
         sc = N.ScenariosDesc()
         S = self.n_scenarios
         sc.n_scenarios = S
@@ -137,12 +140,19 @@ class ScenarioTable:
             sc.dense_kind = 1 if dt.endswith("int32") else 2
             if not dt.endswith(("int32", "int64")):
                 raise ValueError("dense durations must be int32 or int64")
-            sc.dense = N.ptr(d)
-            sc.dense_ld = int(d.shape[1]) if d.ndim == 2 else S
+            if d.ndim != 2:
+                raise ValueError("dense durations must be a [rows][scenarios] matrix")
             if hasattr(d, "stride") and callable(d.stride):
-                sc.dense_ld = int(d.stride(0))
-            elif isinstance(d, np.ndarray):
-                sc.dense_ld = d.strides[0] // d.itemsize
+                ld, inner = int(d.stride(0)), int(d.stride(1))
+            else:
+                ld, inner = d.strides[0] // d.itemsize, d.strides[1] // d.itemsize
+            if inner != 1 or d.shape[1] < S or ld < S:
+                raise ValueError("dense durations need unit inner stride and at least "
+                                 "n_scenarios columns")
+            if rows is not None and d.shape[0] < rows:
+                raise ValueError(f"dense durations have {d.shape[0]} rows, the graph {rows}")
+            sc.dense = N.ptr(d)
+            sc.dense_ld = ld
         if self.overrides:
             rows = np.array(sorted(self.overrides), np.int32)
             vals = np.ascontiguousarray(np.stack([np.asarray(self.overrides[r], np.int64)
@@ -205,7 +215,7 @@ def simulate_batch(frozen: FrozenGraph, table: ScenarioTable, policy: str = "def
         missing = frozen.unordered_ids()
         raise Deadlock(f"{len(missing)} tasks never became ready (first ids: {missing[:10]})")
     keep: list = []
-    sc = table.desc(keep)
+    sc = table.desc(keep, frozen.n)
     rows, L = frozen.n, frozen.L
     ms = np.zeros(S, np.int64)
     lb = np.zeros((S, max(L, 1)), np.int64)
@@ -276,7 +286,7 @@ def breakdown_batch_device(frozen: FrozenGraph, table: ScenarioTable, *, start, 
     """ks_breakdown on device tensors (start / makespan from
     simulate_batch_device on the same table); asynchronous on ``stream``."""
     keep: list = []
-    sc = table.desc(keep)
+    sc = table.desc(keep, frozen.n)
     bd = N.BreakdownDesc()
     rc = frozen.row_classes()
     keep.append(rc)
@@ -300,7 +310,7 @@ def simulate_batch_device(frozen: FrozenGraph, table: ScenarioTable, *, makespan
     """Device tensors in/out (ks_simulate): asynchronous on ``stream``
     (a cudaStream_t as int, e.g. torch.cuda.current_stream().cuda_stream)."""
     keep: list = []
-    sc = table.desc(keep)
+    sc = table.desc(keep, frozen.n)
     out = N.SimOut()
     out.makespan = N.ptr(makespan)
     out.lane_busy = N.ptr(lane_busy)

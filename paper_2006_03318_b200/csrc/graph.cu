@@ -1489,6 +1489,11 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
   const int S = sc->n_scenarios;
   if (S <= 0) fail(KS_ERR_INVALID, "n_scenarios must be positive");
   if (policy < 0 || policy > 2) fail(KS_ERR_INVALID, "unknown policy");
+  // every path indexes dense[r * dense_ld + s] and start[r * start_ld + s]
+  if (sc->dense_kind != 0 && sc->dense != nullptr && sc->dense_ld < S)
+    fail(KS_ERR_INVALID, "dense_ld must be >= n_scenarios");
+  if (out->start != nullptr && out->start_ld < S)
+    fail(KS_ERR_INVALID, "start_ld must be >= n_scenarios");
   bool use_max = path == KS_PATH_MAXPLUS ||
                  (path == KS_PATH_AUTO && g->chained && out->schedule == nullptr);
   if (!use_max && g->n_chains > 0)
@@ -2025,6 +2030,10 @@ int simulate_host_impl(const ks_graph* g, const ks_scenarios_desc* sc, int polic
   if (!g || !sc || !out) fail(KS_ERR_INVALID, "null argument");
   const int S = sc->n_scenarios;
   if (S <= 0) fail(KS_ERR_INVALID, "n_scenarios must be positive");
+  if (sc->dense_kind != 0 && sc->dense != nullptr && sc->dense_ld < S)
+    fail(KS_ERR_INVALID, "dense_ld must be >= n_scenarios");
+  if (out->start != nullptr && out->start_ld < S)
+    fail(KS_ERR_INVALID, "start_ld must be >= n_scenarios");
   DevGuard guard(g->device);
   const long long N = std::max(g->n, 1);
   const bool dense = sc->dense_kind != 0 && sc->dense != nullptr;
@@ -2274,6 +2283,7 @@ int breakdown_impl(const ks_graph* g, const ks_scenarios_desc* sc, const int64_t
     p.dur = buf;
     p.dld = S;
   }
+  if (start_ld < S) fail(KS_ERR_INVALID, "start_ld must be >= n_scenarios");
   p.start = reinterpret_cast<const long long*>(start);
   p.start_ld = start_ld;
   p.makespan = reinterpret_cast<const long long*>(makespan);

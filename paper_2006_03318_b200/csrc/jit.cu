@@ -13,6 +13,7 @@
 #include <cstdio>
 
 #include <cstring>
+#include <atomic>
 #include <map>
 #include <mutex>
 #include <string>
@@ -190,6 +191,11 @@ CUfunction get_function(const std::vector<int>& codes, int dk, int V, bool dyn, 
   return fn;
 }
 
+void log_line(const std::string& msg) {
+  std::lock_guard<std::mutex> lk(g_mu);
+  if (g_jit_log.size() < (1u << 20)) g_jit_log += "\n" + msg;
+}
+
 }  // namespace
 
 // Launch the specialised kernel; cudaErrorNotSupported when JIT is unavailable
@@ -199,7 +205,9 @@ cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const LaneChainParams*
                                      const std::vector<int>& codes, int grid, int BD, size_t smem,
                                      cudaStream_t stream) {
   if (codes.empty() || codes.size() > 32) {
-    g_jit_log += "\nskipped: " + std::to_string(codes.size()) + " handler codes";
+    static std::atomic<bool> logged{false};  // once per process, not per call
+    if (!logged.exchange(true))
+      log_line("skipped: " + std::to_string(codes.size()) + " handler codes");
     return cudaErrorNotSupported;
   }
   int dev = 0;
@@ -217,7 +225,7 @@ cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const LaneChainParams*
   if (!fn) return cudaErrorNotSupported;
   const CUresult ar = g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
   if (ar != CUDA_SUCCESS) {
-    g_jit_log += "\ncuFuncSetAttribute failed: " + std::to_string((int)ar);
+    log_line("cuFuncSetAttribute failed: " + std::to_string((int)ar));
     return cudaErrorNotSupported;
   }
   alignas(64) unsigned char tm[128];
@@ -230,7 +238,7 @@ cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const LaneChainParams*
   const CUresult r = g_drv.launch(fn, grid, 1, 1, BD, 1, 1, (unsigned)smem, (CUstream)stream, args,
                                   nullptr);
   if (r != CUDA_SUCCESS) {
-    g_jit_log += "\ncuLaunchKernel failed: " + std::to_string((int)r);
+    log_line("cuLaunchKernel failed: " + std::to_string((int)r));
     return cudaErrorNotSupported;
   }
   note_launch();
@@ -238,7 +246,13 @@ cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const LaneChainParams*
   return cudaSuccess;
 }
 
-const char* jit_log() { return g_jit_log.c_str(); }
+// A per-thread snapshot: the shared log may grow while the caller reads it.
+const char* jit_log() {
+  thread_local std::string snap;
+  std::lock_guard<std::mutex> lk(g_mu);
+  snap = g_jit_log;
+  return snap.c_str();
+}
 
 }  // namespace ddsim
 

@@ -45,3 +45,36 @@ def strip_trace(obj: dict) -> dict:
 def policy_of(rec: dict) -> tuple[str, dict]:
     pol = (rec.get("pipeline") or {}).get("schedule_policy") or {}
     return pol.get("name", "default"), dict(pol.get("params", {}))
+
+
+def check_recurrence_device(fz, dense, start, makespan, lane_busy, col_block: int = 4096):
+    """Every (task, scenario) of a device max-plus result against the
+    recurrence start(v) = max(ready(v), max_{u->v} start(u)+dur(u)+gap(u)),
+    floored at 0 (sim.py:89-142 on lane-chained graphs == synthetic.py:35-48),
+    plus makespan = max(start + dur) (gap excluded, sim.py:125) and lane busy
+    = per-lane duration sums (sim.py:124).  Torch on the result's device, in
+    scenario blocks; raises AssertionError on the first difference."""
+    import numpy as np
+    import torch
+
+    dev = start.device
+    rows, S = start.shape[0], makespan.shape[0]
+    src = torch.from_numpy(fz.row_of[fz.edge_src].astype(np.int64)).to(dev)
+    dst = torch.from_numpy(fz.row_of[fz.edge_dst].astype(np.int64)).to(dev)
+    gap = torch.from_numpy(fz.gap[fz.order]).to(dev)
+    ready = torch.from_numpy(fz.ready[fz.order]).to(dev)
+    lane = torch.from_numpy(fz.lane[fz.order].astype(np.int64)).to(dev)
+    for c0 in range(0, S, col_block):
+        c1 = min(S, c0 + col_block)
+        st = start[:rows, c0:c1]
+        d = dense[:rows, c0:c1].to(torch.int64)
+        rel = st + d + gap[:, None]
+        want = ready[:, None].clamp(min=0).expand(rows, c1 - c0).contiguous()
+        want.index_reduce_(0, dst, rel[src], "amax", include_self=True)
+        bad = (want != st).nonzero()
+        assert bad.numel() == 0, f"recurrence violated at (row, scenario) {bad[0].tolist()}"
+        fin = (st + d).amax(dim=0)
+        assert torch.equal(fin, makespan[c0:c1]), "makespan != max(start + dur)"
+        lb = torch.zeros((fz.L, c1 - c0), dtype=torch.int64, device=dev)
+        lb.index_add_(0, lane, d)
+        assert torch.equal(lb.t(), lane_busy[c0:c1, :fz.L]), "lane busy != per-lane sums"

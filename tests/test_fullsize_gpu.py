@@ -98,3 +98,38 @@ def test_config3_full_sweep():
         h = apply_pipeline(g, TransformPipeline(steps=steps))
         st, m, _lb, _ = OracleGraph.from_graph(h).simulate("default")
         assert res.makespan[s] == m and res.start_of(s) == st
+
+
+def test_config4_bench_variant_vs_oracle():
+    """The exact launch the config-4 bench times: 65,536 scenarios, int32
+    jitter durations from bench.make_jitter_dense, default environment (V = 2
+    scenarios per thread, NVRTC if-chain handler, global spill slots).  Five
+    scenarios against the C oracle's Alg. 1 (every start, makespan, lane busy)
+    and every (task, scenario) against the max-plus recurrence on the device."""
+    import os
+
+    import torch
+
+    import bench
+    from helpers import check_recurrence_device
+    from paper_2006_03318_b200 import _native as N
+    from paper_2006_03318_b200.batch import simulate_batch_device
+
+    for k in ("DDSIM_LANES_V", "DDSIM_LANES_DYN", "DDSIM_NO_JIT", "DDSIM_NO_LANES"):
+        assert k not in os.environ, k
+    w, fz = bench.build_workload(0)
+    S = bench.S_PER_GPU
+    dense = bench.make_jitter_dense(fz, S, 1000, 0)
+    start = torch.empty((fz.n, S), dtype=torch.int64, device="cuda:0")
+    ms = torch.empty(S, dtype=torch.int64, device="cuda:0")
+    lb = torch.empty((S, fz.L), dtype=torch.int64, device="cuda:0")
+    simulate_batch_device(fz, ScenarioTable(n_scenarios=S, dense=dense), makespan=ms,
+                          lane_busy=lb, start=start,
+                          stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    log = (N.lib().ks_jit_log() or b"").decode()
+    assert "compiled 0:1:2:" in log, log        # device 0, int32 tiles, V = 2, if-chain
+    assert fz.info.n_slots > fz.info.n_slots_smem  # global spill slots in use
+    cols = [0, 1, 18_945, S // 2 + 1, S - 1]
+    assert bench.oracle_check(w, fz, dense, start, ms, lb, cols) == cols
+    check_recurrence_device(fz, dense, start, ms, lb)

@@ -78,3 +78,50 @@ def test_gather_results_world2_gloo(S):
     want = (np.arange(S, dtype=np.int64) * 1000)[:, None].repeat(3, 1).tolist()
     for _rank, full in out:
         assert full == want
+
+
+def _sim_worker(rank, world, port, q):
+    """One rank of a sharded sweep: both ranks on device 0 (a one-GPU box),
+    a real simulate_batch of this rank's contiguous scenario shard, results
+    gathered once over gloo."""
+    import torch.distributed as dist
+    from paper_2006_03318_b200.batch import ScenarioTable, simulate_batch
+    from paper_2006_03318_b200.frozen import FrozenGraph
+    from paper_2006_03318_b200.shard import gather_results, shard_range, table_rows
+    from paper_2006_03318_b200.workloads import resnet_like_graph
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    g = resnet_like_graph(n_pairs=300, seed=3)
+    fz = FrozenGraph.from_graph(g, device=0)
+    S = 203
+    rng = np.random.default_rng(7)
+    base = fz.duration[fz.order]
+    dense = ((2 * base[:, None] * rng.integers(900, 1101, (fz.n, S)) + 1000) // 2000)
+    table = ScenarioTable(n_scenarios=S, dense=dense.astype(np.int64))
+    s0, s1 = shard_range(S, world, rank)
+    sub = table_rows(table, s0, s1)
+    sub.dense = np.ascontiguousarray(sub.dense)
+    res = simulate_batch(fz, sub)
+    local = np.concatenate([res.makespan[:, None], res.lane_busy], axis=1)
+    full = gather_results(local, S)
+    if rank == 0:
+        whole = simulate_batch(fz, table)
+        q.put(("ok", full.tolist(),
+               np.concatenate([whole.makespan[:, None], whole.lane_busy], axis=1).tolist()))
+    dist.destroy_process_group()
+
+
+@pytest.mark.gpu
+def test_sharded_simulate_world2_gloo_matches_single_rank():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_sim_worker, args=(r, 2, port, q)) for r in range(2)]
+    for p in procs:
+        p.start()
+    tag, sharded, single = q.get(timeout=300)
+    for p in procs:
+        p.join(timeout=120)
+        assert p.exitcode == 0
+    assert tag == "ok" and sharded == single

@@ -225,6 +225,11 @@ KERNEL_PATHS = {
     "lanes-static": {"DDSIM_NO_JIT": "1"},
     "lanes-branch-free": {"DDSIM_LANES_DYN": "1"},
     "lanes-if-chain": {"DDSIM_LANES_DYN": "0"},
+    # two scenarios per thread: the variant the config-4 bench times (S >= 18,944)
+    "lanes-v2-jit": {"DDSIM_LANES_V": "2"},
+    "lanes-v2-if-chain": {"DDSIM_LANES_V": "2", "DDSIM_LANES_DYN": "0"},
+    "lanes-v2-branch-free": {"DDSIM_LANES_V": "2", "DDSIM_LANES_DYN": "1"},
+    "lanes-v2-static": {"DDSIM_LANES_V": "2", "DDSIM_NO_JIT": "1"},
     "dense": {"DDSIM_NO_LANES": "1"},
     "general": {"DDSIM_NO_LANES": "1", "DDSIM_NO_DENSE": "1"},
 }
