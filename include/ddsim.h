@@ -117,6 +117,11 @@ typedef struct {
   int32_t n_slots;          /* value slots live at once (smem + spill)       */
   int32_t n_slots_smem;
   int32_t n_levels;         /* longest chain length (levels)                 */
+  /* lane-register program (chained graphs with <= 4 lanes, maxplus_lanes):  */
+  int32_t has_lanes;
+  int32_t n_lane_slots_smem;   /* value slots in shared memory                  */
+  int32_t n_lane_slots_global; /* value slots spilled to global memory          */
+  int32_t n_lane_cuts;         /* rows where the segment-parallel path may cut  */
 } ks_graph_info;
 
 /* Build the device-resident frozen graph on `device`.  Frozen row r holds the

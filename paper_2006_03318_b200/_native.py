@@ -58,7 +58,8 @@ class GraphDesc(C.Structure):
 class GraphInfo(C.Structure):
     _fields_ = [(n, C.c_int32) for n in (
         "n_tasks", "n_lanes", "n_edges_unique", "chained", "n_ordered", "n_slots",
-        "n_slots_smem", "n_levels")]
+        "n_slots_smem", "n_levels", "has_lanes", "n_lane_slots_smem", "n_lane_slots_global",
+        "n_lane_cuts")]
 
 
 class ScaleStep(C.Structure):

@@ -50,14 +50,18 @@ def _run(cmd: list[str], log: Path | None = None) -> str:
 
 
 def _embed_sources() -> None:
-    """csrc/lanes_body.cuh -> generated/lanes_body_src.inc (NVRTC source text)."""
-    body = (CSRC / "lanes_body.cuh").read_text()
+    """NVRTC source texts: csrc/lanes_body.cuh -> generated/lanes_body_src.inc,
+    csrc/lanes_seg.cuh -> generated/lanes_seg_src.inc (generated at build time,
+    not tracked)."""
     gen = CSRC / "generated"
     gen.mkdir(exist_ok=True)
-    out = gen / "lanes_body_src.inc"
-    text = 'static const char* kLanesBodySrc = R"DDSIM_SRC(' + body + ')DDSIM_SRC";\n'
-    if not out.exists() or out.read_text() != text:
-        out.write_text(text)
+    for src, name, var in (("lanes_body.cuh", "lanes_body_src.inc", "kLanesBodySrc"),
+                           ("lanes_seg.cuh", "lanes_seg_src.inc", "kSegBodySrc")):
+        body = (CSRC / src).read_text()
+        out = gen / name
+        text = f'static const char* {var} = R"DDSIM_SRC(' + body + ')DDSIM_SRC";\n'
+        if not out.exists() or out.read_text() != text:
+            out.write_text(text)
 
 
 def build_library(verbose: bool = False) -> Path:

@@ -238,6 +238,23 @@ cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const LaneChainParams*
                                      const std::vector<int>& codes, int grid, int BD, size_t smem,
                                      cudaStream_t stream);
 int maxplus_lanes_vec(int S);
+// Segment-parallel lanes path (mirrors ddsim_lanes::SegParams)
+struct LaneSegParams {
+  const int* cuts;
+  int K;
+  int LN;
+  int* trans;
+  long long* state;
+  long long s_pad;
+};
+cudaError_t launch_maxplus_lanes_seg(const LaneParams& p, const LaneChainParams* cp,
+                                     const int* dense32, int dkind, const std::vector<int>& codes,
+                                     const LaneSegParams& sg, int BD, cudaStream_t stream);
+cudaError_t launch_lanes_seg_jit(bool transfer, const LaneParams& p, const LaneChainParams* cp,
+                                 const void* tmap128, int dkind, int LN,
+                                 const std::vector<int>& codes, const void* segp, int gx, int gy,
+                                 int BD, size_t smem, cudaStream_t stream);
+bool jit_available();
 cudaError_t launch_expand_durations(const long long* base, const unsigned* group,
                                     const int* ovr_map, const long long* ovr, const int* scale_ptr,
                                     const ScaleStepDev* scale, int rows, int S, long long ld,

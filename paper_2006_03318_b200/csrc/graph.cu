@@ -197,6 +197,12 @@ struct ks_graph {
   int ln_rec = 0;          // lanes records (= frozen rows)
   int lksm = 0, lkglob = 0;
   std::vector<int> lane_codes;  // handler codes in decreasing frequency
+  // segment-parallel evaluation (SegParams, lanes_body.cuh): chunk-aligned rows
+  // where no slot value is live and no chain is split, and the prefix sums of
+  // the records' gaps (chain records: their members' gaps)
+  std::vector<int> lane_cuts;
+  std::vector<long long> lane_gap_prefix;
+  bool lane_ready = false;      // some record has a ready floor
   LaneRec* d_lprog = nullptr;
   int* d_lside_off = nullptr;
   int* d_lside_slots = nullptr;
@@ -1231,8 +1237,41 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
       rec.h = (unsigned char)((unsigned)d->lane[v] | (mask << 2) | (rec.gap != 0 ? 128u : 0u));
       lprog[r] = rec;
     }
+    // segment cuts: boundaries b (multiples of the 16-record chunk) with no
+    // slot value live across them (produced before b, read at or after b)
+    // and not inside a chain's no-op rows
+    std::vector<int> cuts;
+    std::vector<long long> gpre(RE + 1, 0);
+    {
+      hvec<int> delta(RE + 2, 0);
+      for (int r = 0; r < RE; ++r)
+        for_values(r, [&](int v) {
+          if (far_use[v] > r) {
+            delta[r + 1]++;
+            delta[far_use[v] + 1]--;
+          }
+        });
+      int live = 0;
+      for (int b = 0; b < RE; ++b) {
+        live += delta[b];
+        if (b > 0 && b % 16 == 0 && live == 0 && ekind[b] != 2) cuts.push_back(b);
+      }
+      for (int r = 0; r < RE; ++r) {
+        long long gsum = 0;
+        if (ekind[r] == 0) {
+          gsum = d->gap[eid[r]];
+        } else if (ekind[r] == 1) {
+          const int c = eid[r];
+          for (int k = d->chain_ptr[c]; k < d->chain_ptr[c + 1]; ++k) gsum += d->gap[d->chain_member[k]];
+        }
+        gpre[r + 1] = gpre[r] + gsum;
+      }
+    }
     // chain members with ready floors stay on the general kernel
     if (ns + ngl < 32000 && !(NC > 0 && any_ready)) {
+      g->lane_cuts = std::move(cuts);
+      g->lane_gap_prefix = std::move(gpre);
+      g->lane_ready = any_ready;
       hvec<long long> freq(256, 0);
       for (int r = 0; r < RE; ++r)
         if (ekind[r] == 0) freq[lprog[r].h]++;
@@ -1482,6 +1521,43 @@ cudaError_t launch_patch_ovr(NodeRec* prog, int n_rec, const int* ovr_map, cudaS
 
 namespace {
 
+// Segment rows for the segment-parallel lanes path, or empty to run the
+// single-pass kernel.  Few scenarios leave most SMs idle (one thread walks
+// every record of its scenario); K segments multiply the parallelism by K at
+// the cost of a transfer pass.  Cuts come from the compiler's clean rows
+// (no live slot value), near K evenly spaced targets.
+std::vector<int> pick_segments(const ks_graph* g, int S, int nsm) {
+  std::vector<int> rows;
+  if (getenv("DDSIM_NO_SEG") || !g->has_lanes || g->lkglob > 0 || g->lane_ready || g->L < 1 ||
+      g->L > 4 || g->lane_cuts.empty() || g->ln_rec < 512)
+    return rows;
+  long long max_s = 16384;
+  if (const char* e = getenv("DDSIM_SEG_MAX_S")) max_s = atoll(e);
+  if (S > max_s) return rows;
+  long long tps = 512;  // target resident threads per SM
+  if (const char* e = getenv("DDSIM_SEG_TPS")) tps = std::max(32LL, atoll(e));
+  long long K = (tps * nsm + S - 1) / S;
+  if (const char* e = getenv("DDSIM_SEG_K")) K = atoll(e);
+  K = std::min<long long>(K, g->ln_rec / 256);  // segments of >= 256 records
+  K = std::min<long long>(K, (long long)g->lane_cuts.size() + 1);
+  if (K < 2) return rows;
+  rows.push_back(0);
+  for (long long k = 1; k < K; ++k) {
+    const long long t = k * (long long)g->ln_rec / K;
+    auto it = std::lower_bound(g->lane_cuts.begin(), g->lane_cuts.end(), (int)t);
+    int best = -1;
+    if (it != g->lane_cuts.end()) best = *it;
+    if (it != g->lane_cuts.begin() && (best < 0 || t - *(it - 1) < best - t)) best = *(it - 1);
+    if (best > rows.back()) rows.push_back(best);
+  }
+  rows.push_back(g->ln_rec);
+  // coefficient entries are int32: every segment's gaps must leave room
+  for (size_t k = 0; k + 1 < rows.size(); ++k)
+    if (g->lane_gap_prefix[rows[k + 1]] - g->lane_gap_prefix[rows[k]] >= (1LL << 29)) return {};
+  if (rows.size() < 3) return {};
+  return rows;
+}
+
 int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, int path,
                   const ks_sim_out* out, cudaStream_t stream) {
   if (!g || !sc || !out) fail(KS_ERR_INVALID, "null argument");
@@ -1619,9 +1695,37 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
     int* flag = T.scratch<int>(1);
     CUDA_TRY(cudaMemsetAsync(flag, 0, sizeof(int), stream));
     p.neg_flag = flag;
-    CUDA_TRY(launch_maxplus_lanes(p, g->n_chains > 0 ? &cp : nullptr,
-                                  dk == 1 ? reinterpret_cast<const int*>(sc->dense) : nullptr, dk,
-                                  &g->lane_codes, stream));
+    const int* d32 = dk == 1 ? reinterpret_cast<const int*>(sc->dense) : nullptr;
+    bool seg_done = false;
+    const std::vector<int> seg = pick_segments(g, S, nsm);
+    if (!seg.empty() && jit_available()) {
+      // one thread per scenario, blocks of <= 128 threads (multiple of 16)
+      const int nb = (S + 127) / 128;
+      const int BDs = std::max(32, ((S + nb - 1) / nb + 15) / 16 * 16);
+      LaneSegParams sg;
+      memset(&sg, 0, sizeof(sg));
+      sg.K = (int)seg.size() - 1;
+      sg.LN = g->L;
+      sg.s_pad = (long long)((S + BDs - 1) / BDs) * BDs;
+      sg.cuts = T.up(seg.data(), seg.size());
+      sg.trans = T.scratch<int>((size_t)(sg.K - 1) * sg.LN * sg.LN * sg.s_pad);
+      sg.state = T.scratch<long long>((size_t)sg.K * sg.LN * sg.s_pad);
+      LaneParams ps = p;
+      ps.s_pad = sg.s_pad;
+      if (ps.makespan) CUDA_TRY(cudaMemsetAsync(ps.makespan, 0, sizeof(long long) * S, stream));
+      if (ps.lane_busy)
+        CUDA_TRY(cudaMemsetAsync(ps.lane_busy, 0, sizeof(long long) * (size_t)S * g->L, stream));
+      const cudaError_t e = launch_maxplus_lanes_seg(ps, g->n_chains > 0 ? &cp : nullptr, d32, dk,
+                                                     g->lane_codes, sg, BDs, stream);
+      if (e == cudaSuccess) {
+        seg_done = true;
+      } else if (e != cudaErrorNotSupported) {
+        CUDA_TRY(e);
+      }
+    }
+    if (!seg_done)
+      CUDA_TRY(launch_maxplus_lanes(p, g->n_chains > 0 ? &cp : nullptr, d32, dk, &g->lane_codes,
+                                    stream));
     MaxplusParams q;
     memset(&q, 0, sizeof(q));
     q.prog = g->d_prog;
@@ -1896,6 +2000,10 @@ int ks_graph_get_info(const ks_graph* g, ks_graph_info* info) {
   info->n_slots = g->n_slots;
   info->n_slots_smem = g->ksm;
   info->n_levels = g->n_levels;
+  info->has_lanes = g->has_lanes ? 1 : 0;
+  info->n_lane_slots_smem = g->lksm;
+  info->n_lane_slots_global = g->lkglob;
+  info->n_lane_cuts = (int)g->lane_cuts.size();
   return KS_OK;
 }
 

@@ -25,6 +25,7 @@ namespace ddsim {
 namespace {
 
 #include "generated/lanes_body_src.inc"  // const char* kLanesBodySrc
+#include "generated/lanes_seg_src.inc"   // const char* kSegBodySrc
 
 typedef int nvrtcResult_t;
 typedef void* nvrtcProgram_t;
@@ -139,21 +140,15 @@ std::string make_source(const std::vector<int>& codes, int dk, int V, bool dyn, 
   return src;
 }
 
-CUfunction get_function(const std::vector<int>& codes, int dk, int V, bool dyn, bool ch,
-                        bool nolb, int device) {
-  std::string key = std::to_string(device) + ":" + std::to_string(dk) + ":" + std::to_string(V) +
-                    (dyn ? ":dyn" : "") + (ch ? ":ch" : "") + (nolb ? ":nolb:" : ":");
-  if (const char* u = getenv("DDSIM_JIT_UNROLL")) key += std::string("u") + u + ":";
-  if (const char* st = getenv("DDSIM_LANES_STAGES")) key += std::string("st") + st + ":";
-  if (const char* b = getenv("DDSIM_LANES_BODY")) key += std::string("b") + b + ":";
-  for (int c : codes) key += std::to_string(c) + ",";
+// Compile `src` once per key (NVRTC -> cubin -> module) and return `fname`;
+// failures are cached as nullptr too (no retry of a failing compile).
+CUfunction get_compiled(const std::string& key, const std::string& src, const char* fname) {
   if (getenv("DDSIM_NO_JIT")) return nullptr;  // checked per call (tests switch paths)
   std::lock_guard<std::mutex> lk(g_mu);
   init_locked();
   if (!g_nv.ok || !g_drv.ok) return nullptr;
   auto it = g_cache.find(key);
   if (it != g_cache.end()) return it->second;
-  const std::string src = make_source(codes, dk, V, dyn, ch, nolb);
   nvrtcProgram_t prog = nullptr;
   CUfunction fn = nullptr;
   if (g_nv.create(&prog, src.c_str(), "ddsim_lanes_jit.cu", 0, nullptr, nullptr) == 0) {
@@ -176,7 +171,7 @@ CUfunction get_function(const std::vector<int>& codes, int dk, int V, bool dyn, 
       const CUresult lr = g_drv.load(&mod, bin.data());
       if (lr != CUDA_SUCCESS) {
         g_jit_log += "\ncuModuleLoadData failed: " + std::to_string((int)lr);
-      } else if (g_drv.getfn(&fn, mod, "ddsim_lanes_jit") != CUDA_SUCCESS) {
+      } else if (g_drv.getfn(&fn, mod, fname) != CUDA_SUCCESS) {
         g_jit_log += "\ncuModuleGetFunction failed";
         fn = nullptr;
       } else {
@@ -187,8 +182,57 @@ CUfunction get_function(const std::vector<int>& codes, int dk, int V, bool dyn, 
     }
     g_nv.destroy(&prog);
   }
-  g_cache[key] = fn;  // nullptr is cached too: do not retry a failing compile
+  g_cache[key] = fn;
   return fn;
+}
+
+CUfunction get_function(const std::vector<int>& codes, int dk, int V, bool dyn, bool ch,
+                        bool nolb, int device) {
+  std::string key = std::to_string(device) + ":" + std::to_string(dk) + ":" + std::to_string(V) +
+                    (dyn ? ":dyn" : "") + (ch ? ":ch" : "") + (nolb ? ":nolb:" : ":");
+  if (const char* u = getenv("DDSIM_JIT_UNROLL")) key += std::string("u") + u + ":";
+  if (const char* st = getenv("DDSIM_LANES_STAGES")) key += std::string("st") + st + ":";
+  if (const char* b = getenv("DDSIM_LANES_BODY")) key += std::string("b") + b + ":";
+  for (int c : codes) key += std::to_string(c) + ",";
+  if (getenv("DDSIM_NO_JIT")) return nullptr;
+  return get_compiled(key, make_source(codes, dk, V, dyn, ch, nolb), "ddsim_lanes_jit");
+}
+
+// Segment kernels (SegParams in lanes_body.cuh): the transfer pass in
+// coefficient form (lanes_seg.cuh) and the replay pass (lanes_body<..., SEG>),
+// both with the graph's handler codes as an if-chain.
+std::string seg_source(const std::vector<int>& codes, int dk, int LN, bool ch, bool transfer) {
+  std::string src = "#define DDSIM_LANES_NO_STD_TYPES 1\n#define DDSIM_UNROLL 2\n";
+  std::string disp = transfer ? "#define DDSIM_DISPATCH(h) hstep_dyn<V>(S, h, d0, d1, gap, sp, ld, store);\n"
+                              : "#define DDSIM_DISPATCH(h) ";
+  std::string sdisp = "#define DDSIM_SYM_DISPATCH(h) ";
+  for (size_t i = 0; i < codes.size(); ++i) {
+    const int c = codes[i];
+    const std::string tp = std::to_string(c & 3) + ", " + std::to_string((c >> 2) & 31) + ", " +
+                           std::to_string((c >> 7) & 1);
+    const std::string cond = (i ? "else if (h == " : "if (h == ") + std::to_string(c) + "u) ";
+    if (!transfer) disp += cond + "hstep<" + tp + ", V>(S, d0, d1, gap, sp, ld, store); ";
+    sdisp += cond + "hsym<" + tp + ", LN>(Y, dv, gp); ";
+  }
+  if (!transfer) disp += "else __trap();\n";
+  sdisp += "else __trap();\n";
+  src += disp + sdisp + kLanesBodySrc + "\n" + kSegBodySrc + "\n";
+  const std::string chp = ch ? ", const __grid_constant__ ddsim_lanes::ChainParams cp" : "";
+  const std::string chr = ch ? "&cp" : "nullptr";
+  if (transfer) {
+    src += "extern \"C\" __global__ void __launch_bounds__(256) ddsim_seg_transfer("
+           "const __grid_constant__ ddsim_lanes::Tmap tmap, const ddsim_lanes::Params p, "
+           "const ddsim_lanes::SegParams sg" + chp + ") {\n  ddsim_lanes::sym_body<" +
+           std::to_string(dk) + ", " + std::to_string(LN) + ", " + (ch ? "true" : "false") +
+           ">(&tmap, p, sg, " + chr + ");\n}\n";
+  } else {
+    src += "extern \"C\" __global__ void __launch_bounds__(256) ddsim_seg_replay("
+           "const __grid_constant__ ddsim_lanes::Tmap tmap, const ddsim_lanes::Params p, "
+           "const ddsim_lanes::SegParams sg" + chp + ") {\n  ddsim_lanes::lanes_body<" +
+           std::to_string(dk) + ", 1, " + (ch ? "true" : "false") + ", true>(&tmap, p, " + chr +
+           ", &sg);\n}\n";
+  }
+  return src;
 }
 
 void log_line(const std::string& msg) {
@@ -244,6 +288,47 @@ cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const LaneChainParams*
   note_launch();
   if (nolb) return launch_lanes_busy(p, dense32, cp != nullptr, stream);
   return cudaSuccess;
+}
+
+// One segment kernel launch (grid gx x K'): transfer or replay.
+cudaError_t launch_lanes_seg_jit(bool transfer, const LaneParams& p, const LaneChainParams* cp,
+                                 const void* tmap128, int dkind, int LN,
+                                 const std::vector<int>& codes, const void* segp, int gx, int gy,
+                                 int BD, size_t smem, cudaStream_t stream) {
+  if (codes.empty() || codes.size() > 32 || LN < 1 || LN > 4) return cudaErrorNotSupported;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::string key = std::string(transfer ? "seg_t:" : "seg_r:") + std::to_string(dev) + ":" +
+                    std::to_string(dkind) + ":" + std::to_string(LN) + (cp ? ":ch:" : ":");
+  for (int c : codes) key += std::to_string(c) + ",";
+  CUfunction fn = get_compiled(key, seg_source(codes, dkind, LN, cp != nullptr, transfer),
+                               transfer ? "ddsim_seg_transfer" : "ddsim_seg_replay");
+  if (!fn) return cudaErrorNotSupported;
+  if (g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem) != CUDA_SUCCESS)
+    return cudaErrorNotSupported;
+  alignas(64) unsigned char tm[128];
+  memcpy(tm, tmap128, 128);
+  LaneParams pp = p;
+  alignas(16) unsigned char sg[sizeof(LaneSegParams)];
+  memcpy(sg, segp, sizeof(sg));
+  LaneChainParams cpv{};
+  if (cp) cpv = *cp;
+  void* args[] = {tm, &pp, sg, &cpv};
+  const CUresult r = g_drv.launch(fn, gx, gy, 1, BD, 1, 1, (unsigned)smem, (CUstream)stream, args,
+                                  nullptr);
+  if (r != CUDA_SUCCESS) {
+    log_line("cuLaunchKernel (segment) failed: " + std::to_string((int)r));
+    return cudaErrorLaunchFailure;
+  }
+  note_launch();
+  return cudaSuccess;
+}
+
+bool jit_available() {
+  if (getenv("DDSIM_NO_JIT")) return false;
+  std::lock_guard<std::mutex> lk(g_mu);
+  init_locked();
+  return g_nv.ok && g_drv.ok;
 }
 
 // A per-thread snapshot: the shared log may grow while the caller reads it.

@@ -67,6 +67,22 @@ struct ChainParams {
   int n_chains;
 };
 
+// Segment-parallel evaluation (small scenario counts): the record stream is
+// cut into K segments at rows where no slot value is live, so a segment's
+// input is the L lane heads only.  seg_transfer (lanes_seg.cuh) computes each
+// segment's (max,+) transfer matrix per scenario, seg_scan composes them into
+// every segment's input lane heads, and the replay (lanes_body<..., SEG>)
+// re-walks each segment from its true input writing the start times.
+struct SegParams {
+  const int* cuts;           // [K+1] segment row boundaries (multiples of kChunkL)
+  int K;
+  int LN;                    // lanes in the transfer matrices (graph lane count)
+  int* trans;                // [K-1][LN*LN][s_pad]: entry (j, i) = longest path weight
+                             // from input lane head i to output lane head j, < 0 = none
+  long long* state;          // [K][LN][s_pad]: lane heads at segment starts (seg_scan)
+  long long s_pad;
+};
+
 // CUtensorMap-compatible opaque kernel parameter (128 B, 64 B aligned)
 struct alignas(64) Tmap {
   unsigned long long w[16];
@@ -328,9 +344,13 @@ __device__ __forceinline__ void chain_record(const Params& p, const ChainParams&
 // Each thread owns V consecutive scenarios (V = 1 or 2).
 // CH: the graph has permutable chains (chain / no-op records).  Without them
 // the chain code is compiled out, so the hot loop keeps its registers.
-template <int DK, int V, bool CH = false>
+// SEG: replay of segment blockIdx.y (rows cuts[y] .. cuts[y+1]) from the lane
+// heads seg_scan computed; makespan / lane busy accumulate with atomics into
+// outputs zeroed by the launcher.
+template <int DK, int V, bool CH = false, bool SEG = false>
 __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
-                                           const ChainParams* cpp = nullptr) {
+                                           const ChainParams* cpp = nullptr,
+                                           const SegParams* sgp = nullptr) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int BD = blockDim.x;
   const int W = BD * V;  // scenarios per CTA
@@ -350,11 +370,16 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
   const int s0 = blockIdx.x * W;
   const int s = s0 + tid * V;
   const bool act = s < p.S;  // S % V == 0 (host)
-  const int nchunks = (p.n_rec + kChunkL - 1) / kChunkL;
+  int r_end = p.n_rec, c_begin = 0;
+  if constexpr (SEG) {
+    c_begin = sgp->cuts[blockIdx.y] / kChunkL;
+    r_end = sgp->cuts[blockIdx.y + 1];
+  }
+  const int nchunks = (r_end + kChunkL - 1) / kChunkL;
   const unsigned tile_bytes = (unsigned)(kChunkL * W) * ES;
   auto issue = [&](int c) {
-    const int st = c % kStagesL;
-    const int nrec = min(kChunkL, p.n_rec - c * kChunkL);
+    const int st = (c - c_begin) % kStagesL;
+    const int nrec = min(kChunkL, r_end - c * kChunkL);
     const unsigned pb = (unsigned)(nrec * sizeof(Rec));
     l_expect(&bars[st], pb + tile_bytes);
     l_bulk(pst + st * kChunkL, p.prog + (long long)c * kChunkL, pb, &bars[st]);
@@ -368,13 +393,23 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
   }
   __syncthreads();
   if (tid == 0)
-    for (int c = 0; c < min(kStagesL, nchunks); ++c) issue(c);
+    for (int c = c_begin; c < min(c_begin + kStagesL, nchunks); ++c) issue(c);
 
   St<V> S;
 #pragma unroll
   for (int l = 0; l <= NLANE; ++l)
 #pragma unroll
     for (int i = 0; i < V; ++i) S.lv[l][i] = 0;
+  if constexpr (SEG) {
+    if (blockIdx.y > 0 && act) {
+      const long long* st0 = sgp->state + (long long)blockIdx.y * sgp->LN * sgp->s_pad + s;
+#pragma unroll
+      for (int l = 0; l < NLANE; ++l)
+        if (l < sgp->LN)
+#pragma unroll
+          for (int i = 0; i < V; ++i) S.lv[l][i] = st0[(long long)l * sgp->s_pad + i];
+    }
+  }
 #pragma unroll
   for (int l = 0; l < NLANE; ++l)
 #pragma unroll
@@ -383,17 +418,17 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
   int neg = 0;
   const long long ld = p.start_ld;
   const bool store = act && p.start != nullptr;
-  long long* sp = store ? p.start + s : nullptr;
+  long long* sp = store ? p.start + (long long)c_begin * kChunkL * ld + s : nullptr;
   const unsigned row_pitch = (unsigned)W * ES;
   const int ksm = p.ksm;
 
 
-  for (int c = 0; c < nchunks; ++c) {
-    const int st = c % kStagesL;
-    l_wait(&bars[st], (unsigned)((c / kStagesL) & 1));
+  for (int c = c_begin; c < nchunks; ++c) {
+    const int st = (c - c_begin) % kStagesL;
+    l_wait(&bars[st], (unsigned)(((c - c_begin) / kStagesL) & 1));
     const unsigned rec0 = prog_s + (unsigned)(st * kChunkL * sizeof(Rec));
     const unsigned t0 = tile_s + (unsigned)(st * kChunkL) * row_pitch + (unsigned)tid * ES * V;
-    const int nrec = min(kChunkL, p.n_rec - c * kChunkL);
+    const int nrec = min(kChunkL, r_end - c * kChunkL);
     int4 raw = l_lds128(rec0);
     // prefetched durations of the next record: int32 pair (DK 1) / int64 pair (DK 2)
     int2 dd = make_int2(0, 0);
@@ -509,6 +544,26 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
 #endif
     __syncthreads();
     if (tid == 0 && c + kStagesL < nchunks) issue(c + kStagesL);
+  }
+  if constexpr (SEG) {
+    if (act) {
+      if (neg < 0 && p.neg_flag) atomicOr(p.neg_flag, 1);
+#pragma unroll
+      for (int i = 0; i < V; ++i) {
+        const long long m = i == 0 ? ms0 : ms1;  // >= 0 on this path
+        if (p.makespan && m > 0)
+          atomicMax(reinterpret_cast<unsigned long long*>(p.makespan + s + i),
+                    (unsigned long long)m);
+        if (p.lane_busy)
+#pragma unroll
+          for (int q = 0; q < NLANE; ++q)
+            if (q < p.L && S.lb[q][i] != 0)
+              atomicAdd(reinterpret_cast<unsigned long long*>(p.lane_busy +
+                                                              (long long)(s + i) * p.L + q),
+                        (unsigned long long)S.lb[q][i]);
+      }
+    }
+    return;
   }
   if (act) {
     if (neg < 0 && p.neg_flag) atomicOr(p.neg_flag, 1);

@@ -1,0 +1,250 @@
+// Segment transfer body (NVRTC source, compiled after lanes_body.cuh): the
+// (max,+) transfer matrix of one segment of the lane-register program, per
+// scenario.  See SegParams in lanes_body.cuh for the three-pass scheme.
+//
+// Recurrence (sim.py:89-142 on lane-chained graphs == synthetic.py:35-48):
+//     rel(v) = max_{u->v} rel(u) + dur(v) + gap(v),   start(v) = max_{u->v} rel(u).
+// Within a segment every value is a (max,+) affine function of the input lane
+// heads h_0 .. h_{L-1}:  rel(v) = max_i (A_v,i + h_i).  A value is carried as
+// its L coefficients; a record costs L maxes per predecessor lane and L adds.
+// The constant term is dominated and dropped: every record reads its own lane
+// head, whose coefficient on its own input is >= 0, and inputs are >= 0
+// (durations >= 0 device-checked, gaps >= 0 and no ready floors host-checked).
+//
+// Coefficients are int32 with "none" = a negative number: entries are path
+// weights within the segment, so they stay below 2^30 when the segment's
+// durations + gaps sum below 2^30 (checked per scenario; otherwise the exact
+// general kernel reruns the launch), and kNegSym + that sum stays negative.
+#pragma once
+
+namespace ddsim_lanes {
+
+constexpr int kNegSym = -(1 << 30);
+
+template <int LN>
+struct Sym {
+  int v[NLANE + 1][LN];  // lane heads' coefficients (+ temp lane)
+};
+
+__device__ __forceinline__ int imax(int a, int b) { return a > b ? a : b; }
+
+template <int OWN, int MASK, int GAP, int LN>
+__device__ __forceinline__ void hsym(Sym<LN>& Y, int d, int gap) {
+  int x[LN];
+#pragma unroll
+  for (int c = 0; c < LN; ++c) x[c] = Y.v[OWN][c];
+#pragma unroll
+  for (int m = 0; m <= NLANE; ++m)
+    if (((MASK >> m) & 1) && m != OWN)
+#pragma unroll
+      for (int c = 0; c < LN; ++c) x[c] = imax(x[c], Y.v[m][c]);
+  const int a = GAP ? d + gap : d;
+#pragma unroll
+  for (int c = 0; c < LN; ++c) Y.v[OWN][c] = x[c] + a;
+}
+
+// Slot columns hold 4 coefficients (16 B per thread) whatever LN is.
+__device__ __forceinline__ void sym_slot_ld(unsigned a, int (&y)[4]) {
+  asm volatile("ld.shared.v4.s32 {%0,%1,%2,%3}, [%4];"
+               : "=r"(y[0]), "=r"(y[1]), "=r"(y[2]), "=r"(y[3]) : "r"(a));
+}
+__device__ __forceinline__ void sym_slot_st(unsigned a, const int (&y)[4]) {
+  asm volatile("st.shared.v4.s32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(y[0]), "r"(y[1]),
+               "r"(y[2]), "r"(y[3]) : "memory");
+}
+
+template <int LN>
+__device__ __forceinline__ void sym_get(const Sym<LN>& Y, int lane, int (&y)[4]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) y[c] = kNegSym;
+#pragma unroll
+  for (int l = 0; l < NLANE; ++l)
+    if (l == lane)
+#pragma unroll
+      for (int c = 0; c < LN; ++c) y[c] = Y.v[l][c];
+}
+template <int LN>
+__device__ __forceinline__ void sym_set(Sym<LN>& Y, int lane, const int (&y)[4]) {
+#pragma unroll
+  for (int l = 0; l < NLANE; ++l)
+    if (l == lane)
+#pragma unroll
+      for (int c = 0; c < LN; ++c) Y.v[l][c] = y[c];
+}
+
+// Permutable chain in coefficient form (chain_record in lanes_body.cuh):
+// members in the scenario's order, predecessors from slots, an absent chain
+// publishes "none" and leaves its lane head alone.
+template <int DK, int LN>
+__device__ __forceinline__ void chain_sym(const Params& p, const ChainParams& cp, Sym<LN>& Y,
+                                          int cid, int row, long long s, bool act,
+                                          unsigned slot_s, unsigned slot_pitch, unsigned col,
+                                          long long& tot, int& neg) {
+  const Chain ch = cp.chains[cid];
+  const bool pres = !act || cp.present == nullptr || cp.present[s * cp.n_chains + cid] != 0;
+  int prev[4];
+  sym_get<LN>(Y, ch.lane, prev);
+  for (int q = 0; q < ch.B; ++q) {
+    const int k = (cp.perm != nullptr && act) ? (int)cp.perm[s * cp.perm_ld + ch.perm_off + q] : q;
+    const Member M = cp.members[ch.mem_off + k];
+    if (pres) {
+      int x[4] = {prev[0], prev[1], prev[2], prev[3]};
+      for (int e = 0; e < M.npred; ++e) {
+        int y[4];
+        sym_slot_ld(slot_s + (unsigned)cp.preds[M.pred_off + e] * slot_pitch + col, y);
+#pragma unroll
+        for (int c = 0; c < 4; ++c) x[c] = imax(x[c], y[c]);
+      }
+      long long d = 0;
+      if (act) {
+        const long long at = (long long)(row + k) * p.dense_ld + s;
+        d = DK == 1 ? (long long)cp.dense32[at] : p.dense64[at];
+      }
+      neg |= (int)(d >> 32);
+      tot += d + M.gap;
+      const int a = (int)d + (int)M.gap;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) prev[c] = x[c] + a;
+    }
+    if (M.out >= 0) {
+      int o[4];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) o[c] = pres ? prev[c] : kNegSym;
+      sym_slot_st(slot_s + (unsigned)M.out * slot_pitch + col, o);
+    }
+  }
+  if (pres) sym_set<LN>(Y, ch.lane, prev);
+}
+
+// One thread per scenario, blockIdx.y = segment (0 .. K-2; the last segment's
+// transfer is never needed).  DDSIM_SYM_DISPATCH(h) expands to the handler
+// if-chain over the graph's codes (it sees Y, dv, gp and LN).
+template <int DK, int LN, bool CH>
+__device__ __forceinline__ void sym_body(const Tmap* tmap, const Params& p, const SegParams& sg,
+                                         const ChainParams* cpp) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int BD = blockDim.x;
+  const int tid = threadIdx.x;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem);
+  Rec* pst = reinterpret_cast<Rec*>(smem + 128);
+  unsigned sbase = su32l(smem);
+  asm volatile("" : "+r"(sbase));
+  const unsigned prog_s = sbase + 128;
+  const unsigned tile_s = prog_s + kStagesL * kChunkL * (unsigned)sizeof(Rec);
+  constexpr unsigned ES = DK == 1 ? 4u : 8u;
+  const unsigned tile_all = (unsigned)(kStagesL * kChunkL * BD) * ES;
+  const unsigned slot_s = tile_s + tile_all;  // [ksm][BD] x 16 B
+  const unsigned col = (unsigned)(tid * 16);
+  const unsigned slot_pitch = (unsigned)(BD * 16);
+  unsigned char* tst = smem + (tile_s - sbase);
+  const int seg = blockIdx.y;
+  const int s0 = blockIdx.x * BD;
+  const int s = s0 + tid;
+  const bool act = s < p.S;
+  const int c_begin = sg.cuts[seg] / kChunkL;
+  const int r_end = sg.cuts[seg + 1];
+  const int nchunks = (r_end + kChunkL - 1) / kChunkL;
+  const unsigned tile_bytes = (unsigned)(kChunkL * BD) * ES;
+  auto issue = [&](int c) {
+    const int st = (c - c_begin) % kStagesL;
+    const int nrec = min(kChunkL, r_end - c * kChunkL);
+    const unsigned pb = (unsigned)(nrec * sizeof(Rec));
+    l_expect(&bars[st], pb + tile_bytes);
+    l_bulk(pst + st * kChunkL, p.prog + (long long)c * kChunkL, pb, &bars[st]);
+    l_tile(tst + (size_t)st * kChunkL * BD * ES, tmap, s0, c * kChunkL, &bars[st]);
+  };
+  if (tid == 0) {
+    for (int i = 0; i < kStagesL; ++i) l_mbar_init(&bars[i]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int c = c_begin; c < min(c_begin + kStagesL, nchunks); ++c) issue(c);
+
+  Sym<LN> Y;
+#pragma unroll
+  for (int l = 0; l <= NLANE; ++l)
+#pragma unroll
+    for (int c = 0; c < LN; ++c) Y.v[l][c] = (l == c) ? 0 : kNegSym;
+  long long tot = 0;  // durations + gaps walked (overflow certificate)
+  int neg = 0;
+  const unsigned row_pitch = (unsigned)BD * ES;
+
+  for (int c = c_begin; c < nchunks; ++c) {
+    const int st = (c - c_begin) % kStagesL;
+    l_wait(&bars[st], (unsigned)(((c - c_begin) / kStagesL) & 1));
+    const unsigned rec0 = prog_s + (unsigned)(st * kChunkL * sizeof(Rec));
+    const unsigned t0 = tile_s + (unsigned)(st * kChunkL) * row_pitch + (unsigned)tid * ES;
+    const int nrec = min(kChunkL, r_end - c * kChunkL);
+    auto record = [&](int j) {
+      const int4 r = l_lds128(rec0 + (unsigned)j * 16u);
+      long long d;
+      if (DK == 1) {
+        int x;
+        asm volatile("ld.shared.s32 %0, [%1];" : "=r"(x) : "r"(t0 + (unsigned)j * row_pitch));
+        d = x;
+      } else {
+        asm volatile("ld.shared.s64 %0, [%1];" : "=l"(d) : "r"(t0 + (unsigned)j * row_pitch));
+      }
+      neg |= (int)(d >> 32);
+      const int gp = r.x;  // gap < 2^30 (host: every segment's gap sum is)
+      const unsigned w = (unsigned)r.w;
+      const unsigned h = w >> 24;
+      const unsigned rare = (w >> 16) & 0xffu;
+      if constexpr (CH) {
+        if (rare & (R_CHAIN | R_NOP)) {
+          if (rare & R_CHAIN)
+            chain_sym<DK, LN>(p, *cpp, Y, (int)(short)(r.z & 0xffff), c * kChunkL + j, s, act,
+                              slot_s, slot_pitch, col, tot, neg);
+          return;
+        }
+      }
+      tot += d + gp;
+      const int dv = (int)d;
+      if (rare & R_PRE) {
+        // slot predecessors (all in shared memory on this path) -> temp lane
+        int x[4] = {kNegSym, kNegSym, kNegSym, kNegSym}, y[4];
+        const int row = c * kChunkL + j;
+        if (rare & R_S0) {
+          sym_slot_ld(slot_s + (unsigned)((r.z << 16) >> 16) * slot_pitch + col, y);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) x[q] = imax(x[q], y[q]);
+        }
+        if (rare & R_S1) {
+          sym_slot_ld(slot_s + (unsigned)(r.z >> 16) * slot_pitch + col, y);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) x[q] = imax(x[q], y[q]);
+        }
+        if ((rare & R_SIDE) && p.side_off)
+          for (int k = p.side_off[row]; k < p.side_off[row + 1]; ++k) {
+            sym_slot_ld(slot_s + (unsigned)p.side_slots[k] * slot_pitch + col, y);
+#pragma unroll
+            for (int q = 0; q < 4; ++q) x[q] = imax(x[q], y[q]);
+          }
+#pragma unroll
+        for (int q = 0; q < LN; ++q) Y.v[NLANE][q] = x[q];
+      }
+      DDSIM_SYM_DISPATCH(h)
+      if (rare & R_OUT_SMEM) {
+        int y[4];
+        sym_get<LN>(Y, (int)(h & 3), y);
+        sym_slot_st(slot_s + (unsigned)((w << 16) >> 16) * slot_pitch + col, y);
+      }
+    };
+#pragma unroll 1
+    for (int j = 0; j < nrec; ++j) record(j);
+    __syncthreads();
+    if (tid == 0 && c + kStagesL < nchunks) issue(c + kStagesL);
+  }
+  if (act) {
+    if ((neg < 0 || tot >= (1LL << 30)) && p.neg_flag) atomicOr(p.neg_flag, 2);
+    int* out = sg.trans + (long long)seg * LN * LN * sg.s_pad + s;
+#pragma unroll
+    for (int j = 0; j < LN; ++j)
+#pragma unroll
+      for (int i = 0; i < LN; ++i) out[(long long)(j * LN + i) * sg.s_pad] = Y.v[j][i];
+  }
+}
+
+}  // namespace ddsim_lanes

@@ -147,6 +147,92 @@ cudaError_t launch_lanes_busy(const LaneParams& p, const int* dense32, bool chai
   return cudaGetLastError();
 }
 
+// 2-D tensor map over the [n_rec][dense_ld] duration matrix, boxes of
+// 16 rows x W scenarios (out-of-range scenarios read as zero).
+static cudaError_t encode_lanes_tmap(CUtensorMap* tmap, const LaneParams& p, const int* dense32,
+                                     int dkind, int W) {
+  memset(tmap, 0, sizeof(*tmap));
+  cudaDriverEntryPointQueryResult q;
+  void* fn = nullptr;
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
+          cudaSuccess || q != cudaDriverEntryPointSuccess)
+    return cudaErrorNotSupported;
+  auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  const size_t es = dkind == 1 ? 4 : 8;
+  const void* base = dkind == 1 ? static_cast<const void*>(dense32)
+                                : static_cast<const void*>(p.dense64);
+  cuuint64_t dims[2] = {(cuuint64_t)p.S, (cuuint64_t)p.n_rec};
+  cuuint64_t strides[1] = {(cuuint64_t)(p.dense_ld * es)};
+  cuuint32_t box[2] = {(cuuint32_t)W, (cuuint32_t)ddsim_lanes::kChunkL};
+  cuuint32_t estr[2] = {1, 1};
+  if (enc(tmap, dkind == 1 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_INT64, 2,
+          const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+          CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+          CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return cudaErrorInvalidValue;
+  return cudaSuccess;
+}
+
+// Compose the segment transfer matrices per scenario (one thread each):
+// state[k+1] = trans[k] (x) state[k] in (max,+), state[0] = 0.  All values are
+// >= 0 on this path, so 0 is the identity of max; entries < 0 mean "no path".
+__global__ void __launch_bounds__(128) seg_scan_kernel(const LaneSegParams sg, int S) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  const int LN = sg.LN;
+  const long long sp = sg.s_pad;
+  long long st[4] = {0, 0, 0, 0};
+  for (int k = 0; k + 1 < sg.K; ++k) {
+    const int* tk = sg.trans + (long long)k * LN * LN * sp + s;
+    int a[16];
+#pragma unroll
+    for (int e = 0; e < 16; ++e) a[e] = e < LN * LN ? tk[(long long)e * sp] : -1;
+    long long nx[4] = {0, 0, 0, 0};
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (j < LN && i < LN) {
+          const int c = a[j * LN + i];
+          if (c >= 0) nx[j] = max(nx[j], (long long)c + st[i]);
+        }
+    long long* out = sg.state + (long long)(k + 1) * LN * sp + s;
+#pragma unroll
+    for (int j = 0; j < 4; ++j)
+      if (j < LN) {
+        st[j] = nx[j];
+        out[(long long)j * sp] = nx[j];
+      }
+  }
+}
+
+// Segment-parallel lanes path (small S): transfer, scan, replay.  The caller
+// provides the scratch (trans / state / device cuts in sg) and zeroes makespan
+// and lane busy; cudaErrorNotSupported when the JIT is unavailable.
+cudaError_t launch_maxplus_lanes_seg(const LaneParams& p, const LaneChainParams* cp,
+                                     const int* dense32, int dkind, const std::vector<int>& codes,
+                                     const LaneSegParams& sg, int BD, cudaStream_t stream) {
+  static_assert(sizeof(LaneSegParams) == sizeof(ddsim_lanes::SegParams), "seg params layout");
+  CUtensorMap tmap;
+  cudaError_t e = encode_lanes_tmap(&tmap, p, dense32, dkind, BD);
+  if (e != cudaSuccess) return e;
+  const int gx = (p.S + BD - 1) / BD;
+  const int stages = ddsim_lanes::kStagesL;
+  const size_t es = dkind == 1 ? 4 : 8;
+  const size_t base = 128 + (size_t)stages * ddsim_lanes::kChunkL * sizeof(ddsim_lanes::Rec) +
+                      (size_t)stages * ddsim_lanes::kChunkL * BD * es;
+  if (sg.K > 1) {
+    e = launch_lanes_seg_jit(true, p, cp, &tmap, dkind, sg.LN, codes, &sg, gx, sg.K - 1, BD,
+                             base + (size_t)p.ksm * BD * 16, stream);
+    if (e != cudaSuccess) return e;
+    seg_scan_kernel<<<(p.S + 127) / 128, 128, 0, stream>>>(sg, p.S);
+    note_launch();
+    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  return launch_lanes_seg_jit(false, p, cp, &tmap, dkind, sg.LN, codes, &sg, gx, sg.K, BD,
+                              base + (size_t)p.ksm * BD * 8, stream);
+}
+
 cudaError_t launch_maxplus_lanes(const LaneParams& p, const LaneChainParams* cp, const int* dense32,
                                  int dkind,
                                  const std::vector<int>* codes, cudaStream_t stream) {
@@ -160,26 +246,9 @@ cudaError_t launch_maxplus_lanes(const LaneParams& p, const LaneChainParams* cp,
   if ((long long)grid * W > p.s_pad) return cudaErrorInvalidValue;
   const size_t smem = lanes_smem(dkind, BD, V, p.ksm);
   CUtensorMap tmap;
-  memset(&tmap, 0, sizeof(tmap));
   {
-    cudaDriverEntryPointQueryResult q;
-    void* fn = nullptr;
-    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) !=
-            cudaSuccess || q != cudaDriverEntryPointSuccess)
-      return cudaErrorNotSupported;
-    auto enc = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
-    const size_t es = dkind == 1 ? 4 : 8;
-    const void* base = dkind == 1 ? static_cast<const void*>(dense32)
-                                  : static_cast<const void*>(p.dense64);
-    cuuint64_t dims[2] = {(cuuint64_t)p.S, (cuuint64_t)p.n_rec};
-    cuuint64_t strides[1] = {(cuuint64_t)(p.dense_ld * es)};
-    cuuint32_t box[2] = {(cuuint32_t)W, (cuuint32_t)ddsim_lanes::kChunkL};
-    cuuint32_t estr[2] = {1, 1};
-    if (enc(&tmap, dkind == 1 ? CU_TENSOR_MAP_DATA_TYPE_INT32 : CU_TENSOR_MAP_DATA_TYPE_INT64, 2,
-            const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-            CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
-      return cudaErrorInvalidValue;
+    const cudaError_t te = encode_lanes_tmap(&tmap, p, dense32, dkind, W);
+    if (te != cudaSuccess) return te;
   }
   // per-graph specialised dispatch first (NVRTC); the static kernel otherwise
   if (codes != nullptr) {
