@@ -199,9 +199,9 @@ struct ks_graph {
   std::vector<int> lane_codes;  // handler codes in decreasing frequency
   // segment-parallel evaluation (SegParams, lanes_body.cuh): chunk-aligned rows
   // where no slot value is live and no chain is split, and the prefix sums of
-  // the records' gaps (chain records: their members' gaps)
+  // the records' base weights max(dur, 0) + gap (chain records: their members')
   std::vector<int> lane_cuts;
-  std::vector<long long> lane_gap_prefix;
+  std::vector<long long> lane_wt_prefix;
   bool lane_ready = false;      // some record has a ready floor
   LaneRec* d_lprog = nullptr;
   int* d_lside_off = nullptr;
@@ -1256,21 +1256,22 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
         live += delta[b];
         if (b > 0 && b % 16 == 0 && live == 0 && ekind[b] != 2) cuts.push_back(b);
       }
+      auto wt = [&](int t) { return std::max<long long>(d->duration[t], 0) + d->gap[t]; };
       for (int r = 0; r < RE; ++r) {
-        long long gsum = 0;
+        long long w = 0;
         if (ekind[r] == 0) {
-          gsum = d->gap[eid[r]];
+          w = wt(eid[r]);
         } else if (ekind[r] == 1) {
           const int c = eid[r];
-          for (int k = d->chain_ptr[c]; k < d->chain_ptr[c + 1]; ++k) gsum += d->gap[d->chain_member[k]];
+          for (int k = d->chain_ptr[c]; k < d->chain_ptr[c + 1]; ++k) w += wt(d->chain_member[k]);
         }
-        gpre[r + 1] = gpre[r] + gsum;
+        gpre[r + 1] = gpre[r] + w;
       }
     }
     // chain members with ready floors stay on the general kernel
     if (ns + ngl < 32000 && !(NC > 0 && any_ready)) {
       g->lane_cuts = std::move(cuts);
-      g->lane_gap_prefix = std::move(gpre);
+      g->lane_wt_prefix = std::move(gpre);
       g->lane_ready = any_ready;
       hvec<long long> freq(256, 0);
       for (int r = 0; r < RE; ++r)
@@ -1531,14 +1532,24 @@ std::vector<int> pick_segments(const ks_graph* g, int S, int nsm) {
   if (getenv("DDSIM_NO_SEG") || !g->has_lanes || g->lkglob > 0 || g->lane_ready || g->L < 1 ||
       g->L > 4 || g->lane_cuts.empty() || g->ln_rec < 512)
     return rows;
-  long long max_s = 16384;
+  // the single-pass kernel reaches the memory roofline once ~256 threads per
+  // SM walk the records (measured: config 4 at 65,536 scenarios, V = 2)
+  long long max_s = 256LL * nsm;
   if (const char* e = getenv("DDSIM_SEG_MAX_S")) max_s = atoll(e);
   if (S > max_s) return rows;
-  long long tps = 512;  // target resident threads per SM
+  // segments: enough for ~4,096 resident scenario-segments per SM (measured
+  // best on configs 2 and 4), each >= 320 records, and short enough that the
+  // base weights of a segment stay below 2^28 ns (int32 coefficients: the
+  // device certificate is 2^30 per scenario; outside it the exact kernel reruns)
+  long long tps = 4096;
   if (const char* e = getenv("DDSIM_SEG_TPS")) tps = std::max(32LL, atoll(e));
+  long long min_len = 320;
+  if (const char* e = getenv("DDSIM_SEG_MIN_LEN")) min_len = std::max(16LL, atoll(e));
   long long K = (tps * nsm + S - 1) / S;
+  K = std::min<long long>(K, g->ln_rec / min_len);
+  const long long total = g->lane_wt_prefix[g->ln_rec];
+  K = std::max<long long>(K, (total >> 28) + 1);
   if (const char* e = getenv("DDSIM_SEG_K")) K = atoll(e);
-  K = std::min<long long>(K, g->ln_rec / 256);  // segments of >= 256 records
   K = std::min<long long>(K, (long long)g->lane_cuts.size() + 1);
   if (K < 2) return rows;
   rows.push_back(0);
@@ -1551,9 +1562,9 @@ std::vector<int> pick_segments(const ks_graph* g, int S, int nsm) {
     if (best > rows.back()) rows.push_back(best);
   }
   rows.push_back(g->ln_rec);
-  // coefficient entries are int32: every segment's gaps must leave room
+  // coefficient entries are int32: a segment's base weights must leave room
   for (size_t k = 0; k + 1 < rows.size(); ++k)
-    if (g->lane_gap_prefix[rows[k + 1]] - g->lane_gap_prefix[rows[k]] >= (1LL << 29)) return {};
+    if (g->lane_wt_prefix[rows[k + 1]] - g->lane_wt_prefix[rows[k]] >= (1LL << 29)) return {};
   if (rows.size() < 3) return {};
   return rows;
 }

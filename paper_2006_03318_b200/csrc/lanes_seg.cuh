@@ -177,15 +177,26 @@ __device__ __forceinline__ void sym_body(const Tmap* tmap, const Params& p, cons
     const unsigned rec0 = prog_s + (unsigned)(st * kChunkL * sizeof(Rec));
     const unsigned t0 = tile_s + (unsigned)(st * kChunkL) * row_pitch + (unsigned)tid * ES;
     const int nrec = min(kChunkL, r_end - c * kChunkL);
-    auto record = [&](int j) {
-      const int4 r = l_lds128(rec0 + (unsigned)j * 16u);
-      long long d;
+    // prefetched record and duration of the next record (the decode and the
+    // shared-memory loads overlap this record's coefficient updates)
+    int4 raw = l_lds128(rec0);
+    long long dn = 0;
+    auto load_d = [&](unsigned ta) {
       if (DK == 1) {
         int x;
-        asm volatile("ld.shared.s32 %0, [%1];" : "=r"(x) : "r"(t0 + (unsigned)j * row_pitch));
-        d = x;
+        asm volatile("ld.shared.s32 %0, [%1];" : "=r"(x) : "r"(ta));
+        dn = x;
       } else {
-        asm volatile("ld.shared.s64 %0, [%1];" : "=l"(d) : "r"(t0 + (unsigned)j * row_pitch));
+        asm volatile("ld.shared.s64 %0, [%1];" : "=l"(dn) : "r"(ta));
+      }
+    };
+    load_d(t0);
+    auto record = [&](int j) {
+      const int4 r = raw;
+      const long long d = dn;
+      if (j + 1 < nrec) {
+        raw = l_lds128(rec0 + (unsigned)(j + 1) * 16u);
+        load_d(t0 + (unsigned)(j + 1) * row_pitch);
       }
       neg |= (int)(d >> 32);
       const int gp = r.x;  // gap < 2^30 (host: every segment's gap sum is)
@@ -232,8 +243,18 @@ __device__ __forceinline__ void sym_body(const Tmap* tmap, const Params& p, cons
         sym_slot_st(slot_s + (unsigned)((w << 16) >> 16) * slot_pitch + col, y);
       }
     };
+#ifdef DDSIM_UNROLL
+    if (nrec == kChunkL) {
+#pragma unroll DDSIM_UNROLL
+      for (int j = 0; j < kChunkL; ++j) record(j);
+    } else {
+#pragma unroll 1
+      for (int j = 0; j < nrec; ++j) record(j);
+    }
+#else
 #pragma unroll 1
     for (int j = 0; j < nrec; ++j) record(j);
+#endif
     __syncthreads();
     if (tid == 0 && c + kStagesL < nchunks) issue(c + kStagesL);
   }

@@ -176,32 +176,44 @@ static cudaError_t encode_lanes_tmap(CUtensorMap* tmap, const LaneParams& p, con
 // Compose the segment transfer matrices per scenario (one thread each):
 // state[k+1] = trans[k] (x) state[k] in (max,+), state[0] = 0.  All values are
 // >= 0 on this path, so 0 is the identity of max; entries < 0 mean "no path".
+template <int LN>
 __global__ void __launch_bounds__(128) seg_scan_kernel(const LaneSegParams sg, int S) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= S) return;
-  const int LN = sg.LN;
+  constexpr int E = LN * LN;
+  constexpr int D = LN <= 2 ? 16 : (LN == 3 ? 8 : 4);  // segments loaded together
   const long long sp = sg.s_pad;
-  long long st[4] = {0, 0, 0, 0};
-  for (int k = 0; k + 1 < sg.K; ++k) {
-    const int* tk = sg.trans + (long long)k * LN * LN * sp + s;
-    int a[16];
+  long long st[LN];
 #pragma unroll
-    for (int e = 0; e < 16; ++e) a[e] = e < LN * LN ? tk[(long long)e * sp] : -1;
-    long long nx[4] = {0, 0, 0, 0};
+  for (int j = 0; j < LN; ++j) st[j] = 0;
+  // the loads do not depend on the state (only the composition chain does):
+  // D segments' coefficients are in flight together
+  for (int k0 = 0; k0 + 1 < sg.K; k0 += D) {
+    int a[D][E];
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
+    for (int q = 0; q < D; ++q)
+      if (k0 + q + 1 < sg.K) {
+        const int* tk = sg.trans + (long long)(k0 + q) * E * sp + s;
 #pragma unroll
-      for (int i = 0; i < 4; ++i)
-        if (j < LN && i < LN) {
-          const int c = a[j * LN + i];
-          if (c >= 0) nx[j] = max(nx[j], (long long)c + st[i]);
+        for (int e = 0; e < E; ++e) a[q][e] = tk[(long long)e * sp];
+      }
+#pragma unroll
+    for (int q = 0; q < D; ++q)
+      if (k0 + q + 1 < sg.K) {
+        long long nx[LN];
+#pragma unroll
+        for (int j = 0; j < LN; ++j) {
+          nx[j] = 0;
+#pragma unroll
+          for (int i = 0; i < LN; ++i)
+            if (a[q][j * LN + i] >= 0) nx[j] = max(nx[j], (long long)a[q][j * LN + i] + st[i]);
         }
-    long long* out = sg.state + (long long)(k + 1) * LN * sp + s;
+        long long* out = sg.state + (long long)(k0 + q + 1) * LN * sp + s;
 #pragma unroll
-    for (int j = 0; j < 4; ++j)
-      if (j < LN) {
-        st[j] = nx[j];
-        out[(long long)j * sp] = nx[j];
+        for (int j = 0; j < LN; ++j) {
+          st[j] = nx[j];
+          out[(long long)j * sp] = nx[j];
+        }
       }
   }
 }
@@ -225,7 +237,13 @@ cudaError_t launch_maxplus_lanes_seg(const LaneParams& p, const LaneChainParams*
     e = launch_lanes_seg_jit(true, p, cp, &tmap, dkind, sg.LN, codes, &sg, gx, sg.K - 1, BD,
                              base + (size_t)p.ksm * BD * 16, stream);
     if (e != cudaSuccess) return e;
-    seg_scan_kernel<<<(p.S + 127) / 128, 128, 0, stream>>>(sg, p.S);
+    const int gs = (p.S + 127) / 128;
+    switch (sg.LN) {
+      case 1: seg_scan_kernel<1><<<gs, 128, 0, stream>>>(sg, p.S); break;
+      case 2: seg_scan_kernel<2><<<gs, 128, 0, stream>>>(sg, p.S); break;
+      case 3: seg_scan_kernel<3><<<gs, 128, 0, stream>>>(sg, p.S); break;
+      default: seg_scan_kernel<4><<<gs, 128, 0, stream>>>(sg, p.S); break;
+    }
     note_launch();
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
