@@ -246,11 +246,15 @@ struct LaneSegParams {
   int* trans;
   long long* state;
   long long s_pad;
+  int* ticket;
+  int* flags;
+  int nb;
+  int pad;
 };
 cudaError_t launch_maxplus_lanes_seg(const LaneParams& p, const LaneChainParams* cp,
                                      const int* dense32, int dkind, const std::vector<int>& codes,
                                      const LaneSegParams& sg, int BD, cudaStream_t stream);
-cudaError_t launch_lanes_seg_jit(bool transfer, const LaneParams& p, const LaneChainParams* cp,
+cudaError_t launch_lanes_seg_jit(int mode, const LaneParams& p, const LaneChainParams* cp,
                                  const void* tmap128, int dkind, int LN,
                                  const std::vector<int>& codes, const void* segp, int gx, int gy,
                                  int BD, size_t smem, cudaStream_t stream);

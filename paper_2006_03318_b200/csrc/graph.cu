@@ -1719,8 +1719,18 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
       sg.LN = g->L;
       sg.s_pad = (long long)((S + BDs - 1) / BDs) * BDs;
       sg.cuts = T.up(seg.data(), seg.size());
-      sg.trans = T.scratch<int>((size_t)(sg.K - 1) * sg.LN * sg.LN * sg.s_pad);
+      sg.nb = (int)(sg.s_pad / BDs);
       sg.state = T.scratch<long long>((size_t)sg.K * sg.LN * sg.s_pad);
+      // fused single pass (look-back) only on request: its publish chain costs
+      // ~2.5 us per segment hop (config 2, K = 92: 0.35 vs 0.17 ms for the
+      // transfer / scan / replay kernels; config 4 at 8,192: 2.68 vs 2.58 ms)
+      if (getenv("DDSIM_SEG_FUSED") != nullptr) {
+        sg.ticket = T.scratch<int>(1 + (size_t)sg.K * sg.nb);
+        sg.flags = sg.ticket + 1;
+        CUDA_TRY(cudaMemsetAsync(sg.ticket, 0, sizeof(int) * (1 + (size_t)sg.K * sg.nb), stream));
+      } else {
+        sg.trans = T.scratch<int>((size_t)(sg.K - 1) * sg.LN * sg.LN * sg.s_pad);
+      }
       LaneParams ps = p;
       ps.s_pad = sg.s_pad;
       if (ps.makespan) CUDA_TRY(cudaMemsetAsync(ps.makespan, 0, sizeof(long long) * S, stream));

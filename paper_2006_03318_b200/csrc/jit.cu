@@ -201,37 +201,31 @@ CUfunction get_function(const std::vector<int>& codes, int dk, int V, bool dyn, 
 // Segment kernels (SegParams in lanes_body.cuh): the transfer pass in
 // coefficient form (lanes_seg.cuh) and the replay pass (lanes_body<..., SEG>),
 // both with the graph's handler codes as an if-chain.
-std::string seg_source(const std::vector<int>& codes, int dk, int LN, bool ch, bool transfer) {
+// mode: 0 replay, 1 transfer, 2 fused (transfer + look-back + replay)
+std::string seg_source(const std::vector<int>& codes, int dk, int LN, bool ch, int mode) {
   std::string src = "#define DDSIM_LANES_NO_STD_TYPES 1\n#define DDSIM_UNROLL 2\n";
-  std::string disp = transfer ? "#define DDSIM_DISPATCH(h) hstep_dyn<V>(S, h, d0, d1, gap, sp, ld, store);\n"
-                              : "#define DDSIM_DISPATCH(h) ";
+  std::string disp = "#define DDSIM_DISPATCH(h) ";
   std::string sdisp = "#define DDSIM_SYM_DISPATCH(h) ";
   for (size_t i = 0; i < codes.size(); ++i) {
     const int c = codes[i];
     const std::string tp = std::to_string(c & 3) + ", " + std::to_string((c >> 2) & 31) + ", " +
                            std::to_string((c >> 7) & 1);
     const std::string cond = (i ? "else if (h == " : "if (h == ") + std::to_string(c) + "u) ";
-    if (!transfer) disp += cond + "hstep<" + tp + ", V>(S, d0, d1, gap, sp, ld, store); ";
+    disp += cond + "hstep<" + tp + ", V>(S, d0, d1, gap, sp, ld, store); ";
     sdisp += cond + "hsym<" + tp + ", LN>(Y, dv, gp); ";
   }
-  if (!transfer) disp += "else __trap();\n";
+  disp += "else __trap();\n";
   sdisp += "else __trap();\n";
   src += disp + sdisp + kLanesBodySrc + "\n" + kSegBodySrc + "\n";
-  const std::string chp = ch ? ", const __grid_constant__ ddsim_lanes::ChainParams cp" : "";
-  const std::string chr = ch ? "&cp" : "nullptr";
-  if (transfer) {
-    src += "extern \"C\" __global__ void __launch_bounds__(256) ddsim_seg_transfer("
-           "const __grid_constant__ ddsim_lanes::Tmap tmap, const ddsim_lanes::Params p, "
-           "const ddsim_lanes::SegParams sg" + chp + ") {\n  ddsim_lanes::sym_body<" +
-           std::to_string(dk) + ", " + std::to_string(LN) + ", " + (ch ? "true" : "false") +
-           ">(&tmap, p, sg, " + chr + ");\n}\n";
-  } else {
-    src += "extern \"C\" __global__ void __launch_bounds__(256) ddsim_seg_replay("
-           "const __grid_constant__ ddsim_lanes::Tmap tmap, const ddsim_lanes::Params p, "
-           "const ddsim_lanes::SegParams sg" + chp + ") {\n  ddsim_lanes::lanes_body<" +
-           std::to_string(dk) + ", 1, " + (ch ? "true" : "false") + ", true>(&tmap, p, " + chr +
-           ", &sg);\n}\n";
-  }
+  const char* names[] = {"ddsim_seg_replay", "ddsim_seg_transfer", "ddsim_seg_fused"};
+  const char* bodies[] = {"replay_body", "sym_body", "fused_body"};
+  src += std::string("extern \"C\" __global__ void __launch_bounds__(256) ") + names[mode] +
+         "(const __grid_constant__ ddsim_lanes::Tmap tmap, const ddsim_lanes::Params p, "
+         "const ddsim_lanes::SegParams sg" +
+         (ch ? ", const __grid_constant__ ddsim_lanes::ChainParams cp" : "") +
+         ") {\n  ddsim_lanes::" + bodies[mode] + "<" + std::to_string(dk) + ", " +
+         std::to_string(LN) + ", " + (ch ? "true" : "false") + ">(&tmap, p, sg, " +
+         (ch ? "&cp" : "nullptr") + ");\n}\n";
   return src;
 }
 
@@ -291,18 +285,20 @@ cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const LaneChainParams*
 }
 
 // One segment kernel launch (grid gx x K'): transfer or replay.
-cudaError_t launch_lanes_seg_jit(bool transfer, const LaneParams& p, const LaneChainParams* cp,
+cudaError_t launch_lanes_seg_jit(int mode, const LaneParams& p, const LaneChainParams* cp,
                                  const void* tmap128, int dkind, int LN,
                                  const std::vector<int>& codes, const void* segp, int gx, int gy,
                                  int BD, size_t smem, cudaStream_t stream) {
-  if (codes.empty() || codes.size() > 32 || LN < 1 || LN > 4) return cudaErrorNotSupported;
+  if (codes.empty() || codes.size() > 32 || LN < 1 || LN > 4 || mode < 0 || mode > 2)
+    return cudaErrorNotSupported;
   int dev = 0;
   cudaGetDevice(&dev);
-  std::string key = std::string(transfer ? "seg_t:" : "seg_r:") + std::to_string(dev) + ":" +
-                    std::to_string(dkind) + ":" + std::to_string(LN) + (cp ? ":ch:" : ":");
+  const char* tags[] = {"seg_r:", "seg_t:", "seg_f:"};
+  const char* names[] = {"ddsim_seg_replay", "ddsim_seg_transfer", "ddsim_seg_fused"};
+  std::string key = std::string(tags[mode]) + std::to_string(dev) + ":" + std::to_string(dkind) +
+                    ":" + std::to_string(LN) + (cp ? ":ch:" : ":");
   for (int c : codes) key += std::to_string(c) + ",";
-  CUfunction fn = get_compiled(key, seg_source(codes, dkind, LN, cp != nullptr, transfer),
-                               transfer ? "ddsim_seg_transfer" : "ddsim_seg_replay");
+  CUfunction fn = get_compiled(key, seg_source(codes, dkind, LN, cp != nullptr, mode), names[mode]);
   if (!fn) return cudaErrorNotSupported;
   if (g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem) != CUDA_SUCCESS)
     return cudaErrorNotSupported;

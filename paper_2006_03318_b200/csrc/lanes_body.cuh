@@ -81,6 +81,10 @@ struct SegParams {
                              // from input lane head i to output lane head j, < 0 = none
   long long* state;          // [K][LN][s_pad]: lane heads at segment starts (seg_scan)
   long long s_pad;
+  int* ticket;               // fused kernel: CTA work order (zeroed per launch)
+  int* flags;                // fused kernel: [K][nb] "state of (segment, block) published"
+  int nb;                    // scenario blocks
+  int pad;
 };
 
 // CUtensorMap-compatible opaque kernel parameter (128 B, 64 B aligned)
@@ -344,18 +348,21 @@ __device__ __forceinline__ void chain_record(const Params& p, const ChainParams&
 // Each thread owns V consecutive scenarios (V = 1 or 2).
 // CH: the graph has permutable chains (chain / no-op records).  Without them
 // the chain code is compiled out, so the hot loop keeps its registers.
-// SEG: replay of segment blockIdx.y (rows cuts[y] .. cuts[y+1]) from the lane
-// heads seg_scan computed; makespan / lane busy accumulate with atomics into
-// outputs zeroed by the launcher.
+// SEG: replay of segment seg_k (rows cuts[k] .. cuts[k+1]) of scenario block
+// blk from the input lane heads `init`; makespan / lane busy accumulate with
+// atomics into outputs zeroed by the launcher.  Its mbarriers sit at smem + 64
+// so a kernel may run it after another pipelined pass (lanes_seg.cuh).
 template <int DK, int V, bool CH = false, bool SEG = false>
 __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
                                            const ChainParams* cpp = nullptr,
-                                           const SegParams* sgp = nullptr) {
+                                           const SegParams* sgp = nullptr, int seg_k = 0,
+                                           int blk = 0, const long long* init = nullptr) {
+  static_assert(!SEG || V == 1, "segment replay runs one scenario per thread");
   extern __shared__ __align__(128) unsigned char smem[];
   const int BD = blockDim.x;
   const int W = BD * V;  // scenarios per CTA
   const int tid = threadIdx.x;
-  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem);
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem + (SEG ? 64 : 0));
   Rec* pst = reinterpret_cast<Rec*>(smem + 128);
   unsigned sbase = su32l(smem);
   asm volatile("" : "+r"(sbase));  // keep in a register (no per-record rematerialisation)
@@ -367,13 +374,13 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
   const unsigned col = (unsigned)(tid * 8 * V);
   const unsigned slot_pitch = (unsigned)(BD * 8 * V);
   int* tst = reinterpret_cast<int*>(smem + (tile_s - sbase));
-  const int s0 = blockIdx.x * W;
+  const int s0 = (SEG ? blk : (int)blockIdx.x) * W;
   const int s = s0 + tid * V;
   const bool act = s < p.S;  // S % V == 0 (host)
   int r_end = p.n_rec, c_begin = 0;
   if constexpr (SEG) {
-    c_begin = sgp->cuts[blockIdx.y] / kChunkL;
-    r_end = sgp->cuts[blockIdx.y + 1];
+    c_begin = sgp->cuts[seg_k] / kChunkL;
+    r_end = sgp->cuts[seg_k + 1];
   }
   const int nchunks = (r_end + kChunkL - 1) / kChunkL;
   const unsigned tile_bytes = (unsigned)(kChunkL * W) * ES;
@@ -401,14 +408,8 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
 #pragma unroll
     for (int i = 0; i < V; ++i) S.lv[l][i] = 0;
   if constexpr (SEG) {
-    if (blockIdx.y > 0 && act) {
-      const long long* st0 = sgp->state + (long long)blockIdx.y * sgp->LN * sgp->s_pad + s;
 #pragma unroll
-      for (int l = 0; l < NLANE; ++l)
-        if (l < sgp->LN)
-#pragma unroll
-          for (int i = 0; i < V; ++i) S.lv[l][i] = st0[(long long)l * sgp->s_pad + i];
-    }
+    for (int l = 0; l < NLANE; ++l) S.lv[l][0] = init[l];
   }
 #pragma unroll
   for (int l = 0; l < NLANE; ++l)

@@ -116,12 +116,15 @@ __device__ __forceinline__ void chain_sym(const Params& p, const ChainParams& cp
   if (pres) sym_set<LN>(Y, ch.lane, prev);
 }
 
-// One thread per scenario, blockIdx.y = segment (0 .. K-2; the last segment's
-// transfer is never needed).  DDSIM_SYM_DISPATCH(h) expands to the handler
-// if-chain over the graph's codes (it sees Y, dv, gp and LN).
+// Transfer of segment `seg` for scenario block `blk` (one thread per
+// scenario; the last segment's transfer is never needed): coef[j][i] = longest
+// path weight from input lane head i to output lane head j (< 0 = none).
+// DDSIM_SYM_DISPATCH(h) expands to the handler if-chain over the graph's codes
+// (it sees Y, dv, gp and LN).
 template <int DK, int LN, bool CH>
-__device__ __forceinline__ void sym_body(const Tmap* tmap, const Params& p, const SegParams& sg,
-                                         const ChainParams* cpp) {
+__device__ __forceinline__ void sym_pass(const Tmap* tmap, const Params& p, const SegParams& sg,
+                                         const ChainParams* cpp, int seg, int blk,
+                                         int (&coef)[LN][LN]) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int BD = blockDim.x;
   const int tid = threadIdx.x;
@@ -137,8 +140,7 @@ __device__ __forceinline__ void sym_body(const Tmap* tmap, const Params& p, cons
   const unsigned col = (unsigned)(tid * 16);
   const unsigned slot_pitch = (unsigned)(BD * 16);
   unsigned char* tst = smem + (tile_s - sbase);
-  const int seg = blockIdx.y;
-  const int s0 = blockIdx.x * BD;
+  const int s0 = blk * BD;
   const int s = s0 + tid;
   const bool act = s < p.S;
   const int c_begin = sg.cuts[seg] / kChunkL;
@@ -258,14 +260,101 @@ __device__ __forceinline__ void sym_body(const Tmap* tmap, const Params& p, cons
     __syncthreads();
     if (tid == 0 && c + kStagesL < nchunks) issue(c + kStagesL);
   }
-  if (act) {
-    if ((neg < 0 || tot >= (1LL << 30)) && p.neg_flag) atomicOr(p.neg_flag, 2);
-    int* out = sg.trans + (long long)seg * LN * LN * sg.s_pad + s;
+  if (act && (neg < 0 || tot >= (1LL << 30)) && p.neg_flag) atomicOr(p.neg_flag, 2);
+#pragma unroll
+  for (int j = 0; j < LN; ++j)
+#pragma unroll
+    for (int i = 0; i < LN; ++i) coef[j][i] = Y.v[j][i];
+}
+
+// Three-kernel path, pass 1: blockIdx.y = segment, coefficients to sg.trans.
+template <int DK, int LN, bool CH>
+__device__ __forceinline__ void sym_body(const Tmap* tmap, const Params& p, const SegParams& sg,
+                                         const ChainParams* cpp) {
+  int coef[LN][LN];
+  sym_pass<DK, LN, CH>(tmap, p, sg, cpp, (int)blockIdx.y, (int)blockIdx.x, coef);
+  const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (s < p.S) {
+    int* out = sg.trans + (long long)blockIdx.y * LN * LN * sg.s_pad + s;
 #pragma unroll
     for (int j = 0; j < LN; ++j)
 #pragma unroll
-      for (int i = 0; i < LN; ++i) out[(long long)(j * LN + i) * sg.s_pad] = Y.v[j][i];
+      for (int i = 0; i < LN; ++i) out[(long long)(j * LN + i) * sg.s_pad] = coef[j][i];
   }
+}
+
+// Three-kernel path, pass 3: replay of segment blockIdx.y from seg_scan's state.
+template <int DK, int LN, bool CH>
+__device__ __forceinline__ void replay_body(const Tmap* tmap, const Params& p,
+                                            const SegParams& sg, const ChainParams* cpp) {
+  long long init[NLANE] = {0, 0, 0, 0};
+  const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (blockIdx.y > 0 && s < p.S)
+#pragma unroll
+    for (int l = 0; l < LN; ++l)
+      init[l] = sg.state[((long long)blockIdx.y * LN + l) * sg.s_pad + s];
+  lanes_body<DK, 1, CH, true>(tmap, p, cpp, &sg, (int)blockIdx.y, (int)blockIdx.x, init);
+}
+
+// Fused single pass with decoupled look-back: CTAs take (segment, block) work
+// items in ticket order (segment-major), compute their segment's transfer,
+// wait until the previous segment of the same block published this segment's
+// input lane heads, publish the next segment's, then replay.  A CTA only waits
+// on an item with a smaller ticket (already running), so the chain always
+// progresses; later items' transfers overlap earlier items' replays.
+template <int DK, int LN, bool CH>
+__device__ __forceinline__ void fused_body(const Tmap* tmap, const Params& p, const SegParams& sg,
+                                           const ChainParams* cpp) {
+  __shared__ int tk;
+  if (threadIdx.x == 0) tk = atomicAdd(sg.ticket, 1);
+  __syncthreads();
+  const int k = tk / sg.nb, b = tk % sg.nb;
+  const long long s = (long long)b * blockDim.x + threadIdx.x;
+  const bool act = s < p.S;
+  const bool last = k + 1 >= sg.K;
+  int coef[LN][LN];
+  if (!last) sym_pass<DK, LN, CH>(tmap, p, sg, cpp, k, b, coef);
+  long long st[NLANE] = {0, 0, 0, 0};
+  if (k > 0) {
+    if (threadIdx.x == 0) {
+      const int* f = sg.flags + (long long)k * sg.nb + b;
+      int v = 0;
+      while (true) {
+        asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(f) : "memory");
+        if (v) break;
+        __nanosleep(64);
+      }
+    }
+    __syncthreads();
+    if (act)
+#pragma unroll
+      for (int l = 0; l < LN; ++l)
+        st[l] = __ldcg(sg.state + ((long long)k * LN + l) * sg.s_pad + s);
+  }
+  if (!last) {
+    if (act) {
+      long long* out = sg.state + (long long)(k + 1) * LN * sg.s_pad + s;
+#pragma unroll
+      for (int j = 0; j < LN; ++j) {
+        long long m = 0;  // values >= 0: 0 is the identity of max
+#pragma unroll
+        for (int i = 0; i < LN; ++i)
+          if (coef[j][i] >= 0) m = max(m, (long long)coef[j][i] + st[i]);
+        __stcg(out + (long long)j * sg.s_pad, m);
+      }
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      int* f = sg.flags + (long long)(k + 1) * sg.nb + b;
+      asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(f), "r"(1) : "memory");
+    }
+  }
+  // the transfer pass's generic shared-memory accesses precede the replay's
+  // TMA writes into the same bytes
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+  lanes_body<DK, 1, CH, true>(tmap, p, cpp, &sg, k, b, st);
 }
 
 }  // namespace ddsim_lanes

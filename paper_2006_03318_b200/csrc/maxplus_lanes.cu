@@ -233,9 +233,13 @@ cudaError_t launch_maxplus_lanes_seg(const LaneParams& p, const LaneChainParams*
   const size_t es = dkind == 1 ? 4 : 8;
   const size_t base = 128 + (size_t)stages * ddsim_lanes::kChunkL * sizeof(ddsim_lanes::Rec) +
                       (size_t)stages * ddsim_lanes::kChunkL * BD * es;
+  const size_t smem_t = base + (size_t)p.ksm * BD * 16, smem_r = base + (size_t)p.ksm * BD * 8;
+  if (sg.ticket != nullptr)  // fused single pass (transfer smem >= replay smem)
+    return launch_lanes_seg_jit(2, p, cp, &tmap, dkind, sg.LN, codes, &sg, gx * sg.K, 1, BD,
+                                smem_t, stream);
   if (sg.K > 1) {
-    e = launch_lanes_seg_jit(true, p, cp, &tmap, dkind, sg.LN, codes, &sg, gx, sg.K - 1, BD,
-                             base + (size_t)p.ksm * BD * 16, stream);
+    e = launch_lanes_seg_jit(1, p, cp, &tmap, dkind, sg.LN, codes, &sg, gx, sg.K - 1, BD, smem_t,
+                             stream);
     if (e != cudaSuccess) return e;
     const int gs = (p.S + 127) / 128;
     switch (sg.LN) {
@@ -247,8 +251,8 @@ cudaError_t launch_maxplus_lanes_seg(const LaneParams& p, const LaneChainParams*
     note_launch();
     if ((e = cudaGetLastError()) != cudaSuccess) return e;
   }
-  return launch_lanes_seg_jit(false, p, cp, &tmap, dkind, sg.LN, codes, &sg, gx, sg.K, BD,
-                              base + (size_t)p.ksm * BD * 8, stream);
+  return launch_lanes_seg_jit(0, p, cp, &tmap, dkind, sg.LN, codes, &sg, gx, sg.K, BD, smem_r,
+                              stream);
 }
 
 cudaError_t launch_maxplus_lanes(const LaneParams& p, const LaneChainParams* cp, const int* dense32,

@@ -79,13 +79,19 @@ def _plain(fz, table, monkeypatch):
         monkeypatch.delenv("DDSIM_NO_SEG")
 
 
-def _seg_engaged(key_prefix="seg_t:"):
-    return key_prefix in (N.lib().ks_jit_log() or b"").decode()
+def _seg_engaged():
+    log = (N.lib().ks_jit_log() or b"").decode()
+    return "seg_t:" in log or "seg_f:" in log
 
 
+@pytest.mark.parametrize("passes", ["fused", "3pass"])
 @pytest.mark.parametrize("K", ["", "2", "7"])
 @pytest.mark.parametrize("S", [1, 96, 333])
-def test_seg_slot_graph_vs_oracle_and_single_pass(S, K, monkeypatch):
+def test_seg_slot_graph_vs_oracle_and_single_pass(S, K, passes, monkeypatch):
+    """Both segment drivers: the transfer / scan / replay kernels (default)
+    and the fused look-back kernel (DDSIM_SEG_FUSED)."""
+    if passes == "fused":
+        monkeypatch.setenv("DDSIM_SEG_FUSED", "1")
     g = slot_graph()
     fz = FrozenGraph.from_graph(g)
     info = fz.info
