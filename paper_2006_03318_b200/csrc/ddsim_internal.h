@@ -250,6 +250,7 @@ struct LaneSegParams {
   int* flags;
   int nb;
   int pad;
+  const long long* gapsum;
 };
 cudaError_t launch_maxplus_lanes_seg(const LaneParams& p, const LaneChainParams* cp,
                                      const int* dense32, int dkind, const std::vector<int>& codes,

@@ -202,6 +202,7 @@ struct ks_graph {
   // the records' base weights max(dur, 0) + gap (chain records: their members')
   std::vector<int> lane_cuts;
   std::vector<long long> lane_wt_prefix;
+  std::vector<long long> lane_gap_prefix;  // prefix sums of the records' gaps
   bool lane_ready = false;      // some record has a ready floor
   LaneRec* d_lprog = nullptr;
   int* d_lside_off = nullptr;
@@ -1241,7 +1242,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     // slot value live across them (produced before b, read at or after b)
     // and not inside a chain's no-op rows
     std::vector<int> cuts;
-    std::vector<long long> gpre(RE + 1, 0);
+    std::vector<long long> gpre(RE + 1, 0), gapre(RE + 1, 0);
     {
       hvec<int> delta(RE + 2, 0);
       for (int r = 0; r < RE; ++r)
@@ -1266,12 +1267,21 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
           for (int k = d->chain_ptr[c]; k < d->chain_ptr[c + 1]; ++k) w += wt(d->chain_member[k]);
         }
         gpre[r + 1] = gpre[r] + w;
+        long long gg = 0;
+        if (ekind[r] == 0) {
+          gg = d->gap[eid[r]];
+        } else if (ekind[r] == 1) {
+          const int c = eid[r];
+          for (int k = d->chain_ptr[c]; k < d->chain_ptr[c + 1]; ++k) gg += d->gap[d->chain_member[k]];
+        }
+        gapre[r + 1] = gapre[r] + gg;
       }
     }
     // chain members with ready floors stay on the general kernel
     if (ns + ngl < 32000 && !(NC > 0 && any_ready)) {
       g->lane_cuts = std::move(cuts);
       g->lane_wt_prefix = std::move(gpre);
+      g->lane_gap_prefix = std::move(gapre);
       g->lane_ready = any_ready;
       hvec<long long> freq(256, 0);
       for (int r = 0; r < RE; ++r)
@@ -1719,6 +1729,12 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
       sg.LN = g->L;
       sg.s_pad = (long long)((S + BDs - 1) / BDs) * BDs;
       sg.cuts = T.up(seg.data(), seg.size());
+      {
+        std::vector<long long> gs(sg.K);
+        for (int k = 0; k < sg.K; ++k)
+          gs[k] = g->lane_gap_prefix[seg[k + 1]] - g->lane_gap_prefix[seg[k]];
+        sg.gapsum = T.up(gs.data(), gs.size());
+      }
       sg.nb = (int)(sg.s_pad / BDs);
       sg.state = T.scratch<long long>((size_t)sg.K * sg.LN * sg.s_pad);
       // fused single pass (look-back) only on request: its publish chain costs

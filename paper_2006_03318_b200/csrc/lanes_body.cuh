@@ -85,6 +85,7 @@ struct SegParams {
   int* flags;                // fused kernel: [K][nb] "state of (segment, block) published"
   int nb;                    // scenario blocks
   int pad;
+  const long long* gapsum;   // [K] gaps of each segment's records (host)
 };
 
 // CUtensorMap-compatible opaque kernel parameter (128 B, 64 B aligned)
@@ -548,7 +549,14 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
   }
   if constexpr (SEG) {
     if (act) {
-      if (neg < 0 && p.neg_flag) atomicOr(p.neg_flag, 1);
+      // the transfer's int32 coefficients are exact when the segment's
+      // durations + gaps stay below 2^30 (lanes_seg.cuh); the replay holds the
+      // duration sums anyway (lane busy), so it certifies the transfer, and a
+      // negative duration voids the fast path for both passes
+      long long wsum = sgp->gapsum[seg_k];
+#pragma unroll
+      for (int q = 0; q < NLANE; ++q) wsum += S.lb[q][0];
+      if ((neg < 0 || wsum >= (1LL << 30)) && p.neg_flag) atomicOr(p.neg_flag, 1);
 #pragma unroll
       for (int i = 0; i < V; ++i) {
         const long long m = i == 0 ? ms0 : ms1;  // >= 0 on this path

@@ -13,8 +13,10 @@
 //
 // Coefficients are int32 with "none" = a negative number: entries are path
 // weights within the segment, so they stay below 2^30 when the segment's
-// durations + gaps sum below 2^30 (checked per scenario; otherwise the exact
-// general kernel reruns the launch), and kNegSym + that sum stays negative.
+// durations + gaps sum below 2^30, and kNegSym + that sum stays negative.  The
+// replay of the same segment checks that sum (and negative durations) per
+// scenario from its lane-busy sums; otherwise the exact general kernel reruns
+// the launch.
 #pragma once
 
 namespace ddsim_lanes {
@@ -78,8 +80,7 @@ __device__ __forceinline__ void sym_set(Sym<LN>& Y, int lane, const int (&y)[4])
 template <int DK, int LN>
 __device__ __forceinline__ void chain_sym(const Params& p, const ChainParams& cp, Sym<LN>& Y,
                                           int cid, int row, long long s, bool act,
-                                          unsigned slot_s, unsigned slot_pitch, unsigned col,
-                                          long long& tot, int& neg) {
+                                          unsigned slot_s, unsigned slot_pitch, unsigned col) {
   const Chain ch = cp.chains[cid];
   const bool pres = !act || cp.present == nullptr || cp.present[s * cp.n_chains + cid] != 0;
   int prev[4];
@@ -100,8 +101,6 @@ __device__ __forceinline__ void chain_sym(const Params& p, const ChainParams& cp
         const long long at = (long long)(row + k) * p.dense_ld + s;
         d = DK == 1 ? (long long)cp.dense32[at] : p.dense64[at];
       }
-      neg |= (int)(d >> 32);
-      tot += d + M.gap;
       const int a = (int)d + (int)M.gap;
 #pragma unroll
       for (int c = 0; c < 4; ++c) prev[c] = x[c] + a;
@@ -169,8 +168,6 @@ __device__ __forceinline__ void sym_pass(const Tmap* tmap, const Params& p, cons
   for (int l = 0; l <= NLANE; ++l)
 #pragma unroll
     for (int c = 0; c < LN; ++c) Y.v[l][c] = (l == c) ? 0 : kNegSym;
-  long long tot = 0;  // durations + gaps walked (overflow certificate)
-  int neg = 0;
   const unsigned row_pitch = (unsigned)BD * ES;
 
   for (int c = c_begin; c < nchunks; ++c) {
@@ -200,7 +197,6 @@ __device__ __forceinline__ void sym_pass(const Tmap* tmap, const Params& p, cons
         raw = l_lds128(rec0 + (unsigned)(j + 1) * 16u);
         load_d(t0 + (unsigned)(j + 1) * row_pitch);
       }
-      neg |= (int)(d >> 32);
       const int gp = r.x;  // gap < 2^30 (host: every segment's gap sum is)
       const unsigned w = (unsigned)r.w;
       const unsigned h = w >> 24;
@@ -209,11 +205,10 @@ __device__ __forceinline__ void sym_pass(const Tmap* tmap, const Params& p, cons
         if (rare & (R_CHAIN | R_NOP)) {
           if (rare & R_CHAIN)
             chain_sym<DK, LN>(p, *cpp, Y, (int)(short)(r.z & 0xffff), c * kChunkL + j, s, act,
-                              slot_s, slot_pitch, col, tot, neg);
+                              slot_s, slot_pitch, col);
           return;
         }
       }
-      tot += d + gp;
       const int dv = (int)d;
       if (rare & R_PRE) {
         // slot predecessors (all in shared memory on this path) -> temp lane
@@ -260,7 +255,6 @@ __device__ __forceinline__ void sym_pass(const Tmap* tmap, const Params& p, cons
     __syncthreads();
     if (tid == 0 && c + kStagesL < nchunks) issue(c + kStagesL);
   }
-  if (act && (neg < 0 || tot >= (1LL << 30)) && p.neg_flag) atomicOr(p.neg_flag, 2);
 #pragma unroll
   for (int j = 0; j < LN; ++j)
 #pragma unroll
