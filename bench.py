@@ -476,6 +476,464 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
+# ---------------------------------------------------------------- configs 1-3, 5
+# `--config N` measures BASELINE.json configs[N-1] with the same contract
+# (device-resident value, e2e through the public host-buffer API, roofline,
+# CPU baseline, oracle parity of the timed output).  Configs 1-3 are sweeps of
+# derived durations (Shrink programs, inserted AllReduce chains); config 5 is
+# trace ingest from JSON text.
+
+CONFIG_NAMES = {
+    1: "config1 resnet50-like iteration (~10k tasks, 1 cpu + 1 stream): baseline + AMP Shrink",
+    2: "config2 bert-large-like per-layer Shrink 2x sweep (~30k tasks, one scenario per layer "
+       "+ baseline)",
+    3: "config3 data-parallel: bert-like trace + per-bucket AllReduce inserts, bandwidth (10) x "
+       "workers (8) x bucket order (50)",
+    5: "config5 trace ingest: 10M-record synthetic trace (8 cpu threads, 16 streams) from JSON "
+       "text -> correlation join, sync links, layer map, frozen CSR graph",
+}
+
+
+def build_config(c: int, device: int):
+    """-> (frozen, table, scenario checker, CPU-baseline closure, info)."""
+    from fractions import Fraction
+
+    from paper_2006_03318_b200 import workloads as W
+    from paper_2006_03318_b200.batch import ScenarioTable, compile_scale_sweep, distributed_sweep
+    from paper_2006_03318_b200.frozen import FrozenGraph
+    from paper_2006_03318_b200.transform import (GPU_TASKS, And, ByLayer, Selector,
+                                                 TransformPipeline, apply_pipeline,
+                                                 scale_durations)
+
+    if c in (1, 2):
+        if c == 1:
+            from paper_2006_03318_b200.scenarios import whatif_amp
+            w = W.resnet50_trace()
+            amp = whatif_amp(w.graph)
+            scen = [[], [(Selector.from_object(x["selector"]), x["factor"]) for x in amp.steps]]
+        else:
+            w = W.bert_trace(buckets_mb=None)
+            scen = [[(And([GPU_TASKS, ByLayer(l)]), "1/2")] for l in w.layers] + [[]]
+        g = w.graph
+        group_of, ptr, steps = compile_scale_sweep(g, scen)
+        fz = FrozenGraph.from_graph(g, group_of=group_of, device=device)
+        table = ScenarioTable(n_scenarios=len(scen), scale_ptr=ptr, scale=steps)
+
+        def graph_of(s):
+            h = g.copy()
+            for sel, f in scen[s]:
+                scale_durations(h, sel, Fraction(str(f)))
+            return h
+        return fz, table, graph_of, {"tasks": fz.n, "scenarios": len(scen)}
+    if c == 3:
+        from paper_2006_03318_b200.scenarios import whatif_distributed
+        w = W.bert_trace(buckets_mb=25.0)
+        g = w.graph
+        buckets = w.trace.gradient_buckets
+        B = len([b for b in buckets.buckets() if buckets.layers_of_bucket(b)])
+        rng = np.random.default_rng(0)
+        configs, perms = [], []
+        for _ in range(50):
+            o = rng.permutation(B)
+            for nw in (1, 2, 4, 8, 16, 32, 64, 128):
+                for bw in (1, 5, 10, 25, 50, 100, 200, 400, 800, 1600):
+                    configs.append({"bandwidth_gbps": bw, "workers": nw})
+                    perms.append(o)
+        sw = distributed_sweep(g, buckets, configs, np.array(perms, np.int16), device=device)
+
+        from paper_2006_03318_b200 import transform as TR
+
+        def graph_of(s):
+            # the reference pipeline's steps in this scenario's bucket order,
+            # applied on the host without the device acyclicity check (the
+            # oracle's Alg. 1 raises on a cycle itself)
+            pipe = whatif_distributed(g, buckets=buckets, **configs[s])
+            steps = [pipe.steps[k] for k in perms[s]] if pipe.steps else []
+            h = g.copy()
+            TR._DEFER["on"] = True
+            try:
+                for stp in steps:
+                    TR.apply_step(h, stp)
+            finally:
+                TR._DEFER["on"] = False
+            return h
+        return sw.frozen, sw.table, graph_of, {"tasks": sw.frozen.n, "scenarios": len(configs),
+                                               "buckets": B}
+    raise ValueError(f"config {c}")
+
+
+def _table_bytes(table) -> int:
+    n = 0
+    for a in (table.scale_ptr, table.scale, table.chain_perm, table.chain_present):
+        if a is not None:
+            n += np.asarray(a).nbytes
+    return n
+
+
+def _oracle_scenarios(fz, graph_of, ms, lb, start, cols) -> list:
+    """Device rows of scenarios `cols` against the C oracle's Alg. 1 on the
+    reference-equivalent transformed graph (checker only)."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    from oracle import OracleGraph
+
+    for s in cols:
+        st, m, lbo, _ = OracleGraph.from_graph(graph_of(s)).simulate("default")
+        col = start[:, s]
+        got = {int(t): int(v) for t, v in zip(fz.row_ids.tolist(), col.tolist()) if v >= 0}
+        if int(ms[s]) != m or got != st:
+            raise AssertionError(f"scenario {s}: device differs from the oracle ({int(ms[s])} vs {m})")
+        want_lb = {str(k): v for k, v in lbo.items()}
+        got_lb = {str(fz.lanes[j]): int(lb[s, j]) for j in range(fz.L) if str(fz.lanes[j]) in want_lb}
+        if got_lb != want_lb:
+            raise AssertionError(f"scenario {s}: lane busy differs from the oracle")
+    return [int(x) for x in cols]
+
+
+def _config_cpu_baseline(graph_of, S, n, target_s=10.0) -> dict:
+    """The reference algorithm per scenario: the scenario's transformed graph
+    (the reference's pipeline semantics) and the C port of Alg. 1 on it, one
+    scenario per host thread (ctypes releases the GIL), on a bounded sample of
+    the sweep's scenarios.  Only the simulate calls are timed."""
+    from concurrent.futures import ThreadPoolExecutor
+
+    sys.path.insert(0, str(ROOT / "oracle"))
+    from oracle import OracleGraph
+
+    threads = os.cpu_count() or 1
+    idx = np.unique(np.linspace(0, S - 1, min(S, 2 * threads)).astype(int))
+    t0 = time.perf_counter()
+    graphs = [OracleGraph.from_graph(graph_of(int(s))) for s in idx]
+    t_build = time.perf_counter() - t0
+    done, t_sim = 0, 0.0
+    with ThreadPoolExecutor(threads) as ex:
+        while t_sim < target_s:
+            t1 = time.perf_counter()
+            list(ex.map(lambda og: og.simulate_raw("default"), graphs))
+            t_sim += time.perf_counter() - t1
+            done += len(graphs)
+    return {"value": done * n / t_sim, "unit": UNIT, "cores": threads, "kind": "port",
+            "sample_scenarios": int(done),
+            "sample": f"{len(graphs)} of {S} scenarios x {n} tasks, simulated {done} times: "
+                      f"oracle/ddsim_oracle.c Alg. 1 on each transformed graph, {threads} threads, "
+                      f"{t_sim:.1f} s (graph transforms {t_build:.1f} s, untimed)"}
+
+
+def run_config(args):
+    import torch
+
+    from paper_2006_03318_b200 import _native as N
+    from paper_2006_03318_b200.batch import simulate_batch, simulate_batch_device
+
+    c = args.config
+    ws, rank, local = _dist()
+    if rank != 0:  # the secondary configs are single-GPU sweeps (replicas only)
+        return
+    dev = local
+    torch.cuda.set_device(dev)
+    fz, table, graph_of, info = build_config(c, dev)
+    S, n, L = table.n_scenarios, fz.n, fz.L
+    st = torch.empty((n, S), dtype=torch.int64, device=f"cuda:{dev}")
+    ms = torch.empty(S, dtype=torch.int64, device=f"cuda:{dev}")
+    lb = torch.empty((S, max(L, 1)), dtype=torch.int64, device=f"cuda:{dev}")
+    stream = torch.cuda.current_stream()
+
+    def step():
+        simulate_batch_device(fz, table, makespan=ms, lane_busy=lb, start=st,
+                              stream=stream.cuda_stream)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    clocks = Clocks(dev)
+    l0 = N.launch_count()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    launches = N.launch_count() - l0
+    elapsed = e0.elapsed_time(e1)
+    clk = clocks.stop()
+    per = elapsed / args.steps
+    checked = _oracle_scenarios(fz, graph_of, ms.cpu().numpy(), lb.cpu().numpy(),
+                                st.cpu().numpy(), sorted({0, S // 2, S - 1}))
+    # e2e: the public host-buffer call (tables uploaded, starts / makespan /
+    # lane busy copied back), wall clock
+    simulate_batch(fz, table)
+    t0 = time.perf_counter()
+    n_e2e = max(1, min(args.steps, 5))
+    for _ in range(n_e2e):
+        r = simulate_batch(fz, table)
+    dt = (time.perf_counter() - t0) / n_e2e
+    assert np.array_equal(r.makespan, ms.cpu().numpy()), "e2e result differs from device run"
+    jit = (N.lib().ks_jit_log() or b"").decode()
+    peak, peak_src = _peaks()
+    bpu = 8  # start write; durations derive on the device from base x scenario program
+    achieved = n * S * bpu / (per / 1e3) / 1e9
+    cb = None if args.no_cpu_baseline else _config_cpu_baseline(graph_of, S, n)
+    line = {
+        "metric": METRIC, "value": n * S / (per / 1e3), "unit": UNIT, "n_gpus": 1,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": per, "higher_is_better": True,
+        "scaling": "replicas only (one GPU per sweep)", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic",
+        "config": {"workload": CONFIG_NAMES[c], **info,
+                   "l2": "outputs stream to HBM every step (no reuse across steps)"},
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
+                     "frac": achieved / peak, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": n * S * bpu, "traffic": None,
+                     "traffic_source": "not captured in this run (see profiles/)",
+                     "path": "segment-parallel" if "seg_t:" in jit else "single-pass"},
+        "cpu_baseline": cb,
+        "e2e": {"value": n * S / dt, "unit": UNIT, "h2d_bytes_per_step": _table_bytes(table),
+                "d2h_bytes_per_step": n * S * 8 + S * 8 + S * L * 8,
+                "api": "batch.simulate_batch (ks_simulate_host)"},
+        "parity_checked": {"scenarios": checked,
+                           "checker": "oracle/ddsim_oracle.c Alg. 1 on the reference-equivalent "
+                                      "transformed graph: every start, makespan, lane busy"},
+        "gpu_launches": launches,
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_config_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    import os as _os
+    _os.environ.setdefault("DDSIM_COMPILE_ONLY", "1")
+    fz, table, graph_of, info = build_config(args.config, -1)
+    vals, cb = [], None
+    for i in range(args.warmup + args.steps):
+        cb = _config_cpu_baseline(graph_of, table.n_scenarios, fz.n,
+                                  target_s=1.0 if i < args.warmup else 6.0)
+        if i >= args.warmup:
+            vals.append(cb["value"])
+    v = statistics.median(vals)
+    print(json.dumps({"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT,
+                      "n_gpus": ws, "steps": args.steps, "warmup": args.warmup,
+                      "higher_is_better": True, "scaling": "replicas only", "vs_baseline": None,
+                      "dtype": "int64", "data": "synthetic",
+                      "config": {"workload": CONFIG_NAMES[args.config], **info,
+                                 "sample_scenarios_per_step": cb["sample_scenarios"]},
+                      "cpu_baseline": dict(cb, value=v),
+                      "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0,
+                              "d2h_bytes_per_step": 0}}), flush=True)
+
+
+class _SubCols:
+    """Rows `idx` of a TraceColumns (the oracle's ingest entry points take
+    any object with these columns)."""
+
+    def __init__(self, cols, idx):
+        for k in ("id", "start", "duration", "correlation", "kind", "is_dtoh", "lane",
+                  "sync_target"):
+            setattr(self, k, np.asarray(getattr(cols, k))[idx])
+        self.lanes = cols.lanes
+        self.n = len(idx)
+        self._lc = np.asarray(cols.lane_class_codes())
+
+    def lane_class_codes(self):
+        return self._lc
+
+
+def _oracle_edges(cols):
+    """Edge arrays of the oracle's build_graph over columns (checker)."""
+    import ctypes as C
+
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as O
+
+    h = O.lib()
+    h.ora_build_graph.argtypes = [C.POINTER(O._OraTrace)] + [C.c_void_p] * 5
+    h.ora_build_graph.restype = C.c_int64
+    t, keep = O._trace_struct(cols)
+    n = max(int(cols.n), 1)
+    cap = 3 * n + int(np.sum(np.asarray(cols.kind) == 6)) * (len(cols.lanes) + 1) + 16
+    sa, da, ka = np.empty(cap, np.int32), np.empty(cap, np.int32), np.empty(cap, np.uint8)
+    gap, launcher = np.empty(n, np.int64), np.empty(n, np.int32)
+    m = h.ora_build_graph(C.byref(t), sa.ctypes.data, da.ctypes.data, ka.ctypes.data,
+                          gap.ctypes.data, launcher.ctypes.data)
+    del keep
+    return sa[:m], da[:m], ka[:m], gap[:cols.n], launcher[:cols.n]
+
+
+def _sorted_edges(src, dst, kind):
+    key = np.lexsort((np.asarray(kind, np.int64), np.asarray(dst, np.int64),
+                      np.asarray(src, np.int64)))
+    return np.asarray(src)[key], np.asarray(dst)[key], np.asarray(kind)[key]
+
+
+def ingest_parity(ct, res, tag, sample_cpu: int = 2000) -> dict:
+    """Config-5 output against the oracle (checker, outside the timed region):
+    the whole edge multiset (src, dst, kind), every gap and every launcher of
+    build_graph over all records; layer tags of a random sample of CPU events
+    (the oracle's layer map is O(records x markers)), GPU events inheriting
+    their launcher's tag."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as O
+
+    cols = ct.cols
+    t0 = time.perf_counter()
+    sa, da, ka, gap, launcher = _oracle_edges(cols)
+    a = _sorted_edges(sa, da, ka)
+    b = _sorted_edges(res.edge_src, res.edge_dst, res.edge_kind)
+    if not (len(a[0]) == len(b[0]) and all(np.array_equal(x, y) for x, y in zip(a, b))):
+        raise AssertionError("ingest edges differ from the oracle's build_graph")
+    if not np.array_equal(gap, res.gap) or not np.array_equal(launcher, res.launcher):
+        raise AssertionError("ingest gaps / launchers differ from the oracle")
+    rng = np.random.default_rng(3)
+    kind = np.asarray(cols.kind)
+    cpu_idx = np.nonzero(np.isin(kind, [0, 1, 4, 6]) & (np.asarray(cols.lane) >= 0))[0]
+    pick = np.sort(rng.choice(cpu_idx, size=min(sample_cpu, len(cpu_idx)), replace=False))
+    tag_m, _tags = ct.marker_tags()
+    sub = _SubCols(cols, pick)
+    want, _bad = O.map_layers_columns(sub, np.full(len(pick), -1, np.int32), ct.m_lane,
+                                      ct.m_start, ct.m_end, tag_m)
+    if not np.array_equal(np.asarray(tag)[pick], want):
+        raise AssertionError("layer tags differ from the oracle's map_tasks_to_layers")
+    gpu = np.nonzero((np.asarray(res.launcher) >= 0))[0]
+    if not np.array_equal(np.asarray(tag)[gpu], np.asarray(tag)[np.asarray(res.launcher)[gpu]]):
+        raise AssertionError("GPU events do not inherit their launcher's layer")
+    return {"edges": int(len(b[0])), "gaps_and_launchers": int(cols.n),
+            "layer_tags_sampled_cpu_events": int(len(pick)),
+            "checker": "oracle/ddsim_oracle.c build_graph (all records) + map_layers (sample)",
+            "check_s": round(time.perf_counter() - t0, 2)}
+
+
+def _ingest_cpu_baseline(n_sample: int = 1_000_000) -> dict:
+    """The reference's ingest algorithm (C port of build_graph rules 1-5 and
+    the O(records x markers) layer containment scan) on one core, on a bounded
+    sample of the config-5 generator: build_graph over a 1M-record trace, the
+    layer scan timed on 2,000 CPU events of it and scaled to all of them."""
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as O
+    from paper_2006_03318_b200.workloads import ingest_document_columns
+
+    ct = ingest_document_columns(n_sample, seed=1)
+    cols = ct.cols
+    t0 = time.perf_counter()
+    _oracle_edges(cols)
+    t_build = time.perf_counter() - t0
+    kind = np.asarray(cols.kind)
+    cpu_idx = np.nonzero(np.isin(kind, [0, 1, 4, 6]))[0]
+    pick = cpu_idx[:: max(1, len(cpu_idx) // 2000)][:2000]
+    tag_m, _ = ct.marker_tags()
+    t1 = time.perf_counter()
+    O.map_layers_columns(_SubCols(cols, pick), np.full(len(pick), -1, np.int32), ct.m_lane,
+                         ct.m_start, ct.m_end, tag_m)
+    t_map = (time.perf_counter() - t1) / len(pick) * len(cpu_idx)
+    n = int(cols.n)
+    return {"value": n / (t_build + t_map), "unit": "records/s", "cores": 1, "kind": "port",
+            "sample_records": n,
+            "sample": f"{n} records ({ct.n_markers} markers): build_graph {t_build:.2f} s + layer "
+                      f"scan {t_map:.1f} s (timed on {len(pick)} CPU events, scaled to "
+                      f"{len(cpu_idx)}); oracle/ddsim_oracle.c, 1 core"}
+
+
+def run_ingest(args):
+    import torch
+
+    from paper_2006_03318_b200 import _native as N
+    from paper_2006_03318_b200.columnar import (dump_trace_columns, frozen_from_ingest,
+                                                 load_trace_columns)
+    from paper_2006_03318_b200.ingest import ingest_arrays, map_layers_arrays
+    from paper_2006_03318_b200.workloads import ingest_document_columns
+
+    ws, rank, local = _dist()
+    if rank != 0:  # ingest is replicas only (global joins; SURVEY 8(e))
+        return
+    torch.cuda.set_device(local)
+    text = dump_trace_columns(ingest_document_columns(args.ingest_records, seed=0))
+    times, stages = [], {}
+    clocks = None
+    l0 = 0
+    for i in range(args.warmup + args.steps):
+        if i == args.warmup:
+            torch.cuda.synchronize()
+            clocks = Clocks(local)
+            l0 = N.launch_count()
+        t0 = time.perf_counter()
+        ct = load_trace_columns(text)
+        t1 = time.perf_counter()
+        res = ingest_arrays(ct.cols)
+        t2 = time.perf_counter()
+        tag_m, tags = ct.marker_tags()
+        tag = map_layers_arrays(ct.cols, res.launcher, ct.m_lane, ct.m_start, ct.m_end, tag_m)
+        t3 = time.perf_counter()
+        fz = frozen_from_ingest(ct, res)
+        torch.cuda.synchronize()
+        t4 = time.perf_counter()
+        if i >= args.warmup:
+            times.append(t4 - t0)
+            for k, v in (("parse_s", t1 - t0), ("ingest_s", t2 - t1), ("layer_map_s", t3 - t2),
+                         ("freeze_s", t4 - t3)):
+                stages.setdefault(k, []).append(v)
+        if i + 1 < args.warmup + args.steps:
+            fz.close()
+            del ct, res, tag, fz
+    launches = N.launch_count() - l0
+    clk = clocks.stop()
+    n = int(ct.n_events)
+    per = statistics.median(times)
+    st = {k: statistics.median(v) for k, v in stages.items()}
+    parity = ingest_parity(ct, res, tag)
+    dev_s = st["ingest_s"] + st["layer_map_s"]
+    peak, peak_src = _peaks()
+    col_bytes = 41 * n
+    line = {
+        "metric": "trace records ingested/sec (JSON text -> device frozen graph)",
+        "value": n / per, "unit": "records/s", "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": per * 1e3, "higher_is_better": True,
+        "scaling": "replicas only (global joins)", "vs_baseline": None, "dtype": "int64",
+        "data": "synthetic",
+        "config": {"workload": CONFIG_NAMES[5], "records": n, "json_bytes": len(text),
+                   "markers": int(ct.n_markers), "edges": int(res.edge_src.shape[0]),
+                   "layers": len(tags), "frozen_chained": bool(fz.chained),
+                   "host_threads": os.cpu_count(),
+                   **{k: round(v, 4) for k, v in st.items()}},
+        "roofline": {"bound": "hbm", "achieved": n * 80 / dev_s / 1e9, "peak": peak,
+                     "unit": "GB/s", "frac": n * 80 / dev_s / 1e9 / peak, "peak_source": peak_src,
+                     "algorithmic_bytes_per_launch": n * 80, "traffic": None,
+                     "note": "device stages (ks_ingest + ks_map_layers) wall time incl. their "
+                             "column transfers; the step is host-bound (parse + freeze)"},
+        "cpu_baseline": None if args.no_cpu_baseline else _ingest_cpu_baseline(),
+        "e2e": {"value": n / per, "unit": "records/s", "h2d_bytes_per_step": col_bytes,
+                "d2h_bytes_per_step": int(res.edge_src.nbytes + res.edge_dst.nbytes +
+                                          res.edge_kind.nbytes + res.gap.nbytes +
+                                          res.launcher.nbytes),
+                "api": "columnar.load_trace_columns -> ingest_arrays -> map_layers_arrays -> "
+                       "frozen_from_ingest (host text in, device frozen graph out)"},
+        "parity_checked": parity,
+        "gpu_launches": launches // max(args.steps, 1),
+        "clocks": clk,
+    }
+    print(json.dumps(line), flush=True)
+
+
+def run_ingest_reference(args):
+    ws, rank, _ = _dist()
+    if rank != 0:
+        return
+    vals, cb = [], None
+    for i in range(args.warmup + args.steps):
+        cb = _ingest_cpu_baseline(200_000 if i < args.warmup else 1_000_000)
+        if i >= args.warmup:
+            vals.append(cb["value"])
+    v = statistics.median(vals)
+    print(json.dumps({"impl": "reference", "metric": "trace records ingested/sec (JSON text -> "
+                      "device frozen graph)", "value": v, "unit": "records/s", "n_gpus": ws,
+                      "steps": args.steps, "warmup": args.warmup, "higher_is_better": True,
+                      "scaling": "replicas only", "vs_baseline": None, "dtype": "int64",
+                      "data": "synthetic",
+                      "config": {"workload": CONFIG_NAMES[5],
+                                 "sample_records_per_step": cb["sample_records"]},
+                      "cpu_baseline": dict(cb, value=v),
+                      "e2e": {"value": v, "unit": "records/s", "h2d_bytes_per_step": 0,
+                              "d2h_bytes_per_step": 0}}), flush=True)
+
+
 def shard_size(total: int, ws: int, scaling: str) -> int:
     """Scenarios per rank: strong = the total split over the ranks (a multiple
     of 32), weak = the total on every rank."""
@@ -526,7 +984,16 @@ def main():
     ap.add_argument("--scenarios", type=int, default=S_PER_GPU)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ingest-records", type=int, default=10_000_000)
+    ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5],
+                    help="BASELINE.json configs[N-1]; 4 (default) is the headline jitter sweep")
     args = ap.parse_args()
+    if args.config != 4:
+        if args.config == 5:
+            (run_ingest_reference if args.impl == "reference" else run_ingest)(args)
+        else:
+            (run_config_reference if args.impl == "reference" else run_config)(args)
+        return
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
         sys.exit(_spawn(args.gpus))
     ws = int(os.environ.get("WORLD_SIZE", "1"))

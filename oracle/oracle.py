@@ -151,6 +151,21 @@ class OracleGraph:
         del keep
         return start_of, int(ms[0]), lane_busy, tr
 
+    def simulate_raw(self, policy: str = "default") -> int:
+        """Alg. 1 with the results left in arrays (the CPU-baseline timing
+        path: the ctypes call releases the GIL, so threads run scenarios in
+        parallel).  Returns the makespan."""
+        g = self._c()
+        n = len(self.ids)
+        start = np.zeros(max(n, 1), np.int64)
+        trace = np.zeros(max(n, 1), np.int32)
+        lb = np.zeros(max(len(self.lanes), 1), np.int64)
+        ms = np.zeros(1, np.int64)
+        if lib().ora_simulate(C.byref(g), POL[policy], start.ctypes.data, trace.ctypes.data,
+                              lb.ctypes.data, ms.ctypes.data) != n:
+            raise RuntimeError("Deadlock")
+        return int(ms[0])
+
     def toposort(self) -> list[int]:
         g = self._c()
         n = len(self.ids)
