@@ -230,6 +230,10 @@ typedef struct {
                                * host maps "no layer" to its own index); NULL =
                                * no per-layer output                           */
   int32_t n_layers;
+  const int32_t* schedule;    /* DEVICE [S][n_tasks] dispatch order of a list-
+                               * scheduled batch (ks_sim_out.schedule of the same
+                               * ks_simulate call); required when the graph is not
+                               * lane-chained, NULL otherwise                   */
 } ks_breakdown_desc;
 
 /* compute_breakdown / per_layer_breakdown of a max-plus batch, on the device,
@@ -240,7 +244,8 @@ typedef struct {
  *                              sum to makespan[s]); all -1 if a lane's
  *                              intervals were not sorted (negative durations)
  *   layer_busy[(layer * 2 + {0 cpu, 1 gpu}) * S + s]  (may be NULL)
- * Needs a lane-chained graph (KS_ERR_UNSUPPORTED otherwise). */
+ * Lane-chained graphs use the static lane orders; list-scheduled batches
+ * pass their dispatch order in bd->schedule (KS_ERR_UNSUPPORTED if neither). */
 int ks_breakdown(const ks_graph* g, const ks_scenarios_desc* sc, const int64_t* start,
                  int64_t start_ld, const int64_t* makespan, const ks_breakdown_desc* bd,
                  int64_t* parts, int64_t* layer_busy, void* stream);

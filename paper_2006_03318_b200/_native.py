@@ -88,7 +88,8 @@ class SimOut(C.Structure):
 
 class BreakdownDesc(C.Structure):
     _fields_ = [("row_class", P), ("comm_as_gpu", C.c_int32), ("dataload_as_cpu", C.c_int32),
-                ("gaps_as_cpu_busy", C.c_int32), ("row_layer", P), ("n_layers", C.c_int32)]
+                ("gaps_as_cpu_busy", C.c_int32), ("row_layer", P), ("n_layers", C.c_int32),
+                ("schedule", P)]
 
 
 KS_BD_CPU, KS_BD_GPU, KS_BD_COMM, KS_BD_CPU_DATALOAD = 0, 1, 2, 3

@@ -126,6 +126,9 @@ class ScenarioTable:
     chain_perm: np.ndarray | None = None # int16[S][sum B]
     chain_present: np.ndarray | None = None  # uint8[S][n_chains]
     vdnn_rank: np.ndarray | None = None  # int32[rows]
+    # schedule policy (name, params) the compiled pipelines ask for
+    # (TransformPipeline.schedule_policy / policy_params); not part of the C descriptor
+    policy: tuple = ("default", None)
 
     def desc(self, keep: list, rows: int | None = None) -> N.ScenariosDesc:
         """C descriptor of the table.  ``rows`` (the frozen graph's row
@@ -249,9 +252,9 @@ def _simulate_batch_with_breakdown(frozen, table, policy, want_start, comm_as_gp
     if frozen.n_ordered < frozen.n:
         missing = frozen.unordered_ids()
         raise Deadlock(f"{len(missing)} tasks never became ready (first ids: {missing[:10]})")
-    if not frozen.chained:
-        raise Unsupported("the batched breakdown needs a lane-chained graph (max-plus path); "
-                          "use breakdown.compute_breakdown on a SimulationResult")
+    listsched = not frozen.chained
+    if listsched and frozen.chains:
+        raise Unsupported("permutable chains need a lane-chained graph for the batched breakdown")
     dev = torch.device("cuda", frozen.device)
     S, rows, L = table.n_scenarios, frozen.n, frozen.L
     dtab = table
@@ -265,14 +268,16 @@ def _simulate_batch_with_breakdown(frozen, table, policy, want_start, comm_as_gp
     row_layer = _row_layer_ids(frozen)
     names = layer_names_of(frozen)
     lbz = torch.empty((max(len(names), 1), 2, S), dtype=torch.int64, device=dev)
+    sched = (torch.empty((S, max(rows, 1)), dtype=torch.int32, device=dev) if listsched
+             else None)
     with torch.cuda.device(dev):
         stream = torch.cuda.current_stream().cuda_stream
         simulate_batch_device(frozen, dtab, makespan=ms, lane_busy=lb, start=st, start_ld=S,
-                              stream=stream, policy=policy)
+                              stream=stream, policy=policy, schedule=sched)
         breakdown_batch_device(frozen, dtab, start=st, makespan=ms, parts=parts, layer_busy=lbz,
                                stream=stream, comm_as_gpu=comm_as_gpu,
                                dataload_as_cpu=dataload_as_cpu, gaps_as_cpu_busy=gaps_as_cpu_busy,
-                               row_layer=row_layer, n_layers=len(names))
+                               row_layer=row_layer, n_layers=len(names), schedule=sched)
         torch.cuda.current_stream().synchronize()
     return BatchResult(frozen=frozen, makespan=ms.cpu().numpy(), lane_busy=lb.cpu().numpy()[:, :L],
                        start=st.cpu().numpy()[:rows] if want_start else None,
@@ -282,9 +287,12 @@ def _simulate_batch_with_breakdown(frozen, table, policy, want_start, comm_as_gp
 def breakdown_batch_device(frozen: FrozenGraph, table: ScenarioTable, *, start, makespan, parts,
                            layer_busy=None, stream: int = 0, comm_as_gpu: bool = True,
                            dataload_as_cpu: bool = True, gaps_as_cpu_busy: bool = True,
-                           row_layer=None, n_layers: int = 0, start_ld: int | None = None) -> None:
+                           row_layer=None, n_layers: int = 0, start_ld: int | None = None,
+                           schedule=None) -> None:
     """ks_breakdown on device tensors (start / makespan from
-    simulate_batch_device on the same table); asynchronous on ``stream``."""
+    simulate_batch_device on the same table); asynchronous on ``stream``.
+    A list-scheduled (not lane-chained) batch passes its dispatch order
+    ``schedule`` [S][rows] int32 from the same simulate_batch_device call."""
     keep: list = []
     sc = table.desc(keep, frozen.n)
     bd = N.BreakdownDesc()
@@ -298,6 +306,7 @@ def breakdown_batch_device(frozen: FrozenGraph, table: ScenarioTable, *, start, 
         keep.append(rl)
         bd.row_layer = rl.ctypes.data if rl.size else None
         bd.n_layers = n_layers or len(layer_names_of(frozen))
+    bd.schedule = N.ptr(schedule)
     ld = start_ld if start_ld is not None else int(start.stride(0))
     N.check(N.lib().ks_breakdown(frozen.handle, C.byref(sc), N.ptr(start), ld, N.ptr(makespan),
                                  C.byref(bd), N.ptr(parts), N.ptr(layer_busy), C.c_void_p(stream)),
@@ -306,9 +315,11 @@ def breakdown_batch_device(frozen: FrozenGraph, table: ScenarioTable, *, start, 
 
 def simulate_batch_device(frozen: FrozenGraph, table: ScenarioTable, *, makespan, lane_busy=None,
                           start=None, start_ld: int | None = None, stream: int = 0,
-                          policy: str = "default", path: int = N.KS_PATH_AUTO) -> None:
+                          policy: str = "default", path: int = N.KS_PATH_AUTO,
+                          schedule=None) -> None:
     """Device tensors in/out (ks_simulate): asynchronous on ``stream``
-    (a cudaStream_t as int, e.g. torch.cuda.current_stream().cuda_stream)."""
+    (a cudaStream_t as int, e.g. torch.cuda.current_stream().cuda_stream).
+    ``schedule`` [S][rows] int32 receives the dispatch order (list scheduler)."""
     keep: list = []
     sc = table.desc(keep, frozen.n)
     out = N.SimOut()
@@ -317,6 +328,9 @@ def simulate_batch_device(frozen: FrozenGraph, table: ScenarioTable, *, makespan
     if start is not None:
         out.start = N.ptr(start)
         out.start_ld = start_ld if start_ld is not None else int(start.stride(0))
+    if schedule is not None:
+        out.schedule = N.ptr(schedule)
+        path = N.KS_PATH_LISTSCHED
     N.check(N.lib().ks_simulate(frozen.handle, C.byref(sc), POLICY_IDS[policy], path,
                                 C.byref(out), C.c_void_p(stream)), "simulate_batch_device")
 
@@ -379,18 +393,24 @@ def compile_pipelines(graph: DependencyGraph, pipelines: list, device: int | Non
     transform.py:285-399) into one scenario table over a frozen copy of
     ``graph``: scale -> scale steps, set_duration -> per-scenario overrides,
     remove -> KS_STEP_REMOVE steps, set_priority -> nothing (a lane-chained
-    graph's schedule does not depend on the policy or priorities).
+    graph's schedule does not depend on the policy or priorities; on other
+    graphs priorities are structure: see _compile_structural).
 
     Selections are evaluated on ``graph`` itself: scale / set_duration /
     set_priority do not change the attributes selectors read, and removal is
     final, so each step touches the same tasks as on the progressively
-    transformed graph.  Returns (FrozenGraph, ScenarioTable); raises
-    Unsupported for insert ops or an unchained graph."""
+    transformed graph.  Pipelines with inserts (or with set_priority steps
+    and one common structure) compile through _compile_structural.
+    Returns (FrozenGraph, ScenarioTable); raises Unsupported when no table
+    expresses the pipelines."""
     from .errors import UnknownTask
     from .transform import select
 
     pipes = [p if isinstance(p, TransformPipeline) else TransformPipeline.from_object(p)
              for p in pipelines]
+    all_ops = {step.get("op") for p in pipes for step in p.steps}
+    if all_ops & INSERT_OPS or ("set_priority" in all_ops and len({structure_key(p) for p in pipes}) == 1):
+        return _compile_structural(graph, pipes, device)
     # 1. distinct selections
     sel_ix: dict = {}
     sel_sets: list[frozenset] = []
@@ -449,8 +469,11 @@ def compile_pipelines(graph: DependencyGraph, pipelines: list, device: int | Non
         for k in sig:
             groups_of_sel[k].append(gid)
     fz = FrozenGraph.from_graph(graph, group_of=group_of, device=device)
-    if not fz.chained:
-        raise Unsupported("compile_pipelines needs a lane-chained graph (max-plus path)")
+    if not fz.chained and "set_priority" in all_ops:
+        raise Unsupported("set_priority steps of different structure on a list-scheduled graph")
+    if not fz.chained and any(op == "remove" for pl in plan for op, _k, _p in pl):
+        raise Unsupported("remove steps on a graph that is not lane-chained are structural "
+                          "(run them through apply_pipeline + simulate)")
     # 3. per-scenario programs
     S = len(pipes)
     ptr = [0]
@@ -486,6 +509,191 @@ def compile_pipelines(graph: DependencyGraph, pipelines: list, device: int | Non
     table = ScenarioTable(n_scenarios=S, overrides=ovr,
                           scale_ptr=np.array(ptr, np.int32) if steps_out else None,
                           scale=arr if steps_out else None)
+    _set_policy(table, graph, fz, pipes)
+    return fz, table
+
+
+def _set_policy(table: ScenarioTable, graph: DependencyGraph, fz: FrozenGraph, pipes: list) -> None:
+    """The pipelines' schedule policy (one per table) and its device
+    parameters (vdnn_prefetch: per-row conv rank, scenarios.py:593-630)."""
+    names = {(p.schedule_policy, repr(p.policy_params)) for p in pipes}
+    if len(names) > 1:
+        raise Unsupported("pipelines of one table must share a schedule policy")
+    p0 = pipes[0]
+    table.policy = (p0.schedule_policy, dict(p0.policy_params or {}))
+    if p0.schedule_policy == "vdnn_prefetch":
+        from .sim import make_policy
+        pol = make_policy(p0.schedule_policy, **(p0.policy_params or {}))
+        vr = pol.device_params(graph, fz).get("vdnn_rank")
+        table.vdnn_rank = np.ascontiguousarray(np.asarray(vr, np.int32)[fz.order])
+
+
+INSERT_OPS = frozenset({"insert", "insert_gpu_with_launch"})
+
+
+def structure_key(pipeline) -> str:
+    """A pipeline with every duration / factor blanked (plus its schedule
+    policy): pipelines with equal keys transform a graph into the same task
+    set, edges, lane orders and priorities, and differ only in durations.
+    A zero launch cost changes the structure (the launch is elided,
+    transform.py:347-353), so only its zero-ness stays in the key."""
+    import json
+
+    p = pipeline if isinstance(pipeline, TransformPipeline) else TransformPipeline.from_object(pipeline)
+    steps = []
+    for step in p.steps:
+        st = dict(step)
+        op = st.get("op")
+        if op == "scale":
+            st["factor"] = None
+        elif op == "set_duration":
+            st["duration_ns"] = None
+        elif op == "insert":
+            st["task"] = {**st["task"], "duration_ns": None}
+        elif op == "insert_gpu_with_launch":
+            st["kernel"] = {**st["kernel"], "duration_ns": None}
+            if st.get("launch_cost_ns") is not None:
+                st["launch_cost_ns"] = int(st["launch_cost_ns"]) > 0
+        steps.append(st)
+    return json.dumps([steps, p.schedule_policy, p.policy_params], sort_keys=True, default=str)
+
+
+def _compile_structural(graph: DependencyGraph, pipes: list, device):
+    """Pipelines with inserts (distributed, p3, blueconnect, vdnn, gist, dgc,
+    scenarios.py:191-470) that share one structure_key: the first pipeline is
+    applied structurally once (apply_pipeline, transform.py:370-396, with its
+    errors), and every pipeline's durations become table columns over that
+    transformed graph:
+
+    * an inserted task's (or launch's) duration and a set_duration value ->
+      a per-scenario override row when it varies across the pipelines;
+    * scale steps -> per-scenario half-up scale programs on groups of tasks
+      with the same sequence of selecting steps after their last base-setting
+      step (a selector is evaluated on the graph as it is at its step, so
+      tasks inserted later are not selected, exactly as in apply_step).
+
+    Unchained results (unsequenced inserts) run on the list scheduler with the
+    pipelines' policy; lane-chained ones on the max-plus kernels."""
+    from .transform import apply_pipeline, apply_step, insert_gpu_with_launch_step, select
+    from . import transform as TR
+
+    keys = {structure_key(p) for p in pipes}
+    if len(keys) != 1:
+        raise Unsupported("pipelines with inserts differ in structure (one table per "
+                          "structure_key; Analysis.whatif_batch groups them)")
+    p0 = pipes[0]
+    for p in pipes:  # every scale factor must be valid (scale_durations raises otherwise)
+        for step in p.steps:
+            if step.get("op") == "scale" and Fraction(str(step["factor"])) <= 0:
+                raise BadPipeline(f"scale factor must be positive, got {step['factor']}")
+    final = apply_pipeline(graph, p0)  # the reference's own errors, in step order
+    # replay pipeline 0 recording what each step touches
+    h = graph.copy()
+    events: dict[int, list] = {}   # task id -> [(step index, "base" | "scale")]
+    base_src: dict[int, tuple] = {}  # task id -> (step index, field) of its per-scenario base
+    numeric_seen = False
+    TR._DEFER["on"] = True
+    try:
+        for i, step in enumerate(p0.steps):
+            op = step.get("op")
+            if op == "scale":
+                for tid in select(h, Selector.from_object(step["selector"])):
+                    events.setdefault(tid, []).append((i, "scale"))
+                numeric_seen = True
+            elif op == "set_duration":
+                events.setdefault(step["task_id"], []).append((i, "base"))
+                base_src[step["task_id"]] = (i, "set")
+                numeric_seen = True
+            elif op == "insert":
+                before = set(h.tasks)
+                apply_step(h, step)
+                (tid,) = set(h.tasks) - before
+                events[tid] = [(i, "base")]
+                base_src[tid] = (i, "insert")
+                continue
+            elif op == "insert_gpu_with_launch":
+                if step.get("launch_cost_ns") is None and numeric_seen:
+                    raise Unsupported("insert_gpu_with_launch without launch_cost_ns after a "
+                                      "duration-changing step (its default cost varies)")
+                launch, kernel = insert_gpu_with_launch_step(h, step)
+                events[kernel] = [(i, "base")]
+                base_src[kernel] = (i, "kernel")
+                if launch in h.tasks and h.tasks[launch].kind is TaskKind.CPU_API and \
+                        launch != kernel:
+                    events[launch] = [(i, "base")]
+                    base_src[launch] = (i, "launch")
+                continue
+            elif op == "remove":
+                before = set(h.tasks)
+                apply_step(h, step)
+                for tid in before - set(h.tasks):
+                    events.pop(tid, None)
+                    base_src.pop(tid, None)
+                continue
+            apply_step(h, step)
+    finally:
+        TR._DEFER["on"] = False
+    assert set(h.tasks) == set(final.tasks)
+    g = final
+    S = len(pipes)
+
+    def value(p, i, field):
+        step = p.steps[i]
+        if field == "set":
+            return int(step["duration_ns"])
+        if field == "insert":
+            return int(step["task"]["duration_ns"])
+        if field == "kernel":
+            return int(step["kernel"]["duration_ns"])
+        cost = step.get("launch_cost_ns")
+        return int(cost) if cost is not None else int(g.tasks[launch_of[i]].duration)
+
+    launch_of = {i: tid for tid, (i, f) in base_src.items() if f == "launch"}
+    # per task: the scale steps after its last base-setting step
+    sig_of: dict[int, tuple] = {}
+    for tid, ev in events.items():
+        last_base = max((i for i, k in ev if k == "base"), default=-1)
+        sig_of[tid] = tuple(i for i, k in ev if k == "scale" and i > last_base)
+    tasks = list(g.tasks)
+    group_id: dict[tuple, int] = {(): 0}
+    group_of = np.zeros(len(tasks), np.uint32)
+    for j, tid in enumerate(tasks):
+        group_of[j] = group_id.setdefault(sig_of.get(tid, ()), len(group_id))
+    # base durations: the original duration, or pipeline 0's base-setting value
+    base_vals: dict[int, np.ndarray] = {}
+    for tid in tasks:
+        ev = events.get(tid, [])
+        last_base = max((i for i, k in ev if k == "base"), default=-1)
+        if last_base >= 0:
+            field = "set" if p0.steps[last_base]["op"] == "set_duration" else base_src[tid][1]
+            vals = np.array([value(p, last_base, field) for p in pipes], np.int64)
+            g.tasks[tid].duration = int(vals[0])
+            if np.any(vals != vals[0]):
+                base_vals[tid] = vals
+        else:
+            g.tasks[tid].duration = int(graph.tasks[tid].duration)
+    fz = FrozenGraph.from_graph(g, group_of=group_of, device=device)
+    index = {int(t): k for k, t in enumerate(fz.ids)}
+    ovr = {int(fz.row_of[index[tid]]): v for tid, v in base_vals.items()}
+    groups_with: dict[int, list[int]] = {}
+    for sig, gid in group_id.items():
+        for i in sig:
+            groups_with.setdefault(i, []).append(gid)
+    ptr, steps_out = [0], []
+    scale_steps = [i for i, st in enumerate(p0.steps) if st.get("op") == "scale"]
+    for p in pipes:
+        for i in scale_steps:
+            f = Fraction(str(p.steps[i]["factor"]))
+            steps_out += [(gid, gid, f.numerator, f.denominator) for gid in groups_with.get(i, ())]
+        ptr.append(len(steps_out))
+    arr = np.zeros(len(steps_out), N.SCALE_STEP_DTYPE)
+    for k, st in enumerate(steps_out):
+        arr[k] = st
+    table = ScenarioTable(n_scenarios=S, overrides=ovr,
+                          scale_ptr=np.array(ptr, np.int32) if steps_out else None,
+                          scale=arr if steps_out else None)
+    _set_policy(table, g, fz, pipes)
+    fz.source_graph = g
     return fz, table
 
 

@@ -57,6 +57,7 @@ __device__ __forceinline__ long long bd_dur(const BreakdownParams& p, int row, i
 template <bool CH>
 __device__ __forceinline__ int bd_row(const BreakdownParams& p, int l, int v, int s, bool chain_on) {
   const int base = p.lane_ptr[l];
+  if (p.srows) return p.srows[(long long)s * p.n + base + v];
   if (!CH) return p.lane_rows[base + v];
   const int c = p.lane_chain[l];
   if (c < 0 || !chain_on) return p.lane_rows[base + v];
@@ -311,6 +312,34 @@ __global__ void __launch_bounds__(128) layer_busy_kernel(const BreakdownParams p
     lb_flush(p, lay * 2, acc_c, s);
     lb_flush(p, lay * 2 + 1, acc_g, s);
   }
+}
+
+// Dispatch order [S][n] -> per-scenario lane sequences srows[s][lane_ptr[l] + k]
+// (the k-th dispatched row of lane l); one thread per scenario, per-lane
+// cursors in registers-or-local memory (L <= 32).
+__global__ void bd_sched_rows_kernel(const int* __restrict__ schedule,
+                                     const int* __restrict__ row_lane,
+                                     const int* __restrict__ lane_ptr, int n, int L, int S,
+                                     int* __restrict__ srows) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  int cur[kBdMaxLanes];
+  for (int l = 0; l < L; ++l) cur[l] = lane_ptr[l];
+  const int* sc = schedule + (long long)s * n;
+  int* out = srows + (long long)s * n;
+  for (int k = 0; k < n; ++k) {
+    const int row = sc[k];
+    out[cur[row_lane[row]]++] = row;
+  }
+}
+
+cudaError_t launch_bd_sched_rows(const int* schedule, const int* row_lane, const int* lane_ptr,
+                                 int n, int L, int S, int* srows, cudaStream_t stream) {
+  if (L > kBdMaxLanes) return cudaErrorInvalidValue;
+  bd_sched_rows_kernel<<<(S + 127) / 128, 128, 0, stream>>>(schedule, row_lane, lane_ptr, n, L, S,
+                                                             srows);
+  note_launch();
+  return cudaGetLastError();
 }
 
 cudaError_t launch_breakdown(const BreakdownParams& p, cudaStream_t stream) {

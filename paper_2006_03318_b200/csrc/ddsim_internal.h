@@ -296,8 +296,11 @@ struct BreakdownParams {
   long long* layer_busy;
   int n_layers;
   int start_may_be_neg;     // removal steps / permutable chains: start -1 marks a dropped task
+  const int* srows;         // [S][n] per-scenario lane sequences (list-scheduled) or null
 };
 cudaError_t launch_breakdown(const BreakdownParams& p, cudaStream_t stream);
+cudaError_t launch_bd_sched_rows(const int* schedule, const int* row_lane, const int* lane_ptr,
+                                 int n, int L, int S, int* srows, cudaStream_t stream);
 
 const char* jit_log();
 int maxplus_lanes_block_dim(int S, int num_sms);

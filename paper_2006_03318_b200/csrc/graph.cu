@@ -243,6 +243,9 @@ struct ks_graph {
   int* d_bd_lane_chain = nullptr;
   BdChain* d_bd_chains = nullptr;
   int* d_bd_member_rows = nullptr;
+  // rows per lane of any graph (list-scheduled breakdown: per-scenario lane
+  // sequences come from the dispatch order)
+  int* d_bd_all_ptr = nullptr;
 };
 
 namespace {
@@ -1382,6 +1385,12 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   // ---- breakdown geometry -------------------------------------------------------
   for (int i = 0; i < n; ++i)
     if (d->gap[i] < 0) g->gap_nonneg = false;
+  if (L > 0) {
+    hvec<int> aptr(L + 1, 0);
+    for (int i = 0; i < n; ++i) aptr[d->lane[i] + 1]++;
+    for (int l = 0; l < L; ++l) aptr[l + 1] += aptr[l];
+    g->d_bd_all_ptr = dev_upload(aptr);
+  }
   if (chained && L > 0) {
     hvec<int> bptr(L + 1, 0), brows, lane_chain(L, -1), pos_in_lane(n, -1);
     for (int l = 0; l < L; ++l) {
@@ -1423,7 +1432,8 @@ void free_graph(ks_graph* g) {
   void* dptrs[] = {g->d_dprog,   g->d_side_off,   g->d_side_slots,  g->d_side_ready,
                    g->d_lprog,   g->d_lside_off,  g->d_lside_slots, g->d_lside_ready,
                    g->d_bd_ptr,  g->d_bd_rows,    g->d_bd_lane_chain, g->d_bd_chains,
-                   g->d_bd_member_rows, g->d_lchains, g->d_lmembers, g->d_lpreds};
+                   g->d_bd_member_rows, g->d_lchains, g->d_lmembers, g->d_lpreds,
+                   g->d_bd_all_ptr};
   for (void* p : dptrs)
     if (p) cudaFree(p);
   void* ptrs[] = {g->d_prog,  g->d_extra, g->d_chains, g->d_members, g->d_child_ptr,
@@ -2383,9 +2393,13 @@ int breakdown_impl(const ks_graph* g, const ks_scenarios_desc* sc, const int64_t
   if (g->device < 0) fail(KS_ERR_NO_DEVICE, "graph was compiled without a device");
   const int S = sc->n_scenarios;
   if (S <= 0) fail(KS_ERR_INVALID, "n_scenarios must be positive");
-  if (!g->bd_ok)
+  const bool sched = bd->schedule != nullptr;
+  if (!g->bd_ok && !sched)
     fail(KS_ERR_UNSUPPORTED,
-         "batched breakdown needs a lane-chained graph (at most one permutable chain per lane)");
+         "batched breakdown needs a lane-chained graph (at most one permutable chain per lane) "
+         "or the list scheduler's dispatch order (ks_breakdown_desc.schedule)");
+  if (sched && g->n_chains > 0)
+    fail(KS_ERR_UNSUPPORTED, "permutable chains run on the max-plus path (no dispatch order)");
   if (g->L > 32) fail(KS_ERR_UNSUPPORTED, "batched breakdown supports at most 32 lanes");
   if (!g->gap_nonneg) fail(KS_ERR_UNSUPPORTED, "batched breakdown needs non-negative gaps");
   if (!bd->row_class) fail(KS_ERR_INVALID, "row_class is required");
@@ -2404,8 +2418,8 @@ int breakdown_impl(const ks_graph* g, const ks_scenarios_desc* sc, const int64_t
   p.L = g->L;
   p.S = S;
   p.n_chains = g->n_chains;
-  p.lane_ptr = g->d_bd_ptr;
-  p.lane_rows = g->d_bd_rows;
+  p.lane_ptr = sched ? g->d_bd_all_ptr : g->d_bd_ptr;
+  p.lane_rows = sched ? nullptr : g->d_bd_rows;
   p.lane_chain = g->d_bd_lane_chain;
   p.chains = g->d_bd_chains;
   p.member_rows = g->d_bd_member_rows;
@@ -2453,6 +2467,15 @@ int breakdown_impl(const ks_graph* g, const ks_scenarios_desc* sc, const int64_t
     p.row_layer = T.up(bd->row_layer, (size_t)g->n);
     p.layer_busy = reinterpret_cast<long long*>(layer_busy);
     p.n_layers = bd->n_layers;
+  }
+  if (sched && g->n > 0) {
+    // per-scenario lane sequences: the dispatch order split by lane (a lane
+    // runs one task at a time, lane_progress = finish + gap, sim.py:128, so
+    // each lane's intervals are sorted and disjoint in dispatch order)
+    int* srows = T.scratch<int>((size_t)g->n * S);
+    CUDA_TRY(launch_bd_sched_rows(bd->schedule, g->d_lane, g->d_bd_all_ptr, g->n, g->L, S, srows,
+                                  stream));
+    p.srows = srows;
   }
   if (g->n > 0) CUDA_TRY(launch_breakdown(p, stream));
   return KS_OK;

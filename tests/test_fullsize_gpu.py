@@ -133,3 +133,29 @@ def test_config4_bench_variant_vs_oracle():
     cols = [0, 1, 18_945, S // 2 + 1, S - 1]
     assert bench.oracle_check(w, fz, dense, start, ms, lb, cols) == cols
     check_recurrence_device(fz, dense, start, ms, lb)
+
+
+def test_config1_full_baseline_and_amp():
+    """Config 1 at its bench size: the ~10k-task ResNet-50-like iteration,
+    baseline + AMP (whatif_amp, scenarios.py:141-149) in one launch; every
+    start time, makespan and lane busy of both scenarios against the oracle
+    on the reference-equivalent transformed graph."""
+    from paper_2006_03318_b200.scenarios import whatif_amp
+    from paper_2006_03318_b200.transform import Selector
+
+    w = W.resnet50_trace()
+    g = w.graph
+    amp = whatif_amp(g)
+    scen = [[], [(Selector.from_object(x["selector"]), x["factor"]) for x in amp.steps]]
+    group_of, ptr, steps = compile_scale_sweep(g, scen)
+    fz = FrozenGraph.from_graph(g, group_of=group_of)
+    assert fz.n >= 9_000
+    res = simulate_batch(fz, ScenarioTable(n_scenarios=2, scale_ptr=ptr, scale=steps))
+    amp_graph = apply_pipeline(g, amp)
+    for s, h in enumerate((g, amp_graph)):
+        st, ms, lb, _ = OracleGraph.from_graph(h).simulate("default")
+        assert res.makespan[s] == ms, s
+        assert res.start_of(s) == st, s
+        assert {str(k): v for k, v in res.lane_busy_of(s).items()} == \
+            {str(k): v for k, v in lb.items()}, s
+    assert res.makespan[1] < res.makespan[0]

@@ -70,10 +70,79 @@ def test_set_duration_scale_interplay(golden):
     assert got == want
 
 
-def test_insert_pipelines_fall_back_pointwise(golden):
+INSERTS = {"distributed", "p3", "blueconnect", "vdnn", "gist", "dgc"}
+
+
+def test_insert_generators_match_reference_reports(golden):
+    """The insert / list-scheduled generators (scenarios.py:191-470) as
+    scenario tables: every golden report of p3, blueconnect, vdnn, gist, dgc
+    and distributed, one table per structure (batch.structure_key)."""
+    from paper_2006_03318_b200.batch import structure_key
+
     docs = {c["name"]: c["doc"] for c in golden["cases"]}
-    a = Analysis.from_text(json.dumps(docs["distributed_2"]))
-    params = [{"workers": 4, "bandwidth_gbps": b} for b in (10, 20)]
-    with pytest.raises(Unsupported):
-        compile_pipelines(a.graph, [a.pipeline_for("distributed", p) for p in params])
-    assert a.whatif_batch("distributed", params) == [a.whatif("distributed", p) for p in params]
+    by_case: dict = {}
+    for rec in golden["whatif"]:
+        if rec["scenario"] in INSERTS and "report" in rec:
+            by_case.setdefault((rec["case"], rec["scenario"]), []).append(rec)
+    n, seen = 0, set()
+    for (case, scen), recs in by_case.items():
+        a = Analysis.from_text(json.dumps(docs[case]))
+        pipes = [a.pipeline_for(scen, r["params"]) for r in recs]
+        groups: dict = {}
+        for p in pipes:
+            groups.setdefault(structure_key(p), []).append(p)
+        for ps in groups.values():
+            fz, table = compile_pipelines(a.graph, ps)  # no per-point fallback
+            seen.add((scen, fz.chained))
+        got = a.whatif_batch(scen, [r["params"] for r in recs])
+        for g, r in zip(got, recs):
+            assert {k: g[k] for k in KEYS} == r["report"], (case, scen, r["params"])
+            n += 1
+    assert n >= 15
+    assert {s for s, _c in seen} == INSERTS
+    assert (("p3", False) in seen) and (("distributed", True) in seen)
+
+
+@pytest.mark.parametrize("scen,case,param,values,fixed", [
+    ("p3", "p3", "bandwidth_gbps", [1, 2, 8, 25, 100],
+     {"layer_gradient_bytes": {"conv1": 1000, "fc2": 8000}, "workers": 2,
+      "slice_size_bytes": 3000, "n_servers": 2}),
+    ("dgc", "allreduce", "compression_ratio", ["1", "1/2", "1/4", "0.01", "3"], {}),
+    ("vdnn", "layered", "pcie_bandwidth_gbps", [1, 16, 128, "1/1000", 10**9], {}),
+    ("gist", "layered", "kernel_cost_ns", [0, 100, 5000, 12345], {"lossy": True}),
+    ("blueconnect", "allreduce", "bandwidth_gbps", [1, 8, 100],
+     {"factorization": "2,2", "workers": 4, "channels": 2}),
+    ("distributed", "distributed_2", "bandwidth_gbps", [1, 10, 20, 40, 400], {"workers": 4}),
+])
+def test_insert_sweeps_one_table_equal_pointwise(golden, scen, case, param, values, fixed):
+    """A parameter sweep of an insert generator is one structure (one table,
+    one launch sequence) and equals the reference composition point by point
+    (apply_pipeline + simulate + compute_breakdown)."""
+    from paper_2006_03318_b200.batch import structure_key
+
+    docs = {c["name"]: c["doc"] for c in golden["cases"]}
+    a = Analysis.from_text(json.dumps(docs[case]))
+    params = [{**fixed, param: v} for v in values]
+    assert len({structure_key(a.pipeline_for(scen, p)) for p in params}) == 1
+    got = a.whatif_batch(scen, params)
+    want = [a._whatif_pointwise(scen, p) for p in params]
+    assert got == want
+    assert len({g["predicted_makespan_ns"] for g in got}) > 1
+
+
+def test_whatif_is_the_batched_device_path(golden):
+    """Analysis.whatif (api.py:43-62) is a one-point whatif_batch: same
+    report as the reference composition, breakdowns computed by ks_breakdown."""
+    from paper_2006_03318_b200 import _native as N
+
+    docs = {c["name"]: c["doc"] for c in golden["cases"]}
+    for case, scen, params in (("gpu_bound", "amp", None), ("p3", "p3", {
+            "layer_gradient_bytes": {"conv1": 1000, "fc2": 8000}, "bandwidth_gbps": 8,
+            "workers": 2, "slice_size_bytes": 3000, "n_servers": 2}),
+            ("layered", "vdnn", None)):
+        a = Analysis.from_text(json.dumps(docs[case]))
+        a.baseline_breakdown()
+        l0 = N.launch_count()
+        got = a.whatif(scen, params)
+        assert N.launch_count() > l0
+        assert got == a._whatif_pointwise(scen, params)
