@@ -122,6 +122,9 @@ typedef struct {
   int32_t n_lane_slots_smem;   /* value slots in shared memory                  */
   int32_t n_lane_slots_global; /* value slots spilled to global memory          */
   int32_t n_lane_cuts;         /* rows where the segment-parallel path may cut  */
+  int32_t seg_chain_begin;     /* chain segment [begin, end) replayed numerically */
+  int32_t seg_chain_end;       /* between two scans (-1: none)                   */
+  int32_t n_carries;           /* values read only in it, live across its start */
 } ks_graph_info;
 
 /* Build the device-resident frozen graph on `device`.  Frozen row r holds the

@@ -59,7 +59,7 @@ class GraphInfo(C.Structure):
     _fields_ = [(n, C.c_int32) for n in (
         "n_tasks", "n_lanes", "n_edges_unique", "chained", "n_ordered", "n_slots",
         "n_slots_smem", "n_levels", "has_lanes", "n_lane_slots_smem", "n_lane_slots_global",
-        "n_lane_cuts")]
+        "n_lane_cuts", "seg_chain_begin", "seg_chain_end", "n_carries")]
 
 
 class ScaleStep(C.Structure):

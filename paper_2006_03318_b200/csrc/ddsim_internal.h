@@ -251,6 +251,11 @@ struct LaneSegParams {
   int nb;
   int pad;
   const long long* gapsum;
+  int kc;
+  int replay_only;
+  const int* carry_ptr;
+  const int* carry_gid;
+  int* carry_coef;
 };
 cudaError_t launch_maxplus_lanes_seg(const LaneParams& p, const LaneChainParams* cp,
                                      const int* dense32, int dkind, const std::vector<int>& codes,

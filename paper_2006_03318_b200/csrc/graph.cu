@@ -203,6 +203,12 @@ struct ks_graph {
   std::vector<int> lane_cuts;
   std::vector<long long> lane_wt_prefix;
   std::vector<long long> lane_gap_prefix;  // prefix sums of the records' gaps
+  // carries: global-slot values live across the cuts before the chain segment
+  // [seg_c0, seg_c1) (the one permutable chain's record and its neighbours,
+  // replayed numerically); the scan evaluates each carry from its producing
+  // segment's transfer coefficients (lanes_seg.cuh)
+  int seg_c0 = -1, seg_c1 = -1;
+  std::vector<int> carry_rows, carry_gid;  // producer row (ascending), global slot id
   bool lane_ready = false;      // some record has a ready floor
   LaneRec* d_lprog = nullptr;
   int* d_lside_off = nullptr;
@@ -1076,9 +1082,30 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
         for (int k = 1; k < d->chain_ptr[c + 1] - d->chain_ptr[c]; ++k) ekind[r0 + k] = 2;
       }
     }
+    // Chain members read every predecessor from a slot.  Among predecessors
+    // on one lane only the latest (highest row) matters: rel is non-decreasing
+    // along a lane when durations and gaps are >= 0 (gaps host-checked,
+    // durations device-checked: a negative one reruns the exact general
+    // kernel, which keeps every edge).
+    auto member_preds = [&](int m, hvec<int>& out) {
+      out.clear();
+      for (int q = pptr[m]; q < pptr[m + 1]; ++q) {
+        const int u = padj[q];
+        bool keep = true;
+        for (int& w : out)
+          if (d->lane[w] == d->lane[u]) {
+            if (g->row_of[u] > g->row_of[w]) w = u;
+            keep = false;
+            break;
+          }
+        if (keep) out.push_back(u);
+      }
+    };
+    hvec<int> mp;
     // which predecessor reads are lane heads at read time?
     hvec<int> head(L, -1);          // task id, or -2 - c after chain c
     hvec<int> far_use(n, -1);       // last slot read of each task value
+    hvec<int> near_use(n, INT32_MAX);  // first slot read
     hvec<unsigned> hmask(RE, 0);
     hvec<int> sp_ptr(RE + 1, 0), sp_list;  // slot-read predecessors per record (CSR)
     for (int r = 0; r < RE; ++r) {
@@ -1094,6 +1121,7 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
           } else {
             sp_list.push_back(u);
             far_use[u] = std::max(far_use[u], r);
+            near_use[u] = std::min(near_use[u], r);
           }
         }
         hmask[r] = mask;
@@ -1101,8 +1129,11 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
       } else if (ekind[r] == 1) {
         const int c = eid[r];
         for (int k = d->chain_ptr[c]; k < d->chain_ptr[c + 1]; ++k) {
-          const int m = d->chain_member[k];
-          for (int q = pptr[m]; q < pptr[m + 1]; ++q) far_use[padj[q]] = std::max(far_use[padj[q]], r);
+          member_preds(d->chain_member[k], mp);
+          for (int u : mp) {
+            far_use[u] = std::max(far_use[u], r);
+            near_use[u] = std::min(near_use[u], r);
+          }
         }
         head[ch_lane[c]] = -2 - c;
       }
@@ -1194,7 +1225,8 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
             memset(&md, 0, sizeof(md));
             md.gap = d->gap[m];
             md.pred_off = (int)lpreds.size();
-            for (int q = pptr[m]; q < pptr[m + 1]; ++q) lpreds.push_back(code_of(padj[q]));
+            member_preds(m, mp);
+            for (int u : mp) lpreds.push_back(code_of(u));
             md.npred = (int)lpreds.size() - md.pred_off;
             md.out = lslot[m] >= 0 ? code_of(m) : -1;
             if (d->ready_time && d->ready_time[m] != 0) any_ready = true;
@@ -1245,20 +1277,81 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     // slot value live across them (produced before b, read at or after b)
     // and not inside a chain's no-op rows
     std::vector<int> cuts;
+    std::vector<int> carry_rows, carry_gid;
+    int seg_c0 = -1, seg_c1 = -1;
     std::vector<long long> gpre(RE + 1, 0), gapre(RE + 1, 0);
     {
       hvec<int> delta(RE + 2, 0);
+      hvec<int> prod(n, -1);  // producer row of each value
       for (int r = 0; r < RE; ++r)
         for_values(r, [&](int v) {
+          prod[v] = r;
           if (far_use[v] > r) {
             delta[r + 1]++;
             delta[far_use[v] + 1]--;
           }
         });
-      int live = 0;
+      hvec<int> live_at(RE + 1, 0);  // values live across row boundary b
+      {
+        int live = 0;
+        for (int b = 0; b <= RE; ++b) {
+          live += delta[b];
+          live_at[b] = live;
+        }
+      }
+      // One permutable chain whose member predecessors live long (e.g. one
+      // AllReduce per gradient bucket, read at the end of the backward pass):
+      // the chain segment [c0, c1) is replayed numerically, and the values
+      // live across c0 (all in global slots, all read inside the chain
+      // segment) become carries, so the backward pass can still be cut.
+      int rc = -1;
+      for (int r = 0; r < RE && NC == 1; ++r)
+        if (ekind[r] == 1) rc = r;
+      if (rc >= 0) {
+        int c1 = RE;
+        for (int b = (rc / 16 + 1) * 16; b < RE; b += 16)
+          if (live_at[b] == 0 && ekind[b] != 2) {
+            c1 = b;
+            break;
+          }
+        for (int c0 = rc / 16 * 16; c0 >= 16 && c0 >= rc / 16 * 16 - 64 * 16 && seg_c0 < 0;
+             c0 -= 16) {
+          if (ekind[c0] == 2) continue;
+          bool ok = true;
+          std::vector<int> cr;
+          for (int v = 0; v < n && ok; ++v) {
+            if (far_use[v] < 0) continue;
+            const bool across = prod[v] < c0 && far_use[v] >= c0;
+            if (across) {
+              if (!lglob[v] || near_use[v] < c0 || far_use[v] >= c1) ok = false;
+              else cr.push_back(v);
+            } else if (lglob[v] && !(prod[v] >= c0 && far_use[v] < c1)) {
+              // a global value outside the chain segment: no transfer form
+              ok = false;
+            }
+          }
+          if (ok && !cr.empty()) {
+            seg_c0 = c0;
+            seg_c1 = c1;
+            std::sort(cr.begin(), cr.end(), [&](int a, int b) { return prod[a] < prod[b]; });
+            for (int v : cr) {
+              carry_rows.push_back(prod[v]);
+              carry_gid.push_back(lslot[v]);
+            }
+          }
+        }
+      }
+      hvec<int> cdelta(RE + 2, 0);  // carries live across b
+      for (size_t q = 0; q < carry_rows.size(); ++q) {
+        cdelta[carry_rows[q] + 1]++;
+        cdelta[seg_c0 + 1]--;  // every carry is live across c0 and read at or after it
+      }
+      int clive = 0;
       for (int b = 0; b < RE; ++b) {
-        live += delta[b];
-        if (b > 0 && b % 16 == 0 && live == 0 && ekind[b] != 2) cuts.push_back(b);
+        clive += cdelta[b];
+        if (b == 0 || b % 16 != 0 || ekind[b] == 2) continue;
+        if (seg_c0 >= 0 && b > seg_c0 && b < seg_c1) continue;
+        if (live_at[b] == 0 || (seg_c0 >= 0 && b <= seg_c0 && live_at[b] == clive)) cuts.push_back(b);
       }
       auto wt = [&](int t) { return std::max<long long>(d->duration[t], 0) + d->gap[t]; };
       for (int r = 0; r < RE; ++r) {
@@ -1283,6 +1376,10 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
     // chain members with ready floors stay on the general kernel
     if (ns + ngl < 32000 && !(NC > 0 && any_ready)) {
       g->lane_cuts = std::move(cuts);
+      g->seg_c0 = seg_c0;
+      g->seg_c1 = seg_c1;
+      g->carry_rows = std::move(carry_rows);
+      g->carry_gid = std::move(carry_gid);
       g->lane_wt_prefix = std::move(gpre);
       g->lane_gap_prefix = std::move(gapre);
       g->lane_ready = any_ready;
@@ -1549,7 +1646,8 @@ namespace {
 // (no live slot value), near K evenly spaced targets.
 std::vector<int> pick_segments(const ks_graph* g, int S, int nsm) {
   std::vector<int> rows;
-  if (getenv("DDSIM_NO_SEG") || !g->has_lanes || g->lkglob > 0 || g->lane_ready || g->L < 1 ||
+  if (getenv("DDSIM_NO_SEG") || !g->has_lanes || (g->lkglob > 0 && g->seg_c0 < 0) ||
+      g->lane_ready || g->L < 1 ||
       g->L > 4 || g->lane_cuts.empty() || g->ln_rec < 512)
     return rows;
   // the single-pass kernel reaches the memory roofline once ~256 threads per
@@ -1582,9 +1680,23 @@ std::vector<int> pick_segments(const ks_graph* g, int S, int nsm) {
     if (best > rows.back()) rows.push_back(best);
   }
   rows.push_back(g->ln_rec);
+  if (g->seg_c0 >= 0) {
+    // the chain segment [c0, c1) is one segment
+    std::vector<int> r2;
+    for (int b : rows)
+      if (b <= g->seg_c0 || b >= g->seg_c1) r2.push_back(b);
+    r2.push_back(g->seg_c0);
+    if (g->seg_c1 < g->ln_rec) r2.push_back(g->seg_c1);
+    std::sort(r2.begin(), r2.end());
+    r2.erase(std::unique(r2.begin(), r2.end()), r2.end());
+    rows.swap(r2);
+  }
   // coefficient entries are int32: a segment's base weights must leave room
+  // (the chain segment has no transfer)
   for (size_t k = 0; k + 1 < rows.size(); ++k)
-    if (g->lane_wt_prefix[rows[k + 1]] - g->lane_wt_prefix[rows[k]] >= (1LL << 29)) return {};
+    if (rows[k] != g->seg_c0 &&
+        g->lane_wt_prefix[rows[k + 1]] - g->lane_wt_prefix[rows[k]] >= (1LL << 29))
+      return {};
   if (rows.size() < 3) return {};
   return rows;
 }
@@ -1747,10 +1859,28 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
       }
       sg.nb = (int)(sg.s_pad / BDs);
       sg.state = T.scratch<long long>((size_t)sg.K * sg.LN * sg.s_pad);
+      sg.kc = -1;
+      sg.replay_only = -1;
+      for (int k = 0; k < sg.K && g->seg_c0 >= 0; ++k)
+        if (seg[k] == g->seg_c0) sg.kc = k;
+      if (g->seg_c0 >= 0 && sg.kc < 0) fail(KS_ERR_INVALID, "segment cuts miss the chain segment");
+      if (sg.kc >= 0 && !g->carry_rows.empty()) {
+        // carries: producing segment of each (rows ascending), their global
+        // slots, and their transfer coefficients [kglob][LN][s_pad]
+        std::vector<int> cptr(sg.K + 1, 0);
+        for (int r : g->carry_rows) {
+          const int k = (int)(std::upper_bound(seg.begin(), seg.end(), r) - seg.begin()) - 1;
+          cptr[k + 1]++;
+        }
+        for (int k = 0; k < sg.K; ++k) cptr[k + 1] += cptr[k];
+        sg.carry_ptr = T.up(cptr.data(), cptr.size());
+        sg.carry_gid = T.up(g->carry_gid.data(), g->carry_gid.size());
+        sg.carry_coef = T.scratch<int>((size_t)p.kglob * sg.LN * sg.s_pad);
+      }
       // fused single pass (look-back) only on request: its publish chain costs
       // ~2.5 us per segment hop (config 2, K = 92: 0.35 vs 0.17 ms for the
       // transfer / scan / replay kernels; config 4 at 8,192: 2.68 vs 2.58 ms)
-      if (getenv("DDSIM_SEG_FUSED") != nullptr) {
+      if (getenv("DDSIM_SEG_FUSED") != nullptr && sg.kc < 0) {
         sg.ticket = T.scratch<int>(1 + (size_t)sg.K * sg.nb);
         sg.flags = sg.ticket + 1;
         CUDA_TRY(cudaMemsetAsync(sg.ticket, 0, sizeof(int) * (1 + (size_t)sg.K * sg.nb), stream));
@@ -1759,6 +1889,7 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
       }
       LaneParams ps = p;
       ps.s_pad = sg.s_pad;
+      if (ps.kglob > 0) ps.gslots = T.scratch<long long>((size_t)ps.kglob * sg.s_pad);
       if (ps.makespan) CUDA_TRY(cudaMemsetAsync(ps.makespan, 0, sizeof(long long) * S, stream));
       if (ps.lane_busy)
         CUDA_TRY(cudaMemsetAsync(ps.lane_busy, 0, sizeof(long long) * (size_t)S * g->L, stream));
@@ -2051,6 +2182,9 @@ int ks_graph_get_info(const ks_graph* g, ks_graph_info* info) {
   info->n_lane_slots_smem = g->lksm;
   info->n_lane_slots_global = g->lkglob;
   info->n_lane_cuts = (int)g->lane_cuts.size();
+  info->seg_chain_begin = g->seg_c0;
+  info->seg_chain_end = g->seg_c1;
+  info->n_carries = (int)g->carry_rows.size();
   return KS_OK;
 }
 

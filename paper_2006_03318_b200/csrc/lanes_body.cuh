@@ -86,6 +86,19 @@ struct SegParams {
   int nb;                    // scenario blocks
   int pad;
   const long long* gapsum;   // [K] gaps of each segment's records (host)
+  // Chain segment kc (-1: none): one permutable chain whose member
+  // predecessors live across cuts.  It has no transfer: its replay runs
+  // between two scans and exports its output lane heads to state[kc + 1].
+  // The values live across its first row ("carries", global slots) are
+  // produced in earlier segments; the transfer pass writes their
+  // coefficients, the scan their values (gslots) before the chain replay.
+  int kc;
+  int replay_only;           // replay launch: >= 0 replays only that segment,
+                             // -1 every segment except kc
+  const int* carry_ptr;      // [K+1] carries produced per segment
+  const int* carry_gid;      // their global slot ids
+  int* carry_coef;           // [kglob][LN][s_pad] coefficients on the producing
+                             // segment's input lane heads (< 0 = none)
 };
 
 // CUtensorMap-compatible opaque kernel parameter (128 B, 64 B aligned)
@@ -556,7 +569,12 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
       long long wsum = sgp->gapsum[seg_k];
 #pragma unroll
       for (int q = 0; q < NLANE; ++q) wsum += S.lb[q][0];
-      if ((neg < 0 || wsum >= (1LL << 30)) && p.neg_flag) atomicOr(p.neg_flag, 1);
+      if ((neg < 0 || (wsum >= (1LL << 30) && seg_k != sgp->kc)) && p.neg_flag)
+        atomicOr(p.neg_flag, 1);
+      if (seg_k == sgp->kc && seg_k + 1 < sgp->K)
+#pragma unroll
+        for (int l = 0; l < NLANE; ++l)
+          if (l < sgp->LN) sgp->state[((long long)(seg_k + 1) * sgp->LN + l) * sgp->s_pad + s] = S.lv[l][0];
 #pragma unroll
       for (int i = 0; i < V; ++i) {
         const long long m = i == 0 ? ms0 : ms1;  // >= 0 on this path

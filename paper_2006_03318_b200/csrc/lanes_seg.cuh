@@ -238,6 +238,13 @@ __device__ __forceinline__ void sym_pass(const Tmap* tmap, const Params& p, cons
         int y[4];
         sym_get<LN>(Y, (int)(h & 3), y);
         sym_slot_st(slot_s + (unsigned)((w << 16) >> 16) * slot_pitch + col, y);
+      } else if ((rare & R_OUT_GLOBAL) && act) {
+        // a carry (read only in the chain segment): its coefficients
+        int y[4];
+        sym_get<LN>(Y, (int)(h & 3), y);
+        int* o = sg.carry_coef + (long long)((int)(w << 16) >> 16) * LN * sg.s_pad + s;
+#pragma unroll
+        for (int q = 0; q < LN; ++q) o[(long long)q * sg.s_pad] = y[q];
       }
     };
 #ifdef DDSIM_UNROLL
@@ -265,6 +272,7 @@ __device__ __forceinline__ void sym_pass(const Tmap* tmap, const Params& p, cons
 template <int DK, int LN, bool CH>
 __device__ __forceinline__ void sym_body(const Tmap* tmap, const Params& p, const SegParams& sg,
                                          const ChainParams* cpp) {
+  if ((int)blockIdx.y == sg.kc) return;  // the chain segment is replayed numerically
   int coef[LN][LN];
   sym_pass<DK, LN, CH>(tmap, p, sg, cpp, (int)blockIdx.y, (int)blockIdx.x, coef);
   const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
@@ -281,13 +289,15 @@ __device__ __forceinline__ void sym_body(const Tmap* tmap, const Params& p, cons
 template <int DK, int LN, bool CH>
 __device__ __forceinline__ void replay_body(const Tmap* tmap, const Params& p,
                                             const SegParams& sg, const ChainParams* cpp) {
+  const int k = sg.replay_only >= 0 ? sg.replay_only : (int)blockIdx.y;
+  if (sg.replay_only < 0 && k == sg.kc) return;  // replayed before the second scan
   long long init[NLANE] = {0, 0, 0, 0};
   const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (blockIdx.y > 0 && s < p.S)
+  if (k > 0 && s < p.S)
 #pragma unroll
     for (int l = 0; l < LN; ++l)
-      init[l] = sg.state[((long long)blockIdx.y * LN + l) * sg.s_pad + s];
-  lanes_body<DK, 1, CH, true>(tmap, p, cpp, &sg, (int)blockIdx.y, (int)blockIdx.x, init);
+      init[l] = sg.state[((long long)k * LN + l) * sg.s_pad + s];
+  lanes_body<DK, 1, CH, true>(tmap, p, cpp, &sg, k, (int)blockIdx.x, init);
 }
 
 // Fused single pass with decoupled look-back: CTAs take (segment, block) work

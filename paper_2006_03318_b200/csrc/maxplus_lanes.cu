@@ -174,10 +174,14 @@ static cudaError_t encode_lanes_tmap(CUtensorMap* tmap, const LaneParams& p, con
 }
 
 // Compose the segment transfer matrices per scenario (one thread each):
-// state[k+1] = trans[k] (x) state[k] in (max,+), state[0] = 0.  All values are
-// >= 0 on this path, so 0 is the identity of max; entries < 0 mean "no path".
+// state[k+1] = trans[k] (x) state[k] in (max,+), state[0] = 0, for segments
+// k in [k_from, k_to) (the state of k_from is read unless k_from == 0).  All
+// values are >= 0 on this path, so 0 is the identity of max; entries < 0 mean
+// "no path".  Carries produced in segment k (values read only in the chain
+// segment) are evaluated from their coefficients on state[k] into gslots.
 template <int LN>
-__global__ void __launch_bounds__(128) seg_scan_kernel(const LaneSegParams sg, int S) {
+__global__ void __launch_bounds__(128) seg_scan_kernel(const LaneSegParams sg, int S, int k_from,
+                                                       int k_to, long long* gslots) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= S) return;
   constexpr int E = LN * LN;
@@ -185,21 +189,34 @@ __global__ void __launch_bounds__(128) seg_scan_kernel(const LaneSegParams sg, i
   const long long sp = sg.s_pad;
   long long st[LN];
 #pragma unroll
-  for (int j = 0; j < LN; ++j) st[j] = 0;
+  for (int j = 0; j < LN; ++j)
+    st[j] = k_from == 0 ? 0 : sg.state[((long long)k_from * LN + j) * sp + s];
   // the loads do not depend on the state (only the composition chain does):
   // D segments' coefficients are in flight together
-  for (int k0 = 0; k0 + 1 < sg.K; k0 += D) {
+  for (int k0 = k_from; k0 < k_to; k0 += D) {
     int a[D][E];
 #pragma unroll
     for (int q = 0; q < D; ++q)
-      if (k0 + q + 1 < sg.K) {
+      if (k0 + q < k_to) {
         const int* tk = sg.trans + (long long)(k0 + q) * E * sp + s;
 #pragma unroll
         for (int e = 0; e < E; ++e) a[q][e] = tk[(long long)e * sp];
       }
 #pragma unroll
     for (int q = 0; q < D; ++q)
-      if (k0 + q + 1 < sg.K) {
+      if (k0 + q < k_to) {
+        if (sg.carry_ptr != nullptr)
+          for (int c = sg.carry_ptr[k0 + q]; c < sg.carry_ptr[k0 + q + 1]; ++c) {
+            const int gid = sg.carry_gid[c];
+            const int* cf = sg.carry_coef + (long long)gid * LN * sp + s;
+            long long v = 0;
+#pragma unroll
+            for (int i = 0; i < LN; ++i) {
+              const int x = cf[(long long)i * sp];
+              if (x >= 0) v = max(v, (long long)x + st[i]);
+            }
+            gslots[(long long)gid * sp + s] = v;
+          }
         long long nx[LN];
 #pragma unroll
         for (int j = 0; j < LN; ++j) {
@@ -216,6 +233,20 @@ __global__ void __launch_bounds__(128) seg_scan_kernel(const LaneSegParams sg, i
         }
       }
   }
+}
+
+static cudaError_t launch_seg_scan(const LaneSegParams& sg, int S, int k_from, int k_to,
+                                   long long* gslots, cudaStream_t stream) {
+  if (k_to <= k_from) return cudaSuccess;
+  const int gs = (S + 127) / 128;
+  switch (sg.LN) {
+    case 1: seg_scan_kernel<1><<<gs, 128, 0, stream>>>(sg, S, k_from, k_to, gslots); break;
+    case 2: seg_scan_kernel<2><<<gs, 128, 0, stream>>>(sg, S, k_from, k_to, gslots); break;
+    case 3: seg_scan_kernel<3><<<gs, 128, 0, stream>>>(sg, S, k_from, k_to, gslots); break;
+    default: seg_scan_kernel<4><<<gs, 128, 0, stream>>>(sg, S, k_from, k_to, gslots); break;
+  }
+  note_launch();
+  return cudaGetLastError();
 }
 
 // Segment-parallel lanes path (small S): transfer, scan, replay.  The caller
@@ -241,15 +272,20 @@ cudaError_t launch_maxplus_lanes_seg(const LaneParams& p, const LaneChainParams*
     e = launch_lanes_seg_jit(1, p, cp, &tmap, dkind, sg.LN, codes, &sg, gx, sg.K - 1, BD, smem_t,
                              stream);
     if (e != cudaSuccess) return e;
-    const int gs = (p.S + 127) / 128;
-    switch (sg.LN) {
-      case 1: seg_scan_kernel<1><<<gs, 128, 0, stream>>>(sg, p.S); break;
-      case 2: seg_scan_kernel<2><<<gs, 128, 0, stream>>>(sg, p.S); break;
-      case 3: seg_scan_kernel<3><<<gs, 128, 0, stream>>>(sg, p.S); break;
-      default: seg_scan_kernel<4><<<gs, 128, 0, stream>>>(sg, p.S); break;
-    }
-    note_launch();
-    if ((e = cudaGetLastError()) != cudaSuccess) return e;
+  }
+  if (sg.kc < 0) {
+    if ((e = launch_seg_scan(sg, p.S, 0, sg.K - 1, p.gslots, stream)) != cudaSuccess) return e;
+  } else {
+    // scan up to the chain segment (carries included), replay the chain
+    // segment (it exports its output lane heads), scan the rest
+    if ((e = launch_seg_scan(sg, p.S, 0, sg.kc, p.gslots, stream)) != cudaSuccess) return e;
+    LaneSegParams one = sg;
+    one.replay_only = sg.kc;
+    e = launch_lanes_seg_jit(0, p, cp, &tmap, dkind, sg.LN, codes, &one, gx, 1, BD, smem_r,
+                             stream);
+    if (e != cudaSuccess) return e;
+    e = launch_seg_scan(sg, p.S, sg.kc + 1, sg.K - 1, p.gslots, stream);
+    if (e != cudaSuccess) return e;
   }
   return launch_lanes_seg_jit(0, p, cp, &tmap, dkind, sg.LN, codes, &sg, gx, sg.K, BD, smem_r,
                               stream);

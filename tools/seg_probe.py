@@ -2,6 +2,7 @@
 
     python tools/seg_probe.py config4 8192 [16384 ...]   (jitter, device-resident)
     python tools/seg_probe.py config2                     (400 per-layer Shrink)
+    python tools/seg_probe.py config3                     (4,000 bucket-order x network)
 
 Each line: workload, S, mode (env), ms per launch (CUDA events, 10 launches
 after 3 warm-up), G updates/s, and whether the result equals the other mode.
@@ -72,6 +73,9 @@ def main():
         fz = FrozenGraph.from_graph(w.graph, group_of=group_of)
         cases.append(("config2", len(scen), fz,
                       ScenarioTable(n_scenarios=len(scen), scale_ptr=ptr, scale=steps)))
+    elif what == "config3":
+        fz, table, _g, _i = bench.build_config(3, 0)
+        cases.append(("config3", table.n_scenarios, fz, table))
     for name, S, fz, table in cases:
         out = {}
         for mode, env in MODES.items():
