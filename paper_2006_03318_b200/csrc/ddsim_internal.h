@@ -226,9 +226,26 @@ cudaError_t launch_maxplus(const MaxplusParams& p, const int* dense32,
                            cudaStream_t stream);
 cudaError_t launch_maxplus_dense(const DenseParams& p, const int* dense32, int dkind,
                                  cudaStream_t stream);
+// Derived durations for the lanes kernels (dkind 0; mirrors
+// ddsim_lanes::DerivedParams): per-row base / group / override row, the
+// override table and the scale programs.
+struct LaneRowDur {
+  long long base;
+  unsigned group;
+  int ovr;
+};
+struct LaneDerivedParams {
+  const LaneRowDur* rows;
+  const long long* ovr;
+  const int* scale_ptr;
+  const ScaleStepDev* scale;
+};
+cudaError_t launch_build_rowdur(const long long* base, const unsigned* group, const int* ovr_map,
+                                int n, LaneRowDur* out, cudaStream_t st);
 cudaError_t launch_maxplus_lanes(const LaneParams& p, const LaneChainParams* cp, const int* dense32,
                                  int dkind,
-                                 const std::vector<int>* codes, cudaStream_t stream);
+                                 const std::vector<int>* codes, cudaStream_t stream,
+                                 const LaneDerivedParams* dp = nullptr);
 // lane_busy[s][l] = sum of the durations of lane l's present rows (lanes
 // program order); the branch-free lanes handler leaves it to this pass.
 cudaError_t launch_lanes_busy(const LaneParams& p, const int* dense32, bool chains,
@@ -236,8 +253,8 @@ cudaError_t launch_lanes_busy(const LaneParams& p, const int* dense32, bool chai
 cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const LaneChainParams* cp,
                                      const int* dense32, const void* tmap128, int dkind, int V,
                                      const std::vector<int>& codes, int grid, int BD, size_t smem,
-                                     cudaStream_t stream);
-int maxplus_lanes_vec(int S);
+                                     cudaStream_t stream, const LaneDerivedParams* dp = nullptr);
+int maxplus_lanes_vec(int S, int dkind = 1);
 // Segment-parallel lanes path (mirrors ddsim_lanes::SegParams)
 struct LaneSegParams {
   const int* cuts;
@@ -259,11 +276,13 @@ struct LaneSegParams {
 };
 cudaError_t launch_maxplus_lanes_seg(const LaneParams& p, const LaneChainParams* cp,
                                      const int* dense32, int dkind, const std::vector<int>& codes,
-                                     const LaneSegParams& sg, int BD, cudaStream_t stream);
+                                     const LaneSegParams& sg, int BD, cudaStream_t stream,
+                                     const LaneDerivedParams* dp = nullptr);
 cudaError_t launch_lanes_seg_jit(int mode, const LaneParams& p, const LaneChainParams* cp,
                                  const void* tmap128, int dkind, int LN,
                                  const std::vector<int>& codes, const void* segp, int gx, int gy,
-                                 int BD, size_t smem, cudaStream_t stream);
+                                 int BD, size_t smem, cudaStream_t stream,
+                                 const LaneDerivedParams* dp = nullptr);
 bool jit_available();
 cudaError_t launch_expand_durations(const long long* base, const unsigned* group,
                                     const int* ovr_map, const long long* ovr, const int* scale_ptr,
@@ -308,7 +327,7 @@ cudaError_t launch_bd_sched_rows(const int* schedule, const int* row_lane, const
                                  int n, int L, int S, int* srows, cudaStream_t stream);
 
 const char* jit_log();
-int maxplus_lanes_block_dim(int S, int num_sms);
+int maxplus_lanes_block_dim(int S, int num_sms, int dkind = 1);
 cudaError_t launch_listsched(const ListParams& p, cudaStream_t stream);
 cudaError_t launch_toposort_lanes(int N, int L, const int* lane_ptr, const int* lane_rows,
                                   const int* child_ptr, const int* child, const int* indeg,

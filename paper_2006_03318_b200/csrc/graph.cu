@@ -1738,9 +1738,21 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
   // derived path is used) and run the lanes kernel on it.
   ks_scenarios_desc expanded;
   const ks_scenarios_desc* orig_sc = sc;
-  const bool expand = use_max && !dense && !T.has_remove && g->has_lanes && g->n_rec > 0 &&
-                      (long long)g->n * S * 8 <= (8LL << 30) && getenv("DDSIM_NO_EXPAND") == nullptr &&
-                      getenv("DDSIM_NO_LANES") == nullptr;
+  // Or the lanes kernels derive them per record (NVRTC kernels only): no
+  // duration matrix in HBM.  Preferred unless the matrix would stay in L2 and
+  // scale programs make the per-record derivation cost instructions on the
+  // latency-bound path (measured: config 3, overrides only, 4,000 x 30k:
+  // 2.43 -> 1.28 ms; config 2, scale programs, 401 x 30k (95 MB): 0.18 ms
+  // expanded vs 0.28 ms derived).
+  const bool l2_sized = (long long)g->n * S * 8 <= (96LL << 20);
+  const bool derive = use_max && !dense && !T.has_remove && g->has_lanes && g->n_rec > 0 &&
+                      (!(sc->scale_ptr && l2_sized) || getenv("DDSIM_FORCE_DERIVED") != nullptr) &&
+                      getenv("DDSIM_NO_DERIVED") == nullptr && getenv("DDSIM_NO_LANES") == nullptr &&
+                      getenv("DDSIM_NO_EXPAND") == nullptr && !g->lane_codes.empty() &&
+                      g->lane_codes.size() <= 32 && jit_available();
+  const bool expand = !derive && use_max && !dense && !T.has_remove && g->has_lanes &&
+                      g->n_rec > 0 && (long long)g->n * S * 8 <= (8LL << 30) &&
+                      getenv("DDSIM_NO_EXPAND") == nullptr && getenv("DDSIM_NO_LANES") == nullptr;
   if (expand) {
     const long long eld = (S + 1) / 2 * 2;  // TMA: 16 B row pitch
     long long* buf = T.scratch<long long>((size_t)g->n * eld);
@@ -1793,9 +1805,9 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
       (sc->dense_kind == 1 ? sc->dense_ld % 4 == 0 : sc->dense_ld % 2 == 0);
   // permutable chains run on the lanes path only for derived (expanded)
   // durations: the exact fallback for them is the general kernel's derived mode
-  const bool lanes_ok = use_max && dense_now && tma_ok && g->has_lanes && sc->n_overrides == 0 &&
-                        !sc->scale_ptr && (g->n_chains == 0 || expand) &&
-                        getenv("DDSIM_NO_LANES") == nullptr;
+  const bool lanes_ok = use_max && g->has_lanes && getenv("DDSIM_NO_LANES") == nullptr &&
+                        (derive || (dense_now && tma_ok && sc->n_overrides == 0 && !sc->scale_ptr &&
+                                    (g->n_chains == 0 || expand)));
   if (lanes_ok) {
     LaneParams p;
     memset(&p, 0, sizeof(p));
@@ -1808,11 +1820,21 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
     p.kglob = g->lkglob;
     p.S = S;
     p.L = g->L;
-    const int dk = sc->dense_kind == 1 ? 1 : 2;
+    const int dk = derive ? 0 : (sc->dense_kind == 1 ? 1 : 2);
     if (dk == 1 && (reinterpret_cast<uintptr_t>(sc->dense) % 16 != 0 || sc->dense_ld % 4 != 0))
       fail(KS_ERR_INVALID, "int32 dense durations need 16B alignment and dense_ld % 4 == 0");
     if (dk == 2) p.dense64 = reinterpret_cast<const long long*>(sc->dense);
-    p.dense_ld = sc->dense_ld;
+    p.dense_ld = dk == 0 ? 0 : sc->dense_ld;
+    LaneDerivedParams dpv;
+    memset(&dpv, 0, sizeof(dpv));
+    if (dk == 0) {
+      LaneRowDur* rd = T.scratch<LaneRowDur>((size_t)g->n);
+      CUDA_TRY(launch_build_rowdur(g->d_dur, g->d_group, T.ovr_map, g->n, rd, stream));
+      dpv.rows = rd;
+      dpv.ovr = T.ovr;
+      dpv.scale_ptr = T.scale_ptr;
+      dpv.scale = T.scale;
+    }
     LaneChainParams cp;
     memset(&cp, 0, sizeof(cp));
     if (g->n_chains > 0) {
@@ -1831,8 +1853,8 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
     p.lane_busy = reinterpret_cast<long long*>(out->lane_busy);
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device);
-    const int BD = maxplus_lanes_block_dim(S, nsm);
-    const int LV = maxplus_lanes_vec(S);
+    const int BD = maxplus_lanes_block_dim(S, nsm, dk);
+    const int LV = maxplus_lanes_vec(S, dk);
     p.s_pad = (long long)((S + LV * BD - 1) / (LV * BD)) * LV * BD;
     if (p.kglob > 0) p.gslots = T.scratch<long long>((size_t)p.kglob * p.s_pad);
     int* flag = T.scratch<int>(1);
@@ -1894,7 +1916,8 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
       if (ps.lane_busy)
         CUDA_TRY(cudaMemsetAsync(ps.lane_busy, 0, sizeof(long long) * (size_t)S * g->L, stream));
       const cudaError_t e = launch_maxplus_lanes_seg(ps, g->n_chains > 0 ? &cp : nullptr, d32, dk,
-                                                     g->lane_codes, sg, BDs, stream);
+                                                     g->lane_codes, sg, BDs, stream,
+                                                     dk == 0 ? &dpv : nullptr);
       if (e == cudaSuccess) {
         seg_done = true;
       } else if (e != cudaErrorNotSupported) {
@@ -1903,7 +1926,7 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
     }
     if (!seg_done)
       CUDA_TRY(launch_maxplus_lanes(p, g->n_chains > 0 ? &cp : nullptr, d32, dk, &g->lane_codes,
-                                    stream));
+                                    stream, dk == 0 ? &dpv : nullptr));
     MaxplusParams q;
     memset(&q, 0, sizeof(q));
     q.prog = g->d_prog;
@@ -1921,7 +1944,7 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
     q.makespan = p.makespan;
     q.lane_busy = p.lane_busy;
     q.run_if = flag;
-    if (g->n_chains > 0) {  // exact rerun in derived mode (chains + original tables)
+    if (g->n_chains > 0 || dk == 0) {  // exact rerun in derived mode (original tables)
       fill_general(q);
       q.dense_kind = 0;
       q.dense64 = nullptr;

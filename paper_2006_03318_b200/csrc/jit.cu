@@ -134,9 +134,13 @@ std::string make_source(const std::vector<int>& codes, int dk, int V, bool dyn, 
   src += disp + body;
   src += "\nextern \"C\" __global__ void __launch_bounds__(256) ddsim_lanes_jit("
          "const __grid_constant__ ddsim_lanes::Tmap tmap, const ddsim_lanes::Params p" +
-         std::string(ch ? ", const __grid_constant__ ddsim_lanes::ChainParams cp" : "") + ") {\n"
-         "  ddsim_lanes::lanes_body<" + std::to_string(dk) + ", " + std::to_string(V) +
-         (ch ? ", true>(&tmap, p, &cp);\n}\n" : ", false>(&tmap, p);\n}\n");
+         std::string(ch ? ", const __grid_constant__ ddsim_lanes::ChainParams cp" : "") +
+         std::string(dk == 0 ? ", const __grid_constant__ ddsim_lanes::DerivedParams dp" : "") +
+         ") {\n  ddsim_lanes::lanes_body<" + std::to_string(dk) + ", " + std::to_string(V) +
+         (ch ? ", true" : ", false") +
+         (dk == 0 ? std::string(", false>(&tmap, p, ") + (ch ? "&cp" : "nullptr") +
+                        ", nullptr, 0, 0, nullptr, &dp);\n}\n"
+                  : std::string(">(&tmap, p") + (ch ? ", &cp" : "") + ");\n}\n");
   return src;
 }
 
@@ -152,8 +156,10 @@ CUfunction get_compiled(const std::string& key, const std::string& src, const ch
   nvrtcProgram_t prog = nullptr;
   CUfunction fn = nullptr;
   if (g_nv.create(&prog, src.c_str(), "ddsim_lanes_jit.cu", 0, nullptr, nullptr) == 0) {
-    const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo"};
-    const int rc = g_nv.compile(prog, 3, opts);
+    // --device-int128: the half-up Shrink of derived durations (lanes_body.cuh)
+    const char* opts[] = {"--gpu-architecture=sm_100a", "-std=c++17", "-lineinfo",
+                          "--device-int128"};
+    const int rc = g_nv.compile(prog, 4, opts);
     size_t ls = 0;
     g_nv.log_size(prog, &ls);
     if (ls > 1) {
@@ -223,9 +229,10 @@ std::string seg_source(const std::vector<int>& codes, int dk, int LN, bool ch, i
          "(const __grid_constant__ ddsim_lanes::Tmap tmap, const ddsim_lanes::Params p, "
          "const ddsim_lanes::SegParams sg" +
          (ch ? ", const __grid_constant__ ddsim_lanes::ChainParams cp" : "") +
+         (dk == 0 ? ", const __grid_constant__ ddsim_lanes::DerivedParams dp" : "") +
          ") {\n  ddsim_lanes::" + bodies[mode] + "<" + std::to_string(dk) + ", " +
          std::to_string(LN) + ", " + (ch ? "true" : "false") + ">(&tmap, p, sg, " +
-         (ch ? "&cp" : "nullptr") + ");\n}\n";
+         (ch ? "&cp" : "nullptr") + (dk == 0 ? ", &dp" : ", nullptr") + ");\n}\n";
   return src;
 }
 
@@ -241,7 +248,7 @@ void log_line(const std::string& msg) {
 cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const LaneChainParams* cp,
                                      const int* dense32, const void* tmap128, int dkind, int V,
                                      const std::vector<int>& codes, int grid, int BD, size_t smem,
-                                     cudaStream_t stream) {
+                                     cudaStream_t stream, const LaneDerivedParams* dp) {
   if (codes.empty() || codes.size() > 32) {
     static std::atomic<bool> logged{false};  // once per process, not per call
     if (!logged.exchange(true))
@@ -257,8 +264,8 @@ cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const LaneChainParams*
   if (const char* e = getenv("DDSIM_LANES_DYN")) dyn = atoi(e) != 0;
   // lane busy by a separate pass for the branch-free handler (absent chain
   // members are recognised by their start -1, so chains need the starts)
-  const bool nolb = dyn && p.lane_busy != nullptr && (cp == nullptr || p.start != nullptr) &&
-                    getenv("DDSIM_DYN_LB") == nullptr;
+  const bool nolb = dyn && dkind != 0 && p.lane_busy != nullptr &&
+                    (cp == nullptr || p.start != nullptr) && getenv("DDSIM_DYN_LB") == nullptr;
   CUfunction fn = get_function(codes, dkind, V, dyn, cp != nullptr, nolb, dev);
   if (!fn) return cudaErrorNotSupported;
   const CUresult ar = g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
@@ -272,9 +279,12 @@ cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const LaneChainParams*
   if (nolb) pp.lane_busy = nullptr;
   LaneChainParams cpv{};
   if (cp) cpv = *cp;
-  void* args[] = {tm, &pp, &cpv};
-  const CUresult r = g_drv.launch(fn, grid, 1, 1, BD, 1, 1, (unsigned)smem, (CUstream)stream, args,
-                                  nullptr);
+  LaneDerivedParams dpv{};
+  if (dp) dpv = *dp;
+  void* args_ch[] = {tm, &pp, &cpv, &dpv};
+  void* args_nc[] = {tm, &pp, &dpv};
+  const CUresult r = g_drv.launch(fn, grid, 1, 1, BD, 1, 1, (unsigned)smem, (CUstream)stream,
+                                  cp ? args_ch : args_nc, nullptr);
   if (r != CUDA_SUCCESS) {
     log_line("cuLaunchKernel failed: " + std::to_string((int)r));
     return cudaErrorNotSupported;
@@ -288,7 +298,8 @@ cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const LaneChainParams*
 cudaError_t launch_lanes_seg_jit(int mode, const LaneParams& p, const LaneChainParams* cp,
                                  const void* tmap128, int dkind, int LN,
                                  const std::vector<int>& codes, const void* segp, int gx, int gy,
-                                 int BD, size_t smem, cudaStream_t stream) {
+                                 int BD, size_t smem, cudaStream_t stream,
+                                 const LaneDerivedParams* dp) {
   if (codes.empty() || codes.size() > 32 || LN < 1 || LN > 4 || mode < 0 || mode > 2)
     return cudaErrorNotSupported;
   int dev = 0;
@@ -309,9 +320,12 @@ cudaError_t launch_lanes_seg_jit(int mode, const LaneParams& p, const LaneChainP
   memcpy(sg, segp, sizeof(sg));
   LaneChainParams cpv{};
   if (cp) cpv = *cp;
-  void* args[] = {tm, &pp, sg, &cpv};
-  const CUresult r = g_drv.launch(fn, gx, gy, 1, BD, 1, 1, (unsigned)smem, (CUstream)stream, args,
-                                  nullptr);
+  LaneDerivedParams dpv{};
+  if (dp) dpv = *dp;
+  void* args_ch[] = {tm, &pp, sg, &cpv, &dpv};
+  void* args_nc[] = {tm, &pp, sg, &dpv};
+  const CUresult r = g_drv.launch(fn, gx, gy, 1, BD, 1, 1, (unsigned)smem, (CUstream)stream,
+                                  cp ? args_ch : args_nc, nullptr);
   if (r != CUDA_SUCCESS) {
     log_line("cuLaunchKernel (segment) failed: " + std::to_string((int)r));
     return cudaErrorLaunchFailure;

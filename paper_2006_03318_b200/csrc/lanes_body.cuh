@@ -67,6 +67,95 @@ struct ChainParams {
   int n_chains;
 };
 
+// Derived durations (DK = 0): no per-scenario duration matrix.  A record's
+// duration is its row's base duration, or the row's per-scenario override,
+// then the scenario's half-up Shrink steps on the row's group
+// (scale_durations, transform.py:174-183) -- what expand_durations_kernel
+// would have materialised, computed where it is consumed.  Rows are staged
+// per chunk by bulk copy like the records.
+struct alignas(16) RowDur {
+  long long base;
+  unsigned group;  // 0: no scale step applies
+  int ovr;         // override row, -1 none
+};
+struct ScaleStep {
+  int lo, hi;
+  long long num, den;
+};
+struct DerivedParams {
+  const RowDur* rows;      // [n_rec]
+  const long long* ovr;    // [n_ovr][S]
+  const int* scale_ptr;    // [S+1] or null
+  const ScaleStep* scale;
+};
+constexpr int kProgRegs = 4;  // scale steps kept in registers per scenario
+struct Prog {
+  int n, e0;
+  int lo[kProgRegs], hi[kProgRegs];
+  long long num[kProgRegs], den[kProgRegs];
+};
+
+// round_half_up(d * num / den) (transform.py:174-183); 128-bit when needed
+__device__ __forceinline__ long long lscale_half_up(long long d, long long num, long long den) {
+  const bool neg = d < 0;
+  const unsigned long long a = neg ? (unsigned long long)(-d) : (unsigned long long)d;
+  const unsigned long long un = (unsigned long long)num, ud = (unsigned long long)den;
+  unsigned long long q;
+  if (a < (1ull << 40) && un < (1ull << 21) && ud < (1ull << 40)) {
+    q = (2ull * a * un + ud) / (2ull * ud);
+  } else {
+    const unsigned __int128 x = (unsigned __int128)a * un * 2u + ud;
+    q = (unsigned long long)(x / ((unsigned __int128)ud * 2u));
+  }
+  return neg ? -(long long)q : (long long)q;
+}
+
+__device__ __forceinline__ void prog_load(const DerivedParams* dp, long long s, bool act, Prog& P) {
+  P.n = 0;
+  P.e0 = 0;
+#pragma unroll
+  for (int q = 0; q < kProgRegs; ++q) {
+    P.lo[q] = 1;
+    P.hi[q] = 0;
+    P.num[q] = 1;
+    P.den[q] = 1;
+  }
+  if (dp == nullptr || dp->scale_ptr == nullptr || !act) return;
+  P.e0 = dp->scale_ptr[s];
+  P.n = dp->scale_ptr[s + 1] - P.e0;
+#pragma unroll
+  for (int q = 0; q < kProgRegs; ++q)
+    if (q < P.n) {
+      const ScaleStep st = dp->scale[P.e0 + q];
+      P.lo[q] = st.lo;
+      P.hi[q] = st.hi;
+      P.num[q] = st.num;
+      P.den[q] = st.den;
+    }
+}
+
+__device__ __forceinline__ long long derived_dur(const DerivedParams* dp, long long base,
+                                                 unsigned group, int ovr, long long s, int S,
+                                                 bool act, const Prog& P) {
+  long long d = base;
+  if (ovr >= 0 && act) d = dp->ovr[(long long)ovr * S + s];
+  if (group != 0u && P.n > 0) {
+    if (P.n <= kProgRegs) {
+#pragma unroll
+      for (int q = 0; q < kProgRegs; ++q)
+        if (q < P.n && group >= (unsigned)P.lo[q] && group <= (unsigned)P.hi[q] && P.num[q] != 0)
+          d = lscale_half_up(d, P.num[q], P.den[q]);
+    } else {
+      for (int e = P.e0; e < P.e0 + P.n; ++e) {
+        const ScaleStep st = dp->scale[e];
+        if (group >= (unsigned)st.lo && group <= (unsigned)st.hi && st.num != 0)
+          d = lscale_half_up(d, st.num, st.den);
+      }
+    }
+  }
+  return d;
+}
+
 // Segment-parallel evaluation (small scenario counts): the record stream is
 // cut into K segments at rows where no slot value is live, so a segment's
 // input is the L lane heads only.  seg_transfer (lanes_seg.cuh) computes each
@@ -302,7 +391,7 @@ __device__ __forceinline__ void chain_record(const Params& p, const ChainParams&
                                              long long s, bool act, bool store, long long* sp,
                                              long long ld, unsigned slot_s, unsigned slot_pitch,
                                              unsigned col, long long& ms0, long long& ms1,
-                                             int& neg) {
+                                             int& neg, const DerivedParams* dp, const Prog& P) {
   const int ksm = p.ksm;
   auto slot_addr = [&](int code, int i) { return slot_s + (unsigned)code * slot_pitch + col + 8u * i; };
   const Chain ch = cp.chains[cid];
@@ -328,7 +417,10 @@ __device__ __forceinline__ void chain_record(const Params& p, const ChainParams&
           x = lmax(x, v);
         }
         long long d = 0;
-        if (act) {
+        if (DK == 0) {
+          const RowDur rd = dp->rows[row + k];
+          d = derived_dur(dp, rd.base, rd.group, rd.ovr, sc, p.S, act, P);
+        } else if (act) {
           const long long at = (long long)(row + k) * p.dense_ld + sc;
           d = DK == 1 ? (long long)cp.dense32[at] : p.dense64[at];
         }
@@ -370,8 +462,10 @@ template <int DK, int V, bool CH = false, bool SEG = false>
 __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
                                            const ChainParams* cpp = nullptr,
                                            const SegParams* sgp = nullptr, int seg_k = 0,
-                                           int blk = 0, const long long* init = nullptr) {
+                                           int blk = 0, const long long* init = nullptr,
+                                           const DerivedParams* dp = nullptr) {
   static_assert(!SEG || V == 1, "segment replay runs one scenario per thread");
+  static_assert(DK != 0 || V == 1, "derived durations: one scenario per thread");
   extern __shared__ __align__(128) unsigned char smem[];
   const int BD = blockDim.x;
   const int W = BD * V;  // scenarios per CTA
@@ -383,7 +477,9 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
   const unsigned prog_s = sbase + 128;
   const unsigned tile_s = prog_s + kStagesL * kChunkL * (unsigned)sizeof(Rec);
   constexpr unsigned ES = DK == 1 ? 4u : 8u;  // tile element bytes (int32 / int64 durations)
-  const unsigned tile_all = (unsigned)(kStagesL * kChunkL * W) * ES;
+  // DK 0: the tile area holds the chunk's RowDur entries (16 B per row)
+  const unsigned tile_all = DK == 0 ? (unsigned)(kStagesL * kChunkL * 16)
+                                    : (unsigned)(kStagesL * kChunkL * W) * ES;
   const unsigned slot_s = tile_s + tile_all;                  // [ksm][BD] x (8 V) B
   const unsigned col = (unsigned)(tid * 8 * V);
   const unsigned slot_pitch = (unsigned)(BD * 8 * V);
@@ -402,6 +498,13 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
     const int st = (c - c_begin) % kStagesL;
     const int nrec = min(kChunkL, r_end - c * kChunkL);
     const unsigned pb = (unsigned)(nrec * sizeof(Rec));
+    if (DK == 0) {
+      l_expect(&bars[st], 2 * pb);
+      l_bulk(pst + st * kChunkL, p.prog + (long long)c * kChunkL, pb, &bars[st]);
+      l_bulk(reinterpret_cast<unsigned char*>(tst) + (size_t)st * kChunkL * 16,
+             dp->rows + (long long)c * kChunkL, pb, &bars[st]);
+      return;
+    }
     l_expect(&bars[st], pb + tile_bytes);
     l_bulk(pst + st * kChunkL, p.prog + (long long)c * kChunkL, pb, &bars[st]);
     l_tile(reinterpret_cast<unsigned char*>(tst) + (size_t)st * kChunkL * W * ES, tmap, s0,
@@ -434,22 +537,29 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
   const long long ld = p.start_ld;
   const bool store = act && p.start != nullptr;
   long long* sp = store ? p.start + (long long)c_begin * kChunkL * ld + s : nullptr;
-  const unsigned row_pitch = (unsigned)W * ES;
+  const unsigned row_pitch = DK == 0 ? 16u : (unsigned)W * ES;
   const int ksm = p.ksm;
+  Prog P;
+  if (DK == 0) prog_load(dp, s, act, P);
 
 
   for (int c = c_begin; c < nchunks; ++c) {
     const int st = (c - c_begin) % kStagesL;
     l_wait(&bars[st], (unsigned)(((c - c_begin) / kStagesL) & 1));
     const unsigned rec0 = prog_s + (unsigned)(st * kChunkL * sizeof(Rec));
-    const unsigned t0 = tile_s + (unsigned)(st * kChunkL) * row_pitch + (unsigned)tid * ES * V;
+    const unsigned t0 = DK == 0 ? tile_s + (unsigned)(st * kChunkL) * 16u
+                                : tile_s + (unsigned)(st * kChunkL) * row_pitch + (unsigned)tid * ES * V;
     const int nrec = min(kChunkL, r_end - c * kChunkL);
     int4 raw = l_lds128(rec0);
     // prefetched durations of the next record: int32 pair (DK 1) / int64 pair (DK 2)
     int2 dd = make_int2(0, 0);
     longlong2 dq = make_longlong2(0, 0);
     auto load_d = [&](unsigned ta) {
-      if (DK == 1) {
+      if (DK == 0) {
+        const int4 rd = l_lds128(ta);
+        dq.x = derived_dur(dp, ((long long)rd.y << 32) | (unsigned)rd.x, (unsigned)rd.z, rd.w, s,
+                           p.S, act, P);
+      } else if (DK == 1) {
         if (V == 2)
           dd = l_lds64i(ta);
         else
@@ -486,7 +596,7 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
         if (rare & (R_CHAIN | R_NOP)) {
           if (rare & R_CHAIN)
             chain_record<DK, V>(p, *cpp, S, (int)(short)(r.z & 0xffff), c * kChunkL + j, s, act,
-                                store, sp, ld, slot_s, slot_pitch, col, ms0, ms1, neg);
+                                store, sp, ld, slot_s, slot_pitch, col, ms0, ms1, neg, dp, P);
           if (store) sp += ld;
           return;
         }

@@ -80,7 +80,8 @@ __device__ __forceinline__ void sym_set(Sym<LN>& Y, int lane, const int (&y)[4])
 template <int DK, int LN>
 __device__ __forceinline__ void chain_sym(const Params& p, const ChainParams& cp, Sym<LN>& Y,
                                           int cid, int row, long long s, bool act,
-                                          unsigned slot_s, unsigned slot_pitch, unsigned col) {
+                                          unsigned slot_s, unsigned slot_pitch, unsigned col,
+                                          const DerivedParams* dp, const Prog& P) {
   const Chain ch = cp.chains[cid];
   const bool pres = !act || cp.present == nullptr || cp.present[s * cp.n_chains + cid] != 0;
   int prev[4];
@@ -97,7 +98,10 @@ __device__ __forceinline__ void chain_sym(const Params& p, const ChainParams& cp
         for (int c = 0; c < 4; ++c) x[c] = imax(x[c], y[c]);
       }
       long long d = 0;
-      if (act) {
+      if (DK == 0) {
+        const RowDur rd = dp->rows[row + k];
+        d = derived_dur(dp, rd.base, rd.group, rd.ovr, s, p.S, act, P);
+      } else if (act) {
         const long long at = (long long)(row + k) * p.dense_ld + s;
         d = DK == 1 ? (long long)cp.dense32[at] : p.dense64[at];
       }
@@ -123,7 +127,7 @@ __device__ __forceinline__ void chain_sym(const Params& p, const ChainParams& cp
 template <int DK, int LN, bool CH>
 __device__ __forceinline__ void sym_pass(const Tmap* tmap, const Params& p, const SegParams& sg,
                                          const ChainParams* cpp, int seg, int blk,
-                                         int (&coef)[LN][LN]) {
+                                         int (&coef)[LN][LN], const DerivedParams* dp) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int BD = blockDim.x;
   const int tid = threadIdx.x;
@@ -134,7 +138,8 @@ __device__ __forceinline__ void sym_pass(const Tmap* tmap, const Params& p, cons
   const unsigned prog_s = sbase + 128;
   const unsigned tile_s = prog_s + kStagesL * kChunkL * (unsigned)sizeof(Rec);
   constexpr unsigned ES = DK == 1 ? 4u : 8u;
-  const unsigned tile_all = (unsigned)(kStagesL * kChunkL * BD) * ES;
+  const unsigned tile_all = DK == 0 ? (unsigned)(kStagesL * kChunkL * 16)
+                                    : (unsigned)(kStagesL * kChunkL * BD) * ES;
   const unsigned slot_s = tile_s + tile_all;  // [ksm][BD] x 16 B
   const unsigned col = (unsigned)(tid * 16);
   const unsigned slot_pitch = (unsigned)(BD * 16);
@@ -150,6 +155,12 @@ __device__ __forceinline__ void sym_pass(const Tmap* tmap, const Params& p, cons
     const int st = (c - c_begin) % kStagesL;
     const int nrec = min(kChunkL, r_end - c * kChunkL);
     const unsigned pb = (unsigned)(nrec * sizeof(Rec));
+    if (DK == 0) {
+      l_expect(&bars[st], 2 * pb);
+      l_bulk(pst + st * kChunkL, p.prog + (long long)c * kChunkL, pb, &bars[st]);
+      l_bulk(tst + (size_t)st * kChunkL * 16, dp->rows + (long long)c * kChunkL, pb, &bars[st]);
+      return;
+    }
     l_expect(&bars[st], pb + tile_bytes);
     l_bulk(pst + st * kChunkL, p.prog + (long long)c * kChunkL, pb, &bars[st]);
     l_tile(tst + (size_t)st * kChunkL * BD * ES, tmap, s0, c * kChunkL, &bars[st]);
@@ -168,20 +179,27 @@ __device__ __forceinline__ void sym_pass(const Tmap* tmap, const Params& p, cons
   for (int l = 0; l <= NLANE; ++l)
 #pragma unroll
     for (int c = 0; c < LN; ++c) Y.v[l][c] = (l == c) ? 0 : kNegSym;
-  const unsigned row_pitch = (unsigned)BD * ES;
+  const unsigned row_pitch = DK == 0 ? 16u : (unsigned)BD * ES;
+  Prog P;
+  if (DK == 0) prog_load(dp, s, act, P);
 
   for (int c = c_begin; c < nchunks; ++c) {
     const int st = (c - c_begin) % kStagesL;
     l_wait(&bars[st], (unsigned)(((c - c_begin) / kStagesL) & 1));
     const unsigned rec0 = prog_s + (unsigned)(st * kChunkL * sizeof(Rec));
-    const unsigned t0 = tile_s + (unsigned)(st * kChunkL) * row_pitch + (unsigned)tid * ES;
+    const unsigned t0 = DK == 0 ? tile_s + (unsigned)(st * kChunkL) * 16u
+                                : tile_s + (unsigned)(st * kChunkL) * row_pitch + (unsigned)tid * ES;
     const int nrec = min(kChunkL, r_end - c * kChunkL);
     // prefetched record and duration of the next record (the decode and the
     // shared-memory loads overlap this record's coefficient updates)
     int4 raw = l_lds128(rec0);
     long long dn = 0;
     auto load_d = [&](unsigned ta) {
-      if (DK == 1) {
+      if (DK == 0) {
+        const int4 rd = l_lds128(ta);
+        dn = derived_dur(dp, ((long long)rd.y << 32) | (unsigned)rd.x, (unsigned)rd.z, rd.w, s,
+                         p.S, act, P);
+      } else if (DK == 1) {
         int x;
         asm volatile("ld.shared.s32 %0, [%1];" : "=r"(x) : "r"(ta));
         dn = x;
@@ -205,7 +223,7 @@ __device__ __forceinline__ void sym_pass(const Tmap* tmap, const Params& p, cons
         if (rare & (R_CHAIN | R_NOP)) {
           if (rare & R_CHAIN)
             chain_sym<DK, LN>(p, *cpp, Y, (int)(short)(r.z & 0xffff), c * kChunkL + j, s, act,
-                              slot_s, slot_pitch, col);
+                              slot_s, slot_pitch, col, dp, P);
           return;
         }
       }
@@ -271,10 +289,10 @@ __device__ __forceinline__ void sym_pass(const Tmap* tmap, const Params& p, cons
 // Three-kernel path, pass 1: blockIdx.y = segment, coefficients to sg.trans.
 template <int DK, int LN, bool CH>
 __device__ __forceinline__ void sym_body(const Tmap* tmap, const Params& p, const SegParams& sg,
-                                         const ChainParams* cpp) {
+                                         const ChainParams* cpp, const DerivedParams* dp) {
   if ((int)blockIdx.y == sg.kc) return;  // the chain segment is replayed numerically
   int coef[LN][LN];
-  sym_pass<DK, LN, CH>(tmap, p, sg, cpp, (int)blockIdx.y, (int)blockIdx.x, coef);
+  sym_pass<DK, LN, CH>(tmap, p, sg, cpp, (int)blockIdx.y, (int)blockIdx.x, coef, dp);
   const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (s < p.S) {
     int* out = sg.trans + (long long)blockIdx.y * LN * LN * sg.s_pad + s;
@@ -288,7 +306,8 @@ __device__ __forceinline__ void sym_body(const Tmap* tmap, const Params& p, cons
 // Three-kernel path, pass 3: replay of segment blockIdx.y from seg_scan's state.
 template <int DK, int LN, bool CH>
 __device__ __forceinline__ void replay_body(const Tmap* tmap, const Params& p,
-                                            const SegParams& sg, const ChainParams* cpp) {
+                                            const SegParams& sg, const ChainParams* cpp,
+                                            const DerivedParams* dp) {
   const int k = sg.replay_only >= 0 ? sg.replay_only : (int)blockIdx.y;
   if (sg.replay_only < 0 && k == sg.kc) return;  // replayed before the second scan
   long long init[NLANE] = {0, 0, 0, 0};
@@ -297,7 +316,7 @@ __device__ __forceinline__ void replay_body(const Tmap* tmap, const Params& p,
 #pragma unroll
     for (int l = 0; l < LN; ++l)
       init[l] = sg.state[((long long)k * LN + l) * sg.s_pad + s];
-  lanes_body<DK, 1, CH, true>(tmap, p, cpp, &sg, k, (int)blockIdx.x, init);
+  lanes_body<DK, 1, CH, true>(tmap, p, cpp, &sg, k, (int)blockIdx.x, init, dp);
 }
 
 // Fused single pass with decoupled look-back: CTAs take (segment, block) work
@@ -308,7 +327,7 @@ __device__ __forceinline__ void replay_body(const Tmap* tmap, const Params& p,
 // progresses; later items' transfers overlap earlier items' replays.
 template <int DK, int LN, bool CH>
 __device__ __forceinline__ void fused_body(const Tmap* tmap, const Params& p, const SegParams& sg,
-                                           const ChainParams* cpp) {
+                                           const ChainParams* cpp, const DerivedParams* dp) {
   __shared__ int tk;
   if (threadIdx.x == 0) tk = atomicAdd(sg.ticket, 1);
   __syncthreads();
@@ -317,7 +336,7 @@ __device__ __forceinline__ void fused_body(const Tmap* tmap, const Params& p, co
   const bool act = s < p.S;
   const bool last = k + 1 >= sg.K;
   int coef[LN][LN];
-  if (!last) sym_pass<DK, LN, CH>(tmap, p, sg, cpp, k, b, coef);
+  if (!last) sym_pass<DK, LN, CH>(tmap, p, sg, cpp, k, b, coef, dp);
   long long st[NLANE] = {0, 0, 0, 0};
   if (k > 0) {
     if (threadIdx.x == 0) {
@@ -358,7 +377,7 @@ __device__ __forceinline__ void fused_body(const Tmap* tmap, const Params& p, co
   // TMA writes into the same bytes
   asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
   __syncthreads();
-  lanes_body<DK, 1, CH, true>(tmap, p, cpp, &sg, k, b, st);
+  lanes_body<DK, 1, CH, true>(tmap, p, cpp, &sg, k, b, st, dp);
 }
 
 }  // namespace ddsim_lanes

@@ -65,14 +65,18 @@ static int lanes_stages() {
 static size_t lanes_smem(int dk, int BD, int V, int ksm) {
   const int stages = lanes_stages();
   size_t b = 128 + (size_t)stages * ddsim_lanes::kChunkL * sizeof(ddsim_lanes::Rec);
-  b += (size_t)stages * ddsim_lanes::kChunkL * BD * V * (dk == 1 ? 4 : 8);
+  if (dk == 0)  // derived durations: the chunk's RowDur entries
+    b += (size_t)stages * ddsim_lanes::kChunkL * sizeof(ddsim_lanes::RowDur);
+  else
+    b += (size_t)stages * ddsim_lanes::kChunkL * BD * V * (dk == 1 ? 4 : 8);
   return b + (size_t)ksm * BD * 8 * V;
 }
 
 // V scenarios per thread (env DDSIM_LANES_V overrides: 1 or 2); two CTAs per
 // SM cover S in one wave.  BD is a multiple of 16 so the grid is close to
 // 2 x #SMs; the TMA box (BD * V ints) stays <= 256.
-int maxplus_lanes_vec(int S) {
+int maxplus_lanes_vec(int S, int dkind) {
+  if (dkind == 0) return 1;  // derived durations: one scenario per thread
   const char* e = getenv("DDSIM_LANES_V");
   // two scenarios per thread only when there are enough scenarios to keep
   // ~4 warps per SM busy with V = 2; small sweeps want more threads instead
@@ -81,8 +85,8 @@ int maxplus_lanes_vec(int S) {
   if (S % v) v = 1;
   return v;
 }
-int maxplus_lanes_block_dim(int S, int num_sms) {
-  const int V = maxplus_lanes_vec(S);
+int maxplus_lanes_block_dim(int S, int num_sms, int dkind) {
+  const int V = maxplus_lanes_vec(S, dkind);
   if (const char* e = getenv("DDSIM_LANES_BD")) {  // experiments (multiple of 16)
     const int bd = atoi(e) / 16 * 16;
     if (bd >= 32 && bd <= 256 / V) return bd;
@@ -173,6 +177,30 @@ static cudaError_t encode_lanes_tmap(CUtensorMap* tmap, const LaneParams& p, con
   return cudaSuccess;
 }
 
+static_assert(sizeof(ddsim_lanes::RowDur) == sizeof(LaneRowDur), "row duration layout");
+static_assert(sizeof(ddsim_lanes::DerivedParams) == sizeof(LaneDerivedParams), "derived layout");
+static_assert(sizeof(ddsim_lanes::ScaleStep) == sizeof(ScaleStepDev), "scale step layout");
+
+__global__ void build_rowdur_kernel(const long long* base, const unsigned* group,
+                                    const int* ovr_map, int n, LaneRowDur* out) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < n; r += gridDim.x * blockDim.x) {
+    LaneRowDur x;
+    x.base = base[r];
+    x.group = group ? group[r] : 0u;
+    x.ovr = ovr_map ? ovr_map[r] : -1;
+    out[r] = x;
+  }
+}
+
+cudaError_t launch_build_rowdur(const long long* base, const unsigned* group, const int* ovr_map,
+                                int n, LaneRowDur* out, cudaStream_t st) {
+  if (n <= 0) return cudaSuccess;
+  build_rowdur_kernel<<<std::min((n + 255) / 256, 148 * 8), 256, 0, st>>>(base, group, ovr_map, n,
+                                                                           out);
+  note_launch();
+  return cudaGetLastError();
+}
+
 // Compose the segment transfer matrices per scenario (one thread each):
 // state[k+1] = trans[k] (x) state[k] in (max,+), state[0] = 0, for segments
 // k in [k_from, k_to) (the state of k_from is read unless k_from == 0).  All
@@ -254,23 +282,26 @@ static cudaError_t launch_seg_scan(const LaneSegParams& sg, int S, int k_from, i
 // and lane busy; cudaErrorNotSupported when the JIT is unavailable.
 cudaError_t launch_maxplus_lanes_seg(const LaneParams& p, const LaneChainParams* cp,
                                      const int* dense32, int dkind, const std::vector<int>& codes,
-                                     const LaneSegParams& sg, int BD, cudaStream_t stream) {
+                                     const LaneSegParams& sg, int BD, cudaStream_t stream,
+                                     const LaneDerivedParams* dp) {
   static_assert(sizeof(LaneSegParams) == sizeof(ddsim_lanes::SegParams), "seg params layout");
   CUtensorMap tmap;
-  cudaError_t e = encode_lanes_tmap(&tmap, p, dense32, dkind, BD);
+  memset(&tmap, 0, sizeof(tmap));
+  cudaError_t e = dkind == 0 ? cudaSuccess : encode_lanes_tmap(&tmap, p, dense32, dkind, BD);
   if (e != cudaSuccess) return e;
   const int gx = (p.S + BD - 1) / BD;
   const int stages = ddsim_lanes::kStagesL;
   const size_t es = dkind == 1 ? 4 : 8;
   const size_t base = 128 + (size_t)stages * ddsim_lanes::kChunkL * sizeof(ddsim_lanes::Rec) +
-                      (size_t)stages * ddsim_lanes::kChunkL * BD * es;
+                      (dkind == 0 ? (size_t)stages * ddsim_lanes::kChunkL * sizeof(ddsim_lanes::RowDur)
+                                  : (size_t)stages * ddsim_lanes::kChunkL * BD * es);
   const size_t smem_t = base + (size_t)p.ksm * BD * 16, smem_r = base + (size_t)p.ksm * BD * 8;
   if (sg.ticket != nullptr)  // fused single pass (transfer smem >= replay smem)
     return launch_lanes_seg_jit(2, p, cp, &tmap, dkind, sg.LN, codes, &sg, gx * sg.K, 1, BD,
-                                smem_t, stream);
+                                smem_t, stream, dp);
   if (sg.K > 1) {
     e = launch_lanes_seg_jit(1, p, cp, &tmap, dkind, sg.LN, codes, &sg, gx, sg.K - 1, BD, smem_t,
-                             stream);
+                             stream, dp);
     if (e != cudaSuccess) return e;
   }
   if (sg.kc < 0) {
@@ -282,38 +313,42 @@ cudaError_t launch_maxplus_lanes_seg(const LaneParams& p, const LaneChainParams*
     LaneSegParams one = sg;
     one.replay_only = sg.kc;
     e = launch_lanes_seg_jit(0, p, cp, &tmap, dkind, sg.LN, codes, &one, gx, 1, BD, smem_r,
-                             stream);
+                             stream, dp);
     if (e != cudaSuccess) return e;
     e = launch_seg_scan(sg, p.S, sg.kc + 1, sg.K - 1, p.gslots, stream);
     if (e != cudaSuccess) return e;
   }
   return launch_lanes_seg_jit(0, p, cp, &tmap, dkind, sg.LN, codes, &sg, gx, sg.K, BD, smem_r,
-                              stream);
+                              stream, dp);
 }
 
 cudaError_t launch_maxplus_lanes(const LaneParams& p, const LaneChainParams* cp, const int* dense32,
                                  int dkind,
-                                 const std::vector<int>* codes, cudaStream_t stream) {
+                                 const std::vector<int>* codes, cudaStream_t stream,
+                                 const LaneDerivedParams* dp) {
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const int V = maxplus_lanes_vec(p.S);
-  const int BD = maxplus_lanes_block_dim(p.S, nsm);
+  const int V = maxplus_lanes_vec(p.S, dkind);
+  const int BD = maxplus_lanes_block_dim(p.S, nsm, dkind);
   const int W = BD * V;
   const int grid = (p.S + W - 1) / W;
   if ((long long)grid * W > p.s_pad) return cudaErrorInvalidValue;
   const size_t smem = lanes_smem(dkind, BD, V, p.ksm);
   CUtensorMap tmap;
-  {
+  memset(&tmap, 0, sizeof(tmap));
+  if (dkind != 0) {
     const cudaError_t te = encode_lanes_tmap(&tmap, p, dense32, dkind, W);
     if (te != cudaSuccess) return te;
   }
   // per-graph specialised dispatch first (NVRTC); the static kernel otherwise
+  // (derived durations exist only as JIT kernels)
   if (codes != nullptr) {
-    const cudaError_t e =
-        launch_maxplus_lanes_jit(p, cp, dense32, &tmap, dkind, V, *codes, grid, BD, smem, stream);
+    const cudaError_t e = launch_maxplus_lanes_jit(p, cp, dense32, &tmap, dkind, V, *codes, grid,
+                                                   BD, smem, stream, dp);
     if (e == cudaSuccess) return cudaGetLastError();
   }
+  if (dkind == 0) return cudaErrorNotSupported;
   // the kernels' parameter types mirror the host structs byte for byte
   static_assert(sizeof(ddsim_lanes::Tmap) == sizeof(CUtensorMap), "tensor map layout");
   static_assert(sizeof(ddsim_lanes::Params) == sizeof(LaneParams), "lane params layout");

@@ -53,7 +53,9 @@ def test_config4_full_graph():
     assert np.array_equal(res.lane_busy.sum(axis=1), dense.astype(np.int64).sum(axis=0))
 
 
-def test_config2_full_sweep():
+@pytest.mark.parametrize("durations", ["expanded", "derived"])
+def test_config2_full_sweep(durations, monkeypatch):
+    monkeypatch.setenv("DDSIM_FORCE_DERIVED" if durations == "derived" else "DDSIM_NO_DERIVED", "1")
     w = W.bert_trace(buckets_mb=None)
     g = w.graph
     scen = [[(And([GPU_TASKS, ByLayer(l)]), "1/2")] for l in w.layers]
@@ -71,7 +73,9 @@ def test_config2_full_sweep():
         assert res.makespan[s] == ms and res.start_of(s) == st
 
 
-def test_config3_full_sweep():
+@pytest.mark.parametrize("durations", ["expanded", "derived"])
+def test_config3_full_sweep(durations, monkeypatch):
+    monkeypatch.setenv("DDSIM_FORCE_DERIVED" if durations == "derived" else "DDSIM_NO_DERIVED", "1")
     w = W.bert_trace(buckets_mb=25.0)
     g = w.graph
     buckets = w.trace.gradient_buckets

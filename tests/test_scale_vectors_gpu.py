@@ -21,7 +21,8 @@ from paper_2006_03318_b200.trace import LaneId, TaskKind
 pytestmark = pytest.mark.gpu
 
 PATHS = {
-    "expand+lanes": ({}, N.KS_PATH_AUTO),
+    "derived-lanes": ({"DDSIM_FORCE_DERIVED": "1"}, N.KS_PATH_AUTO),
+    "expand+lanes": ({"DDSIM_NO_DERIVED": "1"}, N.KS_PATH_AUTO),
     "lanes-general": ({"DDSIM_NO_EXPAND": "1"}, N.KS_PATH_AUTO),
     "general": ({"DDSIM_NO_EXPAND": "1", "DDSIM_NO_LANES": "1"}, N.KS_PATH_AUTO),
     "listsched": ({}, N.KS_PATH_LISTSCHED),

@@ -138,10 +138,14 @@ def test_batch_dense_durations_vs_oracle(golden, name, dtype, S):
             {str(k2): v for k2, v in lb.items()}
 
 
-@pytest.mark.parametrize("mode", ["expand+lanes", "general"])
+@pytest.mark.parametrize("mode", ["derived-lanes", "expand+lanes", "general"])
 def test_batch_amp_and_layer_sweep_vs_oracle(golden, mode, monkeypatch):
     if mode == "general":
         monkeypatch.setenv("DDSIM_NO_EXPAND", "1")
+    elif mode == "derived-lanes":
+        monkeypatch.setenv("DDSIM_FORCE_DERIVED", "1")
+    else:
+        monkeypatch.setenv("DDSIM_NO_DERIVED", "1")
     g = _genspec_graph(golden, "genspec_1002")
     compute = Or([ByNameSubstring("sgemm"), ByNameSubstring("scudnn")])
     amp = [(And([GPU_TASKS, compute]), "1/3"), (And([GPU_TASKS, Not(compute)]), "1/2")]
