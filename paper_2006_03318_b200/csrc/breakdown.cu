@@ -80,7 +80,11 @@ __device__ __forceinline__ void bd_prefetch(const BreakdownParams& p, LaneCursor
   const int row = bd_row<CH>(p, l, c.v, s, c.chain_on);
   ++c.v;
   c.nrow = row;
-  c.nst = __ldcs(&p.start[(long long)row * p.start_ld + s]);
+  // default caching: the scenarios of a warp reach a row at slightly
+  // different times (their seek positions differ), so each 32 B sector serves
+  // 4 threads across a short interval; an evict-first load re-fetched it
+  c.nst = p.stream_loads ? __ldcs(&p.start[(long long)row * p.start_ld + s])
+                         : p.start[(long long)row * p.start_ld + s];
   c.nd = bd_dur(p, row, s);
   c.nrc = __ldg(&p.row_class[row]);
   c.ngap = __ldg(&p.gap[row]);
@@ -144,15 +148,35 @@ __device__ __forceinline__ long long mul_div(long long a, long long k, long long
   return (long long)(((__int128)a * k) / K);
 }
 
-// Pass 1: zero the outputs and flag scenarios with a negative duration.
-__global__ void bd_prepare_kernel(const BreakdownParams p) {
+// Pass 1: zero the outputs and the negative-duration flags; pass 2 flags
+// scenarios with a negative duration, row chunks x scenarios in parallel
+// (coalesced across the scenarios of a warp).
+__global__ void bd_zero_kernel(const BreakdownParams p) {
   for (int s = blockIdx.x * blockDim.x + threadIdx.x; s < p.S; s += gridDim.x * blockDim.x) {
-    int bad = 0;
-    for (int row = 0; row < p.n; ++row) bad |= bd_dur(p, row, s) < 0;
-    p.bad[s] = bad;
+    p.bad[s] = 0;
     long long* o = p.parts + (long long)s * 4;
     o[0] = o[1] = o[2] = o[3] = 0;
   }
+}
+constexpr int kBdNegRows = 1024;
+__global__ void bd_negative_kernel(const BreakdownParams p) {
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= p.S) return;
+  const int r0 = blockIdx.y * kBdNegRows, r1 = min(p.n, r0 + kBdNegRows);
+  int bad = 0;
+  if (p.dkind == 1) {
+    const int* d = static_cast<const int*>(p.dur) + s;
+#pragma unroll 8
+    for (int row = r0; row < r1; ++row) bad |= __ldcs(d + (long long)row * p.dld);
+    bad = bad < 0;
+  } else {
+    const long long* d = static_cast<const long long*>(p.dur) + s;
+    long long b = 0;
+#pragma unroll 8
+    for (int row = r0; row < r1; ++row) b |= __ldcs(d + (long long)row * p.dld);
+    bad = b < 0;
+  }
+  if (bad) atomicOr(p.bad + s, 1);
 }
 
 // LM: lane capacity (>= L), a compile-time bound so that the per-lane cursors
@@ -238,6 +262,200 @@ __global__ void __launch_bounds__(128) breakdown_kernel(const BreakdownParams p)
         if (c.cls == 0) ++cc; else ++gc;
         c.active = true;
       }
+    }
+  }
+  unsigned long long* u = reinterpret_cast<unsigned long long*>(o);
+  if (acc0) atomicAdd(u + 0, (unsigned long long)acc0);
+  if (acc1) atomicAdd(u + 1, (unsigned long long)acc1);
+  if (acc2) atomicAdd(u + 2, (unsigned long long)acc2);
+  if (acc3) atomicAdd(u + 3, (unsigned long long)acc3);
+}
+
+// Lean merge (L <= 8): the per-lane cursor state lives in shared memory
+// (structure of arrays, [lane][thread]) so an event touches its lane through a
+// dynamic index -- one copy of the advance code per event instead of LM
+// divergent copies.  Only the per-lane next event time and the prefetched next
+// interval (start, duration) stay in registers, updated by predicated selects.
+constexpr int kBdLeanBD = 128;
+template <int LM>
+struct BdLean {
+  int v[LM][kBdLeanBD];        // next position to prefetch
+  int len[LM][kBdLeanBD];
+  int nrow[LM][kBdLeanBD];     // prefetched row (-1: none)
+  int cls[LM][kBdLeanBD];      // class of the current interval (0 cpu, 1 gpu)
+  int act[LM][kBdLeanBD];      // inside the current interval
+  unsigned char on[LM][kBdLeanBD];  // the lane's chain is present
+  long long b[LM][kBdLeanBD];  // end of the current interval
+};
+
+template <int LM, bool EXACT, bool CH>
+__global__ void __launch_bounds__(kBdLeanBD) breakdown_lean_kernel(const BreakdownParams p) {
+  __shared__ BdLean<LM> sh;
+  const int tid = threadIdx.x;
+  const int s = blockIdx.x * kBdLeanBD + tid;
+  const int k = blockIdx.y;
+  if (s >= p.S) return;
+  long long* o = p.parts + (long long)s * 4;
+  if (p.bad[s]) {
+    if (k == 0) o[0] = o[1] = o[2] = o[3] = -1;
+    return;
+  }
+  const long long ms = p.makespan[s];
+  const long long T0 = mul_div(ms, k, p.K), T1 = mul_div(ms, k + 1, p.K);
+  if (T1 <= T0) return;
+  long long e[LM], pst[LM], pd[LM];  // next event; prefetched next interval
+#pragma unroll
+  for (int l = 0; l < LM; ++l) e[l] = pst[l] = pd[l] = LLONG_MAX;
+
+  // prefetch lane l's row at position v (into pst / pd of lane l)
+  auto prefetch = [&](int l) {
+    const int v = sh.v[l][tid];
+    int row = -1;
+    long long a = 0, d = 0;
+    if (v < sh.len[l][tid]) {
+      row = bd_row<CH>(p, l, v, s, sh.on[l][tid] != 0);
+      a = p.stream_loads ? __ldcs(&p.start[(long long)row * p.start_ld + s])
+                         : p.start[(long long)row * p.start_ld + s];
+      d = bd_dur(p, row, s);
+      sh.v[l][tid] = v + 1;
+    }
+    sh.nrow[l][tid] = row;
+#pragma unroll
+    for (int q = 0; q < LM; ++q)
+      if (q == l) {
+        pst[q] = a;
+        pd[q] = d;
+      }
+  };
+  // make the prefetched interval of lane l current (skipping removed / empty
+  // ones) and prefetch the following; e[l] = its start, LLONG_MAX when done
+  auto consume = [&](int l) {
+    long long ne = LLONG_MAX;
+    while (true) {
+      const int row = sh.nrow[l][tid];
+      if (row < 0) break;
+      long long st = 0, d = 0;
+#pragma unroll
+      for (int q = 0; q < LM; ++q)
+        if (q == l) {
+          st = pst[q];
+          d = pd[q];
+        }
+      prefetch(l);
+      if (st < 0) continue;  // removed task / absent chain member (start -1)
+      const int rc = __ldg(&p.row_class[row]);
+      long long end = st + d;
+      int cls;
+      if (rc == BD_CPU || rc == BD_CPU_DATALOAD) {
+        if (rc == BD_CPU_DATALOAD && !p.dataload_as_cpu) continue;
+        if (p.gaps_as_cpu_busy) end += __ldg(&p.gap[row]);
+        cls = 0;
+      } else if (rc == BD_GPU) {
+        cls = 1;
+      } else {
+        cls = p.comm_as_gpu ? 1 : 0;
+      }
+      if (end <= st) continue;
+      // absorb the lane's following intervals while they continue this one
+      // back to back with the same class ([a, b) + [b, c) = [a, c) for the
+      // coverage counts): kernels queued on a stream and CPU calls separated
+      // only by their gaps mostly do, so most intervals never reach the merge
+      while (end < T1) {  // (past the window end the merge stops anyway)
+        const int nr = sh.nrow[l][tid];
+        if (nr < 0) break;
+        long long nst = 0, nd = 0;
+#pragma unroll
+        for (int q = 0; q < LM; ++q)
+          if (q == l) {
+            nst = pst[q];
+            nd = pd[q];
+          }
+        if (nst != end) break;
+        const int rc2 = __ldg(&p.row_class[nr]);
+        long long end2 = nst + nd;
+        int cls2;
+        if (rc2 == BD_CPU || rc2 == BD_CPU_DATALOAD) {
+          if (rc2 == BD_CPU_DATALOAD && !p.dataload_as_cpu) break;
+          if (p.gaps_as_cpu_busy) end2 += __ldg(&p.gap[nr]);
+          cls2 = 0;
+        } else if (rc2 == BD_GPU) {
+          cls2 = 1;
+        } else {
+          cls2 = p.comm_as_gpu ? 1 : 0;
+        }
+        if (cls2 != cls || end2 < end) break;
+        end = end2;
+        prefetch(l);
+      }
+      sh.cls[l][tid] = cls;
+      sh.b[l][tid] = end;
+      sh.act[l][tid] = 0;
+      ne = st;
+      break;
+    }
+#pragma unroll
+    for (int q = 0; q < LM; ++q)
+      if (q == l) e[q] = ne;
+  };
+
+#pragma unroll
+  for (int l = 0; l < LM; ++l) {
+    sh.v[l][tid] = 0;
+    sh.len[l][tid] = 0;
+    sh.nrow[l][tid] = -1;
+    sh.act[l][tid] = 0;
+    sh.on[l][tid] = 0;
+    if (!EXACT && l >= p.L) continue;
+    const int c_ix = CH ? p.lane_chain[l] : -1;
+    bool chain_on = false;
+    int len = p.lane_ptr[l + 1] - p.lane_ptr[l];
+    if (CH && c_ix >= 0) {
+      chain_on = p.present == nullptr || p.present[(long long)s * p.n_chains + c_ix] != 0;
+      if (chain_on) len += p.chains[c_ix].B;
+    }
+    sh.len[l][tid] = len;
+    sh.on[l][tid] = chain_on ? 1 : 0;
+    sh.v[l][tid] = len > 0 && T0 > 0 ? bd_seek<CH>(p, l, len, s, chain_on, T0) : 0;
+    prefetch(l);
+    consume(l);
+  }
+  long long acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;  // cpu_only, gpu_only, parallel, idle
+  int cc = 0, gc = 0;
+  long long t = T0;
+  while (true) {
+    int best = 0;
+    long long ev = e[0];
+#pragma unroll
+    for (int l = 1; l < LM; ++l)
+      if (e[l] < ev) {
+        ev = e[l];
+        best = l;
+      }
+    const long long te = min(ev, T1);
+    if (te > t) {
+      const long long span = te - t;
+      if (cc > 0 && gc > 0)
+        acc2 += span;
+      else if (cc > 0)
+        acc0 += span;
+      else if (gc > 0)
+        acc1 += span;
+      else
+        acc3 += span;
+      t = te;
+    }
+    if (ev >= T1) break;
+    const int c = sh.cls[best][tid];
+    if (sh.act[best][tid]) {  // the current interval of lane `best` ends
+      if (c == 0) --cc; else --gc;
+      consume(best);
+    } else {                  // it starts
+      if (c == 0) ++cc; else ++gc;
+      sh.act[best][tid] = 1;
+      const long long b = sh.b[best][tid];
+#pragma unroll
+      for (int q = 0; q < LM; ++q)
+        if (q == best) e[q] = b;
     }
   }
   unsigned long long* u = reinterpret_cast<unsigned long long*>(o);
@@ -342,16 +560,98 @@ cudaError_t launch_bd_sched_rows(const int* schedule, const int* row_lane, const
   return cudaGetLastError();
 }
 
+// Vectorised per-layer busy for int32 durations without dropped tasks: four
+// consecutive scenarios per thread (one 16 B load per row), same run-length
+// accumulation and flushes as layer_busy_kernel.
+__global__ void __launch_bounds__(128) layer_busy4_kernel(const BreakdownParams p) {
+  const int s = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
+  if (s >= p.S) return;
+  int lay = -1;
+  long long ac[4] = {0, 0, 0, 0}, ag[4] = {0, 0, 0, 0};
+  constexpr int U = 8;
+  const int rbeg = blockIdx.y * kLbRowChunk;
+  const int rend = min(p.n, rbeg + kLbRowChunk);
+  const int* dur = static_cast<const int*>(p.dur);
+  auto flush = [&]() {
+    if (lay < 0) return;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+      if (s + i < p.S) {
+        lb_flush(p, lay * 2, ac[i], s + i);
+        lb_flush(p, lay * 2 + 1, ag[i], s + i);
+      }
+  };
+  for (int r0 = rbeg; r0 < rend; r0 += U) {
+    int4 d[U];
+    int ly[U], gpu[U];
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      const int row = r0 + j;
+      ly[j] = -1;
+      gpu[j] = 0;
+      d[j] = make_int4(0, 0, 0, 0);
+      if (row < rend) {
+        const int rc = __ldg(&p.row_class[row]);
+        if (rc != BD_COMM) {
+          ly[j] = __ldg(&p.row_layer[row]);
+          gpu[j] = rc == BD_GPU;
+        }
+        d[j] = __ldcs(reinterpret_cast<const int4*>(dur + (long long)row * p.dld + s));
+      }
+    }
+#pragma unroll
+    for (int j = 0; j < U; ++j) {
+      if (ly[j] < 0) continue;
+      if (ly[j] != lay) {
+        flush();
+        lay = ly[j];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) ac[i] = ag[i] = 0;
+      }
+      const long long v[4] = {d[j].x, d[j].y, d[j].z, d[j].w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i) {
+        if (gpu[j]) ag[i] += v[i];
+        else ac[i] += v[i];
+      }
+    }
+  }
+  flush();
+}
+
 cudaError_t launch_breakdown(const BreakdownParams& p, cudaStream_t stream) {
   if (p.S <= 0) return cudaSuccess;
   if (p.L > kBdMaxLanes) return cudaErrorInvalidValue;
   const int BD = 128;
   const int grid = (p.S + BD - 1) / BD;
   if (p.parts) {
-    bd_prepare_kernel<<<std::min(grid, 148 * 16), BD, 0, stream>>>(p);
+    bd_zero_kernel<<<std::min(grid, 148 * 16), BD, 0, stream>>>(p);
+    note_launch();
+    if ((p.n + kBdNegRows - 1) / kBdNegRows > 65535) return cudaErrorInvalidValue;
+    bd_negative_kernel<<<dim3(grid, (p.n + kBdNegRows - 1) / kBdNegRows), BD, 0, stream>>>(p);
     note_launch();
     const dim3 g2(grid, p.K);
     const bool ch = p.n_chains > 0;
+    static_assert(kBdLeanBD == 128, "lean kernel block = BD");
+    if (p.L <= 8 && getenv("DDSIM_BD_OLD") == nullptr) {
+#define BD_LEAN(LM, EX)                                                      \
+  do {                                                                       \
+    if (ch)                                                                  \
+      breakdown_lean_kernel<LM, EX, true><<<g2, BD, 0, stream>>>(p);         \
+    else                                                                     \
+      breakdown_lean_kernel<LM, EX, false><<<g2, BD, 0, stream>>>(p);        \
+  } while (0)
+      switch (p.L) {
+        case 1: BD_LEAN(1, true); break;
+        case 2: BD_LEAN(2, true); break;
+        case 3: BD_LEAN(3, true); break;
+        case 4: BD_LEAN(4, true); break;
+        default: BD_LEAN(8, false);
+      }
+#undef BD_LEAN
+      note_launch();
+      goto layers;
+    }
 #define BD_LAUNCH(LM, EX)                                                     \
   do {                                                                        \
     if (ch)                                                                   \
@@ -375,12 +675,19 @@ cudaError_t launch_breakdown(const BreakdownParams& p, cudaStream_t stream) {
 #undef BD_LAUNCH
     note_launch();
   }
+layers:
   if (p.layer_busy && p.row_layer) {
     cudaError_t e = launch_fill_i64(p.layer_busy, 0, (long long)p.n_layers * 2 * p.S, stream);
     if (e != cudaSuccess) return e;
     if ((p.n + kLbRowChunk - 1) / kLbRowChunk > 65535) return cudaErrorInvalidValue;  // > 134M rows
     const dim3 g3(grid, (p.n + kLbRowChunk - 1) / kLbRowChunk);
-    if (p.start_may_be_neg)
+    const bool vec4 = !p.start_may_be_neg && p.dkind == 1 && p.dld % 4 == 0 &&
+                      reinterpret_cast<uintptr_t>(p.dur) % 16 == 0 &&
+                      getenv("DDSIM_BD_LB_SCALAR") == nullptr;
+    if (vec4) {
+      const int g4 = ((p.S + 3) / 4 + BD - 1) / BD;
+      layer_busy4_kernel<<<dim3(g4, g3.y), BD, 0, stream>>>(p);
+    } else if (p.start_may_be_neg)
       layer_busy_kernel<true><<<g3, BD, 0, stream>>>(p);
     else
       layer_busy_kernel<false><<<g3, BD, 0, stream>>>(p);

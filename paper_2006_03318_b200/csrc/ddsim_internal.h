@@ -321,6 +321,7 @@ struct BreakdownParams {
   int n_layers;
   int start_may_be_neg;     // removal steps / permutable chains: start -1 marks a dropped task
   const int* srows;         // [S][n] per-scenario lane sequences (list-scheduled) or null
+  int stream_loads;         // experiments: evict-first start loads (DDSIM_BD_STREAM)
 };
 cudaError_t launch_breakdown(const BreakdownParams& p, cudaStream_t stream);
 cudaError_t launch_bd_sched_rows(const int* schedule, const int* row_lane, const int* lane_ptr,

@@ -2610,15 +2610,17 @@ int breakdown_impl(const ks_graph* g, const ks_scenarios_desc* sc, const int64_t
   p.bad = T.scratch<int>((size_t)S);
   p.start_may_be_neg = (g->n_chains > 0 || T.has_remove) ? 1 : 0;
   {
-    // time windows per scenario: enough (scenario, window) threads to fill the
-    // GPU, at least ~512 rows of work per window
+    // time windows per scenario: (scenario, window) threads for ~4 waves of
+    // the lean merge (measured at 65,536 x 100k: K = 5 / 10 / 20 -> 92 / 67 /
+    // 76 ms), at least ~512 rows of work per window
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device);
-    const long long target = (long long)nsm * 2048;
+    const long long target = (long long)nsm * 4096;
     long long K = (target + S - 1) / S;
     K = std::min<long long>(K, std::max(1, g->n / 512));
     p.K = (int)std::max<long long>(1, std::min<long long>(K, 65535));
     if (const char* e = getenv("DDSIM_BD_WINDOWS")) p.K = std::max(1, atoi(e));
+    p.stream_loads = getenv("DDSIM_BD_STREAM") != nullptr;
   }
   if (layer_busy && bd->row_layer) {
     p.row_layer = T.up(bd->row_layer, (size_t)g->n);
