@@ -785,7 +785,56 @@ def _sorted_edges(src, dst, kind):
     return np.asarray(src)[key], np.asarray(dst)[key], np.asarray(kind)[key]
 
 
-def ingest_parity(ct, res, tag, sample_cpu: int = 2000) -> dict:
+def frozen_parity(cols, sa, da, gap, fz) -> dict:
+    """The device-frozen graph against the oracle (checker): its row order is a
+    topological order of the oracle's build_graph edges, and Alg. 1 on the
+    oracle's graph (sim.py:89-142, base durations) gives the start times,
+    makespan and lane busy the device simulates on the frozen graph (the first
+    simulate builds the kernel programs)."""
+    import ctypes as C
+
+    sys.path.insert(0, str(ROOT / "oracle"))
+    import oracle as O
+    from paper_2006_03318_b200.batch import ScenarioTable, simulate_batch
+
+    t0 = time.perf_counter()
+    n = int(cols.n)
+    pos = np.empty(n, np.int64)
+    pos[fz.order] = np.arange(n)
+    if fz.n_ordered != n or not np.all(pos[sa] < pos[da]):
+        raise AssertionError("device freeze order is not topological on the oracle's edges")
+    ids = np.asarray(cols.id, np.int64)
+    rank = np.empty(n, np.int32)
+    rank[np.argsort(ids, kind="stable")] = np.arange(n, dtype=np.int32)
+    og = O.OracleGraph(ids=ids, lanes=list(cols.lanes), dur=np.asarray(cols.duration, np.int64),
+                       gap=np.asarray(gap, np.int64), ready=np.zeros(n, np.int64),
+                       lane=np.asarray(cols.lane, np.int32), rank=rank,
+                       prio=np.zeros(n, np.int32), flags=np.zeros(n, np.uint8),
+                       vrank=np.full(n, -1, np.int32), src=np.asarray(sa, np.int32),
+                       dst=np.asarray(da, np.int32))
+    g = og._c()
+    start = np.zeros(n, np.int64)
+    trace = np.zeros(n, np.int32)
+    lb = np.zeros(max(len(og.lanes), 1), np.int64)
+    ms = np.zeros(1, np.int64)
+    if O.lib().ora_simulate(C.byref(g), O.POL["default"], start.ctypes.data, trace.ctypes.data,
+                            lb.ctypes.data, ms.ctypes.data) != n:
+        raise AssertionError("oracle deadlock on the ingest graph")
+    t1 = time.perf_counter()
+    res = simulate_batch(fz, ScenarioTable(n_scenarios=1))
+    t2 = time.perf_counter()
+    dev_start = np.empty(n, np.int64)
+    dev_start[fz.order] = res.start[:, 0]
+    if int(res.makespan[0]) != int(ms[0]) or not np.array_equal(dev_start, start) \
+            or not np.array_equal(res.lane_busy[0], lb[:fz.L]):
+        raise AssertionError("simulate on the device-frozen graph differs from the oracle")
+    return {"frozen_order_topological_on_oracle_edges": True,
+            "simulate_base_vs_oracle": "every start, makespan, lane busy",
+            "oracle_simulate_s": round(t1 - t0, 2),
+            "first_simulate_incl_program_build_s": round(t2 - t1, 2)}
+
+
+def ingest_parity(ct, res, tag, sample_cpu: int = 2000, fz=None) -> dict:
     """Config-5 output against the oracle (checker, outside the timed region):
     the whole edge multiset (src, dst, kind), every gap and every launcher of
     build_graph over all records; layer tags of a random sample of CPU events
@@ -816,10 +865,13 @@ def ingest_parity(ct, res, tag, sample_cpu: int = 2000) -> dict:
     gpu = np.nonzero((np.asarray(res.launcher) >= 0))[0]
     if not np.array_equal(np.asarray(tag)[gpu], np.asarray(tag)[np.asarray(res.launcher)[gpu]]):
         raise AssertionError("GPU events do not inherit their launcher's layer")
-    return {"edges": int(len(b[0])), "gaps_and_launchers": int(cols.n),
-            "layer_tags_sampled_cpu_events": int(len(pick)),
-            "checker": "oracle/ddsim_oracle.c build_graph (all records) + map_layers (sample)",
-            "check_s": round(time.perf_counter() - t0, 2)}
+    out = {"edges": int(len(b[0])), "gaps_and_launchers": int(cols.n),
+           "layer_tags_sampled_cpu_events": int(len(pick)),
+           "checker": "oracle/ddsim_oracle.c build_graph (all records) + map_layers (sample)",
+           "check_s": round(time.perf_counter() - t0, 2)}
+    if fz is not None:
+        out["frozen"] = frozen_parity(cols, sa, da, gap, fz)
+    return out
 
 
 def _ingest_cpu_baseline(n_sample: int = 1_000_000) -> dict:
@@ -877,7 +929,7 @@ def run_ingest(args):
         t0 = time.perf_counter()
         ct = load_trace_columns(text)
         t1 = time.perf_counter()
-        res = ingest_arrays(ct.cols)
+        res = ingest_arrays(ct.cols, keep_device=True)
         t2 = time.perf_counter()
         tag_m, tags = ct.marker_tags()
         tag = map_layers_arrays(ct.cols, res.launcher, ct.m_lane, ct.m_start, ct.m_end, tag_m)
@@ -898,7 +950,7 @@ def run_ingest(args):
     n = int(ct.n_events)
     per = statistics.median(times)
     st = {k: statistics.median(v) for k, v in stages.items()}
-    parity = ingest_parity(ct, res, tag)
+    parity = ingest_parity(ct, res, tag, fz=fz)
     dev_s = st["ingest_s"] + st["layer_map_s"]
     peak, peak_src = _peaks()
     col_bytes = 41 * n
@@ -920,11 +972,10 @@ def run_ingest(args):
                              "column transfers; the step is host-bound (parse + freeze)"},
         "cpu_baseline": None if args.no_cpu_baseline else _ingest_cpu_baseline(),
         "e2e": {"value": n / per, "unit": "records/s", "h2d_bytes_per_step": col_bytes,
-                "d2h_bytes_per_step": int(res.edge_src.nbytes + res.edge_dst.nbytes +
-                                          res.edge_kind.nbytes + res.gap.nbytes +
-                                          res.launcher.nbytes),
-                "api": "columnar.load_trace_columns -> ingest_arrays -> map_layers_arrays -> "
-                       "frozen_from_ingest (host text in, device frozen graph out)"},
+                "d2h_bytes_per_step": int(res.launcher.nbytes + 4 * n),
+                "api": "columnar.load_trace_columns -> ingest_arrays(keep_device) -> "
+                       "map_layers_arrays -> frozen_from_ingest (host text in, device frozen "
+                       "graph out: ks_graph_create_from_ingest)"},
         "parity_checked": parity,
         "gpu_launches": launches // max(args.steps, 1),
         "clocks": clk,

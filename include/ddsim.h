@@ -127,6 +127,11 @@ typedef struct {
   int32_t n_carries;           /* values read only in it, live across its start */
 } ks_graph_info;
 
+/* Lane-chained flag and topological-prefix length, without building the
+ * kernel programs (ks_graph_get_info, ks_graph_levels, ks_simulate*,
+ * ks_breakdown and ks_toposort build them on first use). */
+int ks_graph_shape(const ks_graph* g, int32_t* chained, int32_t* n_ordered);
+
 /* Build the device-resident frozen graph on `device`.  Frozen row r holds the
  * task order_out[r] (dense input index); rows 0..n_ordered-1 are a topological
  * order.  order_out may be NULL. */
@@ -305,6 +310,27 @@ typedef struct {
 
 int ks_ingest(const ks_trace_cols* tc, int device, int check_overlaps,
               ks_ingest_out* out);
+
+/* ks_ingest that keeps its edges, lane order and gaps on the device for
+ * ks_graph_create_from_ingest (no host round trip of the graph): `out`
+ * receives n_edges, lane_order_ptr and launcher only (its edge / lane order /
+ * gap buffers may be NULL).  Free *dev_out with ks_ingest_dev_free. */
+typedef struct ks_ingest_dev ks_ingest_dev;
+int ks_ingest_keep(const ks_trace_cols* tc, int device, int check_overlaps,
+                   ks_ingest_out* out, ks_ingest_dev** dev_out);
+/* Host copies of a kept ingest's edges / lane order / gaps (any may be NULL). */
+int ks_ingest_dev_copy(const ks_ingest_dev* h, int32_t* edge_src, int32_t* edge_dst,
+                       uint8_t* edge_kind, int32_t* lane_order, int64_t* gap);
+void ks_ingest_dev_free(ks_ingest_dev* h);
+/* The frozen graph of a kept ingest (build_graph -> DependencyGraph freeze,
+ * graph.py:75-148, 198-245), compiled on its device: unique-edge and
+ * predecessor CSR by radix sort, a trace-time topological order verified on
+ * every edge (else the host compiler orders it), frozen rows and per-row
+ * arrays gathered on the device.  id_rank: HOST [n] rank of the event ids
+ * (NULL = ids ascending in event order); flags: HOST [n] KS_TASK_* or NULL.
+ * Kernel programs are built on first use (ks_graph_shape is free). */
+int ks_graph_create_from_ingest(const ks_ingest_dev* h, const int32_t* id_rank,
+                                const uint8_t* flags, ks_graph** out, int32_t* order_out);
 
 /* ---- layer mapping (layers.py:30-81) ------------------------------------ */
 typedef struct {

@@ -152,6 +152,12 @@ class TraceWriteDesc(C.Structure):
 _SIGNATURES = [
     ("ks_graph_create", C.c_int, [C.POINTER(GraphDesc), C.c_int, C.POINTER(P), P]),
     ("ks_graph_get_info", C.c_int, [P, C.POINTER(GraphInfo)]),
+    ("ks_ingest_keep", C.c_int, [C.POINTER(TraceCols), C.c_int, C.c_int, C.POINTER(IngestOut),
+                                 C.POINTER(C.c_void_p)]),
+    ("ks_ingest_dev_copy", C.c_int, [P, P, P, P, P, P]),
+    ("ks_ingest_dev_free", None, [P]),
+    ("ks_graph_create_from_ingest", C.c_int, [P, P, P, C.POINTER(C.c_void_p), P]),
+    ("ks_graph_shape", C.c_int, [P, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]),
     ("ks_graph_levels", C.c_int, [P, P]),
     ("ks_graph_destroy", C.c_int, [P]),
     ("ks_simulate", C.c_int, [P, C.POINTER(ScenariosDesc), C.c_int, C.c_int, C.POINTER(SimOut), P]),

@@ -283,7 +283,8 @@ def ingest_document(text, *, strict: bool = False, check_overlaps: bool = False,
     from .ingest import ingest_arrays, map_layers_arrays
 
     ct = load_trace_columns(text, threads=threads)
-    res = ingest_arrays(ct.cols, strict=strict, check_overlaps=check_overlaps, device=device)
+    res = ingest_arrays(ct.cols, strict=strict, check_overlaps=check_overlaps, device=device,
+                        keep_device=freeze)
     tag_m, tags = ct.marker_tags()
     tag = map_layers_arrays(ct.cols, res.launcher, ct.m_lane, ct.m_start, ct.m_end, tag_m,
                             device=device)
@@ -301,12 +302,16 @@ def frozen_from_ingest(ct: ColumnarTrace, res, device: int | None = None):
     flags = ((c.kind == KIND_CODE[TaskKind.COMM]).astype(np.uint8) * N.KS_TASK_COMM
              | (vdnn_name[ct.name_id] if n else np.zeros(0, bool)).astype(np.uint8)
              * N.KS_TASK_VDNN_MALLOC)
+    dataload = c.kind == KIND_CODE[TaskKind.DATA_LOAD]
+    if getattr(res, "handle", None) is not None:  # KeptIngest: freeze on the device
+        return FrozenGraph.from_device_ingest(res, ids=c.id, duration=c.duration, lane=c.lane,
+                                              lanes=c.lanes, flags=flags, dataload=dataload)
     return FrozenGraph(ids=c.id, duration=c.duration, gap=res.gap, ready=np.zeros(n, np.int64),
                        lane=c.lane, priority=np.zeros(n, np.int32), flags=flags,
                        group=np.zeros(n, np.uint32), edge_src=res.edge_src, edge_dst=res.edge_dst,
                        lane_order_ptr=res.lane_order_ptr, lane_order=res.lane_order,
                        lanes=c.lanes, device=N.env_device() if device is None else device,
-                       dataload=c.kind == KIND_CODE[TaskKind.DATA_LOAD])
+                       dataload=dataload)
 
 
 __all__ = ["ColumnarTrace", "ColumnarIngest", "load_trace_columns", "dump_trace_columns",

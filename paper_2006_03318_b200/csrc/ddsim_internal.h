@@ -4,6 +4,7 @@
 #include <cuda.h>
 #include <stdint.h>
 
+#include <string>
 #include <vector>
 
 #include "../../include/ddsim.h"
@@ -346,4 +347,47 @@ void note_launch(int n = 1);
 // call re-maps: measured +15 ms on the first config-4 launch after a sync).
 void keep_device_pool(int device);
 
+// Ingest outputs kept on the device (ks_ingest_keep) for the device freeze.
+struct IngestDev {
+  int device = 0;
+  long long n = 0, m = 0;
+  int L = 0;
+  int* lane = nullptr;         // [n] event lane
+  long long* start = nullptr;  // [n]
+  long long* dur = nullptr;    // [n]
+  long long* gap = nullptr;    // [n] compute_gaps
+  int* src = nullptr;          // [m] edges (event indices), multiset
+  int* dst = nullptr;
+  unsigned char* ekind = nullptr;  // [m] KS_EDGE_*
+  int* lane_order = nullptr;   // [n] events per lane by (start, id)
+  std::vector<int> lane_order_ptr;         // [L+1]
+  std::vector<unsigned char> lane_class;   // [L] 0 cpu, 1 gpu, 2 comm
+  void release();
+};
+
+// Device freeze of an ingested trace (freeze.cu); the device arrays pass to
+// the graph (cudaMalloc, freed by free_graph).
+struct DeviceFreeze {
+  long long n = 0, m_unique = 0;
+  bool ok = false;                // the relaxed trace-time order is topological
+  int rounds = 0;                 // relaxation rounds
+  std::vector<int> order;         // host copy: row -> event
+  int* order_d = nullptr;
+  unsigned long long* ukeys = nullptr;  // [m_unique] (u << 32 | v) ascending
+  unsigned long long* pkeys = nullptr;  // [m_unique] (v << 32 | u) ascending
+  int *child_ptr = nullptr, *child = nullptr, *indeg = nullptr;  // rows, multiset
+  int *lane_r = nullptr, *rank_r = nullptr, *prio_r = nullptr;
+  long long *dur_r = nullptr, *gap_r = nullptr, *ready_r = nullptr;
+  unsigned char* flags_r = nullptr;
+  unsigned* group_r = nullptr;
+};
+int freeze_from_ingest(const IngestDev& I, const int32_t* id_rank_h, const uint8_t* flags_h,
+                       DeviceFreeze& F, std::string& err);
+void free_device_freeze(DeviceFreeze& F);
+
 }  // namespace ddsim
+
+// C-ABI handle of a kept ingest (include/ddsim.h: ks_ingest_keep)
+struct ks_ingest_dev {
+  ddsim::IngestDev d;
+};

@@ -24,6 +24,7 @@
 #include <queue>
 #include <string>
 #include <exception>
+#include <memory>
 #include <mutex>
 #include <thread>
 #include <vector>
@@ -176,8 +177,36 @@ constexpr int kShortRange = 48;
 
 using namespace ddsim;
 
+// What build_programs reads: owned copies of the descriptor arrays it uses
+// (the caller's arrays need only live until ks_graph_create returns) and the
+// compile_graph intermediates (unique edges, predecessor lists, record order).
+struct LazyPrograms {
+  int n = 0, L = 0, NC = 0, R = 0;
+  long long E = 0;
+  bool chained = false;
+  ks_graph_desc desc;
+  hvec<int64_t> duration, gap, ready;
+  hvec<int32_t> lane, lane_order_ptr, lane_order, chain_ptr, chain_member, chain_head, chain_tail;
+  hvec<uint32_t> group;
+  hvec<unsigned long long> keys;
+  hvec<int> optr, pptr, padj, corder, rec_first_row, ch_lane, tail_of, cptr, cadj;
+  // graphs frozen on the device (ks_graph_create_from_ingest): the host arrays
+  // above are filled from these on first use (materialize_from_device)
+  bool from_device = false;
+  unsigned long long* d_ukeys = nullptr;  // (u << 32 | v) unique, ascending
+  unsigned long long* d_pkeys = nullptr;  // (v << 32 | u) unique, ascending
+  int* d_lane_order = nullptr;
+  long long m_unique = 0;
+  ~LazyPrograms() {
+    if (d_ukeys) cudaFree(d_ukeys);
+    if (d_pkeys) cudaFree(d_pkeys);
+    if (d_lane_order) cudaFree(d_lane_order);
+  }
+};
 struct ks_graph {
   int device = 0;
+  std::once_flag programs_once;
+  std::unique_ptr<LazyPrograms> lazy;  // until build_programs
   int n = 0, L = 0;
   int n_ordered = 0;
   int n_edges_unique = 0;
@@ -303,6 +332,8 @@ struct HostTimer {  // DDSIM_INGEST_TIMING=1: wall time of compile_graph's secti
     t0 = t1;
   }
 };
+
+void ensure_programs(const ks_graph* g);
 
 void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   HostTimer gt;
@@ -624,6 +655,160 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   g->rows_are_records = (NC == 0);
 
   gt.mark("rows");
+  // ---- list-scheduler arrays and per-row device arrays (eager: every path) --
+  {
+
+  // ---- list-scheduler arrays (frozen rows, multiset edges) -------------------
+  hvec<int> ch_ptr(n + 1, 0), ch_adj(E), indeg(n, 0);
+  hvec<int> lane_r(n), rank_r(n), prio_r(n);
+  hvec<long long> dur_r(n), gap_r(n), ready_r(n);
+  hvec<unsigned char> flags_r(n);
+  hvec<unsigned> group_r(n);
+  hvec<int> esr(E), edr(E);  // edge endpoints as frozen rows
+  host_parallel_for(E, [&](long long b, long long e) {
+    for (long long k = b; k < e; ++k) {
+      esr[k] = g->row_of[d->edge_src[k]];
+      edr[k] = g->row_of[d->edge_dst[k]];
+    }
+  });
+  // multiset CSR by parallel atomic count / scatter; each child list is then
+  // sorted so the layout is deterministic (the schedulers pick by key, not by
+  // list position)
+  host_parallel_for(E, [&](long long b, long long e) {
+    for (long long k = b; k < e; ++k) {
+      __atomic_fetch_add(&ch_ptr[esr[k] + 1], 1, __ATOMIC_RELAXED);
+      __atomic_fetch_add(&indeg[edr[k]], 1, __ATOMIC_RELAXED);
+    }
+  });
+  for (int i = 0; i < n; ++i) ch_ptr[i + 1] += ch_ptr[i];
+  {
+    hvec<int> fill(ch_ptr.begin(), ch_ptr.end() - 1);
+    host_parallel_for(E, [&](long long b, long long e) {
+      for (long long k = b; k < e; ++k) ch_adj[__atomic_fetch_add(&fill[esr[k]], 1, __ATOMIC_RELAXED)] = edr[k];
+    });
+    host_parallel_for(n, [&](long long b, long long e) {
+      for (long long r = b; r < e; ++r)
+        if (ch_ptr[r + 1] - ch_ptr[r] > 1) std::sort(ch_adj.begin() + ch_ptr[r], ch_adj.begin() + ch_ptr[r + 1]);
+    });
+  }
+  host_parallel_for(n, [&](long long b, long long e) {
+  for (int r = (int)b; r < (int)e; ++r) {
+    const int t = g->order[r];
+    lane_r[r] = d->lane[t];
+    rank_r[r] = d->id_rank[t];
+    prio_r[r] = d->priority ? d->priority[t] : 0;
+    dur_r[r] = d->duration[t];
+    gap_r[r] = d->gap[t];
+    ready_r[r] = d->ready_time ? d->ready_time[t] : 0;
+    flags_r[r] = d->flags ? d->flags[t] : 0;
+    group_r[r] = d->group ? d->group[t] : 0u;
+  }
+  });
+
+  g->d_child_ptr = dev_upload(ch_ptr);
+  g->d_child = dev_upload(ch_adj);
+  g->d_indeg = dev_upload(indeg);
+  g->d_lane = dev_upload(lane_r);
+  g->d_dur = dev_upload(dur_r);
+  g->d_gap = dev_upload(gap_r);
+  g->d_ready = dev_upload(ready_r);
+  g->d_rank = dev_upload(rank_r);
+  g->d_prio = dev_upload(prio_r);
+  g->d_flags = dev_upload(flags_r);
+  g->d_group = dev_upload(group_r);
+  
+  }
+  gt.mark("row arrays");
+  // ---- what the program builders read, kept for build_programs -----------------
+  {
+    auto st = std::make_unique<LazyPrograms>();
+    LazyPrograms& S = *st;
+    S.n = n;
+    S.L = L;
+    S.E = E;
+    S.NC = NC;
+    S.R = R;
+    S.chained = chained;
+    auto own = [&](auto& dst, const auto* src, size_t cnt) {
+      if (!src) return;
+      dst.resize(cnt);
+      host_parallel_for((long long)cnt, [&](long long b, long long e) {
+        std::copy(src + b, src + e, dst.begin() + b);
+      });
+    };
+    own(S.duration, d->duration, (size_t)n);
+    own(S.gap, d->gap, (size_t)n);
+    bool any_ready = false;
+    for (int i = 0; i < n && d->ready_time && !any_ready; ++i) any_ready = d->ready_time[i] != 0;
+    if (any_ready) own(S.ready, d->ready_time, (size_t)n);
+    own(S.lane, d->lane, (size_t)n);
+    if (d->group) own(S.group, d->group, (size_t)n);
+    if (d->lane_order_ptr) {
+      own(S.lane_order_ptr, d->lane_order_ptr, (size_t)L + 1);
+      const long long K0 = L > 0 ? d->lane_order_ptr[0] : 0, K = L > 0 ? d->lane_order_ptr[L] : 0;
+      S.lane_order.resize((size_t)std::max(0LL, K));
+      if (K > K0) std::copy(d->lane_order + K0, d->lane_order + K, S.lane_order.begin() + K0);
+    }
+    if (NC > 0) {
+      own(S.chain_ptr, d->chain_ptr, (size_t)NC + 1);
+      own(S.chain_member, d->chain_member, (size_t)S.chain_ptr[NC]);
+      if (d->chain_head) own(S.chain_head, d->chain_head, (size_t)NC);
+      if (d->chain_tail) own(S.chain_tail, d->chain_tail, (size_t)NC);
+    }
+    memset(&S.desc, 0, sizeof(S.desc));
+    S.desc.n_tasks = n;
+    S.desc.n_lanes = L;
+    S.desc.duration = S.duration.data();
+    S.desc.gap = S.gap.data();
+    S.desc.ready_time = S.ready.empty() ? nullptr : S.ready.data();
+    S.desc.lane = S.lane.data();
+    S.desc.group = S.group.empty() ? nullptr : S.group.data();
+    S.desc.lane_order_ptr = S.lane_order_ptr.empty() ? nullptr : S.lane_order_ptr.data();
+    S.desc.lane_order = S.lane_order.data();
+    S.desc.n_chains = NC;
+    S.desc.chain_ptr = S.chain_ptr.data();
+    S.desc.chain_member = S.chain_member.data();
+    S.desc.chain_head = S.chain_head.empty() ? nullptr : S.chain_head.data();
+    S.desc.chain_tail = S.chain_tail.empty() ? nullptr : S.chain_tail.data();
+    S.keys = std::move(keys);
+    S.optr = std::move(optr);
+    S.pptr = std::move(pptr);
+    S.padj = std::move(padj);
+    S.corder = std::move(corder);
+    S.rec_first_row = std::move(rec_first_row);
+    S.ch_lane = std::move(ch_lane);
+    S.tail_of = std::move(tail_of);
+    S.cptr = std::move(cptr);
+    S.cadj = std::move(cadj);
+    g->lazy = std::move(st);
+  }
+  gt.mark("keep");
+  if (getenv("DDSIM_EAGER_PROGRAMS") != nullptr) ensure_programs(g);
+}
+
+// The kernel programs of a frozen graph -- general records (maxplus.cu),
+// dense register-forwarding program (maxplus_dense.cu), lane-register program
+// (maxplus_lanes.cu), breakdown lane sequences -- are built on the first call
+// that needs them (ensure_programs), from the graph compile_graph kept.
+void build_programs(ks_graph* g, LazyPrograms& S) {
+  HostTimer gt;
+  const ks_graph_desc* d = &S.desc;
+  const int n = S.n, L = S.L, NC = S.NC, R = S.R;
+  const long long E = S.E;
+  (void)E;
+  const bool chained = S.chained;
+  const int NN = n + NC;
+  (void)NN;
+  auto& keys = S.keys;
+  auto& optr = S.optr;
+  auto& pptr = S.pptr;
+  auto& padj = S.padj;
+  auto& corder = S.corder;
+  auto& rec_first_row = S.rec_first_row;
+  auto& ch_lane = S.ch_lane;
+  auto& tail_of = S.tail_of;
+  auto& cptr = S.cptr;
+  auto& cadj = S.cadj;
   // ---- levels ------------------------------------------------------------------
   // Without chains: pull form in record space -- level(i) = 1 + max over the
   // record's predecessors, which are recent records (cache-resident); the
@@ -1415,70 +1600,8 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
   }
 
   });
-  sect.run("listsched", [&] {
-  // ---- list-scheduler arrays (frozen rows, multiset edges) -------------------
-  hvec<int> ch_ptr(n + 1, 0), ch_adj(E), indeg(n, 0);
-  hvec<int> lane_r(n), rank_r(n), prio_r(n);
-  hvec<long long> dur_r(n), gap_r(n), ready_r(n);
-  hvec<unsigned char> flags_r(n);
-  hvec<unsigned> group_r(n);
-  hvec<int> esr(E), edr(E);  // edge endpoints as frozen rows
-  host_parallel_for(E, [&](long long b, long long e) {
-    for (long long k = b; k < e; ++k) {
-      esr[k] = g->row_of[d->edge_src[k]];
-      edr[k] = g->row_of[d->edge_dst[k]];
-    }
-  });
-  // multiset CSR by parallel atomic count / scatter; each child list is then
-  // sorted so the layout is deterministic (the schedulers pick by key, not by
-  // list position)
-  host_parallel_for(E, [&](long long b, long long e) {
-    for (long long k = b; k < e; ++k) {
-      __atomic_fetch_add(&ch_ptr[esr[k] + 1], 1, __ATOMIC_RELAXED);
-      __atomic_fetch_add(&indeg[edr[k]], 1, __ATOMIC_RELAXED);
-    }
-  });
-  for (int i = 0; i < n; ++i) ch_ptr[i + 1] += ch_ptr[i];
-  {
-    hvec<int> fill(ch_ptr.begin(), ch_ptr.end() - 1);
-    host_parallel_for(E, [&](long long b, long long e) {
-      for (long long k = b; k < e; ++k) ch_adj[__atomic_fetch_add(&fill[esr[k]], 1, __ATOMIC_RELAXED)] = edr[k];
-    });
-    host_parallel_for(n, [&](long long b, long long e) {
-      for (long long r = b; r < e; ++r)
-        if (ch_ptr[r + 1] - ch_ptr[r] > 1) std::sort(ch_adj.begin() + ch_ptr[r], ch_adj.begin() + ch_ptr[r + 1]);
-    });
-  }
-  host_parallel_for(n, [&](long long b, long long e) {
-  for (int r = (int)b; r < (int)e; ++r) {
-    const int t = g->order[r];
-    lane_r[r] = d->lane[t];
-    rank_r[r] = d->id_rank[t];
-    prio_r[r] = d->priority ? d->priority[t] : 0;
-    dur_r[r] = d->duration[t];
-    gap_r[r] = d->gap[t];
-    ready_r[r] = d->ready_time ? d->ready_time[t] : 0;
-    flags_r[r] = d->flags ? d->flags[t] : 0;
-    group_r[r] = d->group ? d->group[t] : 0u;
-  }
-  });
-
-  g->d_child_ptr = dev_upload(ch_ptr);
-  g->d_child = dev_upload(ch_adj);
-  g->d_indeg = dev_upload(indeg);
-  g->d_lane = dev_upload(lane_r);
-  g->d_dur = dev_upload(dur_r);
-  g->d_gap = dev_upload(gap_r);
-  g->d_ready = dev_upload(ready_r);
-  g->d_rank = dev_upload(rank_r);
-  g->d_prio = dev_upload(prio_r);
-  g->d_flags = dev_upload(flags_r);
-  g->d_group = dev_upload(group_r);
-  });
   sect.join();
   gt.mark("programs");
-  // ---- upload -----------------------------------------------------------------
-  gt.mark("upload");
   // ---- breakdown geometry -------------------------------------------------------
   for (int i = 0; i < n; ++i)
     if (d->gap[i] < 0) g->gap_nonneg = false;
@@ -1522,6 +1645,89 @@ void compile_graph(const ks_graph_desc* d, ks_graph* g) {
       g->d_bd_member_rows = dev_upload(mrows);
     }
   }
+}
+
+// Host arrays of a device-frozen graph (no chains, rows == records): the
+// descriptor columns from the per-row device arrays, the unique-edge and
+// predecessor lists from the sorted device keys.
+void materialize_from_device(ks_graph* g, LazyPrograms& S) {
+  const int n = g->n, L = g->L;
+  const long long nu = S.m_unique;
+  auto down = [&](auto& h, const auto* d, size_t cnt) {
+    h.resize(cnt);
+    if (cnt) CUDA_TRY(cudaMemcpy(h.data(), d, cnt * sizeof(h[0]), cudaMemcpyDeviceToHost));
+  };
+  hvec<int64_t> dur_r, gap_r;
+  hvec<int> lane_r, rank_r;
+  down(dur_r, g->d_dur, (size_t)n);
+  down(gap_r, g->d_gap, (size_t)n);
+  down(lane_r, g->d_lane, (size_t)n);
+  down(rank_r, g->d_rank, (size_t)n);
+  down(S.keys, S.d_ukeys, (size_t)nu);
+  hvec<unsigned long long> pk;
+  down(pk, S.d_pkeys, (size_t)nu);
+  down(S.lane_order, S.d_lane_order, (size_t)n);
+  g->row_of.resize(n);
+  g->rank_row.resize(n);
+  S.duration.resize(n);
+  S.gap.resize(n);
+  S.lane.resize(n);
+  host_parallel_for(n, [&](long long b, long long e) {
+    for (int r = (int)b; r < (int)e; ++r) {
+      const int t = g->order[r];
+      g->row_of[t] = r;
+      g->rank_row[r] = rank_r[r];
+      S.duration[t] = dur_r[r];
+      S.gap[t] = gap_r[r];
+      S.lane[t] = lane_r[r];
+    }
+  });
+  S.optr.assign(n + 1, 0);
+  S.pptr.assign(n + 1, 0);
+  for (long long q = 0; q < nu; ++q) {
+    S.optr[(S.keys[q] >> 32) + 1]++;
+    S.pptr[(pk[q] >> 32) + 1]++;
+  }
+  for (int i = 0; i < n; ++i) {
+    S.optr[i + 1] += S.optr[i];
+    S.pptr[i + 1] += S.pptr[i];
+  }
+  S.padj.resize(nu);
+  S.cadj.resize(nu);
+  host_parallel_for(nu, [&](long long b, long long e) {
+    for (long long q = b; q < e; ++q) {
+      S.padj[q] = (int)(pk[q] & 0xffffffffu);
+      S.cadj[q] = (int)(S.keys[q] & 0xffffffffu);
+    }
+  });
+  S.cptr = S.optr;
+  S.corder.assign(g->order.begin(), g->order.end());
+  S.rec_first_row.resize(n);
+  std::iota(S.rec_first_row.begin(), S.rec_first_row.end(), 0);
+  memset(&S.desc, 0, sizeof(S.desc));
+  S.desc.n_tasks = n;
+  S.desc.n_lanes = L;
+  S.desc.duration = S.duration.data();
+  S.desc.gap = S.gap.data();
+  S.desc.lane = S.lane.data();
+  S.desc.lane_order_ptr = S.lane_order_ptr.data();
+  S.desc.lane_order = S.lane_order.data();
+  S.from_device = false;
+}
+
+void ensure_programs(const ks_graph* gc) {
+  ks_graph* g = const_cast<ks_graph*>(gc);
+  std::call_once(g->programs_once, [g] {
+    if (!g->lazy) return;
+    DevGuard guard(g->device);
+    HostTimer gt;
+    if (g->lazy->from_device) {
+      materialize_from_device(g, *g->lazy);
+      gt.mark("materialize");
+    }
+    build_programs(g, *g->lazy);
+    g->lazy.reset();
+  });
 }
 
 void free_graph(ks_graph* g) {
@@ -1705,6 +1911,7 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
                   const ks_sim_out* out, cudaStream_t stream) {
   if (!g || !sc || !out) fail(KS_ERR_INVALID, "null argument");
   if (g->device < 0) fail(KS_ERR_NO_DEVICE, "graph was compiled without a device");
+  ensure_programs(g);
   const int S = sc->n_scenarios;
   if (S <= 0) fail(KS_ERR_INVALID, "n_scenarios must be positive");
   if (policy < 0 || policy > 2) fail(KS_ERR_INVALID, "unknown policy");
@@ -2191,8 +2398,110 @@ int ks_graph_create(const ks_graph_desc* desc, int device, ks_graph** out, int32
   KS_GUARD_END
 }
 
+int ks_graph_create_from_ingest(const ks_ingest_dev* h, const int32_t* id_rank,
+                                const uint8_t* flags, ks_graph** out, int32_t* order_out) {
+  KS_GUARD_BEGIN
+  if (!h || !out) fail(KS_ERR_INVALID, "null argument");
+  const IngestDev& I = h->d;
+  if (I.n > INT32_MAX - 1 || I.m > INT32_MAX - 1) fail(KS_ERR_UNSUPPORTED, "more than 2^31 events");
+  DevGuard guard(I.device);
+  keep_device_pool(I.device);
+  HostTimer gt;
+  const int n = (int)I.n, L = I.L;
+  DeviceFreeze F;
+  std::string err;
+  const int rc = freeze_from_ingest(I, id_rank, flags, F, err);
+  if (rc != KS_OK) fail(rc, err);
+  gt.mark(F.ok ? "device freeze" : "device freeze (fallback)");
+  if (gt.on) std::fprintf(stderr, "[compile_graph] relaxation rounds %d\n", F.rounds);
+  if (!F.ok) {
+    // no trace-time topological order: the host compiler (depth-first Kahn)
+    hvec<int32_t> src(I.m), dst(I.m), lo(I.n), lane(I.n), rank(I.n), prio(I.n, 0);
+    hvec<int64_t> dur(I.n), gap(I.n), ready(I.n, 0);
+    CUDA_TRY(cudaMemcpy(src.data(), I.src, 4 * I.m, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(dst.data(), I.dst, 4 * I.m, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(lo.data(), I.lane_order, 4 * I.n, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(lane.data(), I.lane, 4 * I.n, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(dur.data(), I.dur, 8 * I.n, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(gap.data(), I.gap, 8 * I.n, cudaMemcpyDeviceToHost));
+    for (int i = 0; i < n; ++i) rank[i] = id_rank ? id_rank[i] : i;
+    ks_graph_desc d;
+    memset(&d, 0, sizeof(d));
+    d.n_tasks = n;
+    d.n_lanes = L;
+    d.duration = dur.data();
+    d.gap = gap.data();
+    d.ready_time = ready.data();
+    d.lane = lane.data();
+    d.id_rank = rank.data();
+    d.priority = prio.data();
+    d.flags = flags;
+    d.n_edges = I.m;
+    d.edge_src = src.data();
+    d.edge_dst = dst.data();
+    d.lane_order_ptr = I.lane_order_ptr.data();
+    d.lane_order = lo.data();
+    return ks_graph_create(&d, I.device, out, order_out);
+  }
+  ks_graph* g = new ks_graph();
+  g->device = I.device;
+  g->n = n;
+  g->L = L;
+  g->chained = true;  // ingest links every lane's events in lane order (rules 1, 2, 5)
+  g->n_chains = 0;
+  g->n_ordered = n;
+  g->n_edges_unique = (int)F.m_unique;
+  g->rows_are_records = true;
+  g->order.assign(F.order.begin(), F.order.end());
+  g->d_child_ptr = F.child_ptr;
+  g->d_child = F.child;
+  g->d_indeg = F.indeg;
+  g->d_lane = F.lane_r;
+  g->d_dur = F.dur_r;
+  g->d_gap = F.gap_r;
+  g->d_ready = F.ready_r;
+  g->d_rank = F.rank_r;
+  g->d_prio = F.prio_r;
+  g->d_flags = F.flags_r;
+  g->d_group = F.group_r;
+  auto st = std::make_unique<LazyPrograms>();
+  st->n = n;
+  st->L = L;
+  st->E = I.m;
+  st->NC = 0;
+  st->R = n;
+  st->chained = true;
+  st->from_device = true;
+  st->d_ukeys = F.ukeys;
+  st->d_pkeys = F.pkeys;
+  st->m_unique = F.m_unique;
+  st->lane_order_ptr.assign(I.lane_order_ptr.begin(), I.lane_order_ptr.end());
+  if (I.n) {
+    CUDA_TRY(cudaMalloc(&st->d_lane_order, sizeof(int) * I.n));
+    CUDA_TRY(cudaMemcpy(st->d_lane_order, I.lane_order, sizeof(int) * I.n, cudaMemcpyDeviceToDevice));
+  }
+  if (F.order_d) cudaFree(F.order_d);
+  g->lazy = std::move(st);
+  if (order_out) std::copy(g->order.begin(), g->order.end(), order_out);
+  *out = g;
+  gt.mark("graph");
+  if (getenv("DDSIM_EAGER_PROGRAMS") != nullptr) ensure_programs(g);
+  return KS_OK;
+  KS_GUARD_END
+}
+
+int ks_graph_shape(const ks_graph* g, int32_t* chained, int32_t* n_ordered) {
+  if (!g) return KS_ERR_INVALID;
+  if (chained) *chained = g->chained ? 1 : 0;
+  if (n_ordered) *n_ordered = g->n_ordered;
+  return KS_OK;
+}
+
 int ks_graph_get_info(const ks_graph* g, ks_graph_info* info) {
   if (!g || !info) return KS_ERR_INVALID;
+  KS_GUARD_BEGIN
+  ensure_programs(g);
+  KS_GUARD_END
   info->n_tasks = g->n;
   info->n_lanes = g->L;
   info->n_edges_unique = g->n_edges_unique;
@@ -2213,6 +2522,9 @@ int ks_graph_get_info(const ks_graph* g, ks_graph_info* info) {
 
 int ks_graph_levels(const ks_graph* g, int32_t* level_out) {
   if (!g || !level_out) return KS_ERR_INVALID;
+  KS_GUARD_BEGIN
+  ensure_programs(g);
+  KS_GUARD_END
   std::copy(g->level.begin(), g->level.end(), level_out);
   return KS_OK;
 }
@@ -2238,6 +2550,7 @@ int ks_simulate(const ks_graph* g, const ks_scenarios_desc* sc, int policy, int 
 int ks_toposort(const ks_graph* g, int32_t* order_out, int32_t* n_out) {
   KS_GUARD_BEGIN
   if (!g) fail(KS_ERR_INVALID, "null graph");
+  ensure_programs(g);
   DevGuard guard(g->device);
   const int n = g->n;
   if (n == 0) {
@@ -2340,6 +2653,7 @@ bool host_pinned(const void* p) {
 int simulate_host_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, int path,
                        const ks_sim_out* out) {
   if (!g || !sc || !out) fail(KS_ERR_INVALID, "null argument");
+  ensure_programs(g);
   const int S = sc->n_scenarios;
   if (S <= 0) fail(KS_ERR_INVALID, "n_scenarios must be positive");
   if (sc->dense_kind != 0 && sc->dense != nullptr && sc->dense_ld < S)
@@ -2547,6 +2861,7 @@ int breakdown_impl(const ks_graph* g, const ks_scenarios_desc* sc, const int64_t
                    int64_t start_ld, const int64_t* makespan, const ks_breakdown_desc* bd,
                    int64_t* parts, int64_t* layer_busy, cudaStream_t stream) {
   if (!g || !sc || !bd || !start || !makespan) fail(KS_ERR_INVALID, "null argument");
+  ensure_programs(g);
   if (g->device < 0) fail(KS_ERR_NO_DEVICE, "graph was compiled without a device");
   const int S = sc->n_scenarios;
   if (S <= 0) fail(KS_ERR_INVALID, "n_scenarios must be positive");

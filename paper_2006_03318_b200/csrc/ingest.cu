@@ -68,7 +68,8 @@ struct Pool {
     return p;
   }
   ~Pool() {
-    for (void* p : ptrs) cudaFreeAsync(p, st);
+    for (void* p : ptrs)
+      if (p) cudaFreeAsync(p, st);
   }
 };
 
@@ -448,8 +449,20 @@ struct StageTimer {
 // default release threshold returns it to the driver at every synchronize).
 static void keep_pool(int device) { keep_device_pool(device); }
 
-extern "C" int ks_ingest(const ks_trace_cols* tc, int device, int check_overlaps,
-                         ks_ingest_out* out) {
+void ddsim::IngestDev::release() {
+  void* p[] = {lane, start, dur, gap, src, dst, ekind, lane_order};
+  for (void* x : p)
+    if (x) cudaFree(x);
+  lane = nullptr;
+  start = dur = gap = nullptr;
+  src = dst = lane_order = nullptr;
+  ekind = nullptr;
+}
+
+// keep != nullptr: the edges, lane order, gaps and the per-event lane / start /
+// duration columns stay on the device in *keep (ks_ingest_keep)
+static int ingest_impl(const ks_trace_cols* tc, int device, int check_overlaps,
+                       ks_ingest_out* out, IngestDev* keep) {
   if (!tc || !out) return KS_ERR_INVALID;
   cudaSetDevice(device);
   keep_pool(device);
@@ -635,13 +648,37 @@ extern "C" int ks_ingest(const ks_trace_cols* tc, int device, int check_overlaps
     int* od = P.get<int>(C);
     unsigned char* ok = P.get<unsigned char>(C);
     const long long m = compact_edges(P, esrc, edst, ekind, eflag, C, os, od, ok);
-    if (m > out->edge_cap) throw IngestError{KS_ERR_INVALID, "edge capacity too small"};
+    if (!keep && m > out->edge_cap) throw IngestError{KS_ERR_INVALID, "edge capacity too small"};
     T_.mark("compact");
-    ICUDA(cudaMemcpyAsync(out->edge_src, os, sizeof(int) * m, cudaMemcpyDeviceToHost, st));
-    ICUDA(cudaMemcpyAsync(out->edge_dst, od, sizeof(int) * m, cudaMemcpyDeviceToHost, st));
-    ICUDA(cudaMemcpyAsync(out->edge_kind, ok, m, cudaMemcpyDeviceToHost, st));
-    ICUDA(cudaMemcpyAsync(out->lane_order, perm, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
-    ICUDA(cudaMemcpyAsync(out->gap, d_gap, sizeof(long long) * n, cudaMemcpyDeviceToHost, st));
+    if (keep) {
+      // hand the buffers over (the pool frees everything else)
+      auto take = [&](void* ptr) {
+        for (auto& q : P.ptrs)
+          if (q == ptr) q = nullptr;
+      };
+      keep->device = device;
+      keep->n = n;
+      keep->m = m;
+      keep->L = L;
+      keep->lane = d_lane;
+      keep->start = d_start;
+      keep->dur = d_dur;
+      keep->gap = d_gap;
+      keep->src = os;
+      keep->dst = od;
+      keep->ekind = ok;
+      keep->lane_order = perm;
+      for (void* q : {(void*)d_lane, (void*)d_start, (void*)d_dur, (void*)d_gap, (void*)os,
+                      (void*)od, (void*)ok, (void*)perm})
+        take(q);
+      keep->lane_class.assign(tc->lane_class, tc->lane_class + L);
+    } else {
+      ICUDA(cudaMemcpyAsync(out->edge_src, os, sizeof(int) * m, cudaMemcpyDeviceToHost, st));
+      ICUDA(cudaMemcpyAsync(out->edge_dst, od, sizeof(int) * m, cudaMemcpyDeviceToHost, st));
+      ICUDA(cudaMemcpyAsync(out->edge_kind, ok, m, cudaMemcpyDeviceToHost, st));
+      ICUDA(cudaMemcpyAsync(out->lane_order, perm, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
+      ICUDA(cudaMemcpyAsync(out->gap, d_gap, sizeof(long long) * n, cudaMemcpyDeviceToHost, st));
+    }
     ICUDA(cudaMemcpyAsync(out->launcher, d_launcher, sizeof(int) * n, cudaMemcpyDeviceToHost, st));
     ICUDA(cudaStreamSynchronize(st));
     // lane_order_ptr: lanes appear in index order in the sorted view
@@ -652,6 +689,7 @@ extern "C" int ks_ingest(const ks_trace_cols* tc, int device, int check_overlaps
     }
     out->lane_order_ptr[L] = pos;
     out->n_edges = m;
+    if (keep) keep->lane_order_ptr.assign(out->lane_order_ptr, out->lane_order_ptr + L + 1);
     T_.mark("copy-back");
   } catch (const IngestError& e) {
     set_last_error(e.msg);
@@ -667,6 +705,55 @@ extern "C" int ks_ingest(const ks_trace_cols* tc, int device, int check_overlaps
   cudaStreamDestroy(st);
   if (rc != KS_OK) cudaGetLastError();  // do not leave a non-sticky error for later calls
   return rc;
+}
+
+extern "C" int ks_ingest(const ks_trace_cols* tc, int device, int check_overlaps,
+                         ks_ingest_out* out) {
+  return ingest_impl(tc, device, check_overlaps, out, nullptr);
+}
+
+extern "C" int ks_ingest_keep(const ks_trace_cols* tc, int device, int check_overlaps,
+                              ks_ingest_out* out, ks_ingest_dev** dev_out) {
+  if (!dev_out) return KS_ERR_INVALID;
+  *dev_out = nullptr;
+  ks_ingest_dev* h = new ks_ingest_dev;
+  const int rc = ingest_impl(tc, device, check_overlaps, out, &h->d);
+  if (rc != KS_OK) {
+    h->d.release();
+    delete h;
+    return rc;
+  }
+  *dev_out = h;
+  return KS_OK;
+}
+
+extern "C" int ks_ingest_dev_copy(const ks_ingest_dev* h, int32_t* edge_src, int32_t* edge_dst,
+                                  uint8_t* edge_kind, int32_t* lane_order, int64_t* gap) {
+  if (!h) return KS_ERR_INVALID;
+  const IngestDev& I = h->d;
+  cudaSetDevice(I.device);
+  cudaError_t e = cudaSuccess;
+  if (edge_src && I.m) e = cudaMemcpy(edge_src, I.src, sizeof(int) * I.m, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && edge_dst && I.m)
+    e = cudaMemcpy(edge_dst, I.dst, sizeof(int) * I.m, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && edge_kind && I.m)
+    e = cudaMemcpy(edge_kind, I.ekind, I.m, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && lane_order && I.n)
+    e = cudaMemcpy(lane_order, I.lane_order, sizeof(int) * I.n, cudaMemcpyDeviceToHost);
+  if (e == cudaSuccess && gap && I.n)
+    e = cudaMemcpy(gap, I.gap, sizeof(long long) * I.n, cudaMemcpyDeviceToHost);
+  if (e != cudaSuccess) {
+    set_last_error(cudaGetErrorString(e));
+    return KS_ERR_CUDA;
+  }
+  return KS_OK;
+}
+
+extern "C" void ks_ingest_dev_free(ks_ingest_dev* h) {
+  if (!h) return;
+  cudaSetDevice(h->d.device);
+  h->d.release();
+  delete h;
 }
 
 extern "C" int ks_map_layers(const ks_trace_cols* tc, const int32_t* launcher,

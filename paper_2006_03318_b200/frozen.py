@@ -110,16 +110,102 @@ class FrozenGraph:
         _tick("ks_graph_create")
         self._h = h
         del keep
-        info = N.GraphInfo()
-        N.check(N.lib().ks_graph_get_info(h, C.byref(info)))
-        self.info = info
+        chained, n_ordered = C.c_int32(0), C.c_int32(0)
+        N.check(N.lib().ks_graph_shape(h, C.byref(chained), C.byref(n_ordered)))
+        self._info = None
         self.order = order                         # frozen row -> dense input index
-        self.row_ids = self.ids[order]             # frozen row -> external id
-        self.row_of = np.empty(self.n, np.int32)   # dense input index -> frozen row
-        self.row_of[order] = np.arange(self.n, dtype=np.int32)
-        self.chained = bool(info.chained)
-        self.n_ordered = int(info.n_ordered)
+        self._row_ids = None
+        self._row_of = None
+        self.chained = bool(chained.value)
+        self.n_ordered = int(n_ordered.value)
         _tick("post")
+
+    @staticmethod
+    def from_device_ingest(kept, *, ids, duration, lane, lanes, flags, dataload) -> "FrozenGraph":
+        """The frozen graph of a KeptIngest, compiled on its device
+        (ks_graph_create_from_ingest: unique-edge / predecessor CSR by radix
+        sort, trace-time topological order verified on every edge, per-row
+        arrays gathered on the device).  The host copies of the gaps and edges
+        (replicas, parity checks) are fetched from the ingest on first use."""
+        fz = FrozenGraph.__new__(FrozenGraph)
+        fz.device = kept.device
+        fz.ids = N.c_i64(ids)
+        fz.n = int(fz.ids.shape[0])
+        fz.lanes = list(lanes)
+        fz.L = len(fz.lanes)
+        fz.duration = N.c_i64(duration)
+        fz.ready = np.zeros(fz.n, np.int64)
+        fz.lane = N.c_i32(lane)
+        fz.priority = np.zeros(fz.n, np.int32)
+        fz.flags = np.ascontiguousarray(flags, dtype=np.uint8)
+        fz.group = np.zeros(fz.n, np.uint32)
+        fz.task_layers = None
+        fz.dataload = dataload
+        if fz.n < 2 or bool(np.all(fz.ids[1:] > fz.ids[:-1])):
+            rank = None
+            fz.id_rank = np.arange(fz.n, dtype=np.int32)
+        else:
+            rank = np.empty(fz.n, np.int32)
+            rank[np.argsort(fz.ids, kind="stable")] = np.arange(fz.n, dtype=np.int32)
+            fz.id_rank = rank
+        fz.chains = []
+        fz._replicas = {}
+        fz._kept = kept
+        order = np.empty(max(fz.n, 1), np.int32)
+        h = C.c_void_p()
+        _tick("host prep")
+        N.check(N.lib().ks_graph_create_from_ingest(kept.handle, N.ptr(rank), N.ptr(fz.flags),
+                                                    C.byref(h), N.ptr(order)),
+                "ks_graph_create_from_ingest")
+        _tick("ks_graph_create_from_ingest")
+        fz._h = h
+        chained, n_ordered = C.c_int32(0), C.c_int32(0)
+        N.check(N.lib().ks_graph_shape(h, C.byref(chained), C.byref(n_ordered)))
+        fz._info = None
+        fz.order = order[:fz.n]
+        fz._row_ids = None
+        fz._row_of = None
+        fz.chained = bool(chained.value)
+        fz.n_ordered = int(n_ordered.value)
+        return fz
+
+    def __getattr__(self, name):
+        # device-frozen graphs: host copies of the ingest's gaps / edges / lane
+        # order on first use
+        kept = self.__dict__.get("_kept")
+        if kept is not None and name in ("gap", "edge_src", "edge_dst", "_lane_order"):
+            val = {"gap": lambda: N.c_i64(kept.gap), "edge_src": lambda: N.c_i32(kept.edge_src),
+                   "edge_dst": lambda: N.c_i32(kept.edge_dst),
+                   "_lane_order": lambda: (N.c_i32(kept.lane_order_ptr),
+                                           N.c_i32(kept.lane_order))}[name]()
+            self.__dict__[name] = val
+            return val
+        raise AttributeError(name)
+
+    @property
+    def info(self):
+        """ks_graph_info (builds the kernel programs on first use)."""
+        if self._info is None:
+            info = N.GraphInfo()
+            N.check(N.lib().ks_graph_get_info(self._h, C.byref(info)), "ks_graph_get_info")
+            self._info = info
+        return self._info
+
+    @property
+    def row_ids(self) -> np.ndarray:
+        """frozen row -> external id"""
+        if self._row_ids is None:
+            self._row_ids = self.ids[self.order]
+        return self._row_ids
+
+    @property
+    def row_of(self) -> np.ndarray:
+        """dense input index -> frozen row"""
+        if self._row_of is None:
+            r = np.empty(self.n, np.int32)
+            r[self.order] = np.arange(self.n, dtype=np.int32)
+            self._row_of = r
+        return self._row_of
 
     @property
     def handle(self):

@@ -22,6 +22,8 @@ import sys
 import time
 from dataclasses import dataclass
 
+import ctypes as C
+
 import numpy as np
 
 from . import _native as N
@@ -94,8 +96,59 @@ def _tick(what):
     _T[0] = t
 
 
+class KeptIngest:
+    """ks_ingest_keep output: edges, lane order and gaps stay on the device
+    for a device freeze (frozen_from_ingest); the IngestResult fields are
+    copied to the host on first access."""
+
+    def __init__(self, cols: TraceColumns, handle, n_edges: int, lane_order_ptr, launcher,
+                 device: int):
+        self.cols = cols
+        self.device = device
+        self.handle = handle
+        self.n_edges = n_edges
+        self.lane_order_ptr = lane_order_ptr
+        self.launcher = launcher
+        self._host = None
+
+    def _fetch(self) -> IngestResult:
+        if self._host is None:
+            n, m = self.cols.n, self.n_edges
+            src, dst = np.empty(max(m, 1), np.int32), np.empty(max(m, 1), np.int32)
+            kind, lo = np.empty(max(m, 1), np.uint8), np.empty(max(n, 1), np.int32)
+            gap = np.empty(max(n, 1), np.int64)
+            N.check(N.lib().ks_ingest_dev_copy(self.handle, N.ptr(src), N.ptr(dst), N.ptr(kind),
+                                               N.ptr(lo), N.ptr(gap)), "ks_ingest_dev_copy")
+            self._host = IngestResult(cols=self.cols, edge_src=src[:m], edge_dst=dst[:m],
+                                      edge_kind=kind[:m], lane_order=lo[:n],
+                                      lane_order_ptr=self.lane_order_ptr, gap=gap[:n],
+                                      launcher=self.launcher)
+        return self._host
+
+    def __getattr__(self, name):
+        if name in ("edge_src", "edge_dst", "edge_kind", "lane_order", "gap", "edge_triples",
+                    "gaps_by_id"):
+            return getattr(self._fetch(), name)
+        raise AttributeError(name)
+
+    def close(self):
+        h = self.__dict__.get("handle")
+        if h is not None and h.value:
+            N.lib().ks_ingest_dev_free(h)
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # noqa: BLE001 - interpreter shutdown
+            pass
+
+
 def ingest_arrays(cols: TraceColumns, strict: bool = False, check_overlaps: bool = False,
-                  device: int | None = None) -> IngestResult:
+                  device: int | None = None, keep_device: bool = False):
+    """ks_ingest on the columns.  keep_device=True: a KeptIngest whose edges /
+    lane order / gaps stay on the device for frozen_from_ingest's device
+    freeze (ks_ingest_keep)."""
     device = N.env_device() if device is None else device
     _tick(None)
     N.require_device(device)
@@ -106,17 +159,25 @@ def ingest_arrays(cols: TraceColumns, strict: bool = False, check_overlaps: bool
     n_sync = int(np.sum(cols.kind == KIND_CODE[next(k for k in KIND_CODE if k.value == "Sync")]))
     cap = 2 * n + n_sync * max(n_gpu_lanes, 1) + 16
     out = N.IngestOut()
-    bufs = {
-        "edge_src": np.empty(cap, np.int32), "edge_dst": np.empty(cap, np.int32),
-        "edge_kind": np.empty(cap, np.uint8), "lane_order": np.empty(max(n, 1), np.int32),
-        "lane_order_ptr": np.empty(len(cols.lanes) + 1, np.int32),
-        "gap": np.empty(max(n, 1), np.int64), "launcher": np.empty(max(n, 1), np.int32),
-    }
+    if keep_device:
+        bufs = {"lane_order_ptr": np.empty(len(cols.lanes) + 1, np.int32),
+                "launcher": np.empty(max(n, 1), np.int32)}
+    else:
+        bufs = {
+            "edge_src": np.empty(cap, np.int32), "edge_dst": np.empty(cap, np.int32),
+            "edge_kind": np.empty(cap, np.uint8), "lane_order": np.empty(max(n, 1), np.int32),
+            "lane_order_ptr": np.empty(len(cols.lanes) + 1, np.int32),
+            "gap": np.empty(max(n, 1), np.int64), "launcher": np.empty(max(n, 1), np.int32),
+        }
     for k, a in bufs.items():
         setattr(out, k, a.ctypes.data)
     out.edge_cap = cap
     _tick("host prep")
-    rc = N.lib().ks_ingest(tc, device, 1 if check_overlaps else 0, out)
+    handle = C.c_void_p()
+    if keep_device:
+        rc = N.lib().ks_ingest_keep(tc, device, 1 if check_overlaps else 0, out, C.byref(handle))
+    else:
+        rc = N.lib().ks_ingest(tc, device, 1 if check_overlaps else 0, out)
     if rc == N.KS_ERR_OVERLAP:
         a, b = int(out.bad_a), int(out.bad_b)
         lane = cols.lanes[int(cols.lane[cols.index_of(a)])]
@@ -128,6 +189,8 @@ def ingest_arrays(cols: TraceColumns, strict: bool = False, check_overlaps: bool
     N.check(rc, "ks_ingest")
     _tick("ks_ingest")
     m = int(out.n_edges)
+    if keep_device:
+        return KeptIngest(cols, handle, m, bufs["lane_order_ptr"], bufs["launcher"][:n], device)
     return IngestResult(cols=cols, edge_src=bufs["edge_src"][:m].copy(),
                         edge_dst=bufs["edge_dst"][:m].copy(),
                         edge_kind=bufs["edge_kind"][:m].copy(), lane_order=bufs["lane_order"][:n],

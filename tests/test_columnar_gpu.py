@@ -78,3 +78,53 @@ def test_million_record_document_roundtrip():
     b = np.array([f"{l}/{p}" for l, p in ci.tags] + ["-"])[ci.layer_tag]
     assert np.array_equal(a, b)
     assert (ci.layer_tag >= 0).mean() > 0.5
+
+
+def _host_frozen(ct, res_host):
+    from paper_2006_03318_b200.columnar import frozen_from_ingest
+    return frozen_from_ingest(ct, res_host)
+
+
+@pytest.mark.parametrize("shift_kernel", [False, True])
+def test_device_freeze_equals_host_freeze(shift_kernel):
+    """ks_graph_create_from_ingest (device: radix-sorted CSR, trace-time order
+    verified on every edge) against the host compiler on the same ingest: same
+    chained flag, a topological row order, and identical simulations of jitter
+    scenarios.  shift_kernel moves a lane's first kernel before its launch, so
+    the trace-time order breaks an edge and the host compiler orders it."""
+    from paper_2006_03318_b200.columnar import frozen_from_ingest
+    from paper_2006_03318_b200.workloads import ingest_document_columns
+
+    ct = ingest_document_columns(120_000, seed=5)
+    cols = ct.cols
+    if shift_kernel:
+        kind = np.asarray(cols.kind)
+        lane = np.asarray(cols.lane)
+        gpu = np.nonzero(kind == 2)[0]
+        first = gpu[np.argmin(np.asarray(cols.start)[gpu])]
+        cols.start[first] = 0  # before its launch; still first on its stream
+        assert np.sum((lane == lane[first]) & (np.asarray(cols.start) == 0)) == 1
+    kept = ingest_arrays(cols, keep_device=True)
+    host = ingest_arrays(cols)
+    fz_d = frozen_from_ingest(ct, kept)
+    fz_h = frozen_from_ingest(ct, host)
+    assert fz_d.chained and fz_h.chained and fz_d.n_ordered == fz_h.n_ordered == cols.n
+    pos = np.empty(cols.n, np.int64)
+    pos[fz_d.order] = np.arange(cols.n)
+    assert np.all(pos[host.edge_src] < pos[host.edge_dst])
+    assert np.array_equal(kept.edge_src, host.edge_src) and np.array_equal(kept.gap, host.gap)
+    S = 8
+    rng = np.random.default_rng(2)
+    base = np.asarray(cols.duration, np.int64)
+    k = rng.integers(900, 1101, size=(cols.n, S))
+    per_task = ((2 * base[:, None] * k + 1000) // 2000).astype(np.int64)
+    rd = simulate_batch(fz_d, ScenarioTable(n_scenarios=S, dense=np.ascontiguousarray(per_task[fz_d.order])))
+    rh = simulate_batch(fz_h, ScenarioTable(n_scenarios=S, dense=np.ascontiguousarray(per_task[fz_h.order])))
+    assert np.array_equal(rd.makespan, rh.makespan)
+    sd = np.empty_like(rd.start)
+    sd[fz_d.order] = rd.start
+    sh = np.empty_like(rh.start)
+    sh[fz_h.order] = rh.start
+    assert np.array_equal(sd, sh)
+    assert np.array_equal(rd.lane_busy, rh.lane_busy)
+    assert fz_d.info.n_edges_unique == fz_h.info.n_edges_unique
