@@ -405,6 +405,23 @@ int ks_trace_markers(const ks_trace* t, const ks_trace_marker_cols* cols);
 int ks_trace_strings(const ks_trace* t, int which, char* bytes, int64_t* offsets);
 void ks_trace_destroy(ks_trace* t);
 
+/* ---- CUPTI activity recording (Daydream's trace collection) ------------
+ * Records this process's CUDA activity -- runtime API calls (CPU thread
+ * lanes), kernels / copies / memsets (stream lanes), synchronisations and
+ * NVTX ranges named "<layer>/<Forward|Backward|WeightUpdate>" (layer
+ * markers) -- into the trace columns ks_trace_parse produces (the reference
+ * reads the same schema from JSON only, trace.py:281-328).  libcupti is
+ * loaded at run time (KS_ERR_UNSUPPORTED without it). */
+typedef struct ks_cupti_trace ks_cupti_trace;
+int ks_cupti_start(void);
+int ks_cupti_stop(ks_cupti_trace** out);
+int ks_cupti_info_get(const ks_cupti_trace* t, ks_trace_info* info, int64_t* t0_ns,
+                      int64_t* dropped);
+int ks_cupti_events(const ks_cupti_trace* t, const ks_trace_event_cols* cols);
+int ks_cupti_markers(const ks_cupti_trace* t, const ks_trace_marker_cols* cols);
+int ks_cupti_strings(const ks_cupti_trace* t, int which, char* bytes, int64_t* offsets);
+void ks_cupti_destroy(ks_cupti_trace* t);
+
 typedef struct {
   int64_t n_events;
   const int64_t* id;

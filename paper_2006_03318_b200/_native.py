@@ -175,6 +175,13 @@ _SIGNATURES = [
     ("ks_trace_markers", C.c_int, [P, C.POINTER(TraceMarkerCols)]),
     ("ks_trace_strings", C.c_int, [P, C.c_int, P, P]),
     ("ks_trace_destroy", None, [P]),
+    ("ks_cupti_start", C.c_int, []),
+    ("ks_cupti_stop", C.c_int, [C.POINTER(P)]),
+    ("ks_cupti_info_get", C.c_int, [P, C.POINTER(TraceInfo), P, P]),
+    ("ks_cupti_events", C.c_int, [P, C.POINTER(TraceEventCols)]),
+    ("ks_cupti_markers", C.c_int, [P, C.POINTER(TraceMarkerCols)]),
+    ("ks_cupti_strings", C.c_int, [P, C.c_int, P, P]),
+    ("ks_cupti_destroy", None, [P]),
     ("ks_trace_write", C.c_int, [C.POINTER(TraceWriteDesc), C.c_int, C.POINTER(P),
                                  C.POINTER(C.c_int64)]),
     ("ks_buffer_free", None, [P]),

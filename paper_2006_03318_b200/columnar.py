@@ -292,6 +292,22 @@ def ingest_document(text, *, strict: bool = False, check_overlaps: bool = False,
     return ColumnarIngest(trace=ct, ingest=res, layer_tag=tag, tags=tags, frozen=fz)
 
 
+def ingest_columns(ct: ColumnarTrace, *, strict: bool = False, check_overlaps: bool = True,
+                   freeze: bool = True, device: int | None = None) -> ColumnarIngest:
+    """ingest_document for columns that did not come through the validating
+    reader (e.g. cupti.record()): the device ingest also checks lane overlaps
+    (check_lane_overlaps, trace.py:255-265) unless told otherwise."""
+    from .ingest import ingest_arrays, map_layers_arrays
+
+    res = ingest_arrays(ct.cols, strict=strict, check_overlaps=check_overlaps, device=device,
+                        keep_device=freeze)
+    tag_m, tags = ct.marker_tags()
+    tag = map_layers_arrays(ct.cols, res.launcher, ct.m_lane, ct.m_start, ct.m_end, tag_m,
+                            device=device)
+    fz = frozen_from_ingest(ct, res, device=device) if freeze else None
+    return ColumnarIngest(trace=ct, ingest=res, layer_tag=tag, tags=tags, frozen=fz)
+
+
 def frozen_from_ingest(ct: ColumnarTrace, res, device: int | None = None):
     """FrozenGraph straight from ingest output (no DependencyGraph objects)."""
     from .frozen import VDNN_MALLOC_PREFIX, FrozenGraph
@@ -315,4 +331,4 @@ def frozen_from_ingest(ct: ColumnarTrace, res, device: int | None = None):
 
 
 __all__ = ["ColumnarTrace", "ColumnarIngest", "load_trace_columns", "dump_trace_columns",
-           "ingest_document", "frozen_from_ingest", "PHASES", "PHASE_CODE"]
+           "ingest_document", "ingest_columns", "frozen_from_ingest", "PHASES", "PHASE_CODE"]

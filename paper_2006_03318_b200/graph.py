@@ -145,6 +145,22 @@ def _cycle_among(graph: DependencyGraph, stuck: set[int]) -> list[int]:
     return sorted(stuck)
 
 
+def is_acyclic(graph: DependencyGraph) -> bool:
+    """Acyclicity without the ordered list: the frozen graph's topological
+    pass (ks_graph_create) orders every task iff there is no cycle, so the
+    lexicographically-first order (verify_acyclic, the device's sequential
+    Kahn walk) is only computed when a caller wants the list or the cycle."""
+    if not graph.tasks:
+        return True
+    from .frozen import FrozenGraph
+
+    fz = FrozenGraph.from_graph(graph)
+    try:
+        return fz.n_ordered == fz.n
+    finally:
+        fz.close()
+
+
 def verify_acyclic(graph: DependencyGraph) -> list[int]:
     """Topological order with smallest-id tie-break; CycleDetected otherwise.
     The order is computed on the device (ks_toposort)."""
