@@ -209,7 +209,17 @@ CUfunction get_function(const std::vector<int>& codes, int dk, int V, bool dyn, 
 // both with the graph's handler codes as an if-chain.
 // mode: 0 replay, 1 transfer, 2 fused (transfer + look-back + replay)
 std::string seg_source(const std::vector<int>& codes, int dk, int LN, bool ch, int mode) {
-  std::string src = "#define DDSIM_LANES_NO_STD_TYPES 1\n#define DDSIM_UNROLL 2\n";
+  std::string src = "#define DDSIM_LANES_NO_STD_TYPES 1\n";
+  // record loop unrolled x2, except with derived durations (DK 0): the
+  // duration derivation doubles the body and instruction-cache misses cost more
+  // than the overlap buys (config 3: 1.28 -> 1.16 ms rolled; config 2, DK 2:
+  // 0.182 ms unrolled vs 0.190 rolled)
+  if (const char* u = getenv("DDSIM_SEG_UNROLL"))  // experiments
+    src += std::string("#define DDSIM_UNROLL ") + u + "\n";
+  else if (dk != 0)
+    src += "#define DDSIM_UNROLL 2\n";
+  std::string bounds = "256";
+  if (const char* mb = getenv("DDSIM_SEG_MINB")) bounds = std::string("128, ") + mb;
   std::string disp = "#define DDSIM_DISPATCH(h) ";
   std::string sdisp = "#define DDSIM_SYM_DISPATCH(h) ";
   for (size_t i = 0; i < codes.size(); ++i) {
@@ -225,7 +235,7 @@ std::string seg_source(const std::vector<int>& codes, int dk, int LN, bool ch, i
   src += disp + sdisp + kLanesBodySrc + "\n" + kSegBodySrc + "\n";
   const char* names[] = {"ddsim_seg_replay", "ddsim_seg_transfer", "ddsim_seg_fused"};
   const char* bodies[] = {"replay_body", "sym_body", "fused_body"};
-  src += std::string("extern \"C\" __global__ void __launch_bounds__(256) ") + names[mode] +
+  src += std::string("extern \"C\" __global__ void __launch_bounds__(") + bounds + ") " + names[mode] +
          "(const __grid_constant__ ddsim_lanes::Tmap tmap, const ddsim_lanes::Params p, "
          "const ddsim_lanes::SegParams sg" +
          (ch ? ", const __grid_constant__ ddsim_lanes::ChainParams cp" : "") +
@@ -308,6 +318,8 @@ cudaError_t launch_lanes_seg_jit(int mode, const LaneParams& p, const LaneChainP
   const char* names[] = {"ddsim_seg_replay", "ddsim_seg_transfer", "ddsim_seg_fused"};
   std::string key = std::string(tags[mode]) + std::to_string(dev) + ":" + std::to_string(dkind) +
                     ":" + std::to_string(LN) + (cp ? ":ch:" : ":");
+  if (const char* u = getenv("DDSIM_SEG_UNROLL")) key += std::string("u") + u + ":";
+  if (const char* mb = getenv("DDSIM_SEG_MINB")) key += std::string("mb") + mb + ":";
   for (int c : codes) key += std::to_string(c) + ",";
   CUfunction fn = get_compiled(key, seg_source(codes, dkind, LN, cp != nullptr, mode), names[mode]);
   if (!fn) return cudaErrorNotSupported;
