@@ -2618,6 +2618,21 @@ int ks_toposort(const ks_graph* g, int32_t* order_out, int32_t* n_out) {
 // ---- host-buffer entry point --------------------------------------------------
 namespace {
 
+// Per-thread reusable resources of ks_simulate_host (the drop-in path calls it
+// once per simulate(): creating two streams, device buffers and a pinned
+// staging buffer per call cost milliseconds).  Buffers up to kHostCacheMax
+// bytes are kept and grown; larger ones are allocated for the call only.
+constexpr size_t kHostCacheMax = 256u << 20;
+struct HostCallCache {
+  int device = -1;
+  cudaStream_t st[2] = {nullptr, nullptr};
+  void* dev[2][6] = {};
+  size_t dev_cap[2][6] = {};
+  char* staging[2] = {nullptr, nullptr};
+  size_t staging_cap[2] = {0, 0};
+};
+thread_local HostCallCache tl_host;
+
 struct ChunkBufs {
   void* dense = nullptr;
   long long* start = nullptr;
@@ -2689,9 +2704,20 @@ int simulate_host_impl(const ks_graph* g, const ks_scenarios_desc* sc, int polic
     }
   while (bounds.back() < S) bounds.push_back(std::min<long long>(S, bounds.back() + sc_chunk));
   const int nchunks = (int)bounds.size() - 1;
-  cudaStream_t st[2];
-  CUDA_TRY(cudaStreamCreateWithFlags(&st[0], cudaStreamNonBlocking));
-  CUDA_TRY(cudaStreamCreateWithFlags(&st[1], cudaStreamNonBlocking));
+  HostCallCache& HC = tl_host;
+  if (HC.device != g->device) {  // first call of this thread on this device
+    for (int k = 0; k < 2; ++k) {
+      for (int j = 0; j < 6; ++j)
+        if (HC.dev[k][j]) cudaFree(HC.dev[k][j]);
+      if (HC.staging[k]) cudaFreeHost(HC.staging[k]);
+    }
+    HC = HostCallCache{};
+    CUDA_TRY(cudaStreamCreateWithFlags(&HC.st[0], cudaStreamNonBlocking));
+    CUDA_TRY(cudaStreamCreateWithFlags(&HC.st[1], cudaStreamNonBlocking));
+    HC.device = g->device;
+  }
+  cudaStream_t st[2] = {HC.st[0], HC.st[1]};
+  std::vector<void*> temp_dev, temp_host;  // uncached (large) buffers of this call
   ChunkBufs buf[2];
   const long long ldc = sc_chunk;  // multiple of 4
   const size_t stage_bytes = (size_t)ldc * (8 + 8 * std::max(g->L, 1) + 4);
@@ -2710,29 +2736,52 @@ int simulate_host_impl(const ks_graph* g, const ks_scenarios_desc* sc, int polic
     copies.push_back(HostCopy{dst, b.staging + stage_off, n});
     CUDA_TRY(cudaLaunchHostFunc(stream, host_copy_fn, &copies.back()));
   };
-  auto alloc = [&](ChunkBufs& b) {
-    if (dense) CUDA_TRY(cudaMalloc(&b.dense, esz * N * ldc));
-    if (out->start) CUDA_TRY(cudaMalloc(&b.start, 8 * N * ldc));
-    if (out->makespan) CUDA_TRY(cudaMalloc(&b.makespan, 8 * ldc));
-    if (out->lane_busy) CUDA_TRY(cudaMalloc(&b.lane_busy, 8 * ldc * std::max(g->L, 1)));
-    if (out->schedule) CUDA_TRY(cudaMalloc(&b.schedule, 4 * N * ldc));
-    if (out->dispatched) CUDA_TRY(cudaMalloc(&b.dispatched, 4 * ldc));
-    CUDA_TRY(cudaHostAlloc(&b.staging, stage_bytes, cudaHostAllocDefault));
+  auto dev_get = [&](int k, int slot, size_t bytes) -> void* {
+    if (bytes > kHostCacheMax) {
+      void* p = nullptr;
+      CUDA_TRY(cudaMalloc(&p, bytes));
+      temp_dev.push_back(p);
+      return p;
+    }
+    if (HC.dev_cap[k][slot] < bytes) {
+      if (HC.dev[k][slot]) cudaFree(HC.dev[k][slot]);
+      HC.dev[k][slot] = nullptr;
+      HC.dev_cap[k][slot] = 0;
+      CUDA_TRY(cudaMalloc(&HC.dev[k][slot], bytes));
+      HC.dev_cap[k][slot] = bytes;
+    }
+    return HC.dev[k][slot];
+  };
+  auto alloc = [&](ChunkBufs& b, int k) {
+    if (dense) b.dense = dev_get(k, 0, esz * N * ldc);
+    if (out->start) b.start = static_cast<long long*>(dev_get(k, 1, 8 * N * ldc));
+    if (out->makespan) b.makespan = static_cast<long long*>(dev_get(k, 2, 8 * ldc));
+    if (out->lane_busy)
+      b.lane_busy = static_cast<long long*>(dev_get(k, 3, 8 * ldc * std::max(g->L, 1)));
+    if (out->schedule) b.schedule = static_cast<int*>(dev_get(k, 4, 4 * N * ldc));
+    if (out->dispatched) b.dispatched = static_cast<int*>(dev_get(k, 5, 4 * ldc));
+    if (stage_bytes > kHostCacheMax) {
+      CUDA_TRY(cudaHostAlloc(&b.staging, stage_bytes, cudaHostAllocDefault));
+      temp_host.push_back(b.staging);
+    } else {
+      if (HC.staging_cap[k] < stage_bytes) {
+        if (HC.staging[k]) cudaFreeHost(HC.staging[k]);
+        HC.staging[k] = nullptr;
+        HC.staging_cap[k] = 0;
+        CUDA_TRY(cudaHostAlloc(&HC.staging[k], stage_bytes, cudaHostAllocDefault));
+        HC.staging_cap[k] = stage_bytes;
+      }
+      b.staging = HC.staging[k];
+    }
   };
   auto release = [&]() {
-    for (auto& b : buf) {
-      void* ps[] = {b.dense, b.start, b.makespan, b.lane_busy, b.schedule, b.dispatched};
-      for (void* p : ps)
-        if (p) cudaFree(p);
-      if (b.staging) cudaFreeHost(b.staging);
-    }
-    cudaStreamDestroy(st[0]);
-    cudaStreamDestroy(st[1]);
+    for (void* p : temp_dev) cudaFree(p);
+    for (void* p : temp_host) cudaFreeHost(p);
   };
   int rc = KS_OK;
   try {
-    alloc(buf[0]);
-    if (nchunks > 1) alloc(buf[1]);
+    alloc(buf[0], 0);
+    if (nchunks > 1) alloc(buf[1], 1);
     // DDSIM_HOST_TRACE=1: per-chunk event timeline on stderr (diagnostics)
     const bool trace = getenv("DDSIM_HOST_TRACE") != nullptr;
     std::vector<cudaEvent_t> ev;
