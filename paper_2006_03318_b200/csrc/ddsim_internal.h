@@ -255,7 +255,7 @@ cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const LaneChainParams*
                                      const int* dense32, const void* tmap128, int dkind, int V,
                                      const std::vector<int>& codes, int grid, int BD, size_t smem,
                                      cudaStream_t stream, const LaneDerivedParams* dp = nullptr);
-int maxplus_lanes_vec(int S, int dkind = 1);
+int maxplus_lanes_vec(int S, int dkind = 1, bool vec_ok = true);
 // Segment-parallel lanes path (mirrors ddsim_lanes::SegParams)
 struct LaneSegParams {
   const int* cuts;
@@ -329,7 +329,7 @@ cudaError_t launch_bd_sched_rows(const int* schedule, const int* row_lane, const
                                  int n, int L, int S, int* srows, cudaStream_t stream);
 
 const char* jit_log();
-int maxplus_lanes_block_dim(int S, int num_sms, int dkind = 1);
+int maxplus_lanes_block_dim(int S, int num_sms, int dkind = 1, bool vec_ok = true);
 cudaError_t launch_listsched(const ListParams& p, cudaStream_t stream);
 cudaError_t launch_toposort_lanes(int N, int L, const int* lane_ptr, const int* lane_rows,
                                   const int* child_ptr, const int* child, const int* indeg,

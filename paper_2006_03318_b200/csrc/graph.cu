@@ -2060,8 +2060,10 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
     p.lane_busy = reinterpret_cast<long long*>(out->lane_busy);
     int nsm = 148;
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device);
-    const int BD = maxplus_lanes_block_dim(S, nsm, dk);
-    const int LV = maxplus_lanes_vec(S, dk);
+    const bool vec_ok = p.start == nullptr ||
+                        (p.start_ld % 2 == 0 && reinterpret_cast<uintptr_t>(p.start) % 16 == 0);
+    const int BD = maxplus_lanes_block_dim(S, nsm, dk, vec_ok);
+    const int LV = maxplus_lanes_vec(S, dk, vec_ok);
     p.s_pad = (long long)((S + LV * BD - 1) / (LV * BD)) * LV * BD;
     if (p.kglob > 0) p.gslots = T.scratch<long long>((size_t)p.kglob * p.s_pad);
     int* flag = T.scratch<int>(1);

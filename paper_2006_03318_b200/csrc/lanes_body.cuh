@@ -250,8 +250,12 @@ __device__ __forceinline__ void hstep(St<V>& S, long long d0, long long d1, long
       if (V == 2) b = lmax(b, S.lv[m][V - 1]);
     }
   if (store) {
-    __stcs(sp, a);
-    if (V == 2) __stcs(sp + 1, b);
+    // V = 2: one 16-byte streaming store of the two adjacent scenarios (the
+    // host picks V = 2 only for 16-byte aligned start rows of even pitch)
+    if (V == 2)
+      __stcs(reinterpret_cast<longlong2*>(sp), make_longlong2(a, b));
+    else
+      __stcs(sp, a);
     sp += ld;
   }
   a += d0;
@@ -288,8 +292,10 @@ __device__ __forceinline__ void hstep_dyn(St<V>& S, unsigned h, long long d0, lo
   long long x = lmax(lmax(lmax(a[0], a[1]), lmax(a[2], a[3])), a[4]);
   long long y = lmax(lmax(lmax(b[0], b[1]), lmax(b[2], b[3])), b[4]);
   if (store) {
-    __stcs(sp, x);
-    if (V == 2) __stcs(sp + 1, y);
+    if (V == 2)
+      __stcs(reinterpret_cast<longlong2*>(sp), make_longlong2(x, y));
+    else
+      __stcs(sp, x);
     sp += ld;
   }
   x += d0 + gap;

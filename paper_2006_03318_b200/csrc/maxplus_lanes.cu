@@ -75,8 +75,8 @@ static size_t lanes_smem(int dk, int BD, int V, int ksm) {
 // V scenarios per thread (env DDSIM_LANES_V overrides: 1 or 2); two CTAs per
 // SM cover S in one wave.  BD is a multiple of 16 so the grid is close to
 // 2 x #SMs; the TMA box (BD * V ints) stays <= 256.
-int maxplus_lanes_vec(int S, int dkind) {
-  if (dkind == 0) return 1;  // derived durations: one scenario per thread
+int maxplus_lanes_vec(int S, int dkind, bool vec_ok) {
+  if (dkind == 0 || !vec_ok) return 1;  // derived durations / unaligned starts: one per thread
   const char* e = getenv("DDSIM_LANES_V");
   // two scenarios per thread only when there are enough scenarios to keep
   // ~4 warps per SM busy with V = 2; small sweeps want more threads instead
@@ -85,8 +85,8 @@ int maxplus_lanes_vec(int S, int dkind) {
   if (S % v) v = 1;
   return v;
 }
-int maxplus_lanes_block_dim(int S, int num_sms, int dkind) {
-  const int V = maxplus_lanes_vec(S, dkind);
+int maxplus_lanes_block_dim(int S, int num_sms, int dkind, bool vec_ok) {
+  const int V = maxplus_lanes_vec(S, dkind, vec_ok);
   if (const char* e = getenv("DDSIM_LANES_BD")) {  // experiments (multiple of 16)
     const int bd = atoi(e) / 16 * 16;
     if (bd >= 32 && bd <= 256 / V) return bd;
@@ -329,8 +329,10 @@ cudaError_t launch_maxplus_lanes(const LaneParams& p, const LaneChainParams* cp,
   int dev = 0, nsm = 148;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  const int V = maxplus_lanes_vec(p.S, dkind);
-  const int BD = maxplus_lanes_block_dim(p.S, nsm, dkind);
+  const bool vec_ok = p.start == nullptr ||
+                      (p.start_ld % 2 == 0 && reinterpret_cast<uintptr_t>(p.start) % 16 == 0);
+  const int V = maxplus_lanes_vec(p.S, dkind, vec_ok);
+  const int BD = maxplus_lanes_block_dim(p.S, nsm, dkind, vec_ok);
   const int W = BD * V;
   const int grid = (p.S + W - 1) / W;
   if ((long long)grid * W > p.s_pad) return cudaErrorInvalidValue;
