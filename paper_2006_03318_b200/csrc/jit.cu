@@ -220,6 +220,13 @@ std::string seg_source(const std::vector<int>& codes, int dk, int LN, bool ch, i
     src += "#define DDSIM_UNROLL 2\n";
   std::string bounds = "256";
   if (const char* mb = getenv("DDSIM_SEG_MINB")) bounds = std::string("128, ") + mb;
+  // TMA pipeline depth: 2 chunks for duration tiles (smaller CTAs, more of them
+  // per SM: config 4 at 8,192 scenarios 2.67 -> 2.48 ms), 4 for derived
+  // durations (no tiles; config 3 insensitive)
+  if (const char* st = getenv("DDSIM_SEG_STAGES"))  // experiments (>= 2)
+    src += std::string("#define DDSIM_STAGES ") + st + "\n";
+  else if (dk != 0)
+    src += "#define DDSIM_STAGES 2\n";
   std::string disp = "#define DDSIM_DISPATCH(h) ";
   std::string sdisp = "#define DDSIM_SYM_DISPATCH(h) ";
   for (size_t i = 0; i < codes.size(); ++i) {
@@ -320,6 +327,7 @@ cudaError_t launch_lanes_seg_jit(int mode, const LaneParams& p, const LaneChainP
                     ":" + std::to_string(LN) + (cp ? ":ch:" : ":");
   if (const char* u = getenv("DDSIM_SEG_UNROLL")) key += std::string("u") + u + ":";
   if (const char* mb = getenv("DDSIM_SEG_MINB")) key += std::string("mb") + mb + ":";
+  if (const char* st = getenv("DDSIM_SEG_STAGES")) key += std::string("st") + st + ":";
   for (int c : codes) key += std::to_string(c) + ",";
   CUfunction fn = get_compiled(key, seg_source(codes, dkind, LN, cp != nullptr, mode), names[mode]);
   if (!fn) return cudaErrorNotSupported;

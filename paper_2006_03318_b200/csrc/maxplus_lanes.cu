@@ -290,7 +290,9 @@ cudaError_t launch_maxplus_lanes_seg(const LaneParams& p, const LaneChainParams*
   cudaError_t e = dkind == 0 ? cudaSuccess : encode_lanes_tmap(&tmap, p, dense32, dkind, BD);
   if (e != cudaSuccess) return e;
   const int gx = (p.S + BD - 1) / BD;
-  const int stages = ddsim_lanes::kStagesL;
+  // must match the depth seg_source compiles into the kernels (jit.cu)
+  int stages = dkind != 0 ? 2 : ddsim_lanes::kStagesL;
+  if (const char* e = getenv("DDSIM_SEG_STAGES")) stages = std::max(2, atoi(e));
   const size_t es = dkind == 1 ? 4 : 8;
   const size_t base = 128 + (size_t)stages * ddsim_lanes::kChunkL * sizeof(ddsim_lanes::Rec) +
                       (dkind == 0 ? (size_t)stages * ddsim_lanes::kChunkL * sizeof(ddsim_lanes::RowDur)
