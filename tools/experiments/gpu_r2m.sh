@@ -1,6 +1,6 @@
 #!/bin/bash
 mkdir -p gpurun_out
-timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/c3_launches.csv python tools/c3one.py > gpurun_out/c3.log 2>&1
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/c3_launches.csv python tools/experiments/c3one.py > gpurun_out/c3.log 2>&1
 tail -2 gpurun_out/c3.log
 python - <<'PY'
 import csv
