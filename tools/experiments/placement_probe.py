@@ -5,7 +5,7 @@ from pathlib import Path
 
 import torch
 
-sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+sys.path.insert(0, str(Path(__file__).resolve().parents[2]))
 import bench  # noqa: E402
 from paper_2006_03318_b200.batch import ScenarioTable, simulate_batch_device  # noqa: E402
 
