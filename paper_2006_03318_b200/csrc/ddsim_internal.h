@@ -335,6 +335,15 @@ cudaError_t launch_toposort_lanes(int N, int L, const int* lane_ptr, const int* 
                                   const int* child_ptr, const int* child, const int* indeg,
                                   const int* rank, int* deg_scratch, int* out, int* count,
                                   cudaStream_t st);
+// A lane head of verify_acyclic's lane walk (listsched.cu): frozen row, id
+// rank, requirement count / offset, the first four requirements (lane, prefix)
+struct alignas(16) TopoRec {
+  int row, rank, rn, r0;
+  int ml[4], mq[4];
+};
+cudaError_t launch_toposort_lanes_req(int N, int L, const int* lane_ptr, const TopoRec* recs,
+                                      const int* req_lane, const int* req_pos, int* out,
+                                      int* count, cudaStream_t st);
 cudaError_t launch_fill_i64(long long* p, long long v, long long n, cudaStream_t s);
 cudaError_t launch_fill_i32(int* p, int v, long long n, cudaStream_t s);
 cudaError_t launch_patch_ovr(NodeRec* prog, int n_rec, const int* ovr_map, cudaStream_t st);

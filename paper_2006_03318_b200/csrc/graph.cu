@@ -281,6 +281,12 @@ struct ks_graph {
   // rows per lane of any graph (list-scheduled breakdown: per-scenario lane
   // sequences come from the dispatch order)
   int* d_bd_all_ptr = nullptr;
+  // toposort_lanes_kernel requirements per row: (lane, emitted prefix length)
+  bool topo_req = false;
+  std::once_flag topo_once;
+  TopoRec* d_topo_rec = nullptr;
+  int* d_req_lane = nullptr;
+  int* d_req_pos = nullptr;
 };
 
 namespace {
@@ -1715,6 +1721,85 @@ void materialize_from_device(ks_graph* g, LazyPrograms& S) {
   S.from_device = false;
 }
 
+// verify_acyclic on the lane heads (toposort_lanes_req_kernel): a head is
+// ready once every predecessor its lane order does not already put before it
+// has been emitted, i.e. once the emitted prefix of that predecessor's lane is
+// long enough.  Per row: (lane, prefix length) requirements, the largest per
+// lane; built on the first ks_toposort call from the device CSR.
+void ensure_topo_req(const ks_graph* gc) {
+  ks_graph* g = const_cast<ks_graph*>(gc);
+  std::call_once(g->topo_once, [g] {
+    if (!g->bd_ok || g->n_chains > 0 || g->L > 32 || g->n == 0 || g->n >= (1 << 27)) return;
+    DevGuard guard(g->device);
+    const int n = g->n, L = g->L;
+    hvec<int> bptr(L + 1), brows(n), cptr(n + 1), lane_r(n);
+    CUDA_TRY(cudaMemcpy(bptr.data(), g->d_bd_ptr, 4 * (L + 1), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(brows.data(), g->d_bd_rows, 4 * (size_t)n, cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(cptr.data(), g->d_child_ptr, 4 * ((size_t)n + 1), cudaMemcpyDeviceToHost));
+    CUDA_TRY(cudaMemcpy(lane_r.data(), g->d_lane, 4 * (size_t)n, cudaMemcpyDeviceToHost));
+    hvec<int> child(cptr[n]);
+    if (cptr[n]) CUDA_TRY(cudaMemcpy(child.data(), g->d_child, 4 * (size_t)cptr[n], cudaMemcpyDeviceToHost));
+    hvec<int> pos(n, 0);
+    for (int l = 0; l < L; ++l)
+      for (int k = bptr[l]; k < bptr[l + 1]; ++k) pos[brows[k]] = k - bptr[l];
+    auto needed = [&](int u, int v) { return !(lane_r[u] == lane_r[v] && pos[u] < pos[v]); };
+    hvec<int> cnt(n + 1, 0);
+    for (int u = 0; u < n; ++u)
+      for (int k = cptr[u]; k < cptr[u + 1]; ++k)
+        if (needed(u, child[k])) cnt[child[k] + 1]++;
+    for (int r = 0; r < n; ++r) cnt[r + 1] += cnt[r];
+    hvec<int> cl(cnt[n]), cp(cnt[n]);
+    {
+      hvec<int> fill(cnt.begin(), cnt.end() - 1);
+      for (int u = 0; u < n; ++u)
+        for (int k = cptr[u]; k < cptr[u + 1]; ++k)
+          if (needed(u, child[k])) {
+            const int o = fill[child[k]]++;
+            cl[o] = lane_r[u];
+            cp[o] = pos[u] + 1;
+          }
+    }
+    hvec<int> rptr(n + 1, 0), rl, rp;  // deduplicated per (row, lane): the largest prefix
+    for (int v = 0; v < n; ++v) {
+      const size_t b = rl.size();
+      for (int k = cnt[v]; k < cnt[v + 1]; ++k) {
+        bool merged = false;
+        for (size_t q = b; q < rl.size(); ++q)
+          if (rl[q] == cl[k]) {
+            rp[q] = std::max(rp[q], cp[k]);
+            merged = true;
+            break;
+          }
+        if (!merged) {
+          rl.push_back(cl[k]);
+          rp.push_back(cp[k]);
+        }
+      }
+      rptr[v + 1] = (int)rl.size();
+    }
+    hvec<int> rank_r(n);
+    CUDA_TRY(cudaMemcpy(rank_r.data(), g->d_rank, 4 * (size_t)n, cudaMemcpyDeviceToHost));
+    hvec<TopoRec> recs(n);  // in lane order (brows)
+    for (int k = 0; k < n; ++k) {
+      const int r = brows[k];
+      TopoRec& x = recs[k];
+      memset(&x, 0, sizeof(x));
+      x.row = r;
+      x.rank = rank_r[r];
+      x.r0 = rptr[r];
+      x.rn = rptr[r + 1] - rptr[r];
+      for (int q = 0; q < 4 && q < x.rn; ++q) {
+        x.ml[q] = rl[x.r0 + q];
+        x.mq[q] = rp[x.r0 + q];
+      }
+    }
+    g->d_topo_rec = dev_upload(recs);
+    g->d_req_lane = dev_upload(rl);
+    g->d_req_pos = dev_upload(rp);
+    g->topo_req = true;
+  });
+}
+
 void ensure_programs(const ks_graph* gc) {
   ks_graph* g = const_cast<ks_graph*>(gc);
   std::call_once(g->programs_once, [g] {
@@ -1736,7 +1821,7 @@ void free_graph(ks_graph* g) {
                    g->d_lprog,   g->d_lside_off,  g->d_lside_slots, g->d_lside_ready,
                    g->d_bd_ptr,  g->d_bd_rows,    g->d_bd_lane_chain, g->d_bd_chains,
                    g->d_bd_member_rows, g->d_lchains, g->d_lmembers, g->d_lpreds,
-                   g->d_bd_all_ptr};
+                   g->d_bd_all_ptr, g->d_topo_rec, g->d_req_lane, g->d_req_pos};
   for (void* p : dptrs)
     if (p) cudaFree(p);
   void* ptrs[] = {g->d_prog,  g->d_extra, g->d_chains, g->d_members, g->d_child_ptr,
@@ -2588,9 +2673,16 @@ int ks_toposort(const ks_graph* g, int32_t* order_out, int32_t* n_out) {
     if (g->chained && g->n_chains == 0 && g->bd_ok && g->L <= 32 &&
         getenv("DDSIM_TOPO_LISTSCHED") == nullptr) {
       // lane-chained: the frontier is the set of lane heads (one warp, lanes in lanes)
-      int* deg = (size_t)n * sizeof(int) > 200 * 1024 ? T.scratch<int>(n) : nullptr;
-      CUDA_TRY(launch_toposort_lanes(n, g->L, g->d_bd_ptr, g->d_bd_rows, g->d_child_ptr, g->d_child,
-                                     g->d_indeg, g->d_rank, deg, p.schedule, p.dispatched, st));
+      if (getenv("DDSIM_TOPO_INDEG") == nullptr) ensure_topo_req(g);
+      if (g->topo_req && getenv("DDSIM_TOPO_INDEG") == nullptr) {
+        CUDA_TRY(launch_toposort_lanes_req(n, g->L, g->d_bd_ptr, g->d_topo_rec, g->d_req_lane,
+                                           g->d_req_pos, p.schedule, p.dispatched, st));
+      } else {
+        int* deg = (size_t)n * sizeof(int) > 200 * 1024 ? T.scratch<int>(n) : nullptr;
+        CUDA_TRY(launch_toposort_lanes(n, g->L, g->d_bd_ptr, g->d_bd_rows, g->d_child_ptr,
+                                       g->d_child, g->d_indeg, g->d_rank, deg, p.schedule,
+                                       p.dispatched, st));
+      }
     } else {
       p.rdy = T.scratch<long long>(2 * (size_t)n);
       p.rem = T.scratch<int>(n);
@@ -2632,6 +2724,24 @@ struct HostCallCache {
   size_t dev_cap[2][6] = {};
   char* staging[2] = {nullptr, nullptr};
   size_t staging_cap[2] = {0, 0};
+  void release() {  // errors ignored (the runtime may already be unloading)
+    if (device < 0) return;
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    for (int k = 0; k < 2; ++k) {
+      for (int j = 0; j < 6; ++j)
+        if (dev[k][j]) cudaFree(dev[k][j]);
+      if (staging[k]) cudaFreeHost(staging[k]);
+      if (st[k]) cudaStreamDestroy(st[k]);
+    }
+    cudaSetDevice(prev);
+    cudaGetLastError();
+    *this = HostCallCache{};
+  }
+  // ks_simulate_host_multi runs each device's shard on a short-lived thread:
+  // its cache goes with it
+  ~HostCallCache() { release(); }
 };
 thread_local HostCallCache tl_host;
 
@@ -2708,12 +2818,7 @@ int simulate_host_impl(const ks_graph* g, const ks_scenarios_desc* sc, int polic
   const int nchunks = (int)bounds.size() - 1;
   HostCallCache& HC = tl_host;
   if (HC.device != g->device) {  // first call of this thread on this device
-    for (int k = 0; k < 2; ++k) {
-      for (int j = 0; j < 6; ++j)
-        if (HC.dev[k][j]) cudaFree(HC.dev[k][j]);
-      if (HC.staging[k]) cudaFreeHost(HC.staging[k]);
-    }
-    HC = HostCallCache{};
+    HC.release();
     CUDA_TRY(cudaStreamCreateWithFlags(&HC.st[0], cudaStreamNonBlocking));
     CUDA_TRY(cudaStreamCreateWithFlags(&HC.st[1], cudaStreamNonBlocking));
     HC.device = g->device;

@@ -357,6 +357,91 @@ __global__ void __launch_bounds__(32) toposort_lanes_kernel(
   if (t == 0) *count = step;
 }
 
+// verify_acyclic on lane-chained graphs without in-degree counters: lane l's
+// head is ready when every predecessor its lane order does not already place
+// before it has been emitted -- for each requirement (lane m, q): the emitted
+// prefix of lane m is >= q.  The emitted prefix lengths live in shared memory
+// (one word per lane, written only by the lane that advances).  Each lane's
+// heads are 48-byte records in lane order (row, id rank, requirements), kept
+// kTopoRing ahead in a shared-memory ring by cp.async (no dependent global
+// loads on the step).  A step: every thread checks its head, a warp arg-min
+// of the ready heads' id ranks (smallest id first, graph.py:129-148), the
+// winner's lane advances and refills its ring.
+constexpr int kTopoRing = 8;
+__device__ __forceinline__ void topo_cp16(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(
+                   static_cast<unsigned>(__cvta_generic_to_shared(dst))),
+               "l"(src)
+               : "memory");
+}
+__device__ __forceinline__ void topo_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void topo_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(kTopoRing - 1) : "memory");
+}
+
+__global__ void __launch_bounds__(32) toposort_lanes_req_kernel(
+    int N, int L, const int* __restrict__ lane_ptr, const TopoRec* __restrict__ recs,
+    const int* __restrict__ req_lane, const int* __restrict__ req_pos, int* out, int* count) {
+  __shared__ int done[32];  // emitted prefix length per lane
+  __shared__ __align__(16) TopoRec ring[32][kTopoRing];
+  const int t = threadIdx.x;
+  done[t] = 0;
+  const bool own = t < L;
+  const int len = own ? lane_ptr[t + 1] - lane_ptr[t] : 0;
+  const TopoRec* base = recs + (own ? lane_ptr[t] : 0);
+  auto issue = [&](int k) {  // record k of this lane -> its ring slot (one group)
+    if (k < len) {
+      const char* src = reinterpret_cast<const char*>(base + k);
+      char* dst = reinterpret_cast<char*>(&ring[t][k % kTopoRing]);
+      topo_cp16(dst, src);
+      topo_cp16(dst + 16, src + 16);
+      topo_cp16(dst + 32, src + 32);
+    }
+    topo_commit();
+  };
+  for (int k = 0; k < kTopoRing; ++k) issue(k);
+  topo_wait();
+  __syncwarp();
+  int pos = 0;
+  int step = 0;
+  for (; step < N; ++step) {
+    bool ready = pos < len;
+    // (id rank, lane) in one word: a single warp min-reduction picks the
+    // smallest ready id (ranks < 2^27, host-checked)
+    unsigned key = 0xffffffffu;
+    if (ready) {
+      const TopoRec& h = ring[t][pos % kTopoRing];
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (k < h.rn && done[h.ml[k]] < h.mq[k]) ready = false;
+      for (int k = 4; ready && k < h.rn; ++k)
+        if (done[req_lane[h.r0 + k]] < req_pos[h.r0 + k]) ready = false;
+      if (ready) key = ((unsigned)h.rank << 5) | (unsigned)t;
+    }
+    key = __reduce_min_sync(0xffffffffu, key);
+    if (key == 0xffffffffu) break;  // nothing ready: a cycle
+    const int who = (int)(key & 31u);
+    if (t == who) {
+      out[step] = ring[t][pos % kTopoRing].row;
+      ++pos;
+      done[t] = pos;
+      issue(pos + kTopoRing - 1);  // refills the slot just consumed
+      topo_wait();                 // record pos has landed
+    }
+    __syncwarp();
+  }
+  if (t == 0) *count = step;
+}
+
+cudaError_t launch_toposort_lanes_req(int N, int L, const int* lane_ptr, const TopoRec* recs,
+                                      const int* req_lane, const int* req_pos, int* out,
+                                      int* count, cudaStream_t st) {
+  if (L > 32) return cudaErrorInvalidValue;
+  toposort_lanes_req_kernel<<<1, 32, 0, st>>>(N, L, lane_ptr, recs, req_lane, req_pos, out, count);
+  note_launch();
+  return cudaGetLastError();
+}
+
 cudaError_t launch_toposort_lanes(int N, int L, const int* lane_ptr, const int* lane_rows,
                                   const int* child_ptr, const int* child, const int* indeg,
                                   const int* rank, int* deg_scratch, int* out, int* count,
