@@ -97,7 +97,7 @@ void init_locked() {
 }
 
 std::string make_source(const std::vector<int>& codes, int dk, int V, bool dyn, bool ch,
-                        bool nolb) {
+                        bool nolb, bool scale) {
   std::string disp = "#define DDSIM_DISPATCH(h) ";
   if (dyn) disp += "hstep_dyn<V>(S, h, d0, d1, gap, sp, ld, store); if (0) ";
   for (size_t i = 0; i < codes.size(); ++i) {
@@ -108,6 +108,7 @@ std::string make_source(const std::vector<int>& codes, int dk, int V, bool dyn, 
   }
   disp += "else __trap();\n";
   std::string src = "#define DDSIM_LANES_NO_STD_TYPES 1\n";
+  if (dk == 0 && !scale) src += "#define DDSIM_DERIVED_SCALE 0\n";
   // record-loop unrolling by 2 lets the next record's decode overlap this
   // record's max-plus chain: branch-free handler config 2 -8 %, config 3 -26 %;
   // if-chain handler config 4 -0.5 % (13.55 -> 13.49 ms, 3 interleaved repeats);
@@ -193,23 +194,26 @@ CUfunction get_compiled(const std::string& key, const std::string& src, const ch
 }
 
 CUfunction get_function(const std::vector<int>& codes, int dk, int V, bool dyn, bool ch,
-                        bool nolb, int device) {
+                        bool nolb, bool scale, int device) {
   std::string key = std::to_string(device) + ":" + std::to_string(dk) + ":" + std::to_string(V) +
-                    (dyn ? ":dyn" : "") + (ch ? ":ch" : "") + (nolb ? ":nolb:" : ":");
+                    (dyn ? ":dyn" : "") + (ch ? ":ch" : "") + (nolb ? ":nolb:" : ":") +
+                    (dk == 0 && !scale ? "noscale:" : "");
   if (const char* u = getenv("DDSIM_JIT_UNROLL")) key += std::string("u") + u + ":";
   if (const char* st = getenv("DDSIM_LANES_STAGES")) key += std::string("st") + st + ":";
   if (const char* b = getenv("DDSIM_LANES_BODY")) key += std::string("b") + b + ":";
   for (int c : codes) key += std::to_string(c) + ",";
   if (getenv("DDSIM_NO_JIT")) return nullptr;
-  return get_compiled(key, make_source(codes, dk, V, dyn, ch, nolb), "ddsim_lanes_jit");
+  return get_compiled(key, make_source(codes, dk, V, dyn, ch, nolb, scale), "ddsim_lanes_jit");
 }
 
 // Segment kernels (SegParams in lanes_body.cuh): the transfer pass in
 // coefficient form (lanes_seg.cuh) and the replay pass (lanes_body<..., SEG>),
 // both with the graph's handler codes as an if-chain.
 // mode: 0 replay, 1 transfer, 2 fused (transfer + look-back + replay)
-std::string seg_source(const std::vector<int>& codes, int dk, int LN, bool ch, int mode) {
+std::string seg_source(const std::vector<int>& codes, int dk, int LN, bool ch, int mode,
+                       bool scale) {
   std::string src = "#define DDSIM_LANES_NO_STD_TYPES 1\n";
+  if (dk == 0 && !scale) src += "#define DDSIM_DERIVED_SCALE 0\n";
   // record loop unrolled x2, except with derived durations (DK 0): the
   // duration derivation doubles the body and instruction-cache misses cost more
   // than the overlap buys (config 3: 1.28 -> 1.16 ms rolled; config 2, DK 2:
@@ -283,7 +287,8 @@ cudaError_t launch_maxplus_lanes_jit(const LaneParams& p, const LaneChainParams*
   // members are recognised by their start -1, so chains need the starts)
   const bool nolb = dyn && dkind != 0 && p.lane_busy != nullptr &&
                     (cp == nullptr || p.start != nullptr) && getenv("DDSIM_DYN_LB") == nullptr;
-  CUfunction fn = get_function(codes, dkind, V, dyn, cp != nullptr, nolb, dev);
+  const bool scale = dp != nullptr && dp->scale_ptr != nullptr;
+  CUfunction fn = get_function(codes, dkind, V, dyn, cp != nullptr, nolb, scale, dev);
   if (!fn) return cudaErrorNotSupported;
   const CUresult ar = g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem);
   if (ar != CUDA_SUCCESS) {
@@ -328,8 +333,11 @@ cudaError_t launch_lanes_seg_jit(int mode, const LaneParams& p, const LaneChainP
   if (const char* u = getenv("DDSIM_SEG_UNROLL")) key += std::string("u") + u + ":";
   if (const char* mb = getenv("DDSIM_SEG_MINB")) key += std::string("mb") + mb + ":";
   if (const char* st = getenv("DDSIM_SEG_STAGES")) key += std::string("st") + st + ":";
+  const bool scale = dp != nullptr && dp->scale_ptr != nullptr;
+  if (dkind == 0 && !scale) key += "noscale:";
   for (int c : codes) key += std::to_string(c) + ",";
-  CUfunction fn = get_compiled(key, seg_source(codes, dkind, LN, cp != nullptr, mode), names[mode]);
+  CUfunction fn = get_compiled(key, seg_source(codes, dkind, LN, cp != nullptr, mode, scale),
+                               names[mode]);
   if (!fn) return cudaErrorNotSupported;
   if (g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem) != CUDA_SUCCESS)
     return cudaErrorNotSupported;

@@ -88,15 +88,21 @@ struct DerivedParams {
   const int* scale_ptr;    // [S+1] or null
   const ScaleStep* scale;
 };
-constexpr int kProgRegs = 4;  // scale steps kept in registers per scenario
+constexpr int kProgRegs = 2;  // scale steps kept in registers per scenario
+// NVRTC defines DDSIM_DERIVED_SCALE 0 when a derived-duration table has no
+// scale programs (overrides only): the program registers and checks vanish
+#ifndef DDSIM_DERIVED_SCALE
+#define DDSIM_DERIVED_SCALE 1
+#endif
 struct Prog {
   int n, e0;
   int lo[kProgRegs], hi[kProgRegs];
   long long num[kProgRegs], den[kProgRegs];
 };
 
-// round_half_up(d * num / den) (transform.py:174-183); 128-bit when needed
-__device__ __forceinline__ long long lscale_half_up(long long d, long long num, long long den) {
+// round_half_up(d * num / den) (transform.py:174-183), 128-bit when needed;
+// out of line so the divisions do not hold registers in the record loops
+__device__ __noinline__ long long lscale_half_up(long long d, long long num, long long den) {
   const bool neg = d < 0;
   const unsigned long long a = neg ? (unsigned long long)(-d) : (unsigned long long)d;
   const unsigned long long un = (unsigned long long)num, ud = (unsigned long long)den;
@@ -113,6 +119,7 @@ __device__ __forceinline__ long long lscale_half_up(long long d, long long num, 
 __device__ __forceinline__ void prog_load(const DerivedParams* dp, long long s, bool act, Prog& P) {
   P.n = 0;
   P.e0 = 0;
+  if (!DDSIM_DERIVED_SCALE) return;
 #pragma unroll
   for (int q = 0; q < kProgRegs; ++q) {
     P.lo[q] = 1;
@@ -139,7 +146,7 @@ __device__ __forceinline__ long long derived_dur(const DerivedParams* dp, long l
                                                  bool act, const Prog& P) {
   long long d = base;
   if (ovr >= 0 && act) d = dp->ovr[(long long)ovr * S + s];
-  if (group != 0u && P.n > 0) {
+  if (DDSIM_DERIVED_SCALE && group != 0u && P.n > 0) {
     if (P.n <= kProgRegs) {
 #pragma unroll
       for (int q = 0; q < kProgRegs; ++q)
