@@ -181,3 +181,57 @@ def test_seg_negative_durations_rerun_exact():
     dense = (base[:, None] + rng.integers(-30_000, 3000, size=(fz.n, S))).astype(np.int32)
     res = simulate_batch(fz, ScenarioTable(n_scenarios=S, dense=dense))
     _oracle_cols(g, fz, dense, res, [0, 13, S - 1])
+
+
+@pytest.mark.parametrize("seed,K", [(1, 6), (2, 17), (3, 40)])
+@pytest.mark.parametrize("durations", ["derived", "expanded"])
+def test_seg_chain_carries_vs_single_pass_and_oracle(seed, K, durations, monkeypatch):
+    """Data-parallel sweeps (one permutable AllReduce chain whose member
+    predecessors live through the backward pass) on random training traces:
+    the segment path with carries and the chain segment replayed between two
+    scans equals the single-pass kernel on every start, makespan and lane busy,
+    and sampled scenarios equal the oracle on the reference-equivalent graph."""
+    from paper_2006_03318_b200 import transform as TR
+    from paper_2006_03318_b200 import workloads as W
+    from paper_2006_03318_b200.batch import distributed_sweep
+    from paper_2006_03318_b200.scenarios import whatif_distributed
+
+    w = W.training_trace(n_layers=60, kernels_fwd=4, kernels_bwd=8, n_wu=300, n_streams=1,
+                         sync_every=200, seed=seed, buckets_mb=8.0)
+    g, buckets = w.graph, w.trace.gradient_buckets
+    B = len([b for b in buckets.buckets() if buckets.layers_of_bucket(b)])
+    rng = np.random.default_rng(seed)
+    configs, perms = [], []
+    for _ in range(24):
+        o = rng.permutation(B)
+        for nw in (1, 4, 16):
+            for bw in (1, 10, 100):
+                configs.append({"bandwidth_gbps": bw, "workers": nw})
+                perms.append(o)
+    monkeypatch.setenv("DDSIM_FORCE_DERIVED" if durations == "derived" else "DDSIM_NO_DERIVED", "1")
+    sw = distributed_sweep(g, buckets, configs, np.array(perms, np.int16))
+    assert sw.frozen.info.n_carries > 0
+    monkeypatch.setenv("DDSIM_SEG_K", str(K))
+    l0 = N.launch_count()
+    seg = simulate_batch(sw.frozen, sw.table)
+    l1 = N.launch_count()
+    monkeypatch.setenv("DDSIM_NO_SEG", "1")
+    single = simulate_batch(sw.frozen, sw.table)
+    l2 = N.launch_count()
+    monkeypatch.delenv("DDSIM_NO_SEG")
+    assert (l1 - l0) >= (l2 - l1) + 3  # transfer, two scans, two replays vs one pass
+    assert np.array_equal(seg.start, single.start)
+    assert np.array_equal(seg.makespan, single.makespan)
+    assert np.array_equal(seg.lane_busy, single.lane_busy)
+    for s in (1, len(configs) // 2, len(configs) - 1):
+        pipe = whatif_distributed(g, buckets=buckets, **configs[s])
+        steps = [pipe.steps[k] for k in perms[s]] if pipe.steps else []
+        h = g.copy()
+        TR._DEFER["on"] = True
+        try:
+            for stp in steps:
+                TR.apply_step(h, stp)
+        finally:
+            TR._DEFER["on"] = False
+        st, ms, _lb, _ = OracleGraph.from_graph(h).simulate("default")
+        assert seg.makespan[s] == ms and seg.start_of(s) == st, s
