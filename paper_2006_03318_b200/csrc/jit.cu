@@ -233,6 +233,7 @@ std::string seg_source(const std::vector<int>& codes, int dk, int LN, bool ch, i
     src += "#define DDSIM_STAGES 2\n";
   std::string disp = "#define DDSIM_DISPATCH(h) ";
   std::string sdisp = "#define DDSIM_SYM_DISPATCH(h) ";
+  std::string sdisp2 = "#define DDSIM_SYM_DISPATCH2(h) ";
   for (size_t i = 0; i < codes.size(); ++i) {
     const int c = codes[i];
     const std::string tp = std::to_string(c & 3) + ", " + std::to_string((c >> 2) & 31) + ", " +
@@ -240,11 +241,19 @@ std::string seg_source(const std::vector<int>& codes, int dk, int LN, bool ch, i
     const std::string cond = (i ? "else if (h == " : "if (h == ") + std::to_string(c) + "u) ";
     disp += cond + "hstep<" + tp + ", V>(S, d0, d1, gap, sp, ld, store); ";
     sdisp += cond + "hsym<" + tp + ", LN>(Y, dv, gp); ";
+    sdisp2 += cond + "{ hsym<" + tp + ", LN>(Y, dv, gp); hsym<" + tp + ", LN>(Y2, dv2, gp); } ";
   }
   disp += "else __trap();\n";
   sdisp += "else __trap();\n";
-  src += disp + sdisp + kLanesBodySrc + "\n" + kSegBodySrc + "\n";
-  const char* names[] = {"ddsim_seg_replay", "ddsim_seg_transfer", "ddsim_seg_fused"};
+  sdisp2 += "else __trap();\n";
+  src += disp + sdisp + sdisp2 + kLanesBodySrc + "\n" + kSegBodySrc + "\n";
+  const char* names[] = {"ddsim_seg_replay", "ddsim_seg_transfer", "ddsim_seg_fused",
+                         "ddsim_seg_transfer2"};
+  if (mode == 3)  // two scenarios per thread, duration tiles, no chains
+    return src + "extern \"C\" __global__ void __launch_bounds__(" + bounds + ") " + names[3] +
+           "(const __grid_constant__ ddsim_lanes::Tmap tmap, const ddsim_lanes::Params p, "
+           "const ddsim_lanes::SegParams sg) {\n  ddsim_lanes::sym_body2<" + std::to_string(dk) +
+           ", " + std::to_string(LN) + ">(&tmap, p, sg);\n}\n";
   const char* bodies[] = {"replay_body", "sym_body", "fused_body"};
   src += std::string("extern \"C\" __global__ void __launch_bounds__(") + bounds + ") " + names[mode] +
          "(const __grid_constant__ ddsim_lanes::Tmap tmap, const ddsim_lanes::Params p, "
@@ -322,12 +331,13 @@ cudaError_t launch_lanes_seg_jit(int mode, const LaneParams& p, const LaneChainP
                                  const std::vector<int>& codes, const void* segp, int gx, int gy,
                                  int BD, size_t smem, cudaStream_t stream,
                                  const LaneDerivedParams* dp) {
-  if (codes.empty() || codes.size() > 32 || LN < 1 || LN > 4 || mode < 0 || mode > 2)
+  if (codes.empty() || codes.size() > 32 || LN < 1 || LN > 4 || mode < 0 || mode > 3)
     return cudaErrorNotSupported;
   int dev = 0;
   cudaGetDevice(&dev);
-  const char* tags[] = {"seg_r:", "seg_t:", "seg_f:"};
-  const char* names[] = {"ddsim_seg_replay", "ddsim_seg_transfer", "ddsim_seg_fused"};
+  const char* tags[] = {"seg_r:", "seg_t:", "seg_f:", "seg_t2:"};
+  const char* names[] = {"ddsim_seg_replay", "ddsim_seg_transfer", "ddsim_seg_fused",
+                         "ddsim_seg_transfer2"};
   std::string key = std::string(tags[mode]) + std::to_string(dev) + ":" + std::to_string(dkind) +
                     ":" + std::to_string(LN) + (cp ? ":ch:" : ":");
   if (const char* u = getenv("DDSIM_SEG_UNROLL")) key += std::string("u") + u + ":";
@@ -352,8 +362,9 @@ cudaError_t launch_lanes_seg_jit(int mode, const LaneParams& p, const LaneChainP
   if (dp) dpv = *dp;
   void* args_ch[] = {tm, &pp, sg, &cpv, &dpv};
   void* args_nc[] = {tm, &pp, sg, &dpv};
+  void* args_2[] = {tm, &pp, sg};
   const CUresult r = g_drv.launch(fn, gx, gy, 1, BD, 1, 1, (unsigned)smem, (CUstream)stream,
-                                  cp ? args_ch : args_nc, nullptr);
+                                  mode == 3 ? args_2 : (cp ? args_ch : args_nc), nullptr);
   if (r != CUDA_SUCCESS) {
     log_line("cuLaunchKernel (segment) failed: " + std::to_string((int)r));
     return cudaErrorLaunchFailure;

@@ -286,6 +286,166 @@ __device__ __forceinline__ void sym_pass(const Tmap* tmap, const Params& p, cons
     for (int i = 0; i < LN; ++i) coef[j][i] = Y.v[j][i];
 }
 
+// Two scenarios per thread (duration tiles, no chains): the transfer pass is
+// instruction-bound (record decode and dispatch dominate the L x L coefficient
+// updates), so a thread decodes each record once for two adjacent scenarios.
+// DDSIM_SYM_DISPATCH2(h) applies the handler to (Y, dv, gp) and (Y2, dv2, gp).
+template <int DK, int LN>
+__device__ __forceinline__ void sym_pass2(const Tmap* tmap, const Params& p, const SegParams& sg,
+                                          int seg, int blk, int (&coef)[LN][LN],
+                                          int (&coef2)[LN][LN]) {
+  static_assert(DK == 1 || DK == 2, "two scenarios per thread: duration tiles only");
+  extern __shared__ __align__(128) unsigned char smem[];
+  const int BD = blockDim.x;
+  const int W = 2 * BD;
+  const int tid = threadIdx.x;
+  unsigned long long* bars = reinterpret_cast<unsigned long long*>(smem);
+  Rec* pst = reinterpret_cast<Rec*>(smem + 128);
+  unsigned sbase = su32l(smem);
+  asm volatile("" : "+r"(sbase));
+  const unsigned prog_s = sbase + 128;
+  const unsigned tile_s = prog_s + kStagesL * kChunkL * (unsigned)sizeof(Rec);
+  constexpr unsigned ES = DK == 1 ? 4u : 8u;
+  const unsigned tile_all = (unsigned)(kStagesL * kChunkL * W) * ES;
+  const unsigned slot_s = tile_s + tile_all;  // [ksm][BD] x 32 B (two scenarios)
+  const unsigned col = (unsigned)(tid * 32);
+  const unsigned slot_pitch = (unsigned)(BD * 32);
+  unsigned char* tst = smem + (tile_s - sbase);
+  const int s0 = blk * W;
+  const int c_begin = sg.cuts[seg] / kChunkL;
+  const int r_end = sg.cuts[seg + 1];
+  const int nchunks = (r_end + kChunkL - 1) / kChunkL;
+  const unsigned tile_bytes = (unsigned)(kChunkL * W) * ES;
+  auto issue = [&](int c) {
+    const int st = (c - c_begin) % kStagesL;
+    const int nrec = min(kChunkL, r_end - c * kChunkL);
+    const unsigned pb = (unsigned)(nrec * sizeof(Rec));
+    l_expect(&bars[st], pb + tile_bytes);
+    l_bulk(pst + st * kChunkL, p.prog + (long long)c * kChunkL, pb, &bars[st]);
+    l_tile(tst + (size_t)st * kChunkL * W * ES, tmap, s0, c * kChunkL, &bars[st]);
+  };
+  if (tid == 0) {
+    for (int i = 0; i < kStagesL; ++i) l_mbar_init(&bars[i]);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  }
+  __syncthreads();
+  if (tid == 0)
+    for (int c = c_begin; c < min(c_begin + kStagesL, nchunks); ++c) issue(c);
+
+  Sym<LN> Y, Y2;
+#pragma unroll
+  for (int l = 0; l <= NLANE; ++l)
+#pragma unroll
+    for (int c = 0; c < LN; ++c) Y.v[l][c] = Y2.v[l][c] = (l == c) ? 0 : kNegSym;
+  const unsigned row_pitch = (unsigned)W * ES;
+
+  for (int c = c_begin; c < nchunks; ++c) {
+    const int st = (c - c_begin) % kStagesL;
+    l_wait(&bars[st], (unsigned)(((c - c_begin) / kStagesL) & 1));
+    const unsigned rec0 = prog_s + (unsigned)(st * kChunkL * sizeof(Rec));
+    const unsigned t0 = tile_s + (unsigned)(st * kChunkL) * row_pitch + (unsigned)tid * ES * 2u;
+    const int nrec = min(kChunkL, r_end - c * kChunkL);
+    int4 raw = l_lds128(rec0);
+    int dn = 0, dn2 = 0;
+    auto load_d = [&](unsigned ta) {
+      if (DK == 1) {
+        const int2 v = l_lds64i(ta);
+        dn = v.x;
+        dn2 = v.y;
+      } else {
+        const longlong2 v = l_lds128ll(ta);
+        dn = (int)v.x;
+        dn2 = (int)v.y;
+      }
+    };
+    load_d(t0);
+    auto record = [&](int j) {
+      const int4 r = raw;
+      const int dv = dn, dv2 = dn2;
+      if (j + 1 < nrec) {
+        raw = l_lds128(rec0 + (unsigned)(j + 1) * 16u);
+        load_d(t0 + (unsigned)(j + 1) * row_pitch);
+      }
+      const int gp = r.x;
+      const unsigned w = (unsigned)r.w;
+      const unsigned h = w >> 24;
+      const unsigned rare = (w >> 16) & 0xffu;
+      if (rare & R_PRE) {
+        int x[4] = {kNegSym, kNegSym, kNegSym, kNegSym}, x2[4] = {kNegSym, kNegSym, kNegSym, kNegSym};
+        int y[4], y2[4];
+        const int row = c * kChunkL + j;
+        auto take = [&](unsigned code) {
+          const unsigned a = slot_s + code * slot_pitch + col;
+          sym_slot_ld(a, y);
+          sym_slot_ld(a + 16u, y2);
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            x[q] = imax(x[q], y[q]);
+            x2[q] = imax(x2[q], y2[q]);
+          }
+        };
+        if (rare & R_S0) take((unsigned)((r.z << 16) >> 16));
+        if (rare & R_S1) take((unsigned)(r.z >> 16));
+        if ((rare & R_SIDE) && p.side_off)
+          for (int k = p.side_off[row]; k < p.side_off[row + 1]; ++k) take((unsigned)p.side_slots[k]);
+#pragma unroll
+        for (int q = 0; q < LN; ++q) {
+          Y.v[NLANE][q] = x[q];
+          Y2.v[NLANE][q] = x2[q];
+        }
+      }
+      DDSIM_SYM_DISPATCH2(h)
+      if (rare & R_OUT_SMEM) {
+        int y[4], y2[4];
+        sym_get<LN>(Y, (int)(h & 3), y);
+        sym_get<LN>(Y2, (int)(h & 3), y2);
+        const unsigned a = slot_s + (unsigned)((w << 16) >> 16) * slot_pitch + col;
+        sym_slot_st(a, y);
+        sym_slot_st(a + 16u, y2);
+      }
+    };
+#ifdef DDSIM_UNROLL
+    if (nrec == kChunkL) {
+#pragma unroll DDSIM_UNROLL
+      for (int j = 0; j < kChunkL; ++j) record(j);
+    } else {
+#pragma unroll 1
+      for (int j = 0; j < nrec; ++j) record(j);
+    }
+#else
+#pragma unroll 1
+    for (int j = 0; j < nrec; ++j) record(j);
+#endif
+    __syncthreads();
+    if (tid == 0 && c + kStagesL < nchunks) issue(c + kStagesL);
+  }
+#pragma unroll
+  for (int j = 0; j < LN; ++j)
+#pragma unroll
+    for (int i = 0; i < LN; ++i) {
+      coef[j][i] = Y.v[j][i];
+      coef2[j][i] = Y2.v[j][i];
+    }
+}
+
+template <int DK, int LN>
+__device__ __forceinline__ void sym_body2(const Tmap* tmap, const Params& p, const SegParams& sg) {
+  int coef[LN][LN], coef2[LN][LN];
+  sym_pass2<DK, LN>(tmap, p, sg, (int)blockIdx.y, (int)blockIdx.x, coef, coef2);
+  const long long s = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 2;
+  if (s + 1 < p.S) {  // S is even on this path (host)
+    int* out = sg.trans + (long long)blockIdx.y * LN * LN * sg.s_pad + s;
+#pragma unroll
+    for (int j = 0; j < LN; ++j)
+#pragma unroll
+      for (int i = 0; i < LN; ++i) {
+        out[(long long)(j * LN + i) * sg.s_pad] = coef[j][i];
+        out[(long long)(j * LN + i) * sg.s_pad + 1] = coef2[j][i];
+      }
+  }
+}
+
 // Three-kernel path, pass 1: blockIdx.y = segment, coefficients to sg.trans.
 template <int DK, int LN, bool CH>
 __device__ __forceinline__ void sym_body(const Tmap* tmap, const Params& p, const SegParams& sg,
