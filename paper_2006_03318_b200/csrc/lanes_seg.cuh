@@ -434,14 +434,15 @@ __device__ __forceinline__ void sym_body2(const Tmap* tmap, const Params& p, con
   int coef[LN][LN], coef2[LN][LN];
   sym_pass2<DK, LN>(tmap, p, sg, (int)blockIdx.y, (int)blockIdx.x, coef, coef2);
   const long long s = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 2;
-  if (s + 1 < p.S) {  // S is even on this path (host)
+  if (s < p.S) {  // (an odd S leaves the last thread's second scenario out)
     int* out = sg.trans + (long long)blockIdx.y * LN * LN * sg.s_pad + s;
+    const bool second = s + 1 < p.S;
 #pragma unroll
     for (int j = 0; j < LN; ++j)
 #pragma unroll
       for (int i = 0; i < LN; ++i) {
         out[(long long)(j * LN + i) * sg.s_pad] = coef[j][i];
-        out[(long long)(j * LN + i) * sg.s_pad + 1] = coef2[j][i];
+        if (second) out[(long long)(j * LN + i) * sg.s_pad + 1] = coef2[j][i];
       }
   }
 }

@@ -304,7 +304,7 @@ cudaError_t launch_maxplus_lanes_seg(const LaneParams& p, const LaneChainParams*
   if (sg.K > 1) {
     // transfer: two scenarios per thread over duration tiles without chains
     // (one record decode for both; the pass is instruction-bound)
-    const bool two = dkind != 0 && cp == nullptr && p.S % 2 == 0 && 2 * BD <= 256 &&
+    const bool two = dkind != 0 && cp == nullptr && 2 * BD <= 256 &&
                      getenv("DDSIM_SEG_T1") == nullptr;
     if (two) {
       CUtensorMap tmap2;
