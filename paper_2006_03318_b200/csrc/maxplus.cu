@@ -381,26 +381,30 @@ namespace ddsim {
 // Derived durations -> dense int64 [rows][ld]: d = base[r], the scenario's
 // override if the row has one, then its scale steps in order (sequential
 // half-up, transform.py:174-183).  One thread per (row, scenario) element.
+// One block row of 64 frozen rows x (blockDim.x scenarios) per block: the
+// scenario index is the thread's column (no 64-bit division per element), the
+// scale program bounds are read once per thread, stores are coalesced rows.
+constexpr int kExpandRows = 64;
 __global__ void expand_durations_kernel(const long long* base, const unsigned* group,
                                         const int* ovr_map, const long long* ovr,
                                         const int* scale_ptr, const ScaleStepDev* scale, int rows,
                                         int S, long long ld, long long* out) {
-  const long long total = (long long)rows * S;
-  for (long long i = blockIdx.x * (long long)blockDim.x + threadIdx.x; i < total;
-       i += (long long)gridDim.x * blockDim.x) {
-    const int r = (int)(i / S), s = (int)(i % S);
+  const int s = blockIdx.x * blockDim.x + threadIdx.x;
+  if (s >= S) return;
+  const int e0 = scale_ptr ? scale_ptr[s] : 0, e1 = scale_ptr ? scale_ptr[s + 1] : 0;
+  for (int rb = blockIdx.y * kExpandRows; rb < rows; rb += gridDim.y * kExpandRows)
+  for (int r = rb; r < min(rows, rb + kExpandRows); ++r) {
     long long d = base[r];
     if (ovr_map && ovr_map[r] >= 0) d = ovr[(long long)ovr_map[r] * S + s];
     const unsigned g = group ? group[r] : 0u;
-    if (g != 0u && scale_ptr) {
-      for (int e = scale_ptr[s]; e < scale_ptr[s + 1]; ++e) {
+    if (g != 0u)
+      for (int e = e0; e < e1; ++e) {
         const ScaleStepDev st = scale[e];
         // num == 0: a removal step (the row's start reads -1; d is unused)
         if (g >= (unsigned)st.lo && g <= (unsigned)st.hi && st.num != 0)
           d = scale_half_up(d, st.num, st.den);
       }
-    }
-    out[(long long)r * ld + s] = d;
+    __stcs(out + (long long)r * ld + s, d);
   }
 }
 
@@ -408,10 +412,10 @@ cudaError_t launch_expand_durations(const long long* base, const unsigned* group
                                     const int* ovr_map, const long long* ovr, const int* scale_ptr,
                                     const ScaleStepDev* scale, int rows, int S, long long ld,
                                     long long* out, cudaStream_t st) {
-  const long long total = (long long)rows * S;
-  if (total == 0) return cudaSuccess;
-  const int grid = (int)std::min<long long>((total + 255) / 256, 148LL * 16);
-  expand_durations_kernel<<<grid, 256, 0, st>>>(base, group, ovr_map, ovr, scale_ptr, scale, rows,
+  if ((long long)rows * S == 0) return cudaSuccess;
+  const int bx = S >= 256 ? 256 : ((S + 31) / 32) * 32;
+  const dim3 grid((S + bx - 1) / bx, std::min((rows + kExpandRows - 1) / kExpandRows, 65535));
+  expand_durations_kernel<<<grid, bx, 0, st>>>(base, group, ovr_map, ovr, scale_ptr, scale, rows,
                                                 S, ld, out);
   note_launch();
   return cudaGetLastError();

@@ -263,9 +263,118 @@ __global__ void __launch_bounds__(128) seg_scan_kernel(const LaneSegParams sg, i
   }
 }
 
+// The same composition as a warp-parallel prefix scan, one warp per scenario:
+// lane q holds segment c0 + q's transfer matrix; a Hillis-Steele inclusive
+// scan of (max,+) products (int64 path weights; "none" < 0) gives every
+// segment's product P_k = A_k (x) ... (x) A_c0, so all 32 input / output
+// states of a chunk follow from the chunk's input state at once.  Exact as the
+// sequential form: every transfer keeps a non-negative diagonal (each lane
+// head's output depends on its own input), so no row is all "none" and the
+// 0-floor of the sequential step never binds.  Few scenarios (configs 1, 2)
+// leave the sequential scan latency-bound on the coefficient loads.
+template <int LN>
+__global__ void __launch_bounds__(128) seg_wscan_kernel(const LaneSegParams sg, int S, int k_from,
+                                                        int k_to, long long* gslots) {
+  const int s = (int)((blockIdx.x * (long long)blockDim.x + threadIdx.x) >> 5);
+  const int q = threadIdx.x & 31;
+  if (s >= S) return;  // whole warps
+  constexpr int E = LN * LN;
+  const long long sp = sg.s_pad;
+  long long st[LN];
+#pragma unroll
+  for (int j = 0; j < LN; ++j)
+    st[j] = k_from == 0 ? 0 : sg.state[((long long)k_from * LN + j) * sp + s];
+  for (int c0 = k_from; c0 < k_to; c0 += 32) {
+    const int k = c0 + q;
+    const bool valid = k < k_to;
+    long long P[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      long long v = (e / LN == e % LN) ? 0 : -1;  // identity for lanes past the end
+      if (valid) {
+        const int x = sg.trans[((long long)k * E + e) * sp + s];
+        v = x >= 0 ? (long long)x : -1;
+      }
+      P[e] = v;
+    }
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      long long Q[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) Q[e] = __shfl_up_sync(0xffffffffu, P[e], off);
+      if (q >= off) {
+        long long R[E];
+#pragma unroll
+        for (int j = 0; j < LN; ++j)
+#pragma unroll
+          for (int i = 0; i < LN; ++i) {
+            long long m = -1;
+#pragma unroll
+            for (int t = 0; t < LN; ++t) {
+              const long long a = P[j * LN + t], b = Q[t * LN + i];
+              if (a >= 0 && b >= 0) m = max(m, a + b);
+            }
+            R[j * LN + i] = m;
+          }
+#pragma unroll
+        for (int e = 0; e < E; ++e) P[e] = R[e];
+      }
+    }
+    // input state of segment k = P_{k-1} (x) st (lane 0: st itself)
+    long long Pm[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) Pm[e] = __shfl_up_sync(0xffffffffu, P[e], 1);
+    long long in[LN], out[LN];
+#pragma unroll
+    for (int j = 0; j < LN; ++j) {
+      long long vi = 0, vo = 0;
+#pragma unroll
+      for (int i = 0; i < LN; ++i) {
+        if (Pm[j * LN + i] >= 0) vi = max(vi, Pm[j * LN + i] + st[i]);
+        if (P[j * LN + i] >= 0) vo = max(vo, P[j * LN + i] + st[i]);
+      }
+      in[j] = q == 0 ? st[j] : vi;
+      out[j] = vo;
+    }
+    if (valid) {
+      if (sg.carry_ptr != nullptr)
+        for (int c = sg.carry_ptr[k]; c < sg.carry_ptr[k + 1]; ++c) {
+          const int gid = sg.carry_gid[c];
+          const int* cf = sg.carry_coef + (long long)gid * LN * sp + s;
+          long long v = 0;
+#pragma unroll
+          for (int i = 0; i < LN; ++i) {
+            const int x = cf[(long long)i * sp];
+            if (x >= 0) v = max(v, (long long)x + in[i]);
+          }
+          gslots[(long long)gid * sp + s] = v;
+        }
+      long long* o = sg.state + (long long)(k + 1) * LN * sp + s;
+#pragma unroll
+      for (int j = 0; j < LN; ++j) o[(long long)j * sp] = out[j];
+    }
+    // the next chunk starts from the last segment's output
+    const int last = min(31, k_to - 1 - c0);
+#pragma unroll
+    for (int j = 0; j < LN; ++j) st[j] = __shfl_sync(0xffffffffu, out[j], last);
+  }
+}
+
 static cudaError_t launch_seg_scan(const LaneSegParams& sg, int S, int k_from, int k_to,
                                    long long* gslots, cudaStream_t stream) {
   if (k_to <= k_from) return cudaSuccess;
+  // warp-parallel scan unless the scenarios alone fill the GPU
+  if (S < 4096 && getenv("DDSIM_SEG_SEQSCAN") == nullptr) {
+    const int gw = (S * 32 + 127) / 128;
+    switch (sg.LN) {
+      case 1: seg_wscan_kernel<1><<<gw, 128, 0, stream>>>(sg, S, k_from, k_to, gslots); break;
+      case 2: seg_wscan_kernel<2><<<gw, 128, 0, stream>>>(sg, S, k_from, k_to, gslots); break;
+      case 3: seg_wscan_kernel<3><<<gw, 128, 0, stream>>>(sg, S, k_from, k_to, gslots); break;
+      default: seg_wscan_kernel<4><<<gw, 128, 0, stream>>>(sg, S, k_from, k_to, gslots); break;
+    }
+    note_launch();
+    return cudaGetLastError();
+  }
   const int gs = (S + 127) / 128;
   switch (sg.LN) {
     case 1: seg_scan_kernel<1><<<gs, 128, 0, stream>>>(sg, S, k_from, k_to, gslots); break;

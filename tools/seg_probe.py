@@ -24,7 +24,7 @@ from paper_2006_03318_b200.batch import ScenarioTable, compile_scale_sweep, simu
 from paper_2006_03318_b200.frozen import FrozenGraph
 from paper_2006_03318_b200.transform import GPU_TASKS, And, ByLayer
 
-MODES = {"seg": {}, "single": {"DDSIM_NO_SEG": "1"}}
+MODES = {"seg": {}, "seqscan": {"DDSIM_SEG_SEQSCAN": "1"}, "single": {"DDSIM_NO_SEG": "1"}}
 
 
 def timed(fz, table, S, env, reps=10):
@@ -83,7 +83,8 @@ def main():
             out[mode] = (t, st.cpu(), ms.cpu())
             print(json.dumps({"workload": name, "S": S, "mode": mode, "env": extra, "ms": round(t, 4),
                               "G_updates_per_s": round(fz.n * S / t / 1e6, 2)}), flush=True)
-        same = torch.equal(out["seg"][1], out["single"][1]) and torch.equal(out["seg"][2], out["single"][2])
+        same = all(torch.equal(out[m][1], out["single"][1]) and torch.equal(out[m][2], out["single"][2])
+                   for m in out)
         print(json.dumps({"workload": name, "S": S, "identical": bool(same),
                           "speedup": round(out["single"][0] / out["seg"][0], 3)}), flush=True)
 
