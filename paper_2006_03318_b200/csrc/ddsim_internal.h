@@ -289,6 +289,10 @@ cudaError_t launch_expand_durations(const long long* base, const unsigned* group
                                     const int* ovr_map, const long long* ovr, const int* scale_ptr,
                                     const ScaleStepDev* scale, int rows, int S, long long ld,
                                     long long* out, cudaStream_t st);
+cudaError_t launch_expand_durations32(const long long* base, const unsigned* group,
+                                      const int* ovr_map, const long long* ovr,
+                                      const int* scale_ptr, const ScaleStepDev* scale, int rows,
+                                      int S, long long ld, int* out, cudaStream_t st);
 // Batched runtime breakdown (breakdown.py:42-111) over a max-plus result.
 struct BdChain {
   int lane, pos;            // inserted after `pos` static rows of its lane

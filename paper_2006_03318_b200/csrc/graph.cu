@@ -214,6 +214,7 @@ struct ks_graph {
   int n_slots = 0, ksm = 0, kglob = 0;
   int n_rec = 0;
   int n_levels = 0;
+  long long dur_abs_max = -1;  // max |base duration| (build_programs; -1: unknown)
   int n_chains = 0;
   int perm_ld = 0;
   bool rows_are_records = true;  // no chains: record i writes row i
@@ -815,6 +816,14 @@ void build_programs(ks_graph* g, LazyPrograms& S) {
   auto& tail_of = S.tail_of;
   auto& cptr = S.cptr;
   auto& cadj = S.cadj;
+  {  // bounds the expanded duration matrix (int32 when it fits, simulate_impl)
+    long long mx = 0;
+    for (int t = 0; t < n; ++t) {
+      const long long v = d->duration[t];
+      mx = std::max(mx, v == LLONG_MIN ? LLONG_MAX : (v < 0 ? -v : v));
+    }
+    g->dur_abs_max = mx;
+  }
   // ---- levels ------------------------------------------------------------------
   // Without chains: pull form in record space -- level(i) = 1 + max over the
   // record's predecessors, which are recent records (cache-resident); the
@@ -1935,6 +1944,37 @@ namespace {
 // every record of its scenario); K segments multiply the parallelism by K at
 // the cost of a transfer pass.  Cuts come from the compiler's clean rows
 // (no live slot value), near K evenly spaced targets.
+// Upper bound of |duration| over every (row, scenario) a table derives: the
+// base / override magnitude through each scenario's scale steps, each step
+// ceil(b * num / den) + 1 (half-up rounds by at most one).  Host tables only.
+bool expand_fits_int32(const ks_graph* g, const ks_scenarios_desc* sc) {
+  if (g->dur_abs_max < 0) return false;
+  const int S = sc->n_scenarios;
+  long long b0 = g->dur_abs_max;
+  if (sc->n_overrides > 0) {
+    const long long cnt = (long long)sc->n_overrides * S;
+    for (long long i = 0; i < cnt; ++i) {
+      const long long v = sc->override[i];
+      if (v == LLONG_MIN) return false;
+      b0 = std::max(b0, v < 0 ? -v : v);
+    }
+  }
+  const long long lim = INT_MAX;
+  if (b0 > lim) return false;
+  if (!sc->scale_ptr || !sc->scale) return true;
+  for (int s = 0; s < S; ++s) {
+    long long b = b0;
+    for (int e = sc->scale_ptr[s]; e < sc->scale_ptr[s + 1]; ++e) {
+      const ks_scale_step& st = sc->scale[e];
+      if (st.num <= 0 || st.den <= 0) continue;  // removal steps
+      const __int128 x = ((__int128)b * st.num + st.den - 1) / st.den + 1;
+      if (x > lim) return false;
+      b = std::max(b, (long long)x);  // steps on other groups leave b
+    }
+  }
+  return true;
+}
+
 std::vector<int> pick_segments(const ks_graph* g, int S, int nsm) {
   std::vector<int> rows;
   if (getenv("DDSIM_NO_SEG") || !g->has_lanes || (g->lkglob > 0 && g->seg_c0 < 0) ||
@@ -1953,9 +1993,11 @@ std::vector<int> pick_segments(const ks_graph* g, int S, int nsm) {
   long long tps = 4096;
   if (const char* e = getenv("DDSIM_SEG_TPS")) tps = std::max(32LL, atoll(e));
   // shorter segments only when a few scenarios must fill the GPU (config 1,
-  // S = 2: 320 -> 96 records per segment, 0.107 -> 0.074 ms; configs 2 / 3
-  // are faster at 320: fewer transfers and scan steps per scenario)
-  long long min_len = 96 + (320 - 96) * std::min<long long>(S, 256) / 256;
+  // S = 2: 320 -> 96 records per segment, 0.107 -> 0.074 ms; config 2,
+  // S = 401: 320 -> 192, 0.143 -> 0.125 ms; config 3, S = 4,000, is fastest
+  // at 320: fewer transfers and scan steps per scenario)
+  long long min_len = S <= 256 ? 96 + 96 * (long long)S / 256
+                      : S < 2048 ? 192 + 128 * ((long long)S - 256) / 1792 : 320;
   if (const char* e = getenv("DDSIM_SEG_MIN_LEN")) min_len = std::max(16LL, atoll(e));
   long long K = (tps * nsm + S - 1) / S;
   K = std::min<long long>(K, g->ln_rec / min_len);
@@ -2049,12 +2091,24 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
                       g->n_rec > 0 && (long long)g->n * S * 8 <= (8LL << 30) &&
                       getenv("DDSIM_NO_EXPAND") == nullptr && getenv("DDSIM_NO_LANES") == nullptr;
   if (expand) {
-    const long long eld = (S + 1) / 2 * 2;  // TMA: 16 B row pitch
-    long long* buf = T.scratch<long long>((size_t)g->n * eld);
-    CUDA_TRY(launch_expand_durations(g->d_dur, g->d_group, T.ovr_map, T.ovr, T.scale_ptr, T.scale,
-                                     g->n, S, eld, buf, stream));
+    // int32 elements when every derived duration provably fits: half the
+    // bytes for the expansion and for each pass that reads it back (config 2)
+    const bool narrow = expand_fits_int32(g, sc) && getenv("DDSIM_EXPAND64") == nullptr;
+    const long long eld = narrow ? (S + 3) / 4 * 4 : (S + 1) / 2 * 2;  // TMA: 16 B row pitch
+    void* buf = nullptr;
+    if (narrow) {
+      int* b32 = T.scratch<int>((size_t)g->n * eld);
+      CUDA_TRY(launch_expand_durations32(g->d_dur, g->d_group, T.ovr_map, T.ovr, T.scale_ptr,
+                                         T.scale, g->n, S, eld, b32, stream));
+      buf = b32;
+    } else {
+      long long* b64 = T.scratch<long long>((size_t)g->n * eld);
+      CUDA_TRY(launch_expand_durations(g->d_dur, g->d_group, T.ovr_map, T.ovr, T.scale_ptr, T.scale,
+                                       g->n, S, eld, b64, stream));
+      buf = b64;
+    }
     expanded = *sc;
-    expanded.dense_kind = 2;
+    expanded.dense_kind = narrow ? 1 : 2;
     expanded.dense = buf;
     expanded.dense_ld = eld;
     expanded.n_overrides = 0;

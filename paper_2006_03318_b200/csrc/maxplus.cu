@@ -385,40 +385,88 @@ namespace ddsim {
 // scenario index is the thread's column (no 64-bit division per element), the
 // scale program bounds are read once per thread, stores are coalesced rows.
 constexpr int kExpandRows = 64;
-__global__ void expand_durations_kernel(const long long* base, const unsigned* group,
-                                        const int* ovr_map, const long long* ovr,
-                                        const int* scale_ptr, const ScaleStepDev* scale, int rows,
-                                        int S, long long ld, long long* out) {
+constexpr int kExpandBatch = 8;   // rows whose (uniform) loads are issued together
+constexpr int kExpandRegSteps = 4;
+// out of line: the divisions hold no registers in the row loop
+__device__ __noinline__ long long expand_scale(long long d, long long num, long long den) {
+  return scale_half_up(d, num, den);
+}
+template <class OutT>
+__global__ void __launch_bounds__(256) expand_durations_kernel(
+    const long long* __restrict__ base, const unsigned* __restrict__ group,
+    const int* __restrict__ ovr_map, const long long* __restrict__ ovr,
+    const int* __restrict__ scale_ptr, const ScaleStepDev* __restrict__ scale, int rows, int S,
+    long long ld, OutT* __restrict__ out) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= S) return;
   const int e0 = scale_ptr ? scale_ptr[s] : 0, e1 = scale_ptr ? scale_ptr[s + 1] : 0;
-  for (int rb = blockIdx.y * kExpandRows; rb < rows; rb += gridDim.y * kExpandRows)
-  for (int r = rb; r < min(rows, rb + kExpandRows); ++r) {
-    long long d = base[r];
-    if (ovr_map && ovr_map[r] >= 0) d = ovr[(long long)ovr_map[r] * S + s];
-    const unsigned g = group ? group[r] : 0u;
-    if (g != 0u)
-      for (int e = e0; e < e1; ++e) {
-        const ScaleStepDev st = scale[e];
-        // num == 0: a removal step (the row's start reads -1; d is unused)
-        if (g >= (unsigned)st.lo && g <= (unsigned)st.hi && st.num != 0)
-          d = scale_half_up(d, st.num, st.den);
+  // the scenario's first steps in registers (a Shrink sweep has one or two)
+  ScaleStepDev rs[kExpandRegSteps];
+#pragma unroll
+  for (int k = 0; k < kExpandRegSteps; ++k) {
+    rs[k] = ScaleStepDev{1, 0, 0, 1};  // empty group range
+    if (e0 + k < e1) rs[k] = scale[e0 + k];
+  }
+  for (int rb = blockIdx.y * kExpandRows; rb < rows; rb += gridDim.y * kExpandRows) {
+    const int re = min(rows, rb + kExpandRows);
+    for (int r0 = rb; r0 < re; r0 += kExpandBatch) {
+      long long d[kExpandBatch];
+      unsigned g[kExpandBatch];
+#pragma unroll
+      for (int j = 0; j < kExpandBatch; ++j) {
+        const int r = min(r0 + j, re - 1);
+        d[j] = base[r];
+        g[j] = group ? group[r] : 0u;
+        if (ovr_map) {
+          const int o = ovr_map[r];
+          if (o >= 0) d[j] = ovr[(long long)o * S + s];
+        }
       }
-    __stcs(out + (long long)r * ld + s, d);
+#pragma unroll
+      for (int j = 0; j < kExpandBatch; ++j) {
+        if (g[j] != 0u) {
+#pragma unroll
+          for (int k = 0; k < kExpandRegSteps; ++k)
+            // num == 0: a removal step (the row's start reads -1; d is unused)
+            if (g[j] >= (unsigned)rs[k].lo && g[j] <= (unsigned)rs[k].hi && rs[k].num != 0)
+              d[j] = expand_scale(d[j], rs[k].num, rs[k].den);
+          for (int e = e0 + kExpandRegSteps; e < e1; ++e) {
+            const ScaleStepDev st = scale[e];
+            if (g[j] >= (unsigned)st.lo && g[j] <= (unsigned)st.hi && st.num != 0)
+              d[j] = expand_scale(d[j], st.num, st.den);
+          }
+        }
+        // int32: the caller bounded every value (expand_fits_int32)
+        if (r0 + j < re) __stcs(out + (long long)(r0 + j) * ld + s, (OutT)d[j]);
+      }
+    }
   }
 }
 
+template <class OutT>
+static cudaError_t launch_expand(const long long* base, const unsigned* group, const int* ovr_map,
+                                 const long long* ovr, const int* scale_ptr,
+                                 const ScaleStepDev* scale, int rows, int S, long long ld,
+                                 OutT* out, cudaStream_t st) {
+  if ((long long)rows * S == 0) return cudaSuccess;
+  const int bx = S >= 256 ? 256 : ((S + 31) / 32) * 32;
+  const dim3 grid((S + bx - 1) / bx, std::min((rows + kExpandRows - 1) / kExpandRows, 65535));
+  expand_durations_kernel<OutT><<<grid, bx, 0, st>>>(base, group, ovr_map, ovr, scale_ptr, scale,
+                                                     rows, S, ld, out);
+  note_launch();
+  return cudaGetLastError();
+}
 cudaError_t launch_expand_durations(const long long* base, const unsigned* group,
                                     const int* ovr_map, const long long* ovr, const int* scale_ptr,
                                     const ScaleStepDev* scale, int rows, int S, long long ld,
                                     long long* out, cudaStream_t st) {
-  if ((long long)rows * S == 0) return cudaSuccess;
-  const int bx = S >= 256 ? 256 : ((S + 31) / 32) * 32;
-  const dim3 grid((S + bx - 1) / bx, std::min((rows + kExpandRows - 1) / kExpandRows, 65535));
-  expand_durations_kernel<<<grid, bx, 0, st>>>(base, group, ovr_map, ovr, scale_ptr, scale, rows,
-                                                S, ld, out);
-  note_launch();
-  return cudaGetLastError();
+  return launch_expand(base, group, ovr_map, ovr, scale_ptr, scale, rows, S, ld, out, st);
+}
+cudaError_t launch_expand_durations32(const long long* base, const unsigned* group,
+                                      const int* ovr_map, const long long* ovr,
+                                      const int* scale_ptr, const ScaleStepDev* scale, int rows,
+                                      int S, long long ld, int* out, cudaStream_t st) {
+  return launch_expand(base, group, ovr_map, ovr, scale_ptr, scale, rows, S, ld, out, st);
 }
 
 }  // namespace ddsim

@@ -53,9 +53,11 @@ def test_config4_full_graph():
     assert np.array_equal(res.lane_busy.sum(axis=1), dense.astype(np.int64).sum(axis=0))
 
 
-@pytest.mark.parametrize("durations", ["expanded", "derived"])
+@pytest.mark.parametrize("durations", ["expanded", "expanded64", "derived"])
 def test_config2_full_sweep(durations, monkeypatch):
     monkeypatch.setenv("DDSIM_FORCE_DERIVED" if durations == "derived" else "DDSIM_NO_DERIVED", "1")
+    if durations == "expanded64":  # int64 matrix (default: int32, the durations fit)
+        monkeypatch.setenv("DDSIM_EXPAND64", "1")
     w = W.bert_trace(buckets_mb=None)
     g = w.graph
     scen = [[(And([GPU_TASKS, ByLayer(l)]), "1/2")] for l in w.layers]

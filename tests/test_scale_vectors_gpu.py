@@ -22,7 +22,8 @@ pytestmark = pytest.mark.gpu
 
 PATHS = {
     "derived-lanes": ({"DDSIM_FORCE_DERIVED": "1"}, N.KS_PATH_AUTO),
-    "expand+lanes": ({"DDSIM_NO_DERIVED": "1"}, N.KS_PATH_AUTO),
+    "expand+lanes": ({"DDSIM_NO_DERIVED": "1"}, N.KS_PATH_AUTO),  # int32 matrix where it fits
+    "expand64+lanes": ({"DDSIM_NO_DERIVED": "1", "DDSIM_EXPAND64": "1"}, N.KS_PATH_AUTO),
     "lanes-general": ({"DDSIM_NO_EXPAND": "1"}, N.KS_PATH_AUTO),
     "general": ({"DDSIM_NO_EXPAND": "1", "DDSIM_NO_LANES": "1"}, N.KS_PATH_AUTO),
     "listsched": ({}, N.KS_PATH_LISTSCHED),
