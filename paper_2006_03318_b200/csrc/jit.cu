@@ -249,12 +249,7 @@ std::string seg_source(const std::vector<int>& codes, int dk, int LN, bool ch, i
   src += disp + sdisp + sdisp2 + kLanesBodySrc + "\n" + kSegBodySrc + "\n";
   const char* names[] = {"ddsim_seg_replay", "ddsim_seg_transfer", "ddsim_seg_fused",
                          "ddsim_seg_transfer2"};
-  if (mode == 3)  // two scenarios per thread, duration tiles, no chains
-    return src + "extern \"C\" __global__ void __launch_bounds__(" + bounds + ") " + names[3] +
-           "(const __grid_constant__ ddsim_lanes::Tmap tmap, const ddsim_lanes::Params p, "
-           "const ddsim_lanes::SegParams sg) {\n  ddsim_lanes::sym_body2<" + std::to_string(dk) +
-           ", " + std::to_string(LN) + ">(&tmap, p, sg);\n}\n";
-  const char* bodies[] = {"replay_body", "sym_body", "fused_body"};
+  const char* bodies[] = {"replay_body", "sym_body", "fused_body", "sym_body2"};
   src += std::string("extern \"C\" __global__ void __launch_bounds__(") + bounds + ") " + names[mode] +
          "(const __grid_constant__ ddsim_lanes::Tmap tmap, const ddsim_lanes::Params p, "
          "const ddsim_lanes::SegParams sg" +
@@ -362,9 +357,8 @@ cudaError_t launch_lanes_seg_jit(int mode, const LaneParams& p, const LaneChainP
   if (dp) dpv = *dp;
   void* args_ch[] = {tm, &pp, sg, &cpv, &dpv};
   void* args_nc[] = {tm, &pp, sg, &dpv};
-  void* args_2[] = {tm, &pp, sg};
   const CUresult r = g_drv.launch(fn, gx, gy, 1, BD, 1, 1, (unsigned)smem, (CUstream)stream,
-                                  mode == 3 ? args_2 : (cp ? args_ch : args_nc), nullptr);
+                                  cp ? args_ch : args_nc, nullptr);
   if (r != CUDA_SUCCESS) {
     log_line("cuLaunchKernel (segment) failed: " + std::to_string((int)r));
     return cudaErrorLaunchFailure;

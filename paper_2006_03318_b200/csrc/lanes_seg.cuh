@@ -286,15 +286,18 @@ __device__ __forceinline__ void sym_pass(const Tmap* tmap, const Params& p, cons
     for (int i = 0; i < LN; ++i) coef[j][i] = Y.v[j][i];
 }
 
-// Two scenarios per thread (duration tiles, no chains): the transfer pass is
-// instruction-bound (record decode and dispatch dominate the L x L coefficient
-// updates), so a thread decodes each record once for two adjacent scenarios.
-// DDSIM_SYM_DISPATCH2(h) applies the handler to (Y, dv, gp) and (Y2, dv2, gp).
-template <int DK, int LN>
+// Two scenarios per thread: the transfer pass is instruction-bound (record
+// decode and dispatch dominate the L x L coefficient updates), so a thread
+// decodes each record once for two adjacent scenarios.  Duration tiles hold
+// both scenarios' durations (one 8/16-byte load); derived durations (DK 0)
+// share the record's RowDur and derive twice.  Chains and carries as sym_pass,
+// per scenario.  DDSIM_SYM_DISPATCH2(h) applies the handler to (Y, dv, gp)
+// and (Y2, dv2, gp).
+template <int DK, int LN, bool CH>
 __device__ __forceinline__ void sym_pass2(const Tmap* tmap, const Params& p, const SegParams& sg,
-                                          int seg, int blk, int (&coef)[LN][LN],
-                                          int (&coef2)[LN][LN]) {
-  static_assert(DK == 1 || DK == 2, "two scenarios per thread: duration tiles only");
+                                          const ChainParams* cpp, int seg, int blk,
+                                          int (&coef)[LN][LN], int (&coef2)[LN][LN],
+                                          const DerivedParams* dp) {
   extern __shared__ __align__(128) unsigned char smem[];
   const int BD = blockDim.x;
   const int W = 2 * BD;
@@ -306,12 +309,15 @@ __device__ __forceinline__ void sym_pass2(const Tmap* tmap, const Params& p, con
   const unsigned prog_s = sbase + 128;
   const unsigned tile_s = prog_s + kStagesL * kChunkL * (unsigned)sizeof(Rec);
   constexpr unsigned ES = DK == 1 ? 4u : 8u;
-  const unsigned tile_all = (unsigned)(kStagesL * kChunkL * W) * ES;
+  const unsigned tile_all = DK == 0 ? (unsigned)(kStagesL * kChunkL * 16)
+                                    : (unsigned)(kStagesL * kChunkL * W) * ES;
   const unsigned slot_s = tile_s + tile_all;  // [ksm][BD] x 32 B (two scenarios)
   const unsigned col = (unsigned)(tid * 32);
   const unsigned slot_pitch = (unsigned)(BD * 32);
   unsigned char* tst = smem + (tile_s - sbase);
   const int s0 = blk * W;
+  const long long s = s0 + 2 * tid, s2 = s + 1;
+  const bool act = s < p.S, act2 = s2 < p.S;
   const int c_begin = sg.cuts[seg] / kChunkL;
   const int r_end = sg.cuts[seg + 1];
   const int nchunks = (r_end + kChunkL - 1) / kChunkL;
@@ -320,6 +326,12 @@ __device__ __forceinline__ void sym_pass2(const Tmap* tmap, const Params& p, con
     const int st = (c - c_begin) % kStagesL;
     const int nrec = min(kChunkL, r_end - c * kChunkL);
     const unsigned pb = (unsigned)(nrec * sizeof(Rec));
+    if (DK == 0) {
+      l_expect(&bars[st], 2 * pb);
+      l_bulk(pst + st * kChunkL, p.prog + (long long)c * kChunkL, pb, &bars[st]);
+      l_bulk(tst + (size_t)st * kChunkL * 16, dp->rows + (long long)c * kChunkL, pb, &bars[st]);
+      return;
+    }
     l_expect(&bars[st], pb + tile_bytes);
     l_bulk(pst + st * kChunkL, p.prog + (long long)c * kChunkL, pb, &bars[st]);
     l_tile(tst + (size_t)st * kChunkL * W * ES, tmap, s0, c * kChunkL, &bars[st]);
@@ -338,18 +350,29 @@ __device__ __forceinline__ void sym_pass2(const Tmap* tmap, const Params& p, con
   for (int l = 0; l <= NLANE; ++l)
 #pragma unroll
     for (int c = 0; c < LN; ++c) Y.v[l][c] = Y2.v[l][c] = (l == c) ? 0 : kNegSym;
-  const unsigned row_pitch = (unsigned)W * ES;
+  const unsigned row_pitch = DK == 0 ? 16u : (unsigned)W * ES;
+  Prog P, P2;
+  if (DK == 0) {
+    prog_load(dp, s, act, P);
+    prog_load(dp, s2, act2, P2);
+  }
 
   for (int c = c_begin; c < nchunks; ++c) {
     const int st = (c - c_begin) % kStagesL;
     l_wait(&bars[st], (unsigned)(((c - c_begin) / kStagesL) & 1));
     const unsigned rec0 = prog_s + (unsigned)(st * kChunkL * sizeof(Rec));
-    const unsigned t0 = tile_s + (unsigned)(st * kChunkL) * row_pitch + (unsigned)tid * ES * 2u;
+    const unsigned t0 = DK == 0 ? tile_s + (unsigned)(st * kChunkL) * 16u
+                                : tile_s + (unsigned)(st * kChunkL) * row_pitch + (unsigned)tid * ES * 2u;
     const int nrec = min(kChunkL, r_end - c * kChunkL);
     int4 raw = l_lds128(rec0);
     int dn = 0, dn2 = 0;
     auto load_d = [&](unsigned ta) {
-      if (DK == 1) {
+      if (DK == 0) {
+        const int4 rd = l_lds128(ta);
+        const long long b = ((long long)rd.y << 32) | (unsigned)rd.x;
+        dn = (int)derived_dur(dp, b, (unsigned)rd.z, rd.w, s, p.S, act, P);
+        dn2 = (int)derived_dur(dp, b, (unsigned)rd.z, rd.w, s2, p.S, act2, P2);
+      } else if (DK == 1) {
         const int2 v = l_lds64i(ta);
         dn = v.x;
         dn2 = v.y;
@@ -371,6 +394,17 @@ __device__ __forceinline__ void sym_pass2(const Tmap* tmap, const Params& p, con
       const unsigned w = (unsigned)r.w;
       const unsigned h = w >> 24;
       const unsigned rare = (w >> 16) & 0xffu;
+      if constexpr (CH) {
+        if (rare & (R_CHAIN | R_NOP)) {
+          if (rare & R_CHAIN) {
+            const int cid = (int)(short)(r.z & 0xffff), row = c * kChunkL + j;
+            chain_sym<DK, LN>(p, *cpp, Y, cid, row, s, act, slot_s, slot_pitch, col, dp, P);
+            chain_sym<DK, LN>(p, *cpp, Y2, cid, row, s2, act2, slot_s, slot_pitch, col + 16u, dp,
+                              P2);
+          }
+          return;
+        }
+      }
       if (rare & R_PRE) {
         int x[4] = {kNegSym, kNegSym, kNegSym, kNegSym}, x2[4] = {kNegSym, kNegSym, kNegSym, kNegSym};
         int y[4], y2[4];
@@ -403,6 +437,17 @@ __device__ __forceinline__ void sym_pass2(const Tmap* tmap, const Params& p, con
         const unsigned a = slot_s + (unsigned)((w << 16) >> 16) * slot_pitch + col;
         sym_slot_st(a, y);
         sym_slot_st(a + 16u, y2);
+      } else if (rare & R_OUT_GLOBAL) {
+        // a carry (read only in the chain segment): its coefficients
+        int y[4], y2[4];
+        sym_get<LN>(Y, (int)(h & 3), y);
+        sym_get<LN>(Y2, (int)(h & 3), y2);
+        int* o = sg.carry_coef + (long long)((int)(w << 16) >> 16) * LN * sg.s_pad + s;
+#pragma unroll
+        for (int q = 0; q < LN; ++q) {
+          if (act) o[(long long)q * sg.s_pad] = y[q];
+          if (act2) o[(long long)q * sg.s_pad + 1] = y2[q];
+        }
       }
     };
 #ifdef DDSIM_UNROLL
@@ -429,10 +474,12 @@ __device__ __forceinline__ void sym_pass2(const Tmap* tmap, const Params& p, con
     }
 }
 
-template <int DK, int LN>
-__device__ __forceinline__ void sym_body2(const Tmap* tmap, const Params& p, const SegParams& sg) {
+template <int DK, int LN, bool CH>
+__device__ __forceinline__ void sym_body2(const Tmap* tmap, const Params& p, const SegParams& sg,
+                                          const ChainParams* cpp, const DerivedParams* dp) {
+  if ((int)blockIdx.y == sg.kc) return;  // the chain segment is replayed numerically
   int coef[LN][LN], coef2[LN][LN];
-  sym_pass2<DK, LN>(tmap, p, sg, (int)blockIdx.y, (int)blockIdx.x, coef, coef2);
+  sym_pass2<DK, LN, CH>(tmap, p, sg, cpp, (int)blockIdx.y, (int)blockIdx.x, coef, coef2, dp);
   const long long s = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * 2;
   if (s < p.S) {  // (an odd S leaves the last thread's second scenario out)
     int* out = sg.trans + (long long)blockIdx.y * LN * LN * sg.s_pad + s;

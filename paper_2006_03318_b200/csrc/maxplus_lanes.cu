@@ -411,20 +411,24 @@ cudaError_t launch_maxplus_lanes_seg(const LaneParams& p, const LaneChainParams*
     return launch_lanes_seg_jit(2, p, cp, &tmap, dkind, sg.LN, codes, &sg, gx * sg.K, 1, BD,
                                 smem_t, stream, dp);
   if (sg.K > 1) {
-    // transfer: two scenarios per thread over duration tiles without chains
-    // (one record decode for both; the pass is instruction-bound)
-    const bool two = dkind != 0 && cp == nullptr && 2 * BD <= 256 &&
-                     getenv("DDSIM_SEG_T1") == nullptr;
+    // transfer: two scenarios per thread (one record decode for both; the
+    // pass is instruction-bound)
+    const bool two = 2 * BD <= 256 && getenv("DDSIM_SEG_T1") == nullptr;
     if (two) {
       CUtensorMap tmap2;
-      e = encode_lanes_tmap(&tmap2, p, dense32, dkind, 2 * BD);
-      if (e != cudaSuccess) return e;
+      memset(&tmap2, 0, sizeof(tmap2));
+      if (dkind != 0) {
+        e = encode_lanes_tmap(&tmap2, p, dense32, dkind, 2 * BD);
+        if (e != cudaSuccess) return e;
+      }
+      const size_t tiles2 = dkind == 0
+                                ? (size_t)stages * ddsim_lanes::kChunkL * sizeof(ddsim_lanes::RowDur)
+                                : (size_t)stages * ddsim_lanes::kChunkL * 2 * BD * es;
       const size_t smem_t2 = 128 + (size_t)stages * ddsim_lanes::kChunkL * sizeof(ddsim_lanes::Rec) +
-                             (size_t)stages * ddsim_lanes::kChunkL * 2 * BD * es +
-                             (size_t)p.ksm * BD * 32;
+                             tiles2 + (size_t)p.ksm * BD * 32;
       const int gx2 = (p.S + 2 * BD - 1) / (2 * BD);
-      e = launch_lanes_seg_jit(3, p, nullptr, &tmap2, dkind, sg.LN, codes, &sg, gx2, sg.K - 1, BD,
-                               smem_t2, stream, nullptr);
+      e = launch_lanes_seg_jit(3, p, cp, &tmap2, dkind, sg.LN, codes, &sg, gx2, sg.K - 1, BD,
+                               smem_t2, stream, dp);
     } else {
       e = launch_lanes_seg_jit(1, p, cp, &tmap, dkind, sg.LN, codes, &sg, gx, sg.K - 1, BD, smem_t,
                                stream, dp);

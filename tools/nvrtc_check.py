@@ -67,13 +67,8 @@ def seg_source(dk: int, LN: int, ch: bool, mode: int, scale: bool) -> str:
         sdisp2 += cond + f"{{ hsym<{_hstep(c)}, LN>(Y, dv, gp); hsym<{_hstep(c)}, LN>(Y2, dv2, gp); }} "
     src += disp + "else __trap();\n" + sdisp + "else __trap();\n" + sdisp2 + "else __trap();\n"
     src += (CSRC / "lanes_body.cuh").read_text() + "\n" + (CSRC / "lanes_seg.cuh").read_text() + "\n"
-    if mode == 3:
-        return src + ("extern \"C\" __global__ void __launch_bounds__(256) ddsim_seg_transfer2("
-                      "const __grid_constant__ ddsim_lanes::Tmap tmap, const ddsim_lanes::Params p, "
-                      f"const ddsim_lanes::SegParams sg) {{\n  ddsim_lanes::sym_body2<{dk}, {LN}>"
-                      "(&tmap, p, sg);\n}\n")
-    name = ["ddsim_seg_replay", "ddsim_seg_transfer", "ddsim_seg_fused"][mode]
-    body = ["replay_body", "sym_body", "fused_body"][mode]
+    name = ["ddsim_seg_replay", "ddsim_seg_transfer", "ddsim_seg_fused", "ddsim_seg_transfer2"][mode]
+    body = ["replay_body", "sym_body", "fused_body", "sym_body2"][mode]
     args = ", const __grid_constant__ ddsim_lanes::ChainParams cp" if ch else ""
     args += ", const __grid_constant__ ddsim_lanes::DerivedParams dp" if dk == 0 else ""
     return src + (f"extern \"C\" __global__ void __launch_bounds__(256) {name}("
@@ -107,11 +102,12 @@ def variants():
                 lanes_source(dk, V, dyn, ch, nolb, scale=True)
         if dk == 0:
             yield f"lanes dk=0 V=1 ch={ch} noscale", lanes_source(0, 1, False, ch, False, False)
-    for dk, LN, ch, mode in itertools.product((0, 1, 2), (2, 3), (False, True), (0, 1)):
+    for dk, LN, ch, mode in itertools.product((0, 1, 2), (2, 3), (False, True), (0, 1, 3)):
         yield f"seg dk={dk} LN={LN} ch={ch} mode={mode}", seg_source(dk, LN, ch, mode, True)
-    for dk, LN in itertools.product((1, 2), (2, 4)):
-        yield f"seg dk={dk} LN={LN} mode=3", seg_source(dk, LN, False, 3, True)
-    yield "seg dk=0 LN=3 ch=True mode=0 noscale", seg_source(0, 3, True, 0, False)
+    for dk in (1, 2):
+        yield f"seg dk={dk} LN=4 mode=3", seg_source(dk, 4, False, 3, True)
+    for mode in (0, 3):
+        yield f"seg dk=0 LN=3 ch=True mode={mode} noscale", seg_source(0, 3, True, mode, False)
 
 
 def main(argv=None) -> int:
