@@ -1993,10 +1993,10 @@ std::vector<int> pick_segments(const ks_graph* g, int S, int nsm) {
   long long tps = 4096;
   if (const char* e = getenv("DDSIM_SEG_TPS")) tps = std::max(32LL, atoll(e));
   // shorter segments only when a few scenarios must fill the GPU (config 1,
-  // S = 2: 320 -> 96 records per segment, 0.107 -> 0.074 ms; config 2,
-  // S = 401: 320 -> 192, 0.143 -> 0.125 ms; config 3, S = 4,000, is fastest
-  // at 320: fewer transfers and scan steps per scenario)
-  long long min_len = S <= 256 ? 96 + 96 * (long long)S / 256
+  // S = 2: 320 -> 96 -> 64 records per segment, 0.107 -> 0.074 -> 0.057 ms
+  // with the block scan; config 2, S = 401: 320 -> 192, 0.143 -> 0.125 ms;
+  // config 3, S = 4,000, is fastest at 320: fewer transfers and scan steps)
+  long long min_len = S <= 256 ? 64 + 128 * (long long)S / 256
                       : S < 2048 ? 192 + 128 * ((long long)S - 256) / 1792 : 320;
   if (const char* e = getenv("DDSIM_SEG_MIN_LEN")) min_len = std::max(16LL, atoll(e));
   long long K = (tps * nsm + S - 1) / S;

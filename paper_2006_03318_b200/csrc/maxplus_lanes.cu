@@ -360,9 +360,160 @@ __global__ void __launch_bounds__(128) seg_wscan_kernel(const LaneSegParams sg, 
   }
 }
 
+// (max,+) product of two LN x LN matrices, newer (x) older; "none" < 0.
+template <int LN>
+__device__ __forceinline__ void mp_mul(const long long* A, const long long* B, long long* R) {
+#pragma unroll
+  for (int j = 0; j < LN; ++j)
+#pragma unroll
+    for (int i = 0; i < LN; ++i) {
+      long long m = -1;
+#pragma unroll
+      for (int t = 0; t < LN; ++t) {
+        const long long a = A[j * LN + t], b = B[t * LN + i];
+        if (a >= 0 && b >= 0) m = max(m, a + b);
+      }
+      R[j * LN + i] = m;
+    }
+}
+
+// Very few scenarios (config 1: S = 2, ~100 segments): one CTA of 32 warps
+// per scenario, warp w scans chunk w of 32 segments, warp 0 scans the 32
+// chunk products, so the whole composition takes two shuffle scans instead of
+// one per chunk in sequence.
+constexpr int kBscanWarps = 16;
+template <int LN>
+__global__ void __launch_bounds__(kBscanWarps * 32) seg_bscan_kernel(const LaneSegParams sg, int S, int k_from,
+                                                         int k_to, long long* gslots) {
+  constexpr int E = LN * LN;
+  __shared__ long long chunk_prod[kBscanWarps][E];
+  __shared__ long long st_sh[LN];
+  const int s = blockIdx.x;
+  const int q = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const long long sp = sg.s_pad;
+  if (threadIdx.x < LN)
+    st_sh[threadIdx.x] = k_from == 0 ? 0 : sg.state[((long long)k_from * LN + threadIdx.x) * sp + s];
+  for (int base = k_from; base < k_to; base += kBscanWarps * 32) {
+    __syncthreads();  // st_sh of this round
+    const int k = base + w * 32 + q;
+    const bool valid = k < k_to;
+    long long P[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+      long long v = (e / LN == e % LN) ? 0 : -1;
+      if (valid) {
+        const int x = sg.trans[((long long)k * E + e) * sp + s];
+        v = x >= 0 ? (long long)x : -1;
+      }
+      P[e] = v;
+    }
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+      long long Q[E], R[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) Q[e] = __shfl_up_sync(0xffffffffu, P[e], off);
+      if (q >= off) {
+        mp_mul<LN>(P, Q, R);
+#pragma unroll
+        for (int e = 0; e < E; ++e) P[e] = R[e];
+      }
+    }
+    if (q == 31)
+#pragma unroll
+      for (int e = 0; e < E; ++e) chunk_prod[w][e] = P[e];
+    __syncthreads();
+    if (w == 0) {  // exclusive prefix over the chunk products
+      long long C[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        C[e] = q < kBscanWarps ? chunk_prod[q][e] : ((e / LN == e % LN) ? 0 : -1);
+#pragma unroll
+      for (int off = 1; off < 32; off <<= 1) {
+        long long Q[E], R[E];
+#pragma unroll
+        for (int e = 0; e < E; ++e) Q[e] = __shfl_up_sync(0xffffffffu, C[e], off);
+        if (q >= off) {
+          mp_mul<LN>(C, Q, R);
+#pragma unroll
+          for (int e = 0; e < E; ++e) C[e] = R[e];
+        }
+      }
+      long long X[E];
+#pragma unroll
+      for (int e = 0; e < E; ++e) {
+        X[e] = __shfl_up_sync(0xffffffffu, C[e], 1);
+        if (q == 0) X[e] = (e / LN == e % LN) ? 0 : -1;
+      }
+      __syncwarp();
+#pragma unroll
+      for (int e = 0; e < E; ++e)
+        if (q < kBscanWarps) chunk_prod[q][e] = X[e];  // now: product of chunks < q
+    }
+    __syncthreads();
+    long long cin[LN];  // the chunk's input state
+#pragma unroll
+    for (int j = 0; j < LN; ++j) {
+      long long v = 0;
+#pragma unroll
+      for (int i = 0; i < LN; ++i) {
+        const long long c = chunk_prod[w][j * LN + i];
+        if (c >= 0) v = max(v, c + st_sh[i]);
+      }
+      cin[j] = v;
+    }
+    long long Pm[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) Pm[e] = __shfl_up_sync(0xffffffffu, P[e], 1);
+    long long in[LN], out[LN];
+#pragma unroll
+    for (int j = 0; j < LN; ++j) {
+      long long vi = 0, vo = 0;
+#pragma unroll
+      for (int i = 0; i < LN; ++i) {
+        if (Pm[j * LN + i] >= 0) vi = max(vi, Pm[j * LN + i] + cin[i]);
+        if (P[j * LN + i] >= 0) vo = max(vo, P[j * LN + i] + cin[i]);
+      }
+      in[j] = q == 0 ? cin[j] : vi;
+      out[j] = vo;
+    }
+    if (valid) {
+      if (sg.carry_ptr != nullptr)
+        for (int c = sg.carry_ptr[k]; c < sg.carry_ptr[k + 1]; ++c) {
+          const int gid = sg.carry_gid[c];
+          const int* cf = sg.carry_coef + (long long)gid * LN * sp + s;
+          long long v = 0;
+#pragma unroll
+          for (int i = 0; i < LN; ++i) {
+            const int x = cf[(long long)i * sp];
+            if (x >= 0) v = max(v, (long long)x + in[i]);
+          }
+          gslots[(long long)gid * sp + s] = v;
+        }
+      long long* o = sg.state + (long long)(k + 1) * LN * sp + s;
+#pragma unroll
+      for (int j = 0; j < LN; ++j) o[(long long)j * sp] = out[j];
+    }
+    __syncthreads();  // every warp has read st_sh
+    if (k == min(k_to, base + kBscanWarps * 32) - 1)  // the round's last segment carries the state on
+#pragma unroll
+      for (int j = 0; j < LN; ++j) st_sh[j] = out[j];
+  }
+}
+
 static cudaError_t launch_seg_scan(const LaneSegParams& sg, int S, int k_from, int k_to,
                                    long long* gslots, cudaStream_t stream) {
   if (k_to <= k_from) return cudaSuccess;
+  if (S <= 16 && k_to - k_from > 32 && getenv("DDSIM_SEG_SEQSCAN") == nullptr &&
+      getenv("DDSIM_SEG_WSCAN") == nullptr) {
+    switch (sg.LN) {
+      case 1: seg_bscan_kernel<1><<<S, kBscanWarps * 32, 0, stream>>>(sg, S, k_from, k_to, gslots); break;
+      case 2: seg_bscan_kernel<2><<<S, kBscanWarps * 32, 0, stream>>>(sg, S, k_from, k_to, gslots); break;
+      case 3: seg_bscan_kernel<3><<<S, kBscanWarps * 32, 0, stream>>>(sg, S, k_from, k_to, gslots); break;
+      default: seg_bscan_kernel<4><<<S, kBscanWarps * 32, 0, stream>>>(sg, S, k_from, k_to, gslots); break;
+    }
+    note_launch();
+    return cudaGetLastError();
+  }
   // warp-parallel scan unless the scenarios alone fill the GPU
   if (S < 4096 && getenv("DDSIM_SEG_SEQSCAN") == nullptr) {
     const int gw = (S * 32 + 127) / 128;

@@ -81,7 +81,34 @@ def _plain(fz, table, monkeypatch):
 
 def _seg_engaged():
     log = (N.lib().ks_jit_log() or b"").decode()
-    return "seg_t:" in log or "seg_f:" in log
+    return "seg_t:" in log or "seg_t2:" in log or "seg_f:" in log
+
+
+@pytest.mark.parametrize("scan", ["block", "warp", "sequential"])
+@pytest.mark.parametrize("S,K", [(1, 40), (5, 600), (16, 1100), (17, 300)])
+def test_seg_scan_kernels_many_segments(S, K, scan, monkeypatch):
+    """The three compositions of the segment transfers -- one CTA per scenario
+    (S <= 16: warp chunks + a scan of the chunk products, several 512-segment
+    rounds at K = 600 / 1100), one warp per scenario, one thread per scenario
+    -- give the single-pass kernel's result."""
+    if scan == "warp":
+        monkeypatch.setenv("DDSIM_SEG_WSCAN", "1")
+    elif scan == "sequential":
+        monkeypatch.setenv("DDSIM_SEG_SEQSCAN", "1")
+    g = slot_graph(n=100_000, seed=5, reach=4)
+    fz = FrozenGraph.from_graph(g)
+    assert fz.info.n_lane_cuts >= 600
+    K = min(K, fz.info.n_lane_cuts)
+    dense = _dense(fz, S, 11)
+    table = ScenarioTable(n_scenarios=S, dense=dense)
+    monkeypatch.setenv("DDSIM_SEG_K", str(K))
+    res = simulate_batch(fz, table)
+    assert _seg_engaged()
+    ref = _plain(fz, table, monkeypatch)
+    assert np.array_equal(res.start, ref.start)
+    assert np.array_equal(res.makespan, ref.makespan)
+    assert np.array_equal(res.lane_busy, ref.lane_busy)
+    _oracle_cols(g, fz, dense, res, [S - 1])
 
 
 @pytest.mark.parametrize("passes", ["fused", "3pass"])
