@@ -765,7 +765,7 @@ def run_config(args):
                      "frac": achieved / peak, "peak_source": peak_src,
                      "algorithmic_bytes_per_launch": n * S * bpu, "traffic": None,
                      "traffic_source": "not captured in this run (see profiles/)",
-                     "path": "segment-parallel" if "seg_t:" in jit else "single-pass"},
+                     "path": "segment-parallel" if "seg_t" in jit else "single-pass"},
         "cpu_baseline": cb,
         "e2e": {"value": n * S / dt, "unit": UNIT, "h2d_bytes_per_step": _table_bytes(table),
                 "d2h_bytes_per_step": S * 8 + S * L * 8,

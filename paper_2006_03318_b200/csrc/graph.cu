@@ -1842,8 +1842,54 @@ void free_graph(ks_graph* g) {
 }
 
 // ---- per-call scenario tables ---------------------------------------------------
+// Device blocks of finished calls, per host thread, reused by the next call on
+// the same stream (stream order makes the reuse safe, as it does for
+// cudaFreeAsync + cudaMallocAsync): a small sweep's call otherwise spends ~8 us
+// of host time in a dozen allocator calls.  Bounded; freed at thread exit.
+struct ScratchPool {
+  struct Blk {
+    void* p;
+    size_t bytes;
+    cudaStream_t st;
+  };
+  std::vector<Blk> free_blks;
+  size_t held = 0;
+  static constexpr size_t kMaxHeld = 512ull << 20;
+  static constexpr size_t kMaxBlks = 64;
+  void* take(size_t bytes, cudaStream_t st) {
+    int best = -1;
+    for (int i = 0; i < (int)free_blks.size(); ++i) {
+      const Blk& b = free_blks[i];
+      if (b.st == st && b.bytes >= bytes && b.bytes <= 2 * bytes + 4096 &&
+          (best < 0 || b.bytes < free_blks[best].bytes))
+        best = i;
+    }
+    if (best < 0) return nullptr;
+    void* p = free_blks[best].p;
+    held -= free_blks[best].bytes;
+    free_blks[best] = free_blks.back();
+    free_blks.pop_back();
+    return p;
+  }
+  void give(void* p, size_t bytes, cudaStream_t st) {
+    if (held + bytes > kMaxHeld || free_blks.size() >= kMaxBlks) {
+      cudaFreeAsync(p, st);
+      return;
+    }
+    free_blks.push_back({p, bytes, st});
+    held += bytes;
+  }
+  ~ScratchPool() {
+    for (const Blk& b : free_blks) cudaFree(b.p);
+  }
+};
+ScratchPool& scratch_pool() {
+  static thread_local ScratchPool pool;
+  return pool;
+}
+
 struct ScenTables {
-  std::vector<void*> bufs;
+  std::vector<std::pair<void*, size_t>> bufs;
   int* scale_ptr = nullptr;
   ScaleStepDev* scale = nullptr;
   long long* ovr = nullptr;
@@ -1853,25 +1899,26 @@ struct ScenTables {
   int* vrank = nullptr;
   bool has_remove = false;  // a scale step removes tasks (KS_STEP_REMOVE)
   cudaStream_t st = nullptr;
+  void* alloc(size_t bytes) {
+    void* p = scratch_pool().take(bytes, st);
+    if (p == nullptr) CUDA_TRY(cudaMallocAsync(&p, bytes, st));
+    bufs.push_back({p, bytes});
+    return p;
+  }
   template <class T>
   T* up(const T* host, size_t count) {
     if (!host || count == 0) return nullptr;
-    T* p = nullptr;
-    CUDA_TRY(cudaMallocAsync(&p, count * sizeof(T), st));
-    bufs.push_back(p);
+    T* p = static_cast<T*>(alloc(count * sizeof(T)));
     CUDA_TRY(cudaMemcpyAsync(p, host, count * sizeof(T), cudaMemcpyHostToDevice, st));
     return p;
   }
   template <class T>
   T* scratch(size_t count) {
-    T* p = nullptr;
     if (count == 0) return nullptr;
-    CUDA_TRY(cudaMallocAsync(&p, count * sizeof(T), st));
-    bufs.push_back(p);
-    return p;
+    return static_cast<T*>(alloc(count * sizeof(T)));
   }
   ~ScenTables() {
-    for (void* p : bufs) cudaFreeAsync(p, st);
+    for (auto& b : bufs) scratch_pool().give(b.first, b.second, st);
   }
   // host staging must outlive async copies: keep vectors alive
   std::vector<std::vector<char>> keep;

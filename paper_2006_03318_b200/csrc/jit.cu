@@ -147,13 +147,18 @@ std::string make_source(const std::vector<int>& codes, int dk, int V, bool dyn, 
 
 // Compile `src` once per key (NVRTC -> cubin -> module) and return `fname`;
 // failures are cached as nullptr too (no retry of a failing compile).
-CUfunction get_compiled(const std::string& key, const std::string& src, const char* fname) {
+// The source is generated only on a cache miss: it is ~100 KB of text, and
+// building it on every launch cost several microseconds of host time per
+// kernel (config 1's whole call is ~60 us of host work).
+template <class MakeSrc>
+CUfunction get_compiled(const std::string& key, MakeSrc make_src, const char* fname) {
   if (getenv("DDSIM_NO_JIT")) return nullptr;  // checked per call (tests switch paths)
   std::lock_guard<std::mutex> lk(g_mu);
   init_locked();
   if (!g_nv.ok || !g_drv.ok) return nullptr;
   auto it = g_cache.find(key);
   if (it != g_cache.end()) return it->second;
+  const std::string src = make_src();
   nvrtcProgram_t prog = nullptr;
   CUfunction fn = nullptr;
   if (g_nv.create(&prog, src.c_str(), "ddsim_lanes_jit.cu", 0, nullptr, nullptr) == 0) {
@@ -203,7 +208,8 @@ CUfunction get_function(const std::vector<int>& codes, int dk, int V, bool dyn, 
   if (const char* b = getenv("DDSIM_LANES_BODY")) key += std::string("b") + b + ":";
   for (int c : codes) key += std::to_string(c) + ",";
   if (getenv("DDSIM_NO_JIT")) return nullptr;
-  return get_compiled(key, make_source(codes, dk, V, dyn, ch, nolb, scale), "ddsim_lanes_jit");
+  return get_compiled(key, [&] { return make_source(codes, dk, V, dyn, ch, nolb, scale); },
+                      "ddsim_lanes_jit");
 }
 
 // Segment kernels (SegParams in lanes_body.cuh): the transfer pass in
@@ -341,7 +347,7 @@ cudaError_t launch_lanes_seg_jit(int mode, const LaneParams& p, const LaneChainP
   const bool scale = dp != nullptr && dp->scale_ptr != nullptr;
   if (dkind == 0 && !scale) key += "noscale:";
   for (int c : codes) key += std::to_string(c) + ",";
-  CUfunction fn = get_compiled(key, seg_source(codes, dkind, LN, cp != nullptr, mode, scale),
+  CUfunction fn = get_compiled(key, [&] { return seg_source(codes, dkind, LN, cp != nullptr, mode, scale); },
                                names[mode]);
   if (!fn) return cudaErrorNotSupported;
   if (g_drv.setattr(fn, CU_FUNC_ATTRIBUTE_MAX_DYNAMIC_SHARED_SIZE_BYTES, (int)smem) != CUDA_SUCCESS)
