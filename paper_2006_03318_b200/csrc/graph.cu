@@ -2141,7 +2141,8 @@ int simulate_impl(const ks_graph* g, const ks_scenarios_desc* sc, int policy, in
     // int32 elements when every derived duration provably fits: half the
     // bytes for the expansion and for each pass that reads it back (config 2)
     const bool narrow = expand_fits_int32(g, sc) && getenv("DDSIM_EXPAND64") == nullptr;
-    const long long eld = narrow ? (S + 3) / 4 * 4 : (S + 1) / 2 * 2;  // TMA: 16 B row pitch
+    // rows start on 128-byte lines (whole-sector stores; TMA needs 16 B)
+    const long long eld = narrow ? (S + 31) / 32 * 32 : (S + 15) / 16 * 16;
     void* buf = nullptr;
     if (narrow) {
       int* b32 = T.scratch<int>((size_t)g->n * eld);

@@ -385,21 +385,25 @@ namespace ddsim {
 // scenario index is the thread's column (no 64-bit division per element), the
 // scale program bounds are read once per thread, stores are coalesced rows.
 constexpr int kExpandRows = 64;
-constexpr int kExpandBatch = 8;   // rows whose (uniform) loads are issued together
-constexpr int kExpandRegSteps = 4;
+constexpr int kExpandRegSteps = 1;  // further steps are read from L1
 // out of line: the divisions hold no registers in the row loop
 __device__ __noinline__ long long expand_scale(long long d, long long num, long long den) {
   return scale_half_up(d, num, den);
 }
-template <class OutT>
-__global__ void __launch_bounds__(256) expand_durations_kernel(
+template <class OutT, bool STREAM, bool OVR>
+__global__ void __launch_bounds__(256, 4) expand_durations_kernel(
     const long long* __restrict__ base, const unsigned* __restrict__ group,
     const int* __restrict__ ovr_map, const long long* __restrict__ ovr,
     const int* __restrict__ scale_ptr, const ScaleStepDev* __restrict__ scale, int rows, int S,
     long long ld, OutT* __restrict__ out) {
+  // the block's rows (base, group, override row) staged in shared memory by
+  // one coalesced load, so a thread's row loop waits on no global load
+  __shared__ long long sb[kExpandRows];
+  __shared__ unsigned sgp[kExpandRows];
+  __shared__ int so[kExpandRows];
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
-  if (s >= S) return;
-  const int e0 = scale_ptr ? scale_ptr[s] : 0, e1 = scale_ptr ? scale_ptr[s + 1] : 0;
+  const bool act = s < S;
+  const int e0 = act && scale_ptr ? scale_ptr[s] : 0, e1 = act && scale_ptr ? scale_ptr[s + 1] : 0;
   // the scenario's first steps in registers (a Shrink sweep has one or two)
   ScaleStepDev rs[kExpandRegSteps];
 #pragma unroll
@@ -407,38 +411,59 @@ __global__ void __launch_bounds__(256) expand_durations_kernel(
     rs[k] = ScaleStepDev{1, 0, 0, 1};  // empty group range
     if (e0 + k < e1) rs[k] = scale[e0 + k];
   }
+  // one range test per row before the per-step tests (most rows are outside
+  // every step of a Shrink sweep scenario); group 0 (no selector) never scales
+  unsigned glo = 0xffffffffu, ghi = 0u;
+#pragma unroll
+  for (int k = 0; k < kExpandRegSteps; ++k)
+    if (e0 + k < e1) {
+      glo = min(glo, (unsigned)max(rs[k].lo, 1));
+      ghi = max(ghi, (unsigned)max(rs[k].hi, 0));
+    }
+  for (int e = e0 + kExpandRegSteps; e < e1; ++e) {
+    glo = min(glo, (unsigned)max(scale[e].lo, 1));
+    ghi = max(ghi, (unsigned)max(scale[e].hi, 0));
+  }
+  const unsigned gspan = ghi >= glo ? ghi - glo : 0u;
+  const bool any = ghi >= glo;
   for (int rb = blockIdx.y * kExpandRows; rb < rows; rb += gridDim.y * kExpandRows) {
-    const int re = min(rows, rb + kExpandRows);
-    for (int r0 = rb; r0 < re; r0 += kExpandBatch) {
-      long long d[kExpandBatch];
-      unsigned g[kExpandBatch];
+    const int nr = min(rows - rb, kExpandRows);
+    __syncthreads();  // the previous block row is consumed
+    for (int i = threadIdx.x; i < nr; i += blockDim.x) {
+      const int r = rb + i;
+      sb[i] = base[r];
+      sgp[i] = group ? group[r] : 0u;
+      so[i] = ovr_map ? ovr_map[r] : -1;
+    }
+    __syncthreads();
+    if (!act) continue;
+    OutT* op = out + (long long)rb * ld + s;
+#pragma unroll 4
+    for (int j = 0; j < nr; ++j, op += ld) {
+      long long d = sb[j];
+      if (OVR) {
+        const int o = so[j];
+        if (o >= 0) d = ovr[(long long)o * S + s];
+      }
+      const unsigned g = sgp[j];
+      if (any && g - glo <= gspan) {
 #pragma unroll
-      for (int j = 0; j < kExpandBatch; ++j) {
-        const int r = min(r0 + j, re - 1);
-        d[j] = base[r];
-        g[j] = group ? group[r] : 0u;
-        if (ovr_map) {
-          const int o = ovr_map[r];
-          if (o >= 0) d[j] = ovr[(long long)o * S + s];
+        for (int k = 0; k < kExpandRegSteps; ++k)
+          // num == 0: a removal step (the row's start reads -1; d is unused)
+          if (g >= (unsigned)rs[k].lo && g <= (unsigned)rs[k].hi && rs[k].num != 0)
+            d = expand_scale(d, rs[k].num, rs[k].den);
+        for (int e = e0 + kExpandRegSteps; e < e1; ++e) {
+          const ScaleStepDev st = scale[e];
+          if (g >= (unsigned)st.lo && g <= (unsigned)st.hi && st.num != 0)
+            d = expand_scale(d, st.num, st.den);
         }
       }
-#pragma unroll
-      for (int j = 0; j < kExpandBatch; ++j) {
-        if (g[j] != 0u) {
-#pragma unroll
-          for (int k = 0; k < kExpandRegSteps; ++k)
-            // num == 0: a removal step (the row's start reads -1; d is unused)
-            if (g[j] >= (unsigned)rs[k].lo && g[j] <= (unsigned)rs[k].hi && rs[k].num != 0)
-              d[j] = expand_scale(d[j], rs[k].num, rs[k].den);
-          for (int e = e0 + kExpandRegSteps; e < e1; ++e) {
-            const ScaleStepDev st = scale[e];
-            if (g[j] >= (unsigned)st.lo && g[j] <= (unsigned)st.hi && st.num != 0)
-              d[j] = expand_scale(d[j], st.num, st.den);
-          }
-        }
-        // int32: the caller bounded every value (expand_fits_int32)
-        if (r0 + j < re) __stcs(out + (long long)(r0 + j) * ld + s, (OutT)d[j]);
-      }
+      // int32: the caller bounded every value (expand_fits_int32).  An
+      // L2-sized matrix stays cached for the passes that read it back.
+      if (STREAM)
+        __stcs(op, (OutT)d);
+      else
+        *op = (OutT)d;
     }
   }
 }
@@ -487,8 +512,19 @@ static cudaError_t launch_expand(const long long* base, const unsigned* group, c
   }
   const int bx = S >= 256 ? 256 : ((S + 31) / 32) * 32;
   const dim3 grid((S + bx - 1) / bx, std::min((rows + kExpandRows - 1) / kExpandRows, 65535));
-  expand_durations_kernel<OutT><<<grid, bx, 0, st>>>(base, group, ovr_map, ovr, scale_ptr, scale,
-                                                     rows, S, ld, out);
+  const bool big = (long long)rows * ld * (long long)sizeof(OutT) > (64LL << 20);
+#define EXPAND_K(ST, OV)                                                                        \
+  expand_durations_kernel<OutT, ST, OV><<<grid, bx, 0, st>>>(base, group, ovr_map, ovr, scale_ptr, \
+                                                             scale, rows, S, ld, out)
+  if (big && ovr_map)
+    EXPAND_K(true, true);
+  else if (big)
+    EXPAND_K(true, false);
+  else if (ovr_map)
+    EXPAND_K(false, true);
+  else
+    EXPAND_K(false, false);
+#undef EXPAND_K
   note_launch();
   return cudaGetLastError();
 }
