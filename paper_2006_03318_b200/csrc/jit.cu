@@ -254,8 +254,8 @@ std::string seg_source(const std::vector<int>& codes, int dk, int LN, bool ch, i
   sdisp2 += "else __trap();\n";
   src += disp + sdisp + sdisp2 + kLanesBodySrc + "\n" + kSegBodySrc + "\n";
   const char* names[] = {"ddsim_seg_replay", "ddsim_seg_transfer", "ddsim_seg_fused",
-                         "ddsim_seg_transfer2"};
-  const char* bodies[] = {"replay_body", "sym_body", "fused_body", "sym_body2"};
+                         "ddsim_seg_transfer2", "ddsim_seg_replay2"};
+  const char* bodies[] = {"replay_body", "sym_body", "fused_body", "sym_body2", "replay_body2"};
   src += std::string("extern \"C\" __global__ void __launch_bounds__(") + bounds + ") " + names[mode] +
          "(const __grid_constant__ ddsim_lanes::Tmap tmap, const ddsim_lanes::Params p, "
          "const ddsim_lanes::SegParams sg" +
@@ -332,13 +332,13 @@ cudaError_t launch_lanes_seg_jit(int mode, const LaneParams& p, const LaneChainP
                                  const std::vector<int>& codes, const void* segp, int gx, int gy,
                                  int BD, size_t smem, cudaStream_t stream,
                                  const LaneDerivedParams* dp) {
-  if (codes.empty() || codes.size() > 32 || LN < 1 || LN > 4 || mode < 0 || mode > 3)
+  if (codes.empty() || codes.size() > 32 || LN < 1 || LN > 4 || mode < 0 || mode > 4)
     return cudaErrorNotSupported;
   int dev = 0;
   cudaGetDevice(&dev);
-  const char* tags[] = {"seg_r:", "seg_t:", "seg_f:", "seg_t2:"};
+  const char* tags[] = {"seg_r:", "seg_t:", "seg_f:", "seg_t2:", "seg_r2:"};
   const char* names[] = {"ddsim_seg_replay", "ddsim_seg_transfer", "ddsim_seg_fused",
-                         "ddsim_seg_transfer2"};
+                         "ddsim_seg_transfer2", "ddsim_seg_replay2"};
   std::string key = std::string(tags[mode]) + std::to_string(dev) + ":" + std::to_string(dkind) +
                     ":" + std::to_string(LN) + (cp ? ":ch:" : ":");
   if (const char* u = getenv("DDSIM_SEG_UNROLL")) key += std::string("u") + u + ":";

@@ -404,7 +404,8 @@ __device__ __forceinline__ void chain_record(const Params& p, const ChainParams&
                                              long long s, bool act, bool store, long long* sp,
                                              long long ld, unsigned slot_s, unsigned slot_pitch,
                                              unsigned col, long long& ms0, long long& ms1,
-                                             int& neg, const DerivedParams* dp, const Prog& P) {
+                                             int& neg, const DerivedParams* dp, const Prog& P,
+                                             const Prog& P2) {
   const int ksm = p.ksm;
   auto slot_addr = [&](int code, int i) { return slot_s + (unsigned)code * slot_pitch + col + 8u * i; };
   const Chain ch = cp.chains[cid];
@@ -426,7 +427,7 @@ __device__ __forceinline__ void chain_record(const Params& p, const ChainParams&
     auto dur_of = [&](int k) -> long long {
       if (DK == 0) {
         const RowDur rd = dp->rows[row + k];
-        return derived_dur(dp, rd.base, rd.group, rd.ovr, sc, p.S, act, P);
+        return derived_dur(dp, rd.base, rd.group, rd.ovr, sc, p.S, act, i == 0 ? P : P2);
       } else if (act) {
         const long long at = (long long)(row + k) * p.dense_ld + sc;
         return DK == 1 ? (long long)cp.dense32[at] : p.dense64[at];
@@ -499,8 +500,6 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
                                            const SegParams* sgp = nullptr, int seg_k = 0,
                                            int blk = 0, const long long* init = nullptr,
                                            const DerivedParams* dp = nullptr) {
-  static_assert(!SEG || V == 1, "segment replay runs one scenario per thread");
-  static_assert(DK != 0 || V == 1, "derived durations: one scenario per thread");
   extern __shared__ __align__(128) unsigned char smem[];
   const int BD = blockDim.x;
   const int W = BD * V;  // scenarios per CTA
@@ -559,9 +558,11 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
   for (int l = 0; l <= NLANE; ++l)
 #pragma unroll
     for (int i = 0; i < V; ++i) S.lv[l][i] = 0;
-  if constexpr (SEG) {
+  if constexpr (SEG) {  // init: [lane][V]
 #pragma unroll
-    for (int l = 0; l < NLANE; ++l) S.lv[l][0] = init[l];
+    for (int l = 0; l < NLANE; ++l)
+#pragma unroll
+      for (int i = 0; i < V; ++i) S.lv[l][i] = init[l * V + i];
   }
 #pragma unroll
   for (int l = 0; l < NLANE; ++l)
@@ -574,9 +575,9 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
   long long* sp = store ? p.start + (long long)c_begin * kChunkL * ld + s : nullptr;
   const unsigned row_pitch = DK == 0 ? 16u : (unsigned)W * ES;
   const int ksm = p.ksm;
-  Prog P;
+  Prog P, P2;  // derived durations: the scale program of each scenario
   if (DK == 0) prog_load(dp, s, act, P);
-
+  if (DK == 0 && V == 2) prog_load(dp, s + 1, act, P2);
 
   for (int c = c_begin; c < nchunks; ++c) {
     const int st = (c - c_begin) % kStagesL;
@@ -592,8 +593,9 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
     auto load_d = [&](unsigned ta) {
       if (DK == 0) {
         const int4 rd = l_lds128(ta);
-        dq.x = derived_dur(dp, ((long long)rd.y << 32) | (unsigned)rd.x, (unsigned)rd.z, rd.w, s,
-                           p.S, act, P);
+        const long long b = ((long long)rd.y << 32) | (unsigned)rd.x;
+        dq.x = derived_dur(dp, b, (unsigned)rd.z, rd.w, s, p.S, act, P);
+        if (V == 2) dq.y = derived_dur(dp, b, (unsigned)rd.z, rd.w, s + 1, p.S, act, P2);
       } else if (DK == 1) {
         if (V == 2)
           dd = l_lds64i(ta);
@@ -631,7 +633,7 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
         if (rare & (R_CHAIN | R_NOP)) {
           if (rare & R_CHAIN)
             chain_record<DK, V>(p, *cpp, S, (int)(short)(r.z & 0xffff), c * kChunkL + j, s, act,
-                                store, sp, ld, slot_s, slot_pitch, col, ms0, ms1, neg, dp, P);
+                                store, sp, ld, slot_s, slot_pitch, col, ms0, ms1, neg, dp, P, P2);
           if (store) sp += ld;
           return;
         }
@@ -711,15 +713,22 @@ __device__ __forceinline__ void lanes_body(const Tmap* tmap, const Params& p,
       // durations + gaps stay below 2^30 (lanes_seg.cuh); the replay holds the
       // duration sums anyway (lane busy), so it certifies the transfer, and a
       // negative duration voids the fast path for both passes
-      long long wsum = sgp->gapsum[seg_k];
+      bool over = false;
 #pragma unroll
-      for (int q = 0; q < NLANE; ++q) wsum += S.lb[q][0];
-      if ((neg < 0 || (wsum >= (1LL << 30) && seg_k != sgp->kc)) && p.neg_flag)
-        atomicOr(p.neg_flag, 1);
+      for (int i = 0; i < V; ++i) {
+        long long wsum = sgp->gapsum[seg_k];
+#pragma unroll
+        for (int q = 0; q < NLANE; ++q) wsum += S.lb[q][i];
+        over |= wsum >= (1LL << 30);
+      }
+      if ((neg < 0 || (over && seg_k != sgp->kc)) && p.neg_flag) atomicOr(p.neg_flag, 1);
       if (seg_k == sgp->kc && seg_k + 1 < sgp->K)
 #pragma unroll
         for (int l = 0; l < NLANE; ++l)
-          if (l < sgp->LN) sgp->state[((long long)(seg_k + 1) * sgp->LN + l) * sgp->s_pad + s] = S.lv[l][0];
+#pragma unroll
+          for (int i = 0; i < V; ++i)
+            if (l < sgp->LN)
+              sgp->state[((long long)(seg_k + 1) * sgp->LN + l) * sgp->s_pad + s + i] = S.lv[l][i];
 #pragma unroll
       for (int i = 0; i < V; ++i) {
         const long long m = i == 0 ? ms0 : ms1;  // >= 0 on this path

@@ -511,20 +511,31 @@ __device__ __forceinline__ void sym_body(const Tmap* tmap, const Params& p, cons
   }
 }
 
-// Three-kernel path, pass 3: replay of segment blockIdx.y from seg_scan's state.
-template <int DK, int LN, bool CH>
+// Three-kernel path, pass 3: replay of segment blockIdx.y from seg_scan's
+// state; RV scenarios per thread (2: one record decode for both, S even).
+template <int DK, int LN, bool CH, int RV = 1>
 __device__ __forceinline__ void replay_body(const Tmap* tmap, const Params& p,
                                             const SegParams& sg, const ChainParams* cpp,
                                             const DerivedParams* dp) {
   const int k = sg.replay_only >= 0 ? sg.replay_only : (int)blockIdx.y;
   if (sg.replay_only < 0 && k == sg.kc) return;  // replayed before the second scan
-  long long init[NLANE] = {0, 0, 0, 0};
-  const long long s = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  long long init[NLANE * RV];
+#pragma unroll
+  for (int q = 0; q < NLANE * RV; ++q) init[q] = 0;
+  const long long s = ((long long)blockIdx.x * blockDim.x + threadIdx.x) * RV;
   if (k > 0 && s < p.S)
 #pragma unroll
     for (int l = 0; l < LN; ++l)
-      init[l] = sg.state[((long long)k * LN + l) * sg.s_pad + s];
-  lanes_body<DK, 1, CH, true>(tmap, p, cpp, &sg, k, (int)blockIdx.x, init, dp);
+#pragma unroll
+      for (int i = 0; i < RV; ++i)
+        init[l * RV + i] = sg.state[((long long)k * LN + l) * sg.s_pad + s + i];
+  lanes_body<DK, RV, CH, true>(tmap, p, cpp, &sg, k, (int)blockIdx.x, init, dp);
+}
+template <int DK, int LN, bool CH>
+__device__ __forceinline__ void replay_body2(const Tmap* tmap, const Params& p,
+                                             const SegParams& sg, const ChainParams* cpp,
+                                             const DerivedParams* dp) {
+  replay_body<DK, LN, CH, 2>(tmap, p, sg, cpp, dp);
 }
 
 // Fused single pass with decoupled look-back: CTAs take (segment, block) work

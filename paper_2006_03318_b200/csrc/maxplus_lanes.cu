@@ -561,23 +561,34 @@ cudaError_t launch_maxplus_lanes_seg(const LaneParams& p, const LaneChainParams*
   if (sg.ticket != nullptr)  // fused single pass (transfer smem >= replay smem)
     return launch_lanes_seg_jit(2, p, cp, &tmap, dkind, sg.LN, codes, &sg, gx * sg.K, 1, BD,
                                 smem_t, stream, dp);
+  // two scenarios per thread (one record decode for both): the transfer
+  // always (instruction-bound), the replay when S is even and the start rows
+  // take 16-byte stores
+  const bool two = 2 * BD <= 256 && getenv("DDSIM_SEG_T1") == nullptr;
+  const bool vec_ok = p.start == nullptr ||
+                      (p.start_ld % 2 == 0 && reinterpret_cast<uintptr_t>(p.start) % 16 == 0);
+  const bool two_r = two && p.S % 2 == 0 && vec_ok && getenv("DDSIM_SEG_R1") == nullptr;
+  CUtensorMap tmap2;
+  memset(&tmap2, 0, sizeof(tmap2));
+  if (two && dkind != 0) {
+    e = encode_lanes_tmap(&tmap2, p, dense32, dkind, 2 * BD);
+    if (e != cudaSuccess) return e;
+  }
+  const size_t base2 = 128 + (size_t)stages * ddsim_lanes::kChunkL * sizeof(ddsim_lanes::Rec) +
+                       (dkind == 0 ? (size_t)stages * ddsim_lanes::kChunkL * sizeof(ddsim_lanes::RowDur)
+                                   : (size_t)stages * ddsim_lanes::kChunkL * 2 * BD * es);
+  const int gx2 = (p.S + 2 * BD - 1) / (2 * BD);
+  const size_t smem_r2 = base2 + (size_t)p.ksm * BD * 16;
+  auto replay = [&](const LaneSegParams& q, int gy) {
+    if (two_r)
+      return launch_lanes_seg_jit(4, p, cp, &tmap2, dkind, q.LN, codes, &q, gx2, gy, BD, smem_r2,
+                                  stream, dp);
+    return launch_lanes_seg_jit(0, p, cp, &tmap, dkind, q.LN, codes, &q, gx, gy, BD, smem_r,
+                                stream, dp);
+  };
   if (sg.K > 1) {
-    // transfer: two scenarios per thread (one record decode for both; the
-    // pass is instruction-bound)
-    const bool two = 2 * BD <= 256 && getenv("DDSIM_SEG_T1") == nullptr;
     if (two) {
-      CUtensorMap tmap2;
-      memset(&tmap2, 0, sizeof(tmap2));
-      if (dkind != 0) {
-        e = encode_lanes_tmap(&tmap2, p, dense32, dkind, 2 * BD);
-        if (e != cudaSuccess) return e;
-      }
-      const size_t tiles2 = dkind == 0
-                                ? (size_t)stages * ddsim_lanes::kChunkL * sizeof(ddsim_lanes::RowDur)
-                                : (size_t)stages * ddsim_lanes::kChunkL * 2 * BD * es;
-      const size_t smem_t2 = 128 + (size_t)stages * ddsim_lanes::kChunkL * sizeof(ddsim_lanes::Rec) +
-                             tiles2 + (size_t)p.ksm * BD * 32;
-      const int gx2 = (p.S + 2 * BD - 1) / (2 * BD);
+      const size_t smem_t2 = base2 + (size_t)p.ksm * BD * 32;
       e = launch_lanes_seg_jit(3, p, cp, &tmap2, dkind, sg.LN, codes, &sg, gx2, sg.K - 1, BD,
                                smem_t2, stream, dp);
     } else {
@@ -594,14 +605,11 @@ cudaError_t launch_maxplus_lanes_seg(const LaneParams& p, const LaneChainParams*
     if ((e = launch_seg_scan(sg, p.S, 0, sg.kc, p.gslots, stream)) != cudaSuccess) return e;
     LaneSegParams one = sg;
     one.replay_only = sg.kc;
-    e = launch_lanes_seg_jit(0, p, cp, &tmap, dkind, sg.LN, codes, &one, gx, 1, BD, smem_r,
-                             stream, dp);
-    if (e != cudaSuccess) return e;
+    if ((e = replay(one, 1)) != cudaSuccess) return e;
     e = launch_seg_scan(sg, p.S, sg.kc + 1, sg.K - 1, p.gslots, stream);
     if (e != cudaSuccess) return e;
   }
-  return launch_lanes_seg_jit(0, p, cp, &tmap, dkind, sg.LN, codes, &sg, gx, sg.K, BD, smem_r,
-                              stream, dp);
+  return replay(sg, sg.K);
 }
 
 cudaError_t launch_maxplus_lanes(const LaneParams& p, const LaneChainParams* cp, const int* dense32,

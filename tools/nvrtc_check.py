@@ -67,8 +67,9 @@ def seg_source(dk: int, LN: int, ch: bool, mode: int, scale: bool) -> str:
         sdisp2 += cond + f"{{ hsym<{_hstep(c)}, LN>(Y, dv, gp); hsym<{_hstep(c)}, LN>(Y2, dv2, gp); }} "
     src += disp + "else __trap();\n" + sdisp + "else __trap();\n" + sdisp2 + "else __trap();\n"
     src += (CSRC / "lanes_body.cuh").read_text() + "\n" + (CSRC / "lanes_seg.cuh").read_text() + "\n"
-    name = ["ddsim_seg_replay", "ddsim_seg_transfer", "ddsim_seg_fused", "ddsim_seg_transfer2"][mode]
-    body = ["replay_body", "sym_body", "fused_body", "sym_body2"][mode]
+    name = ["ddsim_seg_replay", "ddsim_seg_transfer", "ddsim_seg_fused", "ddsim_seg_transfer2",
+            "ddsim_seg_replay2"][mode]
+    body = ["replay_body", "sym_body", "fused_body", "sym_body2", "replay_body2"][mode]
     args = ", const __grid_constant__ ddsim_lanes::ChainParams cp" if ch else ""
     args += ", const __grid_constant__ ddsim_lanes::DerivedParams dp" if dk == 0 else ""
     return src + (f"extern \"C\" __global__ void __launch_bounds__(256) {name}("
@@ -102,11 +103,11 @@ def variants():
                 lanes_source(dk, V, dyn, ch, nolb, scale=True)
         if dk == 0:
             yield f"lanes dk=0 V=1 ch={ch} noscale", lanes_source(0, 1, False, ch, False, False)
-    for dk, LN, ch, mode in itertools.product((0, 1, 2), (2, 3), (False, True), (0, 1, 3)):
+    for dk, LN, ch, mode in itertools.product((0, 1, 2), (2, 3), (False, True), (0, 1, 3, 4)):
         yield f"seg dk={dk} LN={LN} ch={ch} mode={mode}", seg_source(dk, LN, ch, mode, True)
     for dk in (1, 2):
         yield f"seg dk={dk} LN=4 mode=3", seg_source(dk, 4, False, 3, True)
-    for mode in (0, 3):
+    for mode in (0, 3, 4):
         yield f"seg dk=0 LN=3 ch=True mode={mode} noscale", seg_source(0, 3, True, mode, False)
 
 
