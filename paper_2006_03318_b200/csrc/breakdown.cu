@@ -29,6 +29,7 @@
 #include <algorithm>
 #include <climits>
 #include <cstdlib>
+#include <type_traits>
 
 namespace ddsim {
 
@@ -296,7 +297,9 @@ __global__ void __launch_bounds__(kBdLeanBD) breakdown_lean_kernel(const Breakdo
   const int k = blockIdx.y;
   if (s >= p.S) return;
   long long* o = p.parts + (long long)s * 4;
-  if (p.bad[s]) {
+  const int bad = p.bad[s];
+  if (p.redo && bad != 2) return;  // only the scenarios the streaming sweep handed back
+  if (bad & 1) {
     if (k == 0) o[0] = o[1] = o[2] = o[3] = -1;
     return;
   }
@@ -619,27 +622,391 @@ __global__ void __launch_bounds__(128) layer_busy4_kernel(const BreakdownParams 
   flush();
 }
 
+// ---- row-order streaming sweep ------------------------------------------------
+//
+// The windowed merge above follows each lane through time, so its next load
+// depends on which lane's event comes first: one dependent global load per
+// interval.  On a lane-chained graph without permutable chains the frozen row
+// order is a topological order in which every lane's rows appear in lane order,
+// so one thread per scenario can instead stream the rows in row order -- the
+// load addresses are data independent (batched, coalesced across the
+// scenarios of a warp, the simulate kernel's own access pattern) -- and:
+//   * grow each lane's open run: an interval that starts exactly where the
+//     lane's open run ends, with the same class, extends it (coverage counts
+//     cannot tell [a, b) + [b, c) from [a, c)); otherwise the open run is closed
+//     into a small per-lane FIFO of pending runs and a new one opens;
+//   * sweep time forward to F = min over unfinished lanes of the lane's
+//     frontier (the end of its last interval: a lane's later intervals start at
+//     or after it, start >= finish + gap, sim.py:128), merging the pending runs
+//     of all lanes in time order with the same cpu / gpu coverage counters and
+//     classification as the merge above (breakdown.py:42-97).
+// A scenario whose lanes drift apart by more than the FIFO depth in row order
+// hands itself back (bad[s] = 2) to the windowed merge, launched after the
+// sweep for those scenarios only.
+constexpr int kBsBD = 64;  // threads (scenarios) per block
+constexpr int kBsD = 4;    // FIFO capacity (pending closed runs per lane)
+constexpr int kBsU = 8;    // rows per staged batch (two batches in flight)
+constexpr int kBsMinS = 32768;  // auto mode: scenarios needed for the sweep
+constexpr long long kBsGapMax = 1LL << 50;  // gaps packed into the row code
+
+// per-row code: bits 0-5 lane, 8-9 class (0 cpu, 1 gpu, 3 not counted), bit 10
+// the lane's last row, bits 12.. the gap counted as CPU busy (0 unless the row
+// is a CPU interval and gaps_as_cpu_busy); -1: a gap too large to pack (the
+// sweep hands every scenario back)
+__global__ void bd_rowinfo_kernel(const BreakdownParams p) {
+  for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < p.n; r += gridDim.x * blockDim.x) {
+    const int l = p.row_lane[r];
+    const int rc = p.row_class[r];
+    int cls;
+    long long gap = 0;
+    if (rc == BD_CPU || rc == BD_CPU_DATALOAD) {
+      if (rc == BD_CPU_DATALOAD && !p.dataload_as_cpu) {
+        cls = 3;
+      } else {
+        cls = 0;
+        if (p.gaps_as_cpu_busy) gap = p.gap[r];
+      }
+    } else if (rc == BD_GPU) {
+      cls = 1;
+    } else {
+      cls = p.comm_as_gpu ? 1 : 0;
+    }
+    const long long last = p.lane_rows[p.lane_ptr[l + 1] - 1] == r ? 1 : 0;
+    p.rinfo[r] = gap >= kBsGapMax ? -1LL : (gap << 12) | (last << 10) | (cls << 8) | l;
+    // per_layer_breakdown key (breakdown.py:100-111): layer * 2 + is-GPU,
+    // -1 for comm rows (the reference skips comm lanes)
+    if (p.linfo) p.linfo[r] = rc == BD_COMM ? -1 : p.row_layer[r] * 2 + (rc == BD_GPU ? 1 : 0);
+  }
+}
+
+template <int DK>
+struct BsStage {
+  long long st[kBsU][kBsBD];
+  typename std::conditional<DK == 1, int, long long>::type d[kBsU][kBsBD];
+  long long info[kBsU];  // row codes, shared by the block
+  int linfo[kBsU];       // per-layer busy keys, shared by the block
+};
+template <int LM, int DK>
+struct BsSmem {
+  BsStage<DK> stage[2];
+  long long fs[LM][kBsD][kBsBD];  // pending run start
+  long long fe[LM][kBsD][kBsBD];  // pending run end * 2 + class
+};
+
+__device__ __forceinline__ void cp_async8(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src));
+}
+__device__ __forceinline__ void cp_async4(void* dst, const void* src) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4;\n" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src));
+}
+
+template <int LM, int DK, bool LB>
+__global__ void __launch_bounds__(kBsBD, 8) breakdown_stream_kernel(const BreakdownParams p) {
+  __shared__ BsSmem<LM, DK> sh;
+  const int tid = threadIdx.x;
+  const int s = blockIdx.x * kBsBD + tid;
+  const bool live = s < p.S;  // idle threads still take part in the block barriers
+  constexpr long long INF = LLONG_MAX;
+  const long long ms = live ? p.makespan[s] : 0;
+  const int depth = p.stream_depth;
+  // per-lane state in registers, always indexed by a compile-time lane (the
+  // row's lane is the same for the whole warp: a uniform switch picks it)
+  long long rs[LM], re[LM];  // open run [rs, re)
+  int rc[LM];                // open run class, -1 none
+  int hd[LM], cnt[LM];       // FIFO of closed runs not yet swept
+  bool act[LM];              // the sweep is inside the lane's head run
+  long long e[LM], fr[LM];   // next sweep event; lane frontier
+#pragma unroll
+  for (int l = 0; l < LM; ++l) {
+    rs[l] = re[l] = 0;
+    rc[l] = -1;
+    hd[l] = cnt[l] = 0;
+    act[l] = false;
+    e[l] = INF;
+    fr[l] = l < p.L && p.lane_ptr[l + 1] > p.lane_ptr[l] ? 0 : INF;
+  }
+  long long acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;  // cpu_only, gpu_only, parallel, idle
+  int cc = 0, gc = 0;
+  long long t = 0;
+
+  // one sweep event on lane q (its head run starts or ends)
+  auto handle = [&](auto qc) {
+    constexpr int q = decltype(qc)::value;
+    if (act[q]) {  // the head run ends
+      const int c = cnt[q] > 0 ? (int)(sh.fe[q][hd[q]][tid] & 1) : rc[q];
+      if (c == 0) --cc; else --gc;
+      act[q] = false;
+      if (cnt[q] > 0) {
+        hd[q] = hd[q] + 1 == kBsD ? 0 : hd[q] + 1;
+        --cnt[q];
+        e[q] = cnt[q] > 0 ? sh.fs[q][hd[q]][tid] : (rc[q] >= 0 ? rs[q] : INF);
+      } else {  // a finished lane's open run
+        rc[q] = -1;
+        e[q] = INF;
+      }
+    } else {  // it starts
+      long long b;
+      int c;
+      if (cnt[q] > 0) {
+        const long long x = sh.fe[q][hd[q]][tid];
+        b = x >> 1;
+        c = (int)(x & 1);
+      } else {
+        b = re[q];
+        c = rc[q];
+      }
+      if (c == 0) ++cc; else ++gc;
+      act[q] = true;
+      e[q] = b;
+    }
+  };
+  // merge the known runs of all lanes up to lim (events at or after lim wait)
+  auto sweep = [&](long long lim) {
+    while (true) {
+      int best = 0;
+      long long ev = e[0];
+#pragma unroll
+      for (int l = 1; l < LM; ++l)
+        if (e[l] < ev) {
+          ev = e[l];
+          best = l;
+        }
+      const long long te = min(ev, lim);
+      if (te > t) {
+        const long long span = te - t;
+        if (cc > 0 && gc > 0)
+          acc2 += span;
+        else if (cc > 0)
+          acc0 += span;
+        else if (gc > 0)
+          acc1 += span;
+        else
+          acc3 += span;
+        t = te;
+      }
+      if (ev >= lim) break;
+      switch (best) {
+        case 0: handle(std::integral_constant<int, 0>()); break;
+        case 1: if (LM > 1) handle(std::integral_constant<int, (LM > 1 ? 1 : 0)>()); break;
+        case 2: if (LM > 2) handle(std::integral_constant<int, (LM > 2 ? 2 : 0)>()); break;
+        default: if (LM > 3) handle(std::integral_constant<int, (LM > 3 ? 3 : 0)>()); break;
+      }
+    }
+  };
+  bool ovf = false;
+  // one row of lane q: grow / close / open the lane's run, move its frontier
+  auto step = [&](auto qc, long long st, long long d, long long info) {
+    constexpr int q = decltype(qc)::value;
+    if (st >= 0) {
+      const long long end = st + d + (info >> 12);
+      const int cls = (int)(info >> 8) & 3;
+      if (cls != 3 && end > st) {
+        if (rc[q] == cls && st == re[q]) {  // continues the open run
+          re[q] = end;
+          if (act[q] && cnt[q] == 0) e[q] = end;
+        } else {
+          if (rc[q] >= 0) {  // close the open run into the FIFO
+            if (cnt[q] >= depth) {
+              ovf = true;
+              return;
+            }
+            int slot = hd[q] + cnt[q];
+            if (slot >= kBsD) slot -= kBsD;
+            sh.fs[q][slot][tid] = rs[q];
+            sh.fe[q][slot][tid] = re[q] * 2 + rc[q];
+            ++cnt[q];
+          } else if (cnt[q] == 0) {  // the lane had no run: this one is its head
+            e[q] = st;
+          }
+          rs[q] = st;
+          re[q] = end;
+          rc[q] = cls;
+        }
+        fr[q] = end;
+      } else {
+        fr[q] = max(fr[q], st);
+      }
+    }
+    if ((info >> 10) & 1) fr[q] = INF;  // the lane's last row
+  };
+
+  const int n = p.n;
+  const int nb = (n + kBsU - 1) / kBsU;
+  // batch b's rows -> stage b & 1: each thread copies its own scenario's
+  // start and duration, threads 0 .. kBsU-1 the block's row codes
+  auto issue = [&](int b) {
+    BsStage<DK>& sg = sh.stage[b & 1];
+    const int r0 = b * kBsU;
+    if (live) {
+#pragma unroll
+      for (int j = 0; j < kBsU; ++j) {
+        const int r = r0 + j;
+        if (r < n) {
+          cp_async8(&sg.st[j][tid], p.start + (long long)r * p.start_ld + s);
+          if (DK == 1)
+            cp_async4(&sg.d[j][tid], static_cast<const int*>(p.dur) + (long long)r * p.dld + s);
+          else
+            cp_async8(&sg.d[j][tid], static_cast<const long long*>(p.dur) + (long long)r * p.dld + s);
+        }
+      }
+    }
+    if (tid < kBsU && r0 + tid < n) {
+      cp_async8(&sg.info[tid], p.rinfo + r0 + tid);
+      if (LB) cp_async4(&sg.linfo[tid], p.linfo + r0 + tid);
+    }
+    asm volatile("cp.async.commit_group;\n" ::);
+  };
+  long long neg = 0;  // OR of every duration (and row code): the negative check rides along
+  // per-layer busy (LB): both classes of the current layer run accumulate in
+  // registers; the thread owns its scenario's column, so a flush is a plain
+  // coalesced read-modify-write of [layer][class][S]
+  int lay = -1;
+  long long lac = 0, lag = 0;
+  auto lflush = [&]() {
+    if (lay < 0) return;
+    long long* lb = p.layer_busy + (long long)lay * 2 * p.S + s;
+    if (lac) lb[0] += lac;
+    if (lag) lb[p.S] += lag;
+  };
+  issue(0);
+  for (int b = 0; b < nb; ++b) {
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    // batch b has landed for every thread, and every thread is done with
+    // batch b - 1, whose stage the next copy overwrites
+    __syncthreads();
+    if (b + 1 < nb) issue(b + 1);
+    if (!live) continue;
+    const BsStage<DK>& sg = sh.stage[b & 1];
+    const int jn = min(kBsU, n - b * kBsU);
+    for (int j = 0; j < jn; ++j) {
+      const long long st = sg.st[j][tid];
+      const long long d = sg.d[j][tid];
+      const long long info = sg.info[j];
+      neg |= d | info;
+      if (LB) {
+        const int lk = sg.linfo[j];
+        if (lk >= 0 && st >= 0) {
+          if ((lk >> 1) != lay) {
+            lflush();
+            lay = lk >> 1;
+            lac = lag = 0;
+          }
+          if (lk & 1) lag += d; else lac += d;
+        }
+      }
+      if (ovf) continue;
+      switch ((int)info & 63) {
+        case 0: step(std::integral_constant<int, 0>(), st, d, info); break;
+        case 1: if (LM > 1) step(std::integral_constant<int, (LM > 1 ? 1 : 0)>(), st, d, info); break;
+        case 2: if (LM > 2) step(std::integral_constant<int, (LM > 2 ? 2 : 0)>(), st, d, info); break;
+        default: if (LM > 3) step(std::integral_constant<int, (LM > 3 ? 3 : 0)>(), st, d, info); break;
+      }
+      long long F = fr[0], ne = e[0];
+#pragma unroll
+      for (int q = 1; q < LM; ++q) {
+        F = min(F, fr[q]);
+        ne = min(ne, e[q]);
+      }
+      const long long lim = min(F, ms);
+      if (ne < lim) sweep(lim);
+    }
+  }
+  if (!live) return;
+  if (LB) lflush();
+  long long* o = p.parts + (long long)s * 4;
+  if (neg < 0) {
+    // a negative duration breaks the lane order (reported as -1, as the
+    // windowed merge does); an unpackable gap hands the scenario back
+    bool negdur = false;
+    for (int r = 0; r < n && !negdur; ++r) {
+      const long long d = DK == 1 ? (long long)static_cast<const int*>(p.dur)[(long long)r * p.dld + s]
+                                  : static_cast<const long long*>(p.dur)[(long long)r * p.dld + s];
+      negdur = d < 0;
+    }
+    if (negdur) {
+      p.bad[s] = 1;
+      o[0] = o[1] = o[2] = o[3] = -1;
+      return;
+    }
+    ovf = true;
+  }
+  if (ovf) {
+    p.bad[s] = 2;
+    return;
+  }
+  sweep(ms);
+  o[0] = acc0;
+  o[1] = acc1;
+  o[2] = acc2;
+  o[3] = acc3;
+}
+
 cudaError_t launch_breakdown(const BreakdownParams& p, cudaStream_t stream) {
   if (p.S <= 0) return cudaSuccess;
   if (p.L > kBdMaxLanes) return cudaErrorInvalidValue;
   const int BD = 128;
   const int grid = (p.S + BD - 1) / BD;
+  bool lb_fused = false;  // per-layer busy computed by the streaming sweep
   if (p.parts) {
     bd_zero_kernel<<<std::min(grid, 148 * 16), BD, 0, stream>>>(p);
     note_launch();
     if ((p.n + kBdNegRows - 1) / kBdNegRows > 65535) return cudaErrorInvalidValue;
-    bd_negative_kernel<<<dim3(grid, (p.n + kBdNegRows - 1) / kBdNegRows), BD, 0, stream>>>(p);
-    note_launch();
     const dim3 g2(grid, p.K);
     const bool ch = p.n_chains > 0;
     static_assert(kBdLeanBD == 128, "lean kernel block = BD");
+    // streaming sweep: lane-chained rows (no dispatch order, no permutable
+    // chains), at most 4 lanes, enough scenarios to fill the SMs with one
+    // thread each (below that the windowed merge splits time instead)
+    const bool sweep_ok = p.row_lane != nullptr && p.rinfo != nullptr && p.srows == nullptr &&
+                          p.n_chains == 0 && p.L <= 4;
+    const bool sweep = sweep_ok && (p.stream_mode > 0 || (p.stream_mode == 0 && p.S >= kBsMinS));
+    BreakdownParams q = p;
+    if (!sweep) {
+      bd_negative_kernel<<<dim3(grid, (p.n + kBdNegRows - 1) / kBdNegRows), BD, 0, stream>>>(p);
+      note_launch();
+    } else {
+      q.stream_depth = p.stream_depth <= 0 || p.stream_depth > kBsD ? kBsD : p.stream_depth;
+      const int gs = (p.S + kBsBD - 1) / kBsBD;
+      // per-layer busy rides along (durations are read once for both)
+      lb_fused = p.layer_busy != nullptr && p.row_layer != nullptr && p.linfo != nullptr;
+      if (lb_fused) {
+        cudaError_t e = launch_fill_i64(p.layer_busy, 0, (long long)p.n_layers * 2 * p.S, stream);
+        if (e != cudaSuccess) return e;
+      } else {
+        q.linfo = nullptr;
+      }
+      bd_rowinfo_kernel<<<std::min((p.n + 255) / 256, 148 * 8), 256, 0, stream>>>(q);
+      note_launch();
+#define BD_SWEEP(LM)                                                          \
+  do {                                                                        \
+    if (p.dkind == 1)                                                         \
+      lb_fused ? breakdown_stream_kernel<LM, 1, true><<<gs, kBsBD, 0, stream>>>(q)   \
+               : breakdown_stream_kernel<LM, 1, false><<<gs, kBsBD, 0, stream>>>(q); \
+    else                                                                      \
+      lb_fused ? breakdown_stream_kernel<LM, 2, true><<<gs, kBsBD, 0, stream>>>(q)   \
+               : breakdown_stream_kernel<LM, 2, false><<<gs, kBsBD, 0, stream>>>(q); \
+  } while (0)
+      switch (p.L) {
+        case 1: BD_SWEEP(1); break;
+        case 2: BD_SWEEP(2); break;
+        case 3: BD_SWEEP(3); break;
+        default: BD_SWEEP(4);
+      }
+#undef BD_SWEEP
+      note_launch();
+      q.redo = 1;  // the windowed merge below recomputes the handed-back scenarios
+    }
     if (p.L <= 8 && getenv("DDSIM_BD_OLD") == nullptr) {
 #define BD_LEAN(LM, EX)                                                      \
   do {                                                                       \
     if (ch)                                                                  \
-      breakdown_lean_kernel<LM, EX, true><<<g2, BD, 0, stream>>>(p);         \
+      breakdown_lean_kernel<LM, EX, true><<<g2, BD, 0, stream>>>(q);         \
     else                                                                     \
-      breakdown_lean_kernel<LM, EX, false><<<g2, BD, 0, stream>>>(p);        \
+      breakdown_lean_kernel<LM, EX, false><<<g2, BD, 0, stream>>>(q);        \
   } while (0)
       switch (p.L) {
         case 1: BD_LEAN(1, true); break;
@@ -676,7 +1043,7 @@ cudaError_t launch_breakdown(const BreakdownParams& p, cudaStream_t stream) {
     note_launch();
   }
 layers:
-  if (p.layer_busy && p.row_layer) {
+  if (p.layer_busy && p.row_layer && !lb_fused) {
     cudaError_t e = launch_fill_i64(p.layer_busy, 0, (long long)p.n_layers * 2 * p.S, stream);
     if (e != cudaSuccess) return e;
     if ((p.n + kLbRowChunk - 1) / kLbRowChunk > 65535) return cudaErrorInvalidValue;  // > 134M rows

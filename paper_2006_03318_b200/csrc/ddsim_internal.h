@@ -327,6 +327,15 @@ struct BreakdownParams {
   int start_may_be_neg;     // removal steps / permutable chains: start -1 marks a dropped task
   const int* srows;         // [S][n] per-scenario lane sequences (list-scheduled) or null
   int stream_loads;         // experiments: evict-first start loads (DDSIM_BD_STREAM)
+  // row-order streaming sweep (breakdown_stream_kernel): lane of every row and
+  // the per-row class / last-in-lane codes it builds; redo: the windowed merge
+  // recomputes only the scenarios the sweep handed back (bad[s] == 2)
+  const int* row_lane;      // [n] or null (streaming sweep unavailable)
+  long long* rinfo;         // [n] scratch
+  int* linfo;               // [n] scratch: per-layer busy keys (layer * 2 + is-GPU, -1 comm)
+  int stream_mode;          // 0 auto, 1 force the sweep, -1 never
+  int stream_depth;         // pending runs per lane the sweep may hold (<= kBsD)
+  int redo;
 };
 cudaError_t launch_breakdown(const BreakdownParams& p, cudaStream_t stream);
 cudaError_t launch_bd_sched_rows(const int* schedule, const int* row_lane, const int* lane_ptr,

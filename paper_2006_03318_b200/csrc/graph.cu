@@ -3197,6 +3197,15 @@ int breakdown_impl(const ks_graph* g, const ks_scenarios_desc* sc, const int64_t
     p.K = (int)std::max<long long>(1, std::min<long long>(K, 65535));
     if (const char* e = getenv("DDSIM_BD_WINDOWS")) p.K = std::max(1, atoi(e));
     p.stream_loads = getenv("DDSIM_BD_STREAM") != nullptr;
+    // row-order streaming sweep (lane-chained graphs): DDSIM_BD_SWEEP=1 forces
+    // it, =-1 disables it; DDSIM_BD_SWEEP_DEPTH caps its pending runs per lane
+    if (!sched && g->n_chains == 0 && g->L <= 4) {
+      p.row_lane = g->d_lane;
+      p.rinfo = T.scratch<long long>((size_t)g->n);
+      if (layer_busy && bd->row_layer) p.linfo = T.scratch<int>((size_t)g->n);
+    }
+    if (const char* e = getenv("DDSIM_BD_SWEEP")) p.stream_mode = atoi(e);
+    if (const char* e = getenv("DDSIM_BD_SWEEP_DEPTH")) p.stream_depth = atoi(e);
   }
   if (layer_busy && bd->row_layer) {
     p.row_layer = T.up(bd->row_layer, (size_t)g->n);

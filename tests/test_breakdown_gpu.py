@@ -25,8 +25,22 @@ from randspec import make_spec
 
 pytestmark = pytest.mark.gpu
 
+# merge kernels: auto choice, the row-order streaming sweep forced (full FIFO,
+# and a one-run FIFO that hands most scenarios back to the windowed merge),
+# and the windowed merge alone
+SWEEP_MODES = {"auto": {}, "sweep": {"DDSIM_BD_SWEEP": "1"},
+               "sweep_depth1": {"DDSIM_BD_SWEEP": "1", "DDSIM_BD_SWEEP_DEPTH": "1"},
+               "windowed": {"DDSIM_BD_SWEEP": "-1"}}
 
-def test_breakdown_matches_reference_reports(golden):
+
+@pytest.fixture(params=list(SWEEP_MODES))
+def bd_mode(request, monkeypatch):
+    for k, v in SWEEP_MODES[request.param].items():
+        monkeypatch.setenv(k, v)
+    return request.param
+
+
+def test_breakdown_matches_reference_reports(golden, bd_mode):
     n = 0
     for rec in golden["whatif"]:
         if "graph" not in rec or "error" in rec.get("sim", {}):
@@ -44,7 +58,7 @@ def test_breakdown_matches_reference_reports(golden):
 
 
 @pytest.mark.parametrize("opts", list(itertools.product([True, False], repeat=3)))
-def test_breakdown_keywords_on_random_traces(opts):
+def test_breakdown_keywords_on_random_traces(opts, bd_mode):
     comm_as_gpu, dataload_as_cpu, gaps = opts
     rng = random.Random(7)
     for i in range(12):
@@ -60,7 +74,7 @@ def test_breakdown_keywords_on_random_traces(opts):
         assert res.breakdown_of(0).to_object() == want, (i, opts)
 
 
-def test_breakdown_of_shrink_and_remove_sweep():
+def test_breakdown_of_shrink_and_remove_sweep(bd_mode):
     w = W.training_trace(n_layers=16, kernels_fwd=3, kernels_bwd=4, n_wu=20, n_streams=2,
                          sync_every=50, seed=4)
     g = w.graph
@@ -97,3 +111,34 @@ def test_breakdown_of_distributed_sweep_with_chains():
         st, ms, _lb, _ = OracleGraph.from_graph(h).simulate("default")
         assert res.makespan[s] == ms, s
         assert res.breakdown_of(s).to_object() == ora_breakdown(h.tasks, st, ms), s
+
+
+@pytest.mark.parametrize("depth", ["1", "2", "8"])
+def test_breakdown_sweep_jittered_batch(depth, monkeypatch):
+    """Many jittered scenarios of a multi-stream training trace through the
+    forced streaming sweep: every scenario's four parts equal the oracle's
+    (scenarios the sweep hands back are recomputed by the windowed merge), and
+    a scenario with one negative duration reports -1."""
+    monkeypatch.setenv("DDSIM_BD_SWEEP", "1")
+    monkeypatch.setenv("DDSIM_BD_SWEEP_DEPTH", depth)
+    w = W.training_trace(n_layers=10, kernels_fwd=3, kernels_bwd=4, n_wu=12, n_streams=3,
+                         sync_every=30, seed=5)
+    g = w.graph
+    fz = FrozenGraph.from_graph(g)
+    assert fz.chained and fz.L <= 4
+    S = 97
+    rng = np.random.default_rng(int(depth))
+    base = fz.duration[fz.order]
+    dense = ((2 * base[:, None] * rng.integers(500, 1501, (fz.n, S)) + 1000) // 2000).astype(np.int64)
+    dense[rng.integers(0, fz.n), S - 3] = -5  # negative duration: precondition fails
+    res = simulate_batch(fz, ScenarioTable(n_scenarios=S, dense=dense), breakdown=True)
+    for s in range(S):
+        if s == S - 3:
+            assert res.parts[s].tolist() == [-1, -1, -1, -1]
+            continue
+        h = g.copy()
+        for r in range(fz.n):
+            h.tasks[int(fz.row_ids[r])].duration = int(dense[r, s])
+        st, ms, _lb, _ = OracleGraph.from_graph(h).simulate("default")
+        assert res.makespan[s] == ms
+        assert res.breakdown_of(s).to_object() == ora_breakdown(h.tasks, st, ms), (s, depth)
