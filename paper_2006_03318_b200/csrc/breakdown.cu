@@ -732,6 +732,13 @@ __global__ void __launch_bounds__(kBsBD, 8) breakdown_stream_kernel(const Breakd
   long long acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;  // cpu_only, gpu_only, parallel, idle
   int cc = 0, gc = 0;
   long long t = 0;
+  // lane holding the smallest frontier: a row of any other lane leaves F (and
+  // so the sweep limit) unchanged, and its new head run starts at or after its
+  // own frontier >= F, so only rows of this lane can make a sweep due
+  int fmin = 0;
+#pragma unroll
+  for (int l = 1; l < LM; ++l)
+    if (fr[l] < fr[fmin]) fmin = l;
 
   // one sweep event on lane q (its head run starts or ends)
   auto handle = [&](auto qc) {
@@ -899,16 +906,22 @@ __global__ void __launch_bounds__(kBsBD, 8) breakdown_stream_kernel(const Breakd
         }
       }
       if (ovf) continue;
-      switch ((int)info & 63) {
+      const int l = (int)info & 63;
+      switch (l) {
         case 0: step(std::integral_constant<int, 0>(), st, d, info); break;
         case 1: if (LM > 1) step(std::integral_constant<int, (LM > 1 ? 1 : 0)>(), st, d, info); break;
         case 2: if (LM > 2) step(std::integral_constant<int, (LM > 2 ? 2 : 0)>(), st, d, info); break;
         default: if (LM > 3) step(std::integral_constant<int, (LM > 3 ? 3 : 0)>(), st, d, info); break;
       }
+      if (l != fmin) continue;
       long long F = fr[0], ne = e[0];
+      fmin = 0;
 #pragma unroll
       for (int q = 1; q < LM; ++q) {
-        F = min(F, fr[q]);
+        if (fr[q] < F) {
+          F = fr[q];
+          fmin = q;
+        }
         ne = min(ne, e[q]);
       }
       const long long lim = min(F, ms);
