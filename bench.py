@@ -188,6 +188,67 @@ def build_workload(device: int):
     return w, fz
 
 
+def measure_breakdown(w, fz, dense, start, ms, S: int, peak: float, stream,
+                      check: bool = True, calls: int = 3) -> dict:
+    """compute_breakdown + per_layer_breakdown (breakdown.py:42-111) of the
+    timed sweep's resident start matrix (ks_breakdown, after the timed region;
+    not part of `value`): device time per call with CUDA events on the
+    launching stream, algorithmic bytes 8 (start) + 4 (duration) per (task,
+    scenario), and scenario 0 checked against the breakdown oracle."""
+    import torch
+
+    from paper_2006_03318_b200.batch import ScenarioTable, breakdown_batch_device, layer_names_of
+
+    rows = fz.n
+    dev = start.device
+    names = layer_names_of(fz)
+    parts = torch.empty((S, 4), dtype=torch.int64, device=dev)
+    lbz = torch.empty((len(names), 2, S), dtype=torch.int64, device=dev)
+    table = ScenarioTable(n_scenarios=S, dense=dense[:, :S] if dense.shape[1] != S else dense)
+
+    def call():
+        breakdown_batch_device(fz, table, start=start, makespan=ms[:S], parts=parts,
+                               layer_busy=lbz, stream=stream.cuda_stream)
+
+    call()
+    stream.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(calls):
+        call()
+    b.record(stream)
+    b.synchronize()
+    sec = a.elapsed_time(b) / calls / 1e3
+    gbs = rows * S * BYTES_PER_UPDATE / sec / 1e9
+    out = {"ms_per_call": sec * 1e3, "updates_per_s": rows * S / sec, "algorithmic_GBps": gbs,
+           "frac_of_peak": gbs / peak, "calls": calls, "layers": len(names),
+           "kernel": "breakdown_stream_kernel (row-order sweep)"
+           if S >= 32768 and fz.L <= 4 and fz.chained else "breakdown_lean_kernel (windowed merge)",
+           "outputs": "parts [S][4] + per-layer busy [layers][2][S]"}
+    if check:
+        sys.path.insert(0, str(ROOT / "oracle"))
+        from breakdown_oracle import breakdown as ora  # checker only
+        s = 0
+        col = start[:, s].cpu().numpy()
+        d = dense[:, s].cpu().numpy().astype(np.int64)
+        g = w.graph.copy()
+        for r in range(rows):
+            g.tasks[int(fz.row_ids[r])].duration = int(d[r])
+        st_of = {int(fz.row_ids[r]): int(col[r]) for r in range(rows)}
+        want = ora(g.tasks, st_of, int(ms[s].item()))
+        got_parts = parts[s].tolist()
+        assert got_parts == [want["cpu_only_ns"], want["gpu_only_ns"], want["parallel_ns"],
+                             want["idle_ns"]], (got_parts, want)
+        lb = lbz[:, :, s].cpu().numpy()
+        for k, name in enumerate(names):
+            if name in want["per_layer"]:
+                pl = want["per_layer"][name]
+                assert [int(lb[k, 0]), int(lb[k, 1])] == [pl["cpu_ns"], pl["gpu_ns"]], name
+        out["parity_checked"] = {"scenarios": [s], "checker": "oracle/breakdown_oracle.py "
+                                 "(breakdown.py:42-111): four parts + every layer"}
+    return out
+
+
 def cpu_baseline(w, fz, target_s: float = 12.0) -> dict:
     """The reference algorithm (C port of Alg. 1) on the host cores, on a
     bounded sample of the same workload (scenarios of the same jitter law)."""
@@ -482,6 +543,9 @@ def run_ours(args):
         _release_registered(registered)
         os.sched_setaffinity(0, all_cpus)  # the CPU baseline uses every core
 
+    bd = None
+    if not args.no_breakdown:
+        bd = measure_breakdown(w, fz, dense, start, ms, S, peak, stream, check=rank == 0)
     cb = None
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         cb = cpu_baseline(w, fz)
@@ -523,6 +587,7 @@ def run_ours(args):
             "result_gather": gather,
             "kernel": kernel_name,
             "clocks": clk,
+            "breakdown": bd,
         }
         print(json.dumps(line), flush=True)
     if ws > 1:
@@ -1122,6 +1187,7 @@ def main():
     ap.add_argument("--scenarios", type=int, default=S_PER_GPU)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-breakdown", action="store_true")
     ap.add_argument("--ingest-records", type=int, default=10_000_000)
     ap.add_argument("--config", type=int, default=4, choices=[1, 2, 3, 4, 5],
                     help="BASELINE.json configs[N-1]; 4 (default) is the headline jitter sweep")
