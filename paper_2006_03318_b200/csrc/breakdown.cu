@@ -868,16 +868,15 @@ __global__ void __launch_bounds__(kBsBD, 8) breakdown_stream_kernel(const Breakd
     asm volatile("cp.async.commit_group;\n" ::);
   };
   long long neg = 0;  // OR of every duration (and row code): the negative check rides along
-  // per-layer busy (LB): both classes of the current layer run accumulate in
-  // registers; the thread owns its scenario's column, so a flush is a plain
-  // coalesced read-modify-write of [layer][class][S]
-  int lay = -1;
-  long long lac = 0, lag = 0;
-  auto lflush = [&]() {
-    if (lay < 0) return;
-    long long* lb = p.layer_busy + (long long)lay * 2 * p.S + s;
-    if (lac) lb[0] += lac;
-    if (lag) lb[p.S] += lag;
+  // per-layer busy (LB): each class keeps its own current layer run in
+  // registers (the CPU thread launches layers ahead of the streams running
+  // them, so in row order the two classes sit in different layers); the thread
+  // owns its scenario's column, so a flush is a plain coalesced
+  // read-modify-write of [layer][class][S]
+  int lay[2] = {-1, -1};
+  long long lacc[2] = {0, 0};
+  auto lflush = [&](int c) {
+    if (lay[c] >= 0 && lacc[c]) p.layer_busy[((long long)lay[c] * 2 + c) * p.S + s] += lacc[c];
   };
   issue(0);
   for (int b = 0; b < nb; ++b) {
@@ -897,12 +896,17 @@ __global__ void __launch_bounds__(kBsBD, 8) breakdown_stream_kernel(const Breakd
       if (LB) {
         const int lk = sg.linfo[j];
         if (lk >= 0 && st >= 0) {
-          if ((lk >> 1) != lay) {
-            lflush();
-            lay = lk >> 1;
-            lac = lag = 0;
-          }
-          if (lk & 1) lag += d; else lac += d;
+          const int c = lk & 1;
+#pragma unroll
+          for (int q = 0; q < 2; ++q)  // static indices keep both runs in registers
+            if (q == c) {
+              if ((lk >> 1) != lay[q]) {
+                lflush(q);
+                lay[q] = lk >> 1;
+                lacc[q] = 0;
+              }
+              lacc[q] += d;
+            }
         }
       }
       if (ovf) continue;
@@ -929,7 +933,10 @@ __global__ void __launch_bounds__(kBsBD, 8) breakdown_stream_kernel(const Breakd
     }
   }
   if (!live) return;
-  if (LB) lflush();
+  if (LB) {
+    lflush(0);
+    lflush(1);
+  }
   long long* o = p.parts + (long long)s * 4;
   if (neg < 0) {
     // a negative duration breaks the lane order (reported as -1, as the
