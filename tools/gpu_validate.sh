@@ -1,6 +1,6 @@
 #!/bin/bash
 # round-2 final validation: GPU suite, smoke, bench for every config, reference arms,
-# launch lists of the small configs (ncu, cold per-launch times)
+# launch lists of the small configs (ncu, cold per-launch times), ncu of the breakdown sweep
 mkdir -p gpurun_out
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm --format=csv > gpurun_out/final_smi.txt
 timeout 1800 python -m pytest tests -m gpu -q > gpurun_out/final_tests.log 2>&1; tail -2 gpurun_out/final_tests.log
@@ -9,7 +9,8 @@ timeout 900 python bench.py > gpurun_out/final_c4.jsonl 2> gpurun_out/final_c4.e
 for c in 1 2 3 5; do timeout 1200 python bench.py --config $c > gpurun_out/final_c$c.jsonl 2> gpurun_out/final_c$c.err; echo "config $c rc=$?"; done
 timeout 600 python bench.py --impl reference > gpurun_out/final_ref_c4.jsonl 2>&1
 for c in 1 2 3 5; do timeout 900 python bench.py --impl reference --config $c > gpurun_out/final_ref_c$c.jsonl 2>&1; done
-for c in 1 2 3; do timeout 300 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/final_launches_c$c.csv python bench.py --config $c --steps 2 --warmup 3 --no-e2e --no-cpu-baseline > /dev/null 2>&1; done
+timeout 900 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum --clock-control none -k regex:"breakdown|bd_" --csv --log-file gpurun_out/final_bd_launches.csv python tools/bench_breakdown.py > /dev/null 2>&1
+timeout 900 ncu --set full --import-source on -k regex:breakdown_stream -c 1 -o gpurun_out/final_bd_stream python tools/bench_breakdown.py > gpurun_out/final_bd_ncu.log 2>&1
 python - <<'PY'
 import json
 for c in (4, 1, 2, 3, 5):
