@@ -487,7 +487,9 @@ template <bool NEG>
 __global__ void __launch_bounds__(128) layer_busy_kernel(const BreakdownParams p) {
   const int s = blockIdx.x * blockDim.x + threadIdx.x;
   if (s >= p.S) return;
-  int lay = -1;  // layer of the current run
+  // one layer run per class: the CPU thread launches layers ahead of the
+  // streams running them, so in row order the two classes sit in different layers
+  int lay_c = -1, lay_g = -1;
   long long acc_c = 0, acc_g = 0;
   constexpr int U = 8;  // rows in flight per thread
   const int rbeg = blockIdx.y * kLbRowChunk;
@@ -515,24 +517,25 @@ __global__ void __launch_bounds__(128) layer_busy_kernel(const BreakdownParams p
 #pragma unroll
     for (int j = 0; j < U; ++j) {
       if (ly[j] < 0 || (NEG && st[j] < 0)) continue;
-      if (ly[j] != lay) {
-        if (lay >= 0) {
-          lb_flush(p, lay * 2, acc_c, s);
-          lb_flush(p, lay * 2 + 1, acc_g, s);
+      if (gpu[j]) {
+        if (ly[j] != lay_g) {
+          if (lay_g >= 0) lb_flush(p, lay_g * 2 + 1, acc_g, s);
+          lay_g = ly[j];
+          acc_g = 0;
         }
-        lay = ly[j];
-        acc_c = acc_g = 0;
-      }
-      if (gpu[j])
         acc_g += d[j];
-      else
+      } else {
+        if (ly[j] != lay_c) {
+          if (lay_c >= 0) lb_flush(p, lay_c * 2, acc_c, s);
+          lay_c = ly[j];
+          acc_c = 0;
+        }
         acc_c += d[j];
+      }
     }
   }
-  if (lay >= 0) {
-    lb_flush(p, lay * 2, acc_c, s);
-    lb_flush(p, lay * 2 + 1, acc_g, s);
-  }
+  if (lay_c >= 0) lb_flush(p, lay_c * 2, acc_c, s);
+  if (lay_g >= 0) lb_flush(p, lay_g * 2 + 1, acc_g, s);
 }
 
 // Dispatch order [S][n] -> per-scenario lane sequences srows[s][lane_ptr[l] + k]
@@ -569,20 +572,17 @@ cudaError_t launch_bd_sched_rows(const int* schedule, const int* row_lane, const
 __global__ void __launch_bounds__(128) layer_busy4_kernel(const BreakdownParams p) {
   const int s = (blockIdx.x * blockDim.x + threadIdx.x) * 4;
   if (s >= p.S) return;
-  int lay = -1;
+  int lay_c = -1, lay_g = -1;  // one layer run per class (as layer_busy_kernel)
   long long ac[4] = {0, 0, 0, 0}, ag[4] = {0, 0, 0, 0};
   constexpr int U = 8;
   const int rbeg = blockIdx.y * kLbRowChunk;
   const int rend = min(p.n, rbeg + kLbRowChunk);
   const int* dur = static_cast<const int*>(p.dur);
-  auto flush = [&]() {
+  auto flush = [&](int lay, int c, const long long* a) {
     if (lay < 0) return;
 #pragma unroll
     for (int i = 0; i < 4; ++i)
-      if (s + i < p.S) {
-        lb_flush(p, lay * 2, ac[i], s + i);
-        lb_flush(p, lay * 2 + 1, ag[i], s + i);
-      }
+      if (s + i < p.S) lb_flush(p, lay * 2 + c, a[i], s + i);
   };
   for (int r0 = rbeg; r0 < rend; r0 += U) {
     int4 d[U];
@@ -605,21 +605,30 @@ __global__ void __launch_bounds__(128) layer_busy4_kernel(const BreakdownParams 
 #pragma unroll
     for (int j = 0; j < U; ++j) {
       if (ly[j] < 0) continue;
-      if (ly[j] != lay) {
-        flush();
-        lay = ly[j];
-#pragma unroll
-        for (int i = 0; i < 4; ++i) ac[i] = ag[i] = 0;
-      }
       const long long v[4] = {d[j].x, d[j].y, d[j].z, d[j].w};
+      if (gpu[j]) {
+        if (ly[j] != lay_g) {
+          flush(lay_g, 1, ag);
+          lay_g = ly[j];
 #pragma unroll
-      for (int i = 0; i < 4; ++i) {
-        if (gpu[j]) ag[i] += v[i];
-        else ac[i] += v[i];
+          for (int i = 0; i < 4; ++i) ag[i] = 0;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) ag[i] += v[i];
+      } else {
+        if (ly[j] != lay_c) {
+          flush(lay_c, 0, ac);
+          lay_c = ly[j];
+#pragma unroll
+          for (int i = 0; i < 4; ++i) ac[i] = 0;
+        }
+#pragma unroll
+        for (int i = 0; i < 4; ++i) ac[i] += v[i];
       }
     }
   }
-  flush();
+  flush(lay_c, 0, ac);
+  flush(lay_g, 1, ag);
 }
 
 // ---- row-order streaming sweep ------------------------------------------------
