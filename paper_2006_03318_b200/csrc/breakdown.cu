@@ -745,9 +745,15 @@ __global__ void __launch_bounds__(kBsBD, 8) breakdown_stream_kernel(const Breakd
   // so the sweep limit) unchanged, and its new head run starts at or after its
   // own frontier >= F, so only rows of this lane can make a sweep due
   int fmin = 0;
+  {
+    long long f0 = fr[0];
 #pragma unroll
-  for (int l = 1; l < LM; ++l)
-    if (fr[l] < fr[fmin]) fmin = l;
+    for (int l = 1; l < LM; ++l)
+      if (fr[l] < f0) {
+        f0 = fr[l];
+        fmin = l;
+      }
+  }
 
   // one sweep event on lane q (its head run starts or ends)
   auto handle = [&](auto qc) {
@@ -854,21 +860,36 @@ __global__ void __launch_bounds__(kBsBD, 8) breakdown_stream_kernel(const Breakd
   const int nb = (n + kBsU - 1) / kBsU;
   // batch b's rows -> stage b & 1: each thread copies its own scenario's
   // start and duration, threads 0 .. kBsU-1 the block's row codes
+  // the thread's start / duration pointers advance by one batch of rows per
+  // issue (strides held in registers: no per-row 64-bit address products)
+  using DT = typename std::conditional<DK == 1, int, long long>::type;
+  const long long sld = p.start_ld, dld = p.dld;
+  const long long* sp = p.start + (live ? s : 0);
+  const DT* dp = static_cast<const DT*>(p.dur) + (live ? s : 0);
   auto issue = [&](int b) {
     BsStage<DK>& sg = sh.stage[b & 1];
     const int r0 = b * kBsU;
     if (live) {
+      const long long* a = sp;
+      const DT* q = dp;
+      if (r0 + kBsU <= n) {
 #pragma unroll
-      for (int j = 0; j < kBsU; ++j) {
-        const int r = r0 + j;
-        if (r < n) {
-          cp_async8(&sg.st[j][tid], p.start + (long long)r * p.start_ld + s);
-          if (DK == 1)
-            cp_async4(&sg.d[j][tid], static_cast<const int*>(p.dur) + (long long)r * p.dld + s);
-          else
-            cp_async8(&sg.d[j][tid], static_cast<const long long*>(p.dur) + (long long)r * p.dld + s);
+        for (int j = 0; j < kBsU; ++j) {
+          cp_async8(&sg.st[j][tid], a);
+          if (DK == 1) cp_async4(&sg.d[j][tid], q); else cp_async8(&sg.d[j][tid], q);
+          a += sld;
+          q += dld;
+        }
+      } else {
+        for (int j = 0; r0 + j < n; ++j) {
+          cp_async8(&sg.st[j][tid], a);
+          if (DK == 1) cp_async4(&sg.d[j][tid], q); else cp_async8(&sg.d[j][tid], q);
+          a += sld;
+          q += dld;
         }
       }
+      sp += sld * kBsU;
+      dp += dld * kBsU;
     }
     if (tid < kBsU && r0 + tid < n) {
       cp_async8(&sg.info[tid], p.rinfo + r0 + tid);
