@@ -223,7 +223,7 @@ def measure_breakdown(w, fz, dense, start, ms, S: int, peak: float, stream,
     out = {"ms_per_call": sec * 1e3, "updates_per_s": rows * S / sec, "algorithmic_GBps": gbs,
            "frac_of_peak": gbs / peak, "calls": calls, "layers": len(names),
            "kernel": "breakdown_stream_kernel (row-order sweep)"
-           if S >= 32768 and fz.L <= 4 and fz.chained else "breakdown_lean_kernel (windowed merge)",
+           if S >= 22528 and fz.L <= 4 and fz.chained else "breakdown_lean_kernel (windowed merge)",
            "outputs": "parts [S][4] + per-layer busy [layers][2][S]"}
     if check:
         sys.path.insert(0, str(ROOT / "oracle"))

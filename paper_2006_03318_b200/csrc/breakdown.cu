@@ -655,7 +655,10 @@ __global__ void __launch_bounds__(128) layer_busy4_kernel(const BreakdownParams 
 constexpr int kBsBD = 64;  // threads (scenarios) per block
 constexpr int kBsD = 4;    // FIFO capacity (pending closed runs per lane)
 constexpr int kBsU = 8;    // rows per staged batch (two batches in flight)
-constexpr int kBsMinS = 32768;  // auto mode: scenarios needed for the sweep
+// auto mode: scenarios needed for the sweep.  Below one wave the sweep is
+// latency-bound at ~21 ms per 100k rows whatever S (one thread per scenario),
+// while the windowed merge scales with S (19.3 ms at 16,384, 36.7 at 32,768)
+constexpr int kBsMinS = 22528;
 constexpr long long kBsGapMax = 1LL << 50;  // gaps packed into the row code
 
 // per-row code: bits 0-5 lane, 8-9 class (0 cpu, 1 gpu, 3 not counted), bit 10
