@@ -113,9 +113,10 @@ def test_breakdown_of_distributed_sweep_with_chains():
         assert res.breakdown_of(s).to_object() == ora_breakdown(h.tasks, st, ms), s
 
 
+@pytest.mark.parametrize("dtype", [np.int32, np.int64])
 @pytest.mark.parametrize("depth", ["1", "2", "8"])
-def test_breakdown_sweep_jittered_batch(depth, monkeypatch):
-    """Many jittered scenarios of a multi-stream training trace through the
+def test_breakdown_sweep_jittered_batch(depth, dtype, monkeypatch):
+    """100 jittered scenarios (int32 and int64 tables) of a multi-stream training trace through the
     forced streaming sweep: every scenario's four parts equal the oracle's
     (scenarios the sweep hands back are recomputed by the windowed merge), and
     a scenario with one negative duration reports -1."""
@@ -126,10 +127,10 @@ def test_breakdown_sweep_jittered_batch(depth, monkeypatch):
     g = w.graph
     fz = FrozenGraph.from_graph(g)
     assert fz.chained and fz.L <= 4
-    S = 97
+    S = 100  # int32 tables need dense_ld % 4 == 0
     rng = np.random.default_rng(int(depth))
     base = fz.duration[fz.order]
-    dense = ((2 * base[:, None] * rng.integers(500, 1501, (fz.n, S)) + 1000) // 2000).astype(np.int64)
+    dense = ((2 * base[:, None] * rng.integers(500, 1501, (fz.n, S)) + 1000) // 2000).astype(dtype)
     dense[rng.integers(0, fz.n), S - 3] = -5  # negative duration: precondition fails
     res = simulate_batch(fz, ScenarioTable(n_scenarios=S, dense=dense), breakdown=True)
     for s in range(S):
@@ -141,4 +142,4 @@ def test_breakdown_sweep_jittered_batch(depth, monkeypatch):
             h.tasks[int(fz.row_ids[r])].duration = int(dense[r, s])
         st, ms, _lb, _ = OracleGraph.from_graph(h).simulate("default")
         assert res.makespan[s] == ms
-        assert res.breakdown_of(s).to_object() == ora_breakdown(h.tasks, st, ms), (s, depth)
+        assert res.breakdown_of(s).to_object() == ora_breakdown(h.tasks, st, ms), (s, depth, dtype)
