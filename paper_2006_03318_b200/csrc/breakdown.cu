@@ -476,7 +476,17 @@ __device__ __forceinline__ void lb_flush(const BreakdownParams& p, int key, long
     atomicAdd(reinterpret_cast<unsigned long long*>(p.layer_busy + (long long)key * p.S + s),
               (unsigned long long)acc);
 }
-constexpr int kLbRowChunk = 2048;  // rows per block row (blockIdx.y)
+constexpr int kLbRowChunk = 2048;  // rows per block row (blockIdx.y), at most
+// fewer rows per chunk when there are few scenarios: one thread walks a chunk
+// of one scenario, so a single-scenario table (the drop-in Analysis.whatif)
+// needs many short chunks to get past one thread's dependent walk
+inline int lb_row_chunk(int n, int S) {
+  const long long chunks = (148LL * 1024 + S - 1) / S;
+  long long c = std::max<long long>(64, (n + chunks - 1) / chunks);
+  c = std::min<long long>(c, kLbRowChunk);
+  c = std::max<long long>(c, (n + 65534) / 65535);  // grid y limit
+  return (int)c;
+}
 
 // NEG: start rows may hold -1 (dropped tasks) and must be read; otherwise
 // only the durations are (a third of the bytes). A layer's CPU launches and GPU
@@ -492,8 +502,8 @@ __global__ void __launch_bounds__(128) layer_busy_kernel(const BreakdownParams p
   int lay_c = -1, lay_g = -1;
   long long acc_c = 0, acc_g = 0;
   constexpr int U = 8;  // rows in flight per thread
-  const int rbeg = blockIdx.y * kLbRowChunk;
-  const int rend = min(p.n, rbeg + kLbRowChunk);
+  const int rbeg = blockIdx.y * p.lb_chunk;
+  const int rend = min(p.n, rbeg + p.lb_chunk);
   for (int r0 = rbeg; r0 < rend; r0 += U) {
     long long st[U], d[U];
     int ly[U], gpu[U];
@@ -575,8 +585,8 @@ __global__ void __launch_bounds__(128) layer_busy4_kernel(const BreakdownParams 
   int lay_c = -1, lay_g = -1;  // one layer run per class (as layer_busy_kernel)
   long long ac[4] = {0, 0, 0, 0}, ag[4] = {0, 0, 0, 0};
   constexpr int U = 8;
-  const int rbeg = blockIdx.y * kLbRowChunk;
-  const int rend = min(p.n, rbeg + kLbRowChunk);
+  const int rbeg = blockIdx.y * p.lb_chunk;
+  const int rend = min(p.n, rbeg + p.lb_chunk);
   const int* dur = static_cast<const int*>(p.dur);
   auto flush = [&](int lay, int c, const long long* a) {
     if (lay < 0) return;
@@ -1099,18 +1109,20 @@ layers:
   if (p.layer_busy && p.row_layer && !lb_fused) {
     cudaError_t e = launch_fill_i64(p.layer_busy, 0, (long long)p.n_layers * 2 * p.S, stream);
     if (e != cudaSuccess) return e;
-    if ((p.n + kLbRowChunk - 1) / kLbRowChunk > 65535) return cudaErrorInvalidValue;  // > 134M rows
-    const dim3 g3(grid, (p.n + kLbRowChunk - 1) / kLbRowChunk);
+    BreakdownParams pl = p;
+    pl.lb_chunk = lb_row_chunk(p.n, p.S);
+    if ((p.n + pl.lb_chunk - 1) / pl.lb_chunk > 65535) return cudaErrorInvalidValue;
+    const dim3 g3(grid, (p.n + pl.lb_chunk - 1) / pl.lb_chunk);
     const bool vec4 = !p.start_may_be_neg && p.dkind == 1 && p.dld % 4 == 0 &&
                       reinterpret_cast<uintptr_t>(p.dur) % 16 == 0 &&
                       getenv("DDSIM_BD_LB_SCALAR") == nullptr;
     if (vec4) {
       const int g4 = ((p.S + 3) / 4 + BD - 1) / BD;
-      layer_busy4_kernel<<<dim3(g4, g3.y), BD, 0, stream>>>(p);
+      layer_busy4_kernel<<<dim3(g4, g3.y), BD, 0, stream>>>(pl);
     } else if (p.start_may_be_neg)
-      layer_busy_kernel<true><<<g3, BD, 0, stream>>>(p);
+      layer_busy_kernel<true><<<g3, BD, 0, stream>>>(pl);
     else
-      layer_busy_kernel<false><<<g3, BD, 0, stream>>>(p);
+      layer_busy_kernel<false><<<g3, BD, 0, stream>>>(pl);
     note_launch();
   }
   return cudaGetLastError();

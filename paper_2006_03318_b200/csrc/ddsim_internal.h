@@ -324,6 +324,7 @@ struct BreakdownParams {
   const int* row_layer;     // [n] or null
   long long* layer_busy;
   int n_layers;
+  int lb_chunk;             // rows per per-layer busy block row (set by launch_breakdown)
   int start_may_be_neg;     // removal steps / permutable chains: start -1 marks a dropped task
   const int* srows;         // [S][n] per-scenario lane sequences (list-scheduled) or null
   int stream_loads;         // experiments: evict-first start loads (DDSIM_BD_STREAM)
