@@ -272,6 +272,28 @@ __global__ void __launch_bounds__(128) breakdown_kernel(const BreakdownParams p)
   if (acc3) atomicAdd(u + 3, (unsigned long long)acc3);
 }
 
+// Class of a row's interval under the call's options (0 cpu, 1 gpu, 3 not
+// counted) and the gap it carries as CPU busy: one 8-byte row code when the
+// row codes were built (bd_rowinfo_kernel), else from row_class / gap
+__device__ __forceinline__ int bd_class(const BreakdownParams& p, int row, long long& gapx) {
+  if (p.rinfo) {
+    const long long info = __ldg(&p.rinfo[row]);
+    if (info >= 0) {
+      gapx = info >> 12;
+      return (int)(info >> 8) & 3;
+    }
+  }
+  const int rc = __ldg(&p.row_class[row]);
+  gapx = 0;
+  if (rc == BD_CPU || rc == BD_CPU_DATALOAD) {
+    if (rc == BD_CPU_DATALOAD && !p.dataload_as_cpu) return 3;
+    if (p.gaps_as_cpu_busy) gapx = __ldg(&p.gap[row]);
+    return 0;
+  }
+  if (rc == BD_GPU) return 1;
+  return p.comm_as_gpu ? 1 : 0;
+}
+
 // Lean merge (L <= 8): the per-lane cursor state lives in shared memory
 // (structure of arrays, [lane][thread]) so an event touches its lane through a
 // dynamic index -- one copy of the advance code per event instead of LM
@@ -346,18 +368,10 @@ __global__ void __launch_bounds__(kBdLeanBD) breakdown_lean_kernel(const Breakdo
         }
       prefetch(l);
       if (st < 0) continue;  // removed task / absent chain member (start -1)
-      const int rc = __ldg(&p.row_class[row]);
-      long long end = st + d;
-      int cls;
-      if (rc == BD_CPU || rc == BD_CPU_DATALOAD) {
-        if (rc == BD_CPU_DATALOAD && !p.dataload_as_cpu) continue;
-        if (p.gaps_as_cpu_busy) end += __ldg(&p.gap[row]);
-        cls = 0;
-      } else if (rc == BD_GPU) {
-        cls = 1;
-      } else {
-        cls = p.comm_as_gpu ? 1 : 0;
-      }
+      long long gapx;
+      const int cls = bd_class(p, row, gapx);
+      if (cls == 3) continue;
+      long long end = st + d + gapx;
       if (end <= st) continue;
       // absorb the lane's following intervals while they continue this one
       // back to back with the same class ([a, b) + [b, c) = [a, c) for the
@@ -374,18 +388,9 @@ __global__ void __launch_bounds__(kBdLeanBD) breakdown_lean_kernel(const Breakdo
             nd = pd[q];
           }
         if (nst != end) break;
-        const int rc2 = __ldg(&p.row_class[nr]);
-        long long end2 = nst + nd;
-        int cls2;
-        if (rc2 == BD_CPU || rc2 == BD_CPU_DATALOAD) {
-          if (rc2 == BD_CPU_DATALOAD && !p.dataload_as_cpu) break;
-          if (p.gaps_as_cpu_busy) end2 += __ldg(&p.gap[nr]);
-          cls2 = 0;
-        } else if (rc2 == BD_GPU) {
-          cls2 = 1;
-        } else {
-          cls2 = p.comm_as_gpu ? 1 : 0;
-        }
+        long long gap2;
+        const int cls2 = bd_class(p, nr, gap2);
+        const long long end2 = nst + nd + gap2;
         if (cls2 != cls || end2 < end) break;
         end = end2;
         prefetch(l);
@@ -677,7 +682,7 @@ constexpr long long kBsGapMax = 1LL << 50;  // gaps packed into the row code
 // sweep hands every scenario back)
 __global__ void bd_rowinfo_kernel(const BreakdownParams p) {
   for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < p.n; r += gridDim.x * blockDim.x) {
-    const int l = p.row_lane[r];
+    const int l = p.row_lane ? p.row_lane[r] : 0;
     const int rc = p.row_class[r];
     int cls;
     long long gap = 0;
@@ -693,7 +698,7 @@ __global__ void bd_rowinfo_kernel(const BreakdownParams p) {
     } else {
       cls = p.comm_as_gpu ? 1 : 0;
     }
-    const long long last = p.lane_rows[p.lane_ptr[l + 1] - 1] == r ? 1 : 0;
+    const long long last = p.lane_rows && p.lane_rows[p.lane_ptr[l + 1] - 1] == r ? 1 : 0;
     p.rinfo[r] = gap >= kBsGapMax ? -1LL : (gap << 12) | (last << 10) | (cls << 8) | l;
     // per_layer_breakdown key (breakdown.py:100-111): layer * 2 + is-GPU,
     // -1 for comm rows (the reference skips comm lanes)
@@ -1028,6 +1033,10 @@ cudaError_t launch_breakdown(const BreakdownParams& p, cudaStream_t stream) {
                           p.n_chains == 0 && p.L <= 4;
     const bool sweep = sweep_ok && (p.stream_mode > 0 || (p.stream_mode == 0 && p.S >= kBsMinS));
     BreakdownParams q = p;
+    if (p.rinfo) {  // packed per-row class / gap codes (both merges read them)
+      bd_rowinfo_kernel<<<std::min((p.n + 255) / 256, 148 * 8), 256, 0, stream>>>(q);
+      note_launch();
+    }
     if (!sweep) {
       bd_negative_kernel<<<dim3(grid, (p.n + kBdNegRows - 1) / kBdNegRows), BD, 0, stream>>>(p);
       note_launch();
@@ -1042,8 +1051,6 @@ cudaError_t launch_breakdown(const BreakdownParams& p, cudaStream_t stream) {
       } else {
         q.linfo = nullptr;
       }
-      bd_rowinfo_kernel<<<std::min((p.n + 255) / 256, 148 * 8), 256, 0, stream>>>(q);
-      note_launch();
 #define BD_SWEEP(LM)                                                          \
   do {                                                                        \
     if (p.dkind == 1)                                                         \

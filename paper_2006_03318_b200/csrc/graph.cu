@@ -3202,9 +3202,11 @@ int breakdown_impl(const ks_graph* g, const ks_scenarios_desc* sc, const int64_t
     p.stream_loads = getenv("DDSIM_BD_STREAM") != nullptr;
     // row-order streaming sweep (lane-chained graphs): DDSIM_BD_SWEEP=1 forces
     // it, =-1 disables it; DDSIM_BD_SWEEP_DEPTH caps its pending runs per lane
+    // packed per-row class / gap codes for both merges; the sweep also needs
+    // the row lanes (lane-chained rows, no permutable chains, <= 4 lanes)
+    p.rinfo = T.scratch<long long>((size_t)g->n);
     if (!sched && g->n_chains == 0 && g->L <= 4) {
       p.row_lane = g->d_lane;
-      p.rinfo = T.scratch<long long>((size_t)g->n);
       if (layer_busy && bd->row_layer) p.linfo = T.scratch<int>((size_t)g->n);
     }
     if (const char* e = getenv("DDSIM_BD_SWEEP")) p.stream_mode = atoi(e);
