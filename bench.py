@@ -688,6 +688,54 @@ def _table_bytes(table) -> int:
     return n
 
 
+def _config_breakdown(fz, table, graph_of, start, ms, stream, calls: int = 5) -> dict:
+    """The sweep's what-if reports (compute_breakdown + per_layer_breakdown,
+    breakdown.py:42-111) from its resident starts through ks_breakdown, after
+    the timed region: CUDA-event time per call and scenario 0 checked against
+    the breakdown oracle on the reference-equivalent transformed graph."""
+    import torch
+
+    from paper_2006_03318_b200.batch import breakdown_batch_device, layer_names_of
+
+    S = table.n_scenarios
+    names = layer_names_of(fz)
+    parts = torch.empty((S, 4), dtype=torch.int64, device=start.device)
+    lbz = torch.empty((len(names), 2, S), dtype=torch.int64, device=start.device)
+
+    def call():
+        breakdown_batch_device(fz, table, start=start, makespan=ms, parts=parts, layer_busy=lbz,
+                               stream=stream.cuda_stream)
+
+    call()
+    stream.synchronize()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    a.record(stream)
+    for _ in range(calls):
+        call()
+    b.record(stream)
+    b.synchronize()
+    sec = a.elapsed_time(b) / calls / 1e3
+    sys.path.insert(0, str(ROOT / "oracle"))
+    from breakdown_oracle import breakdown as ora  # checker only
+    s = 0
+    col = start[:, s].cpu().numpy()
+    st_of = {int(t): int(v) for t, v in zip(fz.row_ids.tolist(), col.tolist()) if v >= 0}
+    g = graph_of(s)
+    want = ora(g.tasks, st_of, int(ms[s].item()))
+    got = parts[s].tolist()
+    assert got == [want["cpu_only_ns"], want["gpu_only_ns"], want["parallel_ns"], want["idle_ns"]], \
+        (got, want)
+    lb = lbz[:, :, s].cpu().numpy()
+    for k, name in enumerate(names):
+        if name in want["per_layer"]:
+            pl = want["per_layer"][name]
+            assert [int(lb[k, 0]), int(lb[k, 1])] == [pl["cpu_ns"], pl["gpu_ns"]], name
+    return {"ms_per_call": sec * 1e3, "scenarios": S, "calls": calls, "layers": len(names),
+            "outputs": "parts [S][4] + per-layer busy [layers][2][S] (the sweep's what-if reports)",
+            "parity_checked": {"scenarios": [s], "checker": "oracle/breakdown_oracle.py "
+                               "(breakdown.py:42-111): four parts + every layer"}}
+
+
 def _oracle_scenarios(fz, graph_of, ms, lb, start, cols) -> list:
     """Device rows of scenarios `cols` against the C oracle's Alg. 1 on the
     reference-equivalent transformed graph (checker only)."""
@@ -816,6 +864,7 @@ def run_config(args):
     assert np.array_equal(r.makespan, h_ms.numpy()), "e2e result differs from device run"
     jit = (N.lib().ks_jit_log() or b"").decode()
     peak, peak_src = _peaks()
+    bd = None if args.no_breakdown else _config_breakdown(fz, table, graph_of, st, ms, stream)
     bpu = 8  # start write; durations derive on the device from base x scenario program
     achieved = n * S * bpu / (per / 1e3) / 1e9
     cb = None if args.no_cpu_baseline else _config_cpu_baseline(graph_of, S, n)
@@ -845,6 +894,7 @@ def run_config(args):
                                       "transformed graph: every start, makespan, lane busy"},
         "gpu_launches": launches,
         "clocks": clk,
+        "breakdown": bd,
     }
     print(json.dumps(line), flush=True)
 
