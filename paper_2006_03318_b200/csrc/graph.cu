@@ -3188,7 +3188,8 @@ int breakdown_impl(const ks_graph* g, const ks_scenarios_desc* sc, const int64_t
   {
     // time windows per scenario: (scenario, window) threads for ~4 waves of
     // the lean merge (measured at 65,536 x 100k: K = 5 / 10 / 20 -> 92 / 67 /
-    // 76 ms), at least ~512 rows of work per window -- ~16 below 1,024
+    // 76 ms), at least ~192 rows of work per window (config 3, 4,000 x 29.6k: 57 -> 152
+    // windows 11.9 -> 10.2 ms) -- ~16 below 1,024
     // scenarios, where one thread's dependent walk is the whole latency
     // (one scenario: 10k rows 0.71 -> 0.26 ms, 100k rows 2.0 -> 1.0 ms with 16-row windows
     // and short per-layer chunks)
@@ -3196,7 +3197,7 @@ int breakdown_impl(const ks_graph* g, const ks_scenarios_desc* sc, const int64_t
     cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, g->device);
     const long long target = (long long)nsm * 4096;
     long long K = (target + S - 1) / S;
-    K = std::min<long long>(K, std::max(1, g->n / (S >= 1024 ? 512 : 16)));
+    K = std::min<long long>(K, std::max(1, g->n / (S >= 1024 ? 192 : 16)));
     p.K = (int)std::max<long long>(1, std::min<long long>(K, 65535));
     if (const char* e = getenv("DDSIM_BD_WINDOWS")) p.K = std::max(1, atoi(e));
     p.stream_loads = getenv("DDSIM_BD_STREAM") != nullptr;
